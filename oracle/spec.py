@@ -1,0 +1,213 @@
+"""The Medusa speculative step over a bounded KV cache (oracle).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+Follows SURVEY §8.c.2 / DESIGN.md §3 step by step, in the paper's terms:
+
+  propose  -- tree tokens from the heads' top-k at the last accepted node
+              ("arity-k (equals to top-k token sampling from heads)",
+              "L-many parallel decoding heads (equals to the number of tree
+              levels)"; "top-k tokens of the first decoding head").
+  verify   -- one forward of all N nodes; "prior to verification, attention mask
+              assumes full acceptance": node n sees the committed prefix,
+              its ancestors and itself (Eq. 2).  Positions continue "from the
+              latest sequence length": pos = Lc + depth.
+  accept   -- "sampled logits are evaluated to pass a certain threshold to be
+              accepted followed by a cumulative product ... The longest
+              candidate sequence that verified its tokens is accepted";
+              typical acceptance with an entropy threshold.
+  compact  -- the pre-allocated KV cache is "a scratch space ... frequently
+              update[d] during verification stage": accepted nodes' K/V
+              move to contiguous committed slots.
+
+Vanilla greedy decoding (the plain definition the greedy mode must reproduce,
+north star) is ``vanilla_generate`` -- token by token, separate code.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import tree as T
+from .model import KVCache, Model, argmax_lowest, topk_desc
+
+
+class KVCapacityError(RuntimeError):
+    """Prefill/verify would exceed the bound x (Eq. 1; OOM reason "Cache")."""
+
+
+def typical_stats(z, temperature: float):
+    """P = softmax(z / T) and the exact entropy H = -sum P log P (0 log 0 = 0)."""
+    y = np.asarray(z, dtype=np.float64) / temperature
+    y = y - y.max()
+    e = np.exp(y)
+    P = e / e.sum()
+    nz = P > 0
+    H = float(-(P[nz] * np.log(P[nz])).sum())
+    return P, H
+
+
+class Session:
+    """b independent sequences sharing one model and one static tree."""
+
+    def __init__(self, model: Model, choices: list[list[int]], batch: int, max_seq_len: int, topk: int = 10):
+        self.m = model
+        self.tree = T.build(choices, topk) if choices else T.build([], topk)
+        self.N = self.tree.N
+        self.l = max(self.tree.max_depth, 0)
+        self.n_heads_used = self.l
+        assert self.l <= len(model.W.medusa), "tree deeper than the number of Medusa heads"
+        self.K = topk
+        self.x = max_seq_len
+        self.b = batch
+        self.kv = KVCache(model.n_layers, batch, model.Hkv, max_seq_len + self.N, model.hd)
+        self.Lc = [0] * batch
+        self.root = [None] * batch
+        self.topk_tok = [None] * batch                   # [l][K] token ids per sequence
+        self.committed = [[] for _ in range(batch)]
+        self.leaves = T.leaves(self.tree)
+        self.dfs = T.dfs_order(self.tree)
+        self.dfs_pos = {n: i for i, n in enumerate(self.dfs)}
+
+    # ------------------------------------------------------------ heads
+    def _propose_state(self, seq, z, hf):
+        self.root[seq] = argmax_lowest(z)                       # Q8: root = argmax in both modes
+        self.topk_tok[seq] = [topk_desc(self.m.head_logits(i, hf), self.K) for i in range(self.l)]
+
+    # ------------------------------------------------------------ prefill
+    def prefill(self, seq: int, tokens) -> None:
+        """Causal forward of one turn's P tokens at positions [Lc, Lc+P).
+        A pending root from a previous turn is dropped (Q15)."""
+        P = len(tokens)
+        if P == 0:
+            return
+        if self.Lc[seq] + P > self.x:
+            raise KVCapacityError(f"prefill {P} at Lc={self.Lc[seq]} exceeds x={self.x}")
+        z = hf = None
+        for i, tok in enumerate(tokens):
+            pos = self.Lc[seq] + i
+            z, hf = self.m.forward_row(self.kv, seq, int(tok), pos, pos, list(range(pos + 1)))
+        self.Lc[seq] += P
+        self.committed[seq].extend(int(t) for t in tokens)
+        self._propose_state(seq, z, hf)
+
+    # ------------------------------------------------------------ step
+    def propose(self, seq: int):
+        """tok[0] = root, tok[n] = T_{depth(n)-1}[rank(n)];  pos[n] = Lc + depth(n)."""
+        tr = self.tree
+        tok = [self.root[seq]] + [self.topk_tok[seq][tr.depth[n] - 1][tr.rank[n]] for n in range(1, self.N)]
+        pos = [self.Lc[seq] + tr.depth[n] for n in range(self.N)]
+        return tok, pos
+
+    def verify(self, seq: int, tok):
+        """Forward all nodes; node n writes K/V to slot Lc+n and attends to
+        [0, Lc) + its ancestors' slots + its own slot, in logical order."""
+        Lc = self.Lc[seq]
+        if Lc >= self.x:
+            raise KVCapacityError(f"verify at Lc={Lc} >= x={self.x}")
+        tr = self.tree
+        Z, HF = [None] * self.N, [None] * self.N
+        for n in range(self.N):                                   # canonical order: parents first
+            keys = list(range(Lc)) + [Lc + a for a in T.ancestors(tr, n)] + [Lc + n]
+            Z[n], HF[n] = self.m.forward_row(self.kv, seq, int(tok[n]), Lc + tr.depth[n], Lc + n, keys)
+        return Z, HF
+
+    def accept(self, tok, Z, mode: str = "greedy", temperature: float = 0.7, eps: float = 0.09, alpha: float = 0.3):
+        """Tree DP: acc(root) = true; acc(c) = acc(parent) and C(parent, c).
+        greedy C: tok[c] == argmax z[parent];  typical C: P_p[tok[c]] > min(eps, alpha e^{-H_p}).
+        Returns (a, chosen node, best_leaf index, path node ids [a+1])."""
+        tr = self.tree
+        acc = [False] * self.N
+        ll = [0.0] * self.N
+        acc[0] = True
+        stats = {}
+        for c in range(1, self.N):
+            p = tr.parent[c]
+            if not acc[p]:
+                continue
+            if mode == "greedy":
+                ok = int(tok[c]) == argmax_lowest(Z[p])
+                lp = 0.0
+            else:
+                if p not in stats:
+                    P, H = typical_stats(Z[p], temperature)
+                    stats[p] = (P, min(eps, alpha * math.exp(-H)))
+                P, thr = stats[p]
+                ok = P[int(tok[c])] > thr
+                lp = math.log(P[int(tok[c])]) if P[int(tok[c])] > 0 else -math.inf
+            if ok:
+                acc[c] = True
+                ll[c] = ll[p] + lp
+        a = max(tr.depth[n] for n in range(self.N) if acc[n])
+        if a == 0:
+            chosen = 0
+        else:
+            cands = [n for n in range(self.N) if acc[n] and tr.depth[n] == a]
+            best = max(ll[n] for n in cands)
+            chosen = min((n for n in cands if ll[n] == best), key=lambda n: self.dfs_pos[n])
+        # best_leaf: first leaf (DFS order) whose path passes through ``chosen``
+        chosen_path = tr.paths[chosen]
+        best_leaf = next(i for i, lf in enumerate(self.leaves) if tr.paths[lf][:len(chosen_path)] == chosen_path)
+        path = T.ancestors(tr, chosen) + [chosen]
+        return a, chosen, best_leaf, path
+
+    def compact(self, seq: int, path, a_eff: int) -> None:
+        """For j = 1..a_eff (ascending): K/V[Lc+j] <- K/V[Lc+path[j]] in every layer
+        and kv head (reading Q13)."""
+        Lc = self.Lc[seq]
+        for j in range(1, a_eff + 1):
+            for li in range(self.m.n_layers):
+                self.kv.K[li][seq][:, Lc + j, :] = self.kv.K[li][seq][:, Lc + path[j], :]
+                self.kv.V[li][seq][:, Lc + j, :] = self.kv.V[li][seq][:, Lc + path[j], :]
+
+    def step(self, seq: int, mode: str = "greedy", budget: int | None = None, **typ):
+        """One full speculative step for one sequence.  Emits tok[path[0..a_eff]],
+        a_eff = min(a, budget-1, x-Lc-1) (Q14, Q15); tau = a_eff + 1."""
+        tok, pos = self.propose(seq)
+        Z, HF = self.verify(seq, tok)
+        a, chosen, best_leaf, path = self.accept(tok, Z, mode, **typ)
+        Lc = self.Lc[seq]
+        a_eff = a
+        if budget is not None:
+            a_eff = min(a_eff, budget - 1)
+        a_eff = min(a_eff, self.x - Lc - 1)
+        assert a_eff >= 0
+        self.compact(seq, path, a_eff)
+        emitted = [int(tok[path[j]]) for j in range(a_eff + 1)]
+        self.Lc[seq] = Lc + a_eff + 1
+        self.committed[seq].extend(emitted)
+        last = path[a_eff]
+        self._propose_state(seq, Z[last], HF[last])
+        return dict(tok=tok, pos=pos, Z=Z, a=a, a_eff=a_eff, best_leaf=best_leaf,
+                    path=path, emitted=emitted, chosen=chosen)
+
+    def generate(self, seq: int, n_new: int, mode: str = "greedy", **typ):
+        """Decode until n_new tokens were emitted in this turn (budget clamp)."""
+        out, taus = [], []
+        while len(out) < n_new:
+            r = self.step(seq, mode, budget=n_new - len(out), **typ)
+            out += r["emitted"]
+            taus.append(len(r["emitted"]))
+        return out, taus
+
+
+def vanilla_generate(model: Model, prompt, n_new: int, max_seq_len: int | None = None):
+    """Plain greedy decoding, one token at a time (the definition the greedy
+    speculative mode must reproduce).  Every generated token is also run through
+    the model, so the returned cache holds K/V for prompt + generated tokens.
+    Returns (generated tokens, kv cache)."""
+    cap = max_seq_len or (len(prompt) + n_new + 1)
+    kv = KVCache(model.n_layers, 1, model.Hkv, cap, model.hd)
+    z = None
+    for i, t in enumerate(prompt):
+        z, _ = model.forward_row(kv, 0, int(t), i, i, list(range(i + 1)))
+    out = []
+    pos = len(prompt)
+    nxt = argmax_lowest(z)
+    while len(out) < n_new:
+        out.append(nxt)
+        z, _ = model.forward_row(kv, 0, nxt, pos, pos, list(range(pos + 1)))
+        pos += 1
+        nxt = argmax_lowest(z)
+    return out, kv

@@ -1,0 +1,147 @@
+"""Medusa static trees (oracle; test infrastructure only).
+
+A tree is given as a Medusa path list ("choices"): each element is the list of
+top-k ranks from the root to a node, root implicit ("static, pre-built and
+pruned attention trees"; SPEC.md path-list format).  Eq. 2 defines the
+attention mask as the union of nodes on the S root-to-leaf paths; "prior to
+verification, attention mask assumes full acceptance", i.e. node i sees
+exactly its ancestors and itself.
+
+Reading (R4/Q4): canonical node order = root, then sort by
+(depth, lexicographic rank path).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+
+class InfeasibleTree(ValueError):
+    pass
+
+
+@dataclass
+class Tree:
+    paths: list[tuple[int, ...]]          # index n -> rank path of node n (root = ())
+    topk: int
+    parent: list[int] = field(default_factory=list)
+    depth: list[int] = field(default_factory=list)
+    rank: list[int] = field(default_factory=list)
+
+    @property
+    def N(self) -> int:
+        return len(self.paths)
+
+    @property
+    def max_depth(self) -> int:
+        return max(self.depth)
+
+    def children(self, n: int) -> list[int]:
+        return [c for c in range(self.N) if self.parent[c] == n]
+
+
+def build(choices: list[list[int]], topk: int = 10) -> Tree:
+    """Validate a path list and return the canonical tree.
+
+    Errors (InfeasibleTree): duplicate path, orphan (a proper prefix missing),
+    rank >= topk, negative rank, empty path.
+    """
+    seen = set()
+    for p in choices:
+        t = tuple(int(r) for r in p)
+        if len(t) == 0:
+            raise InfeasibleTree("empty path")
+        if any(r < 0 or r >= topk for r in t):
+            raise InfeasibleTree(f"rank out of range in {t}")
+        if t in seen:
+            raise InfeasibleTree(f"duplicate path {t}")
+        seen.add(t)
+    for t in seen:
+        for j in range(1, len(t)):
+            if t[:j] not in seen:
+                raise InfeasibleTree(f"orphan path {t}: missing {t[:j]}")
+    ordered = [()] + sorted(seen, key=lambda t: (len(t), t))
+    index = {t: i for i, t in enumerate(ordered)}
+    tree = Tree(paths=ordered, topk=topk)
+    for t in ordered:
+        tree.depth.append(len(t))
+        tree.rank.append(t[-1] if t else -1)
+        tree.parent.append(index[t[:-1]] if t else -1)
+    return tree
+
+
+def ancestors(tree: Tree, n: int) -> list[int]:
+    """Ancestors of n from the root down (root first), excluding n."""
+    out = []
+    p = tree.parent[n]
+    while p >= 0:
+        out.append(p)
+        p = tree.parent[p]
+    return out[::-1]
+
+
+def ancestor_mask(tree: Tree) -> list[list[int]]:
+    """N x N 0/1 matrix, entry (i, j) = 1 iff j is i or an ancestor of i (Eq. 2)."""
+    N = tree.N
+    m = [[0] * N for _ in range(N)]
+    for i in range(N):
+        m[i][i] = 1
+        for j in ancestors(tree, i):
+            m[i][j] = 1
+    return m
+
+
+def leaves(tree: Tree) -> list[int]:
+    """Leaf node ids in DFS (lexicographic rank-path) order."""
+    has_child = [False] * tree.N
+    for c in range(1, tree.N):
+        has_child[tree.parent[c]] = True
+    ls = [n for n in range(tree.N) if not has_child[n]]
+    return sorted(ls, key=lambda n: tree.paths[n])
+
+
+def dfs_order(tree: Tree) -> list[int]:
+    """All node ids in DFS pre-order (lexicographic rank path)."""
+    return sorted(range(tree.N), key=lambda n: tree.paths[n])
+
+
+def candidate_paths(tree: Tree) -> list[list[int]]:
+    """S candidate sequences as node-id lists root..leaf, padded with -1 to
+    length max_depth+1 ("total candidate sequences S")."""
+    L = tree.max_depth + 1
+    out = []
+    for leaf in leaves(tree):
+        ids = ancestors(tree, leaf) + [leaf]
+        out.append(ids + [-1] * (L - len(ids)))
+    return out
+
+
+def level_counts(tree: Tree) -> list[int]:
+    cnt = [0] * (tree.max_depth + 1)
+    for d in tree.depth:
+        cnt[d] += 1
+    return cnt
+
+
+def stats(tree: Tree) -> dict:
+    """(N, S, l) and the per-level label, e.g. '1-10-23-23-7'."""
+    return dict(N=tree.N, S=len(leaves(tree)), depth=tree.max_depth,
+                label="-".join(str(c) for c in level_counts(tree)))
+
+
+def truncate(choices: list[list[int]], depth: int) -> list[list[int]]:
+    """Keep nodes of depth <= ``depth`` (a Medusa tree used with fewer heads)."""
+    return [list(p) for p in choices if len(p) <= depth]
+
+
+def prune_right_to_left(choices: list[list[int]], target_nodes: int, topk: int = 10) -> list[list[int]]:
+    """Reading R4 of P:247 ("Medusa's right-to-left pruning"): repeatedly delete
+    the leaf whose rank path is lexicographically largest (the rightmost leaf in
+    DFS order) until ``target_nodes`` nodes (root included) remain."""
+    tree = build(choices, topk)
+    if target_nodes < 1 or target_nodes > tree.N:
+        raise InfeasibleTree("target outside [1, N]")
+    cur = set(tuple(p) for p in choices)
+    while len(cur) + 1 > target_nodes:
+        lv = [t for t in cur if not any(len(u) == len(t) + 1 and u[:len(t)] == t for u in cur)]
+        cur.remove(max(lv))
+    return [list(t) for t in sorted(cur, key=lambda t: (len(t), t))]
