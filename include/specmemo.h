@@ -1,0 +1,184 @@
+/*
+ * specmemo.h -- C ABI of the B200-native Medusa tree-verification hot path
+ * (SpecMemo, arxiv 2506.01986).  Implemented by libspecmemo.so (sm_100a).
+ *
+ * Citations: P:<n> = /root/reference/PAPER.md line n, S:<n> = SPEC.md line n.
+ * Readings of the paper (Q1..Q26, R0..R11) are listed in DESIGN.md §3.
+ *
+ * Conventions
+ *  - Every call returns sm_status; nothing throws across the ABI.  On error,
+ *    sm_last_error() returns a thread-local message.  Argument errors are
+ *    detected on the host before anything is enqueued.
+ *  - Pointers named d_* are DEVICE pointers (cudaMalloc / torch CUDA tensors),
+ *    h_* are HOST pointers.  Weights and the KV-cache memory are allocated by
+ *    the caller and BORROWED: they must outlive the handles.  Handles and the
+ *    library's internal workspace are owned by the library (freed by *_destroy).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    All device work is stream-ordered; sm_step is CUDA-graph replayed and
+ *    never synchronises with the host.
+ *  - bf16 tensors are row-major, PyTorch nn.Linear layout [out][in].
+ */
+#ifndef SPECMEMO_H
+#define SPECMEMO_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SM_OK = 0,
+  SM_ERR_INVALID_ARG = 1,      /* bad pointer / shape / config; nothing enqueued (SPEC exit 1) */
+  SM_ERR_INFEASIBLE_TREE = 2,  /* orphan / duplicate path, rank >= topk, depth > heads (SPEC exit 2)   */
+  SM_ERR_KV_CAPACITY = 3,      /* prefill / verify would exceed the bound x (OOM reason "Cache") */
+  SM_ERR_DEVICE_OOM = 4,       /* workspace allocation failed (reason Model|Cache|Buffer)        */
+  SM_ERR_CUDA = 5,
+  SM_ERR_NCCL = 6,
+  SM_ERR_UNSUPPORTED = 7
+} sm_status;
+
+typedef struct sm_tree sm_tree;
+typedef struct sm_model sm_model;
+typedef struct sm_kv sm_kv;
+
+/* ------------------------------------------------------------------ trees
+ * A static Medusa tree in path-list form ("choices", root implicit), e.g.
+ * [[0],[0,0],[1],...] (P:55 static pre-built trees; S:227 path-list format).
+ * Eq. 2: node n attends to its ancestors and itself ("attention mask
+ * assumes full acceptance").  Canonical node order: root = 0, then sort
+ * by (depth, lexicographic rank path) (reading Q4).
+ *   ranks_flat    concatenated rank paths (host)
+ *   path_offsets  n_paths+1 offsets into ranks_flat (host)
+ *   topk          arity K ("arity-k equals top-k sampling from heads")
+ * Errors: SM_ERR_INFEASIBLE_TREE (orphan, duplicate, empty path, rank >= topk),
+ *         SM_ERR_INVALID_ARG (n_paths > 255, i.e. N > 256).
+ * n_paths = 0 gives the 1-node tree (vanilla decoding).                      */
+sm_status sm_tree_create(const int32_t *h_ranks_flat, const int32_t *h_path_offsets, int n_paths, int topk,
+                         sm_tree **out);
+/* Chain tree of n nodes (node i = depth i): used for prefill chunks.        */
+sm_status sm_tree_create_chain(int n, sm_tree **out);
+/* Query the canonical tables (host outputs, any pointer may be NULL):
+ *   N, S (leaves), depth (max depth l), parent[N], node_depth[N], rank[N],
+ *   anc_bits[N][4] (bit j of word j/64 = node j is n or an ancestor of n),
+ *   leaf_paths[S][depth+1] node ids root..leaf in DFS order, -1 padded.      */
+sm_status sm_tree_query(const sm_tree *t, int *N, int *S, int *depth, int32_t *h_parent, int32_t *h_node_depth,
+                        int32_t *h_rank, uint64_t *h_anc_bits, int32_t *h_leaf_paths);
+void sm_tree_destroy(sm_tree *t);
+
+/* ------------------------------------------------------------------ model */
+typedef struct {
+  int n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ffn, vocab, n_medusa;
+  float rms_eps, rope_theta;
+  int max_rows;      /* max token rows per forward (b*N or a prefill chunk), <= 256 */
+  int max_batch;     /* max sequences b                                          */
+  int max_seq_len;   /* max positions (RoPE table length) = x + N                */
+} sm_model_cfg;
+
+/* Device pointers to bf16 weights ([out][in]); arrays are host arrays of
+ * device pointers, one entry per layer / Medusa head.  Medusa-1 head i:
+ * u_i = U_i (h + SiLU(R_i h + b_i)) (Eq. 4 size pin; reading Q6).       */
+typedef struct {
+  const void *embed;       /* [V][d]                          */
+  const void *final_norm;  /* [d]                             */
+  const void *lm_head;     /* [V][d]                          */
+  const void *const *attn_norm, *const *wqkv, *const *wo;           /* [d], [(H+2Hkv)hd][d], [d][H hd] */
+  const void *const *mlp_norm, *const *wgate_up, *const *wdown;     /* [d], [2F][d] (gate;up), [d][F]  */
+  const void *const *medusa_R, *const *medusa_b, *const *medusa_U;  /* [d][d], [d], [V][d]             */
+} sm_weights;
+
+/* Tensor-parallel placement (north star: TP over NVLink, all-reduce after
+ * o_proj and down_proj).  tp_size must be 1 in this build (else UNSUPPORTED). */
+typedef struct {
+  int tp_rank, tp_size;
+  unsigned char nccl_id[128];
+} sm_dist;
+
+sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *w, const sm_dist *dist, sm_model **out);
+void sm_model_destroy(sm_model *m);
+
+/* Fill a bf16 buffer with the counter-hash weights of SURVEY §8.d.1:
+ * w[i] = bf16(f32((h>>40) - 2^23) * 2^-23 * f32(0.02*sqrt(3))),
+ * h = splitmix64(seed ^ stream<<40 ^ (start+i)).  mode 1 = N(0,1)-ish (sum of
+ * four 16-bit uniforms, for the K1 sweep), mode 0 = the weight law above.     */
+sm_status sm_generate_bf16(void *d_dst, size_t numel, uint64_t seed, uint64_t stream_id, uint64_t start, int mode,
+                           void *stream);
+
+/* ------------------------------------------------------------------ bounded KV cache
+ * Eq. 1 with d restored (reading Q14): bytes =
+ *   2 * layers * batch * kv_heads/tp * head_dim * (max_seq_len + tree_nodes) * 2.
+ * The last N slots of each sequence are the tree scratch ("scratch space").
+ * Layout: [layer][K|V][b][Hkv][x+N][hd] bf16.                                  */
+sm_status sm_kv_bytes(const sm_model_cfg *cfg, int tp_size, int batch, int max_seq_len, int tree_nodes,
+                      size_t *bytes);
+/* Bind caller memory (>= sm_kv_bytes) as the cache of `batch` sequences for
+ * tree t; zero-fills it and sets every length to 0.                           */
+sm_status sm_kv_bind(sm_model *m, const sm_tree *t, int batch, int max_seq_len, void *d_mem, size_t bytes,
+                     sm_kv **out);
+/* Device pointer to the int32 committed lengths Lc[b] (for stage tests).    */
+sm_status sm_kv_lengths_device(const sm_kv *kv, int32_t **d_len);
+/* Copy Lc[b] to the host (synchronises the kv's stream).                    */
+sm_status sm_kv_lengths(const sm_kv *kv, int32_t *h_len);
+void sm_kv_destroy(sm_kv *kv);
+
+/* Prefill one turn of n tokens of sequence `seq` (causal forward at positions
+ * [Lc, Lc+n)), then set the pending root (argmax) and the heads' top-k
+ * at the last token.  A pending root of a previous turn is dropped (Q15).
+ * SM_ERR_KV_CAPACITY if the host-tracked Lc + n > x.  d_tokens: device int32. */
+sm_status sm_prefill(sm_model *m, sm_kv *kv, int seq, const int32_t *d_tokens, int n, void *stream);
+
+typedef enum { SM_ACCEPT_GREEDY = 0, SM_ACCEPT_TYPICAL = 1 } sm_accept_mode;
+typedef struct {
+  sm_accept_mode mode;
+  float temperature, eps, alpha;   /* typical: P[tok] > min(eps, alpha*exp(-H)) at temperature T (Q10) */
+  const int32_t *d_max_new;        /* [b] remaining per-turn budget, NULL = unbounded (Q15)           */
+  const int32_t *d_forced_path;    /* [b][l+1] test hook, NULL = off: accept this node path instead   */
+} sm_accept_cfg;
+
+/* Device outputs of one step (caller-allocated int32 buffers):
+ *   acc_len[b] = a (max accepted depth), best_leaf[b] (DFS leaf index),
+ *   path[b][l+1] accepted node ids (-1 padded), emit_tok[b][l+1] emitted tokens,
+ *   n_emit[b] = tau = a_eff + 1 (0 if inactive), status[b] (0 ok, 3 capacity). */
+typedef struct {
+  int32_t *acc_len, *best_leaf, *path, *emit_tok, *n_emit, *status;
+} sm_accept_out;
+
+/* a1 propose: tree tokens tok[n] = topk[depth(n)-1][rank(n)], tok[0] = root
+ * (P:67); positions Lc + depth.  d_tree_tok [b][N], d_pos [b][N]. */
+sm_status sm_propose(sm_model *m, sm_kv *kv, int32_t *d_tree_tok, int32_t *d_pos, void *stream);
+/* a2+a3 verify: one forward of all b*N nodes with the tree mask (Eq. 2), K/V
+ * written to slots [Lc, Lc+N).  d_logits nullable: fp32 [b][N][V] copy.      */
+sm_status sm_verify(sm_model *m, sm_kv *kv, const int32_t *d_tree_tok, float *d_logits, void *stream);
+/* a4+a5 accept (greedy/typical tree DP) + in-place compaction of the
+ * accepted nodes' K/V + next-state heads/top-k at the accepted node.   */
+sm_status sm_accept(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, const sm_accept_out *out, void *stream);
+/* Full step a1..a5 for the whole batch (P:252-257 batched decoding, ragged
+ * lengths).  Captured into a CUDA graph on first use per (mode, hooks) and
+ * replayed; graph-capturable itself.                                          */
+sm_status sm_step(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, const sm_accept_out *out, void *stream);
+/* Number of kernels one sm_step launches (for the bench's gpu_launches).     */
+sm_status sm_step_launches(const sm_kv *kv, int *n);
+/* Device pointers to the pending state: root[b], topk[b][n_medusa][K] (int32). */
+sm_status sm_state_device(const sm_kv *kv, int32_t **d_root, int32_t **d_topk);
+
+/* ------------------------------------------------------------------ stage kernels (parity tests)
+ * K1 tree attention on caller buffers.  q [b][N][H][hd] bf16; k/v caches
+ * [b][Hkv][cap][hd] bf16 with the N tree rows at [Lc, Lc+N); d_len[b] int32 Lc;
+ * out [b][N][H][hd] bf16.  Node n attends keys [0, Lc) and the tree slots of
+ * its ancestors and itself, scale 1/sqrt(hd), softmax in fp32.               */
+sm_status sm_tree_attention(const sm_tree *t, const void *d_q, const void *d_k, const void *d_v,
+                            const int32_t *d_len, int batch, int n_heads, int n_kv_heads, int head_dim, int cap,
+                            void *d_out, void *stream);
+/* K2 tcgen05 GEMM: out[M][N] fp32 = x[M][K] bf16 * w[N][K]^T bf16.  M <= 256. */
+sm_status sm_gemm_bf16(const void *d_x, const void *d_w, float *d_out, int M, int N, int K, void *stream);
+/* K3 top-k rows of fp32 logits: idx[r][k] by (value desc, index asc).        */
+sm_status sm_topk_f32(const float *d_logits, int rows, int V, int k, int32_t *d_idx, void *stream);
+
+const char *sm_last_error(void);
+const char *sm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECMEMO_H */

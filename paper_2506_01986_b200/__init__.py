@@ -1,0 +1,328 @@
+"""B200-native Medusa tree-verification hot path (SpecMemo, arxiv 2506.01986).
+
+Thin ctypes binding over ``libspecmemo.so`` (include/specmemo.h).  Argument
+marshalling only: every step of the path runs in the library's sm_100a kernels.
+PyTorch provides device memory and streams.  There is no CPU fallback: if the
+library is missing or the device is not sm_100, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libspecmemo.so")
+
+SM_OK, SM_ERR_INVALID_ARG, SM_ERR_INFEASIBLE_TREE, SM_ERR_KV_CAPACITY = 0, 1, 2, 3
+SM_ERR_DEVICE_OOM, SM_ERR_CUDA, SM_ERR_NCCL, SM_ERR_UNSUPPORTED = 4, 5, 6, 7
+GREEDY, TYPICAL = 0, 1
+
+
+class SpecMemoError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[sm_status {status}] {msg}")
+        self.status = status
+
+
+class KVCapacityError(SpecMemoError):
+    pass
+
+
+class InfeasibleTreeError(SpecMemoError):
+    pass
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is not built; run `python -m paper_2506_01986_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        L.sm_last_error.restype = ctypes.c_char_p
+        L.sm_version.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(status: int) -> None:
+    if status != SM_OK:
+        msg = lib().sm_last_error().decode()
+        cls = {SM_ERR_KV_CAPACITY: KVCapacityError, SM_ERR_INFEASIBLE_TREE: InfeasibleTreeError}.get(status, SpecMemoError)
+        raise cls(status, msg)
+
+
+# ------------------------------------------------------------------ C structs
+class ModelCfg(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in ("n_layers", "d_model", "n_heads", "n_kv_heads", "head_dim", "d_ffn",
+                                            "vocab", "n_medusa")] + \
+               [("rms_eps", ctypes.c_float), ("rope_theta", ctypes.c_float)] + \
+               [(n, ctypes.c_int) for n in ("max_rows", "max_batch", "max_seq_len")]
+
+
+_PP = ctypes.POINTER(ctypes.c_void_p)
+
+
+class Weights(ctypes.Structure):
+    _fields_ = [("embed", ctypes.c_void_p), ("final_norm", ctypes.c_void_p), ("lm_head", ctypes.c_void_p)] + \
+               [(n, _PP) for n in ("attn_norm", "wqkv", "wo", "mlp_norm", "wgate_up", "wdown",
+                                   "medusa_R", "medusa_b", "medusa_U")]
+
+
+class Dist(ctypes.Structure):
+    _fields_ = [("tp_rank", ctypes.c_int), ("tp_size", ctypes.c_int), ("nccl_id", ctypes.c_ubyte * 128)]
+
+
+class AcceptCfg(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int), ("temperature", ctypes.c_float), ("eps", ctypes.c_float),
+                ("alpha", ctypes.c_float), ("d_max_new", ctypes.c_void_p), ("d_forced_path", ctypes.c_void_p)]
+
+
+class AcceptOutC(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("acc_len", "best_leaf", "path", "emit_tok", "n_emit", "status")]
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+def _stream(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+# ------------------------------------------------------------------ trees
+class Tree:
+    """Static Medusa tree from a path list (root implicit), canonical order
+    (depth, rank path) -- Eq. 2 / P:67-72."""
+
+    def __init__(self, choices, topk: int = 10, chain: int | None = None):
+        self._h = ctypes.c_void_p()
+        if chain is not None:
+            _check(lib().sm_tree_create_chain(ctypes.c_int(chain), ctypes.byref(self._h)))
+        else:
+            flat = [int(r) for p in choices for r in p]
+            offs = [0]
+            for p in choices:
+                offs.append(offs[-1] + len(p))
+            fa = (ctypes.c_int32 * max(1, len(flat)))(*flat)
+            oa = (ctypes.c_int32 * len(offs))(*offs)
+            _check(lib().sm_tree_create(fa, oa, ctypes.c_int(len(choices)), ctypes.c_int(topk), ctypes.byref(self._h)))
+        q = self.query()
+        self.N, self.S, self.depth = q["N"], q["S"], q["depth"]
+        self.topk = topk
+
+    def query(self) -> dict:
+        N, S, dep = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _check(lib().sm_tree_query(self._h, ctypes.byref(N), ctypes.byref(S), ctypes.byref(dep), None, None, None,
+                                   None, None))
+        n, s, l = N.value, S.value, dep.value
+        parent = np.zeros(n, np.int32)
+        nd = np.zeros(n, np.int32)
+        rank = np.zeros(n, np.int32)
+        anc = np.zeros((n, 4), np.uint64)
+        lp = np.zeros((s, l + 1), np.int32)
+        P = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        _check(lib().sm_tree_query(self._h, None, None, None, P(parent), P(nd), P(rank), P(anc), P(lp)))
+        return dict(N=n, S=s, depth=l, parent=parent, node_depth=nd, rank=rank, anc=anc, leaf_paths=lp)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.sm_tree_destroy(self._h)
+
+
+# ------------------------------------------------------------------ weights (device generator)
+def generate_bf16(t, seed: int, stream_id: int, start: int = 0, mode: int = 0, stream=None) -> None:
+    """Fill a bf16 CUDA tensor with the counter-hash law (synth.weight_bits /
+    synth.normal_bits), on the device."""
+    _check(lib().sm_generate_bf16(ctypes.c_void_p(_ptr(t)), ctypes.c_size_t(t.numel()), ctypes.c_uint64(seed),
+                                  ctypes.c_uint64(stream_id), ctypes.c_uint64(start), ctypes.c_int(mode),
+                                  ctypes.c_void_p(_stream(stream))))
+
+
+def allocate_weights(cfg: dict, n_medusa: int, seed: int = 0, medusa_init: bool = False, device="cuda") -> dict:
+    """Random-init bf16 weights of a Llama + Medusa-1 model, generated on the GPU
+    with the same streams as the oracle (synth stream registry)."""
+    import torch
+
+    import synth
+    d, H, Hkv, hd, F, V, L = (cfg[k] for k in ("d_model", "n_heads", "n_kv_heads", "head_dim", "d_ffn", "vocab",
+                                                "n_layers"))
+    bf = torch.bfloat16
+    W = {"embed": torch.empty(V, d, dtype=bf, device=device), "lm_head": torch.empty(V, d, dtype=bf, device=device),
+         "final_norm": torch.ones(d, dtype=bf, device=device), "layers": [], "medusa": []}
+    generate_bf16(W["embed"], seed, synth.STREAM_EMBED)
+    generate_bf16(W["lm_head"], seed, synth.STREAM_LM_HEAD)
+    for li in range(L):
+        wqkv = torch.empty((H + 2 * Hkv) * hd, d, dtype=bf, device=device)
+        generate_bf16(wqkv[: H * hd], seed, synth.stream_layer(li, "wq"))
+        generate_bf16(wqkv[H * hd:(H + Hkv) * hd], seed, synth.stream_layer(li, "wk"))
+        generate_bf16(wqkv[(H + Hkv) * hd:], seed, synth.stream_layer(li, "wv"))
+        wo = torch.empty(d, H * hd, dtype=bf, device=device)
+        generate_bf16(wo, seed, synth.stream_layer(li, "wo"))
+        wgu = torch.empty(2 * F, d, dtype=bf, device=device)
+        generate_bf16(wgu[:F], seed, synth.stream_layer(li, "wg"))
+        generate_bf16(wgu[F:], seed, synth.stream_layer(li, "wu"))
+        wd = torch.empty(d, F, dtype=bf, device=device)
+        generate_bf16(wd, seed, synth.stream_layer(li, "wd"))
+        W["layers"].append(dict(attn_norm=torch.ones(d, dtype=bf, device=device), wqkv=wqkv, wo=wo,
+                                mlp_norm=torch.ones(d, dtype=bf, device=device), wgate_up=wgu, wdown=wd))
+    for i in range(n_medusa):
+        if medusa_init:
+            R = torch.zeros(d, d, dtype=bf, device=device)
+            U = W["lm_head"]
+        else:
+            R = torch.empty(d, d, dtype=bf, device=device)
+            generate_bf16(R, seed, synth.stream_medusa(i, "R"))
+            U = torch.empty(V, d, dtype=bf, device=device)
+            generate_bf16(U, seed, synth.stream_medusa(i, "U"))
+        W["medusa"].append(dict(R=R, b=torch.zeros(d, dtype=bf, device=device), U=U))
+    return W
+
+
+def weights_bytes(cfg: dict, n_medusa: int) -> int:
+    d, H, Hkv, hd, F, V, L = (cfg[k] for k in ("d_model", "n_heads", "n_kv_heads", "head_dim", "d_ffn", "vocab",
+                                                "n_layers"))
+    layer = (H + 2 * Hkv) * hd * d + d * H * hd + 3 * F * d
+    return 2 * (L * layer + 2 * V * d + n_medusa * (d * d + V * d))
+
+
+# ------------------------------------------------------------------ model / kv
+class Model:
+    def __init__(self, cfg: dict, weights: dict, max_rows: int, max_batch: int, max_seq_len: int):
+        c = ModelCfg(cfg["n_layers"], cfg["d_model"], cfg["n_heads"], cfg["n_kv_heads"], cfg["head_dim"],
+                     cfg["d_ffn"], cfg["vocab"], len(weights["medusa"]), cfg.get("rms_eps", 1e-5),
+                     cfg.get("rope_theta", 1e4), max_rows, max_batch, max_seq_len)
+        L = cfg["n_layers"]
+        arr = lambda key: (ctypes.c_void_p * max(1, L))(*[_ptr(l[key]) for l in weights["layers"]])  # noqa: E731
+        marr = lambda key: (ctypes.c_void_p * max(1, len(weights["medusa"])))(  # noqa: E731
+            *[_ptr(h[key]) for h in weights["medusa"]])
+        self._arrays = [arr(k) for k in ("attn_norm", "wqkv", "wo", "mlp_norm", "wgate_up", "wdown")] + \
+                       [marr(k) for k in ("R", "b", "U")]
+        w = Weights(_ptr(weights["embed"]), _ptr(weights["final_norm"]), _ptr(weights["lm_head"]),
+                    *[ctypes.cast(a, _PP) for a in self._arrays])
+        self._h = ctypes.c_void_p()
+        self.cfg, self.c = cfg, c
+        self.weights = weights          # keep borrowed memory alive
+        _check(lib().sm_model_create(ctypes.byref(c), ctypes.byref(w), None, ctypes.byref(self._h)))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.sm_model_destroy(self._h)
+
+
+def kv_bytes(cfg: dict, batch: int, max_seq_len: int, tree_nodes: int, tp_size: int = 1) -> int:
+    c = ModelCfg(cfg["n_layers"], cfg["d_model"], cfg["n_heads"], cfg["n_kv_heads"], cfg["head_dim"], cfg["d_ffn"],
+                 cfg["vocab"], 0, 1e-5, 1e4, 1, 1, 1)
+    out = ctypes.c_size_t()
+    _check(lib().sm_kv_bytes(ctypes.byref(c), tp_size, batch, max_seq_len, tree_nodes, ctypes.byref(out)))
+    return out.value
+
+
+class AcceptOut:
+    """Device int32 outputs of one step (sm_accept_out)."""
+
+    def __init__(self, batch: int, depth: int, device="cuda"):
+        import torch
+        z = lambda *s: torch.zeros(*s, dtype=torch.int32, device=device)  # noqa: E731
+        self.acc_len, self.best_leaf, self.n_emit, self.status = z(batch), z(batch), z(batch), z(batch)
+        self.path, self.emit_tok = z(batch, depth + 1), z(batch, depth + 1)
+        self.c = AcceptOutC(*[_ptr(t) for t in (self.acc_len, self.best_leaf, self.path, self.emit_tok, self.n_emit,
+                                                 self.status)])
+
+
+def accept_cfg(mode: int = GREEDY, temperature: float = 0.7, eps: float = 0.09, alpha: float = 0.3,
+               max_new=None, forced_path=None) -> AcceptCfg:
+    return AcceptCfg(mode, temperature, eps, alpha, _ptr(max_new), _ptr(forced_path))
+
+
+class KVCache:
+    """Bounded KV cache (Eq. 1 with d + N tree-scratch slots) bound to one tree."""
+
+    def __init__(self, model: Model, tree: Tree, batch: int, max_seq_len: int):
+        import torch
+        self.model, self.tree, self.batch, self.x = model, tree, batch, max_seq_len
+        self.nbytes = kv_bytes(model.cfg, batch, max_seq_len, tree.N)
+        self.mem = torch.empty(self.nbytes // 2, dtype=torch.bfloat16, device="cuda")
+        self._h = ctypes.c_void_p()
+        _check(lib().sm_kv_bind(model._h, tree._h, batch, max_seq_len, ctypes.c_void_p(_ptr(self.mem)),
+                                ctypes.c_size_t(self.nbytes), ctypes.byref(self._h)))
+
+    def layout(self):
+        """[L][2][b][Hkv][x+N][hd] view of the cache memory."""
+        c = self.model.cfg
+        return self.mem.view(c["n_layers"], 2, self.batch, c["n_kv_heads"], self.x + self.tree.N, c["head_dim"])
+
+    def lengths(self) -> np.ndarray:
+        out = np.zeros(self.batch, np.int32)
+        _check(lib().sm_kv_lengths(self._h, out.ctypes.data_as(ctypes.c_void_p)))
+        return out
+
+    def state(self):
+        """(root[b], topk[b][n_medusa][K]) device tensors (views, not copies)."""
+        import torch
+        r, t = ctypes.c_void_p(), ctypes.c_void_p()
+        _check(lib().sm_state_device(self._h, ctypes.byref(r), ctypes.byref(t)))
+        nmed = max(1, self.model.c.n_medusa)
+        return r.value, t.value, nmed
+
+    def prefill(self, seq: int, tokens, stream=None) -> None:
+        _check(lib().sm_prefill(self.model._h, self._h, seq, ctypes.c_void_p(_ptr(tokens)), tokens.numel(),
+                                ctypes.c_void_p(_stream(stream))))
+
+    def propose(self, tree_tok, pos=None, stream=None) -> None:
+        _check(lib().sm_propose(self.model._h, self._h, ctypes.c_void_p(_ptr(tree_tok)), ctypes.c_void_p(_ptr(pos)),
+                                ctypes.c_void_p(_stream(stream))))
+
+    def verify(self, tree_tok, logits=None, stream=None) -> None:
+        _check(lib().sm_verify(self.model._h, self._h, ctypes.c_void_p(_ptr(tree_tok)), ctypes.c_void_p(_ptr(logits)),
+                               ctypes.c_void_p(_stream(stream))))
+
+    def accept(self, cfg: AcceptCfg, out: AcceptOut, stream=None) -> None:
+        _check(lib().sm_accept(self.model._h, self._h, ctypes.byref(cfg), ctypes.byref(out.c),
+                               ctypes.c_void_p(_stream(stream))))
+
+    def step(self, cfg: AcceptCfg, out: AcceptOut, stream=None) -> None:
+        _check(lib().sm_step(self.model._h, self._h, ctypes.byref(cfg), ctypes.byref(out.c),
+                             ctypes.c_void_p(_stream(stream))))
+
+    def step_launches(self) -> int:
+        n = ctypes.c_int()
+        _check(lib().sm_step_launches(self._h, ctypes.byref(n)))
+        return n.value
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.sm_kv_destroy(self._h)
+
+
+# ------------------------------------------------------------------ stage kernels
+def tree_attention(tree: Tree, q, k, v, lengths, n_heads: int, n_kv_heads: int, out, stream=None) -> None:
+    """K1 on caller buffers: q/out [b][N][H][hd], k/v [b][Hkv][cap][hd] bf16, lengths int32 [b]."""
+    b, cap, hd = k.shape[0], k.shape[2], k.shape[3]
+    _check(lib().sm_tree_attention(tree._h, ctypes.c_void_p(_ptr(q)), ctypes.c_void_p(_ptr(k)),
+                                   ctypes.c_void_p(_ptr(v)), ctypes.c_void_p(_ptr(lengths)), b, n_heads, n_kv_heads,
+                                   hd, cap, ctypes.c_void_p(_ptr(out)), ctypes.c_void_p(_stream(stream))))
+
+
+def gemm_bf16(x, w, out, stream=None) -> None:
+    """K2: out[M][N] fp32 = x[M][K] @ w[N][K]^T (tcgen05)."""
+    M, K = x.shape
+    N = w.shape[0]
+    _check(lib().sm_gemm_bf16(ctypes.c_void_p(_ptr(x)), ctypes.c_void_p(_ptr(w)), ctypes.c_void_p(_ptr(out)), M, N, K,
+                              ctypes.c_void_p(_stream(stream))))
+
+
+def topk_f32(logits, k: int, out, stream=None) -> None:
+    rows, V = logits.shape
+    _check(lib().sm_topk_f32(ctypes.c_void_p(_ptr(logits)), rows, V, k, ctypes.c_void_p(_ptr(out)),
+                             ctypes.c_void_p(_stream(stream))))
+
+
+def version() -> str:
+    return lib().sm_version().decode()

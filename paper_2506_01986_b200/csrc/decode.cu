@@ -1,0 +1,258 @@
+// decode.cu -- device-resident control of one speculative step (no host syncs):
+//   propose  (a1, K3)  tree tokens from the heads' top-k at the accepted node
+//   accept   (a4, K4)  greedy / typical tree DP, longest accepted path
+//   compact  (a5, K5)  in-place gather/scatter of the accepted nodes' K/V
+//   commit            Lc += tau, pending root, head input row
+// plus the counter-hash weight generator.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sm {
+
+// ------------------------------------------------------------------ propose
+// tok[n] = root for n = 0, else topk[b][depth(n)-1][rank(n)]
+__global__ void propose_kernel(TreeDev t, const int32_t *root, const int32_t *topk, int K, int nmed, int32_t *tree_tok,
+                               int32_t *pos, const int32_t *len) {
+  const int bb = blockIdx.x, n = threadIdx.x;
+  if (n >= t.N) return;
+  int tok;
+  if (n == 0) {
+    tok = root[bb];
+  } else {
+    tok = topk[((size_t)bb * nmed + (t.depth[n] - 1)) * K + t.rank[n]];
+  }
+  tree_tok[(size_t)bb * t.N + n] = tok;
+  if (pos) pos[(size_t)bb * t.N + n] = len[bb] + t.depth[n];
+}
+cudaError_t propose_launch(TreeDev t, const int32_t *root, const int32_t *topk, int K, int nmed, int b,
+                           int32_t *tree_tok, int32_t *pos, const int32_t *len, cudaStream_t st) {
+  propose_kernel<<<b, 256, 0, st>>>(t, root, topk, K, nmed, tree_tok, pos, len);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ accept (tree DP)
+// acc(0) = 1; acc(c) = acc(parent) & C(parent, c).
+//   greedy : C = tok[c] == argmax z[parent]                        (reading Q9)
+//   typical: C = P_p[tok_c] > min(eps, alpha * exp(-H_p)), P at temperature T,
+//            H = log s - t/s from the single-pass (m, s, t) stats   (Q10)
+// a = deepest accepted depth; among those, max log-likelihood then lowest DFS
+// position (Q11); emission clamped by the turn budget and the KV bound x.
+__global__ void __launch_bounds__(256) accept_kernel(const __grid_constant__ AcceptArgs a) {
+  __shared__ int s_cond[kMaxTreeNodes];
+  __shared__ float s_lp[kMaxTreeNodes];
+  __shared__ int s_chosen;
+  const int bb = blockIdx.x, n = threadIdx.x;
+  const int N = a.t.N;
+  const size_t rowbase = (size_t)bb * N;
+  if (n < N) {
+    int cond = 1;
+    float lp = 0.f;
+    if (n > 0) {
+      const int p = a.t.parent[n];
+      const int tokc = a.tok[rowbase + n];
+      if (a.mode == 0) {
+        cond = tokc == a.argmax[rowbase + p];
+      } else {
+        const float *st = a.stats + 3 * (rowbase + p);
+        const float m = st[0], s = st[1], tt = st[2];
+        const float y = a.z[(rowbase + p) * (size_t)a.V + tokc] * a.inv_temp;
+        const float logs = logf(s);
+        const float logP = (y - m) - logs;
+        const float H = logs - tt / s;
+        const float thr = fminf(a.eps, a.alpha * expf(-H));
+        cond = expf(logP) > thr;
+        lp = logP;
+      }
+    }
+    s_cond[n] = cond;
+    s_lp[n] = lp;
+  }
+  __syncthreads();
+  if (n == 0) {
+    // walk every node's ancestor chain (depth <= l), pick (depth, ll, -dfs) max
+    int best = 0, bdep = 0, bdfs = a.t.dfs_pos[0];
+    float bll = 0.f;
+    if (a.forced_path) {
+      const int32_t *fp = a.forced_path + (size_t)bb * (a.t.l + 1);
+      for (int j = 0; j <= a.t.l; ++j)
+        if (fp[j] >= 0) best = fp[j];
+    } else {
+      for (int c = 1; c < N; ++c) {
+        int ok = 1, x = c;
+        float ll = 0.f;
+        while (x > 0) {
+          ok &= s_cond[x];
+          ll += s_lp[x];
+          x = a.t.parent[x];
+        }
+        if (!ok) continue;
+        const int dep = a.t.depth[c], dfs = a.t.dfs_pos[c];
+        if (dep > bdep || (dep == bdep && (ll > bll || (ll == bll && dfs < bdfs)))) {
+          best = c;
+          bdep = dep;
+          bll = ll;
+          bdfs = dfs;
+        }
+      }
+    }
+    s_chosen = best;
+  }
+  __syncthreads();
+  if (n != 0) return;
+  const int chosen = s_chosen;
+  const int adepth = a.t.depth[chosen];
+  const int L1 = a.t.l + 1;
+  int path[8];
+  {
+    int x = chosen;
+    for (int j = adepth; j >= 0; --j) {
+      path[j] = x;
+      x = a.t.parent[x];
+    }
+  }
+  const int Lc = a.len[bb];
+  const int budget = a.max_new ? a.max_new[bb] : 0x7fffffff;
+  int a_eff, status = 0;
+  if (budget <= 0) {
+    a_eff = -1;
+  } else if (Lc >= a.x_bound) {
+    a_eff = -1;
+    status = 3;  // SM_ERR_KV_CAPACITY
+  } else {
+    a_eff = min(adepth, min(budget - 1, a.x_bound - Lc - 1));
+  }
+  a.acc_len[bb] = adepth;
+  a.best_leaf[bb] = a.t.first_leaf[chosen];
+  for (int j = 0; j < L1; ++j) {
+    a.path[(size_t)bb * L1 + j] = j <= adepth ? path[j] : -1;
+    a.emit_tok[(size_t)bb * L1 + j] = j <= a_eff ? a.tok[rowbase + path[j]] : -1;
+  }
+  a.n_emit[bb] = a_eff + 1;
+  a.status[bb] = status;
+  if (a_eff >= 0) {
+    const int row = (int)rowbase + path[a_eff];
+    a.acc_row[bb] = row;
+    a.root_next[bb] = a.argmax[row];
+  }
+}
+cudaError_t accept_launch(const AcceptArgs &a, cudaStream_t st) {
+  accept_kernel<<<a.b, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ compaction
+// For j = 1..a_eff: K/V[Lc + j] <- K/V[Lc + path[j]] (all layers, kv heads).
+// Reads of every source row complete (barrier) before any write: a parallel
+// copy would otherwise race where path[j'] = j for j' < j.
+// grid = (L * 2, b, Hkv); 16-byte chunks.
+__global__ void compact_kernel(bf16 *kv_base, int b, int Hkv, int cap, int hd, const int32_t *len,
+                               const int32_t *path, int path_ld, const int32_t *n_emit) {
+  const int lk = blockIdx.x, bb = blockIdx.y, h = blockIdx.z;
+  const int a_eff = n_emit[bb] - 1;
+  if (a_eff <= 0) return;
+  const int Lc = len[bb];
+  const int chunks = hd / 8;  // uint4 per row
+  bf16 *base = kv_base + (((size_t)lk * b + bb) * Hkv + h) * (size_t)cap * hd;
+  const int total = a_eff * chunks;
+  uint4 v[2];
+  int cnt = 0;
+  for (int i = threadIdx.x; i < total && cnt < 2; i += blockDim.x, ++cnt) {
+    const int j = 1 + i / chunks, c = i % chunks;
+    const int src = path[(size_t)bb * path_ld + j];
+    v[cnt] = reinterpret_cast<const uint4 *>(base + (size_t)(Lc + src) * hd)[c];
+  }
+  __syncthreads();
+  cnt = 0;
+  for (int i = threadIdx.x; i < total && cnt < 2; i += blockDim.x, ++cnt) {
+    const int j = 1 + i / chunks, c = i % chunks;
+    const int src = path[(size_t)bb * path_ld + j];
+    if (src != j) reinterpret_cast<uint4 *>(base + (size_t)(Lc + j) * hd)[c] = v[cnt];
+  }
+}
+cudaError_t compact_launch(bf16 *kv_base, int L, int b, int Hkv, int cap, int hd, const int32_t *len,
+                           const int32_t *path, int path_ld, const int32_t *n_emit, cudaStream_t st) {
+  // each thread holds up to 2 chunks: threads >= ceil(l * hd/8 / 2)
+  const int threads = 128;  // covers a_eff <= 16 rows at hd = 128 (256 chunks)
+  dim3 grid(L * 2, b, Hkv);
+  compact_kernel<<<grid, threads, 0, st>>>(kv_base, b, Hkv, cap, hd, len, path, path_ld, n_emit);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ commit
+__global__ void commit_kernel(int32_t *len, const int32_t *n_emit, int32_t *root, const int32_t *root_next,
+                              const int32_t *acc_row, const bf16 *hf, int d, bf16 *head_in, int32_t *emitted_total) {
+  const int bb = blockIdx.x;
+  const int ne = n_emit[bb];
+  if (ne <= 0) return;
+  const bf16 *src = hf + (size_t)acc_row[bb] * d;
+  bf16 *dst = head_in + (size_t)bb * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = src[i];
+  if (threadIdx.x == 0) {
+    len[bb] += ne;
+    root[bb] = root_next[bb];
+    if (emitted_total) emitted_total[bb] += ne;
+  }
+}
+cudaError_t commit_launch(int b, int32_t *len, const int32_t *n_emit, int32_t *root, const int32_t *root_next,
+                          const int32_t *acc_row, const bf16 *hf, int d, bf16 *head_in, int32_t *emitted_total,
+                          cudaStream_t st) {
+  commit_kernel<<<b, 256, 0, st>>>(len, n_emit, root, root_next, acc_row, hf, d, head_in, emitted_total);
+  return cudaGetLastError();
+}
+
+__global__ void advance_len_kernel(int32_t *len, int seq, int n) { len[seq] += n; }
+cudaError_t advance_len_launch(int32_t *len, int seq, int n, cudaStream_t st) {
+  advance_len_kernel<<<1, 1, 0, st>>>(len, seq, n);
+  return cudaGetLastError();
+}
+
+__global__ void set_root_kernel(int32_t *root, int seq, const int32_t *argmax_row, const bf16 *hf_row, int d,
+                                bf16 *head_in_row) {
+  if (threadIdx.x == 0) root[seq] = argmax_row[0];
+  for (int i = threadIdx.x; i < d; i += blockDim.x) head_in_row[i] = hf_row[i];
+}
+cudaError_t set_root_launch(int32_t *root, int seq, const int32_t *argmax_row, const bf16 *hf_row, int d,
+                            bf16 *head_in_row, cudaStream_t st) {
+  set_root_kernel<<<1, 256, 0, st>>>(root, seq, argmax_row, hf_row, d, head_in_row);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ weight generator
+SM_DEV uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__global__ void generate_kernel(uint16_t *dst, size_t numel, uint64_t seed, uint64_t stream_id, uint64_t start,
+                                int mode) {
+  const uint64_t base = seed ^ (stream_id << 40);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < numel; i += (size_t)gridDim.x * blockDim.x) {
+    const uint64_t h = splitmix64(base ^ (start + i));
+    float w;
+    if (mode == 0) {
+      const int k = (int)(h >> 40) - (1 << 23);
+      w = __fmul_rn(__fmul_rn((float)k, 1.1920928955078125e-07f /* 2^-23 */), 0.034641016151377546f);
+    } else {
+      float acc = 0.f;
+#pragma unroll
+      for (int sh = 0; sh < 64; sh += 16) {
+        const int k = (int)((h >> sh) & 0xFFFFull) - (1 << 15);
+        acc = __fadd_rn(acc, __fmul_rn((float)k, 3.0517578125e-05f /* 2^-15 */));
+      }
+      w = __fmul_rn(acc, 0.8660254037844386f);
+    }
+    const __nv_bfloat16 b = __float2bfloat16_rn(w);
+    dst[i] = *reinterpret_cast<const uint16_t *>(&b);
+  }
+}
+cudaError_t generate_bf16_launch(void *dst, size_t numel, uint64_t seed, uint64_t stream_id, uint64_t start, int mode,
+                                 cudaStream_t st) {
+  if (numel == 0) return cudaSuccess;
+  size_t blocks = (numel + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  generate_kernel<<<(unsigned)blocks, 256, 0, st>>>(static_cast<uint16_t *>(dst), numel, seed, stream_id, start, mode);
+  return cudaGetLastError();
+}
+
+}  // namespace sm

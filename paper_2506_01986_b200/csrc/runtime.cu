@@ -1,0 +1,968 @@
+// runtime.cu -- host runtime behind the C ABI (include/specmemo.h): tree, model
+// and bounded-KV objects, step orchestration (propose -> verify -> accept ->
+// compact -> next heads) entirely stream-ordered, captured once into a CUDA
+// graph and replayed; lengths live on the device so no step syncs the host.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/specmemo.h"
+#include "kernels.h"
+
+using namespace sm;
+
+static thread_local std::string g_err;
+static sm_status fail(sm_status s, const std::string &msg) {
+  g_err = msg;
+  return s;
+}
+#define CK(call)                                                                                     \
+  do {                                                                                               \
+    cudaError_t e_ = (call);                                                                         \
+    if (e_ != cudaSuccess) return fail(SM_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+#define CKS(call)                       \
+  do {                                  \
+    sm_status s_ = (call);              \
+    if (s_ != SM_OK) return s_;         \
+  } while (0)
+
+// ---------------------------------------------------------------- tensor maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+// 2D bf16 map over [rows][cols] (row-major), box [box_rows][box_cols].
+static sm_status make_tmap(CUtensorMap *m, const void *base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                           uint32_t box_cols, bool sw128) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(SM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t gdim[2] = {cols, rows};
+  cuuint64_t gstride[1] = {cols * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), gdim, gstride, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(SM_ERR_INVALID_ARG, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ") rows=" +
+                                        std::to_string(rows) + " cols=" + std::to_string(cols));
+  return SM_OK;
+}
+static sm_status weight_map(CUtensorMap *m, const void *w, int N, int K) {
+  if (K % 8) return fail(SM_ERR_INVALID_ARG, "GEMM K must be a multiple of 8");
+  return make_tmap(m, w, (uint64_t)N, (uint64_t)K, 128, 64, true);
+}
+static sm_status act_map(CUtensorMap *m, const void *x, int rows, int K) {
+  return make_tmap(m, x, (uint64_t)rows, (uint64_t)K, 16, 64, true);
+}
+static sm_status kv_map(CUtensorMap *m, const void *base, uint64_t rows, int hd) {
+  const bool sw = hd >= 64;
+  return make_tmap(m, base, rows, (uint64_t)hd, 64, sw ? 64 : (uint32_t)hd, sw);
+}
+
+template <typename T>
+static sm_status dalloc(T **p, size_t n, const char *what) {
+  *p = nullptr;
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void **>(p), n * sizeof(T));
+  if (e != cudaSuccess) return fail(SM_ERR_DEVICE_OOM, std::string("Buffer: cudaMalloc ") + what);
+  return SM_OK;
+}
+
+// ---------------------------------------------------------------- tree
+struct sm_tree {
+  int N = 1, S = 1, l = 0, topk = 1;
+  std::vector<std::vector<int>> paths;  // canonical order, root = {}
+  std::vector<int32_t> parent, depth, rank, dfs_pos, first_leaf, leaf_paths;
+  std::vector<uint64_t> anc;  // [N][kAncWords]
+  int32_t *d_parent = nullptr, *d_depth = nullptr, *d_rank = nullptr, *d_dfs = nullptr, *d_first_leaf = nullptr;
+  uint64_t *d_anc = nullptr;
+  bool on_device = false;
+  TreeDev dev() const { return TreeDev{N, S, l, d_parent, d_depth, d_rank, d_dfs, d_first_leaf, d_anc}; }
+};
+
+static sm_status tree_finish(sm_tree *t) {
+  const int N = (int)t->paths.size();
+  t->N = N;
+  std::map<std::vector<int>, int> id;
+  for (int i = 0; i < N; ++i) id[t->paths[i]] = i;
+  t->parent.assign(N, -1);
+  t->depth.assign(N, 0);
+  t->rank.assign(N, -1);
+  t->anc.assign((size_t)N * kAncWords, 0ull);
+  std::vector<int> nchild(N, 0);
+  for (int i = 0; i < N; ++i) {
+    const auto &p = t->paths[i];
+    t->depth[i] = (int)p.size();
+    if (!p.empty()) {
+      t->rank[i] = p.back();
+      t->parent[i] = id[std::vector<int>(p.begin(), p.end() - 1)];
+      nchild[t->parent[i]]++;
+    }
+    for (int x = i; x >= 0; x = (x == 0 ? -1 : t->parent[x])) t->anc[(size_t)i * kAncWords + x / 64] |= 1ull << (x % 64);
+  }
+  t->l = N ? *std::max_element(t->depth.begin(), t->depth.end()) : 0;
+  // DFS order = lexicographic order of rank paths
+  std::vector<int> order(N);
+  for (int i = 0; i < N; ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return t->paths[a] < t->paths[b]; });
+  t->dfs_pos.assign(N, 0);
+  for (int i = 0; i < N; ++i) t->dfs_pos[order[i]] = i;
+  std::vector<int> leaves;
+  for (int i : order)
+    if (nchild[i] == 0) leaves.push_back(i);
+  t->S = (int)leaves.size();
+  t->first_leaf.assign(N, 0);
+  for (int n = 0; n < N; ++n) {
+    const auto &pn = t->paths[n];
+    for (int li = 0; li < t->S; ++li) {
+      const auto &pl = t->paths[leaves[li]];
+      if (pl.size() >= pn.size() && std::equal(pn.begin(), pn.end(), pl.begin())) {
+        t->first_leaf[n] = li;
+        break;
+      }
+    }
+  }
+  t->leaf_paths.assign((size_t)t->S * (t->l + 1), -1);
+  for (int li = 0; li < t->S; ++li) {
+    int x = leaves[li];
+    for (int j = t->depth[x]; j >= 0; --j, x = t->parent[x]) t->leaf_paths[(size_t)li * (t->l + 1) + j] = x;
+  }
+  return SM_OK;
+}
+
+static sm_status tree_upload(sm_tree *t) {
+  if (t->on_device) return SM_OK;
+  const int N = t->N;
+  CKS(dalloc(&t->d_parent, N, "tree"));
+  CKS(dalloc(&t->d_depth, N, "tree"));
+  CKS(dalloc(&t->d_rank, N, "tree"));
+  CKS(dalloc(&t->d_dfs, N, "tree"));
+  CKS(dalloc(&t->d_first_leaf, N, "tree"));
+  CKS(dalloc(&t->d_anc, (size_t)N * kAncWords, "tree"));
+  CK(cudaMemcpy(t->d_parent, t->parent.data(), N * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(t->d_depth, t->depth.data(), N * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(t->d_rank, t->rank.data(), N * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(t->d_dfs, t->dfs_pos.data(), N * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(t->d_first_leaf, t->first_leaf.data(), N * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(t->d_anc, t->anc.data(), (size_t)N * kAncWords * 8, cudaMemcpyHostToDevice));
+  t->on_device = true;
+  return SM_OK;
+}
+
+extern "C" sm_status sm_tree_create(const int32_t *ranks_flat, const int32_t *path_offsets, int n_paths, int topk,
+                                    sm_tree **out) {
+  if (!out || n_paths < 0 || topk < 1 || (n_paths > 0 && (!ranks_flat || !path_offsets)))
+    return fail(SM_ERR_INVALID_ARG, "sm_tree_create: bad arguments");
+  if (n_paths + 1 > kMaxTreeNodes) return fail(SM_ERR_INVALID_ARG, "sm_tree_create: more than 256 nodes");
+  std::vector<std::vector<int>> ps;
+  for (int i = 0; i < n_paths; ++i) {
+    const int a = path_offsets[i], b = path_offsets[i + 1];
+    if (b <= a) return fail(SM_ERR_INFEASIBLE_TREE, "empty path");
+    std::vector<int> p(ranks_flat + a, ranks_flat + b);
+    for (int r : p)
+      if (r < 0 || r >= topk) return fail(SM_ERR_INFEASIBLE_TREE, "rank out of range");
+    ps.push_back(p);
+  }
+  std::sort(ps.begin(), ps.end(), [](const std::vector<int> &a, const std::vector<int> &b) {
+    return a.size() != b.size() ? a.size() < b.size() : a < b;
+  });
+  for (size_t i = 1; i < ps.size(); ++i)
+    if (ps[i] == ps[i - 1]) return fail(SM_ERR_INFEASIBLE_TREE, "duplicate path");
+  std::map<std::vector<int>, int> have;
+  for (auto &p : ps) have[p] = 1;
+  for (auto &p : ps)
+    if (p.size() > 1 && !have.count(std::vector<int>(p.begin(), p.end() - 1)))
+      return fail(SM_ERR_INFEASIBLE_TREE, "orphan path");
+  sm_tree *t = new sm_tree();
+  t->topk = topk;
+  t->paths.push_back({});
+  for (auto &p : ps) t->paths.push_back(p);
+  tree_finish(t);
+  *out = t;
+  return SM_OK;
+}
+
+extern "C" sm_status sm_tree_create_chain(int n, sm_tree **out) {
+  if (!out || n < 1 || n > kMaxTreeNodes) return fail(SM_ERR_INVALID_ARG, "sm_tree_create_chain: 1 <= n <= 256");
+  sm_tree *t = new sm_tree();
+  t->topk = 1;
+  for (int i = 0; i < n; ++i) t->paths.push_back(std::vector<int>(i, 0));
+  tree_finish(t);
+  *out = t;
+  return SM_OK;
+}
+
+extern "C" sm_status sm_tree_query(const sm_tree *t, int *N, int *S, int *depth, int32_t *parent, int32_t *node_depth,
+                                   int32_t *rank, uint64_t *anc_bits, int32_t *leaf_paths) {
+  if (!t) return fail(SM_ERR_INVALID_ARG, "sm_tree_query: null tree");
+  if (N) *N = t->N;
+  if (S) *S = t->S;
+  if (depth) *depth = t->l;
+  if (parent) std::memcpy(parent, t->parent.data(), t->N * 4);
+  if (node_depth) std::memcpy(node_depth, t->depth.data(), t->N * 4);
+  if (rank) std::memcpy(rank, t->rank.data(), t->N * 4);
+  if (anc_bits) std::memcpy(anc_bits, t->anc.data(), (size_t)t->N * kAncWords * 8);
+  if (leaf_paths) std::memcpy(leaf_paths, t->leaf_paths.data(), t->leaf_paths.size() * 4);
+  return SM_OK;
+}
+
+extern "C" void sm_tree_destroy(sm_tree *t) {
+  if (!t) return;
+  if (!t->on_device) {
+    delete t;
+    return;
+  }
+  cudaFree(t->d_parent);
+  cudaFree(t->d_depth);
+  cudaFree(t->d_rank);
+  cudaFree(t->d_dfs);
+  cudaFree(t->d_first_leaf);
+  cudaFree(t->d_anc);
+  delete t;
+}
+
+// ---------------------------------------------------------------- model
+struct sm_model {
+  sm_model_cfg cfg;
+  int L, d, H, Hkv, hd, F, V, nmed, G, R, B, qkv_n;
+  const bf16 *embed, *final_norm, *lm_head;
+  std::vector<const bf16 *> attn_norm, wqkv, wo, mlp_norm, wgu, wdown, mR, mb, mU;
+  // workspace
+  float *x = nullptr, *part = nullptr, *z = nullptr, *stats = nullptr;
+  bf16 *h = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr, *hf = nullptr, *head_in = nullptr,
+       *r_buf = nullptr;
+  int32_t *argmax = nullptr;
+  float2 *rope = nullptr;
+  size_t part_elems = 0;
+  // GEMM prototypes (tensor maps prebuilt)
+  std::vector<GemmArgs> g_qkv, g_o, g_gu, g_down;
+  GemmArgs g_lm, g_R, g_U;
+  sm_tree *chain = nullptr;
+  cudaStream_t cap_stream = nullptr;
+};
+
+static GemmArgs gemm_proto(int N, int K, int batch) {
+  GemmArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.N = N;
+  a.K = K;
+  a.batch = batch;
+  return a;
+}
+// elements of the partial buffer a GEMM needs at `ld_rows` rows per split slice
+static size_t gemm_part_elems(const GemmArgs &proto, int M, int ld_rows) {
+  GemmArgs a = proto;
+  gemm_plan(a, proto.N, proto.K, M, proto.batch);
+  return (size_t)a.batch * a.splits * ld_rows * proto.N;
+}
+
+struct GemmRun {
+  int splits;
+  long long split_stride;
+  long long batch_stride;
+};
+static sm_status run_gemm(const GemmArgs &proto, int M, int ld_rows, int x_row0, float *out, cudaStream_t st,
+                          GemmRun *info, int &nl) {
+  GemmArgs a = proto;
+  gemm_plan(a, proto.N, proto.K, M, proto.batch);
+  a.ldo = proto.N;
+  a.x_row0 = x_row0;
+  a.split_stride = (long long)ld_rows * proto.N;
+  const long long bstride = (long long)a.splits * a.split_stride;
+  for (int i = 0; i < a.batch; ++i) a.out[i] = out + i * bstride;
+  CK(gemm_launch(a, st));
+  ++nl;
+  if (info) *info = GemmRun{a.splits, a.split_stride, bstride};
+  return SM_OK;
+}
+
+extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *w, const sm_dist *dist,
+                                     sm_model **out) {
+  if (!cfg || !w || !out) return fail(SM_ERR_INVALID_ARG, "sm_model_create: null argument");
+  if (dist && dist->tp_size > 1)
+    return fail(SM_ERR_UNSUPPORTED, "tensor parallelism (tp_size > 1) is not built in this version");
+  const sm_model_cfg &c = *cfg;
+  if (c.n_layers < 1 || c.d_model % 64 || c.n_heads < 1 || c.n_kv_heads < 1 || c.n_heads % c.n_kv_heads ||
+      (c.head_dim != 16 && c.head_dim != 32 && c.head_dim != 64 && c.head_dim != 128) || c.d_ffn % 64 ||
+      c.vocab % 4 || c.n_medusa < 0 || c.n_medusa > kMaxGemmBatch || c.max_rows < 1 || c.max_rows > 256 ||
+      c.max_batch < 1 || c.max_seq_len < 1 || (c.n_heads * c.head_dim) % 64)
+    return fail(SM_ERR_INVALID_ARG, "sm_model_create: unsupported shape (d, F multiple of 64; hd in {16,32,64,128}; "
+                                    "max_rows <= 256; n_medusa <= 5)");
+  if (c.vocab * 4 > 200 * 1024) return fail(SM_ERR_INVALID_ARG, "vocab too large for the shared-memory top-k");
+  sm_model *m = new sm_model();
+  m->cfg = c;
+  m->L = c.n_layers;
+  m->d = c.d_model;
+  m->H = c.n_heads;
+  m->Hkv = c.n_kv_heads;
+  m->hd = c.head_dim;
+  m->F = c.d_ffn;
+  m->V = c.vocab;
+  m->nmed = c.n_medusa;
+  m->G = c.n_heads / c.n_kv_heads;
+  m->R = c.max_rows;
+  m->B = c.max_batch;
+  m->qkv_n = (c.n_heads + 2 * c.n_kv_heads) * c.head_dim;
+  m->embed = (const bf16 *)w->embed;
+  m->final_norm = (const bf16 *)w->final_norm;
+  m->lm_head = (const bf16 *)w->lm_head;
+  for (int l = 0; l < m->L; ++l) {
+    m->attn_norm.push_back((const bf16 *)w->attn_norm[l]);
+    m->wqkv.push_back((const bf16 *)w->wqkv[l]);
+    m->wo.push_back((const bf16 *)w->wo[l]);
+    m->mlp_norm.push_back((const bf16 *)w->mlp_norm[l]);
+    m->wgu.push_back((const bf16 *)w->wgate_up[l]);
+    m->wdown.push_back((const bf16 *)w->wdown[l]);
+  }
+  for (int i = 0; i < m->nmed; ++i) {
+    m->mR.push_back((const bf16 *)w->medusa_R[i]);
+    m->mb.push_back((const bf16 *)w->medusa_b[i]);
+    m->mU.push_back((const bf16 *)w->medusa_U[i]);
+  }
+  const int R = m->R, B = m->B, d = m->d, Hhd = m->H * m->hd;
+  sm_status s;
+#define ALLOC(p, n, what)                 \
+  if ((s = dalloc(&p, n, what)) != SM_OK) { \
+    sm_model_destroy(m);                  \
+    return s;                             \
+  }
+  ALLOC(m->x, (size_t)R * d, "x");
+  ALLOC(m->h, (size_t)R * d, "h");
+  ALLOC(m->q, (size_t)R * Hhd, "q");
+  ALLOC(m->attn, (size_t)R * Hhd, "attn");
+  ALLOC(m->act, (size_t)R * m->F, "act");
+  ALLOC(m->hf, (size_t)R * d, "hf");
+  ALLOC(m->z, (size_t)R * m->V, "logits");
+  ALLOC(m->argmax, (size_t)R, "argmax");
+  ALLOC(m->stats, (size_t)R * 3, "stats");
+  ALLOC(m->head_in, (size_t)B * d, "head_in");
+  ALLOC(m->r_buf, (size_t)std::max(1, m->nmed) * B * d, "r_buf");
+  ALLOC(m->rope, (size_t)c.max_seq_len * (m->hd / 2), "rope");
+  cudaMemset(m->x, 0, (size_t)R * d * 4);
+  cudaMemset(m->h, 0, (size_t)R * d * 2);
+  cudaMemset(m->attn, 0, (size_t)R * Hhd * 2);
+  cudaMemset(m->act, 0, (size_t)R * m->F * 2);
+  cudaMemset(m->hf, 0, (size_t)R * d * 2);
+  cudaMemset(m->head_in, 0, (size_t)B * d * 2);
+  cudaMemset(m->r_buf, 0, (size_t)std::max(1, m->nmed) * B * d * 2);
+  // RoPE table: cos/sin built in fp64, stored fp32 (rounding contract R3)
+  {
+    const int half = m->hd / 2;
+    std::vector<float2> tab((size_t)c.max_seq_len * half);
+    for (int p = 0; p < c.max_seq_len; ++p)
+      for (int i = 0; i < half; ++i) {
+        const double ang = (double)p * std::pow((double)c.rope_theta, -2.0 * i / (double)m->hd);
+        tab[(size_t)p * half + i] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+      }
+    if (cudaMemcpy(m->rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice) != cudaSuccess) {
+      sm_model_destroy(m);
+      return fail(SM_ERR_CUDA, "rope upload");
+    }
+  }
+  // GEMM prototypes
+  auto mk = [&](const void *wp, int N, int K, const void *xp, int xrows, GemmArgs &a) -> sm_status {
+    a = gemm_proto(N, K, 1);
+    CKS(weight_map(&a.tmW[0], wp, N, K));
+    CKS(act_map(&a.tmX[0], xp, xrows, K));
+    return SM_OK;
+  };
+  size_t need = 0;
+  for (int l = 0; l < m->L && s == SM_OK; ++l) {
+    GemmArgs a;
+    if ((s = mk(m->wqkv[l], m->qkv_n, d, m->h, R, a)) != SM_OK) break;
+    m->g_qkv.push_back(a);
+    need = std::max(need, gemm_part_elems(a, R, R));
+    if ((s = mk(m->wo[l], d, Hhd, m->attn, R, a)) != SM_OK) break;
+    m->g_o.push_back(a);
+    need = std::max(need, gemm_part_elems(a, R, R));
+    if ((s = mk(m->wgu[l], 2 * m->F, d, m->h, R, a)) != SM_OK) break;
+    m->g_gu.push_back(a);
+    need = std::max(need, gemm_part_elems(a, R, R));
+    if ((s = mk(m->wdown[l], d, m->F, m->act, R, a)) != SM_OK) break;
+    m->g_down.push_back(a);
+    need = std::max(need, gemm_part_elems(a, R, R));
+  }
+  if (s == SM_OK) s = mk(m->lm_head, m->V, d, m->hf, R, m->g_lm);
+  if (s != SM_OK) {
+    sm_model_destroy(m);
+    return s;
+  }
+  need = std::max(need, gemm_part_elems(m->g_lm, R, R));
+  if (m->nmed > 0) {
+    m->g_R = gemm_proto(d, d, m->nmed);
+    m->g_U = gemm_proto(m->V, d, m->nmed);
+    for (int i = 0; i < m->nmed && s == SM_OK; ++i) {
+      if ((s = weight_map(&m->g_R.tmW[i], m->mR[i], d, d)) != SM_OK) break;
+      if ((s = act_map(&m->g_R.tmX[i], m->head_in, B, d)) != SM_OK) break;
+      if ((s = weight_map(&m->g_U.tmW[i], m->mU[i], m->V, d)) != SM_OK) break;
+      s = act_map(&m->g_U.tmX[i], m->r_buf + (size_t)i * B * d, B, d);
+    }
+    if (s != SM_OK) {
+      sm_model_destroy(m);
+      return s;
+    }
+    need = std::max(need, gemm_part_elems(m->g_R, B, B));
+    need = std::max(need, gemm_part_elems(m->g_U, B, B));
+  }
+  m->part_elems = need;
+  ALLOC(m->part, need, "gemm partials");
+#undef ALLOC
+  if ((s = sm_tree_create_chain(R, &m->chain)) != SM_OK || (s = tree_upload(m->chain)) != SM_OK) {
+    sm_model_destroy(m);
+    return s;
+  }
+  if (cudaStreamCreateWithFlags(&m->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    sm_model_destroy(m);
+    return fail(SM_ERR_CUDA, "stream create");
+  }
+  *out = m;
+  return SM_OK;
+}
+
+extern "C" void sm_model_destroy(sm_model *m) {
+  if (!m) return;
+  cudaFree(m->x);
+  cudaFree(m->part);
+  cudaFree(m->z);
+  cudaFree(m->stats);
+  cudaFree(m->h);
+  cudaFree(m->q);
+  cudaFree(m->attn);
+  cudaFree(m->act);
+  cudaFree(m->hf);
+  cudaFree(m->head_in);
+  cudaFree(m->r_buf);
+  cudaFree(m->argmax);
+  cudaFree(m->rope);
+  if (m->chain) sm_tree_destroy(m->chain);
+  if (m->cap_stream) cudaStreamDestroy(m->cap_stream);
+  delete m;
+}
+
+extern "C" sm_status sm_generate_bf16(void *dst, size_t numel, uint64_t seed, uint64_t stream_id, uint64_t start,
+                                      int mode, void *stream) {
+  if (!dst && numel) return fail(SM_ERR_INVALID_ARG, "sm_generate_bf16: null dst");
+  CK(generate_bf16_launch(dst, numel, seed, stream_id, start, mode, (cudaStream_t)stream));
+  return SM_OK;
+}
+
+// ---------------------------------------------------------------- bounded KV
+struct GraphKey {
+  int mode;
+  float T, eps, alpha;
+  const void *max_new, *forced, *o0, *o1, *o2, *o3, *o4, *o5;
+  bool operator<(const GraphKey &o) const {
+    return std::tie(mode, T, eps, alpha, max_new, forced, o0, o1, o2, o3, o4, o5) <
+           std::tie(o.mode, o.T, o.eps, o.alpha, o.max_new, o.forced, o.o0, o.o1, o.o2, o.o3, o.o4, o.o5);
+  }
+};
+
+struct sm_kv {
+  sm_model *m;
+  sm_tree *t;  // private copy of the tree
+  int b, x, cap, N;
+  bf16 *base;
+  size_t bytes;
+  int32_t *len = nullptr, *root = nullptr, *topk = nullptr, *acc_row = nullptr, *root_next = nullptr,
+          *emitted = nullptr, *tree_tok = nullptr;
+  float *att_o = nullptr, *att_ml = nullptr;
+  int att_nsplit_max = 16;
+  CUtensorMap tmKV;
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+  int step_launches = 0;
+  cudaStream_t last_stream = nullptr;
+};
+
+static size_t kv_elems_per_layer(const sm_model_cfg *c, int tp, int b, int cap) {
+  return (size_t)2 * b * (c->n_kv_heads / tp) * (size_t)cap * c->head_dim;
+}
+
+extern "C" sm_status sm_kv_bytes(const sm_model_cfg *cfg, int tp_size, int batch, int max_seq_len, int tree_nodes,
+                                 size_t *bytes) {
+  if (!cfg || !bytes || tp_size < 1 || batch < 1 || max_seq_len < 1 || tree_nodes < 1 ||
+      cfg->n_kv_heads % tp_size)
+    return fail(SM_ERR_INVALID_ARG, "sm_kv_bytes: bad arguments");
+  *bytes = kv_elems_per_layer(cfg, tp_size, batch, max_seq_len + tree_nodes) * cfg->n_layers * 2;
+  return SM_OK;
+}
+
+extern "C" sm_status sm_kv_bind(sm_model *m, const sm_tree *tree, int batch, int max_seq_len, void *d_mem,
+                                size_t bytes, sm_kv **out) {
+  if (!m || !tree || !d_mem || !out || batch < 1 || batch > m->B || max_seq_len < 1)
+    return fail(SM_ERR_INVALID_ARG, "sm_kv_bind: bad arguments");
+  if (tree->l > m->nmed) return fail(SM_ERR_INFEASIBLE_TREE, "tree depth exceeds the number of Medusa heads");
+  if (tree->topk > 32) return fail(SM_ERR_INVALID_ARG, "topk > 32");
+  if (batch * tree->N > m->R) return fail(SM_ERR_INVALID_ARG, "batch * tree nodes exceeds max_rows");
+  size_t need;
+  CKS(sm_kv_bytes(&m->cfg, 1, batch, max_seq_len, tree->N, &need));
+  if (bytes < need) return fail(SM_ERR_KV_CAPACITY, "Cache: KV memory smaller than sm_kv_bytes");
+  if (max_seq_len + tree->N > m->cfg.max_seq_len)
+    return fail(SM_ERR_INVALID_ARG, "max_seq_len + N exceeds the model's RoPE table (cfg.max_seq_len)");
+  sm_kv *kv = new sm_kv();
+  kv->m = m;
+  kv->t = new sm_tree(*tree);
+  kv->t->on_device = false;
+  kv->b = batch;
+  kv->x = max_seq_len;
+  kv->N = tree->N;
+  kv->cap = max_seq_len + tree->N;
+  kv->base = (bf16 *)d_mem;
+  kv->bytes = need;
+  sm_status s;
+  if ((s = tree_upload(kv->t)) != SM_OK || (s = dalloc(&kv->len, batch, "len")) != SM_OK ||
+      (s = dalloc(&kv->root, batch, "root")) != SM_OK ||
+      (s = dalloc(&kv->topk, (size_t)batch * std::max(1, m->nmed) * kv->t->topk, "topk")) != SM_OK ||
+      (s = dalloc(&kv->acc_row, batch, "acc_row")) != SM_OK ||
+      (s = dalloc(&kv->root_next, batch, "root_next")) != SM_OK ||
+      (s = dalloc(&kv->emitted, batch, "emitted")) != SM_OK ||
+      (s = dalloc(&kv->tree_tok, (size_t)batch * kv->N, "tree_tok")) != SM_OK ||
+      (s = dalloc(&kv->att_o, (size_t)kv->att_nsplit_max * m->R * m->H * m->hd, "attn partials")) != SM_OK ||
+      (s = dalloc(&kv->att_ml, (size_t)kv->att_nsplit_max * m->R * m->H * 2, "attn partials")) != SM_OK) {
+    sm_kv_destroy(kv);
+    return s;
+  }
+  const uint64_t rows = (uint64_t)need / 2 / m->hd;
+  if ((s = kv_map(&kv->tmKV, d_mem, rows, m->hd)) != SM_OK) {
+    sm_kv_destroy(kv);
+    return s;
+  }
+  cudaMemset(d_mem, 0, need);  // finite contents everywhere (masked keys still meet P = 0 * V)
+  cudaMemset(kv->len, 0, batch * 4);
+  cudaMemset(kv->root, 0, batch * 4);
+  cudaMemset(kv->topk, 0, (size_t)batch * std::max(1, m->nmed) * kv->t->topk * 4);
+  cudaMemset(kv->emitted, 0, batch * 4);
+  cudaMemset(kv->acc_row, 0, batch * 4);
+  cudaMemset(kv->root_next, 0, batch * 4);
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    sm_kv_destroy(kv);
+    return fail(SM_ERR_CUDA, "kv bind memset");
+  }
+  *out = kv;
+  return SM_OK;
+}
+
+extern "C" void sm_kv_destroy(sm_kv *kv) {
+  if (!kv) return;
+  for (auto &g : kv->graphs) cudaGraphExecDestroy(g.second);
+  cudaFree(kv->len);
+  cudaFree(kv->root);
+  cudaFree(kv->topk);
+  cudaFree(kv->acc_row);
+  cudaFree(kv->root_next);
+  cudaFree(kv->emitted);
+  cudaFree(kv->tree_tok);
+  cudaFree(kv->att_o);
+  cudaFree(kv->att_ml);
+  if (kv->t) sm_tree_destroy(kv->t);
+  delete kv;
+}
+
+extern "C" sm_status sm_kv_lengths_device(const sm_kv *kv, int32_t **d_len) {
+  if (!kv || !d_len) return fail(SM_ERR_INVALID_ARG, "null");
+  *d_len = kv->len;
+  return SM_OK;
+}
+extern "C" sm_status sm_kv_lengths(const sm_kv *kv, int32_t *h_len) {
+  if (!kv || !h_len) return fail(SM_ERR_INVALID_ARG, "null");
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(h_len, kv->len, kv->b * 4, cudaMemcpyDeviceToHost));
+  return SM_OK;
+}
+extern "C" sm_status sm_state_device(const sm_kv *kv, int32_t **d_root, int32_t **d_topk) {
+  if (!kv) return fail(SM_ERR_INVALID_ARG, "null");
+  if (d_root) *d_root = kv->root;
+  if (d_topk) *d_topk = kv->topk;
+  return SM_OK;
+}
+
+// ---------------------------------------------------------------- forward (a2 + a3)
+static void attn_plan(const sm_model *m, const sm_kv *kv, int nseq, int Nq, int &chunk, int &nsplit) {
+  const int units = nseq * m->Hkv * attention_row_blocks(Nq, m->G);
+  const int want = std::max(1, (2 * kNumSMs + units - 1) / units);
+  const int T = kv->cap;
+  auto up64 = [](int v) { return (v + 63) / 64 * 64; };
+  chunk = std::max(64, up64((T + want - 1) / want));
+  chunk = std::max(chunk, up64((T + kv->att_nsplit_max - 1) / kv->att_nsplit_max));
+  nsplit = (T + chunk - 1) / chunk;
+}
+
+// tokens d_tok [nseq * Nq] -> hf [nseq * Nq][d]; K/V rows of every layer written
+static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, int nseq, int seq_base, int Nq,
+                                 const TreeDev &tree, cudaStream_t st, int &nl) {
+  const int M = nseq * Nq;
+  const int d = m->d;
+  GemmRun gr;
+  CK(embed_launch(d_tok, m->embed, m->x, M, d, st));
+  ++nl;
+  int chunk, nsplit;
+  attn_plan(m, kv, nseq, Nq, chunk, nsplit);
+  const long long layer_rows = (long long)2 * kv->b * m->Hkv * kv->cap;
+  const long long half_rows = (long long)kv->b * m->Hkv * kv->cap;
+  RowCtx rc{M, Nq, seq_base, kv->len, tree.depth};
+  const float *prev_part = nullptr;
+  GemmRun prev{0, 0, 0};
+  for (int l = 0; l < m->L; ++l) {
+    CK(resid_norm_launch(prev_part, prev.splits, prev.split_stride, d, m->x, m->attn_norm[l], m->h, M, d,
+                         m->cfg.rms_eps, st));
+    ++nl;
+    CKS(run_gemm(m->g_qkv[l], M, m->R, 0, m->part, st, &gr, nl));
+    bf16 *kc = kv->base + (size_t)l * layer_rows * m->hd;
+    bf16 *vc = kc + (size_t)half_rows * m->hd;
+    CK(qkv_epilogue_launch(m->part, gr.splits, gr.split_stride, m->qkv_n, rc, m->H, m->Hkv, m->hd, m->rope, m->q,
+                           kc, vc, kv->cap, st));
+    ++nl;
+    AttnArgs aa;
+    std::memset(&aa, 0, sizeof(aa));
+    aa.tmK = kv->tmKV;
+    aa.tmV = kv->tmKV;
+    aa.q = m->q;
+    aa.out = m->attn;
+    aa.part_o = kv->att_o;
+    aa.part_ml = kv->att_ml;
+    aa.len = kv->len;
+    aa.anc = tree.anc;
+    aa.k_row0 = (long long)l * layer_rows;
+    aa.v_row0 = aa.k_row0 + half_rows;
+    aa.seq_rows = (long long)m->Hkv * kv->cap;
+    aa.cap = kv->cap;
+    aa.Nq = Nq;
+    aa.H = m->H;
+    aa.Hkv = m->Hkv;
+    aa.G = m->G;
+    aa.nseq = nseq;
+    aa.seq_base = seq_base;
+    aa.chunk = chunk;
+    aa.nsplit = nsplit;
+    aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)m->hd));
+    CK(attention_launch(aa, m->hd, st));
+    nl += nsplit > 1 ? 2 : 1;
+    CKS(run_gemm(m->g_o[l], M, m->R, 0, m->part, st, &gr, nl));
+    CK(resid_norm_launch(m->part, gr.splits, gr.split_stride, d, m->x, m->mlp_norm[l], m->h, M, d, m->cfg.rms_eps,
+                         st));
+    ++nl;
+    CKS(run_gemm(m->g_gu[l], M, m->R, 0, m->part, st, &gr, nl));
+    CK(silu_mul_launch(m->part, gr.splits, gr.split_stride, 2 * m->F, m->F, m->act, M, st));
+    ++nl;
+    CKS(run_gemm(m->g_down[l], M, m->R, 0, m->part, st, &gr, nl));
+    prev_part = m->part;
+    prev = gr;
+  }
+  CK(resid_norm_launch(prev_part, prev.splits, prev.split_stride, d, m->x, m->final_norm, m->hf, M, d,
+                       m->cfg.rms_eps, st));
+  ++nl;
+  return SM_OK;
+}
+
+// heads at rows [row0, row0 + nb) of head_in -> topk rows [row0, row0 + nb)
+static sm_status enqueue_heads(sm_model *m, sm_kv *kv, int row0, int nb, cudaStream_t st, int &nl) {
+  if (m->nmed == 0 || kv->t->l == 0) return SM_OK;
+  const int d = m->d, B = m->B;
+  GemmRun gr;
+  CKS(run_gemm(m->g_R, nb, B, row0, m->part, st, &gr, nl));
+  CK(heads_epilogue_grouped_launch(m->part, gr.splits, gr.split_stride, d, gr.batch_stride, m->nmed, nb, d,
+                                   m->head_in + (size_t)row0 * d, m->mb.data(), m->r_buf + (size_t)row0 * d,
+                                   (long long)B * d, st));
+  ++nl;
+  CKS(run_gemm(m->g_U, nb, B, row0, m->part, st, &gr, nl));
+  const int K = kv->t->topk;
+  CK(topk_grouped_launch(m->part, gr.splits, gr.split_stride, m->V, m->V, m->nmed, nb, gr.batch_stride, K,
+                         kv->topk + (size_t)row0 * m->nmed * K, m->nmed * K, st));
+  ++nl;
+  return SM_OK;
+}
+
+extern "C" sm_status sm_prefill(sm_model *m, sm_kv *kv, int seq, const int32_t *d_tokens, int n, void *stream) {
+  if (!m || !kv || seq < 0 || seq >= kv->b || (n > 0 && !d_tokens) || n < 0)
+    return fail(SM_ERR_INVALID_ARG, "sm_prefill: bad arguments");
+  if (n == 0) return SM_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int32_t Lc = 0;
+  CK(cudaStreamSynchronize(st));
+  CK(cudaMemcpy(&Lc, kv->len + seq, 4, cudaMemcpyDeviceToHost));
+  if (Lc + n > kv->x) return fail(SM_ERR_KV_CAPACITY, "Cache: prefill would exceed the KV bound x");
+  int nl = 0;
+  const TreeDev chain = m->chain->dev();
+  const int R = m->R;
+  int done = 0, last = 0;
+  while (done < n) {
+    const int P = std::min(R, n - done);
+    CKS(enqueue_forward(m, kv, d_tokens + done, 1, seq, P, chain, st, nl));
+    CK(advance_len_launch(kv->len, seq, P, st));
+    done += P;
+    last = P;
+  }
+  // last token: LM head row, pending root, heads' top-k (reading Q8)
+  GemmRun gr;
+  CKS(run_gemm(m->g_lm, 1, R, last - 1, m->part, st, &gr, nl));
+  CK(logits_finalize_launch(m->part, gr.splits, gr.split_stride, m->V, m->V, nullptr, 1, 1.0f, m->z, m->V,
+                            m->argmax, m->stats, st));
+  CK(set_root_launch(kv->root, seq, m->argmax, m->hf + (size_t)(last - 1) * m->d, m->d,
+                     m->head_in + (size_t)seq * m->d, st));
+  CKS(enqueue_heads(m, kv, seq, 1, st, nl));
+  CK(cudaGetLastError());
+  kv->last_stream = st;
+  return SM_OK;
+}
+
+static sm_status enqueue_propose(sm_model *m, sm_kv *kv, int32_t *tree_tok, int32_t *pos, cudaStream_t st, int &nl) {
+  CK(propose_launch(kv->t->dev(), kv->root, kv->topk, kv->t->topk, std::max(1, m->nmed), kv->b, tree_tok, pos,
+                    kv->len, st));
+  ++nl;
+  return SM_OK;
+}
+
+static sm_status enqueue_verify(sm_model *m, sm_kv *kv, const int32_t *tree_tok, cudaStream_t st, int &nl) {
+  const int M = kv->b * kv->N;
+  CKS(enqueue_forward(m, kv, tree_tok, kv->b, 0, kv->N, kv->t->dev(), st, nl));
+  GemmRun gr;
+  CKS(run_gemm(m->g_lm, M, m->R, 0, m->part, st, &gr, nl));
+  CK(logits_finalize_launch(m->part, gr.splits, gr.split_stride, m->V, m->V, nullptr, M, 1.0f, m->z, m->V, m->argmax,
+                            m->stats, st));
+  ++nl;
+  return SM_OK;
+}
+
+static sm_status enqueue_accept(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, const sm_accept_out *o,
+                                cudaStream_t st, int &nl) {
+  const int M = kv->b * kv->N;
+  float inv_temp = 1.0f;
+  if (cfg->mode == SM_ACCEPT_TYPICAL) {
+    inv_temp = 1.0f / cfg->temperature;
+    // typical statistics at temperature T on the stored logits (one fp32 pass)
+    CK(logits_finalize_launch(m->z, 1, 0, m->V, m->V, nullptr, M, inv_temp, nullptr, m->V, m->argmax, m->stats, st));
+    ++nl;
+  }
+  AcceptArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.t = kv->t->dev();
+  a.b = kv->b;
+  a.K = kv->t->topk;
+  a.V = m->V;
+  a.x_bound = kv->x;
+  a.mode = cfg->mode == SM_ACCEPT_TYPICAL ? 1 : 0;
+  a.inv_temp = inv_temp;
+  a.eps = cfg->eps;
+  a.alpha = cfg->alpha;
+  a.tok = kv->tree_tok;
+  a.argmax = m->argmax;
+  a.stats = m->stats;
+  a.z = m->z;
+  a.len = kv->len;
+  a.max_new = cfg->d_max_new;
+  a.forced_path = cfg->d_forced_path;
+  a.acc_len = o->acc_len;
+  a.best_leaf = o->best_leaf;
+  a.path = o->path;
+  a.emit_tok = o->emit_tok;
+  a.n_emit = o->n_emit;
+  a.status = o->status;
+  a.acc_row = kv->acc_row;
+  a.root_next = kv->root_next;
+  CK(accept_launch(a, st));
+  ++nl;
+  CK(compact_launch(kv->base, m->L, kv->b, m->Hkv, kv->cap, m->hd, kv->len, o->path, kv->t->l + 1, o->n_emit, st));
+  ++nl;
+  CK(commit_launch(kv->b, kv->len, o->n_emit, kv->root, kv->root_next, kv->acc_row, m->hf, m->d, m->head_in,
+                   kv->emitted, st));
+  ++nl;
+  CKS(enqueue_heads(m, kv, 0, kv->b, st, nl));
+  return SM_OK;
+}
+
+static sm_status check_accept(const sm_accept_cfg *cfg, const sm_accept_out *o) {
+  if (!cfg || !o || !o->acc_len || !o->best_leaf || !o->path || !o->emit_tok || !o->n_emit || !o->status)
+    return fail(SM_ERR_INVALID_ARG, "accept: null cfg/out pointer");
+  if (cfg->mode == SM_ACCEPT_TYPICAL && !(cfg->temperature > 0.f))
+    return fail(SM_ERR_INVALID_ARG, "typical acceptance needs temperature > 0");
+  return SM_OK;
+}
+
+extern "C" sm_status sm_propose(sm_model *m, sm_kv *kv, int32_t *d_tree_tok, int32_t *d_pos, void *stream) {
+  if (!m || !kv || !d_tree_tok) return fail(SM_ERR_INVALID_ARG, "sm_propose: bad arguments");
+  int nl = 0;
+  CKS(enqueue_propose(m, kv, d_tree_tok, d_pos, (cudaStream_t)stream, nl));
+  return SM_OK;
+}
+
+extern "C" sm_status sm_verify(sm_model *m, sm_kv *kv, const int32_t *d_tree_tok, float *d_logits, void *stream) {
+  if (!m || !kv || !d_tree_tok) return fail(SM_ERR_INVALID_ARG, "sm_verify: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  int nl = 0;
+  if (d_tree_tok != kv->tree_tok)
+    CK(cudaMemcpyAsync(kv->tree_tok, d_tree_tok, (size_t)kv->b * kv->N * 4, cudaMemcpyDeviceToDevice, st));
+  CKS(enqueue_verify(m, kv, kv->tree_tok, st, nl));
+  if (d_logits)
+    CK(cudaMemcpyAsync(d_logits, m->z, (size_t)kv->b * kv->N * m->V * 4, cudaMemcpyDeviceToDevice, st));
+  kv->last_stream = st;
+  return SM_OK;
+}
+
+extern "C" sm_status sm_accept(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, const sm_accept_out *out,
+                               void *stream) {
+  if (!m || !kv) return fail(SM_ERR_INVALID_ARG, "sm_accept: bad arguments");
+  CKS(check_accept(cfg, out));
+  int nl = 0;
+  CKS(enqueue_accept(m, kv, cfg, out, (cudaStream_t)stream, nl));
+  kv->last_stream = (cudaStream_t)stream;
+  return SM_OK;
+}
+
+static sm_status enqueue_step(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, const sm_accept_out *o,
+                              cudaStream_t st, int &nl) {
+  CKS(enqueue_propose(m, kv, kv->tree_tok, nullptr, st, nl));
+  CKS(enqueue_verify(m, kv, kv->tree_tok, st, nl));
+  CKS(enqueue_accept(m, kv, cfg, o, st, nl));
+  return SM_OK;
+}
+
+extern "C" sm_status sm_step(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, const sm_accept_out *out,
+                             void *stream) {
+  if (!m || !kv) return fail(SM_ERR_INVALID_ARG, "sm_step: bad arguments");
+  CKS(check_accept(cfg, out));
+  cudaStream_t st = (cudaStream_t)stream;
+  GraphKey key{(int)cfg->mode, cfg->temperature, cfg->eps, cfg->alpha, cfg->d_max_new, cfg->d_forced_path,
+               out->acc_len, out->best_leaf, out->path, out->emit_tok, out->n_emit, out->status};
+  auto it = kv->graphs.find(key);
+  if (it == kv->graphs.end()) {
+    cudaStreamCaptureStatus cs;
+    CK(cudaStreamIsCapturing(st, &cs));
+    if (cs != cudaStreamCaptureStatusNone) {  // caller is capturing: enqueue directly
+      int nl = 0;
+      CKS(enqueue_step(m, kv, cfg, out, st, nl));
+      return SM_OK;
+    }
+    cudaGraph_t g;
+    int nl = 0;
+    CK(cudaStreamBeginCapture(m->cap_stream, cudaStreamCaptureModeRelaxed));
+    sm_status s = enqueue_step(m, kv, cfg, out, m->cap_stream, nl);
+    cudaError_t e = cudaStreamEndCapture(m->cap_stream, &g);
+    if (s != SM_OK) return s;
+    if (e != cudaSuccess) return fail(SM_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    cudaGraphExec_t ex;
+    e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(SM_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    it = kv->graphs.emplace(key, ex).first;
+    kv->step_launches = nl;
+  }
+  CK(cudaGraphLaunch(it->second, st));
+  kv->last_stream = st;
+  return SM_OK;
+}
+
+extern "C" sm_status sm_step_launches(const sm_kv *kv, int *n) {
+  if (!kv || !n) return fail(SM_ERR_INVALID_ARG, "null");
+  *n = kv->step_launches;
+  return SM_OK;
+}
+
+// ---------------------------------------------------------------- stage APIs (parity tests, K1 sweep)
+static void *g_scratch = nullptr;
+static size_t g_scratch_bytes = 0;
+static sm_status scratch(size_t bytes, void **p) {
+  if (bytes > g_scratch_bytes) {
+    cudaFree(g_scratch);
+    g_scratch = nullptr;
+    g_scratch_bytes = 0;
+    if (cudaMalloc(&g_scratch, bytes) != cudaSuccess) return fail(SM_ERR_DEVICE_OOM, "Buffer: stage scratch");
+    g_scratch_bytes = bytes;
+  }
+  *p = g_scratch;
+  return SM_OK;
+}
+
+extern "C" sm_status sm_tree_attention(const sm_tree *t, const void *d_q, const void *d_k, const void *d_v,
+                                       const int32_t *d_len, int batch, int n_heads, int n_kv_heads, int head_dim,
+                                       int cap, void *d_out, void *stream) {
+  if (!t || !d_q || !d_k || !d_v || !d_len || !d_out || batch < 1 || n_kv_heads < 1 || n_heads % n_kv_heads ||
+      cap < t->N)
+    return fail(SM_ERR_INVALID_ARG, "sm_tree_attention: bad arguments");
+  if (head_dim != 16 && head_dim != 32 && head_dim != 64 && head_dim != 128)
+    return fail(SM_ERR_INVALID_ARG, "head_dim must be 16/32/64/128");
+  sm_tree *tt = const_cast<sm_tree *>(t);
+  CKS(tree_upload(tt));
+  const int G = n_heads / n_kv_heads;
+  const int units = batch * n_kv_heads * attention_row_blocks(t->N, G);
+  const int want = std::max(1, (2 * kNumSMs + units - 1) / units);
+  auto up64 = [](int v) { return (v + 63) / 64 * 64; };
+  int chunk = std::max(64, up64((cap + want - 1) / want));
+  int nsplit = (cap + chunk - 1) / chunk;
+  if (nsplit > 64) {
+    chunk = up64((cap + 63) / 64);
+    nsplit = (cap + chunk - 1) / chunk;
+  }
+  AttnArgs aa;
+  std::memset(&aa, 0, sizeof(aa));
+  const uint64_t rows = (uint64_t)batch * n_kv_heads * cap;
+  CKS(kv_map(&aa.tmK, d_k, rows, head_dim));
+  CKS(kv_map(&aa.tmV, d_v, rows, head_dim));
+  const long long M = (long long)batch * t->N;
+  void *scr = nullptr;
+  if (nsplit > 1) CKS(scratch((size_t)nsplit * M * n_heads * (head_dim + 2) * 4, &scr));
+  aa.q = (const bf16 *)d_q;
+  aa.out = (bf16 *)d_out;
+  aa.part_o = (float *)scr;
+  aa.part_ml = nsplit > 1 ? (float *)scr + (size_t)nsplit * M * n_heads * head_dim : nullptr;
+  aa.len = d_len;
+  aa.anc = tt->d_anc;
+  aa.k_row0 = 0;
+  aa.v_row0 = 0;
+  aa.seq_rows = (long long)n_kv_heads * cap;
+  aa.cap = cap;
+  aa.Nq = t->N;
+  aa.H = n_heads;
+  aa.Hkv = n_kv_heads;
+  aa.G = G;
+  aa.nseq = batch;
+  aa.seq_base = 0;
+  aa.chunk = chunk;
+  aa.nsplit = nsplit;
+  aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)head_dim));
+  CK(attention_launch(aa, head_dim, (cudaStream_t)stream));
+  return SM_OK;
+}
+
+extern "C" sm_status sm_gemm_bf16(const void *d_x, const void *d_w, float *d_out, int M, int N, int K,
+                                  void *stream) {
+  if (!d_x || !d_w || !d_out || M < 1 || M > 256 || N < 1 || K < 8 || K % 8)
+    return fail(SM_ERR_INVALID_ARG, "sm_gemm_bf16: bad arguments (M <= 256, K % 8 == 0)");
+  GemmArgs a = gemm_proto(N, K, 1);
+  CKS(weight_map(&a.tmW[0], d_w, N, K));
+  CKS(act_map(&a.tmX[0], d_x, M, K));
+  void *scr = nullptr;
+  CKS(scratch(gemm_part_elems(a, M, M) * 4, &scr));
+  int nl = 0;
+  GemmRun gr;
+  cudaStream_t st = (cudaStream_t)stream;
+  CKS(run_gemm(a, M, M, 0, (float *)scr, st, &gr, nl));
+  CK(sum_splits_launch((float *)scr, gr.splits, gr.split_stride, N, d_out, M, N, st));
+  return SM_OK;
+}
+
+extern "C" sm_status sm_topk_f32(const float *d_logits, int rows, int V, int k, int32_t *d_idx, void *stream) {
+  if (!d_logits || !d_idx || rows < 1 || V < k || k < 1 || V * 4 > 200 * 1024)
+    return fail(SM_ERR_INVALID_ARG, "sm_topk_f32: bad arguments");
+  CK(topk_launch(d_logits, 1, 0, V, V, rows, k, d_idx, k, (cudaStream_t)stream));
+  return SM_OK;
+}
+
+extern "C" const char *sm_last_error(void) { return g_err.c_str(); }
+extern "C" const char *sm_version(void) { return "specmemo-b200 0.1 (sm_100a: tcgen05 GEMM, mma.sync tree attention)"; }

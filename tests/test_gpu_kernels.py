@@ -1,0 +1,131 @@
+"""Stage parity of the CUDA kernels against the oracle (needs a B200).
+
+K2 GEMM vs numpy fp64; K1 tree attention vs oracle Model.attention over the
+gathered key list; K3 top-k vs the oracle's (value desc, index asc) order;
+the device weight generator bit for bit against synth."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import model as OM
+from oracle import tree as OT
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sm():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_2506_01986_b200 as sm
+    sm.lib()
+    return sm
+
+
+def bf16_tensor(bits: np.ndarray, shape):
+    return torch.from_numpy(bits.view(np.int16).reshape(shape).copy()).view(torch.bfloat16).cuda()
+
+
+def to64(t):
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+# ------------------------------------------------------------------ generator
+@pytest.mark.parametrize("seed,stream,n,mode,start", [(0, 5, 100003, 0, 0), (3, 2, 4097, 0, 77), (1, 9, 50001, 1, 0)])
+def test_device_generator_bitwise(sm, seed, stream, n, mode, start):
+    t = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    sm.generate_bf16(t, seed, stream, start=start, mode=mode)
+    torch.cuda.synchronize()
+    got = t.view(torch.int16).cpu().numpy().view(np.uint16)
+    if mode == 0:
+        ref = synth.weight_bits(seed, stream, n, start=start)
+    else:
+        assert start == 0
+        ref = synth.normal_bits(seed, stream, n)
+    assert np.array_equal(got, ref)
+
+
+# ------------------------------------------------------------------ K2 GEMM
+@pytest.mark.parametrize("M,N,K", [(1, 128, 64), (16, 4096, 4096), (37, 192, 320), (64, 12288, 512),
+                                   (200, 1000, 72), (256, 384, 1024), (64, 4096, 11008)])
+def test_gemm_matches_fp64(sm, M, N, K):
+    x = bf16_tensor(synth.normal_bits(1, 100 + M, M * K), (M, K))
+    w = bf16_tensor(synth.weight_bits(2, 200 + N, N * K), (N, K))
+    out = torch.full((M, N), float("nan"), dtype=torch.float32, device="cuda")
+    sm.gemm_bf16(x, w, out)
+    torch.cuda.synchronize()
+    X, W = to64(x), to64(w)
+    ref = X @ W.T
+    bound = np.abs(X) @ np.abs(W).T
+    err = np.abs(out.cpu().numpy().astype(np.float64) - ref)
+    assert np.all(np.isfinite(out.cpu().numpy()))
+    assert np.all(err <= 2e-6 * bound + 1e-30), float((err / (bound + 1e-30)).max())
+
+
+# ------------------------------------------------------------------ K1 tree attention
+class _Geom:
+    def __init__(self, H, Hkv, hd):
+        self.H, self.hd, self.G = H, hd, H // Hkv
+
+
+def attention_oracle(tree_choices, chain_n, q, k, v, lens, H, Hkv):
+    """Per node: keys = [0, Lc) + ancestors' tree slots + own slot (Eq. 2)."""
+    tr = OT.build(tree_choices) if chain_n is None else OT.build(synth.CHAIN(chain_n - 1), topk=1)
+    Q, K, V = to64(q), to64(k), to64(v)
+    b, N, _, hd = Q.shape
+    g = _Geom(H, Hkv, hd)
+    out = np.zeros_like(Q)
+    for bi in range(b):
+        Lc = int(lens[bi])
+        for n in range(N):
+            keys = list(range(Lc)) + [Lc + a for a in OT.ancestors(tr, n)] + [Lc + n]
+            Kc = K[bi][:, keys, :].transpose(1, 0, 2)
+            Vc = V[bi][:, keys, :].transpose(1, 0, 2)
+            out[bi, n] = OM.Model.attention(g, Q[bi, n], Kc, Vc)
+    return out
+
+
+ATTN_CASES = [
+    # (name, choices, chain, b, H, Hkv, hd, lens, cap_extra)
+    ("c1_tiny16", synth.TINY16, None, 1, 4, 4, 16, [32], 16),
+    ("v64_mha_ragged", synth.V64, None, 2, 4, 4, 128, [0, 333], 40),
+    ("v64_gqa8", synth.V64, None, 3, 8, 1, 128, [100, 517, 1], 7),
+    ("sweep128", synth.SWEEP_TREES[128], None, 1, 2, 2, 128, [1000], 0),
+    ("sweep256_gqa", synth.SWEEP_TREES[256], None, 1, 4, 2, 64, [130], 3),
+    ("chain_prefill", None, 200, 2, 4, 2, 64, [0, 65], 5),
+    ("hd32", synth.V64[:31], None, 2, 4, 4, 32, [64, 63], 1),
+]
+
+
+@pytest.mark.parametrize("case", ATTN_CASES, ids=[c[0] for c in ATTN_CASES])
+def test_tree_attention_matches_oracle(sm, case):
+    name, choices, chain, b, H, Hkv, hd, lens, extra = case
+    tree = sm.Tree(choices, topk=10) if chain is None else sm.Tree(None, chain=chain)
+    N = tree.N
+    cap = max(lens) + N + extra
+    q = bf16_tensor(synth.normal_bits(5, 1, b * N * H * hd), (b, N, H, hd))
+    k = bf16_tensor(synth.normal_bits(5, 2, b * Hkv * cap * hd), (b, Hkv, cap, hd))
+    v = bf16_tensor(synth.normal_bits(5, 3, b * Hkv * cap * hd), (b, Hkv, cap, hd))
+    L = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    out = torch.full((b, N, H, hd), float("nan"), dtype=torch.bfloat16, device="cuda")
+    sm.tree_attention(tree, q, k, v, L, H, Hkv, out)
+    torch.cuda.synchronize()
+    ref = attention_oracle(choices, chain, q, k, v, lens, H, Hkv)
+    got = to64(out)
+    assert np.all(np.isfinite(got))
+    err = np.abs(got - ref)
+    assert np.all(err <= 2e-2 + 2e-2 * np.abs(ref)), float(err.max())
+
+
+# ------------------------------------------------------------------ K3 top-k
+def test_topk_matches_oracle_with_ties(sm):
+    rng = np.random.default_rng(0)
+    rows, V, k = 6, 32000, 10
+    z = (np.round(rng.standard_normal((rows, V)) * 4) / 4).astype(np.float32)
+    z[2, 100:120] = z[2].max()                   # a block of exact ties at the top
+    zt = torch.from_numpy(z).cuda()
+    out = torch.zeros(rows, k, dtype=torch.int32, device="cuda")
+    sm.topk_f32(zt, k, out)
+    torch.cuda.synchronize()
+    for r in range(rows):
+        assert out[r].cpu().tolist() == OM.topk_desc(z[r].astype(np.float64), k)
