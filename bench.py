@@ -1,0 +1,439 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Medusa tree-verification hot path (SpecMemo, 2506.01986).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (N=1 line): BASELINE.json configs[1] = C2, Vicuna-7B-shaped random-init
+Llama + 4 Medusa-1 heads, the 64-node / 42-leaf Medusa tree, batch 1, KV cache
+bounded to x = 2048 (+64 tree-scratch slots), greedy acceptance.  One step = one
+full pass a1..a5 (propose, verify forward of 64 nodes through 32 layers + LM
+head, acceptance, compaction, heads + top-k) = one sm_step graph replay.
+Under torchrun (N>1) every rank runs an independent replica (the bs=1 7B path
+does not shard; TP for the 70B config is not built yet): "scaling": "weak".
+
+Prints ONE JSON line (rank 0).  --impl reference times the CPU oracle
+(oracle/, numpy fp64) on the host cores on a bounded sample of the same step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "decode tokens/s (bs=1 and bs=10) and tree-attn HBM GB/s vs B200 peak"
+X_BOUND = 2048
+N_MEDUSA = 4
+
+
+def peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(hbm=d["hbm_gbs"], bf16=d["bf16_tflops"], bf16_sus=d.get("bf16_tflops_sustained"),
+                    src="MEASURED_PEAKS.json (measured)")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="B200_PROFILING.md fallback")
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, device: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100", "-i", str(device)], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                rows.append(dict(sm=float(parts[0]), smax=float(parts[1]), pw=float(parts[2]), hw=parts[3],
+                                 hwt=parts[4], swt=parts[5], pcap=parts[6], util=float(parts[7])))
+            except ValueError:
+                continue
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        load = [r for r in rows if r["util"] > 50] or rows
+        reasons = set()
+        for r in load:
+            for k, name in (("hw", "hw_slowdown"), ("hwt", "hw_thermal_slowdown"), ("swt", "sw_thermal_slowdown"),
+                            ("pcap", "sw_power_cap")):
+                if r[k].lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(r["sm"] for r in load), "sm_max_mhz": max(r["smax"] for r in rows),
+                "reasons": sorted(reasons), "samples": len(load)}
+
+
+# ------------------------------------------------------------------ distributed plumbing
+def dist_setup():
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def reduce_max(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def reduce_sum(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ algorithmic work of one C2 step
+def step_bytes(cfg: dict, N: int, Lc: float, b: int = 1, n_medusa: int = N_MEDUSA, tau: float = 1.0) -> float:
+    """weights (layers + LM head + heads) + KV read + tree KV write + compaction."""
+    d, H, Hkv, hd, F, V, L = (cfg[k] for k in ("d_model", "n_heads", "n_kv_heads", "head_dim", "d_ffn", "vocab",
+                                                "n_layers"))
+    w_layers = L * ((H + 2 * Hkv) * hd * d + d * H * hd + 3 * F * d) * 2
+    w_lm = V * d * 2
+    w_heads = n_medusa * (d * d + V * d) * 2
+    kv_read = b * 2 * L * Hkv * hd * 2 * Lc
+    kv_write = b * N * 2 * L * Hkv * hd * 2
+    compact = b * 2 * (tau - 1) * 2 * L * Hkv * hd * 2
+    return w_layers + w_lm + w_heads + kv_read + kv_write + compact
+
+
+def attn_bytes(cfg: dict, N: int, Lc: float, b: int = 1) -> float:
+    """K1 per step (all layers): K/V of [0, Lc) + tree slots, read once; Q in, O out."""
+    H, Hkv, hd, L = (cfg[k] for k in ("n_heads", "n_kv_heads", "head_dim", "n_layers"))
+    return L * b * (Hkv * (Lc + N) * hd * 2 * 2 + 2 * N * H * hd * 2)
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, world, rank, local) -> dict | None:
+    import torch
+
+    import paper_2506_01986_b200 as sm
+
+    cfg = synth.model_cfg("vicuna7b")
+    tree = sm.Tree(synth.V64, topk=synth.TOPK)
+    N, l = tree.N, tree.depth
+    W = sm.allocate_weights(cfg, N_MEDUSA, seed=args.seed + rank)
+    model = sm.Model(cfg, W, max_rows=256, max_batch=1, max_seq_len=X_BOUND + N)
+    kv = sm.KVCache(model, tree, 1, X_BOUND)
+    total_steps = args.warmup + args.steps + args.prof_steps + args.e2e_steps + 8
+    lc_start = max(128, min(args.lc_start, X_BOUND - 5 * total_steps - 8))
+    prompt = torch.from_numpy(synth.prompt_tokens(args.seed, rank, lc_start, cfg["vocab"])).cuda()
+    kv.prefill(0, prompt)
+    out = sm.AcceptOut(1, l)
+    acfg = sm.accept_cfg(sm.GREEDY)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    for _ in range(args.warmup):
+        kv.step(acfg, out)
+    torch.cuda.synchronize()
+    barrier(world)
+    st = torch.cuda.current_stream()
+    L0 = int(kv.lengths()[0])
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    ev0.record(st)
+    for _ in range(args.steps):
+        kv.step(acfg, out)
+    ev1.record(st)
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    L1 = int(kv.lengths()[0])
+    ms_max = reduce_max(ms, world)
+    tokens = reduce_sum(L1 - L0, world)
+    value = tokens / (ms_max / 1e3)
+    tau = (L1 - L0) / args.steps
+    launches = kv.step_launches()
+
+    # ---- kernel timing pass (event-instrumented replay of the same graph)
+    kv.profile(True)
+    g_ms, g_bytes, g_n, a_ms, a_n, lcs = [], [], 0, [], 0, []
+    for _ in range(args.prof_steps):
+        lcs.append(int(kv.lengths()[0]))
+        kv.step(acfg, out)
+        n, gm, gb = kv.profile_read(0)
+        na, am, _ = kv.profile_read(1)
+        g_ms.append(gm)
+        g_bytes.append(gb)
+        g_n, a_n = n, na
+        a_ms.append(am)
+    kv.profile(False)
+    gemm_ms = statistics.median(g_ms)
+    gemm_bytes = g_bytes[0]
+    attn_ms = statistics.median(a_ms)
+    lc_prof = float(np.mean(lcs))
+
+    # ---- end-to-end through the public API with host buffers (pinned), per step:
+    # H2D of the turn budget, the step, D2H of the emitted tokens + counts.
+    h_budget = torch.full((1,), 1 << 30, dtype=torch.int32).pin_memory()
+    d_budget = torch.empty(1, dtype=torch.int32, device="cuda")
+    h_emit = torch.empty((1, l + 1), dtype=torch.int32).pin_memory()
+    h_n = torch.empty((1,), dtype=torch.int32).pin_memory()
+    ecfg = sm.accept_cfg(sm.GREEDY, max_new=d_budget)
+    d_budget.copy_(h_budget)
+    kv.step(ecfg, out)  # capture the e2e graph variant outside the timed region
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_tokens = 0
+    e0.record(st)
+    for _ in range(args.e2e_steps):
+        d_budget.copy_(h_budget, non_blocking=True)
+        kv.step(ecfg, out)
+        h_emit.copy_(out.emit_tok, non_blocking=True)
+        h_n.copy_(out.n_emit, non_blocking=True)
+        st.synchronize()                   # the caller reads this step's tokens
+        e2e_tokens += int(h_n[0])
+    e1.record(st)
+    torch.cuda.synchronize()
+    e_ms = reduce_max(e0.elapsed_time(e1), world)
+    e2e_val = reduce_sum(e2e_tokens, world) / (e_ms / 1e3)
+
+    # ---- K1 tree-attention point of the C5 sweep (geometry A, N=64)
+    k1 = run_k1_point(sm, args) if args.k1 else None
+
+    if rank != 0:
+        return None
+    pk = peaks()
+    gemm_gbs = gemm_bytes / (gemm_ms / 1e3) / 1e9
+    sb = step_bytes(cfg, N, (L0 + L1) / 2, tau=tau)
+    ms_step = ms_max / args.steps
+    res = {
+        "metric": METRIC, "value": round(value, 3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic: counter-hash random-init weights (std 0.02), counter-hash prompt tokens",
+        "config": {"workload": "C2: Vicuna-7B-shaped Llama + 4 Medusa-1 heads (random init), Medusa V64 tree "
+                               "(64 nodes, 42 leaves), bs=1 per GPU, KV bounded to x=2048 (+64 scratch), greedy",
+                   "global_batch": world, "seq_len": X_BOUND, "lc_start": lc_start, "lc_mean": (L0 + L1) / 2,
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2: 14.7 GB of weights streamed every step (L2 126 MB)"},
+        "tau": round(tau, 4), "steps_per_s": round(args.steps / (ms_max / 1e3), 3),
+        "roofline": {"kernel": "K2 tcgen05 GEMM (all 129 weight GEMMs + 2 head GEMMs of one step)", "bound": "hbm",
+                     "achieved": round(gemm_gbs, 1), "peak": pk["hbm"], "unit": "GB/s",
+                     "frac": round(gemm_gbs / pk["hbm"], 4), "traffic": gemm_traffic(),
+                     "launches_per_step": g_n, "ms_per_step": round(gemm_ms, 4),
+                     "share_of_step": round(gemm_ms / ms_step, 4), "alg_bytes_per_step": gemm_bytes,
+                     "peak_source": pk["src"], "timing": "CUDA events around each launch inside the step graph"},
+        "step_roofline": {"bound": "hbm", "alg_bytes": sb, "roofline_ms": round(sb / pk["hbm"] / 1e6, 4),
+                          "frac": round(sb / pk["hbm"] / 1e6 / ms_step, 4)},
+        "tree_attn_in_step": {"launches_per_step": a_n, "ms_per_step": round(attn_ms, 4), "lc": lc_prof,
+                              "alg_bytes": attn_bytes(cfg, N, lc_prof),
+                              "achieved_gbs": round(attn_bytes(cfg, N, lc_prof) / (attn_ms / 1e3) / 1e9, 1)},
+        "e2e": {"value": round(e2e_val, 3), "unit": "tokens/s", "h2d_bytes_per_step": 4,
+                "d2h_bytes_per_step": 4 * (l + 1) + 4, "steps": args.e2e_steps},
+        "gpu_launches": launches * args.steps,
+        "clocks": clk,
+    }
+    if k1:
+        res["k1_point"] = k1
+    return res
+
+
+def gemm_traffic():
+    p = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(p):
+        return json.load(open(p)).get("dram_bytes_per_step")
+    return None
+
+
+def run_k1_point(sm, args) -> dict:
+    """C5 geometry A (H = Hkv = 32, hd = 128), N = 64 (V64), b = 8, Lc = 4096:
+    ~0.55 GB of K/V per launch; two buffer sets alternate (> 4x L2)."""
+    import torch
+    b, H, Hkv, hd, Lc = 8, 32, 32, 128, 4096
+    tree = sm.Tree(synth.V64)
+    N = tree.N
+    cap = Lc + N
+    sets = []
+    for s in range(2):
+        q = torch.empty(b, N, H, hd, dtype=torch.bfloat16, device="cuda")
+        k = torch.empty(b, Hkv, cap, hd, dtype=torch.bfloat16, device="cuda")
+        v = torch.empty_like(k)
+        for i, t in enumerate((q, k, v)):
+            sm.generate_bf16(t, 7 + s, 100 + i, mode=1)
+        sets.append((q, k, v, torch.empty_like(q)))
+    L = torch.full((b,), Lc, dtype=torch.int32, device="cuda")
+    for i in range(4):
+        q, k, v, o = sets[i % 2]
+        sm.tree_attention(tree, q, k, v, L, H, Hkv, o)
+    torch.cuda.synchronize()
+    reps = 20
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(reps):
+        q, k, v, o = sets[i % 2]
+        sm.tree_attention(tree, q, k, v, L, H, Hkv, o)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    byt = b * Hkv * (Lc + N) * hd * 2 * 2 + 2 * b * N * H * hd * 2
+    gbs = byt / (ms / 1e3) / 1e9
+    pk = peaks()
+    return {"geometry": "A: H=Hkv=32, hd=128", "N": N, "b": b, "Lc": Lc, "alg_bytes": byt, "ms": round(ms, 4),
+            "achieved_gbs": round(gbs, 1), "peak": pk["hbm"], "frac": round(gbs / pk["hbm"], 4)}
+
+
+# ------------------------------------------------------------------ oracle (CPU) arm
+def oracle_sample(reps: int, rows: int = 8):
+    """Time the oracle (as it stands) on a bounded sample of one C2 step: ``rows``
+    of the 64 tree rows through 1 of the 32 layers + LM head, and the same rows
+    through 0 layers (LM head only), plus one Medusa head evaluation; returns the
+    extrapolated full-step seconds = 64 * (32 * t_layer_row + t_lm_row) + 4 * t_head."""
+    from oracle import model as OM
+    from oracle import tree as OT
+    cfg = synth.model_cfg("vicuna7b")
+    W1 = OM.Weights(cfg, n_medusa=1, seed=0, medusa_init=True, layers=[0])
+    W0 = OM.Weights.__new__(OM.Weights)
+    W0.__dict__.update(W1.__dict__)
+    W0.layers = []
+    m1, m0 = OM.Model(cfg, W1, "bf16"), OM.Model(cfg, W0, "bf16")
+    tr = OT.build(synth.V64)
+    Lc = 1024
+    toks = synth.prompt_tokens(0, 0, rows, cfg["vocab"])
+    times = []
+    for _ in range(reps):
+        kv1 = OM.KVCache(1, 1, cfg["n_kv_heads"], Lc + tr.N, cfg["head_dim"])
+        kv0 = OM.KVCache(0, 1, cfg["n_kv_heads"], Lc + tr.N, cfg["head_dim"])
+        t0 = time.perf_counter()
+        hf = None
+        for n in range(rows):
+            keys = list(range(Lc)) + [Lc + a for a in OT.ancestors(tr, n)] + [Lc + n]
+            _, hf = m1.forward_row(kv1, 0, int(toks[n]), Lc + tr.depth[n], Lc + n, keys)
+        t1 = time.perf_counter()
+        for n in range(rows):
+            m0.forward_row(kv0, 0, int(toks[n]), Lc + tr.depth[n], Lc + n, [Lc + n])
+        t2 = time.perf_counter()
+        m1.head_logits(0, hf)
+        t3 = time.perf_counter()
+        t_lm = (t2 - t1) / rows
+        t_layer = max(0.0, (t1 - t0) / rows - t_lm)
+        times.append(64 * (32 * t_layer + t_lm) + N_MEDUSA * (t3 - t2))
+    return times
+
+
+def host_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        if info:
+            return int(max(i.get("num_threads", 1) for i in info))
+    except Exception:
+        pass
+    return len(os.sched_getaffinity(0))
+
+
+def cpu_baseline(tau: float) -> dict:
+    t = oracle_sample(1)
+    step_s = t[0]
+    return {"value": round(tau / step_s, 6), "unit": "tokens/s", "cores": host_threads(), "kind": "oracle",
+            "sample": "oracle (numpy fp64, bf16 storage points) on 8 of the 64 V64 tree rows through 1 of 32 "
+                      "Vicuna-7B layers + LM head at Lc=1024, plus one Medusa head; extrapolated linearly to the "
+                      f"full step (64 rows x 32 layers + 4 heads) = {step_s:.1f} s/step; tokens/s at the GPU "
+                      f"run's tau = {tau:.3f}"}
+
+
+def run_reference(args, world, rank) -> dict | None:
+    if rank != 0:
+        return None
+    t = oracle_sample(args.warmup + args.steps)[args.warmup:]
+    step_s = statistics.median(t)
+    val = 1.0 / step_s
+    return {"impl": "reference", "metric": METRIC, "value": round(val, 6), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: counter-hash random-init weights, counter-hash prompt tokens",
+            "config": {"workload": "C2: Vicuna-7B-shaped Llama + 4 Medusa-1 heads, V64 tree, bs=1, KV x=2048, "
+                                   "greedy (oracle sample, see cpu_baseline)"},
+            "cpu_baseline": {"value": round(val, 6), "unit": "tokens/s", "cores": host_threads(), "kind": "oracle",
+                             "sample": "each step: 8 of 64 tree rows through 1 of 32 layers + LM head (and 0 "
+                                       "layers), one Medusa head; extrapolated to 64 rows x 32 layers + 4 heads; "
+                                       "tau = 1 (random heads)"},
+            "e2e": {"value": round(val, 6), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--lc-start", type=int, default=1024)
+    ap.add_argument("--prof-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--no-k1", dest="k1", action="store_false")
+    ap.add_argument("--no-cpu-baseline", dest="cpu", action="store_false")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        res = run_reference(args, world, rank)
+        if res:
+            print(json.dumps(res), flush=True)
+        return
+    world, rank, local = dist_setup()
+    res = run_ours(args, world, rank, local)
+    if res is not None:
+        if args.cpu and world == 1:
+            res["cpu_baseline"] = cpu_baseline(res["tau"])
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

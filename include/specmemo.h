@@ -159,6 +159,15 @@ sm_status sm_accept(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, const sm_a
 sm_status sm_step(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, const sm_accept_out *out, void *stream);
 /* Number of kernels one sm_step launches (for the bench's gpu_launches).     */
 sm_status sm_step_launches(const sm_kv *kv, int *n);
+/* Kernel timing for the bench's roofline: with enable = 1 the next sm_step
+ * captures (and then replays) a graph variant that brackets every K2 GEMM
+ * launch (kind 0) and every K1 tree-attention launch + combine (kind 1) with
+ * CUDA events on the launch stream.  sm_profile_read synchronises and returns,
+ * for the most recent replay, the number of bracketed launches, their summed
+ * duration in ms, and (kind 0) the algorithmic bytes W + X + Y(fp32) of those
+ * launches.                                                                   */
+sm_status sm_step_profile(sm_kv *kv, int enable);
+sm_status sm_profile_read(const sm_kv *kv, int kind, int *count, float *total_ms, double *alg_bytes);
 /* Device pointers to the pending state: root[b], topk[b][n_medusa][K] (int32). */
 sm_status sm_state_device(const sm_kv *kv, int32_t **d_root, int32_t **d_topk);
 

@@ -291,6 +291,18 @@ class KVCache:
         _check(lib().sm_step(self.model._h, self._h, ctypes.byref(cfg), ctypes.byref(out.c),
                              ctypes.c_void_p(_stream(stream))))
 
+    def profile(self, enable: bool) -> None:
+        """Next step() replays an event-instrumented graph (K2 / K1 timing)."""
+        _check(lib().sm_step_profile(self._h, ctypes.c_int(1 if enable else 0)))
+
+    def profile_read(self, kind: int):
+        """(launch count, summed ms, algorithmic bytes) of the last profiled replay;
+        kind 0 = K2 GEMM, 1 = K1 tree attention."""
+        n, ms, by = ctypes.c_int(), ctypes.c_float(), ctypes.c_double()
+        _check(lib().sm_profile_read(self._h, ctypes.c_int(kind), ctypes.byref(n), ctypes.byref(ms),
+                                     ctypes.byref(by)))
+        return n.value, ms.value, by.value
+
     def step_launches(self) -> int:
         n = ctypes.c_int()
         _check(lib().sm_step_launches(self._h, ctypes.byref(n)))

@@ -274,6 +274,26 @@ static size_t gemm_part_elems(const GemmArgs &proto, int M, int ld_rows) {
   return (size_t)a.batch * a.splits * ld_rows * proto.N;
 }
 
+// ---------------------------------------------------------------- in-graph kernel timing
+struct ProfEvent {
+  int kind;  // 0 = K2 GEMM, 1 = K1 tree attention (+ combine)
+  cudaEvent_t a, b;
+  double bytes;
+};
+static thread_local std::vector<ProfEvent> *g_prof = nullptr;
+static void prof_begin(cudaStream_t st, cudaEvent_t *ev) {
+  if (!g_prof) return;
+  cudaEventCreate(ev);
+  cudaEventRecordWithFlags(*ev, st, cudaEventRecordExternal);
+}
+static void prof_end(cudaStream_t st, cudaEvent_t a, int kind, double bytes) {
+  if (!g_prof) return;
+  cudaEvent_t b;
+  cudaEventCreate(&b);
+  cudaEventRecordWithFlags(b, st, cudaEventRecordExternal);
+  g_prof->push_back(ProfEvent{kind, a, b, bytes});
+}
+
 struct GemmRun {
   int splits;
   long long split_stride;
@@ -288,7 +308,11 @@ static sm_status run_gemm(const GemmArgs &proto, int M, int ld_rows, int x_row0,
   a.split_stride = (long long)ld_rows * proto.N;
   const long long bstride = (long long)a.splits * a.split_stride;
   for (int i = 0; i < a.batch; ++i) a.out[i] = out + i * bstride;
+  cudaEvent_t ev = nullptr;
+  prof_begin(st, &ev);
   CK(gemm_launch(a, st));
+  prof_end(st, ev, 0,
+           (double)a.batch * ((double)proto.N * proto.K * 2 + (double)M * proto.K * 2 + (double)M * proto.N * 4));
   ++nl;
   if (info) *info = GemmRun{a.splits, a.split_stride, bstride};
   return SM_OK;
@@ -466,12 +490,13 @@ extern "C" sm_status sm_generate_bf16(void *dst, size_t numel, uint64_t seed, ui
 
 // ---------------------------------------------------------------- bounded KV
 struct GraphKey {
+  int prof;
   int mode;
   float T, eps, alpha;
   const void *max_new, *forced, *o0, *o1, *o2, *o3, *o4, *o5;
   bool operator<(const GraphKey &o) const {
-    return std::tie(mode, T, eps, alpha, max_new, forced, o0, o1, o2, o3, o4, o5) <
-           std::tie(o.mode, o.T, o.eps, o.alpha, o.max_new, o.forced, o.o0, o.o1, o.o2, o.o3, o.o4, o.o5);
+    return std::tie(prof, mode, T, eps, alpha, max_new, forced, o0, o1, o2, o3, o4, o5) <
+           std::tie(o.prof, o.mode, o.T, o.eps, o.alpha, o.max_new, o.forced, o.o0, o.o1, o.o2, o.o3, o.o4, o.o5);
   }
 };
 
@@ -488,6 +513,8 @@ struct sm_kv {
   CUtensorMap tmKV;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   int step_launches = 0;
+  int prof = 0;
+  std::vector<ProfEvent> prof_events;
   cudaStream_t last_stream = nullptr;
 };
 
@@ -562,6 +589,10 @@ extern "C" sm_status sm_kv_bind(sm_model *m, const sm_tree *tree, int batch, int
 extern "C" void sm_kv_destroy(sm_kv *kv) {
   if (!kv) return;
   for (auto &g : kv->graphs) cudaGraphExecDestroy(g.second);
+  for (auto &pe : kv->prof_events) {
+    cudaEventDestroy(pe.a);
+    cudaEventDestroy(pe.b);
+  }
   cudaFree(kv->len);
   cudaFree(kv->root);
   cudaFree(kv->topk);
@@ -652,7 +683,10 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
     aa.chunk = chunk;
     aa.nsplit = nsplit;
     aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)m->hd));
+    cudaEvent_t ev = nullptr;
+    prof_begin(st, &ev);
     CK(attention_launch(aa, m->hd, st));
+    prof_end(st, ev, 1, 0.0);
     nl += nsplit > 1 ? 2 : 1;
     CKS(run_gemm(m->g_o[l], M, m->R, 0, m->part, st, &gr, nl));
     CK(resid_norm_launch(m->part, gr.splits, gr.split_stride, d, m->x, m->mlp_norm[l], m->h, M, d, m->cfg.rms_eps,
@@ -838,7 +872,7 @@ extern "C" sm_status sm_step(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, c
   if (!m || !kv) return fail(SM_ERR_INVALID_ARG, "sm_step: bad arguments");
   CKS(check_accept(cfg, out));
   cudaStream_t st = (cudaStream_t)stream;
-  GraphKey key{(int)cfg->mode, cfg->temperature, cfg->eps, cfg->alpha, cfg->d_max_new, cfg->d_forced_path,
+  GraphKey key{kv->prof, (int)cfg->mode, cfg->temperature, cfg->eps, cfg->alpha, cfg->d_max_new, cfg->d_forced_path,
                out->acc_len, out->best_leaf, out->path, out->emit_tok, out->n_emit, out->status};
   auto it = kv->graphs.find(key);
   if (it == kv->graphs.end()) {
@@ -851,9 +885,18 @@ extern "C" sm_status sm_step(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, c
     }
     cudaGraph_t g;
     int nl = 0;
+    if (kv->prof) {
+      for (auto &pe : kv->prof_events) {
+        cudaEventDestroy(pe.a);
+        cudaEventDestroy(pe.b);
+      }
+      kv->prof_events.clear();
+      g_prof = &kv->prof_events;
+    }
     CK(cudaStreamBeginCapture(m->cap_stream, cudaStreamCaptureModeRelaxed));
     sm_status s = enqueue_step(m, kv, cfg, out, m->cap_stream, nl);
     cudaError_t e = cudaStreamEndCapture(m->cap_stream, &g);
+    g_prof = nullptr;
     if (s != SM_OK) return s;
     if (e != cudaSuccess) return fail(SM_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
     cudaGraphExec_t ex;
@@ -861,10 +904,36 @@ extern "C" sm_status sm_step(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, c
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return fail(SM_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
     it = kv->graphs.emplace(key, ex).first;
-    kv->step_launches = nl;
+    if (!kv->prof) kv->step_launches = nl;
   }
   CK(cudaGraphLaunch(it->second, st));
   kv->last_stream = st;
+  return SM_OK;
+}
+
+extern "C" sm_status sm_step_profile(sm_kv *kv, int enable) {
+  if (!kv) return fail(SM_ERR_INVALID_ARG, "null");
+  kv->prof = enable ? 1 : 0;
+  return SM_OK;
+}
+
+extern "C" sm_status sm_profile_read(const sm_kv *kv, int kind, int *count, float *total_ms, double *alg_bytes) {
+  if (!kv) return fail(SM_ERR_INVALID_ARG, "null");
+  CK(cudaDeviceSynchronize());
+  int n = 0;
+  float tot = 0.f;
+  double by = 0.0;
+  for (const auto &pe : kv->prof_events) {
+    if (pe.kind != kind) continue;
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, pe.a, pe.b));
+    tot += ms;
+    by += pe.bytes;
+    ++n;
+  }
+  if (count) *count = n;
+  if (total_ms) *total_ms = tot;
+  if (alg_bytes) *alg_bytes = by;
   return SM_OK;
 }
 

@@ -78,7 +78,11 @@ def greedy_margin(Z, path, a_eff, tree):
     return min(gaps)
 
 
-@pytest.mark.parametrize("seed", [0, 1, 2])
+# Seeds 0, 1, 6, 10 are screened by the oracle: every argmax decision along the
+# 32-token trajectory has a top1-top2 gap >= GUARD.  Seeds 2, 3, 7 contain
+# near-ties (gap 5e-4, 1.6e-4, 2e-5): there only the steps before the first
+# ambiguous decision are compared (the trajectory may legitimately fork after).
+@pytest.mark.parametrize("seed", [0, 1, 6, 10, 2, 3, 7])
 def test_c1_greedy_tokens_equal_oracle_and_vanilla(sm, seed):
     prompt = synth.prompt_tokens(seed, 0, 32, CFG["vocab"])
     # oracle trajectory + margins
@@ -103,7 +107,8 @@ def test_c1_greedy_tokens_equal_oracle_and_vanilla(sm, seed):
         if mg < GUARD:
             n_ok = i
             break
-    assert n_ok >= min(8, len(margins)), f"seed {seed} too ambiguous: margins {margins}"
+    if seed in (0, 1, 6, 10):
+        assert n_ok == len(margins), f"screened seed {seed} lost its margin: {margins}"
     ntok = sum(st[2] for st in ref_steps[:n_ok])
     assert got[0][:ntok] == ref[:ntok]
     for i in range(n_ok):
@@ -209,9 +214,11 @@ def test_teacher_forced_full_acceptance_and_compaction(sm):
 def test_typical_matches_oracle_until_ambiguous(sm):
     prompt = synth.prompt_tokens(5, 0, 24, CFG["vocab"])
     typ = dict(temperature=0.7, eps=0.09, alpha=0.3)
-    s = oracle_session(synth.TINY16, 3, 1, 64)
+    # near-uniform tiny-model rows (H ~ 5.5 nats) accept almost every candidate:
+    # tau ~ 4, so 12 steps need ~48 slots beyond the prompt
+    s = oracle_session(synth.TINY16, 3, 1, 128)
     s.prefill(0, prompt)
-    W, tree, model, kv = build_gpu(sm, CFG, 3, synth.TINY16, 1, 64)
+    W, tree, model, kv = build_gpu(sm, CFG, 3, synth.TINY16, 1, 128)
     kv.prefill(0, torch.from_numpy(prompt).cuda())
     out = sm.AcceptOut(1, tree.depth)
     cfg = sm.accept_cfg(sm.TYPICAL, **typ)
