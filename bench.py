@@ -105,24 +105,25 @@ def dist_setup():
     return world, rank, local
 
 
-def reduce_max(v: float, world: int) -> float:
+def _reduce(v: float, world: int, op: str) -> float:
+    """All-reduce one scalar over the job (max of per-rank device times, sum of
+    per-rank token counts).  NCCL on the GPU box; gloo (CPU tensors) in tests."""
     if world == 1:
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
     return float(t.item())
+
+
+def reduce_max(v: float, world: int) -> float:
+    return _reduce(v, world, "max")
 
 
 def reduce_sum(v: float, world: int) -> float:
-    if world == 1:
-        return v
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return float(t.item())
+    return _reduce(v, world, "sum")
 
 
 def barrier(world: int):
@@ -157,6 +158,9 @@ def run_ours(args, world, rank, local) -> dict | None:
 
     import paper_2506_01986_b200 as sm
 
+    for kv_opt in filter(None, os.environ.get("SM_OPT", "").split(",")):  # experiment knobs (sm_set_option)
+        k, v = kv_opt.split("=")
+        sm.lib().sm_set_option(k.encode(), int(v))
     cfg = synth.model_cfg("vicuna7b")
     tree = sm.Tree(synth.V64, topk=synth.TOPK)
     N, l = tree.N, tree.depth

@@ -84,7 +84,11 @@ typedef struct {
   const void *final_norm;  /* [d]                             */
   const void *lm_head;     /* [V][d]                          */
   const void *const *attn_norm, *const *wqkv, *const *wo;           /* [d], [(H+2Hkv)hd][d], [d][H hd] */
-  const void *const *mlp_norm, *const *wgate_up, *const *wdown;     /* [d], [2F][d] (gate;up), [d][F]  */
+  const void *const *mlp_norm, *const *wgate_up, *const *wdown;     /* [d], [2F][d], [d][F]            */
+  /* wgate_up rows are interleaved in blocks of 64: rows [128t, 128t+64) = gate
+   * rows [64t, 64t+64), rows [128t+64, 128t+128) = up rows [64t, 64t+64); one
+   * 128-row GEMM tile then holds matching gate/up features for the fused
+   * SiLU(gate)*up epilogue.  F must be a multiple of 64.                      */
   const void *const *medusa_R, *const *medusa_b, *const *medusa_U;  /* [d][d], [d], [V][d]             */
 } sm_weights;
 
@@ -183,6 +187,12 @@ sm_status sm_tree_attention(const sm_tree *t, const void *d_q, const void *d_k, 
 sm_status sm_gemm_bf16(const void *d_x, const void *d_w, float *d_out, int M, int N, int K, void *stream);
 /* K3 top-k rows of fp32 logits: idx[r][k] by (value desc, index asc).        */
 sm_status sm_topk_f32(const float *d_logits, int rows, int V, int k, int32_t *d_idx, void *stream);
+
+/* Runtime options for experiments (take effect for launches enqueued or graphs
+ * captured afterwards): "pdl" (0/1, programmatic dependent launch of the step's
+ * kernels), "gemm_ctas" (persistent K2 grid size, 0 = one CTA per SM).
+ * Unknown names return SM_ERR_INVALID_ARG.                                     */
+sm_status sm_set_option(const char *name, int value);
 
 const char *sm_last_error(void);
 const char *sm_version(void);

@@ -165,9 +165,14 @@ def allocate_weights(cfg: dict, n_medusa: int, seed: int = 0, medusa_init: bool 
         generate_bf16(wqkv[(H + Hkv) * hd:], seed, synth.stream_layer(li, "wv"))
         wo = torch.empty(d, H * hd, dtype=bf, device=device)
         generate_bf16(wo, seed, synth.stream_layer(li, "wo"))
-        wgu = torch.empty(2 * F, d, dtype=bf, device=device)
-        generate_bf16(wgu[:F], seed, synth.stream_layer(li, "wg"))
-        generate_bf16(wgu[F:], seed, synth.stream_layer(li, "wu"))
+        # gate/up fused with rows interleaved per 64: [g0..g63, u0..u63, g64..] so one
+        # 128-row GEMM tile holds matching gate and up features (SiLU*mul epilogue)
+        g = torch.empty(F, d, dtype=bf, device=device)
+        u = torch.empty(F, d, dtype=bf, device=device)
+        generate_bf16(g, seed, synth.stream_layer(li, "wg"))
+        generate_bf16(u, seed, synth.stream_layer(li, "wu"))
+        wgu = torch.stack([g.view(F // 64, 64, d), u.view(F // 64, 64, d)], dim=1).reshape(2 * F, d).contiguous()
+        del g, u
         wd = torch.empty(d, F, dtype=bf, device=device)
         generate_bf16(wd, seed, synth.stream_layer(li, "wd"))
         W["layers"].append(dict(attn_norm=torch.ones(d, dtype=bf, device=device), wqkv=wqkv, wo=wo,

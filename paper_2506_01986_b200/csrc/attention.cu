@@ -47,6 +47,8 @@ __global__ void __launch_bounds__(128) tree_attn_kernel(const __grid_constant__ 
   uint64_t *s_anc = reinterpret_cast<uint64_t *>(smem + C::kStages * 2 * C::kTile);  // [64 rows][kAncWords]
   uint64_t *full = s_anc + 64 * kAncWords;
 
+  pdl_trigger();
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int split = blockIdx.x, rblk = blockIdx.y;
   const int sl = blockIdx.z / a.Hkv, h = blockIdx.z % a.Hkv;
@@ -265,6 +267,8 @@ __global__ void __launch_bounds__(128) tree_attn_kernel(const __grid_constant__ 
 
 // one block per output row (m, q head); HD threads
 __global__ void attn_combine_kernel(const __grid_constant__ AttnArgs a, int HD) {
+  pdl_trigger();
+  pdl_wait();
   const long long row = blockIdx.x;
   const int m = (int)(row / a.H);
   const int sl = m / a.Nq;
@@ -298,11 +302,9 @@ static cudaError_t launch_hd(const AttnArgs &a, cudaStream_t st) {
     attr = true;
   }
   dim3 grid(a.nsplit, attention_row_blocks(a.Nq, a.G), a.nseq * a.Hkv);
-  tree_attn_kernel<HD><<<grid, 128, C::kSmem, st>>>(a);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(tree_attn_kernel<HD>, grid, dim3(128), C::kSmem, st, a);
   if (e != cudaSuccess || a.nsplit == 1) return e;
-  attn_combine_kernel<<<(unsigned)((long long)a.nseq * a.Nq * a.H), HD, 0, st>>>(a, HD);
-  return cudaGetLastError();
+  return launch_pdl(attn_combine_kernel, dim3((unsigned)((long long)a.nseq * a.Nq * a.H)), dim3(HD), 0, st, a, HD);
 }
 
 cudaError_t attention_launch(const AttnArgs &a, int head_dim, cudaStream_t st) {

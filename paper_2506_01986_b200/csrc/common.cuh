@@ -20,6 +20,11 @@ SM_DEV float bfbits2f(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16);
 
 SM_DEV uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+// Programmatic dependent launch: wait for the preceding kernel (all reads of its
+// outputs and all writes must come after), and let the next kernel launch.
+SM_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+SM_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 SM_DEV float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

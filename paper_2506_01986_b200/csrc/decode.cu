@@ -13,6 +13,8 @@ namespace sm {
 // tok[n] = root for n = 0, else topk[b][depth(n)-1][rank(n)]
 __global__ void propose_kernel(TreeDev t, const int32_t *root, const int32_t *topk, int K, int nmed, int32_t *tree_tok,
                                int32_t *pos, const int32_t *len) {
+  pdl_trigger();
+  pdl_wait();
   const int bb = blockIdx.x, n = threadIdx.x;
   if (n >= t.N) return;
   int tok;
@@ -26,8 +28,7 @@ __global__ void propose_kernel(TreeDev t, const int32_t *root, const int32_t *to
 }
 cudaError_t propose_launch(TreeDev t, const int32_t *root, const int32_t *topk, int K, int nmed, int b,
                            int32_t *tree_tok, int32_t *pos, const int32_t *len, cudaStream_t st) {
-  propose_kernel<<<b, 256, 0, st>>>(t, root, topk, K, nmed, tree_tok, pos, len);
-  return cudaGetLastError();
+  return launch_pdl(propose_kernel, dim3(b), dim3(256), 0, st, t, root, topk, K, nmed, tree_tok, pos, len);
 }
 
 // ------------------------------------------------------------------ accept (tree DP)
@@ -38,6 +39,8 @@ cudaError_t propose_launch(TreeDev t, const int32_t *root, const int32_t *topk, 
 // a = deepest accepted depth; among those, max log-likelihood then lowest DFS
 // position (Q11); emission clamped by the turn budget and the KV bound x.
 __global__ void __launch_bounds__(256) accept_kernel(const __grid_constant__ AcceptArgs a) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ int s_cond[kMaxTreeNodes];
   __shared__ float s_lp[kMaxTreeNodes];
   __shared__ int s_chosen;
@@ -136,8 +139,7 @@ __global__ void __launch_bounds__(256) accept_kernel(const __grid_constant__ Acc
   }
 }
 cudaError_t accept_launch(const AcceptArgs &a, cudaStream_t st) {
-  accept_kernel<<<a.b, 256, 0, st>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(accept_kernel, dim3(a.b), dim3(256), 0, st, a);
 }
 
 // ------------------------------------------------------------------ compaction
@@ -147,6 +149,8 @@ cudaError_t accept_launch(const AcceptArgs &a, cudaStream_t st) {
 // grid = (L * 2, b, Hkv); 16-byte chunks.
 __global__ void compact_kernel(bf16 *kv_base, int b, int Hkv, int cap, int hd, const int32_t *len,
                                const int32_t *path, int path_ld, const int32_t *n_emit) {
+  pdl_trigger();
+  pdl_wait();
   const int lk = blockIdx.x, bb = blockIdx.y, h = blockIdx.z;
   const int a_eff = n_emit[bb] - 1;
   if (a_eff <= 0) return;
@@ -174,13 +178,14 @@ cudaError_t compact_launch(bf16 *kv_base, int L, int b, int Hkv, int cap, int hd
   // each thread holds up to 2 chunks: threads >= ceil(l * hd/8 / 2)
   const int threads = 128;  // covers a_eff <= 16 rows at hd = 128 (256 chunks)
   dim3 grid(L * 2, b, Hkv);
-  compact_kernel<<<grid, threads, 0, st>>>(kv_base, b, Hkv, cap, hd, len, path, path_ld, n_emit);
-  return cudaGetLastError();
+  return launch_pdl(compact_kernel, grid, dim3(threads), 0, st, kv_base, b, Hkv, cap, hd, len, path, path_ld, n_emit);
 }
 
 // ------------------------------------------------------------------ commit
 __global__ void commit_kernel(int32_t *len, const int32_t *n_emit, int32_t *root, const int32_t *root_next,
                               const int32_t *acc_row, const bf16 *hf, int d, bf16 *head_in, int32_t *emitted_total) {
+  pdl_trigger();
+  pdl_wait();
   const int bb = blockIdx.x;
   const int ne = n_emit[bb];
   if (ne <= 0) return;
@@ -196,25 +201,29 @@ __global__ void commit_kernel(int32_t *len, const int32_t *n_emit, int32_t *root
 cudaError_t commit_launch(int b, int32_t *len, const int32_t *n_emit, int32_t *root, const int32_t *root_next,
                           const int32_t *acc_row, const bf16 *hf, int d, bf16 *head_in, int32_t *emitted_total,
                           cudaStream_t st) {
-  commit_kernel<<<b, 256, 0, st>>>(len, n_emit, root, root_next, acc_row, hf, d, head_in, emitted_total);
-  return cudaGetLastError();
+  return launch_pdl(commit_kernel, dim3(b), dim3(256), 0, st, len, n_emit, root, root_next, acc_row, hf, d, head_in,
+                    emitted_total);
 }
 
-__global__ void advance_len_kernel(int32_t *len, int seq, int n) { len[seq] += n; }
+__global__ void advance_len_kernel(int32_t *len, int seq, int n) {
+  pdl_trigger();
+  pdl_wait();
+  len[seq] += n;
+}
 cudaError_t advance_len_launch(int32_t *len, int seq, int n, cudaStream_t st) {
-  advance_len_kernel<<<1, 1, 0, st>>>(len, seq, n);
-  return cudaGetLastError();
+  return launch_pdl(advance_len_kernel, dim3(1), dim3(1), 0, st, len, seq, n);
 }
 
 __global__ void set_root_kernel(int32_t *root, int seq, const int32_t *argmax_row, const bf16 *hf_row, int d,
                                 bf16 *head_in_row) {
+  pdl_trigger();
+  pdl_wait();
   if (threadIdx.x == 0) root[seq] = argmax_row[0];
   for (int i = threadIdx.x; i < d; i += blockDim.x) head_in_row[i] = hf_row[i];
 }
 cudaError_t set_root_launch(int32_t *root, int seq, const int32_t *argmax_row, const bf16 *hf_row, int d,
                             bf16 *head_in_row, cudaStream_t st) {
-  set_root_kernel<<<1, 256, 0, st>>>(root, seq, argmax_row, hf_row, d, head_in_row);
-  return cudaGetLastError();
+  return launch_pdl(set_root_kernel, dim3(1), dim3(256), 0, st, root, seq, argmax_row, hf_row, d, head_in_row);
 }
 
 // ------------------------------------------------------------------ weight generator

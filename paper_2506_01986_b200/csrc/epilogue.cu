@@ -1,15 +1,18 @@
-// epilogue.cu -- the consumers of the GEMM partials, each fusing the fixed-order
-// split-K reduction with the next elementwise step of the verify forward
-// (rounding contract R1..R10):
-//   embed         x = E[tok]                                  (R1)
-//   resid_norm    x += sum_s o/down partials; h = bf16(rms(x)*g)   (R5/R7 + R2/R8)
-//   qkv_epilogue  q,k,v = sum_s; RoPE(fp32, fp64-built table); q -> bf16,
-//                 k,v -> bf16 into cache slots Lc + n at position Lc + depth(n)   (R3)
-//   silu_mul      a = bf16(SiLU(g) * u)                       (R6)
-//   logits        z = sum_s (fp32), argmax (lowest index on ties) and the
-//                 single-pass typical statistics (m, s, t) of y = z/T   (R9)
-//   heads         r_i = bf16(h + SiLU(R_i h + b_i))          (R10)
-//   topk          top-K of head logits by (value desc, index asc)  (K3)
+// epilogue.cu -- consumers of the K2 GEMM partials.  Each one performs the
+// deterministic stream-K reduction (contributor order) fused with the next
+// elementwise step of the verify forward (rounding contract R1..R10, DESIGN.md
+// §3.2), with enough parallelism to finish in a few microseconds:
+//   embed            x = E[tok]                                        (R1)
+//   resid_norm       x += y (o / down); h = bf16(rms(x) * g)           (R5/R7 + R2/R8)
+//   qkv_consumer     RoPE(q, k) in fp32 at pos Lc + depth, q/k/v -> bf16, k/v into
+//                    cache slot Lc + node                               (R3)
+//   silu_consumer    act = bf16(SiLU(gate) * up)                        (R6)
+//   logits_consumer  z = y (fp32), argmax (lowest index on ties), single-pass
+//                    typical statistics (m, s, t) of z / T               (R9)
+//   heads_r          r_i = bf16(h + SiLU(R_i h + b_i))                  (R10)
+//   topk             top-K of head logits by (value desc, index asc)    (K3)
+// All kernels are launched with programmatic dependent launch: they trigger the
+// next launch immediately and wait for their producer before touching memory.
 #include <float.h>
 
 #include "common.cuh"
@@ -35,146 +38,146 @@ SM_DEV float block_sum(float v, float *red) {
   return r;
 }
 
-// ------------------------------------------------------------------ split sum (stage API)
-__global__ void sum_splits_kernel(const float *part, int splits, long long sstride, int ldp, float *out, int N) {
-  const int m = blockIdx.y;
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= N) return;
-  float acc = 0.f;
-  for (int s = 0; s < splits; ++s) acc += part[s * sstride + (size_t)m * ldp + n];
-  out[(size_t)m * N + n] = acc;
-}
-cudaError_t sum_splits_launch(const float *part, int splits, long long split_stride, int ldp, float *out, int M, int N,
-                              cudaStream_t st) {
-  dim3 grid((N + 255) / 256, M);
-  sum_splits_kernel<<<grid, 256, 0, st>>>(part, splits, split_stride, ldp, out, N);
-  return cudaGetLastError();
-}
-
 // ------------------------------------------------------------------ embed
 __global__ void embed_kernel(const int32_t *tok, const bf16 *E, float *x, int d) {
+  pdl_trigger();
+  pdl_wait();
   const int m = blockIdx.x;
   const bf16 *row = E + (size_t)tok[m] * d;
   float *xr = x + (size_t)m * d;
   for (int i = threadIdx.x; i < d; i += blockDim.x) xr[i] = bf2f(row[i]);
 }
 cudaError_t embed_launch(const int32_t *tok, const bf16 *E, float *x, int M, int d, cudaStream_t st) {
-  embed_kernel<<<M, 256, 0, st>>>(tok, E, x, d);
-  return cudaGetLastError();
+  return launch_pdl(embed_kernel, dim3(M), dim3(256), 0, st, tok, E, x, d);
 }
 
 // ------------------------------------------------------------------ residual + RMSNorm
-__global__ void __launch_bounds__(256) resid_norm_kernel(const float *part, int splits, long long sstride, int ldp,
-                                                         float *x, const bf16 *g, bf16 *h, int d, float eps) {
+constexpr int kNormThreads = 512;
+__global__ void __launch_bounds__(kNormThreads) resid_norm_kernel(PartialView pv, int has_pv, float *x, const bf16 *g,
+                                                                  bf16 *h, int d, float eps) {
   __shared__ float red[32];
+  pdl_trigger();
+  pdl_wait();
   const int m = blockIdx.x;
   float *xr = x + (size_t)m * d;
+  float4 v[4];  // d <= 4 * 4 * kNormThreads = 8192
   float ss = 0.f;
-  for (int i = threadIdx.x * 4; i < d; i += 256 * 4) {
-    float4 v = *reinterpret_cast<float4 *>(xr + i);
-    if (part) {
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int s = 0; s < splits; ++s) {  // fixed split order -> deterministic
-        const float4 p = *reinterpret_cast<const float4 *>(part + s * sstride + (size_t)m * ldp + i);
-        acc.x += p.x;
-        acc.y += p.y;
-        acc.z += p.z;
-        acc.w += p.w;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = (threadIdx.x + k * kNormThreads) * 4;
+    v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < d) {
+      float4 a = *reinterpret_cast<float4 *>(xr + i);
+      if (has_pv) {
+        const float4 y = sk_sum4(pv, 0, m, i);  // R5/R7: fp32 residual += fp32 projection
+        a.x += y.x;
+        a.y += y.y;
+        a.z += y.z;
+        a.w += y.w;
+        *reinterpret_cast<float4 *>(xr + i) = a;
       }
-      v.x += acc.x;  // R5/R7: fp32 residual += fp32 projection
-      v.y += acc.y;
-      v.z += acc.z;
-      v.w += acc.w;
-      *reinterpret_cast<float4 *>(xr + i) = v;
+      v[k] = a;
+      ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
     }
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
-  ss = block_sum<256>(ss, red);
+  ss = block_sum<kNormThreads>(ss, red);
   const float rs = 1.0f / sqrtf(ss / (float)d + eps);
-  for (int i = threadIdx.x * 4; i < d; i += 256 * 4) {
-    const float4 v = *reinterpret_cast<const float4 *>(xr + i);
-    const __nv_bfloat162 g01 = *reinterpret_cast<const __nv_bfloat162 *>(g + i);
-    const __nv_bfloat162 g23 = *reinterpret_cast<const __nv_bfloat162 *>(g + i + 2);
-    uint2 o;
-    o.x = pack_bf16(v.x * rs * __low2float(g01), v.y * rs * __high2float(g01));
-    o.y = pack_bf16(v.z * rs * __low2float(g23), v.w * rs * __high2float(g23));
-    *reinterpret_cast<uint2 *>(h + (size_t)m * d + i) = o;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = (threadIdx.x + k * kNormThreads) * 4;
+    if (i < d) {
+      const __nv_bfloat162 g01 = *reinterpret_cast<const __nv_bfloat162 *>(g + i);
+      const __nv_bfloat162 g23 = *reinterpret_cast<const __nv_bfloat162 *>(g + i + 2);
+      uint2 o;
+      o.x = pack_bf16(v[k].x * rs * __low2float(g01), v[k].y * rs * __high2float(g01));
+      o.y = pack_bf16(v[k].z * rs * __low2float(g23), v[k].w * rs * __high2float(g23));
+      *reinterpret_cast<uint2 *>(h + (size_t)m * d + i) = o;
+    }
   }
 }
-cudaError_t resid_norm_launch(const float *part, int splits, long long split_stride, int ldp, float *x,
-                              const bf16 *g, bf16 *h, int M, int d, float eps, cudaStream_t st) {
-  resid_norm_kernel<<<M, 256, 0, st>>>(part, splits, split_stride, ldp, x, g, h, d, eps);
-  return cudaGetLastError();
+cudaError_t resid_norm_launch(const PartialView *pv, float *x, const bf16 *g, bf16 *h, int M, int d, float eps,
+                              cudaStream_t st) {
+  if (d > 16 * kNormThreads || d % 4) return cudaErrorInvalidValue;
+  PartialView v{};
+  if (pv) v = *pv;
+  return launch_pdl(resid_norm_kernel, dim3(M), dim3(kNormThreads), 0, st, v, pv ? 1 : 0, x, g, h, d, eps);
 }
 
-// ------------------------------------------------------------------ QKV epilogue (RoPE + cache write)
-__global__ void __launch_bounds__(256) qkv_epilogue_kernel(const float *part, int splits, long long sstride, int ldp,
-                                                           RowCtx rc, int H, int Hkv, int hd, const float2 *rope,
-                                                           bf16 *q, bf16 *kc, bf16 *vc, int cap) {
-  const int m = blockIdx.x;
-  const int sl = m / rc.Nq, n = m % rc.Nq;
+// ------------------------------------------------------------------ QKV consumer (RoPE + cache write)
+// thread -> 4 consecutive rotary pairs (c .. c+3) of one head of one token row
+__global__ void __launch_bounds__(256) qkv_consumer_kernel(PartialView pv, RowCtx rc, int H, int Hkv, int hd,
+                                                           const float2 *rope, bf16 *q, bf16 *kc, bf16 *vc, int cap) {
+  pdl_trigger();
+  pdl_wait();
+  const int m = blockIdx.y;
+  const int half = hd / 2;
+  const int quads = half / 4;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (H + 2 * Hkv) * quads) return;
+  const int hh = idx / quads, c = (idx % quads) * 4;
+  const int n0 = hh * hd + c;
+  const float4 a = sk_sum4(pv, 0, m, n0);
+  const float4 b = sk_sum4(pv, 0, m, n0 + half);
+  float x0[4] = {a.x, a.y, a.z, a.w}, x1[4] = {b.x, b.y, b.z, b.w};
+  const int sl = m / rc.Nq, node = m % rc.Nq;
   const int seq = rc.seq_base + sl;
   const int Lc = rc.len[seq];
-  const int pos = Lc + rc.depth[n];
-  const int slot = Lc + n;
-  const int half = hd / 2;
-  const int npairs = (H + 2 * Hkv) * half;
-  const float *pr = part + (size_t)m * ldp;
-  for (int i = threadIdx.x; i < npairs; i += blockDim.x) {
-    const int hh = i / half, c = i % half;
-    const int col = hh * hd + c;
-    float v0 = 0.f, v1 = 0.f;
-    for (int s = 0; s < splits; ++s) {
-      v0 += pr[s * sstride + col];
-      v1 += pr[s * sstride + col + half];
+  if (hh < H + Hkv) {  // rotate-half RoPE at pos = Lc + depth
+    const float2 *cs = rope + (size_t)(Lc + rc.depth[node]) * half + c;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 r = cs[e];
+      const float y0 = x0[e] * r.x - x1[e] * r.y;
+      const float y1 = x1[e] * r.x + x0[e] * r.y;
+      x0[e] = y0;
+      x1[e] = y1;
     }
-    if (hh < H + Hkv) {  // q and k heads: rotate-half RoPE at pos
-      const float2 cs = rope[(size_t)pos * half + c];
-      const float r0 = v0 * cs.x - v1 * cs.y;
-      const float r1 = v1 * cs.x + v0 * cs.y;
-      v0 = r0;
-      v1 = r1;
-    }
-    bf16 *dst;
-    if (hh < H) {
-      dst = q + ((size_t)m * H + hh) * hd;
-    } else if (hh < H + Hkv) {
-      dst = kc + (((size_t)seq * Hkv + (hh - H)) * cap + slot) * hd;
-    } else {
-      dst = vc + (((size_t)seq * Hkv + (hh - H - Hkv)) * cap + slot) * hd;
-    }
-    dst[c] = f2bf(v0);
-    dst[c + half] = f2bf(v1);
   }
+  bf16 *dst;
+  if (hh < H) {
+    dst = q + ((size_t)m * H + hh) * hd;
+  } else if (hh < H + Hkv) {
+    dst = kc + (((size_t)seq * Hkv + (hh - H)) * cap + Lc + node) * hd;
+  } else {
+    dst = vc + (((size_t)seq * Hkv + (hh - H - Hkv)) * cap + Lc + node) * hd;
+  }
+  uint2 lo, hi;
+  lo.x = pack_bf16(x0[0], x0[1]);
+  lo.y = pack_bf16(x0[2], x0[3]);
+  hi.x = pack_bf16(x1[0], x1[1]);
+  hi.y = pack_bf16(x1[2], x1[3]);
+  *reinterpret_cast<uint2 *>(dst + c) = lo;
+  *reinterpret_cast<uint2 *>(dst + c + half) = hi;
 }
-cudaError_t qkv_epilogue_launch(const float *part, int splits, long long split_stride, int ldp, RowCtx rc, int H,
-                                int Hkv, int hd, const float2 *rope, bf16 *q, bf16 *kcache, bf16 *vcache, int cap,
-                                cudaStream_t st) {
-  qkv_epilogue_kernel<<<rc.M, 256, 0, st>>>(part, splits, split_stride, ldp, rc, H, Hkv, hd, rope, q, kcache, vcache,
-                                            cap);
-  return cudaGetLastError();
+cudaError_t qkv_consumer_launch(const PartialView &pv, RowCtx rc, int H, int Hkv, int hd, const float2 *rope, bf16 *q,
+                                bf16 *kcache, bf16 *vcache, int cap, cudaStream_t st) {
+  const int work = (H + 2 * Hkv) * (hd / 8);
+  return launch_pdl(qkv_consumer_kernel, dim3((work + 255) / 256, rc.M), dim3(256), 0, st, pv, rc, H, Hkv, hd, rope,
+                    q, kcache, vcache, cap);
 }
 
-// ------------------------------------------------------------------ SiLU(g) * u
-__global__ void __launch_bounds__(256) silu_mul_kernel(const float *part, int splits, long long sstride, int ldp, int F,
-                                                       bf16 *act) {
+// ------------------------------------------------------------------ SiLU(gate) * up
+// fused weight rows: tile t = [gate 64t..64t+63 | up 64t..64t+63]
+__global__ void __launch_bounds__(256) silu_consumer_kernel(PartialView pv, int F, bf16 *act) {
+  pdl_trigger();
+  pdl_wait();
   const int m = blockIdx.y;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= F) return;
-  const float *pr = part + (size_t)m * ldp;
-  float gg = 0.f, uu = 0.f;
-  for (int s = 0; s < splits; ++s) {
-    gg += pr[s * sstride + j];
-    uu += pr[s * sstride + F + j];
-  }
-  const float si = gg / (1.0f + expf(-gg));
-  act[(size_t)m * F + j] = f2bf(si * uu);
+  const int f = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (f >= F) return;
+  const int ng = (f >> 6) * 128 + (f & 63);
+  const float4 g = sk_sum4(pv, 0, m, ng);
+  const float4 u = sk_sum4(pv, 0, m, ng + 64);
+  const float gg[4] = {g.x, g.y, g.z, g.w}, uu[4] = {u.x, u.y, u.z, u.w};
+  float o[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) o[e] = gg[e] / (1.0f + expf(-gg[e])) * uu[e];
+  uint2 w;
+  w.x = pack_bf16(o[0], o[1]);
+  w.y = pack_bf16(o[2], o[3]);
+  *reinterpret_cast<uint2 *>(act + (size_t)m * F + f) = w;
 }
-cudaError_t silu_mul_launch(const float *part, int splits, long long split_stride, int ldp, int F, bf16 *act, int M,
-                            cudaStream_t st) {
-  dim3 grid((F + 255) / 256, M);
-  silu_mul_kernel<<<grid, 256, 0, st>>>(part, splits, split_stride, ldp, F, act);
-  return cudaGetLastError();
+cudaError_t silu_consumer_launch(const PartialView &pv, int F, bf16 *act, cudaStream_t st) {
+  return launch_pdl(silu_consumer_kernel, dim3((F / 4 + 255) / 256, pv.M), dim3(256), 0, st, pv, F, act);
 }
 
 // ------------------------------------------------------------------ logits: argmax + typical stats
@@ -192,6 +195,18 @@ SM_DEV MST mst_merge(MST a, MST b) {
   r.t = ea * (a.t + (a.m - M) * a.s) + eb * (b.t + (b.m - M) * b.s);
   return r;
 }
+SM_DEV void mst_add(MST &acc, float y) {
+  if (y > acc.m) {
+    const float e = (acc.m == -INFINITY) ? 0.f : expf(acc.m - y);
+    acc.t = (acc.m == -INFINITY) ? 0.f : e * (acc.t + (acc.m - y) * acc.s);
+    acc.s = acc.s * e + 1.f;
+    acc.m = y;
+  } else {
+    const float e = expf(y - acc.m);
+    acc.s += e;
+    acc.t += e * (y - acc.m);
+  }
+}
 SM_DEV void argmax_merge(float &v, int &i, float v2, int i2) {
   if (v2 > v || (v2 == v && i2 < i)) {
     v = v2;
@@ -199,37 +214,33 @@ SM_DEV void argmax_merge(float &v, int &i, float v2, int i2) {
   }
 }
 
-__global__ void __launch_bounds__(512) logits_finalize_kernel(const float *part, int splits, long long sstride,
-                                                              int ldp, int V, const int32_t *row_index,
-                                                              float inv_temp, float *z_out, int ldz, int32_t *argmax,
-                                                              float *stats) {
+template <bool FROM_PARTIALS>
+__global__ void __launch_bounds__(512) logits_kernel(PartialView pv, const float *z_in, int V, float inv_temp,
+                                                     float *z_out, int32_t *argmax, float *stats) {
   __shared__ float sv[32];
   __shared__ int si[32];
   __shared__ MST smst[32];
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
-  const int m = row_index ? row_index[r] : r;
-  const float *pr = part + (size_t)m * ldp;
   float bv = -INFINITY;
   int bi = 0x7fffffff;
   MST acc{-INFINITY, 0.f, 0.f};
-  for (int j = threadIdx.x; j < V; j += blockDim.x) {
-    float z = 0.f;
-    for (int s = 0; s < splits; ++s) z += pr[s * sstride + j];
-    if (z_out) z_out[(size_t)r * ldz + j] = z;
-    argmax_merge(bv, bi, z, j);
-    const float y = z * inv_temp;
-    if (y > acc.m) {
-      const float e = (acc.m == -INFINITY) ? 0.f : expf(acc.m - y);
-      acc.t = (acc.m == -INFINITY) ? 0.f : e * (acc.t + (acc.m - y) * acc.s);
-      acc.s = acc.s * e + 1.f;
-      acc.m = y;
+  for (int j = threadIdx.x * 4; j < V; j += blockDim.x * 4) {
+    float4 z4;
+    if constexpr (FROM_PARTIALS) {
+      z4 = sk_sum4(pv, 0, r, j);
+      if (z_out) *reinterpret_cast<float4 *>(z_out + (size_t)r * V + j) = z4;
     } else {
-      const float e = expf(y - acc.m);
-      acc.s += e;
-      acc.t += e * (y - acc.m);
+      z4 = *reinterpret_cast<const float4 *>(z_in + (size_t)r * V + j);
+    }
+    const float zz[4] = {z4.x, z4.y, z4.z, z4.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      argmax_merge(bv, bi, zz[e], j + e);
+      mst_add(acc, zz[e] * inv_temp);
     }
   }
-  // warp reduce
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const float v2 = __shfl_xor_sync(0xffffffffu, bv, o);
@@ -259,30 +270,39 @@ __global__ void __launch_bounds__(512) logits_finalize_kernel(const float *part,
     }
   }
 }
-cudaError_t logits_finalize_launch(const float *part, int splits, long long split_stride, int ldp, int V,
-                                   const int32_t *row_index, int rows, float inv_temp, float *z_out, int ldz,
-                                   int32_t *argmax, float *stats, cudaStream_t st) {
-  logits_finalize_kernel<<<rows, 512, 0, st>>>(part, splits, split_stride, ldp, V, row_index, inv_temp, z_out, ldz,
-                                               argmax, stats);
-  return cudaGetLastError();
+cudaError_t logits_consumer_launch(const PartialView &pv, float inv_temp, float *z_out, int32_t *argmax, float *stats,
+                                   cudaStream_t st) {
+  return launch_pdl(logits_kernel<true>, dim3(pv.M), dim3(512), 0, st, pv, (const float *)nullptr, pv.N, inv_temp,
+                    z_out, argmax, stats);
+}
+cudaError_t logits_finalize_launch(const float *z, int V, int rows, float inv_temp, int32_t *argmax, float *stats,
+                                   cudaStream_t st) {
+  PartialView pv{};
+  return launch_pdl(logits_kernel<false>, dim3(rows), dim3(512), 0, st, pv, z, V, inv_temp, (float *)nullptr, argmax,
+                    stats);
 }
 
 // ------------------------------------------------------------------ top-k (K3)
-// One block per row: the split-summed row is staged in shared memory, then K
-// rounds of a block argmax by (value desc, index asc); taken entries become NaN.
-__global__ void __launch_bounds__(1024) topk_kernel(const float *part, int splits, long long sstride, int ldp, int V,
-                                                    int k, int32_t *idx, int ld_idx, int rows_per_group,
-                                                    long long group_stride) {
+// One block per row: the row is staged in shared memory, then K rounds of a
+// block argmax by (value desc, index asc); taken entries become NaN.
+template <bool FROM_PARTIALS>
+__global__ void __launch_bounds__(1024) topk_kernel(PartialView pv, const float *rows_in, int nb, int V, int k,
+                                                    int32_t *idx) {
   extern __shared__ float srow[];
   __shared__ float wv[32];
   __shared__ int wi[32];
-  const int r = blockIdx.x;
-  const int grp = r / rows_per_group, rr = r % rows_per_group;
-  const float *pr = part + grp * group_stride + (size_t)rr * ldp;
-  for (int j = threadIdx.x; j < V; j += blockDim.x) {
-    float z = 0.f;
-    for (int s = 0; s < splits; ++s) z += pr[s * sstride + j];
-    srow[j] = z;
+  pdl_trigger();
+  pdl_wait();
+  const int r = blockIdx.x;  // FROM_PARTIALS: r = head * nb + b
+  const int head = r / nb, bb = r % nb;
+  for (int j = threadIdx.x * 4; j < V; j += blockDim.x * 4) {
+    float4 z4;
+    if constexpr (FROM_PARTIALS) {
+      z4 = sk_sum4(pv, head, bb, j);
+    } else {
+      z4 = *reinterpret_cast<const float4 *>(rows_in + (size_t)r * V + j);
+    }
+    *reinterpret_cast<float4 *>(srow + j) = z4;
   }
   __syncthreads();
   for (int kk = 0; kk < k; ++kk) {
@@ -305,68 +325,72 @@ __global__ void __launch_bounds__(1024) topk_kernel(const float *part, int split
     __syncthreads();
     if (threadIdx.x == 0) {
       for (int w = 1; w < (int)(blockDim.x >> 5); ++w) argmax_merge(bv, bi, wv[w], wi[w]);
-      // output layout: row r = grp * rows_per_group + rr -> idx[(rr * groups + grp) * k]
-      idx[(size_t)rr * ld_idx + grp * k + kk] = bi;
+      // FROM_PARTIALS: idx[b][head][k]; plain rows: idx[r][k]
+      const size_t o = FROM_PARTIALS ? ((size_t)bb * (gridDim.x / nb) + head) * k + kk : (size_t)r * k + kk;
+      idx[o] = bi;
       if (bi >= 0 && bi < V) srow[bi] = __int_as_float(0x7fc00000);
     }
     __syncthreads();
   }
 }
-cudaError_t topk_launch(const float *part, int splits, long long split_stride, int ldp, int V, int rows, int k,
-                        int32_t *idx, int ld_idx, cudaStream_t st) {
-  // generic single-group form (rows independent, idx[r * ld_idx + kk])
-  const size_t smem = (size_t)V * sizeof(float);
+template <bool FP>
+static cudaError_t topk_attr(size_t smem) {
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(topk_kernel<FP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = smem;
   }
-  topk_kernel<<<rows, 1024, smem, st>>>(part, splits, split_stride, ldp, V, k, idx, ld_idx, rows, 0);
-  return cudaGetLastError();
+  return cudaSuccess;
 }
-// grouped form used by the Medusa heads: rows = groups * rows_per_group
-cudaError_t topk_grouped_launch(const float *part, int splits, long long split_stride, int ldp, int V, int groups,
-                                int rows_per_group, long long group_stride, int k, int32_t *idx, int ld_idx,
-                                cudaStream_t st) {
+cudaError_t topk_consumer_launch(const PartialView &pv, int nmed, int nb, int V, int k, int32_t *idx, cudaStream_t st) {
   const size_t smem = (size_t)V * sizeof(float);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
-  topk_kernel<<<groups * rows_per_group, 1024, smem, st>>>(part, splits, split_stride, ldp, V, k, idx, ld_idx,
-                                                           rows_per_group, group_stride);
-  return cudaGetLastError();
+  cudaError_t e = topk_attr<true>(smem);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(topk_kernel<true>, dim3(nmed * nb), dim3(1024), smem, st, pv, (const float *)nullptr, nb, V, k,
+                    idx);
+}
+cudaError_t topk_launch(const float *logits, int rows, int V, int k, int32_t *idx, cudaStream_t st) {
+  const size_t smem = (size_t)V * sizeof(float);
+  cudaError_t e = topk_attr<false>(smem);
+  if (e != cudaSuccess) return e;
+  PartialView pv{};
+  return launch_pdl(topk_kernel<false>, dim3(rows), dim3(1024), smem, st, pv, logits, rows, V, k, idx);
 }
 
-// ------------------------------------------------------------------ Medusa head ResBlock epilogue
+// ------------------------------------------------------------------ Medusa head ResBlock consumer
 struct BetaPtrs {
   const bf16 *p[kMaxGemmBatch];
 };
-__global__ void heads_epilogue_kernel(const float *part, int splits, long long sstride, int ldp, long long head_stride,
-                                      int b, int d, const bf16 *head_in, BetaPtrs beta, bf16 *r_out,
-                                      long long r_stride) {
+__global__ void heads_r_kernel(PartialView pv, int d, const bf16 *head_in, BetaPtrs beta, bf16 *r_out,
+                               long long r_stride) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.z, bb = blockIdx.y;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= d) return;
-  const float *pr = part + i * head_stride + (size_t)bb * ldp;
-  float t = 0.f;
-  for (int s = 0; s < splits; ++s) t += pr[s * sstride + j];
-  t += bf2f(beta.p[i][j]);
+  const float t = sk_sum1(pv, i, bb, j) + bf2f(beta.p[i][j]);
   const float hv = bf2f(head_in[(size_t)bb * d + j]);
   r_out[i * r_stride + (size_t)bb * d + j] = f2bf(hv + t / (1.0f + expf(-t)));
 }
-cudaError_t heads_epilogue_grouped_launch(const float *part, int splits, long long split_stride, int ldp,
-                                          long long head_stride, int nmed, int b, int d, const bf16 *head_in,
-                                          const bf16 *const *beta, bf16 *r_out, long long r_stride, cudaStream_t st) {
+cudaError_t heads_r_consumer_launch(const PartialView &pv, int nmed, int nb, int d, const bf16 *head_in,
+                                    const bf16 *const *beta, bf16 *r_out, long long r_stride, cudaStream_t st) {
   BetaPtrs bp{};
   for (int i = 0; i < nmed && i < kMaxGemmBatch; ++i) bp.p[i] = beta[i];
-  dim3 grid((d + 255) / 256, b, nmed);
-  heads_epilogue_kernel<<<grid, 256, 0, st>>>(part, splits, split_stride, ldp, head_stride, b, d, head_in, bp, r_out,
-                                             r_stride);
-  return cudaGetLastError();
+  return launch_pdl(heads_r_kernel, dim3((d + 255) / 256, nb, nmed), dim3(256), 0, st, pv, d, head_in, bp, r_out,
+                    r_stride);
+}
+
+// ------------------------------------------------------------------ plain (stage API)
+__global__ void plain_kernel(PartialView pv, float *out) {
+  pdl_trigger();
+  pdl_wait();
+  const int m = blockIdx.y;
+  const int n0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  for (int e = 0; e < 4 && n0 + e < pv.N; ++e) out[(size_t)m * pv.N + n0 + e] = sk_sum1(pv, 0, m, n0 + e);
+}
+cudaError_t plain_consumer_launch(const PartialView &pv, float *out, cudaStream_t st) {
+  return launch_pdl(plain_kernel, dim3((pv.N + 1023) / 1024, pv.M), dim3(256), 0, st, pv, out);
 }
 
 }  // namespace sm

@@ -1,16 +1,28 @@
-// gemm.cu -- K2: small-M bf16 GEMM on 5th-gen tensor cores (tcgen05 + TMEM + TMA).
+// gemm.cu -- K2: small-M bf16 GEMM on 5th-gen tensor cores (tcgen05 + TMEM + TMA),
+// persistent and stream-K balanced; fp32 partials reduced by the consumer.
 //
-//   out[split][m][n] = sum_{k in split} x[m][k] * w[n][k]        (fp32 partials)
+//   y[m][n] = sum_k x[m][k] * w[n][k]      (x: token rows, w: nn.Linear weight)
 //
 // Swap-AB: the weight tile (128 output features x 64 k, K-major, SWIZZLE_128B)
-// is the UMMA A operand (M = 128 lanes of TMEM), the token rows (BN <= 256,
-// padded to 16) are the UMMA N dimension.  This keeps M = b*N = 1..256 token
-// rows from wasting the 128-row MMA.  Warp roles: warp 0 lane 0
-// issues TMA into a STAGES-deep mbarrier ring, warp 1 lane 0 issues tcgen05.mma
-// and tcgen05.commit (frees the smem slot), then all 4 warps drain the fp32
-// accumulator with tcgen05.ld and write coalesced fp32 partials.  Split-K over
-// CTAs fills the 148 SMs; the fixed-order reduction of the partials is fused
-// into the consumer kernels (epilogue.cu), so results are deterministic.
+// is the UMMA A operand (M = 128 TMEM lanes); the token rows (BN <= 256, padded
+// to 16) are the UMMA N dimension, so b*N = 1..256 rows never waste the 128-row
+// MMA.  The path is HBM-bound: every weight byte is read once.
+//
+// Work split: U = tiles x k-blocks units are divided evenly over P CTAs (one per
+// SM), so no SM idles in a partial wave.  A CTA walks its contiguous unit range;
+// each maximal run inside one tile is a "segment" whose fp32 accumulator goes to
+// the partial slot (tile, contributor) -- no atomics, no fences, no serial
+// fixup tail.  The consumer kernels (epilogue.cu) sum a tile's contributors in
+// CTA order (deterministic) and fuse the next elementwise step.
+//
+// Warp roles (192 threads): warp 0 = TMA producer (1 lane), warp 1 = tcgen05.mma
+// issuer (1 lane) + TMEM allocator, warps 2..5 = epilogue (tcgen05.ld; warp w
+// reads TMEM lanes 32*(w%4)..+31).  Two TMEM accumulators let the MMA of the
+// next segment overlap the write-out of the previous one.
+//
+// Programmatic dependent launch: weights do not depend on the previous kernel,
+// so the producer streams the first STAGES weight tiles before
+// griddepcontrol.wait; activations are loaded after it.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -18,96 +30,167 @@ namespace sm {
 
 template <int BN>
 struct GemmCfg {
-  static constexpr int kA = 128 * 64 * 2;          // weight tile bytes
-  static constexpr int kB = BN * 64 * 2;           // activation tile bytes
+  static constexpr int kA = 128 * 64 * 2;  // weight tile bytes
+  static constexpr int kB = BN * 64 * 2;   // activation tile bytes
   static constexpr int kStage = kA + kB;
-  static constexpr int kStages = BN <= 16 ? 6 : BN <= 32 ? 5 : BN <= 64 ? 4 : BN <= 128 ? 6 : 4;
-  static constexpr int kTmemCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
-  static constexpr int kSmem = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kStages = (216 * 1024) / kStage;
+  static constexpr int kChunk = BN < 32 ? BN : 32;  // token columns per tcgen05.ld
+  static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+  static constexpr int kSmem = kStages * kStage + 1024 + 256;
 };
 
+SM_DEV void tmem_ld32(uint32_t taddr, float *v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%"
+      "19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+template <int C>
+SM_DEV void tmem_ldc(uint32_t taddr, float *v) {
+  if constexpr (C == 32) {
+    tmem_ld32(taddr, v);
+  } else {
+    float t[16];
+    tmem_ld16(taddr, t);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = t[i];
+  }
+}
+
 template <int BN>
-__global__ void __launch_bounds__(128, 1) gemm_bf16_tc_kernel(const __grid_constant__ GemmArgs args) {
+__global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_constant__ GemmArgs a) {
   using C = GemmCfg<BN>;
+  constexpr int CH = C::kChunk;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = smem;
   uint8_t *sB = smem + C::kStages * C::kA;
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::kStages * C::kStage);
   uint64_t *empty = full + C::kStages;
-  uint64_t *done = empty + C::kStages;
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(done + 1);
+  uint64_t *tfull = empty + C::kStages;  // [2]
+  uint64_t *tempty = tfull + 2;          // [2]
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mt = blockIdx.x, split = blockIdx.y;
-  const int bi = blockIdx.z % args.batch, tt = blockIdx.z / args.batch;
-  const int kb0 = split * args.kb_per_split;
-  const int nkb = min(args.kb_total - kb0, args.kb_per_split);
-  const CUtensorMap *tmW = &args.tmW[bi];
-  const CUtensorMap *tmX = &args.tmX[bi];
+  const SplitPlan &pl = a.plan;
+  const int c = blockIdx.x;
+  const long long u0 = sk_unit0(c, pl), u1 = sk_unit0(c + 1, pl);
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(tmW);
-    tma_prefetch_desc(tmX);
+    tma_prefetch_desc(&a.tmW[0]);
+    tma_prefetch_desc(&a.tmX[0]);
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(done, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 128);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<C::kTmemCols>(tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_trigger();  // let the consumer launch now and wait on our completion
   const uint32_t tmem = *tslot;
 
-  if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer
-    const uint64_t pol_w = policy_evict_first();   // weights stream through once
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % C::kStages;
-      if (i >= C::kStages) mbar_wait(&empty[s], ((i / C::kStages) - 1) & 1);
-      mbar_arrive_expect_tx(&full[s], C::kStage);
-      const int kc = (kb0 + i) * 64;
-      tma_load_2d_hint(sA + s * C::kA, tmW, &full[s], kc, mt * 128, pol_w);
-#pragma unroll
-      for (int r = 0; r < BN / 16; ++r) tma_load_2d(sB + s * C::kB + r * 2048, tmX, &full[s], kc, args.x_row0 + tt * BN + r * 16);
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer (single thread)
-    constexpr uint32_t idesc = umma_idesc_bf16(128, BN);
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % C::kStages;
-      mbar_wait(&full[s], (i / C::kStages) & 1);
-      tc_fence_after();
-      const uint64_t ad = umma_desc_sw128(smem_u32(sA + s * C::kA));
-      const uint64_t bd = umma_desc_sw128(smem_u32(sB + s * C::kB));
-#pragma unroll
-      for (int k = 0; k < 4; ++k)  // UMMA_K = 16 bf16 = 32 B -> +2 in the 16-byte address field
-        umma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0);
-      umma_commit(&empty[s]);
-    }
-    umma_commit(done);
-  }
-  __syncwarp();
-
-  // ---------------- epilogue: TMEM -> registers -> fp32 partials (all 4 warps)
-  mbar_wait(done, 0);
-  tc_fence_after();
-  const int n = mt * 128 + warp * 32 + lane;  // output feature = TMEM lane
-  float *out = args.out[bi] + (size_t)split * args.split_stride;
-  const int m_base = tt * BN;
-#pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 16) {
-    float v[16];
-    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
-    if (n < args.N) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int m = m_base + c0 + j;
-        if (m < args.M) out[(size_t)m * args.ldo + n] = v[j];
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      const uint64_t pol_w = policy_evict_first();
+      const int pre = (u1 - u0) < (long long)C::kStages ? (int)(u1 - u0) : C::kStages;
+      for (int i = 0; i < pre; ++i) {  // weights first: independent of the previous kernel
+        const long long u = u0 + i;
+        int bi, tt, mt;
+        sk_decode(sk_tile(u, pl), pl, bi, tt, mt);
+        mbar_arrive_expect_tx(&full[i], C::kStage);
+        tma_load_2d_hint(sA + i * C::kA, &a.tmW[bi], &full[i], sk_kb(u, pl) * 64, mt * 128, pol_w);
       }
+      pdl_wait();  // activations only after the producer kernel completed
+      for (int i = 0; i < pre; ++i) {
+        const long long u = u0 + i;
+        int bi, tt, mt;
+        sk_decode(sk_tile(u, pl), pl, bi, tt, mt);
+#pragma unroll
+        for (int r = 0; r < BN / 16; ++r)
+          tma_load_2d(sB + i * C::kB + r * 2048, &a.tmX[bi], &full[i], sk_kb(u, pl) * 64,
+                      a.x_row0 + tt * BN + r * 16);
+      }
+      for (long long u = u0 + pre; u < u1; ++u) {
+        const int i = (int)(u - u0);
+        const int s = i % C::kStages;
+        mbar_wait(&empty[s], ((i / C::kStages) - 1) & 1);
+        int bi, tt, mt;
+        sk_decode(sk_tile(u, pl), pl, bi, tt, mt);
+        const int kc = sk_kb(u, pl) * 64;
+        mbar_arrive_expect_tx(&full[s], C::kStage);
+        tma_load_2d_hint(sA + s * C::kA, &a.tmW[bi], &full[s], kc, mt * 128, pol_w);
+#pragma unroll
+        for (int r = 0; r < BN / 16; ++r)
+          tma_load_2d(sB + s * C::kB + r * 2048, &a.tmX[bi], &full[s], kc, a.x_row0 + tt * BN + r * 16);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      constexpr uint32_t idesc = umma_idesc_bf16(128, BN);
+      int seg = 0;
+      bool seg_start = true;
+      for (long long u = u0; u < u1; ++u) {
+        const int i = (int)(u - u0);
+        const int s = i % C::kStages;
+        const int buf = seg & 1;
+        if (seg_start && seg >= 2) mbar_wait(&tempty[buf], ((seg >> 1) - 1) & 1);
+        mbar_wait(&full[s], (i / C::kStages) & 1);
+        tc_fence_after();
+        const uint64_t ad = umma_desc_sw128(smem_u32(sA + s * C::kA));
+        const uint64_t bd = umma_desc_sw128(smem_u32(sB + s * C::kB));
+        const uint32_t td = tmem + buf * BN;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) umma_bf16(td, ad + 2 * k, bd + 2 * k, idesc, (!seg_start || k > 0) ? 1u : 0u);
+        umma_commit(&empty[s]);
+        seg_start = false;
+        if ((u + 1) % pl.kb_total == 0 || u + 1 == u1) {
+          umma_commit(&tfull[buf]);
+          ++seg;
+          seg_start = true;
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue warps 2..5: TMEM lanes 32*(warp%4) .. +31
+    const int wq = warp & 3;
+    const int lrow = wq * 32 + lane;  // feature row inside the tile (= TMEM lane)
+    int seg = 0;
+    long long u = u0;
+    while (u < u1) {
+      const int t = sk_tile(u, pl);
+      const long long seg_end = min(u1, (long long)(t + 1) * pl.kb_total);
+      const int buf = seg & 1;
+      mbar_wait(&tfull[buf], (seg >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem + ((uint32_t)(wq * 32) << 16) + buf * BN;
+      float *dst = sk_partial(a.ws, pl, t, c - sk_cta_of((long long)t * pl.kb_total, pl));
+      for (int c0 = 0; c0 < BN; c0 += CH) {
+        float v[CH];
+        tmem_ldc<CH>(tbase + c0, v);
+#pragma unroll
+        for (int j = 0; j < CH; ++j) dst[(size_t)(c0 + j) * 128 + lrow] = v[j];  // coalesced 512 B rows
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[buf]);
+      u = seg_end;
+      ++seg;
     }
   }
   tc_fence_before();
@@ -115,18 +198,32 @@ __global__ void __launch_bounds__(128, 1) gemm_bf16_tc_kernel(const __grid_const
   if (warp == 1) tmem_dealloc<C::kTmemCols>(tmem);
 }
 
+static bool g_pdl = true;
+static int g_ctas = 0;
+void gemm_set_pdl(bool on) { g_pdl = on; }
+bool gemm_pdl() { return g_pdl; }
+void gemm_set_ctas(int n) { g_ctas = n; }
+
 template <int BN>
-static cudaError_t launch_bn(const GemmArgs &a, int m_tiles, int token_tiles, cudaStream_t st) {
+static cudaError_t launch_bn(const GemmArgs &a, cudaStream_t st) {
   using C = GemmCfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    cudaError_t e = cudaFuncSetAttribute(gemm_streamk_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dim3 grid(m_tiles, a.splits, a.batch * token_tiles);
-  gemm_bf16_tc_kernel<BN><<<grid, 128, C::kSmem, st>>>(a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(a.plan.P);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_streamk_kernel<BN>, a);
 }
 
 int gemm_pick_bn(int M) {
@@ -137,33 +234,35 @@ int gemm_pick_bn(int M) {
   return 256;
 }
 
-// Choose split-K so that tiles * splits covers >= 2 waves of 148 SMs (memory-bound
-// regime: every SM must be streaming weights), keeping >= 2 k-blocks per split.
 void gemm_plan(GemmArgs &a, int N, int K, int M, int batch) {
   a.N = N;
   a.K = K;
   a.M = M;
   a.batch = batch;
-  a.bn = gemm_pick_bn(M);
-  const int m_tiles = (N + 127) / 128;
-  const int token_tiles = (M + a.bn - 1) / a.bn;
-  const int tiles = m_tiles * token_tiles * batch;
-  a.kb_total = (K + 63) / 64;
-  int splits = (2 * kNumSMs + tiles - 1) / tiles;
-  splits = max(1, min(splits, a.kb_total / 2 > 0 ? a.kb_total / 2 : 1));
-  a.kb_per_split = (a.kb_total + splits - 1) / splits;
-  a.splits = (a.kb_total + a.kb_per_split - 1) / a.kb_per_split;
+  SplitPlan &p = a.plan;
+  p.bn = gemm_pick_bn(M);
+  p.m_tiles = (N + 127) / 128;
+  p.token_tiles = (M + p.bn - 1) / p.bn;
+  p.tiles = p.m_tiles * p.token_tiles * batch;
+  p.kb_total = (K + 63) / 64;
+  const long long U = (long long)p.tiles * p.kb_total;
+  const int want = g_ctas > 0 ? g_ctas : kNumSMs;
+  p.P = (int)(U < want ? U : want);
+  p.U = U;
+  // contributors per tile <= ceil(KB / floor(U/P)) + 1
+  const long long per = U / p.P;
+  p.maxc = (int)((p.kb_total + per - 1) / per) + 1;
 }
 
+size_t gemm_ws_floats(const GemmArgs &a) { return (size_t)a.plan.tiles * a.plan.maxc * a.plan.bn * 128; }
+
 cudaError_t gemm_launch(const GemmArgs &a, cudaStream_t st) {
-  const int m_tiles = (a.N + 127) / 128;
-  const int token_tiles = (a.M + a.bn - 1) / a.bn;
-  switch (a.bn) {
-    case 16: return launch_bn<16>(a, m_tiles, token_tiles, st);
-    case 32: return launch_bn<32>(a, m_tiles, token_tiles, st);
-    case 64: return launch_bn<64>(a, m_tiles, token_tiles, st);
-    case 128: return launch_bn<128>(a, m_tiles, token_tiles, st);
-    default: return launch_bn<256>(a, m_tiles, token_tiles, st);
+  switch (a.plan.bn) {
+    case 16: return launch_bn<16>(a, st);
+    case 32: return launch_bn<32>(a, st);
+    case 64: return launch_bn<64>(a, st);
+    case 128: return launch_bn<128>(a, st);
+    default: return launch_bn<256>(a, st);
   }
 }
 

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace sm {
 
 typedef __nv_bfloat16 bf16;
@@ -13,20 +15,85 @@ constexpr int kMaxGemmBatch = 5;
 constexpr int kMaxTreeNodes = 256;
 constexpr int kAncWords = kMaxTreeNodes / 64;
 
-// ---------------------------------------------------------------- K2 GEMM
+struct RowCtx {                // forward rows m = (seq - seq_base) * Nq + n
+  int M, Nq, seq_base;
+  const int32_t *len;          // Lc[seq]
+  const int32_t *depth;        // [Nq]
+};
+
+// ---------------------------------------------------------------- K2 GEMM split plan
+// Stream-K partition: U = tiles * kb_total units split evenly over P CTAs, CTA c
+// owns [U*c/P, U*(c+1)/P).  Tile t = (bi * token_tiles + tt) * m_tiles + mt
+// covers 128 output features x bn token rows.  Every (tile, contributing CTA)
+// writes an fp32 partial [bn][128] at slot t * maxc + (c - first CTA of t).
+struct SplitPlan {
+  long long U;
+  int P, bn, m_tiles, token_tiles, tiles, kb_total, maxc;
+};
+__host__ __device__ inline long long sk_unit0(int c, const SplitPlan &p) { return p.U * c / p.P; }
+__host__ __device__ inline int sk_cta_of(long long u, const SplitPlan &p) {
+  return (int)(((u + 1) * p.P + p.U - 1) / p.U) - 1;
+}
+__host__ __device__ inline int sk_tile(long long u, const SplitPlan &p) { return (int)(u / p.kb_total); }
+__host__ __device__ inline int sk_kb(long long u, const SplitPlan &p) { return (int)(u % p.kb_total); }
+__host__ __device__ inline void sk_decode(int t, const SplitPlan &p, int &bi, int &tt, int &mt) {
+  mt = t % p.m_tiles;
+  const int r = t / p.m_tiles;
+  tt = r % p.token_tiles;
+  bi = r / p.token_tiles;
+}
+__host__ __device__ inline float *sk_partial(float *ws, const SplitPlan &p, int t, int k) {
+  return ws + ((size_t)t * p.maxc + k) * p.bn * 128;
+}
+// Where a GEMM's partials live, for the consumer kernels.
+struct PartialView {
+  SplitPlan plan;
+  const float *ws;
+  int N, M;
+};
+// Deterministic sum (contributor order) of y[bi][m][n .. n+3] (n % 4 == 0).
+__device__ inline float4 sk_sum4(const PartialView &v, int bi, int m, int n) {
+  const SplitPlan &p = v.plan;
+  const int tt = m / p.bn, mt = n >> 7;
+  const int t = (bi * p.token_tiles + tt) * p.m_tiles + mt;
+  const int cf = sk_cta_of((long long)t * p.kb_total, p), cl = sk_cta_of((long long)(t + 1) * p.kb_total - 1, p);
+  const size_t off = (size_t)(m - tt * p.bn) * 128 + (n & 127);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int k = 0; k <= cl - cf; ++k) {
+    const float4 x = __ldcg(reinterpret_cast<const float4 *>(v.ws + ((size_t)t * p.maxc + k) * p.bn * 128 + off));
+    acc.x += x.x;
+    acc.y += x.y;
+    acc.z += x.z;
+    acc.w += x.w;
+  }
+  return acc;
+}
+__device__ inline float sk_sum1(const PartialView &v, int bi, int m, int n) {
+  const SplitPlan &p = v.plan;
+  const int tt = m / p.bn, mt = n >> 7;
+  const int t = (bi * p.token_tiles + tt) * p.m_tiles + mt;
+  const int cf = sk_cta_of((long long)t * p.kb_total, p), cl = sk_cta_of((long long)(t + 1) * p.kb_total - 1, p);
+  const size_t off = (size_t)(m - tt * p.bn) * 128 + (n & 127);
+  float acc = 0.f;
+  for (int k = 0; k <= cl - cf; ++k) acc += __ldcg(v.ws + ((size_t)t * p.maxc + k) * p.bn * 128 + off);
+  return acc;
+}
+
 struct GemmArgs {
   CUtensorMap tmW[kMaxGemmBatch];  // weight [N][K] bf16, box 64(k) x 128(rows), SWIZZLE_128B
   CUtensorMap tmX[kMaxGemmBatch];  // activation [rows][K] bf16, box 64(k) x 16(rows), SWIZZLE_128B
-  float *out[kMaxGemmBatch];       // fp32 partials [splits][ldm][ldo]
-  int N, K, M, batch, bn;
-  int kb_total, kb_per_split, splits;
-  int ldo;                         // leading dim of out (>= N)
+  int N, K, M, batch;
   int x_row0;                      // first activation row (TMA row offset)
-  long long split_stride;          // elements between split slices
+  SplitPlan plan;
+  float *ws;                       // partial slots, gemm_ws_floats() floats
 };
 void gemm_plan(GemmArgs &a, int N, int K, int M, int batch);
 cudaError_t gemm_launch(const GemmArgs &a, cudaStream_t st);
 int gemm_pick_bn(int M);
+size_t gemm_ws_floats(const GemmArgs &a);
+void gemm_set_pdl(bool on);
+bool gemm_pdl();
+void gemm_set_ctas(int n);
 
 // ---------------------------------------------------------------- K1 tree attention
 struct AttnArgs {
@@ -46,36 +113,34 @@ struct AttnArgs {
 cudaError_t attention_launch(const AttnArgs &a, int head_dim, cudaStream_t st);
 int attention_row_blocks(int Nq, int G);
 
-// ---------------------------------------------------------------- elementwise / epilogues
-struct RowCtx {                // forward rows m = (seq - seq_base) * Nq + n
-  int M, Nq, seq_base;
-  const int32_t *len;          // Lc[seq]
-  const int32_t *depth;        // [Nq]
-};
-// out[m][n] = sum_s part[s][m][n]
-cudaError_t sum_splits_launch(const float *part, int splits, long long split_stride, int ldp, float *out, int M, int N,
-                              cudaStream_t st);
+// ---------------------------------------------------------------- GEMM consumers (epilogue.cu)
+// Every consumer waits on the producer GEMM with griddepcontrol.wait and lets
+// its own dependent launch early (programmatic dependent launch).
 cudaError_t embed_launch(const int32_t *tok, const bf16 *E, float *x, int M, int d, cudaStream_t st);
-// x[m] += sum_s part[s][m] (if part), then h = bf16(rmsnorm(x) * g)
-cudaError_t resid_norm_launch(const float *part, int splits, long long split_stride, int ldp, float *x,
-                              const bf16 *g, bf16 *h, int M, int d, float eps, cudaStream_t st);
-cudaError_t qkv_epilogue_launch(const float *part, int splits, long long split_stride, int ldp, RowCtx rc, int H,
-                                int Hkv, int hd, const float2 *rope, bf16 *q, bf16 *kcache, bf16 *vcache, int cap,
-                                cudaStream_t st);
-cudaError_t silu_mul_launch(const float *part, int splits, long long split_stride, int ldp, int F, bf16 *act, int M,
-                            cudaStream_t st);
-// logits rows: z = sum of partials; argmax (lowest index on ties) and the
-// single-pass typical stats (m, s, t) of y = z / T; optional fp32 copy.
-cudaError_t logits_finalize_launch(const float *part, int splits, long long split_stride, int ldp, int V,
-                                   const int32_t *row_index, int rows, float inv_temp, float *z_out, int ldz,
-                                   int32_t *argmax, float *stats, cudaStream_t st);
-cudaError_t topk_launch(const float *part, int splits, long long split_stride, int ldp, int V, int rows, int k,
-                        int32_t *idx, int ld_idx, cudaStream_t st);
-// rows = groups * rows_per_group; row (grp, rr) reads part + grp*group_stride + rr*ldp
-// and writes idx[rr * ld_idx + grp * k + kk]
-cudaError_t topk_grouped_launch(const float *part, int splits, long long split_stride, int ldp, int V, int groups,
-                                int rows_per_group, long long group_stride, int k, int32_t *idx, int ld_idx,
-                                cudaStream_t st);
+// x[m] += y[m] (if pv), then h = bf16(rmsnorm(x) * g)    (R5/R7 + R2/R8)
+cudaError_t resid_norm_launch(const PartialView *pv, float *x, const bf16 *g, bf16 *h, int M, int d, float eps,
+                              cudaStream_t st);
+// q/k/v = y; RoPE(q, k) at pos Lc + depth; q -> q[m][H][hd], k/v -> cache slot Lc + node   (R3)
+cudaError_t qkv_consumer_launch(const PartialView &pv, RowCtx rc, int H, int Hkv, int hd, const float2 *rope, bf16 *q,
+                                bf16 *kcache, bf16 *vcache, int cap, cudaStream_t st);
+// act[m][f] = bf16(SiLU(gate) * up), gate/up interleaved per 64 rows    (R6)
+cudaError_t silu_consumer_launch(const PartialView &pv, int F, bf16 *act, cudaStream_t st);
+// LM rows: z = y (fp32, optional copy), argmax (lowest index on ties) and the
+// single-pass typical statistics (m, s, t) of z * inv_temp    (R9)
+cudaError_t logits_consumer_launch(const PartialView &pv, float inv_temp, float *z_out, int32_t *argmax, float *stats,
+                                   cudaStream_t st);
+// plain fp32 rows (z or head logits) -> argmax/stats
+cudaError_t logits_finalize_launch(const float *z, int V, int rows, float inv_temp, int32_t *argmax, float *stats,
+                                   cudaStream_t st);
+// Medusa ResBlock: r[i][b][:] = bf16(h[b] + SiLU(y_i[b] + beta_i))    (R10)
+cudaError_t heads_r_consumer_launch(const PartialView &pv, int nmed, int nb, int d, const bf16 *head_in,
+                                    const bf16 *const *beta, bf16 *r_out, long long r_stride, cudaStream_t st);
+// top-k of the U-head logits y_i[b][:]: idx[b][i][k], (value desc, index asc)    (K3)
+cudaError_t topk_consumer_launch(const PartialView &pv, int nmed, int nb, int V, int k, int32_t *idx, cudaStream_t st);
+// stage API: top-k of plain fp32 rows
+cudaError_t topk_launch(const float *logits, int rows, int V, int k, int32_t *idx, cudaStream_t st);
+// stage API: out[m][n] = y[m][n]
+cudaError_t plain_consumer_launch(const PartialView &pv, float *out, cudaStream_t st);
 
 // ---------------------------------------------------------------- decode control (K3/K4/K5)
 struct TreeDev {
@@ -110,10 +175,25 @@ cudaError_t commit_launch(int b, int32_t *len, const int32_t *n_emit, int32_t *r
 cudaError_t advance_len_launch(int32_t *len, int seq, int n, cudaStream_t st);
 cudaError_t set_root_launch(int32_t *root, int seq, const int32_t *argmax_row, const bf16 *hf_row, int d,
                             bf16 *head_in_row, cudaStream_t st);
-cudaError_t heads_epilogue_grouped_launch(const float *part, int splits, long long split_stride, int ldp,
-                                          long long head_stride, int nmed, int b, int d, const bf16 *head_in,
-                                          const bf16 *const *beta, bf16 *r_out, long long r_stride, cudaStream_t st);
 cudaError_t generate_bf16_launch(void *dst, size_t numel, uint64_t seed, uint64_t stream_id, uint64_t start, int mode,
                                  cudaStream_t st);
+
+// ---------------------------------------------------------------- PDL launch helper
+// Launch with programmatic stream serialization when enabled (gemm_pdl()).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args &&...args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = gemm_pdl() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 }  // namespace sm

@@ -251,7 +251,8 @@ struct sm_model {
        *r_buf = nullptr;
   int32_t *argmax = nullptr;
   float2 *rope = nullptr;
-  size_t part_elems = 0;
+  float *ws = nullptr;      // stream-K fp32 partial slots (shared by consecutive GEMMs)
+  size_t ws_floats = 0;
   // GEMM prototypes (tensor maps prebuilt)
   std::vector<GemmArgs> g_qkv, g_o, g_gu, g_down;
   GemmArgs g_lm, g_R, g_U;
@@ -266,12 +267,6 @@ static GemmArgs gemm_proto(int N, int K, int batch) {
   a.K = K;
   a.batch = batch;
   return a;
-}
-// elements of the partial buffer a GEMM needs at `ld_rows` rows per split slice
-static size_t gemm_part_elems(const GemmArgs &proto, int M, int ld_rows) {
-  GemmArgs a = proto;
-  gemm_plan(a, proto.N, proto.K, M, proto.batch);
-  return (size_t)a.batch * a.splits * ld_rows * proto.N;
 }
 
 // ---------------------------------------------------------------- in-graph kernel timing
@@ -294,28 +289,34 @@ static void prof_end(cudaStream_t st, cudaEvent_t a, int kind, double bytes) {
   g_prof->push_back(ProfEvent{kind, a, b, bytes});
 }
 
-struct GemmRun {
-  int splits;
-  long long split_stride;
-  long long batch_stride;
-};
-static sm_status run_gemm(const GemmArgs &proto, int M, int ld_rows, int x_row0, float *out, cudaStream_t st,
-                          GemmRun *info, int &nl) {
-  GemmArgs a = proto;
-  gemm_plan(a, proto.N, proto.K, M, proto.batch);
-  a.ldo = proto.N;
+// Launch one stream-K GEMM over rows [x_row0, x_row0 + M) of the prototype's
+// activation map; its fp32 partials land in ws and are described by *pv.
+static sm_status run_gemm(GemmArgs a, int M, int x_row0, float *ws, size_t ws_floats, cudaStream_t st, int &nl,
+                          PartialView *pv) {
+  gemm_plan(a, a.N, a.K, M, a.batch);
   a.x_row0 = x_row0;
-  a.split_stride = (long long)ld_rows * proto.N;
-  const long long bstride = (long long)a.splits * a.split_stride;
-  for (int i = 0; i < a.batch; ++i) a.out[i] = out + i * bstride;
+  a.ws = ws;
+  if (gemm_ws_floats(a) > ws_floats) return fail(SM_ERR_INVALID_ARG, "GEMM partial workspace too small");
   cudaEvent_t ev = nullptr;
   prof_begin(st, &ev);
   CK(gemm_launch(a, st));
-  prof_end(st, ev, 0,
-           (double)a.batch * ((double)proto.N * proto.K * 2 + (double)M * proto.K * 2 + (double)M * proto.N * 4));
+  prof_end(st, ev, 0, (double)a.batch * ((double)a.N * a.K * 2 + (double)M * a.K * 2 + (double)M * a.N * 4));
   ++nl;
-  if (info) *info = GemmRun{a.splits, a.split_stride, bstride};
+  *pv = PartialView{a.plan, ws, a.N, M};
   return SM_OK;
+}
+// Largest partial workspace a prototype can need for M in [1, max_m].
+static size_t ws_need(const GemmArgs &proto, int max_m) {
+  size_t need = 0;
+  for (int M = 1; M <= max_m; M = (M < 16 ? 16 : M * 2)) {
+    GemmArgs a = proto;
+    gemm_plan(a, a.N, a.K, std::min(M, max_m), a.batch);
+    need = std::max(need, gemm_ws_floats(a));
+    if (M >= max_m) break;
+  }
+  GemmArgs a = proto;
+  gemm_plan(a, a.N, a.K, max_m, a.batch);
+  return std::max(need, gemm_ws_floats(a));
 }
 
 extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *w, const sm_dist *dist,
@@ -408,28 +409,27 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
     CKS(act_map(&a.tmX[0], xp, xrows, K));
     return SM_OK;
   };
-  size_t need = 0;
   for (int l = 0; l < m->L && s == SM_OK; ++l) {
     GemmArgs a;
     if ((s = mk(m->wqkv[l], m->qkv_n, d, m->h, R, a)) != SM_OK) break;
     m->g_qkv.push_back(a);
-    need = std::max(need, gemm_part_elems(a, R, R));
     if ((s = mk(m->wo[l], d, Hhd, m->attn, R, a)) != SM_OK) break;
     m->g_o.push_back(a);
-    need = std::max(need, gemm_part_elems(a, R, R));
     if ((s = mk(m->wgu[l], 2 * m->F, d, m->h, R, a)) != SM_OK) break;
     m->g_gu.push_back(a);
-    need = std::max(need, gemm_part_elems(a, R, R));
     if ((s = mk(m->wdown[l], d, m->F, m->act, R, a)) != SM_OK) break;
     m->g_down.push_back(a);
-    need = std::max(need, gemm_part_elems(a, R, R));
   }
   if (s == SM_OK) s = mk(m->lm_head, m->V, d, m->hf, R, m->g_lm);
   if (s != SM_OK) {
     sm_model_destroy(m);
     return s;
   }
-  need = std::max(need, gemm_part_elems(m->g_lm, R, R));
+  size_t need = 0;  // stream-K partial workspace: max over every GEMM the model runs
+  for (int l = 0; l < m->L; ++l)
+    need = std::max({need, ws_need(m->g_qkv[l], R), ws_need(m->g_o[l], R), ws_need(m->g_gu[l], R),
+                     ws_need(m->g_down[l], R)});
+  need = std::max(need, ws_need(m->g_lm, R));
   if (m->nmed > 0) {
     m->g_R = gemm_proto(d, d, m->nmed);
     m->g_U = gemm_proto(m->V, d, m->nmed);
@@ -443,11 +443,10 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
       sm_model_destroy(m);
       return s;
     }
-    need = std::max(need, gemm_part_elems(m->g_R, B, B));
-    need = std::max(need, gemm_part_elems(m->g_U, B, B));
+    need = std::max({need, ws_need(m->g_R, B), ws_need(m->g_U, B)});
   }
-  m->part_elems = need;
-  ALLOC(m->part, need, "gemm partials");
+  ALLOC(m->ws, need, "stream-K partials");
+  m->ws_floats = need;
 #undef ALLOC
   if ((s = sm_tree_create_chain(R, &m->chain)) != SM_OK || (s = tree_upload(m->chain)) != SM_OK) {
     sm_model_destroy(m);
@@ -465,6 +464,7 @@ extern "C" void sm_model_destroy(sm_model *m) {
   if (!m) return;
   cudaFree(m->x);
   cudaFree(m->part);
+  cudaFree(m->ws);
   cudaFree(m->z);
   cudaFree(m->stats);
   cudaFree(m->h);
@@ -640,7 +640,6 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
                                  const TreeDev &tree, cudaStream_t st, int &nl) {
   const int M = nseq * Nq;
   const int d = m->d;
-  GemmRun gr;
   CK(embed_launch(d_tok, m->embed, m->x, M, d, st));
   ++nl;
   int chunk, nsplit;
@@ -648,17 +647,17 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
   const long long layer_rows = (long long)2 * kv->b * m->Hkv * kv->cap;
   const long long half_rows = (long long)kv->b * m->Hkv * kv->cap;
   RowCtx rc{M, Nq, seq_base, kv->len, tree.depth};
-  const float *prev_part = nullptr;
-  GemmRun prev{0, 0, 0};
+  PartialView pv, pv_down{};
+  bool have_down = false;
   for (int l = 0; l < m->L; ++l) {
-    CK(resid_norm_launch(prev_part, prev.splits, prev.split_stride, d, m->x, m->attn_norm[l], m->h, M, d,
-                         m->cfg.rms_eps, st));
+    // x += down (previous layer, R7); h = bf16(rms(x) * g1)   (R2)
+    CK(resid_norm_launch(have_down ? &pv_down : nullptr, m->x, m->attn_norm[l], m->h, M, d, m->cfg.rms_eps, st));
     ++nl;
-    CKS(run_gemm(m->g_qkv[l], M, m->R, 0, m->part, st, &gr, nl));
     bf16 *kc = kv->base + (size_t)l * layer_rows * m->hd;
     bf16 *vc = kc + (size_t)half_rows * m->hd;
-    CK(qkv_epilogue_launch(m->part, gr.splits, gr.split_stride, m->qkv_n, rc, m->H, m->Hkv, m->hd, m->rope, m->q,
-                           kc, vc, kv->cap, st));
+    CKS(run_gemm(m->g_qkv[l], M, 0, m->ws, m->ws_floats, st, nl, &pv));
+    // RoPE, q -> m->q, k/v -> cache slots Lc + node (R3)
+    CK(qkv_consumer_launch(pv, rc, m->H, m->Hkv, m->hd, m->rope, m->q, kc, vc, kv->cap, st));
     ++nl;
     AttnArgs aa;
     std::memset(&aa, 0, sizeof(aa));
@@ -688,19 +687,18 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
     CK(attention_launch(aa, m->hd, st));
     prof_end(st, ev, 1, 0.0);
     nl += nsplit > 1 ? 2 : 1;
-    CKS(run_gemm(m->g_o[l], M, m->R, 0, m->part, st, &gr, nl));
-    CK(resid_norm_launch(m->part, gr.splits, gr.split_stride, d, m->x, m->mlp_norm[l], m->h, M, d, m->cfg.rms_eps,
-                         st));
+    CKS(run_gemm(m->g_o[l], M, 0, m->ws, m->ws_floats, st, nl, &pv));
+    // x += o (R5); h = bf16(rms(x) * g2)
+    CK(resid_norm_launch(&pv, m->x, m->mlp_norm[l], m->h, M, d, m->cfg.rms_eps, st));
     ++nl;
-    CKS(run_gemm(m->g_gu[l], M, m->R, 0, m->part, st, &gr, nl));
-    CK(silu_mul_launch(m->part, gr.splits, gr.split_stride, 2 * m->F, m->F, m->act, M, st));
+    CKS(run_gemm(m->g_gu[l], M, 0, m->ws, m->ws_floats, st, nl, &pv));
+    CK(silu_consumer_launch(pv, m->F, m->act, st));  // act = bf16(SiLU(g) * u) (R6)
     ++nl;
-    CKS(run_gemm(m->g_down[l], M, m->R, 0, m->part, st, &gr, nl));
-    prev_part = m->part;
-    prev = gr;
+    CKS(run_gemm(m->g_down[l], M, 0, m->ws, m->ws_floats, st, nl, &pv_down));
+    have_down = true;
   }
-  CK(resid_norm_launch(prev_part, prev.splits, prev.split_stride, d, m->x, m->final_norm, m->hf, M, d,
-                       m->cfg.rms_eps, st));
+  // x += down; hf = bf16(rms(x) * gf)   (R8)
+  CK(resid_norm_launch(have_down ? &pv_down : nullptr, m->x, m->final_norm, m->hf, M, d, m->cfg.rms_eps, st));
   ++nl;
   return SM_OK;
 }
@@ -709,16 +707,14 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
 static sm_status enqueue_heads(sm_model *m, sm_kv *kv, int row0, int nb, cudaStream_t st, int &nl) {
   if (m->nmed == 0 || kv->t->l == 0) return SM_OK;
   const int d = m->d, B = m->B;
-  GemmRun gr;
-  CKS(run_gemm(m->g_R, nb, B, row0, m->part, st, &gr, nl));
-  CK(heads_epilogue_grouped_launch(m->part, gr.splits, gr.split_stride, d, gr.batch_stride, m->nmed, nb, d,
-                                   m->head_in + (size_t)row0 * d, m->mb.data(), m->r_buf + (size_t)row0 * d,
-                                   (long long)B * d, st));
+  PartialView pv;
+  CKS(run_gemm(m->g_R, nb, row0, m->ws, m->ws_floats, st, nl, &pv));
+  CK(heads_r_consumer_launch(pv, m->nmed, nb, d, m->head_in + (size_t)row0 * d, m->mb.data(),
+                             m->r_buf + (size_t)row0 * d, (long long)B * d, st));
   ++nl;
-  CKS(run_gemm(m->g_U, nb, B, row0, m->part, st, &gr, nl));
+  CKS(run_gemm(m->g_U, nb, row0, m->ws, m->ws_floats, st, nl, &pv));
   const int K = kv->t->topk;
-  CK(topk_grouped_launch(m->part, gr.splits, gr.split_stride, m->V, m->V, m->nmed, nb, gr.batch_stride, K,
-                         kv->topk + (size_t)row0 * m->nmed * K, m->nmed * K, st));
+  CK(topk_consumer_launch(pv, m->nmed, nb, m->V, K, kv->topk + (size_t)row0 * m->nmed * K, st));
   ++nl;
   return SM_OK;
 }
@@ -744,10 +740,9 @@ extern "C" sm_status sm_prefill(sm_model *m, sm_kv *kv, int seq, const int32_t *
     last = P;
   }
   // last token: LM head row, pending root, heads' top-k (reading Q8)
-  GemmRun gr;
-  CKS(run_gemm(m->g_lm, 1, R, last - 1, m->part, st, &gr, nl));
-  CK(logits_finalize_launch(m->part, gr.splits, gr.split_stride, m->V, m->V, nullptr, 1, 1.0f, m->z, m->V,
-                            m->argmax, m->stats, st));
+  PartialView pv;
+  CKS(run_gemm(m->g_lm, 1, last - 1, m->ws, m->ws_floats, st, nl, &pv));
+  CK(logits_consumer_launch(pv, 1.0f, m->z, m->argmax, m->stats, st));
   CK(set_root_launch(kv->root, seq, m->argmax, m->hf + (size_t)(last - 1) * m->d, m->d,
                      m->head_in + (size_t)seq * m->d, st));
   CKS(enqueue_heads(m, kv, seq, 1, st, nl));
@@ -766,10 +761,9 @@ static sm_status enqueue_propose(sm_model *m, sm_kv *kv, int32_t *tree_tok, int3
 static sm_status enqueue_verify(sm_model *m, sm_kv *kv, const int32_t *tree_tok, cudaStream_t st, int &nl) {
   const int M = kv->b * kv->N;
   CKS(enqueue_forward(m, kv, tree_tok, kv->b, 0, kv->N, kv->t->dev(), st, nl));
-  GemmRun gr;
-  CKS(run_gemm(m->g_lm, M, m->R, 0, m->part, st, &gr, nl));
-  CK(logits_finalize_launch(m->part, gr.splits, gr.split_stride, m->V, m->V, nullptr, M, 1.0f, m->z, m->V, m->argmax,
-                            m->stats, st));
+  PartialView pv;
+  CKS(run_gemm(m->g_lm, M, 0, m->ws, m->ws_floats, st, nl, &pv));
+  CK(logits_consumer_launch(pv, 1.0f, m->z, m->argmax, m->stats, st));
   ++nl;
   return SM_OK;
 }
@@ -781,7 +775,7 @@ static sm_status enqueue_accept(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg
   if (cfg->mode == SM_ACCEPT_TYPICAL) {
     inv_temp = 1.0f / cfg->temperature;
     // typical statistics at temperature T on the stored logits (one fp32 pass)
-    CK(logits_finalize_launch(m->z, 1, 0, m->V, m->V, nullptr, M, inv_temp, nullptr, m->V, m->argmax, m->stats, st));
+    CK(logits_finalize_launch(m->z, m->V, M, inv_temp, m->argmax, m->stats, st));
     ++nl;
   }
   AcceptArgs a;
@@ -1016,20 +1010,33 @@ extern "C" sm_status sm_gemm_bf16(const void *d_x, const void *d_w, float *d_out
   GemmArgs a = gemm_proto(N, K, 1);
   CKS(weight_map(&a.tmW[0], d_w, N, K));
   CKS(act_map(&a.tmX[0], d_x, M, K));
+  const size_t need = ws_need(a, M);
   void *scr = nullptr;
-  CKS(scratch(gemm_part_elems(a, M, M) * 4, &scr));
+  CKS(scratch(need * 4, &scr));
   int nl = 0;
-  GemmRun gr;
-  cudaStream_t st = (cudaStream_t)stream;
-  CKS(run_gemm(a, M, M, 0, (float *)scr, st, &gr, nl));
-  CK(sum_splits_launch((float *)scr, gr.splits, gr.split_stride, N, d_out, M, N, st));
+  PartialView pv;
+  CKS(run_gemm(a, M, 0, (float *)scr, need, (cudaStream_t)stream, nl, &pv));
+  CK(plain_consumer_launch(pv, d_out, (cudaStream_t)stream));
   return SM_OK;
 }
 
 extern "C" sm_status sm_topk_f32(const float *d_logits, int rows, int V, int k, int32_t *d_idx, void *stream) {
-  if (!d_logits || !d_idx || rows < 1 || V < k || k < 1 || V * 4 > 200 * 1024)
-    return fail(SM_ERR_INVALID_ARG, "sm_topk_f32: bad arguments");
-  CK(topk_launch(d_logits, 1, 0, V, V, rows, k, d_idx, k, (cudaStream_t)stream));
+  if (!d_logits || !d_idx || rows < 1 || V < k || k < 1 || V * 4 > 200 * 1024 || V % 4)
+    return fail(SM_ERR_INVALID_ARG, "sm_topk_f32: bad arguments (V % 4 == 0)");
+  CK(topk_launch(d_logits, rows, V, k, d_idx, (cudaStream_t)stream));
+  return SM_OK;
+}
+
+extern "C" sm_status sm_set_option(const char *name, int value) {
+  if (!name) return fail(SM_ERR_INVALID_ARG, "sm_set_option: null name");
+  const std::string n(name);
+  if (n == "pdl") {
+    gemm_set_pdl(value != 0);
+  } else if (n == "gemm_ctas") {
+    gemm_set_ctas(value);
+  } else {
+    return fail(SM_ERR_INVALID_ARG, "sm_set_option: unknown option " + n);
+  }
   return SM_OK;
 }
 
