@@ -14,9 +14,14 @@
 //  * Q K^T and P V on tensor cores (mma.sync m16n8k16 bf16, ldmatrix from the
 //    swizzled tiles), fp32 online softmax with quad warp-shuffle max/sum;
 //  * the ancestor bitmask (N x 4 u64) masks only tiles that reach past Lc;
-//  * split-KV across CTAs for parallelism at b*Hkv < 148 with a combine kernel.
-// The key range per split is fixed on the host from the capacity, so the launch
-// is CUDA-graph safe while Lc lives on the device.
+//  * split-KV for parallelism at b*Hkv < 148: the nsplit CTAs of one (row block,
+//    seq, kv head) form a thread-block cluster; each stages its (m, l, O) rows in
+//    shared memory and the cluster combines them through DSMEM (no combine
+//    kernel, no global partials).  Key ranges come from the device-side Lc, so
+//    the launch is CUDA-graph safe;
+//  * programmatic dependent launch: the committed prefix [0, Lc) does not change
+//    during the forward, so its first K/V tiles are requested before
+//    griddepcontrol.wait; Q and the tree tiles only after it.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -48,20 +53,19 @@ __global__ void __launch_bounds__(128) tree_attn_kernel(const __grid_constant__ 
   uint64_t *full = s_anc + 64 * kAncWords;
 
   pdl_trigger();
-  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int split = blockIdx.x, rblk = blockIdx.y;
+  const int split = blockIdx.x, rblk = blockIdx.y;  // split = rank inside the (nsplit, 1, 1) cluster
   const int sl = blockIdx.z / a.Hkv, h = blockIdx.z % a.Hkv;
   const int seq = a.seq_base + sl;
-  const int Lc = a.len[seq];
+  const int Lc = a.len[seq];  // only the step's last kernels change Lc: safe before the wait
   const int T = Lc + a.Nq;
-  const int key0 = split * a.chunk;
-  const int key1 = min(T, key0 + a.chunk);
-  if (key0 >= key1) return;  // whole CTA: split beyond this sequence's keys
+  const int chunk = ((T + a.nsplit - 1) / a.nsplit + 63) / 64 * 64;
+  const int key0 = min(T, split * chunk);
+  const int key1 = min(T, key0 + chunk);
   const int ntiles = (key1 - key0 + 63) / 64;
   const int R = a.Nq * a.G;
 
-  // tree mask rows of this CTA (node of each query row)
+  // tree mask rows of this CTA (node of each query row); constant tables
   for (int i = threadIdx.x; i < 64 * kAncWords; i += blockDim.x) {
     const int r = rblk * 64 + i / kAncWords;
     s_anc[i] = (r < R) ? a.anc[(r / a.G) * kAncWords + (i % kAncWords)] : 0ull;
@@ -93,8 +97,13 @@ __global__ void __launch_bounds__(128) tree_attn_kernel(const __grid_constant__ 
       tma_load_2d(vb, &a.tmV, &full[s], 0, (int)(vbase_row + p));
     }
   };
+  const int first = min(C::kStages, ntiles);
+  int pre = 0;  // prefix tiles (entirely below Lc) requested before the dependency wait
   if (threadIdx.x == 0)
-    for (int i = 0; i < min(C::kStages, ntiles); ++i) issue(i);
+    while (pre < first && key0 + (pre + 1) * 64 <= Lc) issue(pre++);
+  pdl_wait();  // q and the tree K/V rows come from the preceding kernel
+  if (threadIdx.x == 0)
+    for (int i = pre; i < first; ++i) issue(i);
 
   // ---- per-thread rows: ra = r0 + g, rb = r0 + g + 8 (mma C-fragment layout)
   const int r0 = rblk * 64 + warp * 16;
@@ -227,67 +236,80 @@ __global__ void __launch_bounds__(128) tree_attn_kernel(const __grid_constant__ 
     if (threadIdx.x == 0 && i + C::kStages < ntiles) issue(i + C::kStages);
   }
 
-  if (!warp_active) return;
   l_a += __shfl_xor_sync(0xffffffffu, l_a, 1);
   l_a += __shfl_xor_sync(0xffffffffu, l_a, 2);
   l_b += __shfl_xor_sync(0xffffffffu, l_b, 1);
   l_b += __shfl_xor_sync(0xffffffffu, l_b, 2);
 
-#pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    const int r = half ? rb : ra;
-    if (r >= R) continue;
+  auto out_row = [&](int r) -> bf16 * {  // global output row of query row r
     const int n = r / a.G, gg = r % a.G;
     const long long m = (long long)sl * a.Nq + n;
-    const long long orow = m * a.H + (long long)h * a.G + gg;
-    const float l = half ? l_b : l_a;
-    const float mm = half ? m_b : m_a;
-    if (a.nsplit == 1) {
-      const float inv = 1.f / l;
-      bf16 *dst = a.out + orow * HD;
+    return a.out + (m * a.H + (long long)h * a.G + gg) * HD;
+  };
+  if (a.nsplit == 1) {
+    if (!warp_active) return;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int r = half ? rb : ra;
+      if (r >= R) continue;
+      const float inv = 1.f / (half ? l_b : l_a);
+      bf16 *dst = out_row(r);
 #pragma unroll
       for (int j = 0; j < HD / 8; ++j) {
         const float v0 = o[j][2 * half] * inv, v1 = o[j][2 * half + 1] * inv;
         *reinterpret_cast<uint32_t *>(dst + 8 * j + 2 * t) = pack_bf16(v0, v1);
       }
-    } else {
-      const long long M = (long long)a.nseq * a.Nq;
-      float *dst = a.part_o + ((long long)split * M * a.H + orow) * HD;
+    }
+    return;
+  }
+  // ---- cluster combine: stage (m, l, O) of the 64 local rows in shared memory
+  // (the K/V ring is idle: every issued tile has been consumed)
+  float *so = reinterpret_cast<float *>(smem);  // [64][HD]
+  float *sml = so + 64 * HD;                    // [64][2]
 #pragma unroll
-      for (int j = 0; j < HD / 8; ++j)
-        *reinterpret_cast<float2 *>(dst + 8 * j + 2 * t) = make_float2(o[j][2 * half], o[j][2 * half + 1]);
-      if (t == 0) {
-        float *ml = a.part_ml + ((long long)split * M * a.H + orow) * 2;
-        ml[0] = mm;
-        ml[1] = l;
-      }
+  for (int half = 0; half < 2; ++half) {
+    const int lr = half ? lb : la;
+    const bool live = warp_active && (half ? rb : ra) < R;
+#pragma unroll
+    for (int j = 0; j < HD / 8; ++j)
+      *reinterpret_cast<float2 *>(so + lr * HD + 8 * j + 2 * t) =
+          live ? make_float2(o[j][2 * half], o[j][2 * half + 1]) : make_float2(0.f, 0.f);
+    if (t == 0) {
+      sml[2 * lr] = live ? (half ? m_b : m_a) : -INFINITY;
+      sml[2 * lr + 1] = live ? (half ? l_b : l_a) : 0.f;
     }
   }
-}
-
-// one block per output row (m, q head); HD threads
-__global__ void attn_combine_kernel(const __grid_constant__ AttnArgs a, int HD) {
-  pdl_trigger();
-  pdl_wait();
-  const long long row = blockIdx.x;
-  const int m = (int)(row / a.H);
-  const int sl = m / a.Nq;
-  const int T = a.len[a.seq_base + sl] + a.Nq;
-  const int ns = min(a.nsplit, (T + a.chunk - 1) / a.chunk);
-  const long long M = (long long)a.nseq * a.Nq;
-  float mx = -INFINITY;
-  for (int s = 0; s < ns; ++s) mx = fmaxf(mx, a.part_ml[((long long)s * M * a.H + row) * 2]);
-  const float base = mx * a.scale_log2;
-  float L = 0.f, acc = 0.f;
-  const int d = threadIdx.x;
-  for (int s = 0; s < ns; ++s) {
-    const float *ml = a.part_ml + ((long long)s * M * a.H + row) * 2;
-    const float w = exp2f(ml[0] * a.scale_log2 - base);
-    if (w == 0.f) continue;
-    L += w * ml[1];
-    acc += w * a.part_o[((long long)s * M * a.H + row) * HD + d];
+  cluster_sync_all();
+  // rank `split` combines local rows [split * 64/nsplit, (split+1) * 64/nsplit)
+  const int rows_per = 64 / a.nsplit;
+  const uint32_t so_u = smem_u32(so), sml_u = smem_u32(sml);
+  for (int e = threadIdx.x; e < rows_per * HD; e += blockDim.x) {
+    const int lr = split * rows_per + e / HD, dcol = e % HD;
+    const int r = rblk * 64 + lr;
+    if (r >= R) continue;
+    // every rank's (m, l, o) is loaded before any is used: one DSMEM round trip
+    float mq[8], lq[8], oq[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const bool ok = q < a.nsplit;
+      mq[q] = ok ? ld_dsmem_f32(mapa_u32(sml_u + 8 * lr, q)) : -INFINITY;
+      lq[q] = ok ? ld_dsmem_f32(mapa_u32(sml_u + 8 * lr + 4, q)) : 0.f;
+      oq[q] = ok ? ld_dsmem_f32(mapa_u32(so_u + 4 * (lr * HD + dcol), q)) : 0.f;
+    }
+    float mx = -INFINITY;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) mx = fmaxf(mx, mq[q]);
+    const float base = mx * sl2;
+    float L = 0.f, acc = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {  // fixed rank order -> deterministic
+      const float w = mq[q] == -INFINITY ? 0.f : exp2f(mq[q] * sl2 - base);
+      L += w * lq[q];
+      acc += w * oq[q];
+    }
+    out_row(r)[dcol] = f2bf(acc / L);
   }
-  a.out[row * HD + d] = f2bf(acc / L);
+  cluster_sync_all();  // keep every CTA's shared memory alive until all remote reads are done
 }
 
 int attention_row_blocks(int Nq, int G) { return (Nq * G + 63) / 64; }
@@ -301,10 +323,28 @@ static cudaError_t launch_hd(const AttnArgs &a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid(a.nsplit, attention_row_blocks(a.Nq, a.G), a.nseq * a.Hkv);
-  cudaError_t e = launch_pdl(tree_attn_kernel<HD>, grid, dim3(128), C::kSmem, st, a);
-  if (e != cudaSuccess || a.nsplit == 1) return e;
-  return launch_pdl(attn_combine_kernel, dim3((unsigned)((long long)a.nseq * a.Nq * a.H)), dim3(HD), 0, st, a, HD);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(a.nsplit, attention_row_blocks(a.Nq, a.G), a.nseq * a.Hkv);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = gemm_pdl() ? 1 : 0;
+  attrs[1].id = cudaLaunchAttributeClusterDimension;
+  attrs[1].val.clusterDim.x = a.nsplit;
+  attrs[1].val.clusterDim.y = 1;
+  attrs[1].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = a.nsplit > 1 ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, tree_attn_kernel<HD>, a);
+}
+
+// nsplit = cluster size in {1, 2, 4, 8}: enough CTAs to cover ~2 waves of SMs
+int attention_nsplit(int units) {
+  int ns = 1;
+  while (ns < 8 && units * ns < 2 * kNumSMs) ns *= 2;
+  return ns;
 }
 
 cudaError_t attention_launch(const AttnArgs &a, int head_dim, cudaStream_t st) {

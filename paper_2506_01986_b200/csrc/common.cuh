@@ -36,6 +36,21 @@ SM_DEV float warp_max(float v) {
   return v;
 }
 
+// ------------------------------------------------------------------ clusters / DSMEM
+SM_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+SM_DEV uint32_t mapa_u32(uint32_t smem_addr, int rank) {  // this CTA's smem address -> rank's copy
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+  return r;
+}
+SM_DEV float ld_dsmem_f32(uint32_t cluster_addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(cluster_addr) : "memory");
+  return v;
+}
+
 // ------------------------------------------------------------------ mbarrier
 SM_DEV void mbar_init(uint64_t *bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -77,6 +92,11 @@ SM_DEV void tma_load_2d_hint(void *smem_dst, const CUtensorMap *m, uint64_t *bar
       "%4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
       "l"((uint64_t)m), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
+}
+// TMA prefetch of a 2D box into L2 only (no shared memory, no completion)
+SM_DEV void tma_prefetch_l2_2d(const CUtensorMap *m, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"((uint64_t)m), "r"(c0), "r"(c1)
+               : "memory");
 }
 SM_DEV uint64_t policy_evict_first() {
   uint64_t p;

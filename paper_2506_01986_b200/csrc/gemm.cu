@@ -108,23 +108,41 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
     if (lane == 0) {
       // ---------------- TMA producer
       const uint64_t pol_w = policy_evict_first();
+      const bool wonly = a.dbg_mode == 1;
+      const uint32_t stage_bytes = wonly ? (uint32_t)C::kA : (uint32_t)C::kStage;
+      auto issue_x = [&](int s, int bi, int tt, int kc) {  // activation rows [tt*BN, tt*BN + BN)
+        if (wonly) return;
+        if constexpr (BN >= 64) {
+#pragma unroll
+          for (int r = 0; r < BN / 64; ++r)
+            tma_load_2d(sB + s * C::kB + r * 8192, &a.tmX64[bi], &full[s], kc, a.x_row0 + tt * BN + r * 64);
+        } else {
+#pragma unroll
+          for (int r = 0; r < BN / 16; ++r)
+            tma_load_2d(sB + s * C::kB + r * 2048, &a.tmX[bi], &full[s], kc, a.x_row0 + tt * BN + r * 16);
+        }
+      };
       const int pre = (u1 - u0) < (long long)C::kStages ? (int)(u1 - u0) : C::kStages;
       for (int i = 0; i < pre; ++i) {  // weights first: independent of the previous kernel
         const long long u = u0 + i;
         int bi, tt, mt;
         sk_decode(sk_tile(u, pl), pl, bi, tt, mt);
-        mbar_arrive_expect_tx(&full[i], C::kStage);
+        mbar_arrive_expect_tx(&full[i], stage_bytes);
         tma_load_2d_hint(sA + i * C::kA, &a.tmW[bi], &full[i], sk_kb(u, pl) * 64, mt * 128, pol_w);
+      }
+      // optionally pull the following weight tiles into L2 across the kernel boundary
+      for (int i = pre; i < pre + a.l2_prefetch && u0 + i < u1; ++i) {
+        const long long u = u0 + i;
+        int bi, tt, mt;
+        sk_decode(sk_tile(u, pl), pl, bi, tt, mt);
+        tma_prefetch_l2_2d(&a.tmW[bi], sk_kb(u, pl) * 64, mt * 128);
       }
       pdl_wait();  // activations only after the producer kernel completed
       for (int i = 0; i < pre; ++i) {
         const long long u = u0 + i;
         int bi, tt, mt;
         sk_decode(sk_tile(u, pl), pl, bi, tt, mt);
-#pragma unroll
-        for (int r = 0; r < BN / 16; ++r)
-          tma_load_2d(sB + i * C::kB + r * 2048, &a.tmX[bi], &full[i], sk_kb(u, pl) * 64,
-                      a.x_row0 + tt * BN + r * 16);
+        issue_x(i, bi, tt, sk_kb(u, pl) * 64);
       }
       for (long long u = u0 + pre; u < u1; ++u) {
         const int i = (int)(u - u0);
@@ -133,11 +151,9 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
         int bi, tt, mt;
         sk_decode(sk_tile(u, pl), pl, bi, tt, mt);
         const int kc = sk_kb(u, pl) * 64;
-        mbar_arrive_expect_tx(&full[s], C::kStage);
+        mbar_arrive_expect_tx(&full[s], stage_bytes);
         tma_load_2d_hint(sA + s * C::kA, &a.tmW[bi], &full[s], kc, mt * 128, pol_w);
-#pragma unroll
-        for (int r = 0; r < BN / 16; ++r)
-          tma_load_2d(sB + s * C::kB + r * 2048, &a.tmX[bi], &full[s], kc, a.x_row0 + tt * BN + r * 16);
+        issue_x(s, bi, tt, kc);
       }
     }
   } else if (warp == 1) {
@@ -156,12 +172,19 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
         const uint64_t ad = umma_desc_sw128(smem_u32(sA + s * C::kA));
         const uint64_t bd = umma_desc_sw128(smem_u32(sB + s * C::kB));
         const uint32_t td = tmem + buf * BN;
+        if (a.dbg_mode == 1) {  // weights-only streaming experiment: no MMA
+          mbar_arrive(&empty[s]);
+        } else {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) umma_bf16(td, ad + 2 * k, bd + 2 * k, idesc, (!seg_start || k > 0) ? 1u : 0u);
-        umma_commit(&empty[s]);
+          for (int k = 0; k < 4; ++k) umma_bf16(td, ad + 2 * k, bd + 2 * k, idesc, (!seg_start || k > 0) ? 1u : 0u);
+          umma_commit(&empty[s]);
+        }
         seg_start = false;
         if ((u + 1) % pl.kb_total == 0 || u + 1 == u1) {
-          umma_commit(&tfull[buf]);
+          if (a.dbg_mode == 1)
+            mbar_arrive(&tfull[buf]);
+          else
+            umma_commit(&tfull[buf]);
           ++seg;
           seg_start = true;
         }
@@ -200,9 +223,13 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
 
 static bool g_pdl = true;
 static int g_ctas = 0;
+static int g_l2pf = 0;
+static int g_dbg_mode = 0;
+void gemm_set_debug_mode(int m) { g_dbg_mode = m; }
 void gemm_set_pdl(bool on) { g_pdl = on; }
 bool gemm_pdl() { return g_pdl; }
 void gemm_set_ctas(int n) { g_ctas = n; }
+void gemm_set_l2_prefetch(int kblocks) { g_l2pf = kblocks < 0 ? 0 : kblocks; }
 
 template <int BN>
 static cudaError_t launch_bn(const GemmArgs &a, cudaStream_t st) {
@@ -256,7 +283,10 @@ void gemm_plan(GemmArgs &a, int N, int K, int M, int batch) {
 
 size_t gemm_ws_floats(const GemmArgs &a) { return (size_t)a.plan.tiles * a.plan.maxc * a.plan.bn * 128; }
 
-cudaError_t gemm_launch(const GemmArgs &a, cudaStream_t st) {
+cudaError_t gemm_launch(const GemmArgs &a0, cudaStream_t st) {
+  GemmArgs a = a0;
+  a.l2_prefetch = g_pdl ? g_l2pf : 0;
+  a.dbg_mode = g_dbg_mode;
   switch (a.plan.bn) {
     case 16: return launch_bn<16>(a, st);
     case 32: return launch_bn<32>(a, st);

@@ -52,19 +52,31 @@ struct PartialView {
   int N, M;
 };
 // Deterministic sum (contributor order) of y[bi][m][n .. n+3] (n % 4 == 0).
+// Loads of up to 8 contributors are issued before any add (one memory round
+// trip instead of one per contributor).
 __device__ inline float4 sk_sum4(const PartialView &v, int bi, int m, int n) {
   const SplitPlan &p = v.plan;
   const int tt = m / p.bn, mt = n >> 7;
   const int t = (bi * p.token_tiles + tt) * p.m_tiles + mt;
   const int cf = sk_cta_of((long long)t * p.kb_total, p), cl = sk_cta_of((long long)(t + 1) * p.kb_total - 1, p);
-  const size_t off = (size_t)(m - tt * p.bn) * 128 + (n & 127);
+  const int nc = cl - cf + 1;
+  const float4 *base =
+      reinterpret_cast<const float4 *>(v.ws + (size_t)t * p.maxc * p.bn * 128 + (size_t)(m - tt * p.bn) * 128 + (n & 127));
+  const size_t stride = (size_t)p.bn * 128 / 4;  // float4 between contributors
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int k = 0; k <= cl - cf; ++k) {
-    const float4 x = __ldcg(reinterpret_cast<const float4 *>(v.ws + ((size_t)t * p.maxc + k) * p.bn * 128 + off));
-    acc.x += x.x;
-    acc.y += x.y;
-    acc.z += x.z;
-    acc.w += x.w;
+  for (int k0 = 0; k0 < nc; k0 += 8) {
+    float4 x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = (k0 + k < nc) ? __ldcg(base + (k0 + k) * stride) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k0 + k < nc) {
+        acc.x += x[k].x;
+        acc.y += x[k].y;
+        acc.z += x[k].z;
+        acc.w += x[k].w;
+      }
+    }
   }
   return acc;
 }
@@ -73,17 +85,29 @@ __device__ inline float sk_sum1(const PartialView &v, int bi, int m, int n) {
   const int tt = m / p.bn, mt = n >> 7;
   const int t = (bi * p.token_tiles + tt) * p.m_tiles + mt;
   const int cf = sk_cta_of((long long)t * p.kb_total, p), cl = sk_cta_of((long long)(t + 1) * p.kb_total - 1, p);
-  const size_t off = (size_t)(m - tt * p.bn) * 128 + (n & 127);
+  const int nc = cl - cf + 1;
+  const float *base = v.ws + (size_t)t * p.maxc * p.bn * 128 + (size_t)(m - tt * p.bn) * 128 + (n & 127);
+  const size_t stride = (size_t)p.bn * 128;
   float acc = 0.f;
-  for (int k = 0; k <= cl - cf; ++k) acc += __ldcg(v.ws + ((size_t)t * p.maxc + k) * p.bn * 128 + off);
+  for (int k0 = 0; k0 < nc; k0 += 8) {
+    float x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = (k0 + k < nc) ? __ldcg(base + (k0 + k) * stride) : 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (k0 + k < nc) acc += x[k];
+  }
   return acc;
 }
 
 struct GemmArgs {
   CUtensorMap tmW[kMaxGemmBatch];  // weight [N][K] bf16, box 64(k) x 128(rows), SWIZZLE_128B
   CUtensorMap tmX[kMaxGemmBatch];  // activation [rows][K] bf16, box 64(k) x 16(rows), SWIZZLE_128B
+  CUtensorMap tmX64[kMaxGemmBatch];  // same activation, box 64(k) x 64(rows): one TMA per 64 token rows
   int N, K, M, batch;
   int x_row0;                      // first activation row (TMA row offset)
+  int l2_prefetch;                 // weight k-blocks per CTA prefetched into L2 before the PDL wait
+  int dbg_mode;                    // experiments: 1 = stream weights only (no X, no MMA)
   SplitPlan plan;
   float *ws;                       // partial slots, gemm_ws_floats() floats
 };
@@ -94,24 +118,26 @@ size_t gemm_ws_floats(const GemmArgs &a);
 void gemm_set_pdl(bool on);
 bool gemm_pdl();
 void gemm_set_ctas(int n);
+void gemm_set_l2_prefetch(int kblocks);
+void gemm_set_debug_mode(int m);
 
 // ---------------------------------------------------------------- K1 tree attention
 struct AttnArgs {
   CUtensorMap tmK, tmV;       // 2D views [rows][hd] of the K and V caches, box 64 rows x min(hd,64)
   const bf16 *q;              // [rows M][H][hd]
   bf16 *out;                  // [M][H][hd]
-  float *part_o;              // [nsplit][M][H][hd]   (nsplit > 1)
-  float *part_ml;             // [nsplit][M][H][2]
   const int32_t *len;         // Lc by absolute sequence index
   const uint64_t *anc;        // [Nq][kAncWords]
   long long k_row0, v_row0;   // tmap row of (seq 0, head 0, slot 0) for K and V of this layer
   long long seq_rows;         // rows per sequence block = Hkv * cap
   int cap;                    // slots per (seq, head)
-  int Nq, H, Hkv, G, nseq, seq_base, chunk, nsplit;
+  int Nq, H, Hkv, G, nseq, seq_base;
+  int nsplit;                 // key splits = cluster size (1, 2, 4, 8), combined through DSMEM
   float scale_log2;           // log2(e) / sqrt(hd)
 };
 cudaError_t attention_launch(const AttnArgs &a, int head_dim, cudaStream_t st);
 int attention_row_blocks(int Nq, int G);
+int attention_nsplit(int units);  // units = row blocks * sequences * kv heads
 
 // ---------------------------------------------------------------- GEMM consumers (epilogue.cu)
 // Every consumer waits on the producer GEMM with griddepcontrol.wait and lets

@@ -69,8 +69,10 @@ static sm_status weight_map(CUtensorMap *m, const void *w, int N, int K) {
   if (K % 8) return fail(SM_ERR_INVALID_ARG, "GEMM K must be a multiple of 8");
   return make_tmap(m, w, (uint64_t)N, (uint64_t)K, 128, 64, true);
 }
-static sm_status act_map(CUtensorMap *m, const void *x, int rows, int K) {
-  return make_tmap(m, x, (uint64_t)rows, (uint64_t)K, 16, 64, true);
+// activation maps of GEMM batch entry i: 16-row and 64-row boxes (BN < 64 / BN >= 64)
+static sm_status act_map(GemmArgs &a, int i, const void *x, int rows, int K) {
+  CKS(make_tmap(&a.tmX[i], x, (uint64_t)rows, (uint64_t)K, 16, 64, true));
+  return make_tmap(&a.tmX64[i], x, (uint64_t)rows, (uint64_t)K, 64, 64, true);
 }
 static sm_status kv_map(CUtensorMap *m, const void *base, uint64_t rows, int hd) {
   const bool sw = hd >= 64;
@@ -289,6 +291,7 @@ static void prof_end(cudaStream_t st, cudaEvent_t a, int kind, double bytes) {
   g_prof->push_back(ProfEvent{kind, a, b, bytes});
 }
 
+static int g_ablate_gemm = 0;  // set while enqueueing ablated per-layer GEMMs
 // Launch one stream-K GEMM over rows [x_row0, x_row0 + M) of the prototype's
 // activation map; its fp32 partials land in ws and are described by *pv.
 static sm_status run_gemm(GemmArgs a, int M, int x_row0, float *ws, size_t ws_floats, cudaStream_t st, int &nl,
@@ -299,7 +302,7 @@ static sm_status run_gemm(GemmArgs a, int M, int x_row0, float *ws, size_t ws_fl
   if (gemm_ws_floats(a) > ws_floats) return fail(SM_ERR_INVALID_ARG, "GEMM partial workspace too small");
   cudaEvent_t ev = nullptr;
   prof_begin(st, &ev);
-  CK(gemm_launch(a, st));
+  if (g_ablate_gemm == 0) CK(gemm_launch(a, st));
   prof_end(st, ev, 0, (double)a.batch * ((double)a.N * a.K * 2 + (double)M * a.K * 2 + (double)M * a.N * 4));
   ++nl;
   *pv = PartialView{a.plan, ws, a.N, M};
@@ -406,7 +409,7 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
   auto mk = [&](const void *wp, int N, int K, const void *xp, int xrows, GemmArgs &a) -> sm_status {
     a = gemm_proto(N, K, 1);
     CKS(weight_map(&a.tmW[0], wp, N, K));
-    CKS(act_map(&a.tmX[0], xp, xrows, K));
+    CKS(act_map(a, 0, xp, xrows, K));
     return SM_OK;
   };
   for (int l = 0; l < m->L && s == SM_OK; ++l) {
@@ -435,9 +438,9 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
     m->g_U = gemm_proto(m->V, d, m->nmed);
     for (int i = 0; i < m->nmed && s == SM_OK; ++i) {
       if ((s = weight_map(&m->g_R.tmW[i], m->mR[i], d, d)) != SM_OK) break;
-      if ((s = act_map(&m->g_R.tmX[i], m->head_in, B, d)) != SM_OK) break;
+      if ((s = act_map(m->g_R, i, m->head_in, B, d)) != SM_OK) break;
       if ((s = weight_map(&m->g_U.tmW[i], m->mU[i], m->V, d)) != SM_OK) break;
-      s = act_map(&m->g_U.tmX[i], m->r_buf + (size_t)i * B * d, B, d);
+      s = act_map(m->g_U, i, m->r_buf + (size_t)i * B * d, B, d);
     }
     if (s != SM_OK) {
       sm_model_destroy(m);
@@ -508,8 +511,7 @@ struct sm_kv {
   size_t bytes;
   int32_t *len = nullptr, *root = nullptr, *topk = nullptr, *acc_row = nullptr, *root_next = nullptr,
           *emitted = nullptr, *tree_tok = nullptr;
-  float *att_o = nullptr, *att_ml = nullptr;
-  int att_nsplit_max = 16;
+  int att_nsplit_max = 32;
   CUtensorMap tmKV;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   int step_launches = 0;
@@ -560,9 +562,7 @@ extern "C" sm_status sm_kv_bind(sm_model *m, const sm_tree *tree, int batch, int
       (s = dalloc(&kv->acc_row, batch, "acc_row")) != SM_OK ||
       (s = dalloc(&kv->root_next, batch, "root_next")) != SM_OK ||
       (s = dalloc(&kv->emitted, batch, "emitted")) != SM_OK ||
-      (s = dalloc(&kv->tree_tok, (size_t)batch * kv->N, "tree_tok")) != SM_OK ||
-      (s = dalloc(&kv->att_o, (size_t)kv->att_nsplit_max * m->R * m->H * m->hd, "attn partials")) != SM_OK ||
-      (s = dalloc(&kv->att_ml, (size_t)kv->att_nsplit_max * m->R * m->H * 2, "attn partials")) != SM_OK) {
+      (s = dalloc(&kv->tree_tok, (size_t)batch * kv->N, "tree_tok")) != SM_OK) {
     sm_kv_destroy(kv);
     return s;
   }
@@ -600,8 +600,6 @@ extern "C" void sm_kv_destroy(sm_kv *kv) {
   cudaFree(kv->root_next);
   cudaFree(kv->emitted);
   cudaFree(kv->tree_tok);
-  cudaFree(kv->att_o);
-  cudaFree(kv->att_ml);
   if (kv->t) sm_tree_destroy(kv->t);
   delete kv;
 }
@@ -625,15 +623,15 @@ extern "C" sm_status sm_state_device(const sm_kv *kv, int32_t **d_root, int32_t 
 }
 
 // ---------------------------------------------------------------- forward (a2 + a3)
-static void attn_plan(const sm_model *m, const sm_kv *kv, int nseq, int Nq, int &chunk, int &nsplit) {
-  const int units = nseq * m->Hkv * attention_row_blocks(Nq, m->G);
-  const int want = std::max(1, (2 * kNumSMs + units - 1) / units);
-  const int T = kv->cap;
-  auto up64 = [](int v) { return (v + 63) / 64 * 64; };
-  chunk = std::max(64, up64((T + want - 1) / want));
-  chunk = std::max(chunk, up64((T + kv->att_nsplit_max - 1) / kv->att_nsplit_max));
-  nsplit = (T + chunk - 1) / chunk;
+static int attn_splits(const sm_model *m, int nseq, int Nq) {
+  return attention_nsplit(nseq * m->Hkv * attention_row_blocks(Nq, m->G));
 }
+
+// Timing ablation (sm_set_option "ablate", experiments only -- results become
+// meaningless): bit 1 skips K1 attention, bit 2 the per-layer GEMM consumers,
+// bit 4 the per-layer GEMMs, bit 8 the Medusa heads.
+static int g_ablate = 0;
+#define KEEP(bit) ((g_ablate & (bit)) == 0)
 
 // tokens d_tok [nseq * Nq] -> hf [nseq * Nq][d]; K/V rows of every layer written
 static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, int nseq, int seq_base, int Nq,
@@ -642,31 +640,33 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
   const int d = m->d;
   CK(embed_launch(d_tok, m->embed, m->x, M, d, st));
   ++nl;
-  int chunk, nsplit;
-  attn_plan(m, kv, nseq, Nq, chunk, nsplit);
+  const int nsplit = attn_splits(m, nseq, Nq);
   const long long layer_rows = (long long)2 * kv->b * m->Hkv * kv->cap;
   const long long half_rows = (long long)kv->b * m->Hkv * kv->cap;
   RowCtx rc{M, Nq, seq_base, kv->len, tree.depth};
   PartialView pv, pv_down{};
   bool have_down = false;
+  g_ablate_gemm = (g_ablate & 4) ? 1 : 0;
   for (int l = 0; l < m->L; ++l) {
     // x += down (previous layer, R7); h = bf16(rms(x) * g1)   (R2)
-    CK(resid_norm_launch(have_down ? &pv_down : nullptr, m->x, m->attn_norm[l], m->h, M, d, m->cfg.rms_eps, st));
-    ++nl;
+    if (KEEP(2)) {
+      CK(resid_norm_launch(have_down ? &pv_down : nullptr, m->x, m->attn_norm[l], m->h, M, d, m->cfg.rms_eps, st));
+      ++nl;
+    }
     bf16 *kc = kv->base + (size_t)l * layer_rows * m->hd;
     bf16 *vc = kc + (size_t)half_rows * m->hd;
     CKS(run_gemm(m->g_qkv[l], M, 0, m->ws, m->ws_floats, st, nl, &pv));
     // RoPE, q -> m->q, k/v -> cache slots Lc + node (R3)
-    CK(qkv_consumer_launch(pv, rc, m->H, m->Hkv, m->hd, m->rope, m->q, kc, vc, kv->cap, st));
-    ++nl;
+    if (KEEP(2)) {
+      CK(qkv_consumer_launch(pv, rc, m->H, m->Hkv, m->hd, m->rope, m->q, kc, vc, kv->cap, st));
+      ++nl;
+    }
     AttnArgs aa;
     std::memset(&aa, 0, sizeof(aa));
     aa.tmK = kv->tmKV;
     aa.tmV = kv->tmKV;
     aa.q = m->q;
     aa.out = m->attn;
-    aa.part_o = kv->att_o;
-    aa.part_ml = kv->att_ml;
     aa.len = kv->len;
     aa.anc = tree.anc;
     aa.k_row0 = (long long)l * layer_rows;
@@ -679,24 +679,30 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
     aa.G = m->G;
     aa.nseq = nseq;
     aa.seq_base = seq_base;
-    aa.chunk = chunk;
     aa.nsplit = nsplit;
     aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)m->hd));
     cudaEvent_t ev = nullptr;
     prof_begin(st, &ev);
-    CK(attention_launch(aa, m->hd, st));
+    if (KEEP(1)) {
+      CK(attention_launch(aa, m->hd, st));
+      ++nl;
+    }
     prof_end(st, ev, 1, 0.0);
-    nl += nsplit > 1 ? 2 : 1;
     CKS(run_gemm(m->g_o[l], M, 0, m->ws, m->ws_floats, st, nl, &pv));
     // x += o (R5); h = bf16(rms(x) * g2)
-    CK(resid_norm_launch(&pv, m->x, m->mlp_norm[l], m->h, M, d, m->cfg.rms_eps, st));
-    ++nl;
+    if (KEEP(2)) {
+      CK(resid_norm_launch(&pv, m->x, m->mlp_norm[l], m->h, M, d, m->cfg.rms_eps, st));
+      ++nl;
+    }
     CKS(run_gemm(m->g_gu[l], M, 0, m->ws, m->ws_floats, st, nl, &pv));
-    CK(silu_consumer_launch(pv, m->F, m->act, st));  // act = bf16(SiLU(g) * u) (R6)
-    ++nl;
+    if (KEEP(2)) {
+      CK(silu_consumer_launch(pv, m->F, m->act, st));  // act = bf16(SiLU(g) * u) (R6)
+      ++nl;
+    }
     CKS(run_gemm(m->g_down[l], M, 0, m->ws, m->ws_floats, st, nl, &pv_down));
     have_down = true;
   }
+  g_ablate_gemm = 0;
   // x += down; hf = bf16(rms(x) * gf)   (R8)
   CK(resid_norm_launch(have_down ? &pv_down : nullptr, m->x, m->final_norm, m->hf, M, d, m->cfg.rms_eps, st));
   ++nl;
@@ -705,7 +711,7 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
 
 // heads at rows [row0, row0 + nb) of head_in -> topk rows [row0, row0 + nb)
 static sm_status enqueue_heads(sm_model *m, sm_kv *kv, int row0, int nb, cudaStream_t st, int &nl) {
-  if (m->nmed == 0 || kv->t->l == 0) return SM_OK;
+  if (m->nmed == 0 || kv->t->l == 0 || !KEEP(8)) return SM_OK;
   const int d = m->d, B = m->B;
   PartialView pv;
   CKS(run_gemm(m->g_R, nb, row0, m->ws, m->ws_floats, st, nl, &pv));
@@ -963,27 +969,14 @@ extern "C" sm_status sm_tree_attention(const sm_tree *t, const void *d_q, const 
   sm_tree *tt = const_cast<sm_tree *>(t);
   CKS(tree_upload(tt));
   const int G = n_heads / n_kv_heads;
-  const int units = batch * n_kv_heads * attention_row_blocks(t->N, G);
-  const int want = std::max(1, (2 * kNumSMs + units - 1) / units);
-  auto up64 = [](int v) { return (v + 63) / 64 * 64; };
-  int chunk = std::max(64, up64((cap + want - 1) / want));
-  int nsplit = (cap + chunk - 1) / chunk;
-  if (nsplit > 64) {
-    chunk = up64((cap + 63) / 64);
-    nsplit = (cap + chunk - 1) / chunk;
-  }
+  const int nsplit = attention_nsplit(batch * n_kv_heads * attention_row_blocks(t->N, G));
   AttnArgs aa;
   std::memset(&aa, 0, sizeof(aa));
   const uint64_t rows = (uint64_t)batch * n_kv_heads * cap;
   CKS(kv_map(&aa.tmK, d_k, rows, head_dim));
   CKS(kv_map(&aa.tmV, d_v, rows, head_dim));
-  const long long M = (long long)batch * t->N;
-  void *scr = nullptr;
-  if (nsplit > 1) CKS(scratch((size_t)nsplit * M * n_heads * (head_dim + 2) * 4, &scr));
   aa.q = (const bf16 *)d_q;
   aa.out = (bf16 *)d_out;
-  aa.part_o = (float *)scr;
-  aa.part_ml = nsplit > 1 ? (float *)scr + (size_t)nsplit * M * n_heads * head_dim : nullptr;
   aa.len = d_len;
   aa.anc = tt->d_anc;
   aa.k_row0 = 0;
@@ -996,7 +989,6 @@ extern "C" sm_status sm_tree_attention(const sm_tree *t, const void *d_q, const 
   aa.G = G;
   aa.nseq = batch;
   aa.seq_base = 0;
-  aa.chunk = chunk;
   aa.nsplit = nsplit;
   aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)head_dim));
   CK(attention_launch(aa, head_dim, (cudaStream_t)stream));
@@ -1009,7 +1001,7 @@ extern "C" sm_status sm_gemm_bf16(const void *d_x, const void *d_w, float *d_out
     return fail(SM_ERR_INVALID_ARG, "sm_gemm_bf16: bad arguments (M <= 256, K % 8 == 0)");
   GemmArgs a = gemm_proto(N, K, 1);
   CKS(weight_map(&a.tmW[0], d_w, N, K));
-  CKS(act_map(&a.tmX[0], d_x, M, K));
+  CKS(act_map(a, 0, d_x, M, K));
   const size_t need = ws_need(a, M);
   void *scr = nullptr;
   CKS(scratch(need * 4, &scr));
@@ -1034,6 +1026,12 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
     gemm_set_pdl(value != 0);
   } else if (n == "gemm_ctas") {
     gemm_set_ctas(value);
+  } else if (n == "l2_prefetch") {
+    gemm_set_l2_prefetch(value);
+  } else if (n == "gemm_mode") {
+    gemm_set_debug_mode(value);
+  } else if (n == "ablate") {
+    g_ablate = value;
   } else {
     return fail(SM_ERR_INVALID_ARG, "sm_set_option: unknown option " + n);
   }

@@ -1,8 +1,9 @@
 #!/bin/bash
-# bench.py under option variants (env SM_OPT="name=val,...")
-for v in "pdl=1" "pdl=0"; do
+# bench.py under option variants (env SM_OPT="name=val,..."); args override the list
+VARS=${@:-"pdl=1"}
+for v in $VARS; do
   echo "== $v"
-  SM_OPT=$v timeout 300 python bench.py --no-cpu-baseline --no-k1 --steps 50 --warmup 5 --e2e-steps 10 2>&1 | python3 -c "
+  SM_OPT=$v timeout 300 python bench.py --no-cpu-baseline --no-k1 --steps 50 --warmup 5 --e2e-steps 10 --prof-steps 2 2>&1 | python3 -c "
 import json,sys
 for l in sys.stdin:
     if l.startswith('{'):
