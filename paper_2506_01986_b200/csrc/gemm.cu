@@ -28,12 +28,12 @@
 
 namespace sm {
 
-template <int BN>
+template <int BN, int SMEMKB>
 struct GemmCfg {
   static constexpr int kA = 128 * 64 * 2;  // weight tile bytes
   static constexpr int kB = BN * 64 * 2;   // activation tile bytes
   static constexpr int kStage = kA + kB;
-  static constexpr int kStages = (216 * 1024) / kStage;
+  static constexpr int kStages = (SMEMKB * 1024) / kStage;  // 216 KB: 1 CTA/SM; 104 KB: 2 may co-reside
   static constexpr int kChunk = BN < 32 ? BN : 32;  // token columns per tcgen05.ld
   static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
   static constexpr int kSmem = kStages * kStage + 1024 + 256;
@@ -65,9 +65,9 @@ SM_DEV void tmem_ldc(uint32_t taddr, float *v) {
   }
 }
 
-template <int BN>
+template <int BN, int SMEMKB>
 __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_constant__ GemmArgs a) {
-  using C = GemmCfg<BN>;
+  using C = GemmCfg<BN, SMEMKB>;
   constexpr int CH = C::kChunk;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -225,18 +225,21 @@ static bool g_pdl = true;
 static int g_ctas = 0;
 static int g_l2pf = 0;
 static int g_dbg_mode = 0;
+static int g_occ = 2;  // GEMM CTAs per SM for BN <= 64 (1..4); grid = 148 * occ
+void gemm_set_small(int v) { g_occ = v < 1 ? 1 : (v > 4 ? 4 : v); }
+int gemm_occ_for(int bn) { return bn <= 64 ? g_occ : 1; }
 void gemm_set_debug_mode(int m) { g_dbg_mode = m; }
 void gemm_set_pdl(bool on) { g_pdl = on; }
 bool gemm_pdl() { return g_pdl; }
 void gemm_set_ctas(int n) { g_ctas = n; }
 void gemm_set_l2_prefetch(int kblocks) { g_l2pf = kblocks < 0 ? 0 : kblocks; }
 
-template <int BN>
+template <int BN, int SMEMKB>
 static cudaError_t launch_bn(const GemmArgs &a, cudaStream_t st) {
-  using C = GemmCfg<BN>;
+  using C = GemmCfg<BN, SMEMKB>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_streamk_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    cudaError_t e = cudaFuncSetAttribute(gemm_streamk_kernel<BN, SMEMKB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -250,7 +253,7 @@ static cudaError_t launch_bn(const GemmArgs &a, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gemm_streamk_kernel<BN>, a);
+  return cudaLaunchKernelEx(&cfg, gemm_streamk_kernel<BN, SMEMKB>, a);
 }
 
 int gemm_pick_bn(int M) {
@@ -273,7 +276,7 @@ void gemm_plan(GemmArgs &a, int N, int K, int M, int batch) {
   p.tiles = p.m_tiles * p.token_tiles * batch;
   p.kb_total = (K + 63) / 64;
   const long long U = (long long)p.tiles * p.kb_total;
-  const int want = g_ctas > 0 ? g_ctas : kNumSMs;
+  const int want = g_ctas > 0 ? g_ctas : kNumSMs * gemm_occ_for(p.bn);
   p.P = (int)(U < want ? U : want);
   p.U = U;
   // contributors per tile <= ceil(KB / floor(U/P)) + 1
@@ -288,11 +291,14 @@ cudaError_t gemm_launch(const GemmArgs &a0, cudaStream_t st) {
   a.l2_prefetch = g_pdl ? g_l2pf : 0;
   a.dbg_mode = g_dbg_mode;
   switch (a.plan.bn) {
-    case 16: return launch_bn<16>(a, st);
-    case 32: return launch_bn<32>(a, st);
-    case 64: return launch_bn<64>(a, st);
-    case 128: return launch_bn<128>(a, st);
-    default: return launch_bn<256>(a, st);
+    case 16: return g_occ == 4 ? launch_bn<16, 50>(a, st) : g_occ == 3 ? launch_bn<16, 68>(a, st)
+                    : g_occ == 2 ? launch_bn<16, 104>(a, st) : launch_bn<16, 216>(a, st);
+    case 32: return g_occ == 4 ? launch_bn<32, 50>(a, st) : g_occ == 3 ? launch_bn<32, 68>(a, st)
+                    : g_occ == 2 ? launch_bn<32, 104>(a, st) : launch_bn<32, 216>(a, st);
+    case 64: return g_occ == 4 ? launch_bn<64, 50>(a, st) : g_occ == 3 ? launch_bn<64, 68>(a, st)
+                    : g_occ == 2 ? launch_bn<64, 104>(a, st) : launch_bn<64, 216>(a, st);
+    case 128: return launch_bn<128, 216>(a, st);
+    default: return launch_bn<256, 216>(a, st);
   }
 }
 

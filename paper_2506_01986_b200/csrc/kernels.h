@@ -120,6 +120,7 @@ bool gemm_pdl();
 void gemm_set_ctas(int n);
 void gemm_set_l2_prefetch(int kblocks);
 void gemm_set_debug_mode(int m);
+void gemm_set_small(int v);
 
 // ---------------------------------------------------------------- K1 tree attention
 struct AttnArgs {

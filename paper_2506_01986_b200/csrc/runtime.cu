@@ -1028,6 +1028,8 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
     gemm_set_ctas(value);
   } else if (n == "l2_prefetch") {
     gemm_set_l2_prefetch(value);
+  } else if (n == "gemm_occ") {
+    gemm_set_small(value);
   } else if (n == "gemm_mode") {
     gemm_set_debug_mode(value);
   } else if (n == "ablate") {
