@@ -152,6 +152,49 @@ def attn_bytes(cfg: dict, N: int, Lc: float, b: int = 1) -> float:
     return L * b * (Hkv * (Lc + N) * hd * 2 * 2 + 2 * N * H * hd * 2)
 
 
+# ------------------------------------------------------------------ workloads (BASELINE.json configs)
+WORKLOADS = {
+    "c2": dict(model="vicuna7b", n_medusa=4, tree="V64", batch=1, x=2048, mode="greedy",
+               desc="C2: Vicuna-7B-shaped Llama + 4 Medusa-1 heads (random init), Medusa V64 tree (64 nodes, "
+                    "42 leaves), bs=1 per GPU, KV bounded to x=2048 (+64 scratch), greedy"),
+    "c1": dict(model="tiny", n_medusa=3, tree="TINY16", batch=1, x=64, mode="greedy", prompt=32,
+               desc="C1: tiny random-init Llama (2 layers, d=64, 4 heads, V=256) + 3 Medusa heads, 16-node tree, "
+                    "bs=1, 32-token prompt, KV x=64"),
+    "c3": dict(model="vicuna13b", n_medusa=4, tree="V64", batch=1, x=2304, mode="typical",
+               desc="C3: Vicuna-13B-shaped + 4 Medusa heads, V64 tree, bs=1, mid-conversation of an 8-turn "
+                    "MT-Bench-length chat (KV bounded to 2304 = sum of turns), typical acceptance T=0.7 eps=0.09 "
+                    "alpha=0.3"),
+    "c4": dict(model="llama70b", n_medusa=3, tree="TINY16", batch=10, x=416, mode="greedy",
+               desc="C4: Llama-2-70B-shaped (GQA 64/8) + 3 Medusa heads, 16-node tree, bs=10 ragged prompts of "
+                    "32-160 tokens + 256 new, KV bounded to 416 (+16), greedy, TP1 (one B200, 140 GB of weights)"),
+}
+
+
+def build_workload(sm, wl: dict, args, rank: int):
+    import torch
+    cfg = synth.model_cfg(wl["model"])
+    choices = {"V64": synth.V64, "TINY16": synth.TINY16}[wl["tree"]]
+    tree = sm.Tree(choices, topk=synth.TOPK)
+    W = sm.allocate_weights(cfg, wl["n_medusa"], seed=args.seed + rank)
+    b, x = wl["batch"], wl["x"]
+    model = sm.Model(cfg, W, max_rows=max(b * tree.N, 256), max_batch=b, max_seq_len=x + tree.N)
+    kv = sm.KVCache(model, tree, b, x)
+    total_steps = args.warmup + args.steps + args.prof_steps + args.e2e_steps + 8
+    if b == 1:
+        if "prompt" in wl:
+            lc_start = wl["prompt"]
+        else:
+            lc_start = max(128, min(args.lc_start, x - 5 * total_steps - 8))
+        prompts = [synth.prompt_tokens(args.seed, rank, lc_start, cfg["vocab"])]
+    else:  # ragged MT-Bench-length prompts (32 + h mod 129)
+        prompts = [synth.prompt_tokens(args.seed, i, synth.prompt_length(args.seed, i), cfg["vocab"]) for i in range(b)]
+        lc_start = int(np.mean([len(p) for p in prompts]))
+    for i, p in enumerate(prompts):
+        kv.prefill(i, torch.from_numpy(p).cuda())
+    mode = sm.TYPICAL if wl["mode"] == "typical" else sm.GREEDY
+    return cfg, tree, model, kv, mode, lc_start
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args, world, rank, local) -> dict | None:
     import torch
@@ -161,18 +204,11 @@ def run_ours(args, world, rank, local) -> dict | None:
     for kv_opt in filter(None, os.environ.get("SM_OPT", "").split(",")):  # experiment knobs (sm_set_option)
         k, v = kv_opt.split("=")
         sm.lib().sm_set_option(k.encode(), int(v))
-    cfg = synth.model_cfg("vicuna7b")
-    tree = sm.Tree(synth.V64, topk=synth.TOPK)
-    N, l = tree.N, tree.depth
-    W = sm.allocate_weights(cfg, N_MEDUSA, seed=args.seed + rank)
-    model = sm.Model(cfg, W, max_rows=256, max_batch=1, max_seq_len=X_BOUND + N)
-    kv = sm.KVCache(model, tree, 1, X_BOUND)
-    total_steps = args.warmup + args.steps + args.prof_steps + args.e2e_steps + 8
-    lc_start = max(128, min(args.lc_start, X_BOUND - 5 * total_steps - 8))
-    prompt = torch.from_numpy(synth.prompt_tokens(args.seed, rank, lc_start, cfg["vocab"])).cuda()
-    kv.prefill(0, prompt)
-    out = sm.AcceptOut(1, l)
-    acfg = sm.accept_cfg(sm.GREEDY)
+    wl = WORKLOADS[args.config]
+    cfg, tree, model, kv, mode, lc_start = build_workload(sm, wl, args, rank)
+    N, l, b = tree.N, tree.depth, kv.batch
+    out = sm.AcceptOut(b, l)
+    acfg = sm.accept_cfg(mode)
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
@@ -181,7 +217,7 @@ def run_ours(args, world, rank, local) -> dict | None:
     torch.cuda.synchronize()
     barrier(world)
     st = torch.cuda.current_stream()
-    L0 = int(kv.lengths()[0])
+    L0 = kv.lengths().astype(np.int64)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier(world)
     torch.cuda.synchronize()
@@ -193,18 +229,18 @@ def run_ours(args, world, rank, local) -> dict | None:
     barrier(world)
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
-    L1 = int(kv.lengths()[0])
+    L1 = kv.lengths().astype(np.int64)
     ms_max = reduce_max(ms, world)
-    tokens = reduce_sum(L1 - L0, world)
+    tokens = reduce_sum(float((L1 - L0).sum()), world)
     value = tokens / (ms_max / 1e3)
-    tau = (L1 - L0) / args.steps
+    tau = float((L1 - L0).sum()) / args.steps / b
     launches = kv.step_launches()
 
     # ---- kernel timing pass (event-instrumented replay of the same graph)
     kv.profile(True)
     g_ms, g_bytes, g_n, a_ms, a_n, lcs = [], [], 0, [], 0, []
     for _ in range(args.prof_steps):
-        lcs.append(int(kv.lengths()[0]))
+        lcs.append(float(kv.lengths().mean()))
         kv.step(acfg, out)
         n, gm, gb = kv.profile_read(0)
         na, am, _ = kv.profile_read(1)
@@ -220,11 +256,11 @@ def run_ours(args, world, rank, local) -> dict | None:
 
     # ---- end-to-end through the public API with host buffers (pinned), per step:
     # H2D of the turn budget, the step, D2H of the emitted tokens + counts.
-    h_budget = torch.full((1,), 1 << 30, dtype=torch.int32).pin_memory()
-    d_budget = torch.empty(1, dtype=torch.int32, device="cuda")
-    h_emit = torch.empty((1, l + 1), dtype=torch.int32).pin_memory()
-    h_n = torch.empty((1,), dtype=torch.int32).pin_memory()
-    ecfg = sm.accept_cfg(sm.GREEDY, max_new=d_budget)
+    h_budget = torch.full((b,), 1 << 30, dtype=torch.int32).pin_memory()
+    d_budget = torch.empty(b, dtype=torch.int32, device="cuda")
+    h_emit = torch.empty((b, l + 1), dtype=torch.int32).pin_memory()
+    h_n = torch.empty((b,), dtype=torch.int32).pin_memory()
+    ecfg = sm.accept_cfg(mode, max_new=d_budget)
     d_budget.copy_(h_budget)
     kv.step(ecfg, out)  # capture the e2e graph variant outside the timed region
     torch.cuda.synchronize()
@@ -238,33 +274,32 @@ def run_ours(args, world, rank, local) -> dict | None:
         h_emit.copy_(out.emit_tok, non_blocking=True)
         h_n.copy_(out.n_emit, non_blocking=True)
         st.synchronize()                   # the caller reads this step's tokens
-        e2e_tokens += int(h_n[0])
+        e2e_tokens += int(h_n.sum())
     e1.record(st)
     torch.cuda.synchronize()
     e_ms = reduce_max(e0.elapsed_time(e1), world)
     e2e_val = reduce_sum(e2e_tokens, world) / (e_ms / 1e3)
 
     # ---- K1 tree-attention point of the C5 sweep (geometry A, N=64)
-    k1 = run_k1_point(sm, args) if args.k1 else None
+    k1 = run_k1_point(sm, args) if args.k1 and args.config == "c2" else None
 
     if rank != 0:
         return None
     pk = peaks()
     gemm_gbs = gemm_bytes / (gemm_ms / 1e3) / 1e9
-    sb = step_bytes(cfg, N, (L0 + L1) / 2, tau=tau)
+    lc_mean = float((L0 + L1).mean() / 2)
+    sb = step_bytes(cfg, N, lc_mean, b=b, n_medusa=wl["n_medusa"], tau=tau)
     ms_step = ms_max / args.steps
     res = {
         "metric": METRIC, "value": round(value, 3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic: counter-hash random-init weights (std 0.02), counter-hash prompt tokens",
-        "config": {"workload": "C2: Vicuna-7B-shaped Llama + 4 Medusa-1 heads (random init), Medusa V64 tree "
-                               "(64 nodes, 42 leaves), bs=1 per GPU, KV bounded to x=2048 (+64 scratch), greedy",
-                   "global_batch": world, "seq_len": X_BOUND, "lc_start": lc_start, "lc_mean": (L0 + L1) / 2,
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                   "l2": "inputs larger than L2: 14.7 GB of weights streamed every step (L2 126 MB)"},
+        "config": {"workload": wl["desc"], "global_batch": world * b, "seq_len": wl["x"], "lc_start": lc_start,
+                   "lc_mean": lc_mean, "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": f"inputs larger than L2: {sb / 1e9:.1f} GB streamed every step (L2 126 MB)"},
         "tau": round(tau, 4), "steps_per_s": round(args.steps / (ms_max / 1e3), 3),
-        "roofline": {"kernel": "K2 tcgen05 GEMM (all 129 weight GEMMs + 2 head GEMMs of one step)", "bound": "hbm",
+        "roofline": {"kernel": f"K2 tcgen05 GEMM (all {g_n} weight GEMM launches of one step)", "bound": "hbm",
                      "achieved": round(gemm_gbs, 1), "peak": pk["hbm"], "unit": "GB/s",
                      "frac": round(gemm_gbs / pk["hbm"], 4), "traffic": gemm_traffic(),
                      "launches_per_step": g_n, "ms_per_step": round(gemm_ms, 4),
@@ -273,10 +308,10 @@ def run_ours(args, world, rank, local) -> dict | None:
         "step_roofline": {"bound": "hbm", "alg_bytes": sb, "roofline_ms": round(sb / pk["hbm"] / 1e6, 4),
                           "frac": round(sb / pk["hbm"] / 1e6 / ms_step, 4)},
         "tree_attn_in_step": {"launches_per_step": a_n, "ms_per_step": round(attn_ms, 4), "lc": lc_prof,
-                              "alg_bytes": attn_bytes(cfg, N, lc_prof),
-                              "achieved_gbs": round(attn_bytes(cfg, N, lc_prof) / (attn_ms / 1e3) / 1e9, 1)},
-        "e2e": {"value": round(e2e_val, 3), "unit": "tokens/s", "h2d_bytes_per_step": 4,
-                "d2h_bytes_per_step": 4 * (l + 1) + 4, "steps": args.e2e_steps},
+                              "alg_bytes": attn_bytes(cfg, N, lc_prof, b=b),
+                              "achieved_gbs": round(attn_bytes(cfg, N, lc_prof, b=b) / (attn_ms / 1e3) / 1e9, 1)},
+        "e2e": {"value": round(e2e_val, 3), "unit": "tokens/s", "h2d_bytes_per_step": 4 * b,
+                "d2h_bytes_per_step": b * (4 * (l + 1) + 4), "steps": args.e2e_steps},
         "gpu_launches": launches * args.steps,
         "clocks": clk,
     }
@@ -414,6 +449,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--lc-start", type=int, default=1024)
     ap.add_argument("--prof-steps", type=int, default=5)
     ap.add_argument("--e2e-steps", type=int, default=50)
@@ -431,7 +467,7 @@ def main():
     world, rank, local = dist_setup()
     res = run_ours(args, world, rank, local)
     if res is not None:
-        if args.cpu and world == 1:
+        if args.cpu and world == 1 and args.config == "c2":
             res["cpu_baseline"] = cpu_baseline(res["tau"])
         print(json.dumps(res), flush=True)
     if world > 1:

@@ -71,7 +71,7 @@ void sm_tree_destroy(sm_tree *t);
 typedef struct {
   int n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ffn, vocab, n_medusa;
   float rms_eps, rope_theta;
-  int max_rows;      /* max token rows per forward (b*N or a prefill chunk), <= 256 */
+  int max_rows;      /* max token rows per forward (b*N; prefill chunks use <= 256), <= 1024 */
   int max_batch;     /* max sequences b                                          */
   int max_seq_len;   /* max positions (RoPE table length) = x + N                */
 } sm_model_cfg;
@@ -183,7 +183,7 @@ sm_status sm_state_device(const sm_kv *kv, int32_t **d_root, int32_t **d_topk);
 sm_status sm_tree_attention(const sm_tree *t, const void *d_q, const void *d_k, const void *d_v,
                             const int32_t *d_len, int batch, int n_heads, int n_kv_heads, int head_dim, int cap,
                             void *d_out, void *stream);
-/* K2 tcgen05 GEMM: out[M][N] fp32 = x[M][K] bf16 * w[N][K]^T bf16.  M <= 256. */
+/* K2 tcgen05 GEMM: out[M][N] fp32 = x[M][K] bf16 * w[N][K]^T bf16.  M <= 1024. */
 sm_status sm_gemm_bf16(const void *d_x, const void *d_w, float *d_out, int M, int N, int K, void *stream);
 /* K3 top-k rows of fp32 logits: idx[r][k] by (value desc, index asc).        */
 sm_status sm_topk_f32(const float *d_logits, int rows, int V, int k, int32_t *d_idx, void *stream);

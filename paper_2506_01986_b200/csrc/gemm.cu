@@ -107,7 +107,8 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer
-      const uint64_t pol_w = policy_evict_first();
+      // weights stream through once; with several token tiles they are re-read right away
+      const uint64_t pol_w = pl.token_tiles > 1 ? policy_evict_last() : policy_evict_first();
       const bool wonly = a.dbg_mode == 1;
       const uint32_t stage_bytes = wonly ? (uint32_t)C::kA : (uint32_t)C::kStage;
       auto issue_x = [&](int s, int bi, int tt, int kc) {  // activation rows [tt*BN, tt*BN + BN)

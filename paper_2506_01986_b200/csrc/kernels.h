@@ -23,7 +23,7 @@ struct RowCtx {                // forward rows m = (seq - seq_base) * Nq + n
 
 // ---------------------------------------------------------------- K2 GEMM split plan
 // Stream-K partition: U = tiles * kb_total units split evenly over P CTAs, CTA c
-// owns [U*c/P, U*(c+1)/P).  Tile t = (bi * token_tiles + tt) * m_tiles + mt
+// owns [U*c/P, U*(c+1)/P).  Tile t = (bi * m_tiles + mt) * token_tiles + tt
 // covers 128 output features x bn token rows.  Every (tile, contributing CTA)
 // writes an fp32 partial [bn][128] at slot t * maxc + (c - first CTA of t).
 struct SplitPlan {
@@ -36,11 +36,16 @@ __host__ __device__ inline int sk_cta_of(long long u, const SplitPlan &p) {
 }
 __host__ __device__ inline int sk_tile(long long u, const SplitPlan &p) { return (int)(u / p.kb_total); }
 __host__ __device__ inline int sk_kb(long long u, const SplitPlan &p) { return (int)(u % p.kb_total); }
+// token tiles of one weight tile are adjacent units, so a re-read of the same
+// 128 x K weight rows for the next token tile is a near-term L2 hit
 __host__ __device__ inline void sk_decode(int t, const SplitPlan &p, int &bi, int &tt, int &mt) {
-  mt = t % p.m_tiles;
-  const int r = t / p.m_tiles;
-  tt = r % p.token_tiles;
-  bi = r / p.token_tiles;
+  tt = t % p.token_tiles;
+  const int r = t / p.token_tiles;
+  mt = r % p.m_tiles;
+  bi = r / p.m_tiles;
+}
+__host__ __device__ inline int sk_tile_of(const SplitPlan &p, int bi, int tt, int mt) {
+  return (bi * p.m_tiles + mt) * p.token_tiles + tt;
 }
 __host__ __device__ inline float *sk_partial(float *ws, const SplitPlan &p, int t, int k) {
   return ws + ((size_t)t * p.maxc + k) * p.bn * 128;
@@ -57,7 +62,7 @@ struct PartialView {
 __device__ inline float4 sk_sum4(const PartialView &v, int bi, int m, int n) {
   const SplitPlan &p = v.plan;
   const int tt = m / p.bn, mt = n >> 7;
-  const int t = (bi * p.token_tiles + tt) * p.m_tiles + mt;
+  const int t = sk_tile_of(p, bi, tt, mt);
   const int cf = sk_cta_of((long long)t * p.kb_total, p), cl = sk_cta_of((long long)(t + 1) * p.kb_total - 1, p);
   const int nc = cl - cf + 1;
   const float4 *base =
@@ -83,7 +88,7 @@ __device__ inline float4 sk_sum4(const PartialView &v, int bi, int m, int n) {
 __device__ inline float sk_sum1(const PartialView &v, int bi, int m, int n) {
   const SplitPlan &p = v.plan;
   const int tt = m / p.bn, mt = n >> 7;
-  const int t = (bi * p.token_tiles + tt) * p.m_tiles + mt;
+  const int t = sk_tile_of(p, bi, tt, mt);
   const int cf = sk_cta_of((long long)t * p.kb_total, p), cl = sk_cta_of((long long)(t + 1) * p.kb_total - 1, p);
   const int nc = cl - cf + 1;
   const float *base = v.ws + (size_t)t * p.maxc * p.bn * 128 + (size_t)(m - tt * p.bn) * 128 + (n & 127);

@@ -330,10 +330,10 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
   const sm_model_cfg &c = *cfg;
   if (c.n_layers < 1 || c.d_model % 64 || c.n_heads < 1 || c.n_kv_heads < 1 || c.n_heads % c.n_kv_heads ||
       (c.head_dim != 16 && c.head_dim != 32 && c.head_dim != 64 && c.head_dim != 128) || c.d_ffn % 64 ||
-      c.vocab % 4 || c.n_medusa < 0 || c.n_medusa > kMaxGemmBatch || c.max_rows < 1 || c.max_rows > 256 ||
+      c.vocab % 4 || c.n_medusa < 0 || c.n_medusa > kMaxGemmBatch || c.max_rows < 1 || c.max_rows > 1024 ||
       c.max_batch < 1 || c.max_seq_len < 1 || (c.n_heads * c.head_dim) % 64)
     return fail(SM_ERR_INVALID_ARG, "sm_model_create: unsupported shape (d, F multiple of 64; hd in {16,32,64,128}; "
-                                    "max_rows <= 256; n_medusa <= 5)");
+                                    "max_rows <= 1024; n_medusa <= 5)");
   if (c.vocab * 4 > 200 * 1024) return fail(SM_ERR_INVALID_ARG, "vocab too large for the shared-memory top-k");
   sm_model *m = new sm_model();
   m->cfg = c;
@@ -451,7 +451,8 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
   ALLOC(m->ws, need, "stream-K partials");
   m->ws_floats = need;
 #undef ALLOC
-  if ((s = sm_tree_create_chain(R, &m->chain)) != SM_OK || (s = tree_upload(m->chain)) != SM_OK) {
+  if ((s = sm_tree_create_chain(std::min(R, kMaxTreeNodes), &m->chain)) != SM_OK ||
+      (s = tree_upload(m->chain)) != SM_OK) {
     sm_model_destroy(m);
     return s;
   }
@@ -739,7 +740,7 @@ extern "C" sm_status sm_prefill(sm_model *m, sm_kv *kv, int seq, const int32_t *
   const int R = m->R;
   int done = 0, last = 0;
   while (done < n) {
-    const int P = std::min(R, n - done);
+    const int P = std::min(std::min(R, kMaxTreeNodes), n - done);  // chain-tree chunks of <= 256 tokens
     CKS(enqueue_forward(m, kv, d_tokens + done, 1, seq, P, chain, st, nl));
     CK(advance_len_launch(kv->len, seq, P, st));
     done += P;
@@ -997,8 +998,8 @@ extern "C" sm_status sm_tree_attention(const sm_tree *t, const void *d_q, const 
 
 extern "C" sm_status sm_gemm_bf16(const void *d_x, const void *d_w, float *d_out, int M, int N, int K,
                                   void *stream) {
-  if (!d_x || !d_w || !d_out || M < 1 || M > 256 || N < 1 || K < 8 || K % 8)
-    return fail(SM_ERR_INVALID_ARG, "sm_gemm_bf16: bad arguments (M <= 256, K % 8 == 0)");
+  if (!d_x || !d_w || !d_out || M < 1 || M > 1024 || N < 1 || K < 8 || K % 8)
+    return fail(SM_ERR_INVALID_ARG, "sm_gemm_bf16: bad arguments (M <= 1024, K % 8 == 0)");
   GemmArgs a = gemm_proto(N, K, 1);
   CKS(weight_map(&a.tmW[0], d_w, N, K));
   CKS(act_map(a, 0, d_x, M, K));
