@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libspecmemo.so")
+LIB_PATH = os.environ.get("SPECMEMO_LIB") or os.path.join(HERE, "libspecmemo.so")  # override: diagnostics builds
 
 SM_OK, SM_ERR_INVALID_ARG, SM_ERR_INFEASIBLE_TREE, SM_ERR_KV_CAPACITY = 0, 1, 2, 3
 SM_ERR_DEVICE_OOM, SM_ERR_CUDA, SM_ERR_NCCL, SM_ERR_UNSUPPORTED = 4, 5, 6, 7
@@ -343,3 +343,8 @@ def topk_f32(logits, k: int, out, stream=None) -> None:
 
 def version() -> str:
     return lib().sm_version().decode()
+
+
+def set_option(name: str, value: int) -> None:
+    """sm_set_option: process-wide launch knobs ("pdl", "gemm_ctas", "attn_tc", ...)."""
+    _check(lib().sm_set_option(name.encode(), int(value)))

@@ -312,7 +312,15 @@ __global__ void __launch_bounds__(128) tree_attn_kernel(const __grid_constant__ 
   cluster_sync_all();  // keep every CTA's shared memory alive until all remote reads are done
 }
 
-int attention_row_blocks(int Nq, int G) { return (Nq * G + 63) / 64; }
+static int g_attn_tc = 1;  // head_dim 128 on tcgen05 (sm_set_option "attn_tc")
+static int g_attn_splits = 0;  // experiments: force the key-split count (sm_set_option "attn_splits", 0 = auto)
+void attention_set_tc(int on) { g_attn_tc = on; }
+void attention_set_splits(int n) { g_attn_splits = n; }
+static bool use_tc(int head_dim) { return g_attn_tc && head_dim == 128; }
+int attention_row_blocks(int Nq, int G, int head_dim) {
+  const int rows = use_tc(head_dim) ? 128 : 64;
+  return (Nq * G + rows - 1) / rows;
+}
 
 template <int HD>
 static cudaError_t launch_hd(const AttnArgs &a, cudaStream_t st) {
@@ -324,7 +332,7 @@ static cudaError_t launch_hd(const AttnArgs &a, cudaStream_t st) {
     attr = true;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(a.nsplit, attention_row_blocks(a.Nq, a.G), a.nseq * a.Hkv);
+  cfg.gridDim = dim3(a.nsplit, (a.Nq * a.G + 63) / 64, a.nseq * a.Hkv);
   cfg.blockDim = dim3(128);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = st;
@@ -341,7 +349,12 @@ static cudaError_t launch_hd(const AttnArgs &a, cudaStream_t st) {
 }
 
 // nsplit = cluster size in {1, 2, 4, 8}: enough CTAs to cover ~2 waves of SMs
-int attention_nsplit(int units) {
+int attention_tc_nsplit(int units);
+cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st);
+
+int attention_nsplit(int units, int head_dim) {
+  if (g_attn_splits == 1 || g_attn_splits == 2 || g_attn_splits == 4 || g_attn_splits == 8) return g_attn_splits;
+  if (use_tc(head_dim)) return attention_tc_nsplit(units);
   int ns = 1;
   while (ns < 8 && units * ns < 2 * kNumSMs) ns *= 2;
   return ns;
@@ -352,7 +365,7 @@ cudaError_t attention_launch(const AttnArgs &a, int head_dim, cudaStream_t st) {
     case 16: return launch_hd<16>(a, st);
     case 32: return launch_hd<32>(a, st);
     case 64: return launch_hd<64>(a, st);
-    case 128: return launch_hd<128>(a, st);
+    case 128: return use_tc(128) ? attention_tc_launch(a, st) : launch_hd<128>(a, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -1,0 +1,527 @@
+// attention_tc.cu -- K1 on 5th-gen tensor cores (head_dim 128): tree-masked
+// attention of up to 128 query rows (N nodes x G query heads of one kv head)
+// per CTA against the committed prefix [0, Lc) and the tree slots [Lc, Lc+N).
+//
+// Eq. 2: node n attends to its ancestors and itself ("attention mask
+// assumes full acceptance") plus the whole cached prefix; scale 1/sqrt(hd).
+//
+//  * S = Q K^T and O += P V are tcgen05.mma (kind::f16, M = 128 query rows) with
+//    fp32 accumulators in TMEM: S double-buffered (2 x 64 columns) so the MMA of
+//    tile i+1 overlaps the softmax of tile i; O (128 columns) stays in TMEM for
+//    the whole key range.  K (K-major) and V (MN-major) tiles of 64 keys are
+//    TMA-loaded (SWIZZLE_128B) into a 4-deep mbarrier ring and used in place;
+//    P is double-buffered so the softmax of tile i+1 does not wait for PV(i).
+//  * softmax: one thread per query row reads its S row with tcgen05.ld, applies
+//    the ancestor mask on tiles past Lc, and keeps a running max that is only
+//    raised when a tile exceeds it by more than 2^8 (then that warp rescales its
+//    O rows in TMEM with tcgen05.ld/st) -- the result is exact because l and O
+//    use the same stale max.  P (bf16) goes to shared memory in the UMMA A
+//    layout.
+//  * split-KV: the nsplit CTAs of a (row block, seq, kv head) form a cluster; each
+//    stages its (m, l, O) rows in its idle K/V ring and the CTA owning a row pulls
+//    the nsplit partials over DSMEM and combines them in a fixed rank order.
+//  * programmatic dependent launch: prefix K/V tiles are requested before
+//    griddepcontrol.wait; Q and the tree tiles after it.
+// Warp roles (192 threads): warps 0-3 softmax / epilogue (TMEM lanes = rows),
+// warp 4 TMA producer, warp 5 MMA issuer + TMEM allocator.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sm {
+
+namespace tc {
+constexpr int HD = 128;
+constexpr int ROWS = 128;                     // query rows per CTA (UMMA M)
+constexpr int KEYS = 64;                      // keys per tile
+constexpr int TILE = KEYS * HD * 2;           // 16 KB: one K (or V) tile
+constexpr int STAGES = 4;
+constexpr int QB = ROWS * HD * 2;             // 32 KB
+constexpr int PB = ROWS * KEYS * 2;           // 16 KB per P buffer (two)
+constexpr int OFF_Q = 0;
+constexpr int OFF_P = OFF_Q + QB;
+constexpr int OFF_KV = OFF_P + 2 * PB;
+constexpr int OFF_BAR = OFF_KV + STAGES * 2 * TILE;
+constexpr int SMEM = OFF_BAR + 256 + 1024;    // + barriers + alignment slack
+constexpr float RESCALE_LOG2 = 8.0f;          // lazy-rescale threshold (log2 units)
+}  // namespace tc
+
+// K-major SWIZZLE_128B operand: byte offset of 16-byte chunk c of row r in a
+// [rows][64 bf16] block (8-row atoms of 1024 B)
+SM_DEV uint32_t sw128_off(int r, int c) { return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + (((c ^ r) & 7) << 4)); }
+
+// UMMA descriptor, MN-major SWIZZLE_128B: 64-element MN atoms LBO apart, 8-row
+// K groups SBO = 1024 B apart
+SM_DEV uint64_t umma_desc_mn_sw128(uint32_t smem_addr, uint32_t lbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// kind::f16 instruction descriptor with operand majors (0 = K, 1 = MN)
+__host__ __device__ constexpr uint32_t idesc_bf16_major(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+SM_DEV float ex2(float x) {  // 2^x, flush-to-zero (MUFU.EX2; -inf -> 0)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+SM_DEV void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+SM_DEV void tmem_ld32_f(uint32_t taddr, float *v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%"
+      "19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+SM_DEV void tmem_st32_f(uint32_t taddr, const float *v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15])), "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])),
+      "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])), "r"(__float_as_uint(v[20])),
+      "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
+      "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])),
+      "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])),
+      "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31])));
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_constant__ AttnArgs a) {
+  using namespace tc;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sQ = smem + OFF_Q;
+  uint8_t *sP = smem + OFF_P;
+  uint8_t *sKV = smem + OFF_KV;
+  uint64_t *kv_full = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
+  uint64_t *kv_empty = kv_full + STAGES;
+  uint64_t *s_full = kv_empty + STAGES;  // [2]
+  uint64_t *s_free = s_full + 2;         // [2]
+  uint64_t *p_full = s_free + 2;         // [2] P buffers
+  uint64_t *o_done = p_full + 2;         // [2] PV(i) commits to o_done[i & 1]
+  uint64_t *q_full = o_done + 2;
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(q_full + 1);
+
+  pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) SM_STAMP(0);
+  const int split = blockIdx.x, rblk = blockIdx.y;  // split = rank in the (nsplit, 1, 1) cluster
+  const int sl = blockIdx.z / a.Hkv, h = blockIdx.z % a.Hkv;
+  const int seq = a.seq_base + sl;
+  const int Lc = a.len[seq];  // changed only by the step's last kernels: safe before the wait
+  const int T = Lc + a.Nq;
+  const int chunk = ((T + a.nsplit - 1) / a.nsplit + KEYS - 1) / KEYS * KEYS;
+  const int key0 = min(T, split * chunk);
+  const int key1 = min(T, key0 + chunk);
+  const int ntiles = (key1 - key0 + KEYS - 1) / KEYS;
+  const int R = a.Nq * a.G;
+  const float sl2 = a.scale_log2;
+
+  const long long kbase_row = a.k_row0 + (long long)seq * a.seq_rows + (long long)h * a.cap;
+  const long long vbase_row = a.v_row0 + (long long)seq * a.seq_rows + (long long)h * a.cap;
+  auto issue = [&](int i) {  // TMA: K and V of key tile i -> ring stage i % STAGES
+    const int s = i % STAGES;
+    uint8_t *kb = sKV + s * 2 * TILE;
+    uint8_t *vb = kb + TILE;
+    const int p = key0 + i * KEYS;
+    mbar_arrive_expect_tx(&kv_full[s], 2 * TILE);
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      tma_load_2d(kb + hf * 8192, &a.tmK, &kv_full[s], hf * 64, (int)(kbase_row + p));
+      tma_load_2d(vb + hf * 8192, &a.tmV, &kv_full[s], hf * 64, (int)(vbase_row + p));
+    }
+  };
+  const int first = min(STAGES, ntiles);
+  int pre = 0;
+  if (threadIdx.x == 128) {  // producer thread: barriers, then the prefix tiles (independent of this step)
+    tma_prefetch_desc(&a.tmK);
+    tma_prefetch_desc(&a.tmV);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_free[b], 128);
+      mbar_init(&p_full[b], 128);
+      mbar_init(&o_done[b], 1);
+    }
+    mbar_init(q_full, 128);
+    fence_barrier_init();
+    while (pre < first && key0 + (pre + 1) * KEYS <= Lc) issue(pre++);
+    SM_STAMP(11);
+  }
+  // softmax threads: the ancestor words of their row's node (static tree tables: safe before the wait)
+  uint64_t anc0 = 0, anc1 = 0, anc2 = 0, anc3 = 0;
+  if (warp < 4) {
+    const int r = rblk * ROWS + threadIdx.x;
+    if (r < R) {
+      const uint64_t *w = a.anc + (r / a.G) * kAncWords;
+      anc0 = w[0];
+      anc1 = w[1];
+      anc2 = w[2];
+      anc3 = w[3];
+    }
+  }
+  static_assert(kAncWords == 4, "ancestor words are kept in 4 registers");
+  if (warp == 5) tmem_alloc<256>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) SM_STAMP(1);
+  const uint32_t tmem = *tslot;  // S0: cols [0,64), S1: [64,128), O: [128,256)
+
+  if (warp == 4) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      pdl_wait();
+      SM_STAMP(12);
+      for (int i = pre; i < first; ++i) issue(i);
+      for (int i = STAGES; i < ntiles; ++i) {
+        mbar_wait(&kv_empty[i % STAGES], ((i / STAGES) - 1) & 1);
+        issue(i);
+      }
+      SM_STAMP(13);
+    }
+  } else if (warp == 5) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0 && ntiles > 0) {
+      constexpr uint32_t idesc_s = idesc_bf16_major(ROWS, KEYS, 0, 0);  // Q (K-major) x K^T (K-major)
+      constexpr uint32_t idesc_o = idesc_bf16_major(ROWS, HD, 0, 1);    // P (K-major) x V (MN-major)
+      const uint32_t q_u = smem_u32(sQ), p_u = smem_u32(sP), kv_u = smem_u32(sKV);
+      mbar_wait(q_full, 0);
+      SM_STAMP(14);
+      auto issue_s = [&](int i) {
+        const int sb = i & 1, st = i % STAGES;
+        if (i >= 2) mbar_wait(&s_free[sb], ((i >> 1) - 1) & 1);
+        mbar_wait(&kv_full[st], (i / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t kb = kv_u + st * 2 * TILE;
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {  // hd in 16-element steps; halves of 64 are separate 8/16 KB blocks
+          const uint64_t ad = umma_desc_sw128(q_u + (k >> 2) * 16384 + (k & 3) * 32);
+          const uint64_t bd = umma_desc_sw128(kb + (k >> 2) * 8192 + (k & 3) * 32);
+          umma_bf16(tmem + sb * KEYS, ad, bd, idesc_s, k > 0);
+        }
+        umma_commit(&s_full[sb]);
+      };
+      issue_s(0);
+      for (int i = 0; i < ntiles; ++i) {
+        if (i + 1 < ntiles) issue_s(i + 1);
+        mbar_wait(&p_full[i & 1], (i >> 1) & 1);
+        tc_fence_after();
+        const uint32_t vb = kv_u + (i % STAGES) * 2 * TILE + TILE;
+#pragma unroll
+        for (int k = 0; k < KEYS / 16; ++k) {  // keys in 16-row steps
+          const uint64_t ad = umma_desc_sw128(p_u + (i & 1) * PB + k * 32);
+          const uint64_t bd = umma_desc_mn_sw128(vb + k * 2048, 8192);
+          umma_bf16(tmem + 2 * KEYS, ad, bd, idesc_o, (i > 0 || k > 0) ? 1u : 0u);
+        }
+        umma_commit(&kv_empty[i % STAGES]);
+        umma_commit(&o_done[i & 1]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax warps 0..3 (row = TMEM lane)
+    const int r = warp * 32 + lane;
+    const int rr = rblk * ROWS + r;
+    const bool live = rr < R;
+    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    pdl_wait();  // q comes from the preceding kernel
+    if (threadIdx.x == 0) SM_STAMP(2);
+    {  // stage this row of Q into the K-major SW128 layout (two 64-column halves)
+      const uint4 *src = nullptr;
+      if (live) {
+        const int n = rr / a.G, gg = rr % a.G;
+        src = reinterpret_cast<const uint4 *>(a.q + (((long long)sl * a.Nq + n) * a.H + (long long)h * a.G + gg) * HD);
+      }
+      uint4 v[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) v[c] = live ? __ldg(src + c) : make_uint4(0, 0, 0, 0);  // all loads in flight
+      const uint32_t q_u = smem_u32(sQ);
+#pragma unroll
+      for (int c = 0; c < 16; ++c) st_shared_v4(q_u + (c >> 3) * 16384 + sw128_off(r, c), v[c].x, v[c].y, v[c].z, v[c].w);
+      fence_proxy_async();
+      mbar_arrive(q_full);
+    }
+    if (threadIdx.x == 0) SM_STAMP(3);
+    const int Nq = a.Nq;
+    const uint32_t p_u = smem_u32(sP);
+    float m_run = -INFINITY, l = 0.f;  // running max in log2 units (lazy), running sum
+    const bool warp_live = rblk * ROWS + warp * 32 < R;  // warps of padding rows only keep the handshakes
+    for (int i = 0; i < ntiles; ++i) {
+      const int sb = i & 1;
+      mbar_wait(&s_full[sb], (i >> 1) & 1);
+      tc_fence_after();
+      if (threadIdx.x == 0) {
+        if (i == 0) SM_STAMP(4);
+        if (i == ntiles - 1) SM_STAMP(5);
+      }
+      if (!warp_live) {
+        tc_fence_before();
+        mbar_arrive(&s_free[sb]);
+        mbar_arrive(&p_full[sb]);
+        continue;
+      }
+      float y[64];
+      tmem_ld32_f(lane_base + sb * KEYS, y);
+      tmem_ld32_f(lane_base + sb * KEYS + 32, y + 32);
+      tc_fence_before();
+      mbar_arrive(&s_free[sb]);
+      const int p0 = key0 + i * KEYS;
+      if (p0 + KEYS > Lc) {  // tile reaches past the prefix: visibility bitmask of its 64 keys (Eq. 2)
+        const int off = p0 - Lc;  // tree slot of key 0 (may be negative)
+        auto word = [&](int q) { return q == 0 ? anc0 : q == 1 ? anc1 : q == 2 ? anc2 : q == 3 ? anc3 : 0ull; };
+        uint64_t vis;
+        if (off < 0) {
+          vis = (~0ull >> (64 + off)) | (anc0 << (-off));  // prefix keys, then tree slots 0..
+        } else {
+          const int q = off >> 6, sh = off & 63;
+          const uint64_t lo = word(q), hi = word(q + 1);
+          vis = sh ? ((lo >> sh) | (hi << (64 - sh))) : lo;
+        }
+        if (Nq - off < 64) vis &= (Nq - off <= 0) ? 0ull : (~0ull >> (64 - (Nq - off)));
+#pragma unroll
+        for (int j = 0; j < 64; ++j) y[j] = ((vis >> j) & 1ull) ? y[j] : -INFINITY;
+      }
+      float mx0 = y[0], mx1 = y[1];
+#pragma unroll
+      for (int j = 2; j < 64; j += 2) {
+        mx0 = fmaxf(mx0, y[j]);
+        mx1 = fmaxf(mx1, y[j + 1]);
+      }
+      const float mx = fmaxf(mx0, mx1) * sl2;
+      // lazy max: raised only when a tile exceeds it by more than 2^8 (exact: l and O share the stale max)
+      float m_new = m_run, alpha = 1.f;
+      bool resc = false;
+      if (m_run == -INFINITY) {
+        m_new = mx;
+      } else if (mx > m_run + RESCALE_LOG2) {
+        m_new = mx;
+        alpha = exp2f(m_run - m_new);
+        resc = true;
+      }
+      const float nb = (m_new == -INFINITY) ? 0.f : -m_new;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+      uint32_t pk[32];
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const float e0 = ex2(fmaf(y[2 * j], sl2, nb)), e1 = ex2(fmaf(y[2 * j + 1], sl2, nb));
+        const float e2 = ex2(fmaf(y[2 * j + 2], sl2, nb)), e3 = ex2(fmaf(y[2 * j + 3], sl2, nb));
+        s0 += e0;
+        s1 += e1;
+        s2 += e2;
+        s3 += e3;
+        pk[j] = pack_bf16(e0, e1);
+        pk[j + 1] = pack_bf16(e2, e3);
+      }
+      l = l * alpha + ((s0 + s1) + (s2 + s3));
+      m_run = m_new;
+      // P buffer (i & 1) is free once PV(i-2) has completed
+      if (i >= 2) mbar_wait(&o_done[sb], ((i >> 1) - 1) & 1);
+      if (__any_sync(0xffffffffu, resc) && i > 0) {
+        mbar_wait(&o_done[sb ^ 1], ((i - 1) >> 1) & 1);  // PV(i-1) done: O is stable
+        tc_fence_after();
+#pragma unroll 1
+        for (int c0 = 0; c0 < HD; c0 += 32) {
+          float o[32];
+          tmem_ld32_f(lane_base + 2 * KEYS + c0, o);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] *= alpha;
+          tmem_st32_f(lane_base + 2 * KEYS + c0, o);
+        }
+      }
+      const uint32_t prow = p_u + sb * PB;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) st_shared_v4(prow + sw128_off(r, c), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(&p_full[sb]);
+    }
+    // final O row
+    if (ntiles > 0) {
+      mbar_wait(&o_done[(ntiles - 1) & 1], ((ntiles - 1) >> 1) & 1);
+      tc_fence_after();
+    }
+    if (threadIdx.x == 0) SM_STAMP(6);
+    const float fin_m = live ? m_run : -INFINITY, fin_l = live ? l : 0.f;
+    if (a.nsplit == 1 && live && ntiles > 0) {
+      const float inv = 1.f / l;
+      bf16 *dst = a.out + (((long long)sl * a.Nq + rr / a.G) * a.H + (long long)h * a.G + rr % a.G) * HD;
+#pragma unroll
+      for (int c0 = 0; c0 < HD; c0 += 32) {
+        float o[32];
+        tmem_ld32_f(lane_base + 2 * KEYS + c0, o);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint4 w;
+          w.x = pack_bf16(o[8 * c] * inv, o[8 * c + 1] * inv);
+          w.y = pack_bf16(o[8 * c + 2] * inv, o[8 * c + 3] * inv);
+          w.z = pack_bf16(o[8 * c + 4] * inv, o[8 * c + 5] * inv);
+          w.w = pack_bf16(o[8 * c + 6] * inv, o[8 * c + 7] * inv);
+          reinterpret_cast<uint4 *>(dst + c0)[c] = w;
+        }
+      }
+    } else if (a.nsplit > 1) {
+      // stage (m, l, O) of this split in the idle K/V ring (own MMAs and loads are complete);
+      // 16-byte chunk c of row r at chunk c ^ (r & 7): conflict-free
+      float *so = reinterpret_cast<float *>(sKV);  // [128][HD]
+      float *sml = so + ROWS * HD;                 // [128][2]
+      sml[2 * r] = fin_m;
+      sml[2 * r + 1] = fin_l;
+      if (warp_live) {  // (padding warps stage nothing: their rows are never read)
+#pragma unroll
+        for (int c0 = 0; c0 < HD; c0 += 32) {
+          float o[32];
+          if (ntiles > 0) {
+            tmem_ld32_f(lane_base + 2 * KEYS + c0, o);
+          } else {  // empty split: weight 0, but the slot must hold finite values
+#pragma unroll
+            for (int j = 0; j < 32; ++j) o[j] = 0.f;
+          }
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<float4 *>(so + r * HD + 4 * ((c0 / 4 + c) ^ (r & 7))) =
+                make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+        }
+      }
+    }
+  }
+
+  if (a.nsplit > 1) {
+    // split-KV combine over DSMEM (pull): rank q owns rows [q*rows_per, (q+1)*rows_per) of the
+    // block and reads only live rows (DSMEM moves ~20 B/clk per SM, so padding rows are skipped)
+    cluster_sync_all();
+    if (threadIdx.x == 0) SM_STAMP(8);
+    const float *so = reinterpret_cast<const float *>(sKV);
+    const float *sml = so + ROWS * HD;
+    float *swt = reinterpret_cast<float *>(sP);  // [rows_per][8] combine weights w_q / L
+    const uint32_t so_u = smem_u32(so), sml_u = smem_u32(sml);
+    const int rows_per = ROWS / a.nsplit;
+    const int lr0 = split * rows_per;
+    for (int lr = threadIdx.x; lr < rows_per; lr += blockDim.x) {
+      float mq[8], lq[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float2 v = q < a.nsplit ? ld_dsmem_f32x2(mapa_u32(sml_u + 8 * (lr0 + lr), q)) : make_float2(-INFINITY, 0.f);
+        mq[q] = v.x;
+        lq[q] = v.y;
+      }
+      float M = -INFINITY;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) M = fmaxf(M, mq[q]);
+      float wq[8], L = 0.f;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {  // fixed rank order -> deterministic
+        wq[q] = mq[q] == -INFINITY ? 0.f : exp2f(mq[q] - M);
+        L += wq[q] * lq[q];
+      }
+      const float inv = 1.f / L;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) swt[lr * 8 + q] = wq[q] * inv;
+    }
+    __syncthreads();
+    const int live_rows = max(0, min(rows_per, R - (rblk * ROWS + lr0)));
+    const int items = live_rows * (HD / 4);
+    for (int e0 = threadIdx.x; e0 < items; e0 += 2 * blockDim.x) {  // two items per pass: 2 x nsplit loads in flight
+      float4 v[2][8];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int e = min(e0 + u * (int)blockDim.x, items - 1);
+        const int lr = e / (HD / 4), c4 = e % (HD / 4);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < a.nsplit) v[u][q] = ld_dsmem_f32x4(mapa_u32(so_u + 4 * ((lr0 + lr) * HD + 4 * (c4 ^ ((lr0 + lr) & 7))), q));
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int e = e0 + u * (int)blockDim.x;
+        if (e >= items) continue;
+        const int lr = e / (HD / 4), c4 = e % (HD / 4);
+        const int row = rblk * ROWS + lr0 + lr;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (q < a.nsplit) {  // fixed rank order -> deterministic
+            const float w = swt[lr * 8 + q];
+            acc.x += w * v[u][q].x;
+            acc.y += w * v[u][q].y;
+            acc.z += w * v[u][q].z;
+            acc.w += w * v[u][q].w;
+          }
+        }
+        const int n = row / a.G, gg = row % a.G;
+        uint2 pk2;
+        pk2.x = pack_bf16(acc.x, acc.y);
+        pk2.y = pack_bf16(acc.z, acc.w);
+        *reinterpret_cast<uint2 *>(a.out + (((long long)sl * a.Nq + n) * a.H + (long long)h * a.G + gg) * HD + 4 * c4) =
+            pk2;
+      }
+    }
+    if (threadIdx.x == 0) SM_STAMP(9);
+    cluster_sync_all();  // peers may still be reading this CTA's shared memory
+    if (threadIdx.x == 0) SM_STAMP(10);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 5) tmem_dealloc<256>(tmem);
+}
+
+#ifdef SM_TRACE
+extern "C" int sm_trace_read(long long *dst, int n) {  // diagnostics build only
+  return (int)cudaMemcpyFromSymbol(dst, g_trace, sizeof(long long) * (size_t)n);
+}
+#endif
+
+int attention_tc_nsplit(int units) {  // 1 CTA per SM: aim for ~one wave of 148
+  int ns = 1;
+  while (ns < 8 && units * ns * 2 <= kNumSMs) ns *= 2;
+  return ns;
+}
+
+cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tree_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(a.nsplit, (a.Nq * a.G + tc::ROWS - 1) / tc::ROWS, a.nseq * a.Hkv);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = tc::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = gemm_pdl() ? 1 : 0;
+  attrs[1].id = cudaLaunchAttributeClusterDimension;
+  attrs[1].val.clusterDim.x = a.nsplit;
+  attrs[1].val.clusterDim.y = 1;
+  attrs[1].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = a.nsplit > 1 ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel, a);
+}
+
+}  // namespace sm

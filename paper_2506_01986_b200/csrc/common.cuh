@@ -50,6 +50,34 @@ SM_DEV float ld_dsmem_f32(uint32_t cluster_addr) {
   asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(cluster_addr) : "memory");
   return v;
 }
+SM_DEV float2 ld_dsmem_f32x2(uint32_t cluster_addr) {
+  float2 v;
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(cluster_addr) : "memory");
+  return v;
+}
+SM_DEV float4 ld_dsmem_f32x4(uint32_t cluster_addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(cluster_addr)
+               : "memory");
+  return v;
+}
+
+// Diagnostics build only (-DSM_TRACE, build(trace=True)): per-CTA clock64 stamps.
+#ifdef SM_TRACE
+constexpr int kTraceCtas = 1024, kTraceSlots = 24;
+static __device__ long long g_trace[kTraceCtas][kTraceSlots];  // per translation unit
+#define SM_STAMP(slot)                                                                           \
+  do {                                                                                           \
+    const int cta_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);             \
+    if (cta_ < kTraceCtas) g_trace[cta_][slot] = clock64();                                      \
+  } while (0)
+#else
+#define SM_STAMP(slot) \
+  do {                 \
+  } while (0)
+#endif
 
 // ------------------------------------------------------------------ mbarrier
 SM_DEV void mbar_init(uint64_t *bar, uint32_t count) {

@@ -142,8 +142,10 @@ struct AttnArgs {
   float scale_log2;           // log2(e) / sqrt(hd)
 };
 cudaError_t attention_launch(const AttnArgs &a, int head_dim, cudaStream_t st);
-int attention_row_blocks(int Nq, int G);
-int attention_nsplit(int units);  // units = row blocks * sequences * kv heads
+int attention_row_blocks(int Nq, int G, int head_dim);
+int attention_nsplit(int units, int head_dim);  // units = row blocks * sequences * kv heads
+void attention_set_splits(int n);               // experiments: force key splits (0 = auto)
+void attention_set_tc(int on);                  // head_dim 128: tcgen05 kernel (1, default) or mma.sync (0)
 
 // ---------------------------------------------------------------- GEMM consumers (epilogue.cu)
 // Every consumer waits on the producer GEMM with griddepcontrol.wait and lets

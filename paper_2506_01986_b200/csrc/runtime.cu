@@ -625,7 +625,7 @@ extern "C" sm_status sm_state_device(const sm_kv *kv, int32_t **d_root, int32_t 
 
 // ---------------------------------------------------------------- forward (a2 + a3)
 static int attn_splits(const sm_model *m, int nseq, int Nq) {
-  return attention_nsplit(nseq * m->Hkv * attention_row_blocks(Nq, m->G));
+  return attention_nsplit(nseq * m->Hkv * attention_row_blocks(Nq, m->G, m->hd), m->hd);
 }
 
 // Timing ablation (sm_set_option "ablate", experiments only -- results become
@@ -970,7 +970,7 @@ extern "C" sm_status sm_tree_attention(const sm_tree *t, const void *d_q, const 
   sm_tree *tt = const_cast<sm_tree *>(t);
   CKS(tree_upload(tt));
   const int G = n_heads / n_kv_heads;
-  const int nsplit = attention_nsplit(batch * n_kv_heads * attention_row_blocks(t->N, G));
+  const int nsplit = attention_nsplit(batch * n_kv_heads * attention_row_blocks(t->N, G, head_dim), head_dim);
   AttnArgs aa;
   std::memset(&aa, 0, sizeof(aa));
   const uint64_t rows = (uint64_t)batch * n_kv_heads * cap;
@@ -1035,6 +1035,10 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
     gemm_set_debug_mode(value);
   } else if (n == "ablate") {
     g_ablate = value;
+  } else if (n == "attn_tc") {
+    attention_set_tc(value);
+  } else if (n == "attn_splits") {
+    attention_set_splits(value);
   } else {
     return fail(SM_ERR_INVALID_ARG, "sm_set_option: unknown option " + n);
   }
@@ -1042,4 +1046,4 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
 }
 
 extern "C" const char *sm_last_error(void) { return g_err.c_str(); }
-extern "C" const char *sm_version(void) { return "specmemo-b200 0.1 (sm_100a: tcgen05 GEMM, mma.sync tree attention)"; }
+extern "C" const char *sm_version(void) { return "specmemo-b200 0.1 (sm_100a: tcgen05 GEMM and tree attention)"; }

@@ -94,12 +94,21 @@ ATTN_CASES = [
     ("sweep256_gqa", synth.SWEEP_TREES[256], None, 1, 4, 2, 64, [130], 3),
     ("chain_prefill", None, 200, 2, 4, 2, 64, [0, 65], 5),
     ("hd32", synth.V64[:31], None, 2, 4, 4, 32, [64, 63], 1),
+    # head_dim 128: 128-row blocks (tcgen05) -- several row blocks, ragged tail, 8-way split
+    ("gqa8_rows512", synth.V64, None, 2, 16, 2, 128, [700, 64], 9),
+    ("chain256_hd128", None, 256, 1, 8, 2, 128, [129], 0),
+    ("split8_long", synth.SWEEP_TREES[16], None, 1, 1, 1, 128, [4000], 2),
+    ("gqa4_v64_c2like", synth.V64, None, 2, 8, 2, 128, [1024, 1500], 0),
 ]
 
 
+@pytest.mark.parametrize("attn_tc", [1, 0], ids=["tc", "mma"])
 @pytest.mark.parametrize("case", ATTN_CASES, ids=[c[0] for c in ATTN_CASES])
-def test_tree_attention_matches_oracle(sm, case):
+def test_tree_attention_matches_oracle(sm, case, attn_tc):
     name, choices, chain, b, H, Hkv, hd, lens, extra = case
+    if attn_tc == 0 and hd != 128:
+        pytest.skip("head_dim < 128 always runs the mma.sync kernel")
+    sm.set_option("attn_tc", attn_tc)
     tree = sm.Tree(choices, topk=10) if chain is None else sm.Tree(None, chain=chain)
     N = tree.N
     cap = max(lens) + N + extra
@@ -114,6 +123,7 @@ def test_tree_attention_matches_oracle(sm, case):
     got = to64(out)
     assert np.all(np.isfinite(got))
     err = np.abs(got - ref)
+    sm.set_option("attn_tc", 1)
     assert np.all(err <= 2e-2 + 2e-2 * np.abs(ref)), float(err.max())
 
 

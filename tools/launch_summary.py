@@ -41,3 +41,10 @@ for k, (n, v, b) in sorted(agg.items(), key=lambda x: -x[1][1]):
     print(f"{k:60s} {n:4d} {v/1e3:9.1f} {100*v/tot:5.1f}% {b/1e6:9.1f} {gbs:7.0f}")
 g = [d.get(T, 0) for d in step if "gemm" in d["name"]]
 print("first layer GEMMs (us):", [round(v / 1e3, 1) for v in g[:4]], " LM/heads:", [round(v / 1e3, 1) for v in g[-3:]])
+if len(sys.argv) > 2:  # write the K2 DRAM traffic per step for bench.py's roofline.traffic
+    import json
+    gb = sum(d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0) for d in step if "gemm" in d["name"])
+    gn = sum(1 for d in step if "gemm" in d["name"])
+    json.dump({"dram_bytes_per_step": gb, "gemm_launches_per_step": gn, "source": path,
+               "note": "ncu launch list, default cache control (caches flushed per launch): upper bound"},
+              open(sys.argv[2], "w"), indent=1)
