@@ -52,55 +52,63 @@ cudaError_t embed_launch(const int32_t *tok, const bf16 *E, float *x, int M, int
 }
 
 // ------------------------------------------------------------------ residual + RMSNorm
-constexpr int kNormThreads = 512;
+// One row per cluster of CS = ceil(d / 1024) CTAs of 256 threads, one float4 per thread:
+// every partial of the row is requested in one round trip; the row's sum of squares is
+// exchanged by pushing each CTA's block sum into every peer's shared memory.
+constexpr int kNormThreads = 256;
+constexpr int kNormCols = 4 * kNormThreads;
 __global__ void __launch_bounds__(kNormThreads) resid_norm_kernel(PartialView pv, int has_pv, float *x, const bf16 *g,
                                                                   bf16 *h, int d, float eps) {
-  __shared__ float red[32];
+  __shared__ float red[kNormThreads / 32];
+  __shared__ float ssq[8];  // ssq[q] = block sum of cluster rank q
   pdl_trigger();
+  cluster_arrive_relaxed();  // phase 1: every CTA of the cluster has started (before any DSMEM store)
   pdl_wait();
-  const int m = blockIdx.x;
+  const int m = blockIdx.y, rank = blockIdx.x, cs = gridDim.x;
+  const int i = rank * kNormCols + threadIdx.x * 4;
   float *xr = x + (size_t)m * d;
-  float4 v[4];  // d <= 4 * 4 * kNormThreads = 8192
-  float ss = 0.f;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int i = (threadIdx.x + k * kNormThreads) * 4;
-    v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (i < d) {
-      float4 a = *reinterpret_cast<float4 *>(xr + i);
-      if (has_pv) {
-        const float4 y = sk_sum4(pv, 0, m, i);  // R5/R7: fp32 residual += fp32 projection
-        a.x += y.x;
-        a.y += y.y;
-        a.z += y.z;
-        a.w += y.w;
-        *reinterpret_cast<float4 *>(xr + i) = a;
-      }
-      v[k] = a;
-      ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (i < d) {
+    float4 ys[16];
+    SkRef ref{};
+    if (has_pv) {
+      ref = sk_ref(pv, 0, m, i);
+      sk_load<16>(ref, ys);
+    }
+    a = *reinterpret_cast<const float4 *>(xr + i);
+    if (has_pv) {
+      const float4 y = sk_reduce<16>(ref, ys);  // R5/R7: fp32 residual += fp32 projection
+      a.x += y.x;
+      a.y += y.y;
+      a.z += y.z;
+      a.w += y.w;
+      *reinterpret_cast<float4 *>(xr + i) = a;
     }
   }
-  ss = block_sum<kNormThreads>(ss, red);
+  float ss = block_sum<kNormThreads>(a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w, red);
+  cluster_wait();
+  if (threadIdx.x < cs) st_dsmem_f32(mapa_u32(smem_u32(&ssq[rank]), threadIdx.x), ss);
+  cluster_sync_all();  // phase 2: all block sums delivered
+  ss = 0.f;
+  for (int q = 0; q < cs; ++q) ss += ssq[q];  // same order in every CTA of the cluster
   const float rs = 1.0f / sqrtf(ss / (float)d + eps);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int i = (threadIdx.x + k * kNormThreads) * 4;
-    if (i < d) {
-      const __nv_bfloat162 g01 = *reinterpret_cast<const __nv_bfloat162 *>(g + i);
-      const __nv_bfloat162 g23 = *reinterpret_cast<const __nv_bfloat162 *>(g + i + 2);
-      uint2 o;
-      o.x = pack_bf16(v[k].x * rs * __low2float(g01), v[k].y * rs * __high2float(g01));
-      o.y = pack_bf16(v[k].z * rs * __low2float(g23), v[k].w * rs * __high2float(g23));
-      *reinterpret_cast<uint2 *>(h + (size_t)m * d + i) = o;
-    }
+  if (i < d) {
+    const __nv_bfloat162 g01 = *reinterpret_cast<const __nv_bfloat162 *>(g + i);
+    const __nv_bfloat162 g23 = *reinterpret_cast<const __nv_bfloat162 *>(g + i + 2);
+    uint2 o;
+    o.x = pack_bf16(a.x * rs * __low2float(g01), a.y * rs * __high2float(g01));
+    o.y = pack_bf16(a.z * rs * __low2float(g23), a.w * rs * __high2float(g23));
+    *reinterpret_cast<uint2 *>(h + (size_t)m * d + i) = o;
   }
 }
 cudaError_t resid_norm_launch(const PartialView *pv, float *x, const bf16 *g, bf16 *h, int M, int d, float eps,
                               cudaStream_t st) {
-  if (d > 16 * kNormThreads || d % 4) return cudaErrorInvalidValue;
+  const int cs = (d + kNormCols - 1) / kNormCols;
+  if (cs > 8 || d % 4) return cudaErrorInvalidValue;
   PartialView v{};
   if (pv) v = *pv;
-  return launch_pdl(resid_norm_kernel, dim3(M), dim3(kNormThreads), 0, st, v, pv ? 1 : 0, x, g, h, d, eps);
+  return launch_pdl_cluster(resid_norm_kernel, dim3(cs, M), dim3(kNormThreads), 0, st, cs, v, pv ? 1 : 0, x, g, h, d,
+                            eps);
 }
 
 // ------------------------------------------------------------------ QKV consumer (RoPE + cache write)
@@ -116,8 +124,12 @@ __global__ void __launch_bounds__(256) qkv_consumer_kernel(PartialView pv, RowCt
   if (idx >= (H + 2 * Hkv) * quads) return;
   const int hh = idx / quads, c = (idx % quads) * 4;
   const int n0 = hh * hd + c;
-  const float4 a = sk_sum4(pv, 0, m, n0);
-  const float4 b = sk_sum4(pv, 0, m, n0 + half);
+  const SkRef ra = sk_ref(pv, 0, m, n0), rb = sk_ref(pv, 0, m, n0 + half);
+  float4 xa[8], xb[8];
+  sk_load<8>(ra, xa);
+  sk_load<8>(rb, xb);
+  const float4 a = sk_reduce<8>(ra, xa);
+  const float4 b = sk_reduce<8>(rb, xb);
   float x0[4] = {a.x, a.y, a.z, a.w}, x1[4] = {b.x, b.y, b.z, b.w};
   const int sl = m / rc.Nq, node = m % rc.Nq;
   const int seq = rc.seq_base + sl;
@@ -165,8 +177,12 @@ __global__ void __launch_bounds__(256) silu_consumer_kernel(PartialView pv, int 
   const int f = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (f >= F) return;
   const int ng = (f >> 6) * 128 + (f & 63);
-  const float4 g = sk_sum4(pv, 0, m, ng);
-  const float4 u = sk_sum4(pv, 0, m, ng + 64);
+  const SkRef rg = sk_ref(pv, 0, m, ng), ru = sk_ref(pv, 0, m, ng + 64);
+  float4 xg[8], xu[8];
+  sk_load<8>(rg, xg);
+  sk_load<8>(ru, xu);
+  const float4 g = sk_reduce<8>(rg, xg);
+  const float4 u = sk_reduce<8>(ru, xu);
   const float gg[4] = {g.x, g.y, g.z, g.w}, uu[4] = {u.x, u.y, u.z, u.w};
   float o[4];
 #pragma unroll

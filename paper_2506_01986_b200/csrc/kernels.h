@@ -85,6 +85,52 @@ __device__ inline float4 sk_sum4(const PartialView &v, int bi, int m, int n) {
   }
   return acc;
 }
+// Split form of sk_sum4 for consumers that need several sums: sk_ref locates the
+// contributors, sk_load issues up to NMAX loads at once, sk_reduce adds them (and any
+// beyond NMAX) in contributor order -- the same order as sk_sum4, so identical results.
+struct SkRef {
+  const float4 *base;
+  size_t stride;  // float4 between contributors
+  int nc;
+};
+__device__ inline SkRef sk_ref(const PartialView &v, int bi, int m, int n) {
+  const SplitPlan &p = v.plan;
+  const int tt = m / p.bn, mt = n >> 7;
+  const int t = sk_tile_of(p, bi, tt, mt);
+  const int cf = sk_cta_of((long long)t * p.kb_total, p), cl = sk_cta_of((long long)(t + 1) * p.kb_total - 1, p);
+  SkRef r;
+  r.nc = cl - cf + 1;
+  r.base = reinterpret_cast<const float4 *>(v.ws + (size_t)t * p.maxc * p.bn * 128 + (size_t)(m - tt * p.bn) * 128 +
+                                            (n & 127));
+  r.stride = (size_t)p.bn * 128 / 4;
+  return r;
+}
+template <int NMAX>
+__device__ inline void sk_load(const SkRef &r, float4 (&x)[NMAX]) {
+#pragma unroll
+  for (int k = 0; k < NMAX; ++k) x[k] = (k < r.nc) ? __ldcg(r.base + k * r.stride) : make_float4(0.f, 0.f, 0.f, 0.f);
+}
+template <int NMAX>
+__device__ inline float4 sk_reduce(const SkRef &r, const float4 (&x)[NMAX]) {
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < NMAX; ++k) {
+    if (k < r.nc) {
+      acc.x += x[k].x;
+      acc.y += x[k].y;
+      acc.z += x[k].z;
+      acc.w += x[k].w;
+    }
+  }
+  for (int k = NMAX; k < r.nc; ++k) {
+    const float4 y = __ldcg(r.base + k * r.stride);
+    acc.x += y.x;
+    acc.y += y.y;
+    acc.z += y.z;
+    acc.w += y.w;
+  }
+  return acc;
+}
 __device__ inline float sk_sum1(const PartialView &v, int bi, int m, int n) {
   const SplitPlan &p = v.plan;
   const int tt = m / p.bn, mt = n >> 7;
@@ -212,7 +258,7 @@ cudaError_t set_root_launch(int32_t *root, int seq, const int32_t *argmax_row, c
 cudaError_t generate_bf16_launch(void *dst, size_t numel, uint64_t seed, uint64_t stream_id, uint64_t start, int mode,
                                  cudaStream_t st);
 
-// ---------------------------------------------------------------- PDL launch helper
+// ---------------------------------------------------------------- PDL launch helpers
 // Launch with programmatic stream serialization when enabled (gemm_pdl()).
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -227,6 +273,26 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   attr[0].val.programmaticStreamSerializationAllowed = gemm_pdl() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+// Same, with a (cx, 1, 1) thread-block cluster.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                      int cx, Args &&...args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = gemm_pdl() ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = cx;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
