@@ -8,8 +8,11 @@ Llama + 4 Medusa-1 heads, the 64-node / 42-leaf Medusa tree, batch 1, KV cache
 bounded to x = 2048 (+64 tree-scratch slots), greedy acceptance.  One step = one
 full pass a1..a5 (propose, verify forward of 64 nodes through 32 layers + LM
 head, acceptance, compaction, heads + top-k) = one sm_step graph replay.
-Under torchrun (N>1) every rank runs an independent replica (the bs=1 7B path
-does not shard; TP for the 70B config is not built yet): "scaling": "weak".
+Under torchrun (N>1): the bs=1 configs (C1-C3) run one independent replica per
+rank ("scaling": "weak"; the bs=1 7B/13B step does not need to shard); C4 (70B
+shape, bs=10) runs tensor-parallel over the N ranks ("scaling": "strong": the
+same 10 sequences, 1/N of the weights and kv heads per GPU), exchanging through
+peer memory (CUDA IPC handles swapped over torch.distributed).
 
 Prints ONE JSON line (rank 0).  --impl reference times the CPU oracle
 (oracle/, numpy fp64) on the host cores on a bounded sample of the same step.
@@ -132,6 +135,22 @@ def barrier(world: int):
         dist.barrier()
 
 
+def exchange_handles(handle: bytes, world: int) -> list:
+    """All ranks' opaque handles, indexed by rank (torch.distributed plumbing)."""
+    if world == 1:
+        return [handle]
+    import torch.distributed as dist
+    out = [None] * world
+    dist.all_gather_object(out, handle)
+    return out
+
+
+def peer_syms(sm, sym, world: int, rank: int) -> list:
+    """Device pointers of every rank's symmetric TP buffer, mapped in this process."""
+    hs = exchange_handles(sm.ipc_handle(sym), world)
+    return [sym.data_ptr() if q == rank else sm.ipc_open(hs[q]) for q in range(world)]
+
+
 # ------------------------------------------------------------------ algorithmic work of one C2 step
 def step_bytes(cfg: dict, N: int, Lc: float, b: int = 1, n_medusa: int = N_MEDUSA, tau: float = 1.0) -> float:
     """weights (layers + LM head + heads) + KV read + tree KV write + compaction."""
@@ -164,20 +183,32 @@ WORKLOADS = {
                desc="C3: Vicuna-13B-shaped + 4 Medusa heads, V64 tree, bs=1, mid-conversation of an 8-turn "
                     "MT-Bench-length chat (KV bounded to 2304 = sum of turns), typical acceptance T=0.7 eps=0.09 "
                     "alpha=0.3"),
-    "c4": dict(model="llama70b", n_medusa=3, tree="TINY16", batch=10, x=416, mode="greedy",
+    "c4": dict(model="llama70b", n_medusa=3, tree="TINY16", batch=10, x=416, mode="greedy", tp=True,
                desc="C4: Llama-2-70B-shaped (GQA 64/8) + 3 Medusa heads, 16-node tree, bs=10 ragged prompts of "
-                    "32-160 tokens + 256 new, KV bounded to 416 (+16), greedy, TP1 (one B200, 140 GB of weights)"),
+                    "32-160 tokens + 256 new, KV bounded to 416 (+16), greedy; tensor parallel over the N GPUs (TP1 = one "
+                    "B200 holding all 140 GB of weights)"),
 }
 
 
-def build_workload(sm, wl: dict, args, rank: int):
+def build_workload(sm, wl: dict, args, rank: int, world: int = 1, tp: int = 1):
+    """tp > 1: rank `rank` of a tensor-parallel group of `tp` = world ranks (same
+    seed everywhere: the shards tile one model); else an independent replica."""
     import torch
     cfg = synth.model_cfg(wl["model"])
     choices = {"V64": synth.V64, "TINY16": synth.TINY16}[wl["tree"]]
     tree = sm.Tree(choices, topk=synth.TOPK)
-    W = sm.allocate_weights(cfg, wl["n_medusa"], seed=args.seed + rank)
     b, x = wl["batch"], wl["x"]
-    model = sm.Model(cfg, W, max_rows=max(b * tree.N, 256), max_batch=b, max_seq_len=x + tree.N)
+    R = max(b * tree.N, 256)
+    peers = None
+    if tp > 1:
+        W = sm.allocate_weights(cfg, wl["n_medusa"], seed=args.seed, tp_rank=rank, tp_size=tp)
+        sym = torch.zeros(sm.tp_sym_bytes(cfg, R, b, wl["n_medusa"]), dtype=torch.uint8, device="cuda")
+        W["_sym"] = sym  # keep alive with the weights
+        peers = peer_syms(sm, sym, world, rank)
+    else:
+        W = sm.allocate_weights(cfg, wl["n_medusa"], seed=args.seed + rank)
+    model = sm.Model(cfg, W, max_rows=R, max_batch=b, max_seq_len=x + tree.N, peer_sym=peers)
+    barrier(world)  # every rank's model exists (its buffer zeroed) before any exchange
     kv = sm.KVCache(model, tree, b, x)
     total_steps = args.warmup + args.steps + args.prof_steps + args.e2e_steps + 8
     if b == 1:
@@ -185,7 +216,7 @@ def build_workload(sm, wl: dict, args, rank: int):
             lc_start = wl["prompt"]
         else:
             lc_start = max(128, min(args.lc_start, x - 5 * total_steps - 8))
-        prompts = [synth.prompt_tokens(args.seed, rank, lc_start, cfg["vocab"])]
+        prompts = [synth.prompt_tokens(args.seed, rank if tp == 1 else 0, lc_start, cfg["vocab"])]
     else:  # ragged MT-Bench-length prompts (32 + h mod 129)
         prompts = [synth.prompt_tokens(args.seed, i, synth.prompt_length(args.seed, i), cfg["vocab"]) for i in range(b)]
         lc_start = int(np.mean([len(p) for p in prompts]))
@@ -205,7 +236,8 @@ def run_ours(args, world, rank, local) -> dict | None:
         k, v = kv_opt.split("=")
         sm.lib().sm_set_option(k.encode(), int(v))
     wl = WORKLOADS[args.config]
-    cfg, tree, model, kv, mode, lc_start = build_workload(sm, wl, args, rank)
+    tp = world if (wl.get("tp") and world > 1) else 1
+    cfg, tree, model, kv, mode, lc_start = build_workload(sm, wl, args, rank, world, tp)
     N, l, b = tree.N, tree.depth, kv.batch
     out = sm.AcceptOut(b, l)
     acfg = sm.accept_cfg(mode)
@@ -231,7 +263,8 @@ def run_ours(args, world, rank, local) -> dict | None:
     ms = ev0.elapsed_time(ev1)
     L1 = kv.lengths().astype(np.int64)
     ms_max = reduce_max(ms, world)
-    tokens = reduce_sum(float((L1 - L0).sum()), world)
+    # replicas: every rank's tokens count; tensor parallel: the group emits one stream
+    tokens = reduce_sum(float((L1 - L0).sum()), world) if tp == 1 else float((L1 - L0).sum())
     value = tokens / (ms_max / 1e3)
     tau = float((L1 - L0).sum()) / args.steps / b
     launches = kv.step_launches()
@@ -278,7 +311,7 @@ def run_ours(args, world, rank, local) -> dict | None:
     e1.record(st)
     torch.cuda.synchronize()
     e_ms = reduce_max(e0.elapsed_time(e1), world)
-    e2e_val = reduce_sum(e2e_tokens, world) / (e_ms / 1e3)
+    e2e_val = (reduce_sum(e2e_tokens, world) if tp == 1 else e2e_tokens) / (e_ms / 1e3)
 
     # ---- K1 tree-attention point of the C5 sweep (geometry A, N=64)
     k1 = run_k1_point(sm, args) if args.k1 and args.config == "c2" else None
@@ -288,15 +321,18 @@ def run_ours(args, world, rank, local) -> dict | None:
     pk = peaks()
     gemm_gbs = gemm_bytes / (gemm_ms / 1e3) / 1e9
     lc_mean = float((L0 + L1).mean() / 2)
-    sb = step_bytes(cfg, N, lc_mean, b=b, n_medusa=wl["n_medusa"], tau=tau)
+    sb = step_bytes(cfg, N, lc_mean, b=b, n_medusa=wl["n_medusa"], tau=tau) / tp  # per GPU
     ms_step = ms_max / args.steps
     res = {
         "metric": METRIC, "value": round(value, 3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+        "scaling": "strong" if tp > 1 else "weak",
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic: counter-hash random-init weights (std 0.02), counter-hash prompt tokens",
-        "config": {"workload": wl["desc"], "global_batch": world * b, "seq_len": wl["x"], "lc_start": lc_start,
-                   "lc_mean": lc_mean, "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+        "config": {"workload": wl["desc"], "global_batch": b if tp > 1 else world * b, "seq_len": wl["x"],
+                   "lc_start": lc_start, "lc_mean": lc_mean,
+                   "parallelism": f"tp{tp} (peer-memory exchanges)" if tp > 1 else
+                   (f"replicas x{world}" if world > 1 else "single GPU"),
                    "l2": f"inputs larger than L2: {sb / 1e9:.1f} GB streamed every step (L2 126 MB)"},
         "tau": round(tau, 4), "steps_per_s": round(args.steps / (ms_max / 1e3), 3),
         "roofline": {"kernel": f"K2 tcgen05 GEMM (all {g_n} weight GEMM launches of one step)", "bound": "hbm",

@@ -92,12 +92,46 @@ typedef struct {
   const void *const *medusa_R, *const *medusa_b, *const *medusa_U;  /* [d][d], [d], [V][d]             */
 } sm_weights;
 
-/* Tensor-parallel placement (north star: TP over NVLink, all-reduce after
- * o_proj and down_proj).  tp_size must be 1 in this build (else UNSUPPORTED). */
+/* ------------------------------------------------------------------ tensor parallelism (a7, e)
+ * North star: TP over NVLink for C4 (SURVEY §8 rows a7 / e).  Rank r of t owns
+ * q heads [r*H/t, (r+1)*H/t), kv heads [r*Hkv/t, ...), FFN features
+ * [r*F/t, ...) and vocabulary rows [r*V/t, ...) (Megatron-style placement; the
+ * paper itself splits layers instead).  sm_weights then holds SHARDS:
+ *   wqkv     [(H/t + 2 Hkv/t) hd][d]  rows of the rank's q heads, then k, then v heads
+ *   wo       [d][H/t hd]              the rank's columns of the full [d][H hd]
+ *   wgate_up [2F/t][d]                the rank's features, 64-row gate/up interleave as above
+ *   wdown    [d][F/t]                 the rank's columns of the full [d][F]
+ *   lm_head, medusa_U [V/t][d]        the rank's vocabulary rows
+ *   embed, norms, medusa_R, medusa_b  full (replicated)
+ * Exchanges (all inside the library's kernels, no NCCL): the residual all-reduce
+ * after o_proj and down_proj is fused into the residual+RMSNorm consumer (each rank
+ * reduces its own split-K partials, publishes the fp32 row slice in its symmetric
+ * buffer, and sums all ranks' slices in rank order, so every rank holds bitwise
+ * the same residual); the LM head's (argmax, max, m, s, t, candidate logit) and
+ * the heads' top-K candidates are merged across ranks by (value desc, index asc).
+ * Synchronisation: per-CTA epoch flags written with st.release.sys into every
+ * peer's buffer and polled with ld.acquire.sys; a wait that exceeds ~10 s sets the
+ * flag read by sm_tp_status and continues (results then invalid).
+ * peer_sym[q] = rank q's symmetric buffer (sm_tp_sym_bytes bytes, caller-owned;
+ * sm_model_create zero-fills the rank's own, so every rank must have returned from
+ * sm_model_create before any rank issues work) as a device pointer usable on this rank's
+ * device: cudaIpcOpenMemHandle across processes (sm_ipc_*), or the plain pointer
+ * when several ranks share one device in one process (tests).  All ranks must
+ * issue the same sequence of prefill / propose / verify / accept / step calls. */
+#define SM_MAX_TP 8
 typedef struct {
-  int tp_rank, tp_size;
-  unsigned char nccl_id[128];
+  int tp_rank, tp_size;          /* tp_size in {1, 2, 4, 8}; divides H, Hkv, F/64 and V/4   */
+  void *peer_sym[SM_MAX_TP];     /* [tp_size] device pointers, [tp_rank] = this rank's own   */
 } sm_dist;
+/* Bytes of one rank's symmetric exchange buffer for cfg (max_rows, max_batch). */
+sm_status sm_tp_sym_bytes(const sm_model_cfg *cfg, size_t *bytes);
+/* *timed_out = 1 if any exchange wait of this model gave up (synchronises).    */
+sm_status sm_tp_status(const sm_model *m, int *timed_out);
+/* CUDA IPC plumbing for multi-process TP: 64-byte handle of a cudaMalloc'd
+ * device buffer, and its mapping in this process (close with sm_ipc_close).   */
+sm_status sm_ipc_get_handle(const void *d_ptr, unsigned char handle[64]);
+sm_status sm_ipc_open(const unsigned char handle[64], void **d_ptr);
+sm_status sm_ipc_close(void *d_ptr);
 
 sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *w, const sm_dist *dist, sm_model **out);
 void sm_model_destroy(sm_model *m);
@@ -108,6 +142,10 @@ void sm_model_destroy(sm_model *m);
  * four 16-bit uniforms, for the K1 sweep), mode 0 = the weight law above.     */
 sm_status sm_generate_bf16(void *d_dst, size_t numel, uint64_t seed, uint64_t stream_id, uint64_t start, int mode,
                            void *stream);
+/* Block [rows][cols] of the full [*][full_cols] matrix of that stream, starting at
+ * (row0, col0): dst[i][j] = w[(row0 + i) * full_cols + col0 + j] (TP column shards). */
+sm_status sm_generate_bf16_2d(void *d_dst, int rows, int cols, int full_cols, int row0, int col0, uint64_t seed,
+                              uint64_t stream_id, int mode, void *stream);
 
 /* ------------------------------------------------------------------ bounded KV cache
  * Eq. 1 with d restored (reading Q14): bytes =

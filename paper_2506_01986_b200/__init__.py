@@ -73,8 +73,11 @@ class Weights(ctypes.Structure):
                                    "medusa_R", "medusa_b", "medusa_U")]
 
 
+MAX_TP = 8
+
+
 class Dist(ctypes.Structure):
-    _fields_ = [("tp_rank", ctypes.c_int), ("tp_size", ctypes.c_int), ("nccl_id", ctypes.c_ubyte * 128)]
+    _fields_ = [("tp_rank", ctypes.c_int), ("tp_size", ctypes.c_int), ("peer_sym", ctypes.c_void_p * MAX_TP)]
 
 
 class AcceptCfg(ctypes.Structure):
@@ -136,6 +139,61 @@ class Tree:
             _lib.sm_tree_destroy(self._h)
 
 
+# ------------------------------------------------------------------ tensor-parallel placement (host logic)
+def tp_shard(cfg: dict, rank: int, t: int) -> dict:
+    """Which rows / columns of each full weight rank `rank` of `t` holds
+    (include/specmemo.h, sm_dist): half-open ranges in the full matrices."""
+    d, H, Hkv, hd, F, V = (cfg[k] for k in ("d_model", "n_heads", "n_kv_heads", "head_dim", "d_ffn", "vocab"))
+    if t not in (1, 2, 4, 8) or not 0 <= rank < t:
+        raise ValueError("tp_size must be 1, 2, 4 or 8 and 0 <= rank < tp_size")
+    if H % t or Hkv % t or F % (64 * t) or V % (4 * t):
+        raise ValueError("tp_size must divide n_heads, n_kv_heads, d_ffn/64 and vocab/4")
+    Hl, Hkvl, Fl, Vl = H // t, Hkv // t, F // t, V // t
+    return dict(
+        q_rows=(rank * Hl * hd, (rank + 1) * Hl * hd),                # of wq [H hd][d]
+        k_rows=(rank * Hkvl * hd, (rank + 1) * Hkvl * hd),            # of wk [Hkv hd][d]
+        v_rows=(rank * Hkvl * hd, (rank + 1) * Hkvl * hd),            # of wv
+        o_cols=(rank * Hl * hd, (rank + 1) * Hl * hd),                # of wo [d][H hd]
+        ffn=(rank * Fl, (rank + 1) * Fl),                             # gate/up rows, down columns
+        vocab=(rank * Vl, (rank + 1) * Vl),                           # lm_head / medusa_U rows
+        H=Hl, Hkv=Hkvl, F=Fl, V=Vl)
+
+
+def generate_bf16_2d(t, full_cols: int, row0: int, col0: int, seed: int, stream_id: int, mode: int = 0,
+                     stream=None) -> None:
+    """t[i][j] = w[(row0 + i) * full_cols + col0 + j] of that stream (column shards)."""
+    rows, cols = t.shape
+    _check(lib().sm_generate_bf16_2d(ctypes.c_void_p(_ptr(t)), ctypes.c_int(rows), ctypes.c_int(cols),
+                                     ctypes.c_int(full_cols), ctypes.c_int(row0), ctypes.c_int(col0),
+                                     ctypes.c_uint64(seed), ctypes.c_uint64(stream_id), ctypes.c_int(mode),
+                                     ctypes.c_void_p(_stream(stream))))
+
+
+def tp_sym_bytes(cfg: dict, max_rows: int, max_batch: int, n_medusa: int) -> int:
+    c = ModelCfg(cfg["n_layers"], cfg["d_model"], cfg["n_heads"], cfg["n_kv_heads"], cfg["head_dim"], cfg["d_ffn"],
+                 cfg["vocab"], n_medusa, cfg.get("rms_eps", 1e-5), cfg.get("rope_theta", 1e4), max_rows, max_batch, 1)
+    n = ctypes.c_size_t()
+    _check(lib().sm_tp_sym_bytes(ctypes.byref(c), ctypes.byref(n)))
+    return n.value
+
+
+def ipc_handle(t) -> bytes:
+    h = (ctypes.c_ubyte * 64)()
+    _check(lib().sm_ipc_get_handle(ctypes.c_void_p(_ptr(t)), h))
+    return bytes(h)
+
+
+def ipc_open(handle: bytes) -> int:
+    h = (ctypes.c_ubyte * 64)(*handle)
+    p = ctypes.c_void_p()
+    _check(lib().sm_ipc_open(h, ctypes.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(ptr: int) -> None:
+    _check(lib().sm_ipc_close(ctypes.c_void_p(ptr)))
+
+
 # ------------------------------------------------------------------ weights (device generator)
 def generate_bf16(t, seed: int, stream_id: int, start: int = 0, mode: int = 0, stream=None) -> None:
     """Fill a bf16 CUDA tensor with the counter-hash law (synth.weight_bits /
@@ -145,36 +203,45 @@ def generate_bf16(t, seed: int, stream_id: int, start: int = 0, mode: int = 0, s
                                   ctypes.c_void_p(_stream(stream))))
 
 
-def allocate_weights(cfg: dict, n_medusa: int, seed: int = 0, medusa_init: bool = False, device="cuda") -> dict:
+def allocate_weights(cfg: dict, n_medusa: int, seed: int = 0, medusa_init: bool = False, device="cuda",
+                     tp_rank: int = 0, tp_size: int = 1) -> dict:
     """Random-init bf16 weights of a Llama + Medusa-1 model, generated on the GPU
-    with the same streams as the oracle (synth stream registry)."""
+    with the same streams as the oracle (synth stream registry).  tp_size > 1:
+    the shard of rank tp_rank (tp_shard), generated in place from the full-matrix
+    counter indices, so the shards of all ranks tile the tp_size = 1 weights."""
     import torch
 
     import synth
     d, H, Hkv, hd, F, V, L = (cfg[k] for k in ("d_model", "n_heads", "n_kv_heads", "head_dim", "d_ffn", "vocab",
                                                 "n_layers"))
+    sh = tp_shard(cfg, tp_rank, tp_size)
+    Hl, Hkvl, Fl, Vl = sh["H"], sh["Hkv"], sh["F"], sh["V"]
     bf = torch.bfloat16
-    W = {"embed": torch.empty(V, d, dtype=bf, device=device), "lm_head": torch.empty(V, d, dtype=bf, device=device),
-         "final_norm": torch.ones(d, dtype=bf, device=device), "layers": [], "medusa": []}
+
+    def rows(dst, stream_id, r0):  # rows [r0, r0 + len) of a [*][d] matrix
+        generate_bf16(dst, seed, stream_id, start=r0 * dst.shape[1])
+
+    W = {"embed": torch.empty(V, d, dtype=bf, device=device), "lm_head": torch.empty(Vl, d, dtype=bf, device=device),
+         "final_norm": torch.ones(d, dtype=bf, device=device), "layers": [], "medusa": [], "tp": (tp_rank, tp_size)}
     generate_bf16(W["embed"], seed, synth.STREAM_EMBED)
-    generate_bf16(W["lm_head"], seed, synth.STREAM_LM_HEAD)
+    rows(W["lm_head"], synth.STREAM_LM_HEAD, sh["vocab"][0])
     for li in range(L):
-        wqkv = torch.empty((H + 2 * Hkv) * hd, d, dtype=bf, device=device)
-        generate_bf16(wqkv[: H * hd], seed, synth.stream_layer(li, "wq"))
-        generate_bf16(wqkv[H * hd:(H + Hkv) * hd], seed, synth.stream_layer(li, "wk"))
-        generate_bf16(wqkv[(H + Hkv) * hd:], seed, synth.stream_layer(li, "wv"))
-        wo = torch.empty(d, H * hd, dtype=bf, device=device)
-        generate_bf16(wo, seed, synth.stream_layer(li, "wo"))
+        wqkv = torch.empty((Hl + 2 * Hkvl) * hd, d, dtype=bf, device=device)
+        rows(wqkv[: Hl * hd], synth.stream_layer(li, "wq"), sh["q_rows"][0])
+        rows(wqkv[Hl * hd:(Hl + Hkvl) * hd], synth.stream_layer(li, "wk"), sh["k_rows"][0])
+        rows(wqkv[(Hl + Hkvl) * hd:], synth.stream_layer(li, "wv"), sh["v_rows"][0])
+        wo = torch.empty(d, Hl * hd, dtype=bf, device=device)
+        generate_bf16_2d(wo, H * hd, 0, sh["o_cols"][0], seed, synth.stream_layer(li, "wo"))
         # gate/up fused with rows interleaved per 64: [g0..g63, u0..u63, g64..] so one
         # 128-row GEMM tile holds matching gate and up features (SiLU*mul epilogue)
-        g = torch.empty(F, d, dtype=bf, device=device)
-        u = torch.empty(F, d, dtype=bf, device=device)
-        generate_bf16(g, seed, synth.stream_layer(li, "wg"))
-        generate_bf16(u, seed, synth.stream_layer(li, "wu"))
-        wgu = torch.stack([g.view(F // 64, 64, d), u.view(F // 64, 64, d)], dim=1).reshape(2 * F, d).contiguous()
+        g = torch.empty(Fl, d, dtype=bf, device=device)
+        u = torch.empty(Fl, d, dtype=bf, device=device)
+        rows(g, synth.stream_layer(li, "wg"), sh["ffn"][0])
+        rows(u, synth.stream_layer(li, "wu"), sh["ffn"][0])
+        wgu = torch.stack([g.view(Fl // 64, 64, d), u.view(Fl // 64, 64, d)], dim=1).reshape(2 * Fl, d).contiguous()
         del g, u
-        wd = torch.empty(d, F, dtype=bf, device=device)
-        generate_bf16(wd, seed, synth.stream_layer(li, "wd"))
+        wd = torch.empty(d, Fl, dtype=bf, device=device)
+        generate_bf16_2d(wd, F, 0, sh["ffn"][0], seed, synth.stream_layer(li, "wd"))
         W["layers"].append(dict(attn_norm=torch.ones(d, dtype=bf, device=device), wqkv=wqkv, wo=wo,
                                 mlp_norm=torch.ones(d, dtype=bf, device=device), wgate_up=wgu, wdown=wd))
     for i in range(n_medusa):
@@ -184,8 +251,8 @@ def allocate_weights(cfg: dict, n_medusa: int, seed: int = 0, medusa_init: bool 
         else:
             R = torch.empty(d, d, dtype=bf, device=device)
             generate_bf16(R, seed, synth.stream_medusa(i, "R"))
-            U = torch.empty(V, d, dtype=bf, device=device)
-            generate_bf16(U, seed, synth.stream_medusa(i, "U"))
+            U = torch.empty(Vl, d, dtype=bf, device=device)
+            rows(U, synth.stream_medusa(i, "U"), sh["vocab"][0])
         W["medusa"].append(dict(R=R, b=torch.zeros(d, dtype=bf, device=device), U=U))
     return W
 
@@ -199,7 +266,13 @@ def weights_bytes(cfg: dict, n_medusa: int) -> int:
 
 # ------------------------------------------------------------------ model / kv
 class Model:
-    def __init__(self, cfg: dict, weights: dict, max_rows: int, max_batch: int, max_seq_len: int):
+    """sm_model over borrowed weights.  Tensor parallel: pass the rank's shard
+    (allocate_weights(..., tp_rank, tp_size)) and peer_sym = every rank's
+    symmetric buffer (tp_sym_bytes) as device pointers usable here; all ranks must
+    be constructed before any rank issues work."""
+
+    def __init__(self, cfg: dict, weights: dict, max_rows: int, max_batch: int, max_seq_len: int,
+                 peer_sym: list | None = None):
         c = ModelCfg(cfg["n_layers"], cfg["d_model"], cfg["n_heads"], cfg["n_kv_heads"], cfg["head_dim"],
                      cfg["d_ffn"], cfg["vocab"], len(weights["medusa"]), cfg.get("rms_eps", 1e-5),
                      cfg.get("rope_theta", 1e4), max_rows, max_batch, max_seq_len)
@@ -214,7 +287,22 @@ class Model:
         self._h = ctypes.c_void_p()
         self.cfg, self.c = cfg, c
         self.weights = weights          # keep borrowed memory alive
-        _check(lib().sm_model_create(ctypes.byref(c), ctypes.byref(w), None, ctypes.byref(self._h)))
+        tp_rank, tp_size = weights.get("tp", (0, 1))
+        self.tp_rank, self.tp_size = tp_rank, tp_size
+        dist = None
+        if tp_size > 1:
+            if peer_sym is None or len(peer_sym) != tp_size:
+                raise ValueError("tensor parallel model needs peer_sym for every rank")
+            dist = Dist(tp_rank, tp_size)
+            for q, p in enumerate(peer_sym):
+                dist.peer_sym[q] = p
+        _check(lib().sm_model_create(ctypes.byref(c), ctypes.byref(w), ctypes.byref(dist) if dist else None,
+                                     ctypes.byref(self._h)))
+
+    def tp_timed_out(self) -> bool:
+        v = ctypes.c_int()
+        _check(lib().sm_tp_status(self._h, ctypes.byref(v)))
+        return bool(v.value)
 
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:
@@ -252,16 +340,17 @@ class KVCache:
     def __init__(self, model: Model, tree: Tree, batch: int, max_seq_len: int):
         import torch
         self.model, self.tree, self.batch, self.x = model, tree, batch, max_seq_len
-        self.nbytes = kv_bytes(model.cfg, batch, max_seq_len, tree.N)
+        self.nbytes = kv_bytes(model.cfg, batch, max_seq_len, tree.N, model.tp_size)
         self.mem = torch.empty(self.nbytes // 2, dtype=torch.bfloat16, device="cuda")
         self._h = ctypes.c_void_p()
         _check(lib().sm_kv_bind(model._h, tree._h, batch, max_seq_len, ctypes.c_void_p(_ptr(self.mem)),
                                 ctypes.c_size_t(self.nbytes), ctypes.byref(self._h)))
 
     def layout(self):
-        """[L][2][b][Hkv][x+N][hd] view of the cache memory."""
+        """[L][2][b][Hkv/tp][x+N][hd] view of the cache memory (this rank's kv heads)."""
         c = self.model.cfg
-        return self.mem.view(c["n_layers"], 2, self.batch, c["n_kv_heads"], self.x + self.tree.N, c["head_dim"])
+        return self.mem.view(c["n_layers"], 2, self.batch, c["n_kv_heads"] // self.model.tp_size,
+                             self.x + self.tree.N, c["head_dim"])
 
     def lengths(self) -> np.ndarray:
         out = np.zeros(self.batch, np.int32)

@@ -370,4 +370,12 @@ cudaError_t attention_launch(const AttnArgs &a, int head_dim, cudaStream_t st) {
   }
 }
 
+void attention_preload() {  // force-load (see gemm_preload)
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, tree_attn_kernel<16>);
+  cudaFuncGetAttributes(&fa, tree_attn_kernel<32>);
+  cudaFuncGetAttributes(&fa, tree_attn_kernel<64>);
+  cudaFuncGetAttributes(&fa, tree_attn_kernel<128>);
+}
+
 }  // namespace sm

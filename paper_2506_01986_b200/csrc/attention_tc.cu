@@ -524,4 +524,9 @@ cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
   return cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel, a);
 }
 
+void attention_tc_preload() {  // force-load (see gemm_preload)
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, tree_attn_tc_kernel);
+}
+
 }  // namespace sm

@@ -69,6 +69,69 @@ SM_DEV float4 ld_dsmem_f32x4(uint32_t cluster_addr) {
   return v;
 }
 
+// ------------------------------------------------------------------ logits statistics
+// Single-pass typical statistics of y over a row: m = max y, s = sum e^(y-m),
+// t = sum e^(y-m) (y-m), so H = log s - t/s (reading Q10); merges are exact
+// re-basings, applied in a fixed order.
+struct MST {
+  float m, s, t;
+};
+SM_DEV MST mst_merge(MST a, MST b) {
+  if (a.m == -INFINITY) return b;
+  if (b.m == -INFINITY) return a;
+  const float M = fmaxf(a.m, b.m);
+  const float ea = expf(a.m - M), eb = expf(b.m - M);
+  MST r;
+  r.m = M;
+  r.s = a.s * ea + b.s * eb;
+  r.t = ea * (a.t + (a.m - M) * a.s) + eb * (b.t + (b.m - M) * b.s);
+  return r;
+}
+SM_DEV void mst_add(MST &acc, float y) {
+  if (y > acc.m) {
+    const float e = (acc.m == -INFINITY) ? 0.f : expf(acc.m - y);
+    acc.t = (acc.m == -INFINITY) ? 0.f : e * (acc.t + (acc.m - y) * acc.s);
+    acc.s = acc.s * e + 1.f;
+    acc.m = y;
+  } else {
+    const float e = expf(y - acc.m);
+    acc.s += e;
+    acc.t += e * (y - acc.m);
+  }
+}
+SM_DEV void argmax_merge(float &v, int &i, float v2, int i2) {
+  if (v2 > v || (v2 == v && i2 < i)) {
+    v = v2;
+    i = i2;
+  }
+}
+
+// ------------------------------------------------------------------ cross-GPU flags (tensor parallel)
+SM_DEV void st_release_sys(long long *p, long long v) {
+  asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+SM_DEV long long ld_acquire_sys(const long long *p) {
+  long long v;
+  asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+SM_DEV unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Wait until *f >= ep; after ~10 s give up, raise *err and continue (no hung GPU).
+SM_DEV void tp_wait_flag(const long long *f, long long ep, int *err) {
+  const unsigned long long t0 = globaltimer_ns();
+  while (ld_acquire_sys(f) < ep) {
+    __nanosleep(64);
+    if (globaltimer_ns() - t0 > 10000000000ull) {
+      atomicExch(err, 1);
+      break;
+    }
+  }
+}
+
 // Diagnostics build only (-DSM_TRACE, build(trace=True)): per-CTA clock64 stamps.
 #ifdef SM_TRACE
 constexpr int kTraceCtas = 1024, kTraceSlots = 24;

@@ -58,7 +58,8 @@ __global__ void __launch_bounds__(256) accept_kernel(const __grid_constant__ Acc
       } else {
         const float *st = a.stats + 3 * (rowbase + p);
         const float m = st[0], s = st[1], tt = st[2];
-        const float y = a.z[(rowbase + p) * (size_t)a.V + tokc] * a.inv_temp;
+        const float zc = a.cand ? a.cand[rowbase + n] : a.z[(rowbase + p) * (size_t)a.V + tokc];
+        const float y = zc * a.inv_temp;
         const float logs = logf(s);
         const float logP = (y - m) - logs;
         const float H = logs - tt / s;
@@ -233,11 +234,14 @@ SM_DEV uint64_t splitmix64(uint64_t z) {
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   return z ^ (z >> 31);
 }
+// dst[i] = w[start + i] (cols == 0) or, for a [rows][cols] block of a [*][full_cols]
+// matrix at (row0, col0), w[(row0 + i / cols) * full_cols + col0 + i % cols]
 __global__ void generate_kernel(uint16_t *dst, size_t numel, uint64_t seed, uint64_t stream_id, uint64_t start,
-                                int mode) {
+                                int mode, int cols, int full_cols, int col0) {
   const uint64_t base = seed ^ (stream_id << 40);
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < numel; i += (size_t)gridDim.x * blockDim.x) {
-    const uint64_t h = splitmix64(base ^ (start + i));
+    const uint64_t src = cols ? start + (i / cols) * (uint64_t)full_cols + col0 + i % cols : start + i;
+    const uint64_t h = splitmix64(base ^ src);
     float w;
     if (mode == 0) {
       const int k = (int)(h >> 40) - (1 << 23);
@@ -260,8 +264,30 @@ cudaError_t generate_bf16_launch(void *dst, size_t numel, uint64_t seed, uint64_
   if (numel == 0) return cudaSuccess;
   size_t blocks = (numel + 255) / 256;
   if (blocks > 148 * 64) blocks = 148 * 64;
-  generate_kernel<<<(unsigned)blocks, 256, 0, st>>>(static_cast<uint16_t *>(dst), numel, seed, stream_id, start, mode);
+  generate_kernel<<<(unsigned)blocks, 256, 0, st>>>(static_cast<uint16_t *>(dst), numel, seed, stream_id, start, mode,
+                                                     0, 0, 0);
   return cudaGetLastError();
+}
+cudaError_t generate_bf16_2d_launch(void *dst, int rows, int cols, int full_cols, int row0, int col0, uint64_t seed,
+                                    uint64_t stream_id, int mode, cudaStream_t st) {
+  const size_t numel = (size_t)rows * cols;
+  if (numel == 0) return cudaSuccess;
+  size_t blocks = (numel + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  generate_kernel<<<(unsigned)blocks, 256, 0, st>>>(static_cast<uint16_t *>(dst), numel, seed, stream_id,
+                                                     (uint64_t)row0 * full_cols, mode, cols, full_cols, col0);
+  return cudaGetLastError();
+}
+
+void decode_preload() {  // force-load (see gemm_preload)
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, propose_kernel);
+  cudaFuncGetAttributes(&fa, accept_kernel);
+  cudaFuncGetAttributes(&fa, compact_kernel);
+  cudaFuncGetAttributes(&fa, commit_kernel);
+  cudaFuncGetAttributes(&fa, advance_len_kernel);
+  cudaFuncGetAttributes(&fa, set_root_kernel);
+  cudaFuncGetAttributes(&fa, generate_kernel);
 }
 
 }  // namespace sm

@@ -111,6 +111,94 @@ cudaError_t resid_norm_launch(const PartialView *pv, float *x, const bf16 *g, bf
                             eps);
 }
 
+// Tensor-parallel variant (a7): the residual all-reduce fused in.  Each rank reduces
+// its own split-K partials of a row slice, publishes the fp32 slice in its symmetric
+// buffer, raises a per-CTA epoch flag in every peer, waits for the peers' flags of
+// the same CTA and sums the t slices in rank order -- every rank then holds bitwise
+// the same residual.  Persistent over rows (grid <= resident capacity) so the CTA a
+// rank waits on is always running on the peer.  The DSMEM sum-of-squares slots are
+// double-buffered by iteration parity.
+__global__ void __launch_bounds__(kNormThreads) resid_norm_tp_kernel(PartialView pv, float *x, const bf16 *g, bf16 *h,
+                                                                     int M, int d, float eps, TpArgs tp) {
+  __shared__ float red[kNormThreads / 32];
+  __shared__ float ssq[2][8];
+  pdl_trigger();
+  cluster_arrive_relaxed();
+  pdl_wait();
+  const int crank = blockIdx.x, cs = gridDim.x;
+  const int i = crank * kNormCols + threadIdx.x * 4;
+  const long long ep = *tp.seq + tp.point + 1;
+  int it = 0;
+  for (int m = blockIdx.y; m < M; m += gridDim.y, ++it) {
+    float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < d) {
+      float4 ys[16];
+      const SkRef ref = sk_ref(pv, 0, m, i);
+      sk_load<16>(ref, ys);
+      y = sk_reduce<16>(ref, ys);
+      __stcg(reinterpret_cast<float4 *>(tp.data[tp.rank] + (size_t)m * d + i), y);
+    }
+    __threadfence_system();
+    __syncthreads();
+    const int idx = m * cs + crank;
+    const int q = threadIdx.x;
+    if (q < tp.t && q != tp.rank) {
+      st_release_sys(tp.flags[q] + (size_t)tp.rank * kTpFlagSlots + idx, ep);
+      tp_wait_flag(tp.flags[tp.rank] + (size_t)q * kTpFlagSlots + idx, ep, tp.err);
+    }
+    __syncthreads();
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < d) {
+      float4 part[kMaxTP];
+#pragma unroll
+      for (int r = 0; r < kMaxTP; ++r)
+        if (r < tp.t)
+          part[r] = r == tp.rank ? y : __ldcv(reinterpret_cast<const float4 *>(tp.data[r] + (size_t)m * d + i));
+      float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int r = 0; r < kMaxTP; ++r) {  // rank order: identical on every rank
+        if (r < tp.t) {
+          sum.x += part[r].x;
+          sum.y += part[r].y;
+          sum.z += part[r].z;
+          sum.w += part[r].w;
+        }
+      }
+      float *xr = x + (size_t)m * d;
+      a = *reinterpret_cast<const float4 *>(xr + i);
+      a.x += sum.x;
+      a.y += sum.y;
+      a.z += sum.z;
+      a.w += sum.w;
+      *reinterpret_cast<float4 *>(xr + i) = a;
+    }
+    float ss = block_sum<kNormThreads>(a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w, red);
+    if (it == 0) cluster_wait();  // every CTA of the cluster has started
+    if (threadIdx.x < cs) st_dsmem_f32(mapa_u32(smem_u32(&ssq[it & 1][crank]), threadIdx.x), ss);
+    cluster_sync_all();
+    ss = 0.f;
+    for (int r = 0; r < cs; ++r) ss += ssq[it & 1][r];
+    const float rs = 1.0f / sqrtf(ss / (float)d + eps);
+    if (i < d) {
+      const __nv_bfloat162 g01 = *reinterpret_cast<const __nv_bfloat162 *>(g + i);
+      const __nv_bfloat162 g23 = *reinterpret_cast<const __nv_bfloat162 *>(g + i + 2);
+      uint2 o;
+      o.x = pack_bf16(a.x * rs * __low2float(g01), a.y * rs * __high2float(g01));
+      o.y = pack_bf16(a.z * rs * __low2float(g23), a.w * rs * __high2float(g23));
+      *reinterpret_cast<uint2 *>(h + (size_t)m * d + i) = o;
+    }
+  }
+  if (it == 0) cluster_wait();  // no rows: complete the start barrier phase
+}
+cudaError_t resid_norm_tp_launch(const PartialView &pv, float *x, const bf16 *g, bf16 *h, int M, int d, float eps,
+                                 const TpArgs &tp, cudaStream_t st) {
+  const int cs = (d + kNormCols - 1) / kNormCols;
+  if (cs > 8 || d % 4 || M * cs > kTpFlagSlots) return cudaErrorInvalidValue;
+  const int rows_par = M < 64 ? M : 64;  // cs x 64 CTAs: always co-resident
+  return launch_pdl_cluster(resid_norm_tp_kernel, dim3(cs, rows_par), dim3(kNormThreads), 0, st, cs, pv, x, g, h, M, d,
+                            eps, tp);
+}
+
 // ------------------------------------------------------------------ QKV consumer (RoPE + cache write)
 // thread -> 4 consecutive rotary pairs (c .. c+3) of one head of one token row
 __global__ void __launch_bounds__(256) qkv_consumer_kernel(PartialView pv, RowCtx rc, int H, int Hkv, int hd,
@@ -197,42 +285,10 @@ cudaError_t silu_consumer_launch(const PartialView &pv, int F, bf16 *act, cudaSt
 }
 
 // ------------------------------------------------------------------ logits: argmax + typical stats
-struct MST {
-  float m, s, t;
-};
-SM_DEV MST mst_merge(MST a, MST b) {
-  if (a.m == -INFINITY) return b;
-  if (b.m == -INFINITY) return a;
-  const float M = fmaxf(a.m, b.m);
-  const float ea = expf(a.m - M), eb = expf(b.m - M);
-  MST r;
-  r.m = M;
-  r.s = a.s * ea + b.s * eb;
-  r.t = ea * (a.t + (a.m - M) * a.s) + eb * (b.t + (b.m - M) * b.s);
-  return r;
-}
-SM_DEV void mst_add(MST &acc, float y) {
-  if (y > acc.m) {
-    const float e = (acc.m == -INFINITY) ? 0.f : expf(acc.m - y);
-    acc.t = (acc.m == -INFINITY) ? 0.f : e * (acc.t + (acc.m - y) * acc.s);
-    acc.s = acc.s * e + 1.f;
-    acc.m = y;
-  } else {
-    const float e = expf(y - acc.m);
-    acc.s += e;
-    acc.t += e * (y - acc.m);
-  }
-}
-SM_DEV void argmax_merge(float &v, int &i, float v2, int i2) {
-  if (v2 > v || (v2 == v && i2 < i)) {
-    v = v2;
-    i = i2;
-  }
-}
-
 template <bool FROM_PARTIALS>
 __global__ void __launch_bounds__(512) logits_kernel(PartialView pv, const float *z_in, int V, float inv_temp,
-                                                     float *z_out, int32_t *argmax, float *stats) {
+                                                     float *z_out, int32_t *argmax, float *stats, int idx_offset,
+                                                     float *amax) {
   __shared__ float sv[32];
   __shared__ int si[32];
   __shared__ MST smst[32];
@@ -278,7 +334,8 @@ __global__ void __launch_bounds__(512) logits_kernel(PartialView pv, const float
       argmax_merge(bv, bi, sv[k], si[k]);
       acc = mst_merge(acc, smst[k]);
     }
-    argmax[r] = bi;
+    argmax[r] = bi + idx_offset;  // vocabulary-parallel slice -> global token id
+    if (amax) amax[r] = bv;
     if (stats) {
       stats[3 * r + 0] = acc.m;
       stats[3 * r + 1] = acc.s;
@@ -287,15 +344,15 @@ __global__ void __launch_bounds__(512) logits_kernel(PartialView pv, const float
   }
 }
 cudaError_t logits_consumer_launch(const PartialView &pv, float inv_temp, float *z_out, int32_t *argmax, float *stats,
-                                   cudaStream_t st) {
+                                   int idx_offset, float *amax, cudaStream_t st) {
   return launch_pdl(logits_kernel<true>, dim3(pv.M), dim3(512), 0, st, pv, (const float *)nullptr, pv.N, inv_temp,
-                    z_out, argmax, stats);
+                    z_out, argmax, stats, idx_offset, amax);
 }
 cudaError_t logits_finalize_launch(const float *z, int V, int rows, float inv_temp, int32_t *argmax, float *stats,
-                                   cudaStream_t st) {
+                                   int idx_offset, float *amax, cudaStream_t st) {
   PartialView pv{};
   return launch_pdl(logits_kernel<false>, dim3(rows), dim3(512), 0, st, pv, z, V, inv_temp, (float *)nullptr, argmax,
-                    stats);
+                    stats, idx_offset, amax);
 }
 
 // ------------------------------------------------------------------ top-k (K3)
@@ -303,7 +360,7 @@ cudaError_t logits_finalize_launch(const float *z, int V, int rows, float inv_te
 // block argmax by (value desc, index asc); taken entries become NaN.
 template <bool FROM_PARTIALS>
 __global__ void __launch_bounds__(1024) topk_kernel(PartialView pv, const float *rows_in, int nb, int V, int k,
-                                                    int32_t *idx) {
+                                                    int32_t *idx, int idx_offset, float *vals) {
   extern __shared__ float srow[];
   __shared__ float wv[32];
   __shared__ int wi[32];
@@ -343,7 +400,8 @@ __global__ void __launch_bounds__(1024) topk_kernel(PartialView pv, const float 
       for (int w = 1; w < (int)(blockDim.x >> 5); ++w) argmax_merge(bv, bi, wv[w], wi[w]);
       // FROM_PARTIALS: idx[b][head][k]; plain rows: idx[r][k]
       const size_t o = FROM_PARTIALS ? ((size_t)bb * (gridDim.x / nb) + head) * k + kk : (size_t)r * k + kk;
-      idx[o] = bi;
+      idx[o] = (bi >= 0 && bi < V) ? bi + idx_offset : bi;  // vocabulary-parallel slice -> global id
+      if (vals) vals[o] = bv;
       if (bi >= 0 && bi < V) srow[bi] = __int_as_float(0x7fc00000);
     }
     __syncthreads();
@@ -359,19 +417,21 @@ static cudaError_t topk_attr(size_t smem) {
   }
   return cudaSuccess;
 }
-cudaError_t topk_consumer_launch(const PartialView &pv, int nmed, int nb, int V, int k, int32_t *idx, cudaStream_t st) {
+cudaError_t topk_consumer_launch(const PartialView &pv, int nmed, int nb, int V, int k, int32_t *idx, int idx_offset,
+                                 float *vals, cudaStream_t st) {
   const size_t smem = (size_t)V * sizeof(float);
   cudaError_t e = topk_attr<true>(smem);
   if (e != cudaSuccess) return e;
   return launch_pdl(topk_kernel<true>, dim3(nmed * nb), dim3(1024), smem, st, pv, (const float *)nullptr, nb, V, k,
-                    idx);
+                    idx, idx_offset, vals);
 }
 cudaError_t topk_launch(const float *logits, int rows, int V, int k, int32_t *idx, cudaStream_t st) {
   const size_t smem = (size_t)V * sizeof(float);
   cudaError_t e = topk_attr<false>(smem);
   if (e != cudaSuccess) return e;
   PartialView pv{};
-  return launch_pdl(topk_kernel<false>, dim3(rows), dim3(1024), smem, st, pv, logits, rows, V, k, idx);
+  return launch_pdl(topk_kernel<false>, dim3(rows), dim3(1024), smem, st, pv, logits, rows, V, k, idx, 0,
+                    (float *)nullptr);
 }
 
 // ------------------------------------------------------------------ Medusa head ResBlock consumer
@@ -407,6 +467,21 @@ __global__ void plain_kernel(PartialView pv, float *out) {
 }
 cudaError_t plain_consumer_launch(const PartialView &pv, float *out, cudaStream_t st) {
   return launch_pdl(plain_kernel, dim3((pv.N + 1023) / 1024, pv.M), dim3(256), 0, st, pv, out);
+}
+
+void epilogue_preload() {  // force-load (see gemm_preload)
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, embed_kernel);
+  cudaFuncGetAttributes(&fa, resid_norm_kernel);
+  cudaFuncGetAttributes(&fa, resid_norm_tp_kernel);
+  cudaFuncGetAttributes(&fa, qkv_consumer_kernel);
+  cudaFuncGetAttributes(&fa, silu_consumer_kernel);
+  cudaFuncGetAttributes(&fa, logits_kernel<true>);
+  cudaFuncGetAttributes(&fa, logits_kernel<false>);
+  cudaFuncGetAttributes(&fa, topk_kernel<true>);
+  cudaFuncGetAttributes(&fa, topk_kernel<false>);
+  cudaFuncGetAttributes(&fa, heads_r_kernel);
+  cudaFuncGetAttributes(&fa, plain_kernel);
 }
 
 }  // namespace sm

@@ -303,4 +303,19 @@ cudaError_t gemm_launch(const GemmArgs &a0, cudaStream_t st) {
   }
 }
 
+// Force-load every instantiation (lazy module loading would otherwise load a kernel at
+// its first launch, which can wait for running kernels -- fatal when those spin on a
+// tensor-parallel peer whose work is enqueued later).
+template <int BN, int SK>
+static void preload_one() {
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, gemm_streamk_kernel<BN, SK>);
+}
+void gemm_preload() {
+  preload_one<16, 50>(), preload_one<16, 68>(), preload_one<16, 104>(), preload_one<16, 216>();
+  preload_one<32, 50>(), preload_one<32, 68>(), preload_one<32, 104>(), preload_one<32, 216>();
+  preload_one<64, 50>(), preload_one<64, 68>(), preload_one<64, 104>(), preload_one<64, 216>();
+  preload_one<128, 216>(), preload_one<256, 216>();
+}
+
 }  // namespace sm

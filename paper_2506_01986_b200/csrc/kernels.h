@@ -208,15 +208,18 @@ cudaError_t silu_consumer_launch(const PartialView &pv, int F, bf16 *act, cudaSt
 // LM rows: z = y (fp32, optional copy), argmax (lowest index on ties) and the
 // single-pass typical statistics (m, s, t) of z * inv_temp    (R9)
 cudaError_t logits_consumer_launch(const PartialView &pv, float inv_temp, float *z_out, int32_t *argmax, float *stats,
+                                   int idx_offset, float *amax,
                                    cudaStream_t st);
 // plain fp32 rows (z or head logits) -> argmax/stats
 cudaError_t logits_finalize_launch(const float *z, int V, int rows, float inv_temp, int32_t *argmax, float *stats,
+                                   int idx_offset, float *amax,
                                    cudaStream_t st);
 // Medusa ResBlock: r[i][b][:] = bf16(h[b] + SiLU(y_i[b] + beta_i))    (R10)
 cudaError_t heads_r_consumer_launch(const PartialView &pv, int nmed, int nb, int d, const bf16 *head_in,
                                     const bf16 *const *beta, bf16 *r_out, long long r_stride, cudaStream_t st);
 // top-k of the U-head logits y_i[b][:]: idx[b][i][k], (value desc, index asc)    (K3)
-cudaError_t topk_consumer_launch(const PartialView &pv, int nmed, int nb, int V, int k, int32_t *idx, cudaStream_t st);
+cudaError_t topk_consumer_launch(const PartialView &pv, int nmed, int nb, int V, int k, int32_t *idx, int idx_offset,
+                                 float *vals, cudaStream_t st);
 // stage API: top-k of plain fp32 rows
 cudaError_t topk_launch(const float *logits, int rows, int V, int k, int32_t *idx, cudaStream_t st);
 // stage API: out[m][n] = y[m][n]
@@ -239,6 +242,7 @@ struct AcceptArgs {
   const int32_t *argmax;       // [b*N]
   const float *stats;          // [b*N][3] (m, s, t) of y = z/T
   const float *z;              // [b*N][V] logits (typical gather)
+  const float *cand;           // nullable: [b*N] z[parent(n)][tok[n]] (tensor parallel: merged)
   const int32_t *len;          // Lc[b]
   const int32_t *max_new;      // nullable
   const int32_t *forced_path;  // nullable [b][l+1]
@@ -257,6 +261,42 @@ cudaError_t set_root_launch(int32_t *root, int seq, const int32_t *argmax_row, c
                             bf16 *head_in_row, cudaStream_t st);
 cudaError_t generate_bf16_launch(void *dst, size_t numel, uint64_t seed, uint64_t stream_id, uint64_t start, int mode,
                                  cudaStream_t st);
+cudaError_t generate_bf16_2d_launch(void *dst, int rows, int cols, int full_cols, int row0, int col0, uint64_t seed,
+                                    uint64_t stream_id, int mode, cudaStream_t st);
+
+// ---------------------------------------------------------------- tensor parallelism (a7)
+constexpr int kMaxTP = 8;
+constexpr int kTpFlagSlots = 8192;  // flags per source rank = max CTAs of one exchange point
+// Symmetric buffer of one rank: [flags: kMaxTP src x kTpFlagSlots int64][data slot 0][data slot 1]
+struct TpArgs {
+  int rank, t;
+  float *data[kMaxTP];            // each rank's data slot of this exchange (point parity), mapped here
+  long long *flags[kMaxTP];       // each rank's flags region, mapped here
+  const long long *seq;           // this rank's epoch base (device)
+  int point;                      // exchange index within the current top-level call
+  int *err;                       // set to 1 when a wait times out
+};
+// Residual all-reduce fused into residual + RMSNorm (pv = this rank's o_proj / down partials).
+cudaError_t resid_norm_tp_launch(const PartialView &pv, float *x, const bf16 *g, bf16 *h, int M, int d, float eps,
+                                 const TpArgs &tp, cudaStream_t st);
+// Merge the vocab-parallel LM head statistics of rows [0, rows): in = this rank's
+// (amax, argmax, m, s, t) per row; cand (nullable) = z[parent(n)][tok[n]] when the rank
+// owns tok[n] (tree rows, typical acceptance); out: merged argmax / stats / cand.
+cudaError_t tp_merge_logits_launch(int rows, const float *amax, int32_t *argmax, float *stats, const float *z_local,
+                                   int Vl, int v0, const int32_t *parent, int N, const int32_t *tok, float *cand,
+                                   const TpArgs &tp, cudaStream_t st);
+// Merge per-rank top-K (value, global index) lists of `entries` (b x head) into idx.
+cudaError_t tp_merge_topk_launch(int entries, int K, const float *vals, const int32_t *idx_local, int32_t *idx_out,
+                                 int nmed, int nb, const TpArgs &tp, cudaStream_t st);
+cudaError_t tp_advance_launch(long long *seq, int n, cudaStream_t st);
+
+// Force-load every kernel of the library (lazy module loading).
+void gemm_preload();
+void attention_preload();
+void attention_tc_preload();
+void decode_preload();
+void epilogue_preload();
+void tp_preload();
 
 // ---------------------------------------------------------------- PDL launch helpers
 // Launch with programmatic stream serialization when enabled (gemm_pdl()).

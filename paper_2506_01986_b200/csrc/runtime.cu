@@ -260,7 +260,50 @@ struct sm_model {
   GemmArgs g_lm, g_R, g_U;
   sm_tree *chain = nullptr;
   cudaStream_t cap_stream = nullptr;
+  // tensor parallelism (a7): local dims above are this rank's shard
+  int tp = 1, tp_rank = 0, v0 = 0;
+  void *sym[kMaxTP] = {};        // every rank's symmetric buffer, mapped on this device
+  size_t sym_slot_floats = 0;
+  long long *tp_seq = nullptr;   // device epoch base
+  int *tp_err = nullptr;         // device: a wait timed out
+  int tp_point = 0;              // host: exchange index within the current top-level call
+  float *amax = nullptr, *cand = nullptr, *tk_val = nullptr;
+  int32_t *tk_idx = nullptr;
 };
+
+static size_t tp_slot_floats(const sm_model_cfg &c) {
+  return std::max({(size_t)c.max_rows * c.d_model, (size_t)c.max_rows * 8,
+                   (size_t)c.max_batch * std::max(1, c.n_medusa) * 64});
+}
+static constexpr size_t kTpFlagBytes = (size_t)kMaxTP * kTpFlagSlots * sizeof(long long);
+// Exchange descriptor for the next exchange point of the current call.
+static TpArgs tp_next(sm_model *m) {
+  TpArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.rank = m->tp_rank;
+  a.t = m->tp;
+  const int pt = m->tp_point++;
+  for (int q = 0; q < m->tp; ++q) {
+    char *b = static_cast<char *>(m->sym[q]);
+    a.flags[q] = reinterpret_cast<long long *>(b);
+    a.data[q] = reinterpret_cast<float *>(b + kTpFlagBytes + (size_t)(pt & 1) * m->sym_slot_floats * sizeof(float));
+  }
+  a.seq = m->tp_seq;
+  a.point = pt;
+  a.err = m->tp_err;
+  return a;
+}
+static void tp_begin(sm_model *m) { m->tp_point = 0; }
+// Advance the epoch base past this call's exchanges (kept even, so the data slot
+// parity of an exchange is its index parity in every call).
+static sm_status tp_end(sm_model *m, cudaStream_t st, int &nl) {
+  if (m->tp > 1 && m->tp_point > 0) {
+    CK(tp_advance_launch(m->tp_seq, (m->tp_point + 1) & ~1, st));
+    ++nl;
+  }
+  m->tp_point = 0;
+  return SM_OK;
+}
 
 static GemmArgs gemm_proto(int N, int K, int batch) {
   GemmArgs a;
@@ -325,30 +368,52 @@ static size_t ws_need(const GemmArgs &proto, int max_m) {
 extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *w, const sm_dist *dist,
                                      sm_model **out) {
   if (!cfg || !w || !out) return fail(SM_ERR_INVALID_ARG, "sm_model_create: null argument");
-  if (dist && dist->tp_size > 1)
-    return fail(SM_ERR_UNSUPPORTED, "tensor parallelism (tp_size > 1) is not built in this version");
   const sm_model_cfg &c = *cfg;
+  const int tp = dist ? dist->tp_size : 1, tp_rank = dist ? dist->tp_rank : 0;
+  if (tp != 1 && tp != 2 && tp != 4 && tp != 8) return fail(SM_ERR_INVALID_ARG, "tp_size must be 1, 2, 4 or 8");
+  if (tp_rank < 0 || tp_rank >= tp) return fail(SM_ERR_INVALID_ARG, "tp_rank out of range");
+  if (tp > 1) {
+    if (c.n_heads % tp || c.n_kv_heads % tp || c.d_ffn % (64 * tp) || c.vocab % (4 * tp))
+      return fail(SM_ERR_INVALID_ARG, "tp_size must divide n_heads, n_kv_heads, d_ffn/64 and vocab/4");
+    for (int q = 0; q < tp; ++q)
+      if (!dist->peer_sym[q]) return fail(SM_ERR_INVALID_ARG, "sm_dist.peer_sym[q] is null");
+  }
   if (c.n_layers < 1 || c.d_model % 64 || c.n_heads < 1 || c.n_kv_heads < 1 || c.n_heads % c.n_kv_heads ||
       (c.head_dim != 16 && c.head_dim != 32 && c.head_dim != 64 && c.head_dim != 128) || c.d_ffn % 64 ||
       c.vocab % 4 || c.n_medusa < 0 || c.n_medusa > kMaxGemmBatch || c.max_rows < 1 || c.max_rows > 1024 ||
       c.max_batch < 1 || c.max_seq_len < 1 || (c.n_heads * c.head_dim) % 64)
     return fail(SM_ERR_INVALID_ARG, "sm_model_create: unsupported shape (d, F multiple of 64; hd in {16,32,64,128}; "
                                     "max_rows <= 1024; n_medusa <= 5)");
-  if (c.vocab * 4 > 200 * 1024) return fail(SM_ERR_INVALID_ARG, "vocab too large for the shared-memory top-k");
+  if (c.vocab / tp * 4 > 200 * 1024) return fail(SM_ERR_INVALID_ARG, "vocab too large for the shared-memory top-k");
+  {  // every kernel resident before any work (see gemm_preload)
+    static bool loaded = false;
+    if (!loaded) {
+      gemm_preload();
+      attention_preload();
+      attention_tc_preload();
+      decode_preload();
+      epilogue_preload();
+      tp_preload();
+      loaded = true;
+    }
+  }
   sm_model *m = new sm_model();
   m->cfg = c;
+  m->tp = tp;
+  m->tp_rank = tp_rank;
   m->L = c.n_layers;
   m->d = c.d_model;
-  m->H = c.n_heads;
-  m->Hkv = c.n_kv_heads;
+  m->H = c.n_heads / tp;  // this rank's shard
+  m->Hkv = c.n_kv_heads / tp;
   m->hd = c.head_dim;
-  m->F = c.d_ffn;
-  m->V = c.vocab;
+  m->F = c.d_ffn / tp;
+  m->V = c.vocab / tp;
+  m->v0 = tp_rank * m->V;
   m->nmed = c.n_medusa;
   m->G = c.n_heads / c.n_kv_heads;
   m->R = c.max_rows;
   m->B = c.max_batch;
-  m->qkv_n = (c.n_heads + 2 * c.n_kv_heads) * c.head_dim;
+  m->qkv_n = (m->H + 2 * m->Hkv) * c.head_dim;
   m->embed = (const bf16 *)w->embed;
   m->final_norm = (const bf16 *)w->final_norm;
   m->lm_head = (const bf16 *)w->lm_head;
@@ -384,6 +449,20 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
   ALLOC(m->head_in, (size_t)B * d, "head_in");
   ALLOC(m->r_buf, (size_t)std::max(1, m->nmed) * B * d, "r_buf");
   ALLOC(m->rope, (size_t)c.max_seq_len * (m->hd / 2), "rope");
+  ALLOC(m->amax, (size_t)R, "amax");
+  ALLOC(m->cand, (size_t)R, "cand");
+  ALLOC(m->tk_val, (size_t)B * std::max(1, m->nmed) * 32, "topk values");
+  ALLOC(m->tk_idx, (size_t)B * std::max(1, m->nmed) * 32, "topk indices");
+  ALLOC(m->tp_seq, 1, "tp epoch");
+  ALLOC(m->tp_err, 1, "tp error flag");
+  cudaMemset(m->tp_seq, 0, sizeof(long long));
+  cudaMemset(m->tp_err, 0, sizeof(int));
+  if (tp > 1) {
+    for (int q = 0; q < tp; ++q) m->sym[q] = dist->peer_sym[q];
+    m->sym_slot_floats = tp_slot_floats(c);
+    // own buffer: flags start below every epoch (the caller barriers before work)
+    cudaMemset(m->sym[tp_rank], 0, kTpFlagBytes + 2 * m->sym_slot_floats * sizeof(float));
+  }
   cudaMemset(m->x, 0, (size_t)R * d * 4);
   cudaMemset(m->h, 0, (size_t)R * d * 2);
   cudaMemset(m->attn, 0, (size_t)R * Hhd * 2);
@@ -480,6 +559,12 @@ extern "C" void sm_model_destroy(sm_model *m) {
   cudaFree(m->r_buf);
   cudaFree(m->argmax);
   cudaFree(m->rope);
+  cudaFree(m->amax);
+  cudaFree(m->cand);
+  cudaFree(m->tk_val);
+  cudaFree(m->tk_idx);
+  cudaFree(m->tp_seq);
+  cudaFree(m->tp_err);
   if (m->chain) sm_tree_destroy(m->chain);
   if (m->cap_stream) cudaStreamDestroy(m->cap_stream);
   delete m;
@@ -489,6 +574,48 @@ extern "C" sm_status sm_generate_bf16(void *dst, size_t numel, uint64_t seed, ui
                                       int mode, void *stream) {
   if (!dst && numel) return fail(SM_ERR_INVALID_ARG, "sm_generate_bf16: null dst");
   CK(generate_bf16_launch(dst, numel, seed, stream_id, start, mode, (cudaStream_t)stream));
+  return SM_OK;
+}
+
+extern "C" sm_status sm_generate_bf16_2d(void *dst, int rows, int cols, int full_cols, int row0, int col0,
+                                         uint64_t seed, uint64_t stream_id, int mode, void *stream) {
+  if ((!dst && rows * cols) || rows < 0 || cols < 0 || row0 < 0 || col0 < 0 || col0 + cols > full_cols)
+    return fail(SM_ERR_INVALID_ARG, "sm_generate_bf16_2d: bad arguments");
+  CK(generate_bf16_2d_launch(dst, rows, cols, full_cols, row0, col0, seed, stream_id, mode, (cudaStream_t)stream));
+  return SM_OK;
+}
+
+// ---------------------------------------------------------------- tensor parallel plumbing
+extern "C" sm_status sm_tp_sym_bytes(const sm_model_cfg *cfg, size_t *bytes) {
+  if (!cfg || !bytes || cfg->max_rows < 1 || cfg->d_model < 1 || cfg->max_batch < 1)
+    return fail(SM_ERR_INVALID_ARG, "sm_tp_sym_bytes: bad arguments");
+  *bytes = kTpFlagBytes + 2 * tp_slot_floats(*cfg) * sizeof(float);
+  return SM_OK;
+}
+extern "C" sm_status sm_tp_status(const sm_model *m, int *timed_out) {
+  if (!m || !timed_out) return fail(SM_ERR_INVALID_ARG, "sm_tp_status: null");
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(timed_out, m->tp_err, sizeof(int), cudaMemcpyDeviceToHost));
+  return SM_OK;
+}
+extern "C" sm_status sm_ipc_get_handle(const void *d_ptr, unsigned char handle[64]) {
+  if (!d_ptr || !handle) return fail(SM_ERR_INVALID_ARG, "sm_ipc_get_handle: null");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, const_cast<void *>(d_ptr)));
+  std::memcpy(handle, &h, 64);
+  return SM_OK;
+}
+extern "C" sm_status sm_ipc_open(const unsigned char handle[64], void **d_ptr) {
+  if (!handle || !d_ptr) return fail(SM_ERR_INVALID_ARG, "sm_ipc_open: null");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  CK(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return SM_OK;
+}
+extern "C" sm_status sm_ipc_close(void *d_ptr) {
+  if (!d_ptr) return fail(SM_ERR_INVALID_ARG, "sm_ipc_close: null");
+  CK(cudaIpcCloseMemHandle(d_ptr));
   return SM_OK;
 }
 
@@ -542,7 +669,7 @@ extern "C" sm_status sm_kv_bind(sm_model *m, const sm_tree *tree, int batch, int
   if (tree->topk > 32) return fail(SM_ERR_INVALID_ARG, "topk > 32");
   if (batch * tree->N > m->R) return fail(SM_ERR_INVALID_ARG, "batch * tree nodes exceeds max_rows");
   size_t need;
-  CKS(sm_kv_bytes(&m->cfg, 1, batch, max_seq_len, tree->N, &need));
+  CKS(sm_kv_bytes(&m->cfg, m->tp, batch, max_seq_len, tree->N, &need));
   if (bytes < need) return fail(SM_ERR_KV_CAPACITY, "Cache: KV memory smaller than sm_kv_bytes");
   if (max_seq_len + tree->N > m->cfg.max_seq_len)
     return fail(SM_ERR_INVALID_ARG, "max_seq_len + N exceeds the model's RoPE table (cfg.max_seq_len)");
@@ -634,6 +761,16 @@ static int attn_splits(const sm_model *m, int nseq, int Nq) {
 static int g_ablate = 0;
 #define KEEP(bit) ((g_ablate & (bit)) == 0)
 
+// x += y (all-reduced across ranks under TP); h = bf16(rms(x) * g)
+static sm_status resid_norm(sm_model *m, const PartialView *pv, const bf16 *g, bf16 *h, int M, cudaStream_t st) {
+  if (m->tp > 1 && pv) {
+    CK(resid_norm_tp_launch(*pv, m->x, g, h, M, m->d, m->cfg.rms_eps, tp_next(m), st));
+  } else {
+    CK(resid_norm_launch(pv, m->x, g, h, M, m->d, m->cfg.rms_eps, st));
+  }
+  return SM_OK;
+}
+
 // tokens d_tok [nseq * Nq] -> hf [nseq * Nq][d]; K/V rows of every layer written
 static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, int nseq, int seq_base, int Nq,
                                  const TreeDev &tree, cudaStream_t st, int &nl) {
@@ -651,7 +788,7 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
   for (int l = 0; l < m->L; ++l) {
     // x += down (previous layer, R7); h = bf16(rms(x) * g1)   (R2)
     if (KEEP(2)) {
-      CK(resid_norm_launch(have_down ? &pv_down : nullptr, m->x, m->attn_norm[l], m->h, M, d, m->cfg.rms_eps, st));
+      CKS(resid_norm(m, have_down ? &pv_down : nullptr, m->attn_norm[l], m->h, M, st));
       ++nl;
     }
     bf16 *kc = kv->base + (size_t)l * layer_rows * m->hd;
@@ -692,7 +829,7 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
     CKS(run_gemm(m->g_o[l], M, 0, m->ws, m->ws_floats, st, nl, &pv));
     // x += o (R5); h = bf16(rms(x) * g2)
     if (KEEP(2)) {
-      CK(resid_norm_launch(&pv, m->x, m->mlp_norm[l], m->h, M, d, m->cfg.rms_eps, st));
+      CKS(resid_norm(m, &pv, m->mlp_norm[l], m->h, M, st));
       ++nl;
     }
     CKS(run_gemm(m->g_gu[l], M, 0, m->ws, m->ws_floats, st, nl, &pv));
@@ -705,7 +842,7 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
   }
   g_ablate_gemm = 0;
   // x += down; hf = bf16(rms(x) * gf)   (R8)
-  CK(resid_norm_launch(have_down ? &pv_down : nullptr, m->x, m->final_norm, m->hf, M, d, m->cfg.rms_eps, st));
+  CKS(resid_norm(m, have_down ? &pv_down : nullptr, m->final_norm, m->hf, M, st));
   ++nl;
   return SM_OK;
 }
@@ -721,8 +858,15 @@ static sm_status enqueue_heads(sm_model *m, sm_kv *kv, int row0, int nb, cudaStr
   ++nl;
   CKS(run_gemm(m->g_U, nb, row0, m->ws, m->ws_floats, st, nl, &pv));
   const int K = kv->t->topk;
-  CK(topk_consumer_launch(pv, m->nmed, nb, m->V, K, kv->topk + (size_t)row0 * m->nmed * K, st));
-  ++nl;
+  int32_t *dst = kv->topk + (size_t)row0 * m->nmed * K;
+  if (m->tp > 1) {  // vocabulary-parallel U: local top-K, then merge across ranks
+    CK(topk_consumer_launch(pv, m->nmed, nb, m->V, K, m->tk_idx, m->v0, m->tk_val, st));
+    CK(tp_merge_topk_launch(nb * m->nmed, K, m->tk_val, m->tk_idx, dst, m->nmed, nb, tp_next(m), st));
+    nl += 2;
+  } else {
+    CK(topk_consumer_launch(pv, m->nmed, nb, m->V, K, dst, 0, nullptr, st));
+    ++nl;
+  }
   return SM_OK;
 }
 
@@ -731,11 +875,12 @@ extern "C" sm_status sm_prefill(sm_model *m, sm_kv *kv, int seq, const int32_t *
     return fail(SM_ERR_INVALID_ARG, "sm_prefill: bad arguments");
   if (n == 0) return SM_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  int32_t Lc = 0;
+  int32_t Lc = 0;  // stream-ordered read (no legacy-stream sync: TP peers may share the device)
+  CK(cudaMemcpyAsync(&Lc, kv->len + seq, 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  CK(cudaMemcpy(&Lc, kv->len + seq, 4, cudaMemcpyDeviceToHost));
   if (Lc + n > kv->x) return fail(SM_ERR_KV_CAPACITY, "Cache: prefill would exceed the KV bound x");
   int nl = 0;
+  tp_begin(m);
   const TreeDev chain = m->chain->dev();
   const int R = m->R;
   int done = 0, last = 0;
@@ -749,10 +894,14 @@ extern "C" sm_status sm_prefill(sm_model *m, sm_kv *kv, int seq, const int32_t *
   // last token: LM head row, pending root, heads' top-k (reading Q8)
   PartialView pv;
   CKS(run_gemm(m->g_lm, 1, last - 1, m->ws, m->ws_floats, st, nl, &pv));
-  CK(logits_consumer_launch(pv, 1.0f, m->z, m->argmax, m->stats, st));
+  CK(logits_consumer_launch(pv, 1.0f, m->z, m->argmax, m->stats, m->v0, m->amax, st));
+  if (m->tp > 1)
+    CK(tp_merge_logits_launch(1, m->amax, m->argmax, m->stats, m->z, m->V, m->v0, nullptr, 1, nullptr, nullptr,
+                              tp_next(m), st));
   CK(set_root_launch(kv->root, seq, m->argmax, m->hf + (size_t)(last - 1) * m->d, m->d,
                      m->head_in + (size_t)seq * m->d, st));
   CKS(enqueue_heads(m, kv, seq, 1, st, nl));
+  CKS(tp_end(m, st, nl));
   CK(cudaGetLastError());
   kv->last_stream = st;
   return SM_OK;
@@ -770,7 +919,7 @@ static sm_status enqueue_verify(sm_model *m, sm_kv *kv, const int32_t *tree_tok,
   CKS(enqueue_forward(m, kv, tree_tok, kv->b, 0, kv->N, kv->t->dev(), st, nl));
   PartialView pv;
   CKS(run_gemm(m->g_lm, M, 0, m->ws, m->ws_floats, st, nl, &pv));
-  CK(logits_consumer_launch(pv, 1.0f, m->z, m->argmax, m->stats, st));
+  CK(logits_consumer_launch(pv, 1.0f, m->z, m->argmax, m->stats, m->v0, m->amax, st));
   ++nl;
   return SM_OK;
 }
@@ -782,7 +931,13 @@ static sm_status enqueue_accept(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg
   if (cfg->mode == SM_ACCEPT_TYPICAL) {
     inv_temp = 1.0f / cfg->temperature;
     // typical statistics at temperature T on the stored logits (one fp32 pass)
-    CK(logits_finalize_launch(m->z, m->V, M, inv_temp, m->argmax, m->stats, st));
+    CK(logits_finalize_launch(m->z, m->V, M, inv_temp, m->argmax, m->stats, m->v0, m->amax, st));
+    ++nl;
+  }
+  const bool tp_cand = m->tp > 1 && cfg->mode == SM_ACCEPT_TYPICAL;
+  if (m->tp > 1) {  // vocabulary-parallel LM head: merge (argmax, stats, candidate logits) across ranks
+    CK(tp_merge_logits_launch(M, m->amax, m->argmax, m->stats, m->z, m->V, m->v0, kv->t->d_parent, kv->N,
+                              kv->tree_tok, tp_cand ? m->cand : nullptr, tp_next(m), st));
     ++nl;
   }
   AcceptArgs a;
@@ -800,6 +955,7 @@ static sm_status enqueue_accept(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg
   a.argmax = m->argmax;
   a.stats = m->stats;
   a.z = m->z;
+  a.cand = tp_cand ? m->cand : nullptr;
   a.len = kv->len;
   a.max_new = cfg->d_max_new;
   a.forced_path = cfg->d_forced_path;
@@ -843,7 +999,9 @@ extern "C" sm_status sm_verify(sm_model *m, sm_kv *kv, const int32_t *d_tree_tok
   int nl = 0;
   if (d_tree_tok != kv->tree_tok)
     CK(cudaMemcpyAsync(kv->tree_tok, d_tree_tok, (size_t)kv->b * kv->N * 4, cudaMemcpyDeviceToDevice, st));
+  tp_begin(m);
   CKS(enqueue_verify(m, kv, kv->tree_tok, st, nl));
+  CKS(tp_end(m, st, nl));
   if (d_logits)
     CK(cudaMemcpyAsync(d_logits, m->z, (size_t)kv->b * kv->N * m->V * 4, cudaMemcpyDeviceToDevice, st));
   kv->last_stream = st;
@@ -855,16 +1013,20 @@ extern "C" sm_status sm_accept(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg,
   if (!m || !kv) return fail(SM_ERR_INVALID_ARG, "sm_accept: bad arguments");
   CKS(check_accept(cfg, out));
   int nl = 0;
+  tp_begin(m);
   CKS(enqueue_accept(m, kv, cfg, out, (cudaStream_t)stream, nl));
+  CKS(tp_end(m, (cudaStream_t)stream, nl));
   kv->last_stream = (cudaStream_t)stream;
   return SM_OK;
 }
 
 static sm_status enqueue_step(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, const sm_accept_out *o,
                               cudaStream_t st, int &nl) {
+  tp_begin(m);
   CKS(enqueue_propose(m, kv, kv->tree_tok, nullptr, st, nl));
   CKS(enqueue_verify(m, kv, kv->tree_tok, st, nl));
   CKS(enqueue_accept(m, kv, cfg, o, st, nl));
+  CKS(tp_end(m, st, nl));
   return SM_OK;
 }
 

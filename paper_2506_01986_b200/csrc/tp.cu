@@ -1,0 +1,138 @@
+// tp.cu -- tensor-parallel exchanges outside the residual path (north star a7/e):
+// merging the vocabulary-parallel LM head statistics and the Medusa heads' top-K
+// candidates across ranks over peer memory, and the per-call epoch advance.
+// Protocol (see include/specmemo.h): a rank writes its payload into its own
+// symmetric buffer (data slot = exchange parity), fences system-wide, raises its
+// epoch flag in every peer's flags region, waits for the peers' flags, then reads
+// the peers' payloads and merges in rank order -- all ranks compute identical
+// results.  One CTA per exchange, so the waits can never depend on an unscheduled
+// CTA.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sm {
+
+SM_DEV void tp_exchange(const TpArgs &tp, long long ep, int slot) {
+  __threadfence_system();
+  __syncthreads();
+  const int q = threadIdx.x;
+  if (q < tp.t && q != tp.rank) {
+    st_release_sys(tp.flags[q] + (size_t)tp.rank * kTpFlagSlots + slot, ep);
+    tp_wait_flag(tp.flags[tp.rank] + (size_t)q * kTpFlagSlots + slot, ep, tp.err);
+  }
+  __syncthreads();
+}
+
+// payload per row: amax, argmax (bits), m, s, t, cand, -, -
+__global__ void __launch_bounds__(1024) tp_merge_logits_kernel(int rows, const float *amax, int32_t *argmax,
+                                                               float *stats, const float *z_local, int Vl, int v0,
+                                                               const int32_t *parent, int N, const int32_t *tok,
+                                                               float *cand, TpArgs tp) {
+  pdl_trigger();
+  pdl_wait();
+  const long long ep = *tp.seq + tp.point + 1;
+  const int r = threadIdx.x;
+  if (r < rows) {
+    float c = __int_as_float(0x7fc00000);  // NaN: this rank does not own the candidate token
+    if (tok) {
+      const int n = r % N, base = r - n;
+      if (n > 0) {
+        const int tk = tok[r];
+        if (tk >= v0 && tk < v0 + Vl) c = z_local[(size_t)(base + parent[n]) * Vl + (tk - v0)];
+      }
+    }
+    float4 *dst = reinterpret_cast<float4 *>(tp.data[tp.rank] + (size_t)r * 8);
+    __stcg(dst, make_float4(amax[r], __int_as_float(argmax[r]), stats[3 * r], stats[3 * r + 1]));
+    __stcg(dst + 1, make_float4(stats[3 * r + 2], c, 0.f, 0.f));
+  }
+  tp_exchange(tp, ep, 0);
+  if (r >= rows) return;
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  MST acc{-INFINITY, 0.f, 0.f};
+  float c = __int_as_float(0x7fc00000);
+  for (int q = 0; q < tp.t; ++q) {  // rank order (vocabulary order)
+    const float4 *src = reinterpret_cast<const float4 *>(tp.data[q] + (size_t)r * 8);
+    const float4 p0 = __ldcv(src), p1 = __ldcv(src + 1);
+    argmax_merge(bv, bi, p0.x, __float_as_int(p0.y));
+    acc = mst_merge(acc, MST{p0.z, p0.w, p1.x});
+    if (p1.y == p1.y) c = p1.y;
+  }
+  argmax[r] = bi;
+  stats[3 * r] = acc.m;
+  stats[3 * r + 1] = acc.s;
+  stats[3 * r + 2] = acc.t;
+  if (cand) cand[r] = c;
+}
+cudaError_t tp_merge_logits_launch(int rows, const float *amax, int32_t *argmax, float *stats, const float *z_local,
+                                   int Vl, int v0, const int32_t *parent, int N, const int32_t *tok, float *cand,
+                                   const TpArgs &tp, cudaStream_t st) {
+  if (rows > 1024) return cudaErrorInvalidValue;
+  return launch_pdl(tp_merge_logits_kernel, dim3(1), dim3(1024), 0, st, rows, amax, argmax, stats, z_local, Vl, v0,
+                    parent, N, tok, cand, tp);
+}
+
+// payload per entry (b, head): K values then K indices (bits)
+__global__ void __launch_bounds__(256) tp_merge_topk_kernel(int entries, int K, const float *vals,
+                                                            const int32_t *idx_local, int32_t *idx_out, TpArgs tp) {
+  pdl_trigger();
+  pdl_wait();
+  const long long ep = *tp.seq + tp.point + 1;
+  for (int e = threadIdx.x; e < entries; e += blockDim.x) {
+    float *dst = tp.data[tp.rank] + (size_t)e * 2 * K;
+    for (int k = 0; k < K; ++k) {
+      __stcg(dst + k, vals[(size_t)e * K + k]);
+      __stcg(dst + K + k, __int_as_float(idx_local[(size_t)e * K + k]));
+    }
+  }
+  tp_exchange(tp, ep, 0);
+  for (int e = threadIdx.x; e < entries; e += blockDim.x) {
+    uint32_t taken[kMaxTP] = {0};  // K <= 32 candidates per rank
+    for (int k = 0; k < K; ++k) {
+      float bv = -INFINITY;
+      int bi = 0x7fffffff, bq = -1, bk = -1;
+      for (int q = 0; q < tp.t; ++q) {
+        const float *src = tp.data[q] + (size_t)e * 2 * K;
+        for (int j = 0; j < K; ++j) {
+          if ((taken[q] >> j) & 1u) continue;
+          const float v = __ldcv(src + j);
+          const int ix = __float_as_int(__ldcv(src + K + j));
+          if (v != v) continue;  // NaN never wins (as in the single-GPU top-k)
+          if (bq < 0 || v > bv || (v == bv && ix < bi)) {
+            bv = v;
+            bi = ix;
+            bq = q;
+            bk = j;
+          }
+        }
+      }
+      if (bq >= 0) taken[bq] |= 1u << bk;
+      idx_out[(size_t)e * K + k] = bi;
+    }
+  }
+}
+cudaError_t tp_merge_topk_launch(int entries, int K, const float *vals, const int32_t *idx_local, int32_t *idx_out,
+                                 int nmed, int nb, const TpArgs &tp, cudaStream_t st) {
+  (void)nmed;
+  (void)nb;
+  if (K > 32) return cudaErrorInvalidValue;
+  return launch_pdl(tp_merge_topk_kernel, dim3(1), dim3(256), 0, st, entries, K, vals, idx_local, idx_out, tp);
+}
+
+__global__ void tp_advance_kernel(long long *seq, int n) {
+  pdl_trigger();
+  pdl_wait();
+  if (threadIdx.x == 0) *seq += n;
+}
+cudaError_t tp_advance_launch(long long *seq, int n, cudaStream_t st) {
+  return launch_pdl(tp_advance_kernel, dim3(1), dim3(32), 0, st, seq, n);
+}
+
+void tp_preload() {  // force-load (see gemm_preload)
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, tp_merge_logits_kernel);
+  cudaFuncGetAttributes(&fa, tp_merge_topk_kernel);
+  cudaFuncGetAttributes(&fa, tp_advance_kernel);
+}
+
+}  // namespace sm

@@ -41,3 +41,49 @@ def test_bench_reductions_gloo(world):
     for _, mx, sm in res:
         assert mx == 15.0            # max over ranks, not the rank's own time
         assert sm == 201.0           # value = tokens of all ranks / max time
+
+
+def _tp_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    import synth
+    from paper_2506_01986_b200 import tp_shard
+    # handle exchange (bench.peer_syms' plumbing) with stand-in 64-byte handles
+    hs = bench.exchange_handles(bytes([rank]) * 64, world)
+    sh = tp_shard(synth.model_cfg("llama70b"), rank, world)
+    shards = [None] * world
+    dist.all_gather_object(shards, sh)
+    q.put((rank, hs, shards))
+    dist.destroy_process_group()
+
+
+def test_tp_plumbing_gloo():
+    """world 2: every rank gets every rank's handle in rank order, and the ranks'
+    shards of the 70B shape tile heads, FFN features and vocabulary exactly."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tp_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for _, hs, shards in res:
+        assert hs == [bytes([r]) * 64 for r in range(world)]
+        for key, full in (("q_rows", 64 * 128), ("k_rows", 8 * 128), ("o_cols", 64 * 128), ("ffn", 28672),
+                          ("vocab", 32000)):
+            ranges = [s[key] for s in shards]
+            assert ranges[0][0] == 0 and ranges[-1][1] == full
+            assert all(ranges[i][1] == ranges[i + 1][0] for i in range(world - 1))
+
+
+def test_tp_shard_rejects_bad_sizes():
+    import synth
+    from paper_2506_01986_b200 import tp_shard
+    with pytest.raises(ValueError):
+        tp_shard(synth.model_cfg("llama70b"), 0, 3)
+    with pytest.raises(ValueError):
+        tp_shard(synth.model_cfg("tiny"), 0, 8)  # F = 256: 8 ranks x 64-row blocks do not fit
