@@ -223,6 +223,7 @@ def build_workload(sm, wl: dict, args, rank: int, world: int = 1, tp: int = 1):
     for i, p in enumerate(prompts):
         kv.prefill(i, torch.from_numpy(p).cuda())
     mode = sm.TYPICAL if wl["mode"] == "typical" else sm.GREEDY
+    kv.prompts = prompts
     return cfg, tree, model, kv, mode, lc_start
 
 
@@ -271,18 +272,20 @@ def run_ours(args, world, rank, local) -> dict | None:
 
     # ---- kernel timing pass (event-instrumented replay of the same graph)
     kv.profile(True)
-    g_ms, g_bytes, g_n, a_ms, a_n, lcs = [], [], 0, [], 0, []
+    g_ms, g_bytes, g_n, a_ms, a_n, lcs, s_ms = [], [], 0, [], 0, [], []
     for _ in range(args.prof_steps):
         lcs.append(float(kv.lengths().mean()))
         kv.step(acfg, out)
         n, gm, gb = kv.profile_read(0)
         na, am, _ = kv.profile_read(1)
+        s_ms.append(kv.profile_read(3)[1])
         g_ms.append(gm)
         g_bytes.append(gb)
         g_n, a_n = n, na
         a_ms.append(am)
     kv.profile(False)
     gemm_ms = statistics.median(g_ms)
+    step_prof_ms = statistics.median(s_ms) if s_ms else float("nan")
     gemm_bytes = g_bytes[0]
     attn_ms = statistics.median(a_ms)
     lc_prof = float(np.mean(lcs))
@@ -313,6 +316,33 @@ def run_ours(args, world, rank, local) -> dict | None:
     e_ms = reduce_max(e0.elapsed_time(e1), world)
     e2e_val = (reduce_sum(e2e_tokens, world) if tp == 1 else e2e_tokens) / (e_ms / 1e3)
 
+    # ---- vanilla greedy decoding on the same kernels and model: a 1-node tree (root
+    # only: verify one row, accept the argmax) -- the speculative speed-up's denominator
+    van = None
+    if args.vanilla and tp == 1:
+        vtree = sm.Tree([], topk=synth.TOPK)
+        kv_v = sm.KVCache(model, vtree, b, wl["x"])
+        for i, p in enumerate(kv.prompts):
+            kv_v.prefill(i, torch.from_numpy(p).cuda())
+        vout = sm.AcceptOut(b, 0)
+        vcfg = sm.accept_cfg(sm.GREEDY)
+        vsteps = min(args.steps, 50)
+        for _ in range(3):
+            kv_v.step(vcfg, vout)
+        torch.cuda.synchronize()
+        V0 = kv_v.lengths().astype(np.int64)
+        v0e, v1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        v0e.record(st)
+        for _ in range(vsteps):
+            kv_v.step(vcfg, vout)
+        v1e.record(st)
+        torch.cuda.synchronize()
+        vms = reduce_max(v0e.elapsed_time(v1e), world)
+        vtok = reduce_sum(float((kv_v.lengths().astype(np.int64) - V0).sum()), world)
+        van = {"value": round(vtok / (vms / 1e3), 3), "unit": "tokens/s", "ms_per_step": round(vms / vsteps, 4),
+               "steps": vsteps, "what": "greedy, 1-node tree (no heads) on the same model and kernels"}
+        del kv_v
+
     # ---- K1 tree-attention point of the C5 sweep (geometry A, N=64)
     k1 = run_k1_point(sm, args) if args.k1 and args.config == "c2" else None
 
@@ -339,7 +369,9 @@ def run_ours(args, world, rank, local) -> dict | None:
                      "achieved": round(gemm_gbs, 1), "peak": pk["hbm"], "unit": "GB/s",
                      "frac": round(gemm_gbs / pk["hbm"], 4), "traffic": gemm_traffic(),
                      "launches_per_step": g_n, "ms_per_step": round(gemm_ms, 4),
-                     "share_of_step": round(gemm_ms / ms_step, 4), "alg_bytes_per_step": gemm_bytes,
+                     "share_of_step": round(gemm_ms / ms_step, 4),
+                     "share_of_profiled_step": round(gemm_ms / step_prof_ms, 4),
+                     "alg_bytes_per_step": gemm_bytes,
                      "peak_source": pk["src"], "timing": "CUDA events around each launch inside the step graph"},
         "step_roofline": {"bound": "hbm", "alg_bytes": sb, "roofline_ms": round(sb / pk["hbm"] / 1e6, 4),
                           "frac": round(sb / pk["hbm"] / 1e6 / ms_step, 4)},
@@ -351,6 +383,9 @@ def run_ours(args, world, rank, local) -> dict | None:
         "gpu_launches": launches * args.steps,
         "clocks": clk,
     }
+    if van:
+        van["speculative_speedup"] = round(value / van["value"], 3)
+        res["vanilla"] = van
     if k1:
         res["k1_point"] = k1
     return res
@@ -489,6 +524,7 @@ def main():
     ap.add_argument("--lc-start", type=int, default=1024)
     ap.add_argument("--prof-steps", type=int, default=5)
     ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--no-vanilla", dest="vanilla", action="store_false", help="skip the vanilla (1-node) timing")
     ap.add_argument("--no-k1", dest="k1", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu", action="store_false")
     args = ap.parse_args()

@@ -203,8 +203,9 @@ sm_status sm_step(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, const sm_acc
 sm_status sm_step_launches(const sm_kv *kv, int *n);
 /* Kernel timing for the bench's roofline: with enable = 1 the next sm_step
  * captures (and then replays) a graph variant that brackets every K2 GEMM
- * launch (kind 0) and every K1 tree-attention launch + combine (kind 1) with
- * CUDA events on the launch stream.  sm_profile_read synchronises and returns,
+ * launch (kind 0), every K1 tree-attention launch + combine (kind 1) and the
+ * whole step (kind 3) with CUDA events on the launch stream (the events
+ * serialise the launches they bracket).  sm_profile_read synchronises and returns,
  * for the most recent replay, the number of bracketed launches, their summed
  * duration in ms, and (kind 0) the algorithmic bytes W + X + Y(fp32) of those
  * launches.                                                                   */

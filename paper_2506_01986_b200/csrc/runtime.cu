@@ -316,7 +316,7 @@ static GemmArgs gemm_proto(int N, int K, int batch) {
 
 // ---------------------------------------------------------------- in-graph kernel timing
 struct ProfEvent {
-  int kind;  // 0 = K2 GEMM, 1 = K1 tree attention (+ combine)
+  int kind;  // 0 = K2 GEMM, 1 = K1 tree attention (+ combine), 3 = whole step
   cudaEvent_t a, b;
   double bytes;
 };
@@ -1057,7 +1057,10 @@ extern "C" sm_status sm_step(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, c
       g_prof = &kv->prof_events;
     }
     CK(cudaStreamBeginCapture(m->cap_stream, cudaStreamCaptureModeRelaxed));
+    cudaEvent_t ev_step = nullptr;
+    prof_begin(m->cap_stream, &ev_step);  // kind 3: the whole (event-serialised) step
     sm_status s = enqueue_step(m, kv, cfg, out, m->cap_stream, nl);
+    prof_end(m->cap_stream, ev_step, 3, 0.0);
     cudaError_t e = cudaStreamEndCapture(m->cap_stream, &g);
     g_prof = nullptr;
     if (s != SM_OK) return s;

@@ -1,0 +1,76 @@
+"""C5 tree-attention sweep (BASELINE configs[4]) on the GPU box.
+
+python tools/k1_sweep.py [--quick] > profiles/r01_k1_sweep.txt
+Geometry A = one 7B layer (H = Hkv = 32), geometry B = one 70B TP8 shard (8 q / 1 kv),
+head_dim 128, tree N in {16, 64, 256}, Lc in {512, 4096, 32768}, batch in {1, 8, 32}
+(bounded to <= 8 GB of K/V per set).  Each point: 20 launches captured in a CUDA graph
+over two alternating buffer sets (> L2), replayed; device time per launch; achieved
+GB/s = algorithmic bytes (K/V of [0, Lc) + tree slots once, Q in, O out) / time."""
+import argparse
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2506_01986_b200 as sm  # noqa: E402
+import synth  # noqa: E402
+
+PEAK = 6549.1
+ap = argparse.ArgumentParser()
+ap.add_argument("--quick", action="store_true")
+ap.add_argument("--tc", type=int, default=1)
+a = ap.parse_args()
+sm.set_option("attn_tc", a.tc)
+trees = {16: sm.Tree(synth.SWEEP_TREES[16]), 64: sm.Tree(synth.V64), 256: sm.Tree(synth.SWEEP_TREES[256])}
+geoms = [("A 32/32", 32, 32), ("B 8/1", 8, 1)]
+Ns = [16, 64, 256]
+Lcs = [512, 4096, 32768]
+bs = [1, 8, 32]
+if a.quick:
+    Ns, Lcs, bs = [64], [512, 4096], [1, 8]
+print(f"{'geom':8s} {'b':>3s} {'N':>4s} {'Lc':>6s} {'MB':>8s} {'us':>9s} {'GB/s':>8s} {'frac':>6s}")
+hd = 128
+for gname, H, Hkv in geoms:
+    for b in bs:
+        for N in Ns:
+            for Lc in Lcs:
+                tree = trees[N]
+                cap = Lc + tree.N
+                kv_bytes = b * Hkv * cap * hd * 2 * 2
+                if kv_bytes > 8e9:
+                    continue
+                sets = []
+                for _ in range(2):
+                    q = torch.randn(b, tree.N, H, hd, device="cuda").bfloat16()
+                    k = torch.randn(b, Hkv, cap, hd, device="cuda").bfloat16()
+                    v = torch.randn(b, Hkv, cap, hd, device="cuda").bfloat16()
+                    sets.append((q, k, v, torch.empty_like(q)))
+                L = torch.full((b,), Lc, dtype=torch.int32, device="cuda")
+                for i in range(2):
+                    q, k, v, o = sets[i]
+                    sm.tree_attention(tree, q, k, v, L, H, Hkv, o)
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                st = torch.cuda.Stream()
+                with torch.cuda.stream(st):
+                    g.capture_begin()
+                    for i in range(20):
+                        q, k, v, o = sets[i % 2]
+                        sm.tree_attention(tree, q, k, v, L, H, Hkv, o, stream=st)
+                    g.capture_end()
+                g.replay()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(3):
+                    g.replay()
+                e1.record()
+                torch.cuda.synchronize()
+                us = e0.elapsed_time(e1) * 1e3 / 60
+                alg = b * Hkv * (Lc + tree.N) * hd * 2 * 2 + 2 * b * tree.N * H * hd * 2
+                gbs = alg / us / 1e3
+                print(f"{gname:8s} {b:3d} {tree.N:4d} {Lc:6d} {alg / 1e6:8.1f} {us:9.1f} {gbs:8.1f} {gbs / PEAK:6.3f}",
+                      flush=True)
+                del sets, g
+                torch.cuda.empty_cache()
