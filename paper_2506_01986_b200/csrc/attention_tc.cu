@@ -365,21 +365,23 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
     }
     if (threadIdx.x == 0) SM_STAMP(6);
     const float fin_m = live ? m_run : -INFINITY, fin_l = live ? l : 0.f;
-    if (a.nsplit == 1 && live && ntiles > 0) {
-      const float inv = 1.f / l;
+    if (a.nsplit == 1 && warp_live && ntiles > 0) {  // warp-uniform: tcgen05.ld is .sync.aligned
+      const float inv = live ? 1.f / l : 0.f;
       bf16 *dst = a.out + (((long long)sl * a.Nq + rr / a.G) * a.H + (long long)h * a.G + rr % a.G) * HD;
 #pragma unroll
       for (int c0 = 0; c0 < HD; c0 += 32) {
         float o[32];
         tmem_ld32_f(lane_base + 2 * KEYS + c0, o);
+        if (live) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint4 w;
-          w.x = pack_bf16(o[8 * c] * inv, o[8 * c + 1] * inv);
-          w.y = pack_bf16(o[8 * c + 2] * inv, o[8 * c + 3] * inv);
-          w.z = pack_bf16(o[8 * c + 4] * inv, o[8 * c + 5] * inv);
-          w.w = pack_bf16(o[8 * c + 6] * inv, o[8 * c + 7] * inv);
-          reinterpret_cast<uint4 *>(dst + c0)[c] = w;
+          for (int c = 0; c < 4; ++c) {
+            uint4 w;
+            w.x = pack_bf16(o[8 * c] * inv, o[8 * c + 1] * inv);
+            w.y = pack_bf16(o[8 * c + 2] * inv, o[8 * c + 3] * inv);
+            w.z = pack_bf16(o[8 * c + 4] * inv, o[8 * c + 5] * inv);
+            w.w = pack_bf16(o[8 * c + 6] * inv, o[8 * c + 7] * inv);
+            reinterpret_cast<uint4 *>(dst + c0)[c] = w;
+          }
         }
       }
     } else if (a.nsplit > 1) {

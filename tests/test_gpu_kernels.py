@@ -99,6 +99,9 @@ ATTN_CASES = [
     ("chain256_hd128", None, 256, 1, 8, 2, 128, [129], 0),
     ("split8_long", synth.SWEEP_TREES[16], None, 1, 1, 1, 128, [4000], 2),
     ("gqa4_v64_c2like", synth.V64, None, 2, 8, 2, 128, [1024, 1500], 0),
+    # one split (no cluster) with padding rows inside a live warp (16 or 48 live rows of 128)
+    ("n16_ns1_mha", synth.SWEEP_TREES[16], None, 4, 32, 32, 128, [512, 100, 7, 300], 0),
+    ("n16_ns1_g3", synth.TINY16, None, 20, 24, 8, 128, [(37 * i) % 300 for i in range(20)], 1),
 ]
 
 
