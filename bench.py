@@ -178,7 +178,8 @@ WORKLOADS = {
                     "42 leaves), bs=1 per GPU, KV bounded to x=2048 (+64 scratch), greedy"),
     "c1": dict(model="tiny", n_medusa=3, tree="TINY16", batch=1, x=64, mode="greedy", prompt=32,
                desc="C1: tiny random-init Llama (2 layers, d=64, 4 heads, V=256) + 3 Medusa heads, 16-node tree, "
-                    "bs=1, 32-token prompt, KV x=64"),
+                    "bs=1, 32-token prompt; KV x=64 in the parity tests, raised here to 32 + (l+1) x steps so every "
+                    "timed step emits"),
     "c3": dict(model="vicuna13b", n_medusa=4, tree="V64", batch=1, x=2304, mode="typical",
                desc="C3: Vicuna-13B-shaped + 4 Medusa heads, V64 tree, bs=1, mid-conversation of an 8-turn "
                     "MT-Bench-length chat (KV bounded to 2304 = sum of turns), typical acceptance T=0.7 eps=0.09 "
@@ -198,6 +199,10 @@ def build_workload(sm, wl: dict, args, rank: int, world: int = 1, tp: int = 1):
     choices = {"V64": synth.V64, "TINY16": synth.TINY16}[wl["tree"]]
     tree = sm.Tree(choices, topk=synth.TOPK)
     b, x = wl["batch"], wl["x"]
+    total_steps = args.warmup + args.steps + args.prof_steps + args.e2e_steps + 8
+    if "prompt" in wl:  # C1's x = 64 holds one 32-token turn; timing runs many steps, so the bound
+        x = max(x, wl["prompt"] + (tree.depth + 1) * total_steps)  # grows to P + (l+1) * steps
+    wl["x_run"] = x
     R = max(b * tree.N, 256)
     peers = None
     if tp > 1:
@@ -210,7 +215,6 @@ def build_workload(sm, wl: dict, args, rank: int, world: int = 1, tp: int = 1):
     model = sm.Model(cfg, W, max_rows=R, max_batch=b, max_seq_len=x + tree.N, peer_sym=peers)
     barrier(world)  # every rank's model exists (its buffer zeroed) before any exchange
     kv = sm.KVCache(model, tree, b, x)
-    total_steps = args.warmup + args.steps + args.prof_steps + args.e2e_steps + 8
     if b == 1:
         if "prompt" in wl:
             lc_start = wl["prompt"]
@@ -321,7 +325,7 @@ def run_ours(args, world, rank, local) -> dict | None:
     van = None
     if args.vanilla and tp == 1:
         vtree = sm.Tree([], topk=synth.TOPK)
-        kv_v = sm.KVCache(model, vtree, b, wl["x"])
+        kv_v = sm.KVCache(model, vtree, b, wl["x_run"])
         for i, p in enumerate(kv.prompts):
             kv_v.prefill(i, torch.from_numpy(p).cuda())
         vout = sm.AcceptOut(b, 0)
@@ -359,7 +363,7 @@ def run_ours(args, world, rank, local) -> dict | None:
         "scaling": "strong" if tp > 1 else "weak",
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic: counter-hash random-init weights (std 0.02), counter-hash prompt tokens",
-        "config": {"workload": wl["desc"], "global_batch": b if tp > 1 else world * b, "seq_len": wl["x"],
+        "config": {"workload": wl["desc"], "global_batch": b if tp > 1 else world * b, "seq_len": wl["x_run"],
                    "lc_start": lc_start, "lc_mean": lc_mean,
                    "parallelism": f"tp{tp} (peer-memory exchanges)" if tp > 1 else
                    (f"replicas x{world}" if world > 1 else "single GPU"),

@@ -71,10 +71,20 @@ void sm_tree_destroy(sm_tree *t);
 typedef struct {
   int n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ffn, vocab, n_medusa;
   float rms_eps, rope_theta;
-  int max_rows;      /* max token rows per forward (b*N; prefill chunks use <= 256), <= 1024 */
+  int max_rows;      /* max token rows per forward (b*N; prefill chunks use <= 256), <= 1024
+                        (<= 341 with SM_DTYPE_FP32)                               */
   int max_batch;     /* max sequences b                                          */
   int max_seq_len;   /* max positions (RoPE table length) = x + N                */
+  int dtype;         /* SM_DTYPE_BF16 (0, default): bf16 activations and K/V, fp32
+                        accumulation (rounding contract R0..R10).
+                        SM_DTYPE_FP32 (1): fp32 parity mode (north star: logits and
+                        KV within 1e-4 of the oracle's fp32 mode) -- activations,
+                        K/V and softmax in fp32; the weights stay the same bf16
+                        tensors (R0); each GEMM multiplies the three exact bf16
+                        planes of its fp32 input on the tensor cores.  tp_size 1 only. */
 } sm_model_cfg;
+#define SM_DTYPE_BF16 0
+#define SM_DTYPE_FP32 1
 
 /* Device pointers to bf16 weights ([out][in]); arrays are host arrays of
  * device pointers, one entry per layer / Medusa head.  Medusa-1 head i:
@@ -149,9 +159,10 @@ sm_status sm_generate_bf16_2d(void *d_dst, int rows, int cols, int full_cols, in
 
 /* ------------------------------------------------------------------ bounded KV cache
  * Eq. 1 with d restored (reading Q14): bytes =
- *   2 * layers * batch * kv_heads/tp * head_dim * (max_seq_len + tree_nodes) * 2.
+ *   2 * layers * batch * kv_heads/tp * head_dim * (max_seq_len + tree_nodes) * w,
+ * w = 2 (bf16) or 4 (cfg->dtype == SM_DTYPE_FP32).
  * The last N slots of each sequence are the tree scratch ("scratch space").
- * Layout: [layer][K|V][b][Hkv][x+N][hd] bf16.                                  */
+ * Layout: [layer][K|V][b][Hkv][x+N][hd] of bf16 (fp32 in the parity mode).      */
 sm_status sm_kv_bytes(const sm_model_cfg *cfg, int tp_size, int batch, int max_seq_len, int tree_nodes,
                       size_t *bytes);
 /* Bind caller memory (>= sm_kv_bytes) as the cache of `batch` sequences for

@@ -16,6 +16,10 @@ Numeric modes
   "bf16"  -- float64 arithmetic, rounded to bf16 (RNE) / fp32 exactly at the
              storage points of the rounding contract R0..R10,
              i.e. where the GPU path stores a bf16 or fp32 tensor.
+  "fp32"  -- the fp32 parity mode (north star: logits and KV within 1e-4):
+             float64 arithmetic rounded to fp32 at every storage point (the
+             GPU's fp32 mode keeps activations, K/V and logits in fp32; the
+             weights are the same bf16-valued tensors, R0).
 
 Every token row goes through the same ``forward_row`` so that a tree node's
 row is bit-identical to the sequential-decoding row of the same token at the
@@ -83,7 +87,7 @@ class Weights:
 # ----------------------------------------------------------------- model
 class Model:
     def __init__(self, cfg: dict, weights: Weights, mode: str = "bf16"):
-        assert mode in ("bf16", "fp64")
+        assert mode in ("bf16", "fp32", "fp64")
         self.cfg = cfg
         self.W = weights
         self.mode = mode
@@ -98,10 +102,13 @@ class Model:
 
     # storage points
     def r16(self, x):
-        return round_bf16(x) if self.mode == "bf16" else np.asarray(x, dtype=np.float64)
+        """A bf16 storage point of the rounding contract (fp32 storage in "fp32" mode)."""
+        if self.mode == "bf16":
+            return round_bf16(x)
+        return round_f32(x) if self.mode == "fp32" else np.asarray(x, dtype=np.float64)
 
     def r32(self, x):
-        return round_f32(x) if self.mode == "bf16" else np.asarray(x, dtype=np.float64)
+        return round_f32(x) if self.mode != "fp64" else np.asarray(x, dtype=np.float64)
 
     # building blocks ----------------------------------------------------
     def rmsnorm(self, x, g):
@@ -116,7 +123,7 @@ class Model:
         i = np.arange(half, dtype=np.float64)
         ang = pos * self.theta ** (-2.0 * i / self.hd)
         c, s = np.cos(ang), np.sin(ang)
-        if self.mode == "bf16":  # GPU tables are fp64-built, stored fp32 (R3)
+        if self.mode != "fp64":  # GPU tables are fp64-built, stored fp32 (R3)
             c, s = round_f32(c), round_f32(s)
         x1, x2 = v[:, :half], v[:, half:]
         return np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], axis=1)

@@ -61,7 +61,10 @@ class ModelCfg(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int) for n in ("n_layers", "d_model", "n_heads", "n_kv_heads", "head_dim", "d_ffn",
                                             "vocab", "n_medusa")] + \
                [("rms_eps", ctypes.c_float), ("rope_theta", ctypes.c_float)] + \
-               [(n, ctypes.c_int) for n in ("max_rows", "max_batch", "max_seq_len")]
+               [(n, ctypes.c_int) for n in ("max_rows", "max_batch", "max_seq_len", "dtype")]
+
+
+DTYPES = {"bf16": 0, "fp32": 1}  # sm_model_cfg.dtype: bf16 path / fp32 parity mode
 
 
 _PP = ctypes.POINTER(ctypes.c_void_p)
@@ -272,10 +275,11 @@ class Model:
     be constructed before any rank issues work."""
 
     def __init__(self, cfg: dict, weights: dict, max_rows: int, max_batch: int, max_seq_len: int,
-                 peer_sym: list | None = None):
+                 peer_sym: list | None = None, dtype: str = "bf16"):
         c = ModelCfg(cfg["n_layers"], cfg["d_model"], cfg["n_heads"], cfg["n_kv_heads"], cfg["head_dim"],
                      cfg["d_ffn"], cfg["vocab"], len(weights["medusa"]), cfg.get("rms_eps", 1e-5),
-                     cfg.get("rope_theta", 1e4), max_rows, max_batch, max_seq_len)
+                     cfg.get("rope_theta", 1e4), max_rows, max_batch, max_seq_len, DTYPES[dtype])
+        self.dtype = dtype
         L = cfg["n_layers"]
         arr = lambda key: (ctypes.c_void_p * max(1, L))(*[_ptr(l[key]) for l in weights["layers"]])  # noqa: E731
         marr = lambda key: (ctypes.c_void_p * max(1, len(weights["medusa"])))(  # noqa: E731
@@ -309,9 +313,9 @@ class Model:
             _lib.sm_model_destroy(self._h)
 
 
-def kv_bytes(cfg: dict, batch: int, max_seq_len: int, tree_nodes: int, tp_size: int = 1) -> int:
+def kv_bytes(cfg: dict, batch: int, max_seq_len: int, tree_nodes: int, tp_size: int = 1, dtype: str = "bf16") -> int:
     c = ModelCfg(cfg["n_layers"], cfg["d_model"], cfg["n_heads"], cfg["n_kv_heads"], cfg["head_dim"], cfg["d_ffn"],
-                 cfg["vocab"], 0, 1e-5, 1e4, 1, 1, 1)
+                 cfg["vocab"], 0, 1e-5, 1e4, 1, 1, 1, DTYPES[dtype])
     out = ctypes.c_size_t()
     _check(lib().sm_kv_bytes(ctypes.byref(c), tp_size, batch, max_seq_len, tree_nodes, ctypes.byref(out)))
     return out.value
@@ -340,17 +344,20 @@ class KVCache:
     def __init__(self, model: Model, tree: Tree, batch: int, max_seq_len: int):
         import torch
         self.model, self.tree, self.batch, self.x = model, tree, batch, max_seq_len
-        self.nbytes = kv_bytes(model.cfg, batch, max_seq_len, tree.N, model.tp_size)
+        self.nbytes = kv_bytes(model.cfg, batch, max_seq_len, tree.N, model.tp_size, model.dtype)
         self.mem = torch.empty(self.nbytes // 2, dtype=torch.bfloat16, device="cuda")
         self._h = ctypes.c_void_p()
         _check(lib().sm_kv_bind(model._h, tree._h, batch, max_seq_len, ctypes.c_void_p(_ptr(self.mem)),
                                 ctypes.c_size_t(self.nbytes), ctypes.byref(self._h)))
 
     def layout(self):
-        """[L][2][b][Hkv/tp][x+N][hd] view of the cache memory (this rank's kv heads)."""
+        """[L][2][b][Hkv/tp][x+N][hd] view of the cache memory (this rank's kv heads;
+        bf16, or fp32 in the parity mode)."""
+        import torch
         c = self.model.cfg
-        return self.mem.view(c["n_layers"], 2, self.batch, c["n_kv_heads"] // self.model.tp_size,
-                             self.x + self.tree.N, c["head_dim"])
+        mem = self.mem.view(torch.float32) if self.model.dtype == "fp32" else self.mem
+        return mem.view(c["n_layers"], 2, self.batch, c["n_kv_heads"] // self.model.tp_size,
+                        self.x + self.tree.N, c["head_dim"])
 
     def lengths(self) -> np.ndarray:
         out = np.zeros(self.batch, np.int32)

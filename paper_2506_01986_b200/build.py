@@ -14,7 +14,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libspecmemo.so")
 LIB_TRACE = os.path.join(HERE, "libspecmemo_trace.so")
-SOURCES = ["gemm.cu", "attention.cu", "attention_tc.cu", "epilogue.cu", "decode.cu", "tp.cu", "runtime.cu"]
+SOURCES = ["gemm.cu", "attention.cu", "attention_tc.cu", "attention_f32.cu", "epilogue.cu", "decode.cu", "tp.cu", "runtime.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

@@ -15,6 +15,8 @@
 // next launch immediately and wait for their producer before touching memory.
 #include <float.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -58,7 +60,7 @@ cudaError_t embed_launch(const int32_t *tok, const bf16 *E, float *x, int M, int
 constexpr int kNormThreads = 256;
 constexpr int kNormCols = 4 * kNormThreads;
 __global__ void __launch_bounds__(kNormThreads) resid_norm_kernel(PartialView pv, int has_pv, float *x, const bf16 *g,
-                                                                  bf16 *h, int d, float eps) {
+                                                                  bf16 *h, int d, float eps, int hp) {
   __shared__ float red[kNormThreads / 32];
   __shared__ float ssq[8];  // ssq[q] = block sum of cluster rank q
   pdl_trigger();
@@ -71,13 +73,14 @@ __global__ void __launch_bounds__(kNormThreads) resid_norm_kernel(PartialView pv
   if (i < d) {
     float4 ys[16];
     SkRef ref{};
-    if (has_pv) {
+    if (has_pv && pv.planes <= 1) {
       ref = sk_ref(pv, 0, m, i);
       sk_load<16>(ref, ys);
     }
     a = *reinterpret_cast<const float4 *>(xr + i);
     if (has_pv) {
-      const float4 y = sk_reduce<16>(ref, ys);  // R5/R7: fp32 residual += fp32 projection
+      // R5/R7: fp32 residual += fp32 projection
+      const float4 y = pv.planes <= 1 ? sk_reduce<16>(ref, ys) : sk_get4(pv, 0, m, i);
       a.x += y.x;
       a.y += y.y;
       a.z += y.z;
@@ -95,20 +98,18 @@ __global__ void __launch_bounds__(kNormThreads) resid_norm_kernel(PartialView pv
   if (i < d) {
     const __nv_bfloat162 g01 = *reinterpret_cast<const __nv_bfloat162 *>(g + i);
     const __nv_bfloat162 g23 = *reinterpret_cast<const __nv_bfloat162 *>(g + i + 2);
-    uint2 o;
-    o.x = pack_bf16(a.x * rs * __low2float(g01), a.y * rs * __high2float(g01));
-    o.y = pack_bf16(a.z * rs * __low2float(g23), a.w * rs * __high2float(g23));
-    *reinterpret_cast<uint2 *>(h + (size_t)m * d + i) = o;
+    store_act4(h, hp, m, d, i, a.x * rs * __low2float(g01), a.y * rs * __high2float(g01),
+               a.z * rs * __low2float(g23), a.w * rs * __high2float(g23));
   }
 }
 cudaError_t resid_norm_launch(const PartialView *pv, float *x, const bf16 *g, bf16 *h, int M, int d, float eps,
-                              cudaStream_t st) {
+                              int hp, cudaStream_t st) {
   const int cs = (d + kNormCols - 1) / kNormCols;
   if (cs > 8 || d % 4) return cudaErrorInvalidValue;
   PartialView v{};
   if (pv) v = *pv;
   return launch_pdl_cluster(resid_norm_kernel, dim3(cs, M), dim3(kNormThreads), 0, st, cs, v, pv ? 1 : 0, x, g, h, d,
-                            eps);
+                            eps, hp);
 }
 
 // Tensor-parallel variant (a7): the residual all-reduce fused in.  Each rank reduces
@@ -201,8 +202,12 @@ cudaError_t resid_norm_tp_launch(const PartialView &pv, float *x, const bf16 *g,
 
 // ------------------------------------------------------------------ QKV consumer (RoPE + cache write)
 // thread -> 4 consecutive rotary pairs (c .. c+3) of one head of one token row
+// F32 (fp32 parity mode): q and the K/V cache hold fp32, partial rows come in 3 planes.
+template <bool F32>
 __global__ void __launch_bounds__(256) qkv_consumer_kernel(PartialView pv, RowCtx rc, int H, int Hkv, int hd,
-                                                           const float2 *rope, bf16 *q, bf16 *kc, bf16 *vc, int cap) {
+                                                           const float2 *rope, void *q_, void *kc_, void *vc_, int cap) {
+  using T = typename std::conditional<F32, float, bf16>::type;
+  T *q = static_cast<T *>(q_), *kc = static_cast<T *>(kc_), *vc = static_cast<T *>(vc_);
   pdl_trigger();
   pdl_wait();
   const int m = blockIdx.y;
@@ -212,12 +217,18 @@ __global__ void __launch_bounds__(256) qkv_consumer_kernel(PartialView pv, RowCt
   if (idx >= (H + 2 * Hkv) * quads) return;
   const int hh = idx / quads, c = (idx % quads) * 4;
   const int n0 = hh * hd + c;
-  const SkRef ra = sk_ref(pv, 0, m, n0), rb = sk_ref(pv, 0, m, n0 + half);
-  float4 xa[8], xb[8];
-  sk_load<8>(ra, xa);
-  sk_load<8>(rb, xb);
-  const float4 a = sk_reduce<8>(ra, xa);
-  const float4 b = sk_reduce<8>(rb, xb);
+  float4 a, b;
+  if constexpr (F32) {
+    a = sk_get4(pv, 0, m, n0);
+    b = sk_get4(pv, 0, m, n0 + half);
+  } else {
+    const SkRef ra = sk_ref(pv, 0, m, n0), rb = sk_ref(pv, 0, m, n0 + half);
+    float4 xa[8], xb[8];
+    sk_load<8>(ra, xa);
+    sk_load<8>(rb, xb);
+    a = sk_reduce<8>(ra, xa);
+    b = sk_reduce<8>(rb, xb);
+  }
   float x0[4] = {a.x, a.y, a.z, a.w}, x1[4] = {b.x, b.y, b.z, b.w};
   const int sl = m / rc.Nq, node = m % rc.Nq;
   const int seq = rc.seq_base + sl;
@@ -233,7 +244,7 @@ __global__ void __launch_bounds__(256) qkv_consumer_kernel(PartialView pv, RowCt
       x1[e] = y1;
     }
   }
-  bf16 *dst;
+  T *dst;
   if (hh < H) {
     dst = q + ((size_t)m * H + hh) * hd;
   } else if (hh < H + Hkv) {
@@ -241,19 +252,27 @@ __global__ void __launch_bounds__(256) qkv_consumer_kernel(PartialView pv, RowCt
   } else {
     dst = vc + (((size_t)seq * Hkv + (hh - H - Hkv)) * cap + Lc + node) * hd;
   }
-  uint2 lo, hi;
-  lo.x = pack_bf16(x0[0], x0[1]);
-  lo.y = pack_bf16(x0[2], x0[3]);
-  hi.x = pack_bf16(x1[0], x1[1]);
-  hi.y = pack_bf16(x1[2], x1[3]);
-  *reinterpret_cast<uint2 *>(dst + c) = lo;
-  *reinterpret_cast<uint2 *>(dst + c + half) = hi;
+  if constexpr (F32) {
+    *reinterpret_cast<float4 *>(dst + c) = make_float4(x0[0], x0[1], x0[2], x0[3]);
+    *reinterpret_cast<float4 *>(dst + c + half) = make_float4(x1[0], x1[1], x1[2], x1[3]);
+  } else {
+    uint2 lo, hi;
+    lo.x = pack_bf16(x0[0], x0[1]);
+    lo.y = pack_bf16(x0[2], x0[3]);
+    hi.x = pack_bf16(x1[0], x1[1]);
+    hi.y = pack_bf16(x1[2], x1[3]);
+    *reinterpret_cast<uint2 *>(dst + c) = lo;
+    *reinterpret_cast<uint2 *>(dst + c + half) = hi;
+  }
 }
-cudaError_t qkv_consumer_launch(const PartialView &pv, RowCtx rc, int H, int Hkv, int hd, const float2 *rope, bf16 *q,
-                                bf16 *kcache, bf16 *vcache, int cap, cudaStream_t st) {
+cudaError_t qkv_consumer_launch(const PartialView &pv, RowCtx rc, int H, int Hkv, int hd, const float2 *rope, void *q,
+                                void *kcache, void *vcache, int cap, cudaStream_t st) {
   const int work = (H + 2 * Hkv) * (hd / 8);
-  return launch_pdl(qkv_consumer_kernel, dim3((work + 255) / 256, rc.M), dim3(256), 0, st, pv, rc, H, Hkv, hd, rope,
-                    q, kcache, vcache, cap);
+  if (pv.planes > 1)
+    return launch_pdl(qkv_consumer_kernel<true>, dim3((work + 255) / 256, rc.M), dim3(256), 0, st, pv, rc, H, Hkv, hd,
+                      rope, q, kcache, vcache, cap);
+  return launch_pdl(qkv_consumer_kernel<false>, dim3((work + 255) / 256, rc.M), dim3(256), 0, st, pv, rc, H, Hkv, hd,
+                    rope, q, kcache, vcache, cap);
 }
 
 // ------------------------------------------------------------------ SiLU(gate) * up
@@ -265,20 +284,23 @@ __global__ void __launch_bounds__(256) silu_consumer_kernel(PartialView pv, int 
   const int f = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (f >= F) return;
   const int ng = (f >> 6) * 128 + (f & 63);
-  const SkRef rg = sk_ref(pv, 0, m, ng), ru = sk_ref(pv, 0, m, ng + 64);
-  float4 xg[8], xu[8];
-  sk_load<8>(rg, xg);
-  sk_load<8>(ru, xu);
-  const float4 g = sk_reduce<8>(rg, xg);
-  const float4 u = sk_reduce<8>(ru, xu);
+  float4 g, u;
+  if (pv.planes > 1) {
+    g = sk_get4(pv, 0, m, ng);
+    u = sk_get4(pv, 0, m, ng + 64);
+  } else {
+    const SkRef rg = sk_ref(pv, 0, m, ng), ru = sk_ref(pv, 0, m, ng + 64);
+    float4 xg[8], xu[8];
+    sk_load<8>(rg, xg);
+    sk_load<8>(ru, xu);
+    g = sk_reduce<8>(rg, xg);
+    u = sk_reduce<8>(ru, xu);
+  }
   const float gg[4] = {g.x, g.y, g.z, g.w}, uu[4] = {u.x, u.y, u.z, u.w};
   float o[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) o[e] = gg[e] / (1.0f + expf(-gg[e])) * uu[e];
-  uint2 w;
-  w.x = pack_bf16(o[0], o[1]);
-  w.y = pack_bf16(o[2], o[3]);
-  *reinterpret_cast<uint2 *>(act + (size_t)m * F + f) = w;
+  store_act4(act, pv.planes, m, F, f, o[0], o[1], o[2], o[3]);
 }
 cudaError_t silu_consumer_launch(const PartialView &pv, int F, bf16 *act, cudaStream_t st) {
   return launch_pdl(silu_consumer_kernel, dim3((F / 4 + 255) / 256, pv.M), dim3(256), 0, st, pv, F, act);
@@ -301,7 +323,7 @@ __global__ void __launch_bounds__(512) logits_kernel(PartialView pv, const float
   for (int j = threadIdx.x * 4; j < V; j += blockDim.x * 4) {
     float4 z4;
     if constexpr (FROM_PARTIALS) {
-      z4 = sk_sum4(pv, 0, r, j);
+      z4 = sk_get4(pv, 0, r, j);
       if (z_out) *reinterpret_cast<float4 *>(z_out + (size_t)r * V + j) = z4;
     } else {
       z4 = *reinterpret_cast<const float4 *>(z_in + (size_t)r * V + j);
@@ -371,7 +393,7 @@ __global__ void __launch_bounds__(1024) topk_kernel(PartialView pv, const float 
   for (int j = threadIdx.x * 4; j < V; j += blockDim.x * 4) {
     float4 z4;
     if constexpr (FROM_PARTIALS) {
-      z4 = sk_sum4(pv, head, bb, j);
+      z4 = sk_get4(pv, head, bb, j);
     } else {
       z4 = *reinterpret_cast<const float4 *>(rows_in + (size_t)r * V + j);
     }
@@ -445,9 +467,19 @@ __global__ void heads_r_kernel(PartialView pv, int d, const bf16 *head_in, BetaP
   const int i = blockIdx.z, bb = blockIdx.y;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= d) return;
-  const float t = sk_sum1(pv, i, bb, j) + bf2f(beta.p[i][j]);
-  const float hv = bf2f(head_in[(size_t)bb * d + j]);
-  r_out[i * r_stride + (size_t)bb * d + j] = f2bf(hv + t / (1.0f + expf(-t)));
+  const float t = sk_get1(pv, i, bb, j) + bf2f(beta.p[i][j]);
+  const float hv = load_act1(head_in, pv.planes, bb, d, j);
+  const float r = hv + t / (1.0f + expf(-t));
+  bf16 *dst = r_out + i * r_stride;
+  if (pv.planes > 1) {
+    bf16 a, b, c;
+    split3_bf16(r, a, b, c);
+    dst[((size_t)bb * 3 + 0) * d + j] = a;
+    dst[((size_t)bb * 3 + 1) * d + j] = b;
+    dst[((size_t)bb * 3 + 2) * d + j] = c;
+  } else {
+    dst[(size_t)bb * d + j] = f2bf(r);
+  }
 }
 cudaError_t heads_r_consumer_launch(const PartialView &pv, int nmed, int nb, int d, const bf16 *head_in,
                                     const bf16 *const *beta, bf16 *r_out, long long r_stride, cudaStream_t st) {
@@ -474,7 +506,8 @@ void epilogue_preload() {  // force-load (see gemm_preload)
   cudaFuncGetAttributes(&fa, embed_kernel);
   cudaFuncGetAttributes(&fa, resid_norm_kernel);
   cudaFuncGetAttributes(&fa, resid_norm_tp_kernel);
-  cudaFuncGetAttributes(&fa, qkv_consumer_kernel);
+  cudaFuncGetAttributes(&fa, qkv_consumer_kernel<false>);
+  cudaFuncGetAttributes(&fa, qkv_consumer_kernel<true>);
   cudaFuncGetAttributes(&fa, silu_consumer_kernel);
   cudaFuncGetAttributes(&fa, logits_kernel<true>);
   cudaFuncGetAttributes(&fa, logits_kernel<false>);

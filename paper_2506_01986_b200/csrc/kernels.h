@@ -50,11 +50,15 @@ __host__ __device__ inline int sk_tile_of(const SplitPlan &p, int bi, int tt, in
 __host__ __device__ inline float *sk_partial(float *ws, const SplitPlan &p, int t, int k) {
   return ws + ((size_t)t * p.maxc + k) * p.bn * 128;
 }
-// Where a GEMM's partials live, for the consumer kernels.
+// Where a GEMM's partials live, for the consumer kernels.  planes = 3 in the fp32
+// parity mode: every logical activation row m was fed to the GEMM as three bf16
+// rows 3m, 3m+1, 3m+2 (hi, mid, lo with hi + mid + lo == the fp32 value exactly),
+// so the logical output row is the sum of those three GEMM rows; M counts logical rows.
 struct PartialView {
   SplitPlan plan;
   const float *ws;
   int N, M;
+  int planes;  // 0 or 1: bf16 activations; 3: fp32 split into three bf16 planes
 };
 // Deterministic sum (contributor order) of y[bi][m][n .. n+3] (n % 4 == 0).
 // Loads of up to 8 contributors are issued before any add (one memory round
@@ -151,6 +155,62 @@ __device__ inline float sk_sum1(const PartialView &v, int bi, int m, int n) {
   return acc;
 }
 
+// Logical-row sums for consumers that accept either activation format (the fp32
+// mode adds the three planes in order hi, mid, lo after each plane's contributor sum).
+__device__ inline float4 sk_get4(const PartialView &v, int bi, int m, int n) {
+  if (v.planes <= 1) return sk_sum4(v, bi, m, n);
+  float4 acc = sk_sum4(v, bi, 3 * m, n);
+#pragma unroll
+  for (int p = 1; p < 3; ++p) {
+    const float4 y = sk_sum4(v, bi, 3 * m + p, n);
+    acc.x += y.x;
+    acc.y += y.y;
+    acc.z += y.z;
+    acc.w += y.w;
+  }
+  return acc;
+}
+__device__ inline float sk_get1(const PartialView &v, int bi, int m, int n) {
+  if (v.planes <= 1) return sk_sum1(v, bi, m, n);
+  return sk_sum1(v, bi, 3 * m, n) + sk_sum1(v, bi, 3 * m + 1, n) + sk_sum1(v, bi, 3 * m + 2, n);
+}
+// fp32 -> three bf16 planes whose sum is exactly x (each residual is exact in fp32).
+__device__ inline void split3_bf16(float x, __nv_bfloat16 &hi, __nv_bfloat16 &mid, __nv_bfloat16 &lo) {
+  hi = __float2bfloat16_rn(x);
+  const float r1 = x - __bfloat162float(hi);
+  mid = __float2bfloat16_rn(r1);
+  lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+}
+// Store 4 consecutive values of logical row m at column c of a [rows * planes][width]
+// bf16 activation buffer (planes = 1: plain bf16 row; 3: interleaved hi/mid/lo rows).
+__device__ inline void store_act4(__nv_bfloat16 *buf, int planes, int m, int width, int c, float a, float b, float cc,
+                                  float d) {
+  if (planes <= 1) {
+    __nv_bfloat162 lo2 = __floats2bfloat162_rn(a, b), hi2 = __floats2bfloat162_rn(cc, d);
+    uint2 o;
+    o.x = *reinterpret_cast<uint32_t *>(&lo2);
+    o.y = *reinterpret_cast<uint32_t *>(&hi2);
+    *reinterpret_cast<uint2 *>(buf + (size_t)m * width + c) = o;
+    return;
+  }
+  const float v[4] = {a, b, cc, d};
+  __nv_bfloat16 p[3][4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) split3_bf16(v[e], p[0][e], p[1][e], p[2][e]);
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    __nv_bfloat16 *dst = buf + ((size_t)m * 3 + q) * width + c;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) dst[e] = p[q][e];
+  }
+}
+// Value of logical row m, column c of such a buffer (exact fp32 in the split form).
+__device__ inline float load_act1(const __nv_bfloat16 *buf, int planes, int m, int width, int c) {
+  if (planes <= 1) return __bfloat162float(buf[(size_t)m * width + c]);
+  const __nv_bfloat16 *r = buf + (size_t)m * 3 * width + c;
+  return __bfloat162float(r[0]) + __bfloat162float(r[width]) + __bfloat162float(r[2 * width]);
+}
+
 struct GemmArgs {
   CUtensorMap tmW[kMaxGemmBatch];  // weight [N][K] bf16, box 64(k) x 128(rows), SWIZZLE_128B
   CUtensorMap tmX[kMaxGemmBatch];  // activation [rows][K] bf16, box 64(k) x 16(rows), SWIZZLE_128B
@@ -189,6 +249,11 @@ struct AttnArgs {
 };
 cudaError_t attention_launch(const AttnArgs &a, int head_dim, cudaStream_t st);
 int attention_row_blocks(int Nq, int G, int head_dim);
+// fp32 parity mode: plain fp32 tree attention (SIMT), q [M][H][hd] fp32, caches fp32
+// [b][Hkv][cap][hd] at (k, v) for this layer, output as three bf16 planes per row.
+cudaError_t attention_f32_launch(const float *q, const float *k, const float *v, const int32_t *len,
+                                 const uint64_t *anc, int Nq, int H, int Hkv, int hd, int cap, int nseq, int seq_base,
+                                 bf16 *out, cudaStream_t st);
 int attention_nsplit(int units, int head_dim);  // units = row blocks * sequences * kv heads
 void attention_set_splits(int n);               // experiments: force key splits (0 = auto)
 void attention_set_tc(int on);                  // head_dim 128: tcgen05 kernel (1, default) or mma.sync (0)
@@ -198,11 +263,13 @@ void attention_set_tc(int on);                  // head_dim 128: tcgen05 kernel 
 // its own dependent launch early (programmatic dependent launch).
 cudaError_t embed_launch(const int32_t *tok, const bf16 *E, float *x, int M, int d, cudaStream_t st);
 // x[m] += y[m] (if pv), then h = bf16(rmsnorm(x) * g)    (R5/R7 + R2/R8)
+// hp = planes of h (1: bf16; 3: fp32 parity mode, split rows)
 cudaError_t resid_norm_launch(const PartialView *pv, float *x, const bf16 *g, bf16 *h, int M, int d, float eps,
-                              cudaStream_t st);
+                              int hp, cudaStream_t st);
 // q/k/v = y; RoPE(q, k) at pos Lc + depth; q -> q[m][H][hd], k/v -> cache slot Lc + node   (R3)
-cudaError_t qkv_consumer_launch(const PartialView &pv, RowCtx rc, int H, int Hkv, int hd, const float2 *rope, bf16 *q,
-                                bf16 *kcache, bf16 *vcache, int cap, cudaStream_t st);
+// pv.planes == 3 (fp32 parity mode): q and the caches are fp32, else bf16.
+cudaError_t qkv_consumer_launch(const PartialView &pv, RowCtx rc, int H, int Hkv, int hd, const float2 *rope, void *q,
+                                void *kcache, void *vcache, int cap, cudaStream_t st);
 // act[m][f] = bf16(SiLU(gate) * up), gate/up interleaved per 64 rows    (R6)
 cudaError_t silu_consumer_launch(const PartialView &pv, int F, bf16 *act, cudaStream_t st);
 // LM rows: z = y (fp32, optional copy), argmax (lowest index on ties) and the
@@ -294,6 +361,7 @@ cudaError_t tp_advance_launch(long long *seq, int n, cudaStream_t st);
 void gemm_preload();
 void attention_preload();
 void attention_tc_preload();
+void attention_f32_preload();
 void decode_preload();
 void epilogue_preload();
 void tp_preload();

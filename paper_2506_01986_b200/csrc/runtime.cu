@@ -245,6 +245,9 @@ extern "C" void sm_tree_destroy(sm_tree *t) {
 struct sm_model {
   sm_model_cfg cfg;
   int L, d, H, Hkv, hd, F, V, nmed, G, R, B, qkv_n;
+  int P = 1;         // activation planes: 1 = bf16, 3 = fp32 parity mode (hi/mid/lo bf16 rows)
+  bool f32 = false;  // fp32 parity mode (sm_model_cfg.dtype)
+  int hdu = 0;       // K/V row length in bf16 units (hd, or 2 hd for fp32 K/V)
   const bf16 *embed, *final_norm, *lm_head;
   std::vector<const bf16 *> attn_norm, wqkv, wo, mlp_norm, wgu, wdown, mR, mb, mU;
   // workspace
@@ -337,10 +340,13 @@ static void prof_end(cudaStream_t st, cudaEvent_t a, int kind, double bytes) {
 static int g_ablate_gemm = 0;  // set while enqueueing ablated per-layer GEMMs
 // Launch one stream-K GEMM over rows [x_row0, x_row0 + M) of the prototype's
 // activation map; its fp32 partials land in ws and are described by *pv.
+// planes = 3 (fp32 parity mode): logical row m is GEMM rows 3m..3m+2.
 static sm_status run_gemm(GemmArgs a, int M, int x_row0, float *ws, size_t ws_floats, cudaStream_t st, int &nl,
-                          PartialView *pv) {
+                          PartialView *pv, int planes = 1) {
+  const int Mlog = M;
+  M *= planes;
   gemm_plan(a, a.N, a.K, M, a.batch);
-  a.x_row0 = x_row0;
+  a.x_row0 = x_row0 * planes;
   a.ws = ws;
   if (gemm_ws_floats(a) > ws_floats) return fail(SM_ERR_INVALID_ARG, "GEMM partial workspace too small");
   cudaEvent_t ev = nullptr;
@@ -348,7 +354,7 @@ static sm_status run_gemm(GemmArgs a, int M, int x_row0, float *ws, size_t ws_fl
   if (g_ablate_gemm == 0) CK(gemm_launch(a, st));
   prof_end(st, ev, 0, (double)a.batch * ((double)a.N * a.K * 2 + (double)M * a.K * 2 + (double)M * a.N * 4));
   ++nl;
-  *pv = PartialView{a.plan, ws, a.N, M};
+  *pv = PartialView{a.plan, ws, a.N, Mlog, planes};
   return SM_OK;
 }
 // Largest partial workspace a prototype can need for M in [1, max_m].
@@ -385,12 +391,17 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
     return fail(SM_ERR_INVALID_ARG, "sm_model_create: unsupported shape (d, F multiple of 64; hd in {16,32,64,128}; "
                                     "max_rows <= 1024; n_medusa <= 5)");
   if (c.vocab / tp * 4 > 200 * 1024) return fail(SM_ERR_INVALID_ARG, "vocab too large for the shared-memory top-k");
+  if (c.dtype != SM_DTYPE_BF16 && c.dtype != SM_DTYPE_FP32) return fail(SM_ERR_INVALID_ARG, "dtype must be 0 or 1");
+  if (c.dtype == SM_DTYPE_FP32 && tp > 1) return fail(SM_ERR_UNSUPPORTED, "fp32 parity mode is single-GPU (tp_size 1)");
+  if (c.dtype == SM_DTYPE_FP32 && 3 * c.max_rows > 1024)
+    return fail(SM_ERR_INVALID_ARG, "fp32 parity mode: max_rows <= 341 (three GEMM rows per token row)");
   {  // every kernel resident before any work (see gemm_preload)
     static bool loaded = false;
     if (!loaded) {
       gemm_preload();
       attention_preload();
       attention_tc_preload();
+      attention_f32_preload();
       decode_preload();
       epilogue_preload();
       tp_preload();
@@ -414,6 +425,9 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
   m->R = c.max_rows;
   m->B = c.max_batch;
   m->qkv_n = (m->H + 2 * m->Hkv) * c.head_dim;
+  m->f32 = c.dtype == SM_DTYPE_FP32;
+  m->P = m->f32 ? 3 : 1;
+  m->hdu = c.head_dim * (m->f32 ? 2 : 1);
   m->embed = (const bf16 *)w->embed;
   m->final_norm = (const bf16 *)w->final_norm;
   m->lm_head = (const bf16 *)w->lm_head;
@@ -430,7 +444,7 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
     m->mb.push_back((const bf16 *)w->medusa_b[i]);
     m->mU.push_back((const bf16 *)w->medusa_U[i]);
   }
-  const int R = m->R, B = m->B, d = m->d, Hhd = m->H * m->hd;
+  const int R = m->R, B = m->B, d = m->d, Hhd = m->H * m->hd, P = m->P;
   sm_status s;
 #define ALLOC(p, n, what)                 \
   if ((s = dalloc(&p, n, what)) != SM_OK) { \
@@ -438,16 +452,16 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
     return s;                             \
   }
   ALLOC(m->x, (size_t)R * d, "x");
-  ALLOC(m->h, (size_t)R * d, "h");
-  ALLOC(m->q, (size_t)R * Hhd, "q");
-  ALLOC(m->attn, (size_t)R * Hhd, "attn");
-  ALLOC(m->act, (size_t)R * m->F, "act");
-  ALLOC(m->hf, (size_t)R * d, "hf");
+  ALLOC(m->h, (size_t)R * d * P, "h");
+  ALLOC(m->q, (size_t)R * Hhd * (m->f32 ? 2 : 1), "q");  // fp32 q in the parity mode
+  ALLOC(m->attn, (size_t)R * Hhd * P, "attn");
+  ALLOC(m->act, (size_t)R * m->F * P, "act");
+  ALLOC(m->hf, (size_t)R * d * P, "hf");
   ALLOC(m->z, (size_t)R * m->V, "logits");
   ALLOC(m->argmax, (size_t)R, "argmax");
   ALLOC(m->stats, (size_t)R * 3, "stats");
-  ALLOC(m->head_in, (size_t)B * d, "head_in");
-  ALLOC(m->r_buf, (size_t)std::max(1, m->nmed) * B * d, "r_buf");
+  ALLOC(m->head_in, (size_t)B * d * P, "head_in");
+  ALLOC(m->r_buf, (size_t)std::max(1, m->nmed) * B * d * P, "r_buf");
   ALLOC(m->rope, (size_t)c.max_seq_len * (m->hd / 2), "rope");
   ALLOC(m->amax, (size_t)R, "amax");
   ALLOC(m->cand, (size_t)R, "cand");
@@ -464,12 +478,12 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
     cudaMemset(m->sym[tp_rank], 0, kTpFlagBytes + 2 * m->sym_slot_floats * sizeof(float));
   }
   cudaMemset(m->x, 0, (size_t)R * d * 4);
-  cudaMemset(m->h, 0, (size_t)R * d * 2);
-  cudaMemset(m->attn, 0, (size_t)R * Hhd * 2);
-  cudaMemset(m->act, 0, (size_t)R * m->F * 2);
-  cudaMemset(m->hf, 0, (size_t)R * d * 2);
-  cudaMemset(m->head_in, 0, (size_t)B * d * 2);
-  cudaMemset(m->r_buf, 0, (size_t)std::max(1, m->nmed) * B * d * 2);
+  cudaMemset(m->h, 0, (size_t)R * d * 2 * P);
+  cudaMemset(m->attn, 0, (size_t)R * Hhd * 2 * P);
+  cudaMemset(m->act, 0, (size_t)R * m->F * 2 * P);
+  cudaMemset(m->hf, 0, (size_t)R * d * 2 * P);
+  cudaMemset(m->head_in, 0, (size_t)B * d * 2 * P);
+  cudaMemset(m->r_buf, 0, (size_t)std::max(1, m->nmed) * B * d * 2 * P);
   // RoPE table: cos/sin built in fp64, stored fp32 (rounding contract R3)
   {
     const int half = m->hd / 2;
@@ -493,39 +507,39 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
   };
   for (int l = 0; l < m->L && s == SM_OK; ++l) {
     GemmArgs a;
-    if ((s = mk(m->wqkv[l], m->qkv_n, d, m->h, R, a)) != SM_OK) break;
+    if ((s = mk(m->wqkv[l], m->qkv_n, d, m->h, R * P, a)) != SM_OK) break;
     m->g_qkv.push_back(a);
-    if ((s = mk(m->wo[l], d, Hhd, m->attn, R, a)) != SM_OK) break;
+    if ((s = mk(m->wo[l], d, Hhd, m->attn, R * P, a)) != SM_OK) break;
     m->g_o.push_back(a);
-    if ((s = mk(m->wgu[l], 2 * m->F, d, m->h, R, a)) != SM_OK) break;
+    if ((s = mk(m->wgu[l], 2 * m->F, d, m->h, R * P, a)) != SM_OK) break;
     m->g_gu.push_back(a);
-    if ((s = mk(m->wdown[l], d, m->F, m->act, R, a)) != SM_OK) break;
+    if ((s = mk(m->wdown[l], d, m->F, m->act, R * P, a)) != SM_OK) break;
     m->g_down.push_back(a);
   }
-  if (s == SM_OK) s = mk(m->lm_head, m->V, d, m->hf, R, m->g_lm);
+  if (s == SM_OK) s = mk(m->lm_head, m->V, d, m->hf, R * P, m->g_lm);
   if (s != SM_OK) {
     sm_model_destroy(m);
     return s;
   }
   size_t need = 0;  // stream-K partial workspace: max over every GEMM the model runs
   for (int l = 0; l < m->L; ++l)
-    need = std::max({need, ws_need(m->g_qkv[l], R), ws_need(m->g_o[l], R), ws_need(m->g_gu[l], R),
-                     ws_need(m->g_down[l], R)});
-  need = std::max(need, ws_need(m->g_lm, R));
+    need = std::max({need, ws_need(m->g_qkv[l], R * P), ws_need(m->g_o[l], R * P), ws_need(m->g_gu[l], R * P),
+                     ws_need(m->g_down[l], R * P)});
+  need = std::max(need, ws_need(m->g_lm, R * P));
   if (m->nmed > 0) {
     m->g_R = gemm_proto(d, d, m->nmed);
     m->g_U = gemm_proto(m->V, d, m->nmed);
     for (int i = 0; i < m->nmed && s == SM_OK; ++i) {
       if ((s = weight_map(&m->g_R.tmW[i], m->mR[i], d, d)) != SM_OK) break;
-      if ((s = act_map(m->g_R, i, m->head_in, B, d)) != SM_OK) break;
+      if ((s = act_map(m->g_R, i, m->head_in, B * P, d)) != SM_OK) break;
       if ((s = weight_map(&m->g_U.tmW[i], m->mU[i], m->V, d)) != SM_OK) break;
-      s = act_map(m->g_U, i, m->r_buf + (size_t)i * B * d, B, d);
+      s = act_map(m->g_U, i, m->r_buf + (size_t)i * B * d * P, B * P, d);
     }
     if (s != SM_OK) {
       sm_model_destroy(m);
       return s;
     }
-    need = std::max({need, ws_need(m->g_R, B), ws_need(m->g_U, B)});
+    need = std::max({need, ws_need(m->g_R, B * P), ws_need(m->g_U, B * P)});
   }
   ALLOC(m->ws, need, "stream-K partials");
   m->ws_floats = need;
@@ -657,7 +671,8 @@ extern "C" sm_status sm_kv_bytes(const sm_model_cfg *cfg, int tp_size, int batch
   if (!cfg || !bytes || tp_size < 1 || batch < 1 || max_seq_len < 1 || tree_nodes < 1 ||
       cfg->n_kv_heads % tp_size)
     return fail(SM_ERR_INVALID_ARG, "sm_kv_bytes: bad arguments");
-  *bytes = kv_elems_per_layer(cfg, tp_size, batch, max_seq_len + tree_nodes) * cfg->n_layers * 2;
+  *bytes = kv_elems_per_layer(cfg, tp_size, batch, max_seq_len + tree_nodes) * cfg->n_layers *
+           (cfg->dtype == SM_DTYPE_FP32 ? 4 : 2);
   return SM_OK;
 }
 
@@ -695,7 +710,7 @@ extern "C" sm_status sm_kv_bind(sm_model *m, const sm_tree *tree, int batch, int
     return s;
   }
   const uint64_t rows = (uint64_t)need / 2 / m->hd;
-  if ((s = kv_map(&kv->tmKV, d_mem, rows, m->hd)) != SM_OK) {
+  if (!m->f32 && (s = kv_map(&kv->tmKV, d_mem, rows, m->hd)) != SM_OK) {  // bf16 kernels' TMA view
     sm_kv_destroy(kv);
     return s;
   }
@@ -766,7 +781,7 @@ static sm_status resid_norm(sm_model *m, const PartialView *pv, const bf16 *g, b
   if (m->tp > 1 && pv) {
     CK(resid_norm_tp_launch(*pv, m->x, g, h, M, m->d, m->cfg.rms_eps, tp_next(m), st));
   } else {
-    CK(resid_norm_launch(pv, m->x, g, h, M, m->d, m->cfg.rms_eps, st));
+    CK(resid_norm_launch(pv, m->x, g, h, M, m->d, m->cfg.rms_eps, m->P, st));
   }
   return SM_OK;
 }
@@ -791,9 +806,9 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
       CKS(resid_norm(m, have_down ? &pv_down : nullptr, m->attn_norm[l], m->h, M, st));
       ++nl;
     }
-    bf16 *kc = kv->base + (size_t)l * layer_rows * m->hd;
-    bf16 *vc = kc + (size_t)half_rows * m->hd;
-    CKS(run_gemm(m->g_qkv[l], M, 0, m->ws, m->ws_floats, st, nl, &pv));
+    bf16 *kc = kv->base + (size_t)l * layer_rows * m->hdu;  // bf16 units (fp32 rows are 2 hd units)
+    bf16 *vc = kc + (size_t)half_rows * m->hdu;
+    CKS(run_gemm(m->g_qkv[l], M, 0, m->ws, m->ws_floats, st, nl, &pv, m->P));
     // RoPE, q -> m->q, k/v -> cache slots Lc + node (R3)
     if (KEEP(2)) {
       CK(qkv_consumer_launch(pv, rc, m->H, m->Hkv, m->hd, m->rope, m->q, kc, vc, kv->cap, st));
@@ -822,22 +837,27 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
     cudaEvent_t ev = nullptr;
     prof_begin(st, &ev);
     if (KEEP(1)) {
-      CK(attention_launch(aa, m->hd, st));
+      if (m->f32)
+        CK(attention_f32_launch(reinterpret_cast<const float *>(m->q), reinterpret_cast<const float *>(kc),
+                                reinterpret_cast<const float *>(vc), kv->len, tree.anc, Nq, m->H, m->Hkv, m->hd,
+                                kv->cap, nseq, seq_base, m->attn, st));
+      else
+        CK(attention_launch(aa, m->hd, st));
       ++nl;
     }
     prof_end(st, ev, 1, 0.0);
-    CKS(run_gemm(m->g_o[l], M, 0, m->ws, m->ws_floats, st, nl, &pv));
+    CKS(run_gemm(m->g_o[l], M, 0, m->ws, m->ws_floats, st, nl, &pv, m->P));
     // x += o (R5); h = bf16(rms(x) * g2)
     if (KEEP(2)) {
       CKS(resid_norm(m, &pv, m->mlp_norm[l], m->h, M, st));
       ++nl;
     }
-    CKS(run_gemm(m->g_gu[l], M, 0, m->ws, m->ws_floats, st, nl, &pv));
+    CKS(run_gemm(m->g_gu[l], M, 0, m->ws, m->ws_floats, st, nl, &pv, m->P));
     if (KEEP(2)) {
       CK(silu_consumer_launch(pv, m->F, m->act, st));  // act = bf16(SiLU(g) * u) (R6)
       ++nl;
     }
-    CKS(run_gemm(m->g_down[l], M, 0, m->ws, m->ws_floats, st, nl, &pv_down));
+    CKS(run_gemm(m->g_down[l], M, 0, m->ws, m->ws_floats, st, nl, &pv_down, m->P));
     have_down = true;
   }
   g_ablate_gemm = 0;
@@ -850,13 +870,13 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
 // heads at rows [row0, row0 + nb) of head_in -> topk rows [row0, row0 + nb)
 static sm_status enqueue_heads(sm_model *m, sm_kv *kv, int row0, int nb, cudaStream_t st, int &nl) {
   if (m->nmed == 0 || kv->t->l == 0 || !KEEP(8)) return SM_OK;
-  const int d = m->d, B = m->B;
+  const int d = m->d, B = m->B, P = m->P;
   PartialView pv;
-  CKS(run_gemm(m->g_R, nb, row0, m->ws, m->ws_floats, st, nl, &pv));
-  CK(heads_r_consumer_launch(pv, m->nmed, nb, d, m->head_in + (size_t)row0 * d, m->mb.data(),
-                             m->r_buf + (size_t)row0 * d, (long long)B * d, st));
+  CKS(run_gemm(m->g_R, nb, row0, m->ws, m->ws_floats, st, nl, &pv, P));
+  CK(heads_r_consumer_launch(pv, m->nmed, nb, d, m->head_in + (size_t)row0 * d * P, m->mb.data(),
+                             m->r_buf + (size_t)row0 * d * P, (long long)B * d * P, st));
   ++nl;
-  CKS(run_gemm(m->g_U, nb, row0, m->ws, m->ws_floats, st, nl, &pv));
+  CKS(run_gemm(m->g_U, nb, row0, m->ws, m->ws_floats, st, nl, &pv, P));
   const int K = kv->t->topk;
   int32_t *dst = kv->topk + (size_t)row0 * m->nmed * K;
   if (m->tp > 1) {  // vocabulary-parallel U: local top-K, then merge across ranks
@@ -893,13 +913,14 @@ extern "C" sm_status sm_prefill(sm_model *m, sm_kv *kv, int seq, const int32_t *
   }
   // last token: LM head row, pending root, heads' top-k (reading Q8)
   PartialView pv;
-  CKS(run_gemm(m->g_lm, 1, last - 1, m->ws, m->ws_floats, st, nl, &pv));
+  CKS(run_gemm(m->g_lm, 1, last - 1, m->ws, m->ws_floats, st, nl, &pv, m->P));
   CK(logits_consumer_launch(pv, 1.0f, m->z, m->argmax, m->stats, m->v0, m->amax, st));
   if (m->tp > 1)
     CK(tp_merge_logits_launch(1, m->amax, m->argmax, m->stats, m->z, m->V, m->v0, nullptr, 1, nullptr, nullptr,
                               tp_next(m), st));
-  CK(set_root_launch(kv->root, seq, m->argmax, m->hf + (size_t)(last - 1) * m->d, m->d,
-                     m->head_in + (size_t)seq * m->d, st));
+  const int dP = m->d * m->P;  // a hidden row: d bf16, or its 3 planes (fp32 mode)
+  CK(set_root_launch(kv->root, seq, m->argmax, m->hf + (size_t)(last - 1) * dP, dP, m->head_in + (size_t)seq * dP,
+                     st));
   CKS(enqueue_heads(m, kv, seq, 1, st, nl));
   CKS(tp_end(m, st, nl));
   CK(cudaGetLastError());
@@ -918,7 +939,7 @@ static sm_status enqueue_verify(sm_model *m, sm_kv *kv, const int32_t *tree_tok,
   const int M = kv->b * kv->N;
   CKS(enqueue_forward(m, kv, tree_tok, kv->b, 0, kv->N, kv->t->dev(), st, nl));
   PartialView pv;
-  CKS(run_gemm(m->g_lm, M, 0, m->ws, m->ws_floats, st, nl, &pv));
+  CKS(run_gemm(m->g_lm, M, 0, m->ws, m->ws_floats, st, nl, &pv, m->P));
   CK(logits_consumer_launch(pv, 1.0f, m->z, m->argmax, m->stats, m->v0, m->amax, st));
   ++nl;
   return SM_OK;
@@ -969,9 +990,9 @@ static sm_status enqueue_accept(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg
   a.root_next = kv->root_next;
   CK(accept_launch(a, st));
   ++nl;
-  CK(compact_launch(kv->base, m->L, kv->b, m->Hkv, kv->cap, m->hd, kv->len, o->path, kv->t->l + 1, o->n_emit, st));
+  CK(compact_launch(kv->base, m->L, kv->b, m->Hkv, kv->cap, m->hdu, kv->len, o->path, kv->t->l + 1, o->n_emit, st));
   ++nl;
-  CK(commit_launch(kv->b, kv->len, o->n_emit, kv->root, kv->root_next, kv->acc_row, m->hf, m->d, m->head_in,
+  CK(commit_launch(kv->b, kv->len, o->n_emit, kv->root, kv->root_next, kv->acc_row, m->hf, m->d * m->P, m->head_in,
                    kv->emitted, st));
   ++nl;
   CKS(enqueue_heads(m, kv, 0, kv->b, st, nl));
@@ -1211,4 +1232,6 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
 }
 
 extern "C" const char *sm_last_error(void) { return g_err.c_str(); }
-extern "C" const char *sm_version(void) { return "specmemo-b200 0.1 (sm_100a: tcgen05 GEMM and tree attention)"; }
+extern "C" const char *sm_version(void) {
+  return "specmemo-b200 0.2 (sm_100a: tcgen05 GEMM and tree attention; bf16 and fp32 parity modes)";
+}

@@ -141,6 +141,26 @@ def test_bf16_mode_close_to_fp64():
     assert np.max(np.abs(outs["fp64"] - outs["bf16"])) > 0   # rounding really happens
 
 
+def test_fp32_mode_matches_hf_llama_float32():
+    """fp32 parity mode (north star: 1e-4): the oracle's fp32-storage rows agree
+    with an independent float32 forward (HF Llama cast to float32) and with the
+    fp64 reference far inside 1e-4, while the rounding is real (differs from fp64)."""
+    cfg, W = _tiny(n_kv_heads=2)
+    toks = synth.prompt_tokens(5, 0, 20, cfg["vocab"])
+    hf = _hf_llama(cfg, W).float()
+    with torch.no_grad():
+        ref32 = hf(torch.tensor(toks[None], dtype=torch.long)).logits[0].double().numpy()
+    outs = {}
+    for mode in ("fp64", "fp32"):
+        m = M.Model(cfg, W, mode)
+        kv = M.KVCache(cfg["n_layers"], 1, cfg["n_kv_heads"], 32, cfg["head_dim"])
+        outs[mode] = np.stack([m.forward_row(kv, 0, int(t), i, i, list(range(i + 1)))[0] for i, t in enumerate(toks)])
+    assert np.max(np.abs(outs["fp32"] - ref32)) < 1e-5
+    assert np.max(np.abs(outs["fp32"] - outs["fp64"])) < 1e-5
+    assert np.max(np.abs(outs["fp32"] - outs["fp64"])) > 0
+    assert np.all(outs["fp32"] == outs["fp32"].astype(np.float32))   # stored as fp32 (R9)
+
+
 def test_medusa_head_special_case():
     """R = 0, beta = 0 ("Medusa-init", reading Q18): u = U hf; with U = W_lm the
     head logits equal the base logits (SiLU(0) = 0)."""

@@ -22,10 +22,10 @@ def _model(mode="bf16", n_medusa=3, **over):
 
 @pytest.fixture(scope="module")
 def models():
-    return {mode: _model(mode) for mode in ("fp64", "bf16")}
+    return {mode: _model(mode) for mode in ("fp64", "fp32", "bf16")}
 
 
-@pytest.mark.parametrize("mode", ["fp64", "bf16"])
+@pytest.mark.parametrize("mode", ["fp64", "fp32", "bf16"])
 def test_greedy_spec_equals_vanilla_and_kv(models, mode):
     """C1: 32-token prompt, 32 greedy tokens, tiny16 tree, x = 64 (BASELINE configs[0])."""
     m = models[mode]
