@@ -233,7 +233,8 @@ sm_status sm_state_device(const sm_kv *kv, int32_t **d_root, int32_t **d_topk);
 sm_status sm_tree_attention(const sm_tree *t, const void *d_q, const void *d_k, const void *d_v,
                             const int32_t *d_len, int batch, int n_heads, int n_kv_heads, int head_dim, int cap,
                             void *d_out, void *stream);
-/* K2 tcgen05 GEMM: out[M][N] fp32 = x[M][K] bf16 * w[N][K]^T bf16.  M <= 1024. */
+/* K2 tcgen05 GEMM: out[M][N] fp32 = x[M][K] bf16 * w[N][K]^T bf16.  M <= 1024.
+ * d_out NULL: only the GEMM runs (its partials stay in library scratch; timing). */
 sm_status sm_gemm_bf16(const void *d_x, const void *d_w, float *d_out, int M, int N, int K, void *stream);
 /* K3 top-k rows of fp32 logits: idx[r][k] by (value desc, index asc).        */
 sm_status sm_topk_f32(const float *d_logits, int rows, int V, int k, int32_t *d_idx, void *stream);

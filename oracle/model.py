@@ -115,6 +115,10 @@ class Model:
         """y = x / sqrt(mean(x^2) + eps) * g  (Llama RMSNorm)."""
         return x / math.sqrt(float(np.mean(x * x)) + self.eps) * g
 
+    def rms_scale(self, x):
+        """rs = 1 / sqrt(mean(x^2) + eps), so that rmsnorm(x, g) = rs * (x * g)."""
+        return 1.0 / math.sqrt(float(np.mean(x * x)) + self.eps)
+
     def rope(self, v, pos):
         """Rotate-half RoPE on each head of v [nh][hd] at integer position pos:
         for i < hd/2, angle = pos * theta^(-2i/hd),
@@ -157,10 +161,12 @@ class Model:
         W = self.W
         x = self.r16(W.embed[tok]).copy()                               # R1 (bf16 row -> fp32 residual)
         for li, Lw in enumerate(W.layers):
-            h = self.r16(self.rmsnorm(x, Lw["attn_norm"]))               # R2
-            q = (Lw["wq"] @ h).reshape(self.H, self.hd)                 # R3 fp32 accumulate
-            k = (Lw["wk"] @ h).reshape(self.Hkv, self.hd)
-            v = (Lw["wv"] @ h).reshape(self.Hkv, self.hd)
+            # R2 (deferred RMSNorm): the stored GEMM input is x*g; the projection is scaled by
+            # rs = 1/sqrt(mean(x^2) + eps) afterwards -- rmsnorm(x, g) @ W^T = rs * ((x*g) @ W^T)
+            h, rs = self.r16(x * Lw["attn_norm"]), self.r32(self.rms_scale(x))
+            q = (rs * (Lw["wq"] @ h)).reshape(self.H, self.hd)          # R3 fp32 accumulate
+            k = (rs * (Lw["wk"] @ h)).reshape(self.Hkv, self.hd)
+            v = (rs * (Lw["wv"] @ h)).reshape(self.Hkv, self.hd)
             q = self.r16(self.rope(self.r32(q), pos))
             k = self.r16(self.rope(self.r32(k), pos))
             v = self.r16(v)
@@ -170,8 +176,8 @@ class Model:
             Vc = kv.V[li][seq][:, key_slots, :].transpose(1, 0, 2)
             o = self.r16(self.attention(q, Kc, Vc).reshape(-1))         # R4
             x = self.r32(x + self.r32(Lw["wo"] @ o))                    # R5 (fp32 residual)
-            h2 = self.r16(self.rmsnorm(x, Lw["mlp_norm"]))
-            a = self.r16(self.silu(self.r32(Lw["wg"] @ h2)) * self.r32(Lw["wu"] @ h2))  # R6
+            h2, rs2 = self.r16(x * Lw["mlp_norm"]), self.r32(self.rms_scale(x))      # R2 (deferred)
+            a = self.r16(self.silu(self.r32(rs2 * (Lw["wg"] @ h2))) * self.r32(rs2 * (Lw["wu"] @ h2)))  # R6
             x = self.r32(x + self.r32(Lw["wd"] @ a))                    # R7
         hf = self.r16(self.rmsnorm(x, W.final_norm))                    # R8
         z = self.r32(W.lm_head @ hf)                                    # R9

@@ -424,7 +424,7 @@ def tree_attention(tree: Tree, q, k, v, lengths, n_heads: int, n_kv_heads: int, 
 
 
 def gemm_bf16(x, w, out, stream=None) -> None:
-    """K2: out[M][N] fp32 = x[M][K] @ w[N][K]^T (tcgen05)."""
+    """K2: out[M][N] fp32 = x[M][K] @ w[N][K]^T (tcgen05); out None = GEMM only (timing)."""
     M, K = x.shape
     N = w.shape[0]
     _check(lib().sm_gemm_bf16(ctypes.c_void_p(_ptr(x)), ctypes.c_void_p(_ptr(w)), ctypes.c_void_p(_ptr(out)), M, N, K,

@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
   uint32_t *tslot = reinterpret_cast<uint32_t *>(q_full + 1);
 
   pdl_trigger();
+  SM_GT_BEGIN();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) SM_STAMP(0);
   const int split = blockIdx.x, rblk = blockIdx.y;  // split = rank in the (nsplit, 1, 1) cluster
@@ -248,6 +249,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
     const bool live = rr < R;
     const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
     pdl_wait();  // q comes from the preceding kernel
+    SM_GT_WAITED();
     if (threadIdx.x == 0) SM_STAMP(2);
     {  // stage this row of Q into the K-major SW128 layout (two 64-column halves)
       const uint4 *src = nullptr;
@@ -488,8 +490,10 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   if (warp == 5) tmem_dealloc<256>(tmem);
+  if (threadIdx.x == 0) SM_GT_END(5);
 }
 
+SM_GT_READER(sm_gtrace_read_attn)
 #ifdef SM_TRACE
 extern "C" int sm_trace_read(long long *dst, int n) {  // diagnostics build only
   return (int)cudaMemcpyFromSymbol(dst, g_trace, sizeof(long long) * (size_t)n);

@@ -141,10 +141,53 @@ static __device__ long long g_trace[kTraceCtas][kTraceSlots];  // per translatio
     const int cta_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);             \
     if (cta_ < kTraceCtas) g_trace[cta_][slot] = clock64();                                      \
   } while (0)
+// Cross-kernel timeline (diagnostics build): one record per CTA {kernel id, globaltimer at
+// entry, after griddepcontrol.wait, at exit}; per translation unit, read by sm_gtrace_read_*.
+constexpr int kGtRecs = 1 << 17;
+static __device__ long long g_gt[kGtRecs][4];
+static __device__ unsigned int g_gt_n;
+SM_DEV long long gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define SM_GT_BEGIN() long long gt0_ = gtime(), gt1_ = 0
+#define SM_GT_WAITED() gt1_ = gtime()
+#define SM_GT_END(kid)                                  \
+  do {                                                  \
+    const unsigned i_ = atomicAdd(&g_gt_n, 1u);         \
+    if (i_ < (unsigned)kGtRecs) {                       \
+      g_gt[i_][0] = (kid);                              \
+      g_gt[i_][1] = gt0_;                               \
+      g_gt[i_][2] = gt1_;                               \
+      g_gt[i_][3] = gtime();                            \
+    }                                                   \
+  } while (0)
+#define SM_GT_READER(name)                                                                   \
+  extern "C" int name(long long *dst, int max_recs) {                                        \
+    unsigned n = 0;                                                                          \
+    cudaMemcpyFromSymbol(&n, g_gt_n, sizeof(n));                                             \
+    n = n < (unsigned)max_recs ? n : (unsigned)max_recs;                                     \
+    n = n < (unsigned)kGtRecs ? n : (unsigned)kGtRecs;                                       \
+    cudaMemcpyFromSymbol(dst, g_gt, sizeof(long long) * 4 * (size_t)n);                      \
+    const unsigned z = 0;                                                                    \
+    cudaMemcpyToSymbol(g_gt_n, &z, sizeof(z));                                               \
+    return (int)n;                                                                           \
+  }
 #else
 #define SM_STAMP(slot) \
   do {                 \
   } while (0)
+#define SM_GT_BEGIN() \
+  do {                \
+  } while (0)
+#define SM_GT_WAITED() \
+  do {                 \
+  } while (0)
+#define SM_GT_END(kid) \
+  do {                 \
+  } while (0)
+#define SM_GT_READER(name)
 #endif
 
 // ------------------------------------------------------------------ mbarrier

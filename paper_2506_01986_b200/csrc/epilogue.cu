@@ -15,12 +15,18 @@
 // next launch immediately and wait for their producer before touching memory.
 #include <float.h>
 
+#include <algorithm>
 #include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
 
 namespace sm {
+
+// Grid cap of the consumer kernels (sm_set_option "consumer_ctas"; experiments): a cap makes
+// them persistent (grid-stride), default = one CTA per work item.
+static int g_consumer_ctas = 1 << 30;
+void consumer_set_ctas(int n) { g_consumer_ctas = n > 0 ? n : (1 << 30); }
 
 template <int NT>
 SM_DEV float block_sum(float v, float *red) {
@@ -59,15 +65,24 @@ cudaError_t embed_launch(const int32_t *tok, const bf16 *E, float *x, int M, int
 // exchanged by pushing each CTA's block sum into every peer's shared memory.
 constexpr int kNormThreads = 256;
 constexpr int kNormCols = 4 * kNormThreads;
+// rs_out != nullptr: deferred RMSNorm (rounding contract R2): h = x * g and rs_out[m] =
+// 1/sqrt(mean(x^2) + eps), applied by the consumer of the next GEMM; else h = x * rs * g.
 __global__ void __launch_bounds__(kNormThreads) resid_norm_kernel(PartialView pv, int has_pv, float *x, const bf16 *g,
-                                                                  bf16 *h, int d, float eps, int hp) {
+                                                                  bf16 *h, int M, int d, float eps, int hp,
+                                                                  float *rs_out) {
+  SM_GT_BEGIN();
   __shared__ float red[kNormThreads / 32];
-  __shared__ float ssq[8];  // ssq[q] = block sum of cluster rank q
+  __shared__ float ssq[2][8];  // ssq[it & 1][q] = block sum of cluster rank q (double-buffered by row)
   pdl_trigger();
   cluster_arrive_relaxed();  // phase 1: every CTA of the cluster has started (before any DSMEM store)
   pdl_wait();
-  const int m = blockIdx.y, rank = blockIdx.x, cs = gridDim.x;
+  SM_GT_WAITED();
+  const int rank = blockIdx.x, cs = gridDim.x;
   const int i = rank * kNormCols + threadIdx.x * 4;
+  int it = 0;
+  // persistent over rows: the grid stays within what is co-resident with a running GEMM,
+  // so every CTA is already waiting when the GEMM completes
+  for (int m = blockIdx.y; m < M; m += gridDim.y, ++it) {
   float *xr = x + (size_t)m * d;
   float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
   if (i < d) {
@@ -89,27 +104,33 @@ __global__ void __launch_bounds__(kNormThreads) resid_norm_kernel(PartialView pv
     }
   }
   float ss = block_sum<kNormThreads>(a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w, red);
-  cluster_wait();
-  if (threadIdx.x < cs) st_dsmem_f32(mapa_u32(smem_u32(&ssq[rank]), threadIdx.x), ss);
+  if (it == 0) cluster_wait();
+  if (threadIdx.x < cs) st_dsmem_f32(mapa_u32(smem_u32(&ssq[it & 1][rank]), threadIdx.x), ss);
   cluster_sync_all();  // phase 2: all block sums delivered
   ss = 0.f;
-  for (int q = 0; q < cs; ++q) ss += ssq[q];  // same order in every CTA of the cluster
-  const float rs = 1.0f / sqrtf(ss / (float)d + eps);
+  for (int q = 0; q < cs; ++q) ss += ssq[it & 1][q];  // same order in every CTA of the cluster
+  const float r = 1.0f / sqrtf(ss / (float)d + eps);
+  if (rs_out && rank == 0 && threadIdx.x == 0) rs_out[m] = r;
+  const float rs = rs_out ? 1.0f : r;
   if (i < d) {
     const __nv_bfloat162 g01 = *reinterpret_cast<const __nv_bfloat162 *>(g + i);
     const __nv_bfloat162 g23 = *reinterpret_cast<const __nv_bfloat162 *>(g + i + 2);
     store_act4(h, hp, m, d, i, a.x * rs * __low2float(g01), a.y * rs * __high2float(g01),
                a.z * rs * __low2float(g23), a.w * rs * __high2float(g23));
   }
+  }
+  if (it == 0) cluster_wait();  // no rows: complete the start barrier phase
+  if (threadIdx.x == 0) SM_GT_END(1);
 }
 cudaError_t resid_norm_launch(const PartialView *pv, float *x, const bf16 *g, bf16 *h, int M, int d, float eps,
-                              int hp, cudaStream_t st) {
+                              int hp, float *rs_out, cudaStream_t st) {
   const int cs = (d + kNormCols - 1) / kNormCols;
   if (cs > 8 || d % 4) return cudaErrorInvalidValue;
   PartialView v{};
   if (pv) v = *pv;
-  return launch_pdl_cluster(resid_norm_kernel, dim3(cs, M), dim3(kNormThreads), 0, st, cs, v, pv ? 1 : 0, x, g, h, d,
-                            eps, hp);
+  const int rows_par = std::min(M, std::max(1, g_consumer_ctas / cs));
+  return launch_pdl_cluster(resid_norm_kernel, dim3(cs, rows_par), dim3(kNormThreads), 0, st, cs, v, pv ? 1 : 0, x, g,
+                            h, M, d, eps, hp, rs_out);
 }
 
 // Tensor-parallel variant (a7): the residual all-reduce fused in.  Each rank reduces
@@ -120,7 +141,8 @@ cudaError_t resid_norm_launch(const PartialView *pv, float *x, const bf16 *g, bf
 // rank waits on is always running on the peer.  The DSMEM sum-of-squares slots are
 // double-buffered by iteration parity.
 __global__ void __launch_bounds__(kNormThreads) resid_norm_tp_kernel(PartialView pv, float *x, const bf16 *g, bf16 *h,
-                                                                     int M, int d, float eps, TpArgs tp) {
+                                                                     int M, int d, float eps, TpArgs tp,
+                                                                     float *rs_out) {
   __shared__ float red[kNormThreads / 32];
   __shared__ float ssq[2][8];
   pdl_trigger();
@@ -179,7 +201,9 @@ __global__ void __launch_bounds__(kNormThreads) resid_norm_tp_kernel(PartialView
     cluster_sync_all();
     ss = 0.f;
     for (int r = 0; r < cs; ++r) ss += ssq[it & 1][r];
-    const float rs = 1.0f / sqrtf(ss / (float)d + eps);
+    const float r = 1.0f / sqrtf(ss / (float)d + eps);
+    if (rs_out && crank == 0 && threadIdx.x == 0) rs_out[m] = r;
+    const float rs = rs_out ? 1.0f : r;  // deferred RMSNorm (R2), as in resid_norm_kernel
     if (i < d) {
       const __nv_bfloat162 g01 = *reinterpret_cast<const __nv_bfloat162 *>(g + i);
       const __nv_bfloat162 g23 = *reinterpret_cast<const __nv_bfloat162 *>(g + i + 2);
@@ -192,12 +216,12 @@ __global__ void __launch_bounds__(kNormThreads) resid_norm_tp_kernel(PartialView
   if (it == 0) cluster_wait();  // no rows: complete the start barrier phase
 }
 cudaError_t resid_norm_tp_launch(const PartialView &pv, float *x, const bf16 *g, bf16 *h, int M, int d, float eps,
-                                 const TpArgs &tp, cudaStream_t st) {
+                                 const TpArgs &tp, float *rs_out, cudaStream_t st) {
   const int cs = (d + kNormCols - 1) / kNormCols;
   if (cs > 8 || d % 4 || M * cs > kTpFlagSlots) return cudaErrorInvalidValue;
   const int rows_par = M < 64 ? M : 64;  // cs x 64 CTAs: always co-resident
   return launch_pdl_cluster(resid_norm_tp_kernel, dim3(cs, rows_par), dim3(kNormThreads), 0, st, cs, pv, x, g, h, M, d,
-                            eps, tp);
+                            eps, tp, rs_out);
 }
 
 // ------------------------------------------------------------------ QKV consumer (RoPE + cache write)
@@ -205,16 +229,22 @@ cudaError_t resid_norm_tp_launch(const PartialView &pv, float *x, const bf16 *g,
 // F32 (fp32 parity mode): q and the K/V cache hold fp32, partial rows come in 3 planes.
 template <bool F32>
 __global__ void __launch_bounds__(256) qkv_consumer_kernel(PartialView pv, RowCtx rc, int H, int Hkv, int hd,
-                                                           const float2 *rope, void *q_, void *kc_, void *vc_, int cap) {
+                                                           const float2 *rope, void *q_, void *kc_, void *vc_, int cap,
+                                                           const float *rs) {
+  SM_GT_BEGIN();
   using T = typename std::conditional<F32, float, bf16>::type;
   T *q = static_cast<T *>(q_), *kc = static_cast<T *>(kc_), *vc = static_cast<T *>(vc_);
   pdl_trigger();
   pdl_wait();
-  const int m = blockIdx.y;
+  SM_GT_WAITED();
   const int half = hd / 2;
   const int quads = half / 4;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (H + 2 * Hkv) * quads) return;
+  const int bpr = ((H + 2 * Hkv) * quads + blockDim.x - 1) / blockDim.x;  // blocks per token row
+  // persistent: ~one CTA per SM, all resident (and waiting) before the GEMM completes
+  for (int item = blockIdx.x; item < rc.M * bpr; item += gridDim.x) {
+  const int m = item / bpr;
+  const int idx = (item % bpr) * blockDim.x + threadIdx.x;
+  if (idx >= (H + 2 * Hkv) * quads) continue;
   const int hh = idx / quads, c = (idx % quads) * 4;
   const int n0 = hh * hd + c;
   float4 a, b;
@@ -229,7 +259,8 @@ __global__ void __launch_bounds__(256) qkv_consumer_kernel(PartialView pv, RowCt
     a = sk_reduce<8>(ra, xa);
     b = sk_reduce<8>(rb, xb);
   }
-  float x0[4] = {a.x, a.y, a.z, a.w}, x1[4] = {b.x, b.y, b.z, b.w};
+  const float r = rs ? rs[m] : 1.0f;  // deferred RMSNorm scale of the input row (R2)
+  float x0[4] = {a.x * r, a.y * r, a.z * r, a.w * r}, x1[4] = {b.x * r, b.y * r, b.z * r, b.w * r};
   const int sl = m / rc.Nq, node = m % rc.Nq;
   const int seq = rc.seq_base + sl;
   const int Lc = rc.len[seq];
@@ -264,25 +295,33 @@ __global__ void __launch_bounds__(256) qkv_consumer_kernel(PartialView pv, RowCt
     *reinterpret_cast<uint2 *>(dst + c) = lo;
     *reinterpret_cast<uint2 *>(dst + c + half) = hi;
   }
+  }
+  if (threadIdx.x == 0) SM_GT_END(2);
 }
 cudaError_t qkv_consumer_launch(const PartialView &pv, RowCtx rc, int H, int Hkv, int hd, const float2 *rope, void *q,
-                                void *kcache, void *vcache, int cap, cudaStream_t st) {
+                                void *kcache, void *vcache, int cap, const float *rs, cudaStream_t st) {
   const int work = (H + 2 * Hkv) * (hd / 8);
+  const int items = (work + 255) / 256 * rc.M;
+  const dim3 grid(std::min(items, g_consumer_ctas));
   if (pv.planes > 1)
-    return launch_pdl(qkv_consumer_kernel<true>, dim3((work + 255) / 256, rc.M), dim3(256), 0, st, pv, rc, H, Hkv, hd,
-                      rope, q, kcache, vcache, cap);
-  return launch_pdl(qkv_consumer_kernel<false>, dim3((work + 255) / 256, rc.M), dim3(256), 0, st, pv, rc, H, Hkv, hd,
-                    rope, q, kcache, vcache, cap);
+    return launch_pdl(qkv_consumer_kernel<true>, grid, dim3(256), 0, st, pv, rc, H, Hkv, hd, rope, q, kcache, vcache,
+                      cap, rs);
+  return launch_pdl(qkv_consumer_kernel<false>, grid, dim3(256), 0, st, pv, rc, H, Hkv, hd, rope, q, kcache, vcache,
+                    cap, rs);
 }
 
 // ------------------------------------------------------------------ SiLU(gate) * up
 // fused weight rows: tile t = [gate 64t..64t+63 | up 64t..64t+63]
-__global__ void __launch_bounds__(256) silu_consumer_kernel(PartialView pv, int F, bf16 *act) {
+__global__ void __launch_bounds__(256) silu_consumer_kernel(PartialView pv, int F, bf16 *act, const float *rs) {
+  SM_GT_BEGIN();
   pdl_trigger();
   pdl_wait();
-  const int m = blockIdx.y;
-  const int f = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
-  if (f >= F) return;
+  SM_GT_WAITED();
+  const int bpr = (F / 4 + blockDim.x - 1) / blockDim.x;  // blocks per token row
+  for (int item = blockIdx.x; item < pv.M * bpr; item += gridDim.x) {  // persistent (see qkv_consumer)
+  const int m = item / bpr;
+  const int f = ((item % bpr) * blockDim.x + threadIdx.x) * 4;
+  if (f >= F) continue;
   const int ng = (f >> 6) * 128 + (f & 63);
   float4 g, u;
   if (pv.planes > 1) {
@@ -296,14 +335,18 @@ __global__ void __launch_bounds__(256) silu_consumer_kernel(PartialView pv, int 
     g = sk_reduce<8>(rg, xg);
     u = sk_reduce<8>(ru, xu);
   }
-  const float gg[4] = {g.x, g.y, g.z, g.w}, uu[4] = {u.x, u.y, u.z, u.w};
+  const float r = rs ? rs[m] : 1.0f;  // deferred RMSNorm scale (R2)
+  const float gg[4] = {g.x * r, g.y * r, g.z * r, g.w * r}, uu[4] = {u.x * r, u.y * r, u.z * r, u.w * r};
   float o[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) o[e] = gg[e] / (1.0f + expf(-gg[e])) * uu[e];
   store_act4(act, pv.planes, m, F, f, o[0], o[1], o[2], o[3]);
+  }
+  if (threadIdx.x == 0) SM_GT_END(3);
 }
-cudaError_t silu_consumer_launch(const PartialView &pv, int F, bf16 *act, cudaStream_t st) {
-  return launch_pdl(silu_consumer_kernel, dim3((F / 4 + 255) / 256, pv.M), dim3(256), 0, st, pv, F, act);
+cudaError_t silu_consumer_launch(const PartialView &pv, int F, bf16 *act, const float *rs, cudaStream_t st) {
+  const int items = (F / 4 + 255) / 256 * pv.M;
+  return launch_pdl(silu_consumer_kernel, dim3(std::min(items, g_consumer_ctas)), dim3(256), 0, st, pv, F, act, rs);
 }
 
 // ------------------------------------------------------------------ logits: argmax + typical stats
@@ -500,6 +543,8 @@ __global__ void plain_kernel(PartialView pv, float *out) {
 cudaError_t plain_consumer_launch(const PartialView &pv, float *out, cudaStream_t st) {
   return launch_pdl(plain_kernel, dim3((pv.N + 1023) / 1024, pv.M), dim3(256), 0, st, pv, out);
 }
+
+SM_GT_READER(sm_gtrace_read_epi)
 
 void epilogue_preload() {  // force-load (see gemm_preload)
   cudaFuncAttributes fa;

@@ -65,7 +65,118 @@ SM_DEV void tmem_ldc(uint32_t taddr, float *v) {
   }
 }
 
-template <int BN, int SMEMKB>
+SM_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }  // the 4 epilogue warps
+
+// Fused tile epilogue (see kernels.h, kEpi*), run by the last contributor of tile t
+// with the 128 epilogue threads: thread et owns the feature pair (p, p + 64) of the
+// tile -- a RoPE pair (hd = 128), a gate/up pair, or two residual columns -- for the
+// token columns ml = half, half + 2, ... of the tile.  Partial slots are read from L2.
+template <int BN>
+SM_DEV void fused_fixup(const GemmArgs &a, int t, int nc, int et) {
+  const SplitPlan &pl = a.plan;
+  const EpiArgs &e = a.e;
+  int bi, tt, mt;
+  sk_decode(t, pl, bi, tt, mt);
+  const int p = et & 63, half = et >> 6, w = et >> 5;
+  const int rows = min(BN, a.M - tt * BN);
+  const float *base = a.ws + (size_t)t * pl.maxc * BN * 128 + p;
+  const size_t kstride = (size_t)BN * 128;
+  constexpr int CB = BN >= 8 ? 4 : 1;  // token columns per batch: CB x 8 contributors x 2 loads in flight
+  constexpr int KM = 8;
+  for (int ml0 = half * CB; ml0 < rows; ml0 += 2 * CB) {
+    float v0[CB][KM], v1[CB][KM];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) {
+      const float *col = base + (size_t)(ml0 + c) * 128;
+#pragma unroll
+      for (int k = 0; k < KM; ++k) {
+        const bool ok = k < nc && ml0 + c < rows;
+        v0[c][k] = ok ? __ldcg(col + k * kstride) : 0.f;
+        v1[c][k] = ok ? __ldcg(col + k * kstride + 64) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < CB; ++c) {
+      const int ml = ml0 + c;
+      float y0 = 0.f, y1 = 0.f;
+#pragma unroll
+      for (int k = 0; k < KM; ++k) {  // contributor order: identical to the consumer kernels' sums
+        if (k < nc) {
+          y0 += v0[c][k];
+          y1 += v1[c][k];
+        }
+      }
+      for (int k = KM; k < nc; ++k) {
+        const float *col = base + (size_t)ml * 128;
+        y0 += __ldcg(col + k * kstride);
+        y1 += __ldcg(col + k * kstride + 64);
+      }
+      const bool live = ml < rows;  // all lanes of a warp share ml (warp_sum below)
+      const int m = tt * BN + (live ? ml : 0);
+      if (a.epi == kEpiQKV) {
+        if (!live) continue;
+        const float r = e.rs_in[m];
+        float x0 = y0 * r, x1 = y1 * r;
+        const int hh = mt, sl = m / e.rc.Nq, node = m % e.rc.Nq;
+        const int seq = e.rc.seq_base + sl;
+        const int Lc = e.rc.len[seq];
+        if (hh < e.H + e.Hkv) {  // rotate-half RoPE at pos = Lc + depth
+          const float2 cs = e.rope[(size_t)(Lc + e.rc.depth[node]) * 64 + p];
+          const float o0 = x0 * cs.x - x1 * cs.y;
+          const float o1 = x1 * cs.x + x0 * cs.y;
+          x0 = o0;
+          x1 = o1;
+        }
+        bf16 *dst;
+        if (hh < e.H)
+          dst = e.q + ((size_t)m * e.H + hh) * 128;
+        else if (hh < e.H + e.Hkv)
+          dst = e.kc + (((size_t)seq * e.Hkv + (hh - e.H)) * e.cap + Lc + node) * 128;
+        else
+          dst = e.vc + (((size_t)seq * e.Hkv + (hh - e.H - e.Hkv)) * e.cap + Lc + node) * 128;
+        dst[p] = __float2bfloat16_rn(x0);
+        dst[p + 64] = __float2bfloat16_rn(x1);
+      } else if (a.epi == kEpiSiLU) {
+        if (!live) continue;
+        const float r = e.rs_in[m];
+        const float gg = y0 * r, uu = y1 * r;
+        e.act[(size_t)m * e.F + mt * 64 + p] = __float2bfloat16_rn(gg / (1.0f + expf(-gg)) * uu);
+      } else {  // kEpiResid
+        const int n0 = mt * 128 + p, n1 = n0 + 64;
+        float sq = 0.f;
+        if (live) {
+          float *xr = e.x + (size_t)m * e.d;
+          const float x0 = xr[n0] + y0, x1 = xr[n1] + y1;
+          xr[n0] = x0;
+          xr[n1] = x1;
+          e.h[(size_t)m * e.d + n0] = __float2bfloat16_rn(x0 * __bfloat162float(e.g[n0]));
+          e.h[(size_t)m * e.d + n1] = __float2bfloat16_rn(x1 * __bfloat162float(e.g[n1]));
+          sq = x0 * x0 + x1 * x1;
+        }
+        sq = warp_sum(sq);  // lanes of a warp share (half, ml)
+        if (live && (et & 31) == 0) e.ss[(size_t)m * (e.d / 64) + mt * 2 + (w & 1)] = sq;
+      }
+    }
+  }
+}
+
+// kEpiResid: the last tile of the launch turns the sum-of-squares partials into the
+// deferred-norm scale rs[m] = 1/sqrt(sum/d + eps), fixed summation order (warp w: rows w, w+4, ...).
+SM_DEV void resid_rs(const GemmArgs &a, int et) {
+  const EpiArgs &e = a.e;
+  const int nss = e.d / 64, lane = et & 31;
+  for (int m = et >> 5; m < a.M; m += 4) {
+    float s = 0.f;
+    for (int j = lane; j < nss; j += 32) s += __ldcg(e.ss + (size_t)m * nss + j);
+    s = warp_sum(s);
+    if (lane == 0) e.rs_out[m] = 1.0f / sqrtf(s / (float)e.d + e.eps);
+  }
+}
+
+// FUSED: compiled with the tile-epilogue fixup (GemmArgs.epi != 0).  The plain variant
+// carries none of that code: its register count (96) leaves room on an SM for the
+// consumer kernel's CTAs to become resident (and wait) while the GEMM still runs.
+template <int BN, int SMEMKB, bool FUSED>
 __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_constant__ GemmArgs a) {
   using C = GemmCfg<BN, SMEMKB>;
   constexpr int CH = C::kChunk;
@@ -78,7 +189,9 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
   uint64_t *tfull = empty + C::kStages;  // [2]
   uint64_t *tempty = tfull + 2;          // [2]
   uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 2);
+  int *s_flag = reinterpret_cast<int *>(tslot + 1);  // fused epilogue: "this CTA fixes up the tile"
 
+  SM_GT_BEGIN();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const SplitPlan &pl = a.plan;
   const int c = blockIdx.x;
@@ -113,10 +226,8 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
       const uint32_t stage_bytes = wonly ? (uint32_t)C::kA : (uint32_t)C::kStage;
       auto issue_x = [&](int s, int bi, int tt, int kc) {  // activation rows [tt*BN, tt*BN + BN)
         if (wonly) return;
-        if constexpr (BN >= 64) {
-#pragma unroll
-          for (int r = 0; r < BN / 64; ++r)
-            tma_load_2d(sB + s * C::kB + r * 8192, &a.tmX64[bi], &full[s], kc, a.x_row0 + tt * BN + r * 64);
+        if constexpr (BN >= 64) {  // tmX64 is encoded with a BN-row box: one request per stage
+          tma_load_2d(sB + s * C::kB, &a.tmX64[bi], &full[s], kc, a.x_row0 + tt * BN);
         } else {
 #pragma unroll
           for (int r = 0; r < BN / 16; ++r)
@@ -139,6 +250,7 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
         tma_prefetch_l2_2d(&a.tmW[bi], sk_kb(u, pl) * 64, mt * 128);
       }
       pdl_wait();  // activations only after the producer kernel completed
+      SM_GT_WAITED();
       for (int i = 0; i < pre; ++i) {
         const long long u = u0 + i;
         int bi, tt, mt;
@@ -213,6 +325,36 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
       }
       tc_fence_before();
       mbar_arrive(&tempty[buf]);
+      if (FUSED && a.epi != kEpiPartial) {  // last contributor of tile t applies the fused epilogue
+        const int et = threadIdx.x - 64;
+        const int cf = sk_cta_of((long long)t * pl.kb_total, pl);
+        const int nc = sk_cta_of((long long)(t + 1) * pl.kb_total - 1, pl) - cf + 1;
+        __threadfence();
+        epi_bar();
+        if (et == 0) *s_flag = atomicAdd(&a.e.tile_cnt[t], 1) == nc - 1;
+        epi_bar();
+        if (*s_flag) {
+          __threadfence();
+          if (a.dbg_mode != 2) fused_fixup<BN>(a, t, nc, et);  // experiments: 2 = protocol only
+          if (a.epi == kEpiResid) {
+            __threadfence();
+            epi_bar();
+            if (et == 0) {
+              a.e.tile_cnt[t] = 0;
+              *s_flag = atomicAdd(a.e.done_cnt, 1) == pl.tiles - 1;
+            }
+            epi_bar();
+            if (*s_flag) {
+              __threadfence();
+              resid_rs(a, et);
+              if (et == 0) *a.e.done_cnt = 0;
+            }
+          } else if (et == 0) {
+            a.e.tile_cnt[t] = 0;
+          }
+        }
+        epi_bar();  // s_flag is reused by the next segment
+      }
       u = seg_end;
       ++seg;
     }
@@ -220,13 +362,16 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<C::kTmemCols>(tmem);
+  if (threadIdx.x == 0) SM_GT_END(1000 + a.N / 128);
 }
 
 static bool g_pdl = true;
 static int g_ctas = 0;
 static int g_l2pf = 0;
 static int g_dbg_mode = 0;
+static int g_force_bn = 0;  // experiments: fixed token-tile width (0 = gemm_pick_bn)
 static int g_occ = 2;  // GEMM CTAs per SM for BN <= 64 (1..4); grid = 148 * occ
+void gemm_set_bn(int bn) { g_force_bn = bn; }
 void gemm_set_small(int v) { g_occ = v < 1 ? 1 : (v > 4 ? 4 : v); }
 int gemm_occ_for(int bn) { return bn <= 64 ? g_occ : 1; }
 void gemm_set_debug_mode(int m) { g_dbg_mode = m; }
@@ -240,7 +385,11 @@ static cudaError_t launch_bn(const GemmArgs &a, cudaStream_t st) {
   using C = GemmCfg<BN, SMEMKB>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_streamk_kernel<BN, SMEMKB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    cudaError_t e = cudaFuncSetAttribute(gemm_streamk_kernel<BN, SMEMKB, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_streamk_kernel<BN, SMEMKB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               C::kSmem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -254,14 +403,21 @@ static cudaError_t launch_bn(const GemmArgs &a, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gemm_streamk_kernel<BN, SMEMKB>, a);
+  if (a.epi != kEpiPartial) return cudaLaunchKernelEx(&cfg, gemm_streamk_kernel<BN, SMEMKB, true>, a);
+  return cudaLaunchKernelEx(&cfg, gemm_streamk_kernel<BN, SMEMKB, false>, a);
 }
 
+// Token-tile width: the smallest supported UMMA N (multiple of 16) covering M, so one
+// token tile holds every row up to 256 (each weight tile then crosses shared memory
+// once) and padding MMA work stays small (C4: b*N = 10 x 16 = 160 rows -> BN 160).
 int gemm_pick_bn(int M) {
   if (M <= 16) return 16;
   if (M <= 32) return 32;
   if (M <= 64) return 64;
+  if (M <= 96) return 96;
   if (M <= 128) return 128;
+  if (M <= 160) return 160;
+  if (M <= 192) return 192;
   return 256;
 }
 
@@ -271,7 +427,7 @@ void gemm_plan(GemmArgs &a, int N, int K, int M, int batch) {
   a.M = M;
   a.batch = batch;
   SplitPlan &p = a.plan;
-  p.bn = gemm_pick_bn(M);
+  p.bn = g_force_bn > 0 ? g_force_bn : gemm_pick_bn(M);
   p.m_tiles = (N + 127) / 128;
   p.token_tiles = (M + p.bn - 1) / p.bn;
   p.tiles = p.m_tiles * p.token_tiles * batch;
@@ -298,7 +454,10 @@ cudaError_t gemm_launch(const GemmArgs &a0, cudaStream_t st) {
                     : g_occ == 2 ? launch_bn<32, 104>(a, st) : launch_bn<32, 216>(a, st);
     case 64: return g_occ == 4 ? launch_bn<64, 50>(a, st) : g_occ == 3 ? launch_bn<64, 68>(a, st)
                     : g_occ == 2 ? launch_bn<64, 104>(a, st) : launch_bn<64, 216>(a, st);
+    case 96: return launch_bn<96, 216>(a, st);
     case 128: return launch_bn<128, 216>(a, st);
+    case 160: return launch_bn<160, 216>(a, st);
+    case 192: return launch_bn<192, 216>(a, st);
     default: return launch_bn<256, 216>(a, st);
   }
 }
@@ -309,13 +468,16 @@ cudaError_t gemm_launch(const GemmArgs &a0, cudaStream_t st) {
 template <int BN, int SK>
 static void preload_one() {
   cudaFuncAttributes fa;
-  cudaFuncGetAttributes(&fa, gemm_streamk_kernel<BN, SK>);
+  cudaFuncGetAttributes(&fa, gemm_streamk_kernel<BN, SK, false>);
+  cudaFuncGetAttributes(&fa, gemm_streamk_kernel<BN, SK, true>);
 }
 void gemm_preload() {
   preload_one<16, 50>(), preload_one<16, 68>(), preload_one<16, 104>(), preload_one<16, 216>();
   preload_one<32, 50>(), preload_one<32, 68>(), preload_one<32, 104>(), preload_one<32, 216>();
   preload_one<64, 50>(), preload_one<64, 68>(), preload_one<64, 104>(), preload_one<64, 216>();
-  preload_one<128, 216>(), preload_one<256, 216>();
+  preload_one<96, 216>(), preload_one<128, 216>(), preload_one<160, 216>(), preload_one<192, 216>();
+  preload_one<256, 216>();
 }
 
+SM_GT_READER(sm_gtrace_read_gemm)
 }  // namespace sm

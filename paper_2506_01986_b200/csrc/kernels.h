@@ -211,16 +211,49 @@ __device__ inline float load_act1(const __nv_bfloat16 *buf, int planes, int m, i
   return __bfloat162float(r[0]) + __bfloat162float(r[width]) + __bfloat162float(r[2 * width]);
 }
 
+// Fused tile epilogues of K2 (GemmArgs.epi != 0, bf16 path with tp = 1): every
+// contributor writes its partial slot, the LAST contributor of a 128-feature tile
+// (arrival counter) sums the slots in contributor order -- the same deterministic
+// order as the consumer kernels -- and applies the next step of the forward itself:
+//   kEpiQKV   y *= rs[m]; RoPE at Lc + depth (hd = 128: tile = head); q, K/V -> cache (R3)
+//   kEpiSiLU  act = bf16(SiLU(rs g) * rs u) from the 64/64 gate/up rows of the tile (R6)
+//   kEpiResid x += y (R5/R7); h = bf16(x * g) for the next GEMM (deferred R2); per-row
+//             sum-of-squares partials; the last tile of the GEMM turns them into rs[m]
+enum { kEpiPartial = 0, kEpiQKV = 1, kEpiSiLU = 2, kEpiResid = 3 };
+struct EpiArgs {
+  const float *rs_in;        // kEpiQKV / kEpiSiLU: deferred-norm scale of the input rows
+  const float2 *rope;        // kEpiQKV
+  RowCtx rc;
+  int H, Hkv, cap;
+  bf16 *q, *kc, *vc;         // q [M][H][128]; this layer's K / V cache base ([b][Hkv][cap][128])
+  bf16 *act;                 // kEpiSiLU: [M][F]
+  int F;
+  float *x;                  // kEpiResid: fp32 residual [M][d]
+  const bf16 *g;             //            next norm's gain [d]
+  bf16 *h;                   //            next GEMM input [M][d] = bf16(x * g)
+  float *ss;                 //            [M][d / 64] sum-of-squares partials
+  float *rs_out;             //            [M]
+  int d;
+  float eps;
+  int *tile_cnt;             // arrival counters (zero between launches; the fixup resets its own)
+  int *done_cnt;             // tiles fixed up in this launch (kEpiResid), reset by the last
+};
+
 struct GemmArgs {
   CUtensorMap tmW[kMaxGemmBatch];  // weight [N][K] bf16, box 64(k) x 128(rows), SWIZZLE_128B
   CUtensorMap tmX[kMaxGemmBatch];  // activation [rows][K] bf16, box 64(k) x 16(rows), SWIZZLE_128B
-  CUtensorMap tmX64[kMaxGemmBatch];  // same activation, box 64(k) x 64(rows): one TMA per 64 token rows
+  CUtensorMap tmX64[kMaxGemmBatch];  // same activation, box 64(k) x BN rows (BN >= 64): one TMA per stage
+  const void *x_base[kMaxGemmBatch];  // host bookkeeping: activation base / rows (re-encode tmX64 per BN)
+  int x_rows[kMaxGemmBatch];
+  int x_box;                          // box rows tmX64 is currently encoded with
   int N, K, M, batch;
   int x_row0;                      // first activation row (TMA row offset)
   int l2_prefetch;                 // weight k-blocks per CTA prefetched into L2 before the PDL wait
   int dbg_mode;                    // experiments: 1 = stream weights only (no X, no MMA)
   SplitPlan plan;
   float *ws;                       // partial slots, gemm_ws_floats() floats
+  int epi;                         // kEpi*: fused tile epilogue (batch 1 only)
+  EpiArgs e;
 };
 void gemm_plan(GemmArgs &a, int N, int K, int M, int batch);
 cudaError_t gemm_launch(const GemmArgs &a, cudaStream_t st);
@@ -232,6 +265,7 @@ void gemm_set_ctas(int n);
 void gemm_set_l2_prefetch(int kblocks);
 void gemm_set_debug_mode(int m);
 void gemm_set_small(int v);
+void gemm_set_bn(int bn);  // experiments: force the token-tile width (16..256 supported set; 0 = auto)
 
 // ---------------------------------------------------------------- K1 tree attention
 struct AttnArgs {
@@ -263,15 +297,17 @@ void attention_set_tc(int on);                  // head_dim 128: tcgen05 kernel 
 // its own dependent launch early (programmatic dependent launch).
 cudaError_t embed_launch(const int32_t *tok, const bf16 *E, float *x, int M, int d, cudaStream_t st);
 // x[m] += y[m] (if pv), then h = bf16(rmsnorm(x) * g)    (R5/R7 + R2/R8)
-// hp = planes of h (1: bf16; 3: fp32 parity mode, split rows)
+// hp = planes of h (1: bf16; 3: fp32 parity mode, split rows).  rs_out != nullptr:
+// deferred RMSNorm (R2): h = x * g, rs_out[m] = 1/sqrt(mean(x^2) + eps); else h = rms(x) * g.
 cudaError_t resid_norm_launch(const PartialView *pv, float *x, const bf16 *g, bf16 *h, int M, int d, float eps,
-                              int hp, cudaStream_t st);
+                              int hp, float *rs_out, cudaStream_t st);
 // q/k/v = y; RoPE(q, k) at pos Lc + depth; q -> q[m][H][hd], k/v -> cache slot Lc + node   (R3)
 // pv.planes == 3 (fp32 parity mode): q and the caches are fp32, else bf16.
+// rs (nullable): per-row deferred RMSNorm scale multiplied into y first.
 cudaError_t qkv_consumer_launch(const PartialView &pv, RowCtx rc, int H, int Hkv, int hd, const float2 *rope, void *q,
-                                void *kcache, void *vcache, int cap, cudaStream_t st);
+                                void *kcache, void *vcache, int cap, const float *rs, cudaStream_t st);
 // act[m][f] = bf16(SiLU(gate) * up), gate/up interleaved per 64 rows    (R6)
-cudaError_t silu_consumer_launch(const PartialView &pv, int F, bf16 *act, cudaStream_t st);
+cudaError_t silu_consumer_launch(const PartialView &pv, int F, bf16 *act, const float *rs, cudaStream_t st);
 // LM rows: z = y (fp32, optional copy), argmax (lowest index on ties) and the
 // single-pass typical statistics (m, s, t) of z * inv_temp    (R9)
 cudaError_t logits_consumer_launch(const PartialView &pv, float inv_temp, float *z_out, int32_t *argmax, float *stats,
@@ -287,6 +323,7 @@ cudaError_t heads_r_consumer_launch(const PartialView &pv, int nmed, int nb, int
 // top-k of the U-head logits y_i[b][:]: idx[b][i][k], (value desc, index asc)    (K3)
 cudaError_t topk_consumer_launch(const PartialView &pv, int nmed, int nb, int V, int k, int32_t *idx, int idx_offset,
                                  float *vals, cudaStream_t st);
+void consumer_set_ctas(int n);  // experiments: cap the consumer grids (persistent), 0 = uncapped
 // stage API: top-k of plain fp32 rows
 cudaError_t topk_launch(const float *logits, int rows, int V, int k, int32_t *idx, cudaStream_t st);
 // stage API: out[m][n] = y[m][n]
@@ -345,7 +382,7 @@ struct TpArgs {
 };
 // Residual all-reduce fused into residual + RMSNorm (pv = this rank's o_proj / down partials).
 cudaError_t resid_norm_tp_launch(const PartialView &pv, float *x, const bf16 *g, bf16 *h, int M, int d, float eps,
-                                 const TpArgs &tp, cudaStream_t st);
+                                 const TpArgs &tp, float *rs_out, cudaStream_t st);
 // Merge the vocab-parallel LM head statistics of rows [0, rows): in = this rank's
 // (amax, argmax, m, s, t) per row; cand (nullable) = z[parent(n)][tok[n]] when the rank
 // owns tok[n] (tree rows, typical acceptance); out: merged argmax / stats / cand.

@@ -71,8 +71,21 @@ static sm_status weight_map(CUtensorMap *m, const void *w, int N, int K) {
 }
 // activation maps of GEMM batch entry i: 16-row and 64-row boxes (BN < 64 / BN >= 64)
 static sm_status act_map(GemmArgs &a, int i, const void *x, int rows, int K) {
+  a.x_base[i] = x;
+  a.x_rows[i] = rows;
+  a.x_box = 64;
   CKS(make_tmap(&a.tmX[i], x, (uint64_t)rows, (uint64_t)K, 16, 64, true));
   return make_tmap(&a.tmX64[i], x, (uint64_t)rows, (uint64_t)K, 64, 64, true);
+}
+// BN >= 64: the kernel loads a stage's BN activation rows with one TMA box of BN rows
+// (request count, not bytes, limits the L2 -> SM fill of small boxes).
+static sm_status act_box(GemmArgs &a) {
+  const int bn = a.plan.bn;
+  if (bn < 64 || bn == a.x_box) return SM_OK;
+  for (int i = 0; i < a.batch; ++i)
+    CKS(make_tmap(&a.tmX64[i], a.x_base[i], (uint64_t)a.x_rows[i], (uint64_t)a.K, (uint32_t)bn, 64, true));
+  a.x_box = bn;
+  return SM_OK;
 }
 static sm_status kv_map(CUtensorMap *m, const void *base, uint64_t rows, int hd) {
   const bool sw = hd >= 64;
@@ -252,6 +265,12 @@ struct sm_model {
   std::vector<const bf16 *> attn_norm, wqkv, wo, mlp_norm, wgu, wdown, mR, mb, mU;
   // workspace
   float *x = nullptr, *part = nullptr, *z = nullptr, *stats = nullptr;
+  float *rs = nullptr;  // [R] deferred RMSNorm scale of the current GEMM input rows (R2)
+  // fused tile epilogues (GemmArgs.epi): bf16, tp = 1, hd = 128, d % 128 == 0
+  bool fused = false;
+  int fuse_mask = 0;
+  float *ss = nullptr;   // [R][d/64] sum-of-squares partials of kEpiResid
+  int *tile_cnt = nullptr, *done_cnt = nullptr;
   bf16 *h = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr, *hf = nullptr, *head_in = nullptr,
        *r_buf = nullptr;
   int32_t *argmax = nullptr;
@@ -338,14 +357,23 @@ static void prof_end(cudaStream_t st, cudaEvent_t a, int kind, double bytes) {
 }
 
 static int g_ablate_gemm = 0;  // set while enqueueing ablated per-layer GEMMs
+static int g_epi_test = 0;     // experiments: sm_gemm_bf16(out = NULL) runs the fused SiLU epilogue
+static int g_fused = 0;  // sm_set_option("fused_epilogue"): K2 tile epilogues instead of consumer kernels
+                         // (bit 1 QKV/RoPE, bit 2 SiLU, bit 4 residual + deferred norm; 0 = consumers)
+static constexpr int kMaxFusedTiles = 1 << 14;
 // Launch one stream-K GEMM over rows [x_row0, x_row0 + M) of the prototype's
 // activation map; its fp32 partials land in ws and are described by *pv.
 // planes = 3 (fp32 parity mode): logical row m is GEMM rows 3m..3m+2.
 static sm_status run_gemm(GemmArgs a, int M, int x_row0, float *ws, size_t ws_floats, cudaStream_t st, int &nl,
-                          PartialView *pv, int planes = 1) {
+                          PartialView *pv, int planes = 1, int epi = kEpiPartial, const EpiArgs *ea = nullptr) {
   const int Mlog = M;
   M *= planes;
   gemm_plan(a, a.N, a.K, M, a.batch);
+  a.epi = epi;
+  if (ea) a.e = *ea;
+  if (epi != kEpiPartial && (a.batch != 1 || a.plan.tiles > kMaxFusedTiles || planes != 1))
+    return fail(SM_ERR_INVALID_ARG, "fused GEMM epilogue: batch 1, bf16, <= 16384 tiles");
+  CKS(act_box(a));
   a.x_row0 = x_row0 * planes;
   a.ws = ws;
   if (gemm_ws_floats(a) > ws_floats) return fail(SM_ERR_INVALID_ARG, "GEMM partial workspace too small");
@@ -428,6 +456,8 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
   m->f32 = c.dtype == SM_DTYPE_FP32;
   m->P = m->f32 ? 3 : 1;
   m->hdu = c.head_dim * (m->f32 ? 2 : 1);
+  m->fused = !m->f32 && tp == 1 && c.head_dim == 128 && c.d_model % 128 == 0 && g_fused != 0;
+  m->fuse_mask = m->fused ? g_fused : 0;
   m->embed = (const bf16 *)w->embed;
   m->final_norm = (const bf16 *)w->final_norm;
   m->lm_head = (const bf16 *)w->lm_head;
@@ -452,6 +482,12 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
     return s;                             \
   }
   ALLOC(m->x, (size_t)R * d, "x");
+  ALLOC(m->rs, (size_t)R, "rms scale");
+  ALLOC(m->ss, (size_t)R * std::max(1, d / 64), "sum-of-squares partials");
+  ALLOC(m->tile_cnt, (size_t)kMaxFusedTiles, "tile counters");
+  ALLOC(m->done_cnt, 1, "tile counters");
+  cudaMemset(m->tile_cnt, 0, (size_t)kMaxFusedTiles * sizeof(int));
+  cudaMemset(m->done_cnt, 0, sizeof(int));
   ALLOC(m->h, (size_t)R * d * P, "h");
   ALLOC(m->q, (size_t)R * Hhd * (m->f32 ? 2 : 1), "q");  // fp32 q in the parity mode
   ALLOC(m->attn, (size_t)R * Hhd * P, "attn");
@@ -560,6 +596,10 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
 extern "C" void sm_model_destroy(sm_model *m) {
   if (!m) return;
   cudaFree(m->x);
+  cudaFree(m->rs);
+  cudaFree(m->ss);
+  cudaFree(m->tile_cnt);
+  cudaFree(m->done_cnt);
   cudaFree(m->part);
   cudaFree(m->ws);
   cudaFree(m->z);
@@ -776,12 +816,16 @@ static int attn_splits(const sm_model *m, int nseq, int Nq) {
 static int g_ablate = 0;
 #define KEEP(bit) ((g_ablate & (bit)) == 0)
 
-// x += y (all-reduced across ranks under TP); h = bf16(rms(x) * g)
-static sm_status resid_norm(sm_model *m, const PartialView *pv, const bf16 *g, bf16 *h, int M, cudaStream_t st) {
+// x += y (all-reduced across ranks under TP); deferred (per-layer norms, R2):
+// h = bf16(x * g) and m->rs = 1/sqrt(mean(x^2) + eps) for the next GEMM's consumer;
+// else (final norm, R8) h = bf16(rms(x) * g).
+static sm_status resid_norm(sm_model *m, const PartialView *pv, const bf16 *g, bf16 *h, int M, cudaStream_t st,
+                            bool deferred) {
+  float *rs = deferred ? m->rs : nullptr;
   if (m->tp > 1 && pv) {
-    CK(resid_norm_tp_launch(*pv, m->x, g, h, M, m->d, m->cfg.rms_eps, tp_next(m), st));
+    CK(resid_norm_tp_launch(*pv, m->x, g, h, M, m->d, m->cfg.rms_eps, tp_next(m), rs, st));
   } else {
-    CK(resid_norm_launch(pv, m->x, g, h, M, m->d, m->cfg.rms_eps, m->P, st));
+    CK(resid_norm_launch(pv, m->x, g, h, M, m->d, m->cfg.rms_eps, m->P, rs, st));
   }
   return SM_OK;
 }
@@ -800,18 +844,47 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
   PartialView pv, pv_down{};
   bool have_down = false;
   g_ablate_gemm = (g_ablate & 4) ? 1 : 0;
+  // Fused path (m->fused): the consumers below run inside the K2 GEMMs as tile
+  // epilogues (kEpi*, gemm.cu); only the first layer's norm and the final norm
+  // remain separate kernels.  Same rounding contract, same summation order.
+  EpiArgs ea;
+  std::memset(&ea, 0, sizeof(ea));
+  ea.rope = m->rope;
+  ea.rc = rc;
+  ea.H = m->H;
+  ea.Hkv = m->Hkv;
+  ea.cap = kv->cap;
+  ea.q = m->q;
+  ea.act = m->act;
+  ea.F = m->F;
+  ea.x = m->x;
+  ea.h = m->h;
+  ea.ss = m->ss;
+  ea.d = d;
+  ea.eps = m->cfg.rms_eps;
+  ea.tile_cnt = m->tile_cnt;
+  ea.done_cnt = m->done_cnt;
+  const int fm = (m->fused && KEEP(2)) ? m->fuse_mask : 0;
+  const bool fq = fm & 1, fs = fm & 2, fr = fm & 4;
   for (int l = 0; l < m->L; ++l) {
-    // x += down (previous layer, R7); h = bf16(rms(x) * g1)   (R2)
-    if (KEEP(2)) {
-      CKS(resid_norm(m, have_down ? &pv_down : nullptr, m->attn_norm[l], m->h, M, st));
+    // x += down (previous layer, R7); h = bf16(x * g1), rs  (deferred R2)
+    if (KEEP(2) && (!fr || l == 0)) {
+      CKS(resid_norm(m, have_down ? &pv_down : nullptr, m->attn_norm[l], m->h, M, st, true));
       ++nl;
     }
     bf16 *kc = kv->base + (size_t)l * layer_rows * m->hdu;  // bf16 units (fp32 rows are 2 hd units)
     bf16 *vc = kc + (size_t)half_rows * m->hdu;
-    CKS(run_gemm(m->g_qkv[l], M, 0, m->ws, m->ws_floats, st, nl, &pv, m->P));
+    if (fq) {  // QKV GEMM with the RoPE + cache-write epilogue
+      ea.kc = kc;
+      ea.vc = vc;
+      ea.rs_in = m->rs;
+      CKS(run_gemm(m->g_qkv[l], M, 0, m->ws, m->ws_floats, st, nl, &pv, 1, kEpiQKV, &ea));
+    } else {
+      CKS(run_gemm(m->g_qkv[l], M, 0, m->ws, m->ws_floats, st, nl, &pv, m->P));
+    }
     // RoPE, q -> m->q, k/v -> cache slots Lc + node (R3)
-    if (KEEP(2)) {
-      CK(qkv_consumer_launch(pv, rc, m->H, m->Hkv, m->hd, m->rope, m->q, kc, vc, kv->cap, st));
+    if (KEEP(2) && !fq) {
+      CK(qkv_consumer_launch(pv, rc, m->H, m->Hkv, m->hd, m->rope, m->q, kc, vc, kv->cap, m->rs, st));
       ++nl;
     }
     AttnArgs aa;
@@ -846,23 +919,41 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
       ++nl;
     }
     prof_end(st, ev, 1, 0.0);
-    CKS(run_gemm(m->g_o[l], M, 0, m->ws, m->ws_floats, st, nl, &pv, m->P));
-    // x += o (R5); h = bf16(rms(x) * g2)
-    if (KEEP(2)) {
-      CKS(resid_norm(m, &pv, m->mlp_norm[l], m->h, M, st));
-      ++nl;
+    // x += o (R5); h = bf16(x * g2), rs  (deferred R2)
+    if (fr) {
+      ea.g = m->mlp_norm[l];
+      ea.rs_out = m->rs;
+      CKS(run_gemm(m->g_o[l], M, 0, m->ws, m->ws_floats, st, nl, &pv, 1, kEpiResid, &ea));
+    } else {
+      CKS(run_gemm(m->g_o[l], M, 0, m->ws, m->ws_floats, st, nl, &pv, m->P));
+      if (KEEP(2)) {
+        CKS(resid_norm(m, &pv, m->mlp_norm[l], m->h, M, st, true));
+        ++nl;
+      }
     }
-    CKS(run_gemm(m->g_gu[l], M, 0, m->ws, m->ws_floats, st, nl, &pv, m->P));
-    if (KEEP(2)) {
-      CK(silu_consumer_launch(pv, m->F, m->act, st));  // act = bf16(SiLU(g) * u) (R6)
-      ++nl;
+    if (fs) {  // act = bf16(SiLU(rs g) * rs u) (R6) in the GEMM's tile epilogue
+      ea.rs_in = m->rs;
+      CKS(run_gemm(m->g_gu[l], M, 0, m->ws, m->ws_floats, st, nl, &pv, 1, kEpiSiLU, &ea));
+    } else {
+      CKS(run_gemm(m->g_gu[l], M, 0, m->ws, m->ws_floats, st, nl, &pv, m->P));
+      if (KEEP(2)) {
+        CK(silu_consumer_launch(pv, m->F, m->act, m->rs, st));  // act = bf16(SiLU(rs g) * rs u) (R6)
+        ++nl;
+      }
     }
-    CKS(run_gemm(m->g_down[l], M, 0, m->ws, m->ws_floats, st, nl, &pv_down, m->P));
-    have_down = true;
+    if (fr && l + 1 < m->L) {  // x += down (R7); h = bf16(x * g1 of the next layer), rs
+      ea.g = m->attn_norm[l + 1];
+      ea.rs_out = m->rs;
+      CKS(run_gemm(m->g_down[l], M, 0, m->ws, m->ws_floats, st, nl, &pv_down, 1, kEpiResid, &ea));
+      have_down = false;  // already added into x
+    } else {  // the final norm (R8, not deferred) needs the whole row: consumer kernel
+      CKS(run_gemm(m->g_down[l], M, 0, m->ws, m->ws_floats, st, nl, &pv_down, m->P));
+      have_down = true;
+    }
   }
   g_ablate_gemm = 0;
   // x += down; hf = bf16(rms(x) * gf)   (R8)
-  CKS(resid_norm(m, have_down ? &pv_down : nullptr, m->final_norm, m->hf, M, st));
+  CKS(resid_norm(m, have_down ? &pv_down : nullptr, m->final_norm, m->hf, M, st, false));
   ++nl;
   return SM_OK;
 }
@@ -1184,7 +1275,7 @@ extern "C" sm_status sm_tree_attention(const sm_tree *t, const void *d_q, const 
 
 extern "C" sm_status sm_gemm_bf16(const void *d_x, const void *d_w, float *d_out, int M, int N, int K,
                                   void *stream) {
-  if (!d_x || !d_w || !d_out || M < 1 || M > 1024 || N < 1 || K < 8 || K % 8)
+  if (!d_x || !d_w || M < 1 || M > 1024 || N < 1 || K < 8 || K % 8)
     return fail(SM_ERR_INVALID_ARG, "sm_gemm_bf16: bad arguments (M <= 1024, K % 8 == 0)");
   GemmArgs a = gemm_proto(N, K, 1);
   CKS(weight_map(&a.tmW[0], d_w, N, K));
@@ -1194,8 +1285,35 @@ extern "C" sm_status sm_gemm_bf16(const void *d_x, const void *d_w, float *d_out
   CKS(scratch(need * 4, &scr));
   int nl = 0;
   PartialView pv;
+  if (g_epi_test && !d_out) {  // experiments: the fused SiLU tile epilogue on scratch buffers
+    static float *rs1 = nullptr;
+    static bf16 *act = nullptr;
+    static int *cnt = nullptr;
+    static size_t act_n = 0;
+    if (!rs1) {
+      CKS(dalloc(&rs1, 1024, "epi test"));
+      CKS(dalloc(&cnt, kMaxFusedTiles + 1, "epi test"));
+      cudaMemset(cnt, 0, (kMaxFusedTiles + 1) * sizeof(int));
+      std::vector<float> ones(1024, 1.0f);
+      cudaMemcpy(rs1, ones.data(), 4096, cudaMemcpyHostToDevice);
+    }
+    if ((size_t)M * N / 2 > act_n) {
+      cudaFree(act);
+      act_n = (size_t)M * N / 2;
+      CKS(dalloc(&act, act_n, "epi test"));
+    }
+    EpiArgs ea;
+    std::memset(&ea, 0, sizeof(ea));
+    ea.rs_in = rs1;
+    ea.act = act;
+    ea.F = N / 2;
+    ea.tile_cnt = cnt;
+    ea.done_cnt = cnt + kMaxFusedTiles;
+    CKS(run_gemm(a, M, 0, (float *)scr, need, (cudaStream_t)stream, nl, &pv, 1, kEpiSiLU, &ea));
+    return SM_OK;
+  }
   CKS(run_gemm(a, M, 0, (float *)scr, need, (cudaStream_t)stream, nl, &pv));
-  CK(plain_consumer_launch(pv, d_out, (cudaStream_t)stream));
+  if (d_out) CK(plain_consumer_launch(pv, d_out, (cudaStream_t)stream));  // NULL: GEMM only (timing)
   return SM_OK;
 }
 
@@ -1215,10 +1333,21 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
     gemm_set_ctas(value);
   } else if (n == "l2_prefetch") {
     gemm_set_l2_prefetch(value);
+  } else if (n == "gemm_bn") {
+    if (value != 0 && value != 16 && value != 32 && value != 64 && value != 96 && value != 128 && value != 160 &&
+        value != 192 && value != 256)
+      return fail(SM_ERR_INVALID_ARG, "gemm_bn must be 0 or one of 16 32 64 96 128 160 192 256");
+    gemm_set_bn(value);
   } else if (n == "gemm_occ") {
     gemm_set_small(value);
   } else if (n == "gemm_mode") {
     gemm_set_debug_mode(value);
+  } else if (n == "fused_epilogue") {  // takes effect for models created afterwards
+    g_fused = value & 7;
+  } else if (n == "consumer_ctas") {
+    consumer_set_ctas(value);
+  } else if (n == "epi_test") {
+    g_epi_test = value;
   } else if (n == "ablate") {
     g_ablate = value;
   } else if (n == "attn_tc") {

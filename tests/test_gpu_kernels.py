@@ -47,7 +47,8 @@ def test_device_generator_bitwise(sm, seed, stream, n, mode, start):
 
 # ------------------------------------------------------------------ K2 GEMM
 @pytest.mark.parametrize("M,N,K", [(1, 128, 64), (16, 4096, 4096), (37, 192, 320), (64, 12288, 512),
-                                   (200, 1000, 72), (256, 384, 1024), (64, 4096, 11008)])
+                                   (200, 1000, 72), (256, 384, 1024), (64, 4096, 11008),
+                                   (80, 4096, 512), (160, 10240, 1024), (150, 1000, 200), (192, 384, 8192)])
 def test_gemm_matches_fp64(sm, M, N, K):
     x = bf16_tensor(synth.normal_bits(1, 100 + M, M * K), (M, K))
     w = bf16_tensor(synth.weight_bits(2, 200 + N, N * K), (N, K))
