@@ -59,6 +59,23 @@ sm_status sm_tree_create(const int32_t *h_ranks_flat, const int32_t *h_path_offs
                          sm_tree **out);
 /* Chain tree of n nodes (node i = depth i): used for prefill chunks.        */
 sm_status sm_tree_create_chain(int n, sm_tree **out);
+/* Tree construction ("Optimizing attention mask").  Host
+ * only (no device work); results are ordinary trees in canonical order.  Readings in
+ * DESIGN.md (Q30, R4).  Errors: SM_ERR_INVALID_ARG (more than 256 nodes, bad k / l),
+ * SM_ERR_INFEASIBLE_TREE (target / features no tree of this kind can meet).
+ *   full        Eq. 2 full tree: sum_{i<=l} k^i nodes.
+ *   prune       R4 in-place pruning of an existing mask to target_nodes (Medusa's
+ *               right-to-left pruning: repeatedly drop the lexicographically largest leaf).
+ *   pruned_full full tree pruned by the scaled logistic per-level rate
+ *               r(i) = r_min + (r_max - r_min) / (1 + exp(-steep (i - mid))) (fig:prunefunc,
+ *               parameters unreadable in the paper: SPEC defaults 0.1 / 0.95 / 2.5 / 2);
+ *               level 1 keeps all k nodes, level i its first ceil((1 - r(i)) k^i).
+ *   custom      a tree with exactly n_nodes nodes and n_leaves leaves, arity <= k, depth
+ *               <= l ("directly builds tree mask structures with exact features"). */
+sm_status sm_tree_create_full(int k, int l, sm_tree **out);
+sm_status sm_tree_prune(const sm_tree *t, int target_nodes, sm_tree **out);
+sm_status sm_tree_create_pruned_full(int k, int l, float r_min, float r_max, float mid, float steep, sm_tree **out);
+sm_status sm_tree_create_custom(int n_nodes, int n_leaves, int k, int l, sm_tree **out);
 /* Query the canonical tables (host outputs, any pointer may be NULL):
  *   N, S (leaves), depth (max depth l), parent[N], node_depth[N], rank[N],
  *   anc_bits[N][4] (bit j of word j/64 = node j is n or an ancestor of n),

@@ -145,3 +145,92 @@ def prune_right_to_left(choices: list[list[int]], target_nodes: int, topk: int =
         lv = [t for t in cur if not any(len(u) == len(t) + 1 and u[:len(t)] == t for u in cur)]
         cur.remove(max(lv))
     return [list(t) for t in sorted(cur, key=lambda t: (len(t), t))]
+
+
+# ----------------------------------------------------------------- f1: SpecMemo tree construction
+def full_tree(k: int, l: int) -> list[list[int]]:
+    """Full k-ary tree of depth l as a path list: Eq. 2's N = sum_{i=0}^{l} k^i nodes."""
+    out, level = [], [[]]
+    for _ in range(l):
+        level = [p + [r] for p in level for r in range(k)]
+        out += level
+    return out
+
+
+def prune_rate(level: int, r_min: float = 0.1, r_max: float = 0.95, mid: float = 2.5, steep: float = 2.0) -> float:
+    """Scaled logistic per-level pruning rate (fig:prunefunc; "low at first levels
+    ... increase the rate on deeper levels"):  r(i) = r_min + (r_max - r_min) / (1 + exp(-steep (i - mid))).
+    The four parameters are unreadable in the paper (an image): parity unpinned; defaults = SPEC S:220."""
+    import math
+    return r_min + (r_max - r_min) / (1.0 + math.exp(-steep * (level - mid)))
+
+
+def prune_full_tree(k: int, l: int, r_min=0.1, r_max=0.95, mid=2.5, steep=2.0) -> list[list[int]]:
+    """Custom tree build via pruning (P:247): level 1 keeps all k nodes (first-level rule, P:245);
+    level i >= 2 keeps the first ceil((1 - r(i)) * k^i) nodes of the full tree's level, left to right
+    (lexicographic rank path = highest-probability tokens first), minus those whose parent was dropped."""
+    import math
+    kept = [[r] for r in range(k)] if l >= 1 else []
+    prev = set(tuple(p) for p in kept)
+    for i in range(2, l + 1):
+        n_i = math.ceil((1.0 - prune_rate(i, r_min, r_max, mid, steep)) * k ** i - 1e-9)
+        level = [list(p) + [r] for p in sorted(prev) for r in range(k)]  # left to right
+        level = level[:n_i]
+        kept += level
+        prev = set(tuple(p) for p in level)
+        if not prev:
+            break
+    return kept
+
+
+def build_custom_tree(n_nodes: int, n_leaves: int, k: int, l: int) -> list[list[int]]:
+    """Custom tree build from tree features (Alg. 1's (N, S) pairs) -- the
+    construction rule is not in the paper (reading Q30): start from the root and
+    c1 = min(k, N-1, S) level-1 nodes; then add the remaining nodes one at a time:
+      (a) N - 1 - c1 - (S - c1) "deepening" additions first: a child of the first leaf in DFS
+          order whose depth < l (leaf count unchanged), so depth concentrates on the left;
+      (b) then "widening" additions: the next-rank child of the first node in BFS order (shallowest,
+          then leftmost) that already has children and fewer than k (one more leaf each); a
+          widening step is taken early only when every leaf already sits at depth l.
+    Raises InfeasibleTree when (N, S, k, l) admits no tree under this rule."""
+    N, S = n_nodes, n_leaves
+    if N < 1 or S < 1 or (N == 1 and S != 1) or S > N - 1 + (N == 1):
+        raise InfeasibleTree("need 1 <= S <= N - 1 (or N = S = 1)")
+    if N == 1:
+        return []
+    c1 = min(k, N - 1, S)
+    paths = [[r] for r in range(c1)]
+    children = {(): c1}
+    leaves_now = c1
+    widen = S - leaves_now
+    deepen = (N - 1 - c1) - widen
+    if widen < 0 or deepen < 0:
+        raise InfeasibleTree("(N, S) not reachable: too many leaves for the nodes")
+
+    def sorted_paths():
+        return sorted(paths)                                            # DFS = lexicographic
+
+    def widen_one():
+        internal = sorted((p for p in [[]] + paths if 0 < children.get(tuple(p), 0) < k), key=lambda p: (len(p), p))
+        if not internal:
+            raise InfeasibleTree("no internal node with free arity to widen")
+        p = internal[0]
+        r = children[tuple(p)]
+        paths.append(p + [r])
+        children[tuple(p)] = r + 1
+
+    while deepen > 0:
+        cands = [p for p in sorted_paths() if len(p) < l and children.get(tuple(p), 0) == 0]
+        if cands:                      # deepening preferred
+            p = cands[0]
+            paths.append(p + [0])
+            children[tuple(p)] = 1
+            deepen -= 1
+        elif widen > 0:                # every leaf is at depth l: widen once, then deepen again
+            widen_one()
+            widen -= 1
+        else:
+            raise InfeasibleTree("no leaf above depth l to deepen")
+    for _ in range(widen):
+        widen_one()
+    return sorted(paths, key=lambda p: (len(p), p))

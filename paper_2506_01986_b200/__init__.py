@@ -123,6 +123,56 @@ class Tree:
         self.N, self.S, self.depth = q["N"], q["S"], q["depth"]
         self.topk = topk
 
+    @classmethod
+    def _from_handle(cls, h: ctypes.c_void_p, topk: int) -> "Tree":
+        t = cls.__new__(cls)
+        t._h = h
+        q = t.query()
+        t.N, t.S, t.depth = q["N"], q["S"], q["depth"]
+        t.topk = topk
+        return t
+
+    # tree construction (f1; include/specmemo.h)
+    @classmethod
+    def full(cls, k: int, l: int) -> "Tree":
+        h = ctypes.c_void_p()
+        _check(lib().sm_tree_create_full(ctypes.c_int(k), ctypes.c_int(l), ctypes.byref(h)))
+        return cls._from_handle(h, k)
+
+    def pruned(self, target_nodes: int) -> "Tree":
+        """R4 right-to-left in-place pruning to target_nodes."""
+        h = ctypes.c_void_p()
+        _check(lib().sm_tree_prune(self._h, ctypes.c_int(target_nodes), ctypes.byref(h)))
+        return Tree._from_handle(h, self.topk)
+
+    @classmethod
+    def pruned_full(cls, k: int, l: int, r_min: float = 0.1, r_max: float = 0.95, mid: float = 2.5,
+                    steep: float = 2.0) -> "Tree":
+        h = ctypes.c_void_p()
+        _check(lib().sm_tree_create_pruned_full(ctypes.c_int(k), ctypes.c_int(l), ctypes.c_float(r_min),
+                                                ctypes.c_float(r_max), ctypes.c_float(mid), ctypes.c_float(steep),
+                                                ctypes.byref(h)))
+        return cls._from_handle(h, k)
+
+    @classmethod
+    def custom(cls, n_nodes: int, n_leaves: int, k: int, l: int) -> "Tree":
+        h = ctypes.c_void_p()
+        _check(lib().sm_tree_create_custom(ctypes.c_int(n_nodes), ctypes.c_int(n_leaves), ctypes.c_int(k),
+                                           ctypes.c_int(l), ctypes.byref(h)))
+        return cls._from_handle(h, k)
+
+    def paths(self) -> list[list[int]]:
+        """Rank paths of nodes 1..N-1 in canonical order (root implicit)."""
+        q = self.query()
+        out = []
+        for n in range(1, q["N"]):
+            p, x = [], n
+            while x > 0:
+                p.append(int(q["rank"][x]))
+                x = int(q["parent"][x])
+            out.append(p[::-1])
+        return out
+
     def query(self) -> dict:
         N, S, dep = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
         _check(lib().sm_tree_query(self._h, ctypes.byref(N), ctypes.byref(S), ctypes.byref(dep), None, None, None,

@@ -421,9 +421,13 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
     const float *sml = so + ROWS * HD;
     float *swt = reinterpret_cast<float *>(sP);  // [rows_per][8] combine weights w_q / L
     const uint32_t so_u = smem_u32(so), sml_u = smem_u32(sml);
-    const int rows_per = ROWS / a.nsplit;
+    // the block's LIVE rows are dealt evenly to the ranks (N*G = 64 of 128 rows: 16 per rank
+    // at 4 splits instead of 32 on two ranks and none on the others)
+    const int live_tot = max(0, min(ROWS, R - rblk * ROWS));
+    const int rows_per = (live_tot + a.nsplit - 1) / a.nsplit;
     const int lr0 = split * rows_per;
-    for (int lr = threadIdx.x; lr < rows_per; lr += blockDim.x) {
+    const int live_rows = max(0, min(rows_per, live_tot - lr0));
+    for (int lr = threadIdx.x; lr < live_rows; lr += blockDim.x) {
       float mq[8], lq[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -445,7 +449,6 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
       for (int q = 0; q < 8; ++q) swt[lr * 8 + q] = wq[q] * inv;
     }
     __syncthreads();
-    const int live_rows = max(0, min(rows_per, R - (rblk * ROWS + lr0)));
     const int items = live_rows * (HD / 4);
     for (int e0 = threadIdx.x; e0 < items; e0 += 2 * blockDim.x) {  // two items per pass: 2 x nsplit loads in flight
       float4 v[2][8];

@@ -23,10 +23,9 @@
 
 namespace sm {
 
-// Grid cap of the consumer kernels (sm_set_option "consumer_ctas"; experiments): a cap makes
-// them persistent (grid-stride), default = one CTA per work item.
-static int g_consumer_ctas = 1 << 30;
-void consumer_set_ctas(int n) { g_consumer_ctas = n > 0 ? n : (1 << 30); }
+// Block size of the qkv / SiLU consumers (sm_set_option "consumer_threads", experiments: 128 or 256).
+static int g_consumer_threads = 256;
+void consumer_set_threads(int n) { g_consumer_threads = n == 128 ? 128 : 256; }
 
 template <int NT>
 SM_DEV float block_sum(float v, float *red) {
@@ -68,21 +67,16 @@ constexpr int kNormCols = 4 * kNormThreads;
 // rs_out != nullptr: deferred RMSNorm (rounding contract R2): h = x * g and rs_out[m] =
 // 1/sqrt(mean(x^2) + eps), applied by the consumer of the next GEMM; else h = x * rs * g.
 __global__ void __launch_bounds__(kNormThreads) resid_norm_kernel(PartialView pv, int has_pv, float *x, const bf16 *g,
-                                                                  bf16 *h, int M, int d, float eps, int hp,
-                                                                  float *rs_out) {
+                                                                  bf16 *h, int d, float eps, int hp, float *rs_out) {
   SM_GT_BEGIN();
   __shared__ float red[kNormThreads / 32];
-  __shared__ float ssq[2][8];  // ssq[it & 1][q] = block sum of cluster rank q (double-buffered by row)
+  __shared__ float ssq[8];  // ssq[q] = block sum of cluster rank q
   pdl_trigger();
   cluster_arrive_relaxed();  // phase 1: every CTA of the cluster has started (before any DSMEM store)
   pdl_wait();
   SM_GT_WAITED();
-  const int rank = blockIdx.x, cs = gridDim.x;
+  const int m = blockIdx.y, rank = blockIdx.x, cs = gridDim.x;
   const int i = rank * kNormCols + threadIdx.x * 4;
-  int it = 0;
-  // persistent over rows: the grid stays within what is co-resident with a running GEMM,
-  // so every CTA is already waiting when the GEMM completes
-  for (int m = blockIdx.y; m < M; m += gridDim.y, ++it) {
   float *xr = x + (size_t)m * d;
   float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
   if (i < d) {
@@ -104,11 +98,11 @@ __global__ void __launch_bounds__(kNormThreads) resid_norm_kernel(PartialView pv
     }
   }
   float ss = block_sum<kNormThreads>(a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w, red);
-  if (it == 0) cluster_wait();
-  if (threadIdx.x < cs) st_dsmem_f32(mapa_u32(smem_u32(&ssq[it & 1][rank]), threadIdx.x), ss);
+  cluster_wait();
+  if (threadIdx.x < cs) st_dsmem_f32(mapa_u32(smem_u32(&ssq[rank]), threadIdx.x), ss);
   cluster_sync_all();  // phase 2: all block sums delivered
   ss = 0.f;
-  for (int q = 0; q < cs; ++q) ss += ssq[it & 1][q];  // same order in every CTA of the cluster
+  for (int q = 0; q < cs; ++q) ss += ssq[q];  // same order in every CTA of the cluster
   const float r = 1.0f / sqrtf(ss / (float)d + eps);
   if (rs_out && rank == 0 && threadIdx.x == 0) rs_out[m] = r;
   const float rs = rs_out ? 1.0f : r;
@@ -118,8 +112,6 @@ __global__ void __launch_bounds__(kNormThreads) resid_norm_kernel(PartialView pv
     store_act4(h, hp, m, d, i, a.x * rs * __low2float(g01), a.y * rs * __high2float(g01),
                a.z * rs * __low2float(g23), a.w * rs * __high2float(g23));
   }
-  }
-  if (it == 0) cluster_wait();  // no rows: complete the start barrier phase
   if (threadIdx.x == 0) SM_GT_END(1);
 }
 cudaError_t resid_norm_launch(const PartialView *pv, float *x, const bf16 *g, bf16 *h, int M, int d, float eps,
@@ -128,9 +120,8 @@ cudaError_t resid_norm_launch(const PartialView *pv, float *x, const bf16 *g, bf
   if (cs > 8 || d % 4) return cudaErrorInvalidValue;
   PartialView v{};
   if (pv) v = *pv;
-  const int rows_par = std::min(M, std::max(1, g_consumer_ctas / cs));
-  return launch_pdl_cluster(resid_norm_kernel, dim3(cs, rows_par), dim3(kNormThreads), 0, st, cs, v, pv ? 1 : 0, x, g,
-                            h, M, d, eps, hp, rs_out);
+  return launch_pdl_cluster(resid_norm_kernel, dim3(cs, M), dim3(kNormThreads), 0, st, cs, v, pv ? 1 : 0, x, g, h, d,
+                            eps, hp, rs_out);
 }
 
 // Tensor-parallel variant (a7): the residual all-reduce fused in.  Each rank reduces
@@ -239,12 +230,9 @@ __global__ void __launch_bounds__(256) qkv_consumer_kernel(PartialView pv, RowCt
   SM_GT_WAITED();
   const int half = hd / 2;
   const int quads = half / 4;
-  const int bpr = ((H + 2 * Hkv) * quads + blockDim.x - 1) / blockDim.x;  // blocks per token row
-  // persistent: ~one CTA per SM, all resident (and waiting) before the GEMM completes
-  for (int item = blockIdx.x; item < rc.M * bpr; item += gridDim.x) {
-  const int m = item / bpr;
-  const int idx = (item % bpr) * blockDim.x + threadIdx.x;
-  if (idx >= (H + 2 * Hkv) * quads) continue;
+  const int m = blockIdx.y;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (H + 2 * Hkv) * quads) return;
   const int hh = idx / quads, c = (idx % quads) * 4;
   const int n0 = hh * hd + c;
   float4 a, b;
@@ -295,18 +283,17 @@ __global__ void __launch_bounds__(256) qkv_consumer_kernel(PartialView pv, RowCt
     *reinterpret_cast<uint2 *>(dst + c) = lo;
     *reinterpret_cast<uint2 *>(dst + c + half) = hi;
   }
-  }
   if (threadIdx.x == 0) SM_GT_END(2);
 }
 cudaError_t qkv_consumer_launch(const PartialView &pv, RowCtx rc, int H, int Hkv, int hd, const float2 *rope, void *q,
                                 void *kcache, void *vcache, int cap, const float *rs, cudaStream_t st) {
   const int work = (H + 2 * Hkv) * (hd / 8);
-  const int items = (work + 255) / 256 * rc.M;
-  const dim3 grid(std::min(items, g_consumer_ctas));
+  const int nt = g_consumer_threads;
+  const dim3 grid((work + nt - 1) / nt, rc.M);
   if (pv.planes > 1)
-    return launch_pdl(qkv_consumer_kernel<true>, grid, dim3(256), 0, st, pv, rc, H, Hkv, hd, rope, q, kcache, vcache,
+    return launch_pdl(qkv_consumer_kernel<true>, grid, dim3(nt), 0, st, pv, rc, H, Hkv, hd, rope, q, kcache, vcache,
                       cap, rs);
-  return launch_pdl(qkv_consumer_kernel<false>, grid, dim3(256), 0, st, pv, rc, H, Hkv, hd, rope, q, kcache, vcache,
+  return launch_pdl(qkv_consumer_kernel<false>, grid, dim3(nt), 0, st, pv, rc, H, Hkv, hd, rope, q, kcache, vcache,
                     cap, rs);
 }
 
@@ -317,11 +304,9 @@ __global__ void __launch_bounds__(256) silu_consumer_kernel(PartialView pv, int 
   pdl_trigger();
   pdl_wait();
   SM_GT_WAITED();
-  const int bpr = (F / 4 + blockDim.x - 1) / blockDim.x;  // blocks per token row
-  for (int item = blockIdx.x; item < pv.M * bpr; item += gridDim.x) {  // persistent (see qkv_consumer)
-  const int m = item / bpr;
-  const int f = ((item % bpr) * blockDim.x + threadIdx.x) * 4;
-  if (f >= F) continue;
+  const int m = blockIdx.y;
+  const int f = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (f >= F) return;
   const int ng = (f >> 6) * 128 + (f & 63);
   float4 g, u;
   if (pv.planes > 1) {
@@ -341,12 +326,11 @@ __global__ void __launch_bounds__(256) silu_consumer_kernel(PartialView pv, int 
 #pragma unroll
   for (int e = 0; e < 4; ++e) o[e] = gg[e] / (1.0f + expf(-gg[e])) * uu[e];
   store_act4(act, pv.planes, m, F, f, o[0], o[1], o[2], o[3]);
-  }
   if (threadIdx.x == 0) SM_GT_END(3);
 }
 cudaError_t silu_consumer_launch(const PartialView &pv, int F, bf16 *act, const float *rs, cudaStream_t st) {
-  const int items = (F / 4 + 255) / 256 * pv.M;
-  return launch_pdl(silu_consumer_kernel, dim3(std::min(items, g_consumer_ctas)), dim3(256), 0, st, pv, F, act, rs);
+  const int nt = g_consumer_threads;
+  return launch_pdl(silu_consumer_kernel, dim3((F / 4 + nt - 1) / nt, pv.M), dim3(nt), 0, st, pv, F, act, rs);
 }
 
 // ------------------------------------------------------------------ logits: argmax + typical stats

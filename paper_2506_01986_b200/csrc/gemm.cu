@@ -234,7 +234,8 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
             tma_load_2d(sB + s * C::kB + r * 2048, &a.tmX[bi], &full[s], kc, a.x_row0 + tt * BN + r * 16);
         }
       };
-      const int pre = (u1 - u0) < (long long)C::kStages ? (int)(u1 - u0) : C::kStages;
+      int pre = (u1 - u0) < (long long)C::kStages ? (int)(u1 - u0) : C::kStages;
+      if (a.pre_stages >= 0 && a.pre_stages < pre) pre = a.pre_stages;
       for (int i = 0; i < pre; ++i) {  // weights first: independent of the previous kernel
         const long long u = u0 + i;
         int bi, tt, mt;
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
       for (long long u = u0 + pre; u < u1; ++u) {
         const int i = (int)(u - u0);
         const int s = i % C::kStages;
-        mbar_wait(&empty[s], ((i / C::kStages) - 1) & 1);
+        if (i >= C::kStages) mbar_wait(&empty[s], ((i / C::kStages) - 1) & 1);
         int bi, tt, mt;
         sk_decode(sk_tile(u, pl), pl, bi, tt, mt);
         const int kc = sk_kb(u, pl) * 64;
@@ -369,9 +370,11 @@ static bool g_pdl = true;
 static int g_ctas = 0;
 static int g_l2pf = 0;
 static int g_dbg_mode = 0;
-static int g_force_bn = 0;  // experiments: fixed token-tile width (0 = gemm_pick_bn)
+static int g_force_bn = 0;
+static int g_pre_stages = -1;  // experiments: weight stages issued before griddepcontrol.wait (-1 = ring)  // experiments: fixed token-tile width (0 = gemm_pick_bn)
 static int g_occ = 2;  // GEMM CTAs per SM for BN <= 64 (1..4); grid = 148 * occ
 void gemm_set_bn(int bn) { g_force_bn = bn; }
+void gemm_set_pre_stages(int n) { g_pre_stages = n; }
 void gemm_set_small(int v) { g_occ = v < 1 ? 1 : (v > 4 ? 4 : v); }
 int gemm_occ_for(int bn) { return bn <= 64 ? g_occ : 1; }
 void gemm_set_debug_mode(int m) { g_dbg_mode = m; }
@@ -446,6 +449,7 @@ size_t gemm_ws_floats(const GemmArgs &a) { return (size_t)a.plan.tiles * a.plan.
 cudaError_t gemm_launch(const GemmArgs &a0, cudaStream_t st) {
   GemmArgs a = a0;
   a.l2_prefetch = g_pdl ? g_l2pf : 0;
+  a.pre_stages = g_pre_stages;
   a.dbg_mode = g_dbg_mode;
   switch (a.plan.bn) {
     case 16: return g_occ == 4 ? launch_bn<16, 50>(a, st) : g_occ == 3 ? launch_bn<16, 68>(a, st)

@@ -250,6 +250,7 @@ struct GemmArgs {
   int x_row0;                      // first activation row (TMA row offset)
   int l2_prefetch;                 // weight k-blocks per CTA prefetched into L2 before the PDL wait
   int dbg_mode;                    // experiments: 1 = stream weights only (no X, no MMA)
+  int pre_stages;                  // weight stages issued before griddepcontrol.wait (-1 = the ring)
   SplitPlan plan;
   float *ws;                       // partial slots, gemm_ws_floats() floats
   int epi;                         // kEpi*: fused tile epilogue (batch 1 only)
@@ -265,7 +266,8 @@ void gemm_set_ctas(int n);
 void gemm_set_l2_prefetch(int kblocks);
 void gemm_set_debug_mode(int m);
 void gemm_set_small(int v);
-void gemm_set_bn(int bn);  // experiments: force the token-tile width (16..256 supported set; 0 = auto)
+void gemm_set_bn(int bn);
+void gemm_set_pre_stages(int n);  // experiments: force the token-tile width (16..256 supported set; 0 = auto)
 
 // ---------------------------------------------------------------- K1 tree attention
 struct AttnArgs {
@@ -323,7 +325,7 @@ cudaError_t heads_r_consumer_launch(const PartialView &pv, int nmed, int nb, int
 // top-k of the U-head logits y_i[b][:]: idx[b][i][k], (value desc, index asc)    (K3)
 cudaError_t topk_consumer_launch(const PartialView &pv, int nmed, int nb, int V, int k, int32_t *idx, int idx_offset,
                                  float *vals, cudaStream_t st);
-void consumer_set_ctas(int n);  // experiments: cap the consumer grids (persistent), 0 = uncapped
+void consumer_set_threads(int n);  // experiments: qkv / SiLU consumer block size  // experiments: cap the consumer grids (persistent), 0 = uncapped
 // stage API: top-k of plain fp32 rows
 cudaError_t topk_launch(const float *logits, int rows, int V, int k, int32_t *idx, cudaStream_t st);
 // stage API: out[m][n] = y[m][n]

@@ -225,6 +225,149 @@ extern "C" sm_status sm_tree_create_chain(int n, sm_tree **out) {
   return SM_OK;
 }
 
+// ---------------------------------------------------------------- tree construction (f1)
+static sm_status tree_from_paths(std::vector<std::vector<int>> ps, int topk, sm_tree **out) {
+  if ((int)ps.size() + 1 > kMaxTreeNodes) return fail(SM_ERR_INVALID_ARG, "tree construction: more than 256 nodes");
+  std::sort(ps.begin(), ps.end(), [](const std::vector<int> &a, const std::vector<int> &b) {
+    return a.size() != b.size() ? a.size() < b.size() : a < b;
+  });
+  sm_tree *t = new sm_tree();
+  t->topk = topk;
+  t->paths.push_back({});
+  for (auto &p : ps) t->paths.push_back(p);
+  tree_finish(t);
+  *out = t;
+  return SM_OK;
+}
+
+extern "C" sm_status sm_tree_create_full(int k, int l, sm_tree **out) {
+  if (!out || k < 1 || l < 0) return fail(SM_ERR_INVALID_ARG, "sm_tree_create_full: k >= 1, l >= 0");
+  double n = 0;
+  for (int i = 1; i <= l; ++i) n += std::pow((double)k, i);
+  if (n + 1 > kMaxTreeNodes) return fail(SM_ERR_INVALID_ARG, "sm_tree_create_full: more than 256 nodes");
+  std::vector<std::vector<int>> ps, level{{}};
+  for (int i = 0; i < l; ++i) {
+    std::vector<std::vector<int>> next;
+    for (auto &p : level)
+      for (int r = 0; r < k; ++r) {
+        auto q = p;
+        q.push_back(r);
+        next.push_back(q);
+      }
+    level = next;
+    ps.insert(ps.end(), level.begin(), level.end());
+  }
+  return tree_from_paths(ps, k, out);
+}
+
+extern "C" sm_status sm_tree_prune(const sm_tree *t, int target_nodes, sm_tree **out) {
+  if (!t || !out) return fail(SM_ERR_INVALID_ARG, "sm_tree_prune: null");
+  if (target_nodes < 1 || target_nodes > t->N) return fail(SM_ERR_INFEASIBLE_TREE, "sm_tree_prune: target outside [1, N]");
+  // R4 (Medusa's right-to-left pruning): drop the leaf with the lexicographically
+  // largest rank path (the rightmost leaf in DFS order) until target_nodes remain.
+  std::vector<std::vector<int>> cur(t->paths.begin() + 1, t->paths.end());
+  while ((int)cur.size() + 1 > target_nodes) {
+    int best = -1;
+    for (int i = 0; i < (int)cur.size(); ++i) {
+      bool leaf = true;
+      for (const auto &q : cur)
+        if (q.size() == cur[i].size() + 1 && std::equal(cur[i].begin(), cur[i].end(), q.begin())) {
+          leaf = false;
+          break;
+        }
+      if (leaf && (best < 0 || cur[i] > cur[best])) best = i;
+    }
+    cur.erase(cur.begin() + best);
+  }
+  return tree_from_paths(cur, t->topk, out);
+}
+
+extern "C" sm_status sm_tree_create_pruned_full(int k, int l, float r_min, float r_max, float mid, float steep,
+                                                sm_tree **out) {
+  if (!out || k < 1 || l < 1) return fail(SM_ERR_INVALID_ARG, "sm_tree_create_pruned_full: k >= 1, l >= 1");
+  // scaled logistic rate r(i) = r_min + (r_max - r_min) / (1 + exp(-steep (i - mid))) (fig:prunefunc);
+  // level 1 keeps all k nodes; level i keeps the first ceil((1 - r(i)) k^i) of its
+  // full-tree nodes, left to right, whose parent was kept.
+  std::vector<std::vector<int>> ps, prev;
+  for (int r = 0; r < k; ++r) prev.push_back({r});
+  ps = prev;
+  for (int i = 2; i <= l && !prev.empty(); ++i) {
+    const double rate = (double)r_min + ((double)r_max - (double)r_min) / (1.0 + std::exp(-(double)steep * (i - (double)mid)));
+    const double want = std::ceil((1.0 - rate) * std::pow((double)k, i) - 1e-9);
+    std::vector<std::vector<int>> level;
+    for (auto &p : prev)
+      for (int r = 0; r < k && (double)level.size() < want; ++r) {
+        auto q = p;
+        q.push_back(r);
+        level.push_back(q);
+      }
+    if (ps.size() + level.size() + 1 > (size_t)kMaxTreeNodes)
+      return fail(SM_ERR_INVALID_ARG, "sm_tree_create_pruned_full: more than 256 nodes");
+    ps.insert(ps.end(), level.begin(), level.end());
+    prev = level;
+  }
+  return tree_from_paths(ps, k, out);
+}
+
+extern "C" sm_status sm_tree_create_custom(int n_nodes, int n_leaves, int k, int l, sm_tree **out) {
+  // Exact (N, S) features, reading Q30: level 1 = min(k, N-1, S) nodes; then
+  // "deepening" additions (child of the first DFS leaf above depth l; leaves unchanged),
+  // taking a "widening" step (next-rank child of the first BFS node with 1..k-1 children;
+  // one more leaf) only when every leaf is at depth l; then the remaining widenings.
+  if (!out || k < 1 || l < 0) return fail(SM_ERR_INVALID_ARG, "sm_tree_create_custom: bad arguments");
+  const int N = n_nodes, S = n_leaves;
+  if (N < 1 || S < 1 || (N == 1 && S != 1) || (N > 1 && S > N - 1))
+    return fail(SM_ERR_INFEASIBLE_TREE, "sm_tree_create_custom: need 1 <= S <= N - 1 (or N = S = 1)");
+  if (N > kMaxTreeNodes) return fail(SM_ERR_INVALID_ARG, "sm_tree_create_custom: more than 256 nodes");
+  if (N == 1) return tree_from_paths({}, k, out);
+  if (l < 1) return fail(SM_ERR_INFEASIBLE_TREE, "sm_tree_create_custom: N > 1 needs l >= 1");
+  const int c1 = std::min({k, N - 1, S});
+  std::vector<std::vector<int>> ps;
+  std::map<std::vector<int>, int> nchild;
+  for (int r = 0; r < c1; ++r) ps.push_back({r});
+  nchild[{}] = c1;
+  int widen = S - c1, deepen = (N - 1 - c1) - widen;
+  if (widen < 0 || deepen < 0) return fail(SM_ERR_INFEASIBLE_TREE, "sm_tree_create_custom: too many leaves");
+  auto widen_one = [&]() -> bool {
+    std::vector<std::vector<int>> cand;
+    if (nchild[{}] > 0 && nchild[{}] < k) cand.push_back({});
+    for (auto &p : ps) {
+      const int c = nchild.count(p) ? nchild[p] : 0;
+      if (c > 0 && c < k) cand.push_back(p);
+    }
+    if (cand.empty()) return false;
+    auto it = std::min_element(cand.begin(), cand.end(), [](const std::vector<int> &a, const std::vector<int> &b) {
+      return a.size() != b.size() ? a.size() < b.size() : a < b;
+    });
+    auto q = *it;
+    const int r = nchild[q];
+    nchild[q] = r + 1;
+    q.push_back(r);
+    ps.push_back(q);
+    return true;
+  };
+  while (deepen > 0) {
+    const std::vector<int> *pick = nullptr;
+    for (auto &p : ps)  // first leaf in DFS (lexicographic) order above depth l
+      if ((int)p.size() < l && !(nchild.count(p) && nchild[p] > 0) && (!pick || p < *pick)) pick = &p;
+    if (pick) {
+      auto q = *pick;
+      nchild[q] = 1;
+      q.push_back(0);
+      ps.push_back(q);
+      --deepen;
+    } else if (widen > 0) {
+      if (!widen_one()) return fail(SM_ERR_INFEASIBLE_TREE, "sm_tree_create_custom: no node to widen");
+      --widen;
+    } else {
+      return fail(SM_ERR_INFEASIBLE_TREE, "sm_tree_create_custom: no leaf above depth l to deepen");
+    }
+  }
+  for (; widen > 0; --widen)
+    if (!widen_one()) return fail(SM_ERR_INFEASIBLE_TREE, "sm_tree_create_custom: no node to widen");
+  return tree_from_paths(ps, k, out);
+}
+
 extern "C" sm_status sm_tree_query(const sm_tree *t, int *N, int *S, int *depth, int32_t *parent, int32_t *node_depth,
                                    int32_t *rank, uint64_t *anc_bits, int32_t *leaf_paths) {
   if (!t) return fail(SM_ERR_INVALID_ARG, "sm_tree_query: null tree");
@@ -1344,8 +1487,10 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
     gemm_set_debug_mode(value);
   } else if (n == "fused_epilogue") {  // takes effect for models created afterwards
     g_fused = value & 7;
-  } else if (n == "consumer_ctas") {
-    consumer_set_ctas(value);
+  } else if (n == "gemm_pre") {
+    gemm_set_pre_stages(value);
+  } else if (n == "consumer_threads") {
+    consumer_set_threads(value);
   } else if (n == "epi_test") {
     g_epi_test = value;
   } else if (n == "ablate") {

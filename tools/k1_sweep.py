@@ -16,7 +16,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2506_01986_b200 as sm  # noqa: E402
 import synth  # noqa: E402
 
-PEAK = 6549.1
+import json  # noqa: E402
+
+_pk = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))
+PEAK = _pk["hbm_gbs"]                   # GB/s
+TPEAK = _pk["bf16_tflops"]              # dense bf16 TF/s (burst: one kernel timed alone)
 ap = argparse.ArgumentParser()
 ap.add_argument("--quick", action="store_true")
 ap.add_argument("--tc", type=int, default=1)
@@ -29,7 +33,10 @@ Lcs = [512, 4096, 32768]
 bs = [1, 8, 32]
 if a.quick:
     Ns, Lcs, bs = [64], [512, 4096], [1, 8]
-print(f"{'geom':8s} {'b':>3s} {'N':>4s} {'Lc':>6s} {'MB':>8s} {'us':>9s} {'GB/s':>8s} {'frac':>6s}")
+print(f"{'geom':8s} {'b':>3s} {'N':>4s} {'Lc':>6s} {'MB':>8s} {'us':>9s} {'GB/s':>8s} {'TF/s':>7s} {'bound':>6s} "
+      f"{'frac':>6s}")
+# flops = 4 H hd sum_b (N Lc + sum_n (depth_n + 1)) (tree part counted sparse);
+# bound = whichever of bytes / HBM peak and flops / tensor peak is larger; frac = that floor / time
 hd = 128
 for gname, H, Hkv in geoms:
     for b in bs:
@@ -69,8 +76,13 @@ for gname, H, Hkv in geoms:
                 torch.cuda.synchronize()
                 us = e0.elapsed_time(e1) * 1e3 / 60
                 alg = b * Hkv * (Lc + tree.N) * hd * 2 * 2 + 2 * b * tree.N * H * hd * 2
+                dep = tree.query()["node_depth"]
+                flops = 4 * H * hd * b * (tree.N * Lc + int((dep + 1).sum()))
                 gbs = alg / us / 1e3
-                print(f"{gname:8s} {b:3d} {tree.N:4d} {Lc:6d} {alg / 1e6:8.1f} {us:9.1f} {gbs:8.1f} {gbs / PEAK:6.3f}",
-                      flush=True)
+                tfs = flops / us / 1e6
+                t_hbm, t_tc = alg / PEAK / 1e3, flops / TPEAK / 1e6  # us
+                bound = "hbm" if t_hbm >= t_tc else "tensor"
+                print(f"{gname:8s} {b:3d} {tree.N:4d} {Lc:6d} {alg / 1e6:8.1f} {us:9.1f} {gbs:8.1f} {tfs:7.1f} {bound:>6s} "
+                      f"{max(t_hbm, t_tc) / us:6.3f}", flush=True)
                 del sets, g
                 torch.cuda.empty_cache()
