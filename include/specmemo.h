@@ -174,6 +174,44 @@ sm_status sm_generate_bf16(void *d_dst, size_t numel, uint64_t seed, uint64_t st
 sm_status sm_generate_bf16_2d(void *d_dst, int rows, int cols, int full_cols, int row0, int col0, uint64_t seed,
                               uint64_t stream_id, int mode, void *stream);
 
+/* ------------------------------------------------------------------ memory-budget planner (f2)
+ * SpecMemo's OptimizerEngine (Algorithm 1) over the memory model of §3.1:
+ *   Eq. 1 KV = 2 h b k d x p, x = n m (d restored, Q14)      Eq. 4 heads = 0.6 GB * l
+ *   Eq. 3 buffers = (b N w + b S l w + b S l l w) p          Eq. 5 base = B p
+ *   Eq. 6 total = base + heads + KV + buffers
+ * accounting = SM_ACCT_B200 binds it to this library instead: KV = sm_kv_bytes (x + N
+ * scratch slots), heads = l (d^2 + d + V d) p, buffers = only the fp32 node logits b N V 4
+ * (the S-indexed gathers of Eq. 3 terms 2-3 do not exist on this path).
+ * Algorithm (readings Q31): default config (default_heads, base tree) if it fits;
+ * else the largest fitting candidate of ExploreTree for the current head count -- the base
+ * tree cut to depth = heads and R4-pruned to 64/44/31/27/16/5 nodes, plus the custom
+ * (64, 56) and (44, 37) trees of tab:treefeatures at 4 heads; else the largest head count
+ * in [2, heads-1] whose default config fits, and explore again; else NEEDS_QUANTIZATION
+ * (QuantizeBaseModel, is not part of this build).  Host only unless max_memory = 0
+ * (then cudaMemGetInfo's free bytes of the current device are the budget).            */
+typedef struct sm_plan_in {
+  sm_model_cfg cfg;          /* shapes; cfg.n_medusa is ignored                          */
+  int batch, n_queries, max_tokens;  /* b, n, m                                           */
+  int default_heads;         /* Alg. 1 default_heads (4)                                  */
+  int prec_bytes;            /* p: 2 (bf16)                                               */
+  int accounting;            /* SM_ACCT_PAPER (0) or SM_ACCT_B200 (1)                     */
+  size_t max_memory;         /* bytes; 0 = free device memory                             */
+  const struct sm_tree *base_tree;   /* default tree (the (64, 42) Medusa tree)           */
+} sm_plan_in;
+typedef struct sm_plan_out {
+  int status;                /* SM_PLAN_DEFAULT 0, _PRUNED 1, _FEWER_HEADS 2, _NEEDS_QUANTIZATION 3 */
+  int heads, N, S;
+  int kind;                  /* 0 default tree, 1 R4-pruned base tree, 2 custom (N, S) tree */
+  long long x;               /* KV bound in committed tokens per sequence = n m           */
+  size_t max_memory, base, heads_bytes, kv, buffers, total;  /* of the returned config   */
+} sm_plan_out;
+#define SM_ACCT_PAPER 0
+#define SM_ACCT_B200 1
+sm_status sm_plan(const sm_plan_in *in, sm_plan_out *out);
+/* Bytes sm_model_create allocates as workspace for cfg (activations, fp32 logits,
+ * stream-K partial slots, tables), excluding weights and KV.                          */
+sm_status sm_workspace_bytes(const sm_model_cfg *cfg, size_t *bytes);
+
 /* ------------------------------------------------------------------ bounded KV cache
  * Eq. 1 with d restored (reading Q14): bytes =
  *   2 * layers * batch * kv_heads/tp * head_dim * (max_seq_len + tree_nodes) * w,

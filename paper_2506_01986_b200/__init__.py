@@ -363,6 +363,46 @@ class Model:
             _lib.sm_model_destroy(self._h)
 
 
+class PlanIn(ctypes.Structure):
+    _fields_ = [("cfg", ModelCfg)] + [(n, ctypes.c_int) for n in ("batch", "n_queries", "max_tokens", "default_heads",
+                                                                "prec_bytes", "accounting")] + \
+               [("max_memory", ctypes.c_size_t), ("base_tree", ctypes.c_void_p)]
+
+
+class PlanOut(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in ("status", "heads", "N", "S", "kind")] + [("x", ctypes.c_longlong)] + \
+               [(n, ctypes.c_size_t) for n in ("max_memory", "base", "heads_bytes", "kv", "buffers", "total")]
+
+
+PLAN_STATUS = {0: "default", 1: "pruned", 2: "fewer_heads", 3: "needs_quantization"}
+PLAN_KIND = {0: "default", 1: "pruned", 2: "custom"}
+
+
+def plan(cfg: dict, base_tree: "Tree", batch: int, n_queries: int, max_tokens: int, max_memory: int = 0,
+         default_heads: int = 4, accounting: str = "b200", prec_bytes: int = 2) -> dict:
+    """SpecMemo memory-budget planner (Algorithm 1 over Eqs. 1, 3-6; include/specmemo.h sm_plan).
+    max_memory = 0: the current device's free memory is the budget."""
+    c = ModelCfg(cfg["n_layers"], cfg["d_model"], cfg["n_heads"], cfg["n_kv_heads"], cfg["head_dim"], cfg["d_ffn"],
+                 cfg["vocab"], 0, cfg.get("rms_eps", 1e-5), cfg.get("rope_theta", 1e4), 1, 1, 1, 0)
+    pin = PlanIn(c, batch, n_queries, max_tokens, default_heads, prec_bytes, {"paper": 0, "b200": 1}[accounting],
+                 max_memory, base_tree._h)
+    out = PlanOut()
+    _check(lib().sm_plan(ctypes.byref(pin), ctypes.byref(out)))
+    return dict(status=PLAN_STATUS[out.status], heads=out.heads, N=out.N, S=out.S, kind=PLAN_KIND[out.kind], x=out.x,
+                max_memory=out.max_memory, base=out.base, heads_bytes=out.heads_bytes, kv=out.kv,
+                buffers=out.buffers, total=out.total)
+
+
+def workspace_bytes(cfg: dict, max_rows: int, max_batch: int, max_seq_len: int, n_medusa: int,
+                    dtype: str = "bf16") -> int:
+    c = ModelCfg(cfg["n_layers"], cfg["d_model"], cfg["n_heads"], cfg["n_kv_heads"], cfg["head_dim"], cfg["d_ffn"],
+                 cfg["vocab"], n_medusa, cfg.get("rms_eps", 1e-5), cfg.get("rope_theta", 1e4), max_rows, max_batch,
+                 max_seq_len, DTYPES[dtype])
+    n = ctypes.c_size_t()
+    _check(lib().sm_workspace_bytes(ctypes.byref(c), ctypes.byref(n)))
+    return n.value
+
+
 def kv_bytes(cfg: dict, batch: int, max_seq_len: int, tree_nodes: int, tp_size: int = 1, dtype: str = "bf16") -> int:
     c = ModelCfg(cfg["n_layers"], cfg["d_model"], cfg["n_heads"], cfg["n_kv_heads"], cfg["head_dim"], cfg["d_ffn"],
                  cfg["vocab"], 0, 1e-5, 1e4, 1, 1, 1, DTYPES[dtype])

@@ -816,6 +816,151 @@ extern "C" sm_status sm_ipc_close(void *d_ptr) {
   return SM_OK;
 }
 
+// ---------------------------------------------------------------- memory-budget planner (f2)
+// Algorithm 1 over Eqs. 1, 3-6; see include/specmemo.h and
+// DESIGN.md reading Q31.  Integer arithmetic throughout (sizes in bytes).
+namespace {
+struct PlanCand {
+  int N, S, kind;  // kind 0 default, 1 R4-pruned base tree, 2 custom
+};
+struct PlanCtx {
+  const sm_plan_in *in;
+  size_t mem_base(int p) const {
+    const sm_model_cfg &c = in->cfg;
+    const long long layer = (long long)(c.n_heads + 2 * c.n_kv_heads) * c.head_dim * c.d_model +
+                            (long long)c.d_model * c.n_heads * c.head_dim + 3LL * c.d_ffn * c.d_model + 2LL * c.d_model;
+    return (size_t)((c.n_layers * layer + 2LL * c.vocab * c.d_model + c.d_model) * p);  // Eq. 5
+  }
+  size_t mem_heads(int l, int p) const {  // Eq. 4 (paper) or the real Medusa-1 heads (b200)
+    if (in->accounting == SM_ACCT_B200) {
+      const long long d = in->cfg.d_model, V = in->cfg.vocab;
+      return (size_t)(l * (d * d + d + V * d) * p);
+    }
+    return (size_t)(0.6e9 * l);
+  }
+  size_t mem_kv(int N, int p) const {  // Eq. 1 with d (+ N scratch slots, b200)
+    const sm_model_cfg &c = in->cfg;
+    const long long x = (long long)in->n_queries * in->max_tokens + (in->accounting == SM_ACCT_B200 ? N : 0);
+    return (size_t)(2LL * c.n_layers * in->batch * c.n_kv_heads * c.head_dim * x * p);
+  }
+  size_t mem_buffers(int N, int S, int l, int p) const {  // Eq. 3 (paper) or fp32 node logits (b200)
+    const long long b = in->batch, w = in->cfg.vocab;
+    if (in->accounting == SM_ACCT_B200) return (size_t)(b * N * w * 4);
+    return (size_t)((b * N * w + b * S * l * w + b * S * (long long)l * l * w) * p);
+  }
+  size_t total(int heads, int N, int S) const {  // Eq. 6
+    const int p = in->prec_bytes;
+    return mem_base(p) + mem_heads(heads, p) + mem_kv(N, p) + mem_buffers(N, S, heads, p);
+  }
+};
+}  // namespace
+
+extern "C" sm_status sm_workspace_bytes(const sm_model_cfg *cfg, size_t *bytes);
+
+extern "C" sm_status sm_plan(const sm_plan_in *in, sm_plan_out *out) {
+  if (!in || !out || !in->base_tree || in->batch < 1 || in->n_queries < 1 || in->max_tokens < 1 ||
+      in->default_heads < 2 || in->prec_bytes < 1 || (in->accounting != SM_ACCT_PAPER && in->accounting != SM_ACCT_B200))
+    return fail(SM_ERR_INVALID_ARG, "sm_plan: bad arguments");
+  std::memset(out, 0, sizeof(*out));
+  size_t budget = in->max_memory;
+  if (budget == 0) {  // bound to the device: its free memory now
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    budget = fr;
+  }
+  PlanCtx P{in};
+  const int p = in->prec_bytes;
+  const sm_tree *bt = in->base_tree;
+  const int N0 = bt->N, S0 = bt->S;
+  out->max_memory = budget;
+  out->x = (long long)in->n_queries * in->max_tokens;  // ComputeMinCache
+  auto fill = [&](int status, int heads, const PlanCand &c) {
+    out->status = status;
+    out->heads = heads;
+    out->N = c.N;
+    out->S = c.S;
+    out->kind = c.kind;
+    out->base = P.mem_base(p);
+    out->heads_bytes = P.mem_heads(heads, p);
+    out->kv = P.mem_kv(c.N, p);
+    out->buffers = P.mem_buffers(c.N, c.S, heads, p);
+    out->total = P.total(heads, c.N, c.S);
+  };
+  int heads = in->default_heads;
+  if (P.total(heads, N0, S0) <= budget) {  // AvailMemory(default config)
+    fill(0, heads, PlanCand{N0, S0, 0});
+    return SM_OK;
+  }
+  int status = 1;
+  for (;;) {
+    // ExploreTree: base tree cut to depth `heads`, R4-pruned to the mask sizes; custom trees at 4 heads
+    std::vector<PlanCand> cands;
+    std::vector<std::vector<int>> cut;
+    for (size_t i = 1; i < bt->paths.size(); ++i)
+      if ((int)bt->paths[i].size() <= heads) cut.push_back(bt->paths[i]);
+    sm_tree *ct = nullptr;
+    CKS(tree_from_paths(cut, bt->topk, &ct));
+    for (int n : {64, 44, 31, 27, 16, 5}) {
+      if (n > ct->N) continue;
+      sm_tree *pt = nullptr;
+      if (sm_tree_prune(ct, n, &pt) != SM_OK) continue;
+      cands.push_back(PlanCand{pt->N, pt->S, 1});
+      sm_tree_destroy(pt);
+    }
+    sm_tree_destroy(ct);
+    if (heads == 4) {  // tab:treefeatures, C row, heads = 4
+      cands.push_back(PlanCand{64, 56, 2});
+      cands.push_back(PlanCand{44, 37, 2});
+    }
+    std::sort(cands.begin(), cands.end(), [](const PlanCand &a, const PlanCand &b) {
+      return a.N != b.N ? a.N > b.N : (a.S != b.S ? a.S > b.S : a.kind > b.kind);
+    });
+    for (const auto &c : cands)
+      if (P.total(heads, c.N, c.S) <= budget) {
+        fill(status, heads, c);
+        return SM_OK;
+      }
+    int nh = heads;
+    for (int h = heads - 1; h >= 2; --h)
+      if (P.total(h, N0, S0) <= budget) {
+        nh = h;
+        break;
+      }
+    if (nh == heads) {  // QuantizeBaseModel: not in this build
+      out->status = 3;
+      out->heads = heads;
+      return SM_OK;
+    }
+    heads = nh;
+    status = 2;
+  }
+}
+
+extern "C" sm_status sm_workspace_bytes(const sm_model_cfg *cfg, size_t *bytes) {
+  if (!cfg || !bytes) return fail(SM_ERR_INVALID_ARG, "sm_workspace_bytes: null");
+  const sm_model_cfg &c = *cfg;
+  const size_t R = c.max_rows, B = c.max_batch, d = c.d_model, P = c.dtype == SM_DTYPE_FP32 ? 3 : 1;
+  const size_t Hhd = (size_t)c.n_heads * c.head_dim, nmed = std::max(1, c.n_medusa);
+  size_t b = 0;
+  b += R * d * 4 + R * 4 + R * std::max<size_t>(1, d / 64) * 4 + (size_t)kMaxFusedTiles * 4 + 4;  // x, rs, ss, counters
+  b += R * d * 2 * P + R * Hhd * 2 * (c.dtype == SM_DTYPE_FP32 ? 2 : 1) + R * Hhd * 2 * P;       // h, q, attn
+  b += R * c.d_ffn * 2 * P + R * d * 2 * P + R * c.vocab * 4 + R * 4 + R * 3 * 4;                // act, hf, z, argmax, stats
+  b += B * d * 2 * P + nmed * B * d * 2 * P + (size_t)c.max_seq_len * (c.head_dim / 2) * 8;       // head_in, r_buf, rope
+  b += 2 * R * 4 + 2 * B * nmed * 32 * 4 + 16;                                                      // amax, cand, top-k
+  // stream-K partial slots: the largest need over the model's GEMMs
+  size_t need = 0;
+  const int Rg = (int)(R * P);
+  for (auto nk : {std::make_pair((c.n_heads + 2 * c.n_kv_heads) * c.head_dim, c.d_model),
+                  std::make_pair(c.d_model, c.n_heads * c.head_dim), std::make_pair(2 * c.d_ffn, c.d_model),
+                  std::make_pair(c.d_model, c.d_ffn), std::make_pair(c.vocab, c.d_model)})
+    need = std::max(need, ws_need(gemm_proto(nk.first, nk.second, 1), Rg));
+  if (c.n_medusa > 0)
+    need = std::max({need, ws_need(gemm_proto(c.d_model, c.d_model, c.n_medusa), (int)(B * P)),
+                     ws_need(gemm_proto(c.vocab, c.d_model, c.n_medusa), (int)(B * P))});
+  *bytes = b + need * 4;
+  return SM_OK;
+}
+
 // ---------------------------------------------------------------- bounded KV
 struct GraphKey {
   int prof;
