@@ -277,6 +277,59 @@ SM_DEV void umma_commit(uint64_t *bar) {
 }
 SM_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 SM_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// ---- 2-SM (CTA pair) variants: tcgen05 cta_group::2 (cluster of 2 CTAs on one TPC)
+SM_DEV uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// D[256 x N] (lanes of both CTAs) += A[256 x K] (128 rows from each CTA's smem at the same
+// address) * B[N x K] (N/2 rows from each CTA's smem).  Issued by the leader CTA only.
+SM_DEV void umma_bf16_cg2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// completion of the leader's MMAs arrives on the mbarrier at this offset in every CTA of mask
+SM_DEV void umma_commit_cg2(uint64_t *bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::
+                   "r"(smem_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
+// TMA into this CTA's smem, completion counted on the mbarrier at cluster address mbar_cl
+// (the leader's barrier: both CTAs' bytes complete one transaction count)
+SM_DEV void tma_load_2d_cg2(void *smem_dst, const CUtensorMap *m, uint32_t mbar_cl, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(smem_u32(smem_dst)),
+      "l"((uint64_t)m), "r"(mbar_cl), "r"(c0), "r"(c1)
+      : "memory");
+}
+SM_DEV void tma_load_2d_cg2_hint(void *smem_dst, const CUtensorMap *m, uint32_t mbar_cl, int c0, int c1,
+                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"((uint64_t)m), "r"(mbar_cl), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+SM_DEV void mbar_arrive_cluster(uint32_t mbar_cl) {  // arrive on a (possibly peer) CTA's mbarrier
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(mbar_cl) : "memory");
+}
+template <int NCOLS>
+SM_DEV void tmem_alloc_cg2(uint32_t *smem_dst) {  // one warp of EACH CTA of the pair
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_dst)),
+               "n"(NCOLS));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+template <int NCOLS>
+SM_DEV void tmem_dealloc_cg2(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS));
+}
+
 template <int NCOLS>
 SM_DEV void tmem_alloc(uint32_t *smem_dst) {  // whole warp
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_dst)),

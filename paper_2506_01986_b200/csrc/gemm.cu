@@ -366,14 +366,168 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
   if (threadIdx.x == 0) SM_GT_END(1000 + a.N / 128);
 }
 
+// ------------------------------------------------------------------ 2-SM variant (cta_group::2)
+// The CTA pair of a cluster computes a 256-row weight tile x BN token rows per unit: CTA r
+// loads weight rows [256 t + 128 r, +128) and token rows [BN/2 r, +BN/2) of the stage, the
+// leader (rank 0) issues tcgen05.mma.cta_group::2 (M = 256, N = BN) reading both CTAs'
+// shared memory, and each CTA's TMEM receives its own 128 weight rows x BN tokens.  Per SM
+// the activation bytes per stage halve (BN/2 rows instead of BN), which is what limits the
+// single-SM kernel for BN >= 96: every stage re-reads the activation tile from L2.
+template <int BN, int SMEMKB>
+struct PairCfg {
+  static constexpr int kA = 128 * 64 * 2;
+  static constexpr int kB = (BN / 2) * 64 * 2;
+  static constexpr int kStage = kA + kB;
+  static constexpr int kStages = (SMEMKB * 1024) / kStage;
+  static constexpr int kTmemCols = 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+  static constexpr int kSmem = kStages * kStage + 1024 + 256;
+};
+
+template <int BN, int SMEMKB>
+__global__ void __launch_bounds__(192, 1) gemm_pair_kernel(const __grid_constant__ GemmArgs a) {
+  using C = PairCfg<BN, SMEMKB>;
+  static_assert(BN % 32 == 0 && BN >= 64, "pair tiles: BN >= 64, BN/2 a multiple of 16");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sA = smem;
+  uint8_t *sB = smem + C::kStages * C::kA;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::kStages * C::kStage);
+  uint64_t *empty = full + C::kStages;
+  uint64_t *tfull = empty + C::kStages;  // [2]
+  uint64_t *tempty = tfull + 2;          // [2] (leader's: 128 arrivals from each CTA)
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+  SM_GT_BEGIN();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const SplitPlan &pl = a.plan;
+  const int rank = (int)cluster_ctarank();
+  const int c = blockIdx.x >> 1;  // cluster = work unit owner
+  const long long u0 = sk_unit0(c, pl), u1 = sk_unit0(c + 1, pl);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&a.tmW[0]);
+    tma_prefetch_desc(&a.tmX64[0]);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 256);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_cg2<C::kTmemCols>(tslot);
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs' barriers initialised before any cross-CTA arrive / TMA
+  tc_fence_after();
+  pdl_trigger();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs; completion counted on the leader's barriers)
+      const uint64_t pol_w = pl.token_tiles > 1 ? policy_evict_last() : policy_evict_first();
+      const uint32_t full_cl0 = mapa_u32(smem_u32(&full[0]), 0);
+      auto load_w = [&](int s, long long u) {
+        int bi, tt, mt;
+        sk_decode(sk_tile(u, pl), pl, bi, tt, mt);
+        if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * C::kStage);  // both CTAs' W and X bytes
+        tma_load_2d_cg2_hint(sA + s * C::kA, &a.tmW[0], full_cl0 + 8 * s, sk_kb(u, pl) * 64, (mt * 2 + rank) * 128,
+                             pol_w);
+      };
+      auto load_x = [&](int s, long long u) {
+        int bi, tt, mt;
+        sk_decode(sk_tile(u, pl), pl, bi, tt, mt);
+        tma_load_2d_cg2(sB + s * C::kB, &a.tmX64[0], full_cl0 + 8 * s, sk_kb(u, pl) * 64,
+                        a.x_row0 + tt * BN + rank * (BN / 2));
+      };
+      int pre = (u1 - u0) < (long long)C::kStages ? (int)(u1 - u0) : C::kStages;
+      if (a.pre_stages >= 0 && a.pre_stages < pre) pre = a.pre_stages;
+      for (int i = 0; i < pre; ++i) load_w(i, u0 + i);  // weights: independent of the previous kernel
+      pdl_wait();
+      SM_GT_WAITED();
+      for (int i = 0; i < pre; ++i) load_x(i, u0 + i);
+      for (long long u = u0 + pre; u < u1; ++u) {
+        const int i = (int)(u - u0);
+        const int s = i % C::kStages;
+        if (i >= C::kStages) mbar_wait(&empty[s], ((i / C::kStages) - 1) & 1);
+        load_w(s, u);
+        load_x(s, u);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ---------------- MMA issuer (leader only): M = 256 across the pair
+      constexpr uint32_t idesc = umma_idesc_bf16(256, BN);
+      int seg = 0;
+      bool seg_start = true;
+      for (long long u = u0; u < u1; ++u) {
+        const int i = (int)(u - u0);
+        const int s = i % C::kStages;
+        const int buf = seg & 1;
+        if (seg_start && seg >= 2) mbar_wait(&tempty[buf], ((seg >> 1) - 1) & 1);
+        mbar_wait(&full[s], (i / C::kStages) & 1);
+        tc_fence_after();
+        const uint64_t ad = umma_desc_sw128(smem_u32(sA + s * C::kA));
+        const uint64_t bd = umma_desc_sw128(smem_u32(sB + s * C::kB));
+        const uint32_t td = tmem + buf * BN;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) umma_bf16_cg2(td, ad + 2 * k, bd + 2 * k, idesc, (!seg_start || k > 0) ? 1u : 0u);
+        umma_commit_cg2(&empty[s], 0x3);
+        seg_start = false;
+        if ((u + 1) % pl.kb_total == 0 || u + 1 == u1) {
+          umma_commit_cg2(&tfull[buf], 0x3);
+          ++seg;
+          seg_start = true;
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue warps 2..5 of both CTAs: this CTA's 128 weight rows
+    const int wq = warp & 3;
+    const int lrow = wq * 32 + lane;
+    const uint32_t tempty_cl0 = mapa_u32(smem_u32(&tempty[0]), 0);
+    int seg = 0;
+    long long u = u0;
+    while (u < u1) {
+      const int t = sk_tile(u, pl);
+      const long long seg_end = min(u1, (long long)(t + 1) * pl.kb_total);
+      const int buf = seg & 1;
+      mbar_wait(&tfull[buf], (seg >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem + ((uint32_t)(wq * 32) << 16) + buf * BN;
+      float *dst = sk_partial(a.ws, pl, t, c - sk_cta_of((long long)t * pl.kb_total, pl), rank);
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(tbase + c0, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) dst[(size_t)(c0 + j) * 128 + lrow] = v[j];
+      }
+      tc_fence_before();
+      mbar_arrive_cluster(tempty_cl0 + 8 * buf);
+      u = seg_end;
+      ++seg;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // no cross-CTA arrivals or MMAs remain
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc_cg2<C::kTmemCols>(tmem);
+  if (threadIdx.x == 0) SM_GT_END(2000 + a.N / 128);
+}
+
 static bool g_pdl = true;
 static int g_ctas = 0;
 static int g_l2pf = 0;
 static int g_dbg_mode = 0;
 static int g_force_bn = 0;
+static int g_pair = 0;  // 2-SM MMA (experiments; measured slower): 0 off, 1 for BN >= 96, 2 for BN >= 64
 static int g_pre_stages = -1;  // experiments: weight stages issued before griddepcontrol.wait (-1 = ring)  // experiments: fixed token-tile width (0 = gemm_pick_bn)
 static int g_occ = 2;  // GEMM CTAs per SM for BN <= 64 (1..4); grid = 148 * occ
 void gemm_set_bn(int bn) { g_force_bn = bn; }
+void gemm_set_pair(int mode) { g_pair = mode < 0 ? 0 : (mode > 2 ? 2 : mode); }
 void gemm_set_pre_stages(int n) { g_pre_stages = n; }
 void gemm_set_small(int v) { g_occ = v < 1 ? 1 : (v > 4 ? 4 : v); }
 int gemm_occ_for(int bn) { return bn <= 64 ? g_occ : 1; }
@@ -413,6 +567,33 @@ static cudaError_t launch_bn(const GemmArgs &a, cudaStream_t st) {
 // Token-tile width: the smallest supported UMMA N (multiple of 16) covering M, so one
 // token tile holds every row up to 256 (each weight tile then crosses shared memory
 // once) and padding MMA work stays small (C4: b*N = 10 x 16 = 160 rows -> BN 160).
+template <int BN, int SMEMKB>
+static cudaError_t launch_pair(const GemmArgs &a, cudaStream_t st) {
+  using C = PairCfg<BN, SMEMKB>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_pair_kernel<BN, SMEMKB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::kSmem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * a.plan.P);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = 2;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, gemm_pair_kernel<BN, SMEMKB>, a);
+}
+
 int gemm_pick_bn(int M) {
   if (M <= 16) return 16;
   if (M <= 32) return 32;
@@ -431,12 +612,15 @@ void gemm_plan(GemmArgs &a, int N, int K, int M, int batch) {
   a.batch = batch;
   SplitPlan &p = a.plan;
   p.bn = g_force_bn > 0 ? g_force_bn : gemm_pick_bn(M);
-  p.m_tiles = (N + 127) / 128;
+  p.pair = (!a.no_pair && batch == 1 && ((g_pair == 1 && p.bn >= 96) || (g_pair == 2 && p.bn >= 64))) ? 2 : 1;
+  p.m_tiles = (N + 128 * p.pair - 1) / (128 * p.pair);
   p.token_tiles = (M + p.bn - 1) / p.bn;
   p.tiles = p.m_tiles * p.token_tiles * batch;
   p.kb_total = (K + 63) / 64;
   const long long U = (long long)p.tiles * p.kb_total;
-  const int want = g_ctas > 0 ? g_ctas : kNumSMs * gemm_occ_for(p.bn);
+  int want = g_ctas > 0 ? g_ctas : kNumSMs * gemm_occ_for(p.bn);
+  if (p.pair == 2)  // clusters of 2 CTAs; 2 CTAs per SM while 2 x BN TMEM columns fit twice
+    want = g_ctas > 0 ? g_ctas / 2 : (p.bn <= 128 ? kNumSMs : kNumSMs / 2);
   p.P = (int)(U < want ? U : want);
   p.U = U;
   // contributors per tile <= ceil(KB / floor(U/P)) + 1
@@ -444,13 +628,27 @@ void gemm_plan(GemmArgs &a, int N, int K, int M, int batch) {
   p.maxc = (int)((p.kb_total + per - 1) / per) + 1;
 }
 
-size_t gemm_ws_floats(const GemmArgs &a) { return (size_t)a.plan.tiles * a.plan.maxc * a.plan.bn * 128; }
+size_t gemm_ws_floats(const GemmArgs &a) {
+  return (size_t)a.plan.tiles * sk_pair(a.plan) * a.plan.maxc * a.plan.bn * 128;
+}
 
 cudaError_t gemm_launch(const GemmArgs &a0, cudaStream_t st) {
   GemmArgs a = a0;
   a.l2_prefetch = g_pdl ? g_l2pf : 0;
   a.pre_stages = g_pre_stages;
   a.dbg_mode = g_dbg_mode;
+  if (a.plan.pair == 2) {
+    switch (a.plan.bn) {
+      case 64: return launch_pair<64, 104>(a, st);
+      case 96: return launch_pair<96, 104>(a, st);
+      case 128: return launch_pair<128, 104>(a, st);
+      // BN >= 160 needs 2 x BN > 256 TMEM columns: one CTA per SM (TMEM holds 512 columns)
+      case 160: return launch_pair<160, 216>(a, st);
+      case 192: return launch_pair<192, 216>(a, st);
+      case 256: return launch_pair<256, 216>(a, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (a.plan.bn) {
     case 16: return g_occ == 4 ? launch_bn<16, 50>(a, st) : g_occ == 3 ? launch_bn<16, 68>(a, st)
                     : g_occ == 2 ? launch_bn<16, 104>(a, st) : launch_bn<16, 216>(a, st);
@@ -481,6 +679,13 @@ void gemm_preload() {
   preload_one<64, 50>(), preload_one<64, 68>(), preload_one<64, 104>(), preload_one<64, 216>();
   preload_one<96, 216>(), preload_one<128, 216>(), preload_one<160, 216>(), preload_one<192, 216>();
   preload_one<256, 216>();
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, gemm_pair_kernel<64, 104>);
+  cudaFuncGetAttributes(&fa, gemm_pair_kernel<96, 104>);
+  cudaFuncGetAttributes(&fa, gemm_pair_kernel<128, 104>);
+  cudaFuncGetAttributes(&fa, gemm_pair_kernel<160, 216>);
+  cudaFuncGetAttributes(&fa, gemm_pair_kernel<192, 216>);
+  cudaFuncGetAttributes(&fa, gemm_pair_kernel<256, 216>);
 }
 
 SM_GT_READER(sm_gtrace_read_gemm)

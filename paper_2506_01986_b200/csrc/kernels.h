@@ -26,9 +26,13 @@ struct RowCtx {                // forward rows m = (seq - seq_base) * Nq + n
 // owns [U*c/P, U*(c+1)/P).  Tile t = (bi * m_tiles + mt) * token_tiles + tt
 // covers 128 output features x bn token rows.  Every (tile, contributing CTA)
 // writes an fp32 partial [bn][128] at slot t * maxc + (c - first CTA of t).
+// pair = 2 (2-SM MMA, tcgen05 cta_group::2): a unit's weight tile is 256 rows, held as two
+// 128-row halves by the two CTAs of a cluster; P counts clusters, m_tiles counts 256-row
+// tiles, and the partial slot of 128-row half r of tile t is (t * pair + r) * maxc + k.
 struct SplitPlan {
   long long U;
   int P, bn, m_tiles, token_tiles, tiles, kb_total, maxc;
+  int pair;
 };
 __host__ __device__ inline long long sk_unit0(int c, const SplitPlan &p) { return p.U * c / p.P; }
 __host__ __device__ inline int sk_cta_of(long long u, const SplitPlan &p) {
@@ -47,8 +51,16 @@ __host__ __device__ inline void sk_decode(int t, const SplitPlan &p, int &bi, in
 __host__ __device__ inline int sk_tile_of(const SplitPlan &p, int bi, int tt, int mt) {
   return (bi * p.m_tiles + mt) * p.token_tiles + tt;
 }
-__host__ __device__ inline float *sk_partial(float *ws, const SplitPlan &p, int t, int k) {
-  return ws + ((size_t)t * p.maxc + k) * p.bn * 128;
+__host__ __device__ inline int sk_pair(const SplitPlan &p) { return p.pair > 1 ? 2 : 1; }
+__host__ __device__ inline float *sk_partial(float *ws, const SplitPlan &p, int t, int k, int r = 0) {
+  return ws + (((size_t)t * sk_pair(p) + r) * p.maxc + k) * p.bn * 128;
+}
+// (unit tile t, first partial slot) of output column n (any 128-row half) for token row m
+__host__ __device__ inline void sk_locate(const SplitPlan &p, int bi, int m, int n, int &t, size_t &slot0) {
+  const int pr = sk_pair(p);
+  const int tt = m / p.bn, mt = n >> 7;
+  t = sk_tile_of(p, bi, tt, mt / pr);
+  slot0 = ((size_t)t * pr + (mt % pr)) * p.maxc;
 }
 // Where a GEMM's partials live, for the consumer kernels.  planes = 3 in the fp32
 // parity mode: every logical activation row m was fed to the GEMM as three bf16
@@ -65,12 +77,14 @@ struct PartialView {
 // trip instead of one per contributor).
 __device__ inline float4 sk_sum4(const PartialView &v, int bi, int m, int n) {
   const SplitPlan &p = v.plan;
-  const int tt = m / p.bn, mt = n >> 7;
-  const int t = sk_tile_of(p, bi, tt, mt);
+  const int tt = m / p.bn;
+  int t;
+  size_t slot0;
+  sk_locate(p, bi, m, n, t, slot0);
   const int cf = sk_cta_of((long long)t * p.kb_total, p), cl = sk_cta_of((long long)(t + 1) * p.kb_total - 1, p);
   const int nc = cl - cf + 1;
   const float4 *base =
-      reinterpret_cast<const float4 *>(v.ws + (size_t)t * p.maxc * p.bn * 128 + (size_t)(m - tt * p.bn) * 128 + (n & 127));
+      reinterpret_cast<const float4 *>(v.ws + slot0 * p.bn * 128 + (size_t)(m - tt * p.bn) * 128 + (n & 127));
   const size_t stride = (size_t)p.bn * 128 / 4;  // float4 between contributors
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int k0 = 0; k0 < nc; k0 += 8) {
@@ -99,13 +113,14 @@ struct SkRef {
 };
 __device__ inline SkRef sk_ref(const PartialView &v, int bi, int m, int n) {
   const SplitPlan &p = v.plan;
-  const int tt = m / p.bn, mt = n >> 7;
-  const int t = sk_tile_of(p, bi, tt, mt);
+  const int tt = m / p.bn;
+  int t;
+  size_t slot0;
+  sk_locate(p, bi, m, n, t, slot0);
   const int cf = sk_cta_of((long long)t * p.kb_total, p), cl = sk_cta_of((long long)(t + 1) * p.kb_total - 1, p);
   SkRef r;
   r.nc = cl - cf + 1;
-  r.base = reinterpret_cast<const float4 *>(v.ws + (size_t)t * p.maxc * p.bn * 128 + (size_t)(m - tt * p.bn) * 128 +
-                                            (n & 127));
+  r.base = reinterpret_cast<const float4 *>(v.ws + slot0 * p.bn * 128 + (size_t)(m - tt * p.bn) * 128 + (n & 127));
   r.stride = (size_t)p.bn * 128 / 4;
   return r;
 }
@@ -137,11 +152,13 @@ __device__ inline float4 sk_reduce(const SkRef &r, const float4 (&x)[NMAX]) {
 }
 __device__ inline float sk_sum1(const PartialView &v, int bi, int m, int n) {
   const SplitPlan &p = v.plan;
-  const int tt = m / p.bn, mt = n >> 7;
-  const int t = sk_tile_of(p, bi, tt, mt);
+  const int tt = m / p.bn;
+  int t;
+  size_t slot0;
+  sk_locate(p, bi, m, n, t, slot0);
   const int cf = sk_cta_of((long long)t * p.kb_total, p), cl = sk_cta_of((long long)(t + 1) * p.kb_total - 1, p);
   const int nc = cl - cf + 1;
-  const float *base = v.ws + (size_t)t * p.maxc * p.bn * 128 + (size_t)(m - tt * p.bn) * 128 + (n & 127);
+  const float *base = v.ws + slot0 * p.bn * 128 + (size_t)(m - tt * p.bn) * 128 + (n & 127);
   const size_t stride = (size_t)p.bn * 128;
   float acc = 0.f;
   for (int k0 = 0; k0 < nc; k0 += 8) {
@@ -251,6 +268,7 @@ struct GemmArgs {
   int l2_prefetch;                 // weight k-blocks per CTA prefetched into L2 before the PDL wait
   int dbg_mode;                    // experiments: 1 = stream weights only (no X, no MMA)
   int pre_stages;                  // weight stages issued before griddepcontrol.wait (-1 = the ring)
+  int no_pair;                     // 1: plan without the 2-SM (cta_group::2) variant
   SplitPlan plan;
   float *ws;                       // partial slots, gemm_ws_floats() floats
   int epi;                         // kEpi*: fused tile epilogue (batch 1 only)
@@ -267,6 +285,7 @@ void gemm_set_l2_prefetch(int kblocks);
 void gemm_set_debug_mode(int m);
 void gemm_set_small(int v);
 void gemm_set_bn(int bn);
+void gemm_set_pair(int mode);  // 2-SM MMA for token tiles >= 96 rows (1), >= 64 (2), off (0)
 void gemm_set_pre_stages(int n);  // experiments: force the token-tile width (16..256 supported set; 0 = auto)
 
 // ---------------------------------------------------------------- K1 tree attention

@@ -80,8 +80,8 @@ static sm_status act_map(GemmArgs &a, int i, const void *x, int rows, int K) {
 // BN >= 64: the kernel loads a stage's BN activation rows with one TMA box of BN rows
 // (request count, not bytes, limits the L2 -> SM fill of small boxes).
 static sm_status act_box(GemmArgs &a) {
-  const int bn = a.plan.bn;
-  if (bn < 64 || bn == a.x_box) return SM_OK;
+  const int bn = a.plan.pair == 2 ? a.plan.bn / 2 : a.plan.bn;  // 2-SM: each CTA loads half the token rows
+  if (a.plan.bn < 64 || bn == a.x_box) return SM_OK;
   for (int i = 0; i < a.batch; ++i)
     CKS(make_tmap(&a.tmX64[i], a.x_base[i], (uint64_t)a.x_rows[i], (uint64_t)a.K, (uint32_t)bn, 64, true));
   a.x_box = bn;
@@ -511,6 +511,7 @@ static sm_status run_gemm(GemmArgs a, int M, int x_row0, float *ws, size_t ws_fl
                           PartialView *pv, int planes = 1, int epi = kEpiPartial, const EpiArgs *ea = nullptr) {
   const int Mlog = M;
   M *= planes;
+  a.no_pair = epi != kEpiPartial ? 1 : 0;  // the fused fixup addresses single-SM partial slots
   gemm_plan(a, a.N, a.K, M, a.batch);
   a.epi = epi;
   if (ea) a.e = *ea;
@@ -1632,6 +1633,8 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
     gemm_set_debug_mode(value);
   } else if (n == "fused_epilogue") {  // takes effect for models created afterwards
     g_fused = value & 7;
+  } else if (n == "gemm_pair") {
+    gemm_set_pair(value);
   } else if (n == "gemm_pre") {
     gemm_set_pre_stages(value);
   } else if (n == "consumer_threads") {

@@ -63,6 +63,17 @@ def test_gemm_matches_fp64(sm, M, N, K):
     assert np.all(err <= 2e-6 * bound + 1e-30), float((err / (bound + 1e-30)).max())
 
 
+@pytest.mark.parametrize("M,N,K", [(64, 4096, 512), (100, 1000, 320), (160, 8192, 1024), (256, 384, 8192),
+                                   (77, 4352, 640)])
+def test_gemm_pair_matches_fp64(sm, M, N, K):
+    """The 2-SM (tcgen05 cta_group::2) K2 variant (sm_set_option gemm_pair = 2: token tiles >= 64)."""
+    sm.set_option("gemm_pair", 2)
+    try:
+        test_gemm_matches_fp64(sm, M, N, K)
+    finally:
+        sm.set_option("gemm_pair", 0)
+
+
 # ------------------------------------------------------------------ K1 tree attention
 class _Geom:
     def __init__(self, H, Hkv, hd):

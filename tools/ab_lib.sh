@@ -1,5 +1,5 @@
 for i in 1 2; do
-for lib in libspecmemo.so libspecmemo_lb4.so; do
+for lib in libspecmemo_old.so libspecmemo.so; do
   echo "== $lib"
   SPECMEMO_LIB=paper_2506_01986_b200/$lib timeout 300 python bench.py --no-cpu-baseline --no-k1 --no-vanilla --steps 100 --warmup 10 --e2e-steps 10 --prof-steps 2 2>&1 | python3 -c "
 import json,sys
