@@ -656,6 +656,7 @@ cudaError_t gemm_launch(const GemmArgs &a0, cudaStream_t st) {
                     : g_occ == 2 ? launch_bn<32, 104>(a, st) : launch_bn<32, 216>(a, st);
     case 64: return g_occ == 4 ? launch_bn<64, 50>(a, st) : g_occ == 3 ? launch_bn<64, 68>(a, st)
                     : g_occ == 2 ? launch_bn<64, 104>(a, st) : launch_bn<64, 216>(a, st);
+    case 80: return launch_bn<80, 104>(a, st);  // experiments (gemm_bn): 2 CTAs per SM at 2 x 80 TMEM columns
     case 96: return launch_bn<96, 216>(a, st);
     case 128: return launch_bn<128, 216>(a, st);
     case 160: return launch_bn<160, 216>(a, st);
@@ -677,7 +678,8 @@ void gemm_preload() {
   preload_one<16, 50>(), preload_one<16, 68>(), preload_one<16, 104>(), preload_one<16, 216>();
   preload_one<32, 50>(), preload_one<32, 68>(), preload_one<32, 104>(), preload_one<32, 216>();
   preload_one<64, 50>(), preload_one<64, 68>(), preload_one<64, 104>(), preload_one<64, 216>();
-  preload_one<96, 216>(), preload_one<128, 216>(), preload_one<160, 216>(), preload_one<192, 216>();
+  preload_one<80, 104>(), preload_one<96, 216>(), preload_one<128, 216>(), preload_one<160, 216>();
+  preload_one<192, 216>();
   preload_one<256, 216>();
   cudaFuncAttributes fa;
   cudaFuncGetAttributes(&fa, gemm_pair_kernel<64, 104>);

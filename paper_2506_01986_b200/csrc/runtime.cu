@@ -1623,9 +1623,9 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
   } else if (n == "l2_prefetch") {
     gemm_set_l2_prefetch(value);
   } else if (n == "gemm_bn") {
-    if (value != 0 && value != 16 && value != 32 && value != 64 && value != 96 && value != 128 && value != 160 &&
-        value != 192 && value != 256)
-      return fail(SM_ERR_INVALID_ARG, "gemm_bn must be 0 or one of 16 32 64 96 128 160 192 256");
+    if (value != 0 && value != 16 && value != 32 && value != 64 && value != 80 && value != 96 && value != 128 &&
+        value != 160 && value != 192 && value != 256)
+      return fail(SM_ERR_INVALID_ARG, "gemm_bn must be 0 or one of 16 32 64 80 96 128 160 192 256");
     gemm_set_bn(value);
   } else if (n == "gemm_occ") {
     gemm_set_small(value);

@@ -10,7 +10,11 @@ import paper_2506_01986_b200 as sm  # noqa: E402
 
 SHAPES = [("qkv", 10240, 8192), ("o", 8192, 8192), ("gu", 57344, 8192), ("down", 8192, 28672)]
 OUT = "--consumer" in sys.argv  # default: GEMM only (stage API with out = NULL)
-for M, bns in ((160, (160, 192, 256)), (640, (128, 160, 256)), (64, (64, 96, 128)), (10, (16, 32))):
+CASES = ((160, (64, 80, 96, 128, 160)), (640, (128, 160, 256)), (256, (64, 128, 256)), (64, (64, 96, 128)),
+         (10, (16, 32)))
+if "--c4" in sys.argv:
+    CASES = ((160, (64, 80, 96, 128, 160)),)
+for M, bns in CASES:
     for bn in bns:
         sm.set_option("gemm_bn", bn)
         res, tot_us, tot_b = [], 0.0, 0

@@ -6,3 +6,5 @@ for c in c1 c3 c4; do timeout 900 python bench.py --config $c --steps 30 --warmu
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo ref=$?
 timeout 900 python tools/k1_sweep.py > gpurun_out/k1_sweep.txt 2>&1; echo sweep=$?
 bash tools/ncu_capture.sh > gpurun_out/ncu_capture.log 2>&1; echo ncu=$?
+timeout 600 python tools/prefill_bench.py > gpurun_out/prefill.txt 2>&1; echo prefill=$?
+timeout 900 python tools/tree_sweep.py > gpurun_out/tree_sweep.txt 2>&1; echo tree=$?
