@@ -106,6 +106,9 @@ SM_DEV void tmem_st32_f(uint32_t taddr, const float *v) {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+// sm_set_option("attn_l2pf"): prefetch the o_proj weights into L2 during attention.  Measured:
+// the o_proj GEMM gains ~0.8 us per layer, attention loses ~2.3 us (its K/V reads compete) -> off.
+__device__ int g_attn_l2pf = 0;
 __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_constant__ AttnArgs a) {
   using namespace tc;
   extern __shared__ uint8_t smem_raw[];
@@ -171,6 +174,14 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
     fence_barrier_init();
     while (pre < first && key0 + (pre + 1) * KEYS <= Lc) issue(pre++);
     SM_STAMP(11);
+    if (a.l2_pf && g_attn_l2pf) {  // experiments: this CTA's slice of the next GEMM's weights -> L2
+      const unsigned ctas = gridDim.x * gridDim.y * gridDim.z;
+      const unsigned cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+      const unsigned long long per = ((a.l2_pf_bytes + ctas - 1) / ctas + 4095) & ~4095ull;
+      const unsigned long long b0 = per * cta, b1 = min(a.l2_pf_bytes, b0 + per);
+      for (unsigned long long off = b0; off < b1; off += 65536)
+        prefetch_l2_bulk(static_cast<const char *>(a.l2_pf) + off, (uint32_t)min(65536ull, b1 - off));
+    }
   }
   // softmax threads: the ancestor words of their row's node (static tree tables: safe before the wait)
   uint64_t anc0 = 0, anc1 = 0, anc2 = 0, anc3 = 0;
@@ -532,6 +543,8 @@ cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
   cfg.numAttrs = a.nsplit > 1 ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel, a);
 }
+
+void attention_set_l2pf(int on) { cudaMemcpyToSymbol(g_attn_l2pf, &on, sizeof(int)); }
 
 void attention_tc_preload() {  // force-load (see gemm_preload)
   cudaFuncAttributes fa;

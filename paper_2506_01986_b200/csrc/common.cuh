@@ -60,6 +60,14 @@ SM_DEV float2 ld_dsmem_f32x2(uint32_t cluster_addr) {
   asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(cluster_addr) : "memory");
   return v;
 }
+SM_DEV void st_dsmem_f32x4(uint32_t cluster_addr, float4 v) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(cluster_addr), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+SM_DEV void st_dsmem_f32x2(uint32_t cluster_addr, float a, float b) {
+  asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(cluster_addr), "f"(a), "f"(b) : "memory");
+}
 SM_DEV float4 ld_dsmem_f32x4(uint32_t cluster_addr) {
   float4 v;
   asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -236,6 +244,10 @@ SM_DEV void tma_load_2d_hint(void *smem_dst, const CUtensorMap *m, uint64_t *bar
 SM_DEV void tma_prefetch_l2_2d(const CUtensorMap *m, int c0, int c1) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"((uint64_t)m), "r"(c0), "r"(c1)
                : "memory");
+}
+// bulk prefetch of [ptr, ptr + bytes) into L2 (bytes a multiple of 16)
+SM_DEV void prefetch_l2_bulk(const void *ptr, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((uint64_t)ptr), "r"(bytes) : "memory");
 }
 SM_DEV uint64_t policy_evict_first() {
   uint64_t p;

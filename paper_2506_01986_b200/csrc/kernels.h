@@ -301,6 +301,10 @@ struct AttnArgs {
   int Nq, H, Hkv, G, nseq, seq_base;
   int nsplit;                 // key splits = cluster size (1, 2, 4, 8), combined through DSMEM
   float scale_log2;           // log2(e) / sqrt(hd)
+  // L2 prefetch of the next GEMM's weights (the o_proj, which cannot start its own prefetch
+  // while the attention CTAs fill the SMs' shared memory); nullable
+  const void *l2_pf;
+  unsigned long long l2_pf_bytes;
 };
 cudaError_t attention_launch(const AttnArgs &a, int head_dim, cudaStream_t st);
 int attention_row_blocks(int Nq, int G, int head_dim);
@@ -312,6 +316,7 @@ cudaError_t attention_f32_launch(const float *q, const float *k, const float *v,
 int attention_nsplit(int units, int head_dim);  // units = row blocks * sequences * kv heads
 void attention_set_splits(int n);               // experiments: force key splits (0 = auto)
 void attention_set_tc(int on);                  // head_dim 128: tcgen05 kernel (1, default) or mma.sync (0)
+void attention_set_l2pf(int on);                // experiments: L2 prefetch of AttnArgs.l2_pf (0, default)
 
 // ---------------------------------------------------------------- GEMM consumers (epilogue.cu)
 // Every consumer waits on the producer GEMM with griddepcontrol.wait and lets

@@ -1196,6 +1196,8 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
     aa.seq_base = seq_base;
     aa.nsplit = nsplit;
     aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)m->hd));
+    aa.l2_pf = m->wo[l];  // o_proj weights stream into L2 while attention runs
+    aa.l2_pf_bytes = (unsigned long long)d * m->H * m->hd * 2;
     cudaEvent_t ev = nullptr;
     prof_begin(st, &ev);
     if (KEEP(1)) {
@@ -1645,6 +1647,8 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
     g_ablate = value;
   } else if (n == "attn_tc") {
     attention_set_tc(value);
+  } else if (n == "attn_l2pf") {
+    attention_set_l2pf(value);
   } else if (n == "attn_splits") {
     attention_set_splits(value);
   } else {
