@@ -529,8 +529,13 @@ static int g_occ = 2;  // GEMM CTAs per SM for BN <= 64 (1..4); grid = 148 * occ
 void gemm_set_bn(int bn) { g_force_bn = bn; }
 void gemm_set_pair(int mode) { g_pair = mode < 0 ? 0 : (mode > 2 ? 2 : mode); }
 void gemm_set_pre_stages(int n) { g_pre_stages = n; }
+static int g_occ_smalln = 0;  // experiments: occupancy for GEMMs with N <= 8192 (0 = g_occ)
 void gemm_set_small(int v) { g_occ = v < 1 ? 1 : (v > 4 ? 4 : v); }
-int gemm_occ_for(int bn) { return bn <= 64 ? g_occ : 1; }
+void gemm_set_occ_smalln(int v) { g_occ_smalln = v < 0 ? 0 : (v > 4 ? 4 : v); }
+int gemm_occ_for(int bn, int N = 1 << 30) {
+  if (bn > 64) return 1;
+  return (g_occ_smalln > 0 && N <= 8192) ? g_occ_smalln : g_occ;
+}
 void gemm_set_debug_mode(int m) { g_dbg_mode = m; }
 void gemm_set_pdl(bool on) { g_pdl = on; }
 bool gemm_pdl() { return g_pdl; }
@@ -618,7 +623,8 @@ void gemm_plan(GemmArgs &a, int N, int K, int M, int batch) {
   p.tiles = p.m_tiles * p.token_tiles * batch;
   p.kb_total = (K + 63) / 64;
   const long long U = (long long)p.tiles * p.kb_total;
-  int want = g_ctas > 0 ? g_ctas : kNumSMs * gemm_occ_for(p.bn);
+  p.occ = gemm_occ_for(p.bn, N);
+  int want = g_ctas > 0 ? g_ctas : kNumSMs * p.occ;
   if (p.pair == 2)  // clusters of 2 CTAs; 2 CTAs per SM while 2 x BN TMEM columns fit twice
     want = g_ctas > 0 ? g_ctas / 2 : (p.bn <= 128 ? kNumSMs : kNumSMs / 2);
   p.P = (int)(U < want ? U : want);
@@ -650,12 +656,12 @@ cudaError_t gemm_launch(const GemmArgs &a0, cudaStream_t st) {
     }
   }
   switch (a.plan.bn) {
-    case 16: return g_occ == 4 ? launch_bn<16, 50>(a, st) : g_occ == 3 ? launch_bn<16, 68>(a, st)
-                    : g_occ == 2 ? launch_bn<16, 104>(a, st) : launch_bn<16, 216>(a, st);
-    case 32: return g_occ == 4 ? launch_bn<32, 50>(a, st) : g_occ == 3 ? launch_bn<32, 68>(a, st)
-                    : g_occ == 2 ? launch_bn<32, 104>(a, st) : launch_bn<32, 216>(a, st);
-    case 64: return g_occ == 4 ? launch_bn<64, 50>(a, st) : g_occ == 3 ? launch_bn<64, 68>(a, st)
-                    : g_occ == 2 ? launch_bn<64, 104>(a, st) : launch_bn<64, 216>(a, st);
+    case 16: return a.plan.occ == 4 ? launch_bn<16, 50>(a, st) : a.plan.occ == 3 ? launch_bn<16, 68>(a, st)
+                    : a.plan.occ == 2 ? launch_bn<16, 104>(a, st) : launch_bn<16, 216>(a, st);
+    case 32: return a.plan.occ == 4 ? launch_bn<32, 50>(a, st) : a.plan.occ == 3 ? launch_bn<32, 68>(a, st)
+                    : a.plan.occ == 2 ? launch_bn<32, 104>(a, st) : launch_bn<32, 216>(a, st);
+    case 64: return a.plan.occ == 4 ? launch_bn<64, 50>(a, st) : a.plan.occ == 3 ? launch_bn<64, 68>(a, st)
+                    : a.plan.occ == 2 ? launch_bn<64, 104>(a, st) : launch_bn<64, 216>(a, st);
     case 80: return launch_bn<80, 104>(a, st);  // experiments (gemm_bn): 2 CTAs per SM at 2 x 80 TMEM columns
     case 96: return launch_bn<96, 216>(a, st);
     case 128: return launch_bn<128, 216>(a, st);

@@ -33,6 +33,7 @@ struct SplitPlan {
   long long U;
   int P, bn, m_tiles, token_tiles, tiles, kb_total, maxc;
   int pair;
+  int occ;  // GEMM CTAs per SM of the launch (smem variant)
 };
 __host__ __device__ inline long long sk_unit0(int c, const SplitPlan &p) { return p.U * c / p.P; }
 __host__ __device__ inline int sk_cta_of(long long u, const SplitPlan &p) {
@@ -285,7 +286,8 @@ void gemm_set_l2_prefetch(int kblocks);
 void gemm_set_debug_mode(int m);
 void gemm_set_small(int v);
 void gemm_set_bn(int bn);
-void gemm_set_pair(int mode);  // 2-SM MMA for token tiles >= 96 rows (1), >= 64 (2), off (0)
+void gemm_set_pair(int mode);
+void gemm_set_occ_smalln(int v);  // experiments: occupancy of GEMMs with N <= 8192  // 2-SM MMA for token tiles >= 96 rows (1), >= 64 (2), off (0)
 void gemm_set_pre_stages(int n);  // experiments: force the token-tile width (16..256 supported set; 0 = auto)
 
 // ---------------------------------------------------------------- K1 tree attention

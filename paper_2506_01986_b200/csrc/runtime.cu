@@ -1635,6 +1635,8 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
     gemm_set_debug_mode(value);
   } else if (n == "fused_epilogue") {  // takes effect for models created afterwards
     g_fused = value & 7;
+  } else if (n == "gemm_occ_smalln") {
+    gemm_set_occ_smalln(value);
   } else if (n == "gemm_pair") {
     gemm_set_pair(value);
   } else if (n == "gemm_pre") {
