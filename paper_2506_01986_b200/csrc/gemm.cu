@@ -379,7 +379,10 @@ struct PairCfg {
   static constexpr int kB = (BN / 2) * 64 * 2;
   static constexpr int kStage = kA + kB;
   static constexpr int kStages = (SMEMKB * 1024) / kStage;
-  static constexpr int kTmemCols = 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+  // TMEM accumulator buffers: two (the MMA of the next segment overlaps the epilogue) unless
+  // two CTAs share the SM and 2 x BN columns would not fit twice into its 512 columns
+  static constexpr int kNBuf = (2 * BN <= 256 || SMEMKB > 104) ? 2 : 1;
+  static constexpr int kTmemCols = kNBuf * BN <= 128 ? 128 : kNBuf * BN <= 256 ? 256 : 512;
   static constexpr int kSmem = kStages * kStage + 1024 + 256;
 };
 
@@ -465,8 +468,8 @@ __global__ void __launch_bounds__(192, 1) gemm_pair_kernel(const __grid_constant
       for (long long u = u0; u < u1; ++u) {
         const int i = (int)(u - u0);
         const int s = i % C::kStages;
-        const int buf = seg & 1;
-        if (seg_start && seg >= 2) mbar_wait(&tempty[buf], ((seg >> 1) - 1) & 1);
+        const int buf = seg % C::kNBuf;
+        if (seg_start && seg >= C::kNBuf) mbar_wait(&tempty[buf], ((seg / C::kNBuf) - 1) & 1);
         mbar_wait(&full[s], (i / C::kStages) & 1);
         tc_fence_after();
         const uint64_t ad = umma_desc_sw128(smem_u32(sA + s * C::kA));
@@ -493,8 +496,8 @@ __global__ void __launch_bounds__(192, 1) gemm_pair_kernel(const __grid_constant
     while (u < u1) {
       const int t = sk_tile(u, pl);
       const long long seg_end = min(u1, (long long)(t + 1) * pl.kb_total);
-      const int buf = seg & 1;
-      mbar_wait(&tfull[buf], (seg >> 1) & 1);
+      const int buf = seg % C::kNBuf;
+      mbar_wait(&tfull[buf], (seg / C::kNBuf) & 1);
       tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(wq * 32) << 16) + buf * BN;
       float *dst = sk_partial(a.ws, pl, t, c - sk_cta_of((long long)t * pl.kb_total, pl), rank);
@@ -523,7 +526,10 @@ static int g_ctas = 0;
 static int g_l2pf = 0;
 static int g_dbg_mode = 0;
 static int g_force_bn = 0;
-static int g_pair = 0;  // 2-SM MMA (experiments; measured slower): 0 off, 1 for BN >= 96, 2 for BN >= 64
+// 2-SM MMA (cta_group::2): 0 off; 1 (default) for token tiles of 96..192 rows and for 256-row
+// tiles when there are several (measured faster there, slower at M = 64 and one 256-row tile,
+// DESIGN.md §5.2); 2 for every tile of >= 64 rows (experiments)
+static int g_pair = 1;
 static int g_pre_stages = -1;  // experiments: weight stages issued before griddepcontrol.wait (-1 = ring)  // experiments: fixed token-tile width (0 = gemm_pick_bn)
 static int g_occ = 2;  // GEMM CTAs per SM for BN <= 64 (1..4); grid = 148 * occ
 void gemm_set_bn(int bn) { g_force_bn = bn; }
@@ -617,7 +623,9 @@ void gemm_plan(GemmArgs &a, int N, int K, int M, int batch) {
   a.batch = batch;
   SplitPlan &p = a.plan;
   p.bn = g_force_bn > 0 ? g_force_bn : gemm_pick_bn(M);
-  p.pair = (!a.no_pair && batch == 1 && ((g_pair == 1 && p.bn >= 96) || (g_pair == 2 && p.bn >= 64))) ? 2 : 1;
+  const int ttiles = (M + p.bn - 1) / p.bn;
+  const bool pair_ok = (g_pair == 1 && p.bn >= 96 && (p.bn < 256 || ttiles > 1)) || (g_pair == 2 && p.bn >= 64);
+  p.pair = (!a.no_pair && batch == 1 && pair_ok) ? 2 : 1;
   p.m_tiles = (N + 128 * p.pair - 1) / (128 * p.pair);
   p.token_tiles = (M + p.bn - 1) / p.bn;
   p.tiles = p.m_tiles * p.token_tiles * batch;
@@ -625,8 +633,7 @@ void gemm_plan(GemmArgs &a, int N, int K, int M, int batch) {
   const long long U = (long long)p.tiles * p.kb_total;
   p.occ = gemm_occ_for(p.bn, N);
   int want = g_ctas > 0 ? g_ctas : kNumSMs * p.occ;
-  if (p.pair == 2)  // clusters of 2 CTAs; 2 CTAs per SM while 2 x BN TMEM columns fit twice
-    want = g_ctas > 0 ? g_ctas / 2 : (p.bn <= 128 ? kNumSMs : kNumSMs / 2);
+  if (p.pair == 2) want = g_ctas > 0 ? g_ctas / 2 : kNumSMs;  // clusters of 2 CTAs, 2 CTAs per SM
   p.P = (int)(U < want ? U : want);
   p.U = U;
   // contributors per tile <= ceil(KB / floor(U/P)) + 1
@@ -648,10 +655,10 @@ cudaError_t gemm_launch(const GemmArgs &a0, cudaStream_t st) {
       case 64: return launch_pair<64, 104>(a, st);
       case 96: return launch_pair<96, 104>(a, st);
       case 128: return launch_pair<128, 104>(a, st);
-      // BN >= 160 needs 2 x BN > 256 TMEM columns: one CTA per SM (TMEM holds 512 columns)
-      case 160: return launch_pair<160, 216>(a, st);
-      case 192: return launch_pair<192, 216>(a, st);
-      case 256: return launch_pair<256, 216>(a, st);
+      // BN >= 160: two CTAs per SM with one TMEM accumulator buffer each (PairCfg::kNBuf)
+      case 160: return launch_pair<160, 104>(a, st);
+      case 192: return launch_pair<192, 104>(a, st);
+      case 256: return launch_pair<256, 104>(a, st);
       default: return cudaErrorInvalidValue;
     }
   }
@@ -691,9 +698,9 @@ void gemm_preload() {
   cudaFuncGetAttributes(&fa, gemm_pair_kernel<64, 104>);
   cudaFuncGetAttributes(&fa, gemm_pair_kernel<96, 104>);
   cudaFuncGetAttributes(&fa, gemm_pair_kernel<128, 104>);
-  cudaFuncGetAttributes(&fa, gemm_pair_kernel<160, 216>);
-  cudaFuncGetAttributes(&fa, gemm_pair_kernel<192, 216>);
-  cudaFuncGetAttributes(&fa, gemm_pair_kernel<256, 216>);
+  cudaFuncGetAttributes(&fa, gemm_pair_kernel<160, 104>);
+  cudaFuncGetAttributes(&fa, gemm_pair_kernel<192, 104>);
+  cudaFuncGetAttributes(&fa, gemm_pair_kernel<256, 104>);
 }
 
 SM_GT_READER(sm_gtrace_read_gemm)
