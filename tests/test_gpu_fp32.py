@@ -267,3 +267,39 @@ def test_fused_epilogues_logits_and_kv(sm):
                 assert ok, (fused, li, c, err)
     # both paths sum the same partials in the same order; only rs's sum of squares differs in order
     assert np.max(np.abs(res[1][0] - res[0][0])) < 1e-2
+
+
+def test_c2_width_batched_pair_path_matches_unbatched(sm):
+    """b = 3 sequences of the V64 tree -> M = 192 token rows: the verify GEMMs take the 2-SM
+    (cta_group::2) K2 variant with one TMEM buffer per CTA; each sequence's logits and K/V must
+    equal its b = 1 run (M = 64, single-SM K2, oracle-checked above) within the bf16 bar (Q29)."""
+    prompts = [synth.prompt_tokens(20 + i, 0, 10 + 3 * i, C2["vocab"]) for i in range(3)]
+    W = sm.allocate_weights(C2, 4, seed=0, medusa_init=True)
+    tree = sm.Tree(synth.V64, topk=10)
+
+    def run(b, ps):
+        model = sm.Model(C2, W, max_rows=b * tree.N, max_batch=b, max_seq_len=64 + tree.N)
+        kv = sm.KVCache(model, tree, b, 64)
+        for i, p in enumerate(ps):
+            kv.prefill(i, torch.from_numpy(p).cuda())
+        tt = torch.zeros(b, tree.N, dtype=torch.int32, device="cuda")
+        kv.propose(tt)
+        logits = torch.zeros(b, tree.N, C2["vocab"], dtype=torch.float32, device="cuda")
+        kv.verify(tt, logits)
+        torch.cuda.synchronize()
+        return tt.cpu(), logits.cpu().double(), kv.layout().float().cpu().double()
+
+    tb, zb, kb = run(3, prompts)
+    for i, p in enumerate(prompts):
+        t1, z1, k1 = run(1, [p])
+        agree = int((tb[i] == t1[0]).sum())
+        assert agree >= 56, agree                       # tree tokens (top-10 near-ties aside)
+        if agree == tree.N:
+            e = (zb[i] - z1[0]).abs()
+            assert float(e.max()) <= 2e-2 * float(z1[0].abs().max())
+            assert float((zb[i] - z1[0]).norm()) <= 2e-2 * float(z1[0].norm())
+        L = len(p)
+        for li in range(2):
+            for c in (0, 1):
+                a, r = kb[li, c, i][:, :L], k1[li, c, 0][:, :L]   # prompt K/V (prefill: M = L rows)
+                assert float((a - r).abs().max()) <= 2e-2 * float(r.abs().max())
