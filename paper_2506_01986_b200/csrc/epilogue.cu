@@ -334,6 +334,16 @@ cudaError_t silu_consumer_launch(const PartialView &pv, int F, bf16 *act, const 
 }
 
 // ------------------------------------------------------------------ logits: argmax + typical stats
+// One row per cluster of kVocabSplit CTAs, each over a contiguous vocabulary slice; the slice
+// results (argmax by (value, lowest index), single-pass (m, s, t)) are pushed into rank 0's
+// shared memory and merged there in rank order (deterministic).  Splitting the vocabulary
+// puts b*N*8 CTAs instead of b*N on the 32000-wide rows (the step's tail is latency-bound).
+constexpr int kVocabSplit = 8;
+SM_DEV void vocab_slice(int V, int rank, int cs, int &j0, int &j1) {
+  const int per = ((V + cs - 1) / cs + 3) & ~3;  // float4-aligned slices
+  j0 = min(V, rank * per);
+  j1 = min(V, j0 + per);
+}
 template <bool FROM_PARTIALS>
 __global__ void __launch_bounds__(512) logits_kernel(PartialView pv, const float *z_in, int V, float inv_temp,
                                                      float *z_out, int32_t *argmax, float *stats, int idx_offset,
@@ -341,13 +351,17 @@ __global__ void __launch_bounds__(512) logits_kernel(PartialView pv, const float
   __shared__ float sv[32];
   __shared__ int si[32];
   __shared__ MST smst[32];
+  __shared__ float part[kVocabSplit][5];  // rank q's (value, index, m, s, t), pushed by q
   pdl_trigger();
+  cluster_arrive_relaxed();  // every CTA of the cluster started before any DSMEM store
   pdl_wait();
-  const int r = blockIdx.x;
+  const int r = blockIdx.y, rank = blockIdx.x, cs = gridDim.x;
+  int j0, j1;
+  vocab_slice(V, rank, cs, j0, j1);
   float bv = -INFINITY;
   int bi = 0x7fffffff;
   MST acc{-INFINITY, 0.f, 0.f};
-  for (int j = threadIdx.x * 4; j < V; j += blockDim.x * 4) {
+  for (int j = j0 + threadIdx.x * 4; j < j1; j += blockDim.x * 4) {
     float4 z4;
     if constexpr (FROM_PARTIALS) {
       z4 = sk_get4(pv, 0, r, j);
@@ -378,109 +392,222 @@ __global__ void __launch_bounds__(512) logits_kernel(PartialView pv, const float
     smst[w] = acc;
   }
   __syncthreads();
+  cluster_wait();
   if (threadIdx.x == 0) {
     for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
       argmax_merge(bv, bi, sv[k], si[k]);
       acc = mst_merge(acc, smst[k]);
     }
-    argmax[r] = bi + idx_offset;  // vocabulary-parallel slice -> global token id
-    if (amax) amax[r] = bv;
+    const uint32_t dst = mapa_u32(smem_u32(&part[rank][0]), 0);
+    st_dsmem_f32(dst, bv);
+    st_dsmem_f32(dst + 4, __int_as_float(bi));
+    st_dsmem_f32(dst + 8, acc.m);
+    st_dsmem_f32(dst + 12, acc.s);
+    st_dsmem_f32(dst + 16, acc.t);
+  }
+  cluster_sync_all();  // every slice result has landed in rank 0
+  if (rank == 0 && threadIdx.x == 0) {
+    float v = -INFINITY;
+    int idx = 0x7fffffff;
+    MST a{-INFINITY, 0.f, 0.f};
+    for (int q = 0; q < cs; ++q) {  // rank order: deterministic
+      argmax_merge(v, idx, part[q][0], __float_as_int(part[q][1]));
+      a = mst_merge(a, MST{part[q][2], part[q][3], part[q][4]});
+    }
+    argmax[r] = idx + idx_offset;  // vocabulary-parallel slice -> global token id
+    if (amax) amax[r] = v;
     if (stats) {
-      stats[3 * r + 0] = acc.m;
-      stats[3 * r + 1] = acc.s;
-      stats[3 * r + 2] = acc.t;
+      stats[3 * r + 0] = a.m;
+      stats[3 * r + 1] = a.s;
+      stats[3 * r + 2] = a.t;
     }
   }
 }
 cudaError_t logits_consumer_launch(const PartialView &pv, float inv_temp, float *z_out, int32_t *argmax, float *stats,
                                    int idx_offset, float *amax, cudaStream_t st) {
-  return launch_pdl(logits_kernel<true>, dim3(pv.M), dim3(512), 0, st, pv, (const float *)nullptr, pv.N, inv_temp,
-                    z_out, argmax, stats, idx_offset, amax);
+  return launch_pdl_cluster(logits_kernel<true>, dim3(kVocabSplit, pv.M), dim3(512), 0, st, kVocabSplit, pv,
+                            (const float *)nullptr, pv.N, inv_temp, z_out, argmax, stats, idx_offset, amax);
 }
 cudaError_t logits_finalize_launch(const float *z, int V, int rows, float inv_temp, int32_t *argmax, float *stats,
                                    int idx_offset, float *amax, cudaStream_t st) {
   PartialView pv{};
-  return launch_pdl(logits_kernel<false>, dim3(rows), dim3(512), 0, st, pv, z, V, inv_temp, (float *)nullptr, argmax,
-                    stats, idx_offset, amax);
+  return launch_pdl_cluster(logits_kernel<false>, dim3(kVocabSplit, rows), dim3(512), 0, st, kVocabSplit, pv, z, V,
+                            inv_temp, (float *)nullptr, argmax, stats, idx_offset, amax);
 }
 
 // ------------------------------------------------------------------ top-k (K3)
-// One block per row: the row is staged in shared memory, then K rounds of a
-// block argmax by (value desc, index asc); taken entries become NaN.
-template <bool FROM_PARTIALS>
+// One CTA of 1024 threads per row, one pass over the row: every thread keeps the top-K of its
+// strided elements in registers, sorted by (value desc, index asc); then K tournament rounds
+// pick the block's best list head (warp shuffles, then warp 0 over the 32 warp winners) and
+// advance the winner's list.  The row's top-K is exactly the K best heads drawn this way
+// (ties: lowest index first).  NaN entries are skipped.
+constexpr int kTopkMax = 32;
+// keep the KM best (value desc, index asc) of the values seen, in registers (static indices only:
+// a runtime list length would put the arrays in local memory); KM >= k, so the row's top-k is
+// drawn from these lists
+template <int KM>
+SM_DEV void topk_insert(float (&v)[KM], int (&ix)[KM], float z, int j) {
+  if (!(z == z)) return;  // NaN
+  if (!(z > v[KM - 1] || (z == v[KM - 1] && j < ix[KM - 1]))) return;
+#pragma unroll
+  for (int s = KM - 1; s > 0; --s) {  // from the bottom: shift entries ranked below (z, j), place it
+    const bool below = z > v[s - 1] || (z == v[s - 1] && j < ix[s - 1]);  // (z, j) ranks above entry s-1
+    if (below) {
+      v[s] = v[s - 1];
+      ix[s] = ix[s - 1];
+    } else if (z > v[s] || (z == v[s] && j < ix[s])) {
+      v[s] = z;
+      ix[s] = j;
+    }
+  }
+  if (z > v[0] || (z == v[0] && j < ix[0])) {
+    v[0] = z;
+    ix[0] = j;
+  }
+}
+SM_DEV bool topk_better(float v1, int i1, float v2, int i2) { return v1 > v2 || (v1 == v2 && i1 < i2); }
+
+// block tournament: K rounds, each drawing the best (value desc, index asc) list head of the
+// block's threads and advancing the winner; `emit(kk, value, index)` runs on one thread per round
+template <int KM, typename Emit>
+SM_DEV void topk_tournament(const float (&v)[KM], const int (&ix)[KM], int k, float *wv, int *wi, int *wt, int *s_win,
+                            Emit emit) {
+  int p = 0;  // next unused entry of this thread's list
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int kk = 0; kk < k; ++kk) {
+    float bv = -INFINITY;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int s = 0; s < KM; ++s)
+      if (s == p) {
+        bv = v[s];
+        bi = ix[s];
+      }
+    int bt = threadIdx.x;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      const int t2 = __shfl_xor_sync(0xffffffffu, bt, o);
+      if (topk_better(v2, i2, bv, bi)) {
+        bv = v2;
+        bi = i2;
+        bt = t2;
+      }
+    }
+    if (lane == 0) {
+      wv[w] = bv;
+      wi[w] = bi;
+      wt[w] = bt;
+    }
+    __syncthreads();
+    if (w == 0) {
+      float cv = lane < nw ? wv[lane] : -INFINITY;
+      int ci = lane < nw ? wi[lane] : 0x7fffffff;
+      int ct = lane < nw ? wt[lane] : -1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float v2 = __shfl_xor_sync(0xffffffffu, cv, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, ci, o);
+        const int t2 = __shfl_xor_sync(0xffffffffu, ct, o);
+        if (topk_better(v2, i2, cv, ci)) {
+          cv = v2;
+          ci = i2;
+          ct = t2;
+        }
+      }
+      if (lane == 0) {
+        emit(kk, cv, ci);
+        *s_win = ct;
+      }
+    }
+    __syncthreads();
+    if ((int)threadIdx.x == *s_win) ++p;
+  }
+}
+
+// One row per cluster of kVocabSplit CTAs over vocabulary slices: every thread keeps the best
+// KM (>= k) of its slice elements in registers; a block tournament draws the slice's top-k,
+// pushed into rank 0 over DSMEM; rank 0 draws the row's top-k from the cs * k candidates the
+// same way.  Every element of the row's top-k is in its slice's top-k, so the result equals the
+// single-pass definition, ties included (lowest index first).  NaN entries are skipped.
+template <bool FROM_PARTIALS, int KM>
 __global__ void __launch_bounds__(1024) topk_kernel(PartialView pv, const float *rows_in, int nb, int V, int k,
                                                     int32_t *idx, int idx_offset, float *vals) {
-  extern __shared__ float srow[];
   __shared__ float wv[32];
-  __shared__ int wi[32];
+  __shared__ int wi[32], wt[32];
+  __shared__ int s_win;
+  __shared__ float cval[kVocabSplit * kTopkMax];
+  __shared__ int cidx[kVocabSplit * kTopkMax];
   pdl_trigger();
+  cluster_arrive_relaxed();
   pdl_wait();
-  const int r = blockIdx.x;  // FROM_PARTIALS: r = head * nb + b
+  const int r = blockIdx.y, rank = blockIdx.x, cs = gridDim.x;  // FROM_PARTIALS: r = head * nb + b
   const int head = r / nb, bb = r % nb;
-  for (int j = threadIdx.x * 4; j < V; j += blockDim.x * 4) {
+  int j0, j1;
+  vocab_slice(V, rank, cs, j0, j1);
+  float v[KM];
+  int ix[KM];
+#pragma unroll
+  for (int s = 0; s < KM; ++s) {
+    v[s] = -INFINITY;
+    ix[s] = 0x7fffffff;
+  }
+  for (int j = j0 + threadIdx.x * 4; j < j1; j += blockDim.x * 4) {
     float4 z4;
     if constexpr (FROM_PARTIALS) {
       z4 = sk_get4(pv, head, bb, j);
     } else {
       z4 = *reinterpret_cast<const float4 *>(rows_in + (size_t)r * V + j);
     }
-    *reinterpret_cast<float4 *>(srow + j) = z4;
+    topk_insert<KM>(v, ix, z4.x, j);
+    topk_insert<KM>(v, ix, z4.y, j + 1);
+    topk_insert<KM>(v, ix, z4.z, j + 2);
+    topk_insert<KM>(v, ix, z4.w, j + 3);
   }
-  __syncthreads();
-  for (int kk = 0; kk < k; ++kk) {
-    float bv = -INFINITY;
-    int bi = 0x7fffffff;
-    for (int j = threadIdx.x; j < V; j += blockDim.x) {
-      const float z = srow[j];
-      if (z == z) argmax_merge(bv, bi, z, j);  // skip NaN (taken)
-    }
+  cluster_wait();  // every CTA of the cluster started: DSMEM pushes are safe
+  topk_tournament<KM>(v, ix, k, wv, wi, wt, &s_win, [&](int kk, float val, int id) {
+    st_dsmem_f32(mapa_u32(smem_u32(&cval[rank * kTopkMax + kk]), 0), val);
+    st_dsmem_f32(mapa_u32(smem_u32(&cidx[rank * kTopkMax + kk]), 0), __int_as_float(id));
+  });
+  cluster_sync_all();  // all slices' candidates are in rank 0
+  if (rank != 0) return;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float v2 = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-      argmax_merge(bv, bi, v2, i2);
-    }
-    if ((threadIdx.x & 31) == 0) {
-      wv[threadIdx.x >> 5] = bv;
-      wi[threadIdx.x >> 5] = bi;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) argmax_merge(bv, bi, wv[w], wi[w]);
-      // FROM_PARTIALS: idx[b][head][k]; plain rows: idx[r][k]
-      const size_t o = FROM_PARTIALS ? ((size_t)bb * (gridDim.x / nb) + head) * k + kk : (size_t)r * k + kk;
-      idx[o] = (bi >= 0 && bi < V) ? bi + idx_offset : bi;  // vocabulary-parallel slice -> global id
-      if (vals) vals[o] = bv;
-      if (bi >= 0 && bi < V) srow[bi] = __int_as_float(0x7fc00000);
-    }
-    __syncthreads();
+  for (int s = 0; s < KM; ++s) {
+    v[s] = -INFINITY;
+    ix[s] = 0x7fffffff;
   }
+  if ((int)threadIdx.x < cs * k) {  // one candidate per thread
+    v[0] = cval[(threadIdx.x / k) * kTopkMax + threadIdx.x % k];
+    ix[0] = cidx[(threadIdx.x / k) * kTopkMax + threadIdx.x % k];
+  }
+  topk_tournament<KM>(v, ix, k, wv, wi, wt, &s_win, [&](int kk, float val, int id) {
+    const bool ok = id >= 0 && id < V;
+    // FROM_PARTIALS: idx[b][head][k]; plain rows: idx[r][k]
+    const size_t o = FROM_PARTIALS ? ((size_t)bb * (gridDim.y / nb) + head) * k + kk : (size_t)r * k + kk;
+    idx[o] = ok ? id + idx_offset : id;  // vocabulary-parallel slice -> global id
+    if (vals) vals[o] = val;
+  });
 }
-template <bool FP>
-static cudaError_t topk_attr(size_t smem) {
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(topk_kernel<FP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
-  return cudaSuccess;
+template <bool FP, int KM>
+static cudaError_t topk_go(dim3 grid, cudaStream_t st, const PartialView &pv, const float *rows, int nb, int V, int k,
+                           int32_t *idx, int off, float *vals) {
+  return launch_pdl_cluster(topk_kernel<FP, KM>, dim3(kVocabSplit, grid.x), dim3(1024), 0, st, kVocabSplit, pv, rows,
+                            nb, V, k, idx, off, vals);
 }
 cudaError_t topk_consumer_launch(const PartialView &pv, int nmed, int nb, int V, int k, int32_t *idx, int idx_offset,
                                  float *vals, cudaStream_t st) {
-  const size_t smem = (size_t)V * sizeof(float);
-  cudaError_t e = topk_attr<true>(smem);
-  if (e != cudaSuccess) return e;
-  return launch_pdl(topk_kernel<true>, dim3(nmed * nb), dim3(1024), smem, st, pv, (const float *)nullptr, nb, V, k,
-                    idx, idx_offset, vals);
+  if (k > kTopkMax || V % 4) return cudaErrorInvalidValue;
+  if (k <= 10) return topk_go<true, 10>(dim3(nmed * nb), st, pv, nullptr, nb, V, k, idx, idx_offset, vals);
+  if (k <= 16) return topk_go<true, 16>(dim3(nmed * nb), st, pv, nullptr, nb, V, k, idx, idx_offset, vals);
+  return topk_go<true, 32>(dim3(nmed * nb), st, pv, nullptr, nb, V, k, idx, idx_offset, vals);
 }
 cudaError_t topk_launch(const float *logits, int rows, int V, int k, int32_t *idx, cudaStream_t st) {
-  const size_t smem = (size_t)V * sizeof(float);
-  cudaError_t e = topk_attr<false>(smem);
-  if (e != cudaSuccess) return e;
+  if (k > kTopkMax || V % 4) return cudaErrorInvalidValue;
   PartialView pv{};
-  return launch_pdl(topk_kernel<false>, dim3(rows), dim3(1024), smem, st, pv, logits, rows, V, k, idx, 0,
-                    (float *)nullptr);
+  if (k <= 10) return topk_go<false, 10>(dim3(rows), st, pv, logits, rows, V, k, idx, 0, nullptr);
+  if (k <= 16) return topk_go<false, 16>(dim3(rows), st, pv, logits, rows, V, k, idx, 0, nullptr);
+  return topk_go<false, 32>(dim3(rows), st, pv, logits, rows, V, k, idx, 0, nullptr);
 }
 
 // ------------------------------------------------------------------ Medusa head ResBlock consumer
@@ -540,8 +667,12 @@ void epilogue_preload() {  // force-load (see gemm_preload)
   cudaFuncGetAttributes(&fa, silu_consumer_kernel);
   cudaFuncGetAttributes(&fa, logits_kernel<true>);
   cudaFuncGetAttributes(&fa, logits_kernel<false>);
-  cudaFuncGetAttributes(&fa, topk_kernel<true>);
-  cudaFuncGetAttributes(&fa, topk_kernel<false>);
+  cudaFuncGetAttributes(&fa, topk_kernel<true, 10>);
+  cudaFuncGetAttributes(&fa, topk_kernel<false, 10>);
+  cudaFuncGetAttributes(&fa, topk_kernel<true, 16>);
+  cudaFuncGetAttributes(&fa, topk_kernel<false, 16>);
+  cudaFuncGetAttributes(&fa, topk_kernel<true, 32>);
+  cudaFuncGetAttributes(&fa, topk_kernel<false, 32>);
   cudaFuncGetAttributes(&fa, heads_r_kernel);
   cudaFuncGetAttributes(&fa, plain_kernel);
 }
