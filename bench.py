@@ -165,6 +165,18 @@ def step_bytes(cfg: dict, N: int, Lc: float, b: int = 1, n_medusa: int = N_MEDUS
     return w_layers + w_lm + w_heads + kv_read + kv_write + compact
 
 
+def step_flops(cfg: dict, tree_depths, Lc: float, b: int = 1, n_medusa: int = N_MEDUSA) -> float:
+    """2 b N (P_layers + P_lm) + 2 b P_heads + 4 H hd L b (N Lc + sum_n (depth_n + 1)),
+    the tree part of attention counted sparse (each node sees its ancestors and itself)."""
+    d, H, Hkv, hd, F, V, L = (cfg[k] for k in ("d_model", "n_heads", "n_kv_heads", "head_dim", "d_ffn", "vocab",
+                                                "n_layers"))
+    N = len(tree_depths)
+    p_layers = L * ((H + 2 * Hkv) * hd * d + d * H * hd + 3 * F * d)
+    p_heads = n_medusa * (d * d + V * d)
+    return (2 * b * N * (p_layers + V * d) + 2 * b * p_heads
+            + 4 * H * hd * L * b * (N * Lc + sum(int(x) + 1 for x in tree_depths)))
+
+
 def attn_bytes(cfg: dict, N: int, Lc: float, b: int = 1) -> float:
     """K1 per step (all layers): K/V of [0, Lc) + tree slots, read once; Q in, O out."""
     H, Hkv, hd, L = (cfg[k] for k in ("n_heads", "n_kv_heads", "head_dim", "n_layers"))
@@ -184,6 +196,10 @@ WORKLOADS = {
                desc="C3: Vicuna-13B-shaped + 4 Medusa heads, V64 tree, bs=1, mid-conversation of an 8-turn "
                     "MT-Bench-length chat (KV bounded to 2304 = sum of turns), typical acceptance T=0.7 eps=0.09 "
                     "alpha=0.3"),
+    "c4v64": dict(model="llama70b", n_medusa=4, tree="V64", batch=10, x=416, mode="greedy", tp=True,
+                  desc="C4 with the paper's default tree: Llama-2-70B-shaped (GQA 64/8) + 4 Medusa heads, V64 tree "
+                       "(64 nodes), bs=10 ragged prompts of 32-160 tokens, KV bounded to 416 (+64), greedy; M = 640 "
+                       "token rows per verify (tensor-bound); tensor parallel over the N GPUs"),
     "c4": dict(model="llama70b", n_medusa=3, tree="TINY16", batch=10, x=416, mode="greedy", tp=True,
                desc="C4: Llama-2-70B-shaped (GQA 64/8) + 3 Medusa heads, 16-node tree, bs=10 ragged prompts of "
                     "32-160 tokens + 256 new, KV bounded to 416 (+16), greedy; tensor parallel over the N GPUs (TP1 = one "
@@ -357,6 +373,13 @@ def run_ours(args, world, rank, local) -> dict | None:
     lc_mean = float((L0 + L1).mean() / 2)
     sb = step_bytes(cfg, N, lc_mean, b=b, n_medusa=wl["n_medusa"], tau=tau) / tp  # per GPU
     ms_step = ms_max / args.steps
+    # the binding roofline of the whole step: max(bytes / HBM, flops / sustained bf16 tensor peak)
+    sf = step_flops(cfg, tree.query()["node_depth"], lc_mean, b=b, n_medusa=wl["n_medusa"]) / tp
+    t_hbm, t_tc = sb / pk["hbm"] / 1e6, sf / (pk["bf16_sus"] or pk["bf16"]) / 1e9  # ms
+    step_roof = {"bound": "hbm" if t_hbm >= t_tc else "tensor", "alg_bytes": sb, "alg_flops": sf,
+                 "roofline_ms": round(max(t_hbm, t_tc), 4), "hbm_ms": round(t_hbm, 4), "tensor_ms": round(t_tc, 4),
+                 "frac": round(max(t_hbm, t_tc) / ms_step, 4),
+                 "tensor_peak": "bf16 sustained (MEASURED_PEAKS.json)"}
     res = {
         "metric": METRIC, "value": round(value, 3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
@@ -377,8 +400,7 @@ def run_ours(args, world, rank, local) -> dict | None:
                      "share_of_profiled_step": round(gemm_ms / step_prof_ms, 4),
                      "alg_bytes_per_step": gemm_bytes,
                      "peak_source": pk["src"], "timing": "CUDA events around each launch inside the step graph"},
-        "step_roofline": {"bound": "hbm", "alg_bytes": sb, "roofline_ms": round(sb / pk["hbm"] / 1e6, 4),
-                          "frac": round(sb / pk["hbm"] / 1e6 / ms_step, 4)},
+        "step_roofline": step_roof,
         "tree_attn_in_step": {"launches_per_step": a_n, "ms_per_step": round(attn_ms, 4), "lc": lc_prof,
                               "alg_bytes": attn_bytes(cfg, N, lc_prof, b=b),
                               "achieved_gbs": round(attn_bytes(cfg, N, lc_prof, b=b) / (attn_ms / 1e3) / 1e9, 1)},
