@@ -124,6 +124,56 @@ cudaError_t resid_norm_launch(const PartialView *pv, float *x, const bf16 *g, bf
                             eps, hp, rs_out);
 }
 
+// Split variant (deferred norm): no cluster exchange -- each CTA's slice sum of squares goes to
+// ss[m][slice] and the next consumer finishes rs (rs_of).  Same arithmetic, same order.
+int resid_norm_slices(int d) { return (d + kNormCols - 1) / kNormCols; }
+__global__ void __launch_bounds__(kNormThreads) resid_norm_split_kernel(PartialView pv, int has_pv, float *x,
+                                                                        const bf16 *g, bf16 *h, int d, int hp,
+                                                                        float *ss_out) {
+  SM_GT_BEGIN();
+  __shared__ float red[kNormThreads / 32];
+  pdl_trigger();
+  pdl_wait();
+  SM_GT_WAITED();
+  const int m = blockIdx.y, rank = blockIdx.x, cs = gridDim.x;
+  const int i = rank * kNormCols + threadIdx.x * 4;
+  float *xr = x + (size_t)m * d;
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (i < d) {
+    float4 ys[16];
+    SkRef ref{};
+    if (has_pv && pv.planes <= 1) {
+      ref = sk_ref(pv, 0, m, i);
+      sk_load<16>(ref, ys);
+    }
+    a = *reinterpret_cast<const float4 *>(xr + i);
+    if (has_pv) {
+      const float4 y = pv.planes <= 1 ? sk_reduce<16>(ref, ys) : sk_get4(pv, 0, m, i);  // R5/R7
+      a.x += y.x;
+      a.y += y.y;
+      a.z += y.z;
+      a.w += y.w;
+      *reinterpret_cast<float4 *>(xr + i) = a;
+    }
+    const __nv_bfloat162 g01 = *reinterpret_cast<const __nv_bfloat162 *>(g + i);
+    const __nv_bfloat162 g23 = *reinterpret_cast<const __nv_bfloat162 *>(g + i + 2);
+    store_act4(h, hp, m, d, i, a.x * __low2float(g01), a.y * __high2float(g01), a.z * __low2float(g23),
+               a.w * __high2float(g23));
+  }
+  const float ss = block_sum<kNormThreads>(a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w, red);
+  if (threadIdx.x == 0) ss_out[(size_t)m * cs + rank] = ss;
+  if (threadIdx.x == 0) SM_GT_END(1);
+}
+cudaError_t resid_norm_split_launch(const PartialView *pv, float *x, const bf16 *g, bf16 *h, int M, int d, int hp,
+                                    float *ss, cudaStream_t st) {
+  const int cs = resid_norm_slices(d);
+  if (d % 4) return cudaErrorInvalidValue;
+  PartialView v{};
+  if (pv) v = *pv;
+  return launch_pdl(resid_norm_split_kernel, dim3(cs, M), dim3(kNormThreads), 0, st, v, pv ? 1 : 0, x, g, h, d, hp,
+                    ss);
+}
+
 // Tensor-parallel variant (a7): the residual all-reduce fused in.  Each rank reduces
 // its own split-K partials of a row slice, publishes the fp32 slice in its symmetric
 // buffer, raises a per-CTA epoch flag in every peer, waits for the peers' flags of
@@ -221,7 +271,7 @@ cudaError_t resid_norm_tp_launch(const PartialView &pv, float *x, const bf16 *g,
 template <bool F32>
 __global__ void __launch_bounds__(256) qkv_consumer_kernel(PartialView pv, RowCtx rc, int H, int Hkv, int hd,
                                                            const float2 *rope, void *q_, void *kc_, void *vc_, int cap,
-                                                           const float *rs) {
+                                                           RsArgs rs) {
   SM_GT_BEGIN();
   using T = typename std::conditional<F32, float, bf16>::type;
   T *q = static_cast<T *>(q_), *kc = static_cast<T *>(kc_), *vc = static_cast<T *>(vc_);
@@ -247,7 +297,7 @@ __global__ void __launch_bounds__(256) qkv_consumer_kernel(PartialView pv, RowCt
     a = sk_reduce<8>(ra, xa);
     b = sk_reduce<8>(rb, xb);
   }
-  const float r = rs ? rs[m] : 1.0f;  // deferred RMSNorm scale of the input row (R2)
+  const float r = rs_of(rs, m);  // deferred RMSNorm scale of the input row (R2)
   float x0[4] = {a.x * r, a.y * r, a.z * r, a.w * r}, x1[4] = {b.x * r, b.y * r, b.z * r, b.w * r};
   const int sl = m / rc.Nq, node = m % rc.Nq;
   const int seq = rc.seq_base + sl;
@@ -286,7 +336,7 @@ __global__ void __launch_bounds__(256) qkv_consumer_kernel(PartialView pv, RowCt
   if (threadIdx.x == 0) SM_GT_END(2);
 }
 cudaError_t qkv_consumer_launch(const PartialView &pv, RowCtx rc, int H, int Hkv, int hd, const float2 *rope, void *q,
-                                void *kcache, void *vcache, int cap, const float *rs, cudaStream_t st) {
+                                void *kcache, void *vcache, int cap, RsArgs rs, cudaStream_t st) {
   const int work = (H + 2 * Hkv) * (hd / 8);
   const int nt = g_consumer_threads;
   const dim3 grid((work + nt - 1) / nt, rc.M);
@@ -299,7 +349,7 @@ cudaError_t qkv_consumer_launch(const PartialView &pv, RowCtx rc, int H, int Hkv
 
 // ------------------------------------------------------------------ SiLU(gate) * up
 // fused weight rows: tile t = [gate 64t..64t+63 | up 64t..64t+63]
-__global__ void __launch_bounds__(256) silu_consumer_kernel(PartialView pv, int F, bf16 *act, const float *rs) {
+__global__ void __launch_bounds__(256) silu_consumer_kernel(PartialView pv, int F, bf16 *act, RsArgs rs) {
   SM_GT_BEGIN();
   pdl_trigger();
   pdl_wait();
@@ -320,7 +370,7 @@ __global__ void __launch_bounds__(256) silu_consumer_kernel(PartialView pv, int 
     g = sk_reduce<8>(rg, xg);
     u = sk_reduce<8>(ru, xu);
   }
-  const float r = rs ? rs[m] : 1.0f;  // deferred RMSNorm scale (R2)
+  const float r = rs_of(rs, m);  // deferred RMSNorm scale (R2)
   const float gg[4] = {g.x * r, g.y * r, g.z * r, g.w * r}, uu[4] = {u.x * r, u.y * r, u.z * r, u.w * r};
   float o[4];
 #pragma unroll
@@ -328,7 +378,7 @@ __global__ void __launch_bounds__(256) silu_consumer_kernel(PartialView pv, int 
   store_act4(act, pv.planes, m, F, f, o[0], o[1], o[2], o[3]);
   if (threadIdx.x == 0) SM_GT_END(3);
 }
-cudaError_t silu_consumer_launch(const PartialView &pv, int F, bf16 *act, const float *rs, cudaStream_t st) {
+cudaError_t silu_consumer_launch(const PartialView &pv, int F, bf16 *act, RsArgs rs, cudaStream_t st) {
   const int nt = g_consumer_threads;
   return launch_pdl(silu_consumer_kernel, dim3((F / 4 + nt - 1) / nt, pv.M), dim3(nt), 0, st, pv, F, act, rs);
 }
@@ -662,6 +712,7 @@ void epilogue_preload() {  // force-load (see gemm_preload)
   cudaFuncGetAttributes(&fa, embed_kernel);
   cudaFuncGetAttributes(&fa, resid_norm_kernel);
   cudaFuncGetAttributes(&fa, resid_norm_tp_kernel);
+  cudaFuncGetAttributes(&fa, resid_norm_split_kernel);
   cudaFuncGetAttributes(&fa, qkv_consumer_kernel<false>);
   cudaFuncGetAttributes(&fa, qkv_consumer_kernel<true>);
   cudaFuncGetAttributes(&fa, silu_consumer_kernel);

@@ -257,6 +257,23 @@ struct EpiArgs {
   int *done_cnt;             // tiles fixed up in this launch (kEpiResid), reset by the last
 };
 
+// Deferred RMSNorm scale of a GEMM's input rows (rounding contract R2): either precomputed
+// (rs[m]: TP / fused paths) or from the per-slice sums of squares the split residual+norm
+// kernel wrote (ss[m][cs], summed in slice order -- the cluster kernel's order).
+struct RsArgs {
+  const float *rs;
+  const float *ss;
+  int cs, d;
+  float eps;
+};
+__device__ inline float rs_of(const RsArgs &a, int m) {
+  if (a.rs) return a.rs[m];
+  if (!a.ss) return 1.0f;
+  float s = 0.f;
+  for (int q = 0; q < a.cs; ++q) s += a.ss[(size_t)m * a.cs + q];
+  return 1.0f / sqrtf(s / (float)a.d + a.eps);
+}
+
 struct GemmArgs {
   CUtensorMap tmW[kMaxGemmBatch];  // weight [N][K] bf16, box 64(k) x 128(rows), SWIZZLE_128B
   CUtensorMap tmX[kMaxGemmBatch];  // activation [rows][K] bf16, box 64(k) x 16(rows), SWIZZLE_128B
@@ -331,11 +348,16 @@ cudaError_t resid_norm_launch(const PartialView *pv, float *x, const bf16 *g, bf
                               int hp, float *rs_out, cudaStream_t st);
 // q/k/v = y; RoPE(q, k) at pos Lc + depth; q -> q[m][H][hd], k/v -> cache slot Lc + node   (R3)
 // pv.planes == 3 (fp32 parity mode): q and the caches are fp32, else bf16.
-// rs (nullable): per-row deferred RMSNorm scale multiplied into y first.
 cudaError_t qkv_consumer_launch(const PartialView &pv, RowCtx rc, int H, int Hkv, int hd, const float2 *rope, void *q,
-                                void *kcache, void *vcache, int cap, const float *rs, cudaStream_t st);
+                                void *kcache, void *vcache, int cap, RsArgs rs, cudaStream_t st);
 // act[m][f] = bf16(SiLU(gate) * up), gate/up interleaved per 64 rows    (R6)
-cudaError_t silu_consumer_launch(const PartialView &pv, int F, bf16 *act, const float *rs, cudaStream_t st);
+cudaError_t silu_consumer_launch(const PartialView &pv, int F, bf16 *act, RsArgs rs, cudaStream_t st);
+// Residual + deferred RMSNorm without the cluster exchange: one CTA per (row, 1024-column
+// slice) adds the partials into x, writes h = bf16(x * g) and the slice's sum of squares
+// ss[m][slice]; the next GEMM's consumer forms rs from them (rs_of).
+cudaError_t resid_norm_split_launch(const PartialView *pv, float *x, const bf16 *g, bf16 *h, int M, int d, int hp,
+                                    float *ss, cudaStream_t st);
+int resid_norm_slices(int d);
 // LM rows: z = y (fp32, optional copy), argmax (lowest index on ties) and the
 // single-pass typical statistics (m, s, t) of z * inv_temp    (R9)
 cudaError_t logits_consumer_launch(const PartialView &pv, float inv_temp, float *z_out, int32_t *argmax, float *stats,

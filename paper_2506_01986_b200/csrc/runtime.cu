@@ -409,6 +409,7 @@ struct sm_model {
   // workspace
   float *x = nullptr, *part = nullptr, *z = nullptr, *stats = nullptr;
   float *rs = nullptr;  // [R] deferred RMSNorm scale of the current GEMM input rows (R2)
+  RsArgs rsa{};         // how the next consumer obtains it (see resid_norm)
   // fused tile epilogues (GemmArgs.epi): bf16, tp = 1, hd = 128, d % 128 == 0
   bool fused = false;
   int fuse_mask = 0;
@@ -1108,13 +1109,20 @@ static int g_ablate = 0;
 // x += y (all-reduced across ranks under TP); deferred (per-layer norms, R2):
 // h = bf16(x * g) and m->rs = 1/sqrt(mean(x^2) + eps) for the next GEMM's consumer;
 // else (final norm, R8) h = bf16(rms(x) * g).
+// The deferred scale reaches the next consumer as m->rsa: from the split kernel's per-slice sums
+// of squares (single GPU, default), or precomputed in m->rs (TP exchange, fused epilogues).
 static sm_status resid_norm(sm_model *m, const PartialView *pv, const bf16 *g, bf16 *h, int M, cudaStream_t st,
                             bool deferred) {
   float *rs = deferred ? m->rs : nullptr;
   if (m->tp > 1 && pv) {
     CK(resid_norm_tp_launch(*pv, m->x, g, h, M, m->d, m->cfg.rms_eps, tp_next(m), rs, st));
+    m->rsa = RsArgs{m->rs, nullptr, 0, m->d, m->cfg.rms_eps};
+  } else if (deferred && !m->fused) {
+    CK(resid_norm_split_launch(pv, m->x, g, h, M, m->d, m->P, m->ss, st));
+    m->rsa = RsArgs{nullptr, m->ss, resid_norm_slices(m->d), m->d, m->cfg.rms_eps};
   } else {
     CK(resid_norm_launch(pv, m->x, g, h, M, m->d, m->cfg.rms_eps, m->P, rs, st));
+    m->rsa = RsArgs{m->rs, nullptr, 0, m->d, m->cfg.rms_eps};
   }
   return SM_OK;
 }
@@ -1173,7 +1181,7 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
     }
     // RoPE, q -> m->q, k/v -> cache slots Lc + node (R3)
     if (KEEP(2) && !fq) {
-      CK(qkv_consumer_launch(pv, rc, m->H, m->Hkv, m->hd, m->rope, m->q, kc, vc, kv->cap, m->rs, st));
+      CK(qkv_consumer_launch(pv, rc, m->H, m->Hkv, m->hd, m->rope, m->q, kc, vc, kv->cap, m->rsa, st));
       ++nl;
     }
     AttnArgs aa;
@@ -1228,7 +1236,7 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
     } else {
       CKS(run_gemm(m->g_gu[l], M, 0, m->ws, m->ws_floats, st, nl, &pv, m->P));
       if (KEEP(2)) {
-        CK(silu_consumer_launch(pv, m->F, m->act, m->rs, st));  // act = bf16(SiLU(rs g) * rs u) (R6)
+        CK(silu_consumer_launch(pv, m->F, m->act, m->rsa, st));  // act = bf16(SiLU(rs g) * rs u) (R6)
         ++nl;
       }
     }
