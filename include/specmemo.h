@@ -230,6 +230,17 @@ sm_status sm_kv_lengths_device(const sm_kv *kv, int32_t **d_len);
 sm_status sm_kv_lengths(const sm_kv *kv, int32_t *h_len);
 void sm_kv_destroy(sm_kv *kv);
 
+/* Pad batching (the paper's batched decoding), a comparison mode
+ * to the default ragged lengths: every step all sequences' caches advance by the batch's
+ * longest acceptance (tau_max); a sequence that accepted fewer tokens leaves pad slots, which
+ * attention masks (-inf); RoPE positions count only real tokens ("positional embeddings
+ * continue from the latest sequence length").  Per-sequence results equal the ragged
+ * mode's up to summation order; the cost is KV slots (and attention over them).  Call before
+ * the first step (after prefill is fine: the next step aligns the lengths with pads); single
+ * GPU only.  sm_kv_lengths then reports cache slots, sm_kv_positions the token counts.      */
+sm_status sm_kv_set_pad_mode(sm_kv *kv, int on);
+sm_status sm_kv_positions(const sm_kv *kv, int32_t *h_pos);
+
 /* Prefill one turn of n tokens of sequence `seq` (causal forward at positions
  * [Lc, Lc+n)), then set the pending root (argmax) and the heads' top-k
  * at the last token.  A pending root of a previous turn is dropped (Q15).

@@ -449,6 +449,16 @@ class KVCache:
         return mem.view(c["n_layers"], 2, self.batch, c["n_kv_heads"] // self.model.tp_size,
                         self.x + self.tree.N, c["head_dim"])
 
+    def set_pad_mode(self, on: bool = True) -> None:
+        """Pad batching (f4): uniform cache advance, pads masked (include/specmemo.h)."""
+        _check(lib().sm_kv_set_pad_mode(self._h, ctypes.c_int(1 if on else 0)))
+
+    def positions(self) -> np.ndarray:
+        """Tokens committed per sequence (= lengths() in the ragged mode)."""
+        out = np.zeros(self.batch, np.int32)
+        _check(lib().sm_kv_positions(self._h, out.ctypes.data_as(ctypes.c_void_p)))
+        return out
+
     def lengths(self) -> np.ndarray:
         out = np.zeros(self.batch, np.int32)
         _check(lib().sm_kv_lengths(self._h, out.ctypes.data_as(ctypes.c_void_p)))

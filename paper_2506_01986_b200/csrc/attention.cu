@@ -159,6 +159,22 @@ __global__ void __launch_bounds__(128) tree_attn_kernel(const __grid_constant__ 
           mma_bf16_16816(sc[2 * jp + 1], qf[kc], b2, b3);
         }
       }
+      if (a.pad && p0 < Lc) {  // pad batching (f4): masked cache slots of this sequence's prefix
+        const uint32_t *pw = a.pad + (size_t)seq * a.pad_words + (p0 >> 5);
+        const uint64_t pm = (uint64_t)pw[0] | ((uint64_t)pw[1] << 32);
+        if (pm) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              if ((pm >> (8 * j + 2 * t + e)) & 1ull) {
+                sc[j][e] = -INFINITY;
+                sc[j][2 + e] = -INFINITY;
+              }
+            }
+          }
+        }
+      }
       // mask: keys >= Lc need the ancestor bit, keys >= T / tail are invisible
       if (p0 + 64 > Lc) {
 #pragma unroll

@@ -19,7 +19,8 @@ constexpr int kF32Threads = 128;
 __global__ void __launch_bounds__(kF32Threads) tree_attn_f32_kernel(const float *q, const float *k, const float *v,
                                                                     const int32_t *len, const uint64_t *anc, int Nq,
                                                                     int H, int Hkv, int hd, int cap, int seq_base,
-                                                                    float scale, bf16 *out) {
+                                                                    const uint32_t *pad, int pad_words, float scale,
+                                                                    bf16 *out) {
   extern __shared__ float f32_smem[];
   __shared__ float red[kF32Threads / 32];
   pdl_trigger();
@@ -35,7 +36,11 @@ __global__ void __launch_bounds__(kF32Threads) tree_attn_f32_kernel(const float 
   __syncthreads();
   const uint64_t *an = anc + (size_t)n * kAncWords;
   const int nk = Lc + Nq;
-  auto visible = [&](int j) { return j < Lc || ((an[(j - Lc) >> 6] >> ((j - Lc) & 63)) & 1ull); };
+  const uint32_t *pw = pad ? pad + (size_t)seq * pad_words : nullptr;  // pad batching (f4)
+  auto visible = [&](int j) {
+    if (j < Lc) return !(pw && ((pw[j >> 5] >> (j & 31)) & 1u));
+    return ((an[(j - Lc) >> 6] >> ((j - Lc) & 63)) & 1ull) != 0;
+  };
   float mx = -FLT_MAX;
   for (int j = tid; j < nk; j += kF32Threads) {
     float s = -FLT_MAX;
@@ -83,7 +88,7 @@ __global__ void __launch_bounds__(kF32Threads) tree_attn_f32_kernel(const float 
 
 cudaError_t attention_f32_launch(const float *q, const float *k, const float *v, const int32_t *len,
                                  const uint64_t *anc, int Nq, int H, int Hkv, int hd, int cap, int nseq, int seq_base,
-                                 bf16 *out, cudaStream_t st) {
+                                 const uint32_t *pad, int pad_words, bf16 *out, cudaStream_t st) {
   const size_t smem = (size_t)(hd + cap) * sizeof(float);
   static size_t attr = 48 * 1024;
   if (smem > attr) {
@@ -94,7 +99,7 @@ cudaError_t attention_f32_launch(const float *q, const float *k, const float *v,
   }
   const float scale = (float)(1.0 / std::sqrt((double)hd));
   return launch_pdl(tree_attn_f32_kernel, dim3(nseq * Nq, H), dim3(kF32Threads), smem, st, q, k, v, len, anc, Nq, H,
-                    Hkv, hd, cap, seq_base, scale, out);
+                    Hkv, hd, cap, seq_base, pad, pad_words, scale, out);
 }
 
 void attention_f32_preload() {

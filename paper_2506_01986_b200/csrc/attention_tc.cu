@@ -302,6 +302,14 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
       tc_fence_before();
       mbar_arrive(&s_free[sb]);
       const int p0 = key0 + i * KEYS;
+      if (a.pad && p0 < Lc) {  // pad batching (f4): masked cache slots of this sequence's prefix
+        const uint32_t *pw = a.pad + (size_t)seq * a.pad_words + (p0 >> 5);
+        const uint64_t pm = (uint64_t)pw[0] | ((uint64_t)pw[1] << 32);
+        if (pm) {
+#pragma unroll
+          for (int j = 0; j < 64; ++j) y[j] = ((pm >> j) & 1ull) ? -INFINITY : y[j];
+        }
+      }
       if (p0 + KEYS > Lc) {  // tile reaches past the prefix: visibility bitmask of its 64 keys (Eq. 2)
         const int off = p0 - Lc;  // tree slot of key 0 (may be negative)
         auto word = [&](int q) { return q == 0 ? anc0 : q == 1 ? anc1 : q == 2 ? anc2 : q == 3 ? anc3 : 0ull; };

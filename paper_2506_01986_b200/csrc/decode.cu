@@ -24,7 +24,7 @@ __global__ void propose_kernel(TreeDev t, const int32_t *root, const int32_t *to
     tok = topk[((size_t)bb * nmed + (t.depth[n] - 1)) * K + t.rank[n]];
   }
   tree_tok[(size_t)bb * t.N + n] = tok;
-  if (pos) pos[(size_t)bb * t.N + n] = len[bb] + t.depth[n];
+  if (pos) pos[(size_t)bb * t.N + n] = len[bb] + t.depth[n];  // P:255 (len = the position base passed in)
 }
 cudaError_t propose_launch(TreeDev t, const int32_t *root, const int32_t *topk, int K, int nmed, int b,
                            int32_t *tree_tok, int32_t *pos, const int32_t *len, cudaStream_t st) {
@@ -194,7 +194,7 @@ __global__ void commit_kernel(int32_t *len, const int32_t *n_emit, int32_t *root
   bf16 *dst = head_in + (size_t)bb * d;
   for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = src[i];
   if (threadIdx.x == 0) {
-    len[bb] += ne;
+    if (len) len[bb] += ne;
     root[bb] = root_next[bb];
     if (emitted_total) emitted_total[bb] += ne;
   }
@@ -206,13 +206,59 @@ cudaError_t commit_launch(int b, int32_t *len, const int32_t *n_emit, int32_t *r
                     emitted_total);
 }
 
-__global__ void advance_len_kernel(int32_t *len, int seq, int n) {
+__global__ void advance_len_kernel(int32_t *len, int seq, int n, int32_t *pos_len) {
   pdl_trigger();
   pdl_wait();
   len[seq] += n;
+  if (pos_len) pos_len[seq] += n;
 }
-cudaError_t advance_len_launch(int32_t *len, int seq, int n, cudaStream_t st) {
-  return launch_pdl(advance_len_kernel, dim3(1), dim3(1), 0, st, len, seq, n);
+cudaError_t advance_len_launch(int32_t *len, int seq, int n, int32_t *pos_len, cudaStream_t st) {
+  return launch_pdl(advance_len_kernel, dim3(1), dim3(1), 0, st, len, seq, n, pos_len);
+}
+
+// ------------------------------------------------------------------ pad batching (f4)
+SM_DEV void pad_mark(uint32_t *row, int s0, int s1) {  // slots [s0, s1) -> pad (one thread)
+  for (int s = s0; s < s1; ++s) row[s >> 5] |= 1u << (s & 31);
+}
+__global__ void pad_align_kernel(int b, int32_t *len, uint32_t *pad, int pad_words) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ int mx;
+  if (threadIdx.x == 0) {
+    int m = 0;
+    for (int i = 0; i < b; ++i) m = max(m, len[i]);
+    mx = m;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < b; i += blockDim.x) {
+    pad_mark(pad + (size_t)i * pad_words, len[i], mx);
+    len[i] = mx;
+  }
+}
+cudaError_t pad_align_launch(int b, int32_t *len, uint32_t *pad, int pad_words, cudaStream_t st) {
+  return launch_pdl(pad_align_kernel, dim3(1), dim3(32), 0, st, b, len, pad, pad_words);
+}
+__global__ void pad_commit_kernel(int b, int32_t *len, int32_t *pos_len, const int32_t *n_emit, uint32_t *pad,
+                                  int pad_words) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ int A;
+  if (threadIdx.x == 0) {
+    int m = 0;
+    for (int i = 0; i < b; ++i) m = max(m, n_emit[i]);
+    A = m;  // the batch's longest acceptance: every sequence's cache advances by it
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < b; i += blockDim.x) {
+    const int ne = max(0, n_emit[i]);
+    pad_mark(pad + (size_t)i * pad_words, len[i] + ne, len[i] + A);
+    len[i] += A;
+    pos_len[i] += ne;
+  }
+}
+cudaError_t pad_commit_launch(int b, int32_t *len, int32_t *pos_len, const int32_t *n_emit, uint32_t *pad,
+                              int pad_words, cudaStream_t st) {
+  return launch_pdl(pad_commit_kernel, dim3(1), dim3(32), 0, st, b, len, pos_len, n_emit, pad, pad_words);
 }
 
 __global__ void set_root_kernel(int32_t *root, int seq, const int32_t *argmax_row, const bf16 *hf_row, int d,
@@ -286,6 +332,8 @@ void decode_preload() {  // force-load (see gemm_preload)
   cudaFuncGetAttributes(&fa, compact_kernel);
   cudaFuncGetAttributes(&fa, commit_kernel);
   cudaFuncGetAttributes(&fa, advance_len_kernel);
+  cudaFuncGetAttributes(&fa, pad_align_kernel);
+  cudaFuncGetAttributes(&fa, pad_commit_kernel);
   cudaFuncGetAttributes(&fa, set_root_kernel);
   cudaFuncGetAttributes(&fa, generate_kernel);
 }

@@ -302,8 +302,8 @@ __global__ void __launch_bounds__(256) qkv_consumer_kernel(PartialView pv, RowCt
   const int sl = m / rc.Nq, node = m % rc.Nq;
   const int seq = rc.seq_base + sl;
   const int Lc = rc.len[seq];
-  if (hh < H + Hkv) {  // rotate-half RoPE at pos = Lc + depth
-    const float2 *cs = rope + (size_t)(Lc + rc.depth[node]) * half + c;
+  if (hh < H + Hkv) {  // rotate-half RoPE at pos = Lc + depth (pad batching: token count + depth)
+    const float2 *cs = rope + (size_t)((rc.pos ? rc.pos[seq] : Lc) + rc.depth[node]) * half + c;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const float2 r = cs[e];

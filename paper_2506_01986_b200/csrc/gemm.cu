@@ -121,7 +121,7 @@ SM_DEV void fused_fixup(const GemmArgs &a, int t, int nc, int et) {
         const int seq = e.rc.seq_base + sl;
         const int Lc = e.rc.len[seq];
         if (hh < e.H + e.Hkv) {  // rotate-half RoPE at pos = Lc + depth
-          const float2 cs = e.rope[(size_t)(Lc + e.rc.depth[node]) * 64 + p];
+          const float2 cs = e.rope[(size_t)((e.rc.pos ? e.rc.pos[seq] : Lc) + e.rc.depth[node]) * 64 + p];
           const float o0 = x0 * cs.x - x1 * cs.y;
           const float o1 = x1 * cs.x + x0 * cs.y;
           x0 = o0;

@@ -17,8 +17,9 @@ constexpr int kAncWords = kMaxTreeNodes / 64;
 
 struct RowCtx {                // forward rows m = (seq - seq_base) * Nq + n
   int M, Nq, seq_base;
-  const int32_t *len;          // Lc[seq]
+  const int32_t *len;          // Lc[seq]: cache slot of node 0
   const int32_t *depth;        // [Nq]
+  const int32_t *pos;          // nullable: RoPE position of node 0 (pad batching: tokens, not slots)
 };
 
 // ---------------------------------------------------------------- K2 GEMM split plan
@@ -324,6 +325,8 @@ struct AttnArgs {
   // while the attention CTAs fill the SMs' shared memory); nullable
   const void *l2_pf;
   unsigned long long l2_pf_bytes;
+  const uint32_t *pad;        // nullable: pad-batching bitmap [seq][pad_words] of masked cache slots (f4)
+  int pad_words;
 };
 cudaError_t attention_launch(const AttnArgs &a, int head_dim, cudaStream_t st);
 int attention_row_blocks(int Nq, int G, int head_dim);
@@ -331,7 +334,7 @@ int attention_row_blocks(int Nq, int G, int head_dim);
 // [b][Hkv][cap][hd] at (k, v) for this layer, output as three bf16 planes per row.
 cudaError_t attention_f32_launch(const float *q, const float *k, const float *v, const int32_t *len,
                                  const uint64_t *anc, int Nq, int H, int Hkv, int hd, int cap, int nseq, int seq_base,
-                                 bf16 *out, cudaStream_t st);
+                                 const uint32_t *pad, int pad_words, bf16 *out, cudaStream_t st);
 int attention_nsplit(int units, int head_dim);  // units = row blocks * sequences * kv heads
 void attention_set_splits(int n);               // experiments: force key splits (0 = auto)
 void attention_set_tc(int on);                  // head_dim 128: tcgen05 kernel (1, default) or mma.sync (0)
@@ -387,6 +390,13 @@ struct TreeDev {
 };
 cudaError_t propose_launch(TreeDev t, const int32_t *root, const int32_t *topk, int K, int nmed, int b,
                            int32_t *tree_tok, int32_t *pos, const int32_t *len, cudaStream_t st);
+// ---- pad batching (f4): all sequences advance their cache by the batch's longest
+// acceptance; the shorter ones' extra slots are pads, masked in attention; positions count tokens.
+// pad_align: len[b] = max len (slots [len_b, max) marked pad); pad_commit: len[b] += max n_emit,
+// pos_len[b] += n_emit[b], slots [len + n_emit_b, len + A) marked pad.
+cudaError_t pad_align_launch(int b, int32_t *len, uint32_t *pad, int pad_words, cudaStream_t st);
+cudaError_t pad_commit_launch(int b, int32_t *len, int32_t *pos_len, const int32_t *n_emit, uint32_t *pad,
+                              int pad_words, cudaStream_t st);
 struct AcceptArgs {
   TreeDev t;
   int b, K, V, x_bound;
@@ -409,8 +419,8 @@ cudaError_t compact_launch(bf16 *kv_base, int L, int b, int Hkv, int cap, int hd
                            const int32_t *path, int path_ld, const int32_t *n_emit, cudaStream_t st);
 cudaError_t commit_launch(int b, int32_t *len, const int32_t *n_emit, int32_t *root, const int32_t *root_next,
                           const int32_t *acc_row, const bf16 *hf, int d, bf16 *head_in, int32_t *emitted_total,
-                          cudaStream_t st);
-cudaError_t advance_len_launch(int32_t *len, int seq, int n, cudaStream_t st);
+                          cudaStream_t st);  // len == nullptr: lengths advanced elsewhere (pad batching)
+cudaError_t advance_len_launch(int32_t *len, int seq, int n, int32_t *pos_len, cudaStream_t st);
 cudaError_t set_root_launch(int32_t *root, int seq, const int32_t *argmax_row, const bf16 *hf_row, int d,
                             bf16 *head_in_row, cudaStream_t st);
 cudaError_t generate_bf16_launch(void *dst, size_t numel, uint64_t seed, uint64_t stream_id, uint64_t start, int mode,

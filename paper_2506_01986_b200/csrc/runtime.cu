@@ -984,6 +984,11 @@ struct sm_kv {
   int32_t *len = nullptr, *root = nullptr, *topk = nullptr, *acc_row = nullptr, *root_next = nullptr,
           *emitted = nullptr, *tree_tok = nullptr;
   int att_nsplit_max = 32;
+  // pad batching (f4): uniform cache advance, pad slots masked, positions count tokens
+  int pad_mode = 0;
+  int32_t *pos_len = nullptr;  // [b] tokens committed (the RoPE position base)
+  uint32_t *pad = nullptr;     // [b][pad_words] masked cache slots
+  int pad_words = 0;
   CUtensorMap tmKV;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   int step_launches = 0;
@@ -1035,7 +1040,9 @@ extern "C" sm_status sm_kv_bind(sm_model *m, const sm_tree *tree, int batch, int
       (s = dalloc(&kv->acc_row, batch, "acc_row")) != SM_OK ||
       (s = dalloc(&kv->root_next, batch, "root_next")) != SM_OK ||
       (s = dalloc(&kv->emitted, batch, "emitted")) != SM_OK ||
-      (s = dalloc(&kv->tree_tok, (size_t)batch * kv->N, "tree_tok")) != SM_OK) {
+      (s = dalloc(&kv->tree_tok, (size_t)batch * kv->N, "tree_tok")) != SM_OK ||
+      (s = dalloc(&kv->pos_len, batch, "pos_len")) != SM_OK ||
+      (s = dalloc(&kv->pad, (size_t)batch * (kv->cap / 32 + 2), "pad bitmap")) != SM_OK) {
     sm_kv_destroy(kv);
     return s;
   }
@@ -1051,6 +1058,9 @@ extern "C" sm_status sm_kv_bind(sm_model *m, const sm_tree *tree, int batch, int
   cudaMemset(kv->emitted, 0, batch * 4);
   cudaMemset(kv->acc_row, 0, batch * 4);
   cudaMemset(kv->root_next, 0, batch * 4);
+  kv->pad_words = kv->cap / 32 + 2;
+  cudaMemset(kv->pos_len, 0, batch * 4);
+  cudaMemset(kv->pad, 0, (size_t)batch * kv->pad_words * 4);
   if (cudaDeviceSynchronize() != cudaSuccess) {
     sm_kv_destroy(kv);
     return fail(SM_ERR_CUDA, "kv bind memset");
@@ -1073,6 +1083,8 @@ extern "C" void sm_kv_destroy(sm_kv *kv) {
   cudaFree(kv->root_next);
   cudaFree(kv->emitted);
   cudaFree(kv->tree_tok);
+  cudaFree(kv->pos_len);
+  cudaFree(kv->pad);
   if (kv->t) sm_tree_destroy(kv->t);
   delete kv;
 }
@@ -1080,6 +1092,23 @@ extern "C" void sm_kv_destroy(sm_kv *kv) {
 extern "C" sm_status sm_kv_lengths_device(const sm_kv *kv, int32_t **d_len) {
   if (!kv || !d_len) return fail(SM_ERR_INVALID_ARG, "null");
   *d_len = kv->len;
+  return SM_OK;
+}
+extern "C" sm_status sm_kv_set_pad_mode(sm_kv *kv, int on) {
+  if (!kv) return fail(SM_ERR_INVALID_ARG, "sm_kv_set_pad_mode: null");
+  if (kv->m->tp > 1) return fail(SM_ERR_UNSUPPORTED, "pad batching: single GPU only");
+  CK(cudaDeviceSynchronize());
+  kv->pad_mode = on ? 1 : 0;
+  CK(cudaMemcpy(kv->pos_len, kv->len, kv->b * 4, cudaMemcpyDeviceToDevice));  // positions = tokens so far
+  CK(cudaMemset(kv->pad, 0, (size_t)kv->b * kv->pad_words * 4));
+  for (auto &g : kv->graphs) cudaGraphExecDestroy(g.second);  // the step's kernel sequence changes
+  kv->graphs.clear();
+  return SM_OK;
+}
+extern "C" sm_status sm_kv_positions(const sm_kv *kv, int32_t *h_pos) {
+  if (!kv || !h_pos) return fail(SM_ERR_INVALID_ARG, "null");
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(h_pos, kv->pad_mode ? kv->pos_len : kv->len, kv->b * 4, cudaMemcpyDeviceToHost));
   return SM_OK;
 }
 extern "C" sm_status sm_kv_lengths(const sm_kv *kv, int32_t *h_len) {
@@ -1137,7 +1166,7 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
   const int nsplit = attn_splits(m, nseq, Nq);
   const long long layer_rows = (long long)2 * kv->b * m->Hkv * kv->cap;
   const long long half_rows = (long long)kv->b * m->Hkv * kv->cap;
-  RowCtx rc{M, Nq, seq_base, kv->len, tree.depth};
+  RowCtx rc{M, Nq, seq_base, kv->len, tree.depth, kv->pad_mode ? kv->pos_len : nullptr};
   PartialView pv, pv_down{};
   bool have_down = false;
   g_ablate_gemm = (g_ablate & 4) ? 1 : 0;
@@ -1204,6 +1233,8 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
     aa.seq_base = seq_base;
     aa.nsplit = nsplit;
     aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)m->hd));
+    aa.pad = kv->pad_mode ? kv->pad : nullptr;
+    aa.pad_words = kv->pad_words;
     aa.l2_pf = m->wo[l];  // o_proj weights stream into L2 while attention runs
     aa.l2_pf_bytes = (unsigned long long)d * m->H * m->hd * 2;
     cudaEvent_t ev = nullptr;
@@ -1212,7 +1243,7 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
       if (m->f32)
         CK(attention_f32_launch(reinterpret_cast<const float *>(m->q), reinterpret_cast<const float *>(kc),
                                 reinterpret_cast<const float *>(vc), kv->len, tree.anc, Nq, m->H, m->Hkv, m->hd,
-                                kv->cap, nseq, seq_base, m->attn, st));
+                                kv->cap, nseq, seq_base, aa.pad, kv->pad_words, m->attn, st));
       else
         CK(attention_launch(aa, m->hd, st));
       ++nl;
@@ -1297,7 +1328,7 @@ extern "C" sm_status sm_prefill(sm_model *m, sm_kv *kv, int seq, const int32_t *
   while (done < n) {
     const int P = std::min(std::min(R, kMaxTreeNodes), n - done);  // chain-tree chunks of <= 256 tokens
     CKS(enqueue_forward(m, kv, d_tokens + done, 1, seq, P, chain, st, nl));
-    CK(advance_len_launch(kv->len, seq, P, st));
+    CK(advance_len_launch(kv->len, seq, P, kv->pad_mode ? kv->pos_len : nullptr, st));
     done += P;
     last = P;
   }
@@ -1320,7 +1351,7 @@ extern "C" sm_status sm_prefill(sm_model *m, sm_kv *kv, int seq, const int32_t *
 
 static sm_status enqueue_propose(sm_model *m, sm_kv *kv, int32_t *tree_tok, int32_t *pos, cudaStream_t st, int &nl) {
   CK(propose_launch(kv->t->dev(), kv->root, kv->topk, kv->t->topk, std::max(1, m->nmed), kv->b, tree_tok, pos,
-                    kv->len, st));
+                    kv->pad_mode ? kv->pos_len : kv->len, st));
   ++nl;
   return SM_OK;
 }
@@ -1382,9 +1413,13 @@ static sm_status enqueue_accept(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg
   ++nl;
   CK(compact_launch(kv->base, m->L, kv->b, m->Hkv, kv->cap, m->hdu, kv->len, o->path, kv->t->l + 1, o->n_emit, st));
   ++nl;
-  CK(commit_launch(kv->b, kv->len, o->n_emit, kv->root, kv->root_next, kv->acc_row, m->hf, m->d * m->P, m->head_in,
-                   kv->emitted, st));
+  CK(commit_launch(kv->b, kv->pad_mode ? nullptr : kv->len, o->n_emit, kv->root, kv->root_next, kv->acc_row, m->hf,
+                   m->d * m->P, m->head_in, kv->emitted, st));
   ++nl;
+  if (kv->pad_mode) {  // every cache advances by the batch's longest acceptance; the rest are pads
+    CK(pad_commit_launch(kv->b, kv->len, kv->pos_len, o->n_emit, kv->pad, kv->pad_words, st));
+    ++nl;
+  }
   CKS(enqueue_heads(m, kv, 0, kv->b, st, nl));
   return SM_OK;
 }
@@ -1434,6 +1469,10 @@ extern "C" sm_status sm_accept(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg,
 static sm_status enqueue_step(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, const sm_accept_out *o,
                               cudaStream_t st, int &nl) {
   tp_begin(m);
+  if (kv->pad_mode) {  // uniform cache lengths (after ragged prefills): pad the shorter ones
+    CK(pad_align_launch(kv->b, kv->len, kv->pad, kv->pad_words, st));
+    ++nl;
+  }
   CKS(enqueue_propose(m, kv, kv->tree_tok, nullptr, st, nl));
   CKS(enqueue_verify(m, kv, kv->tree_tok, st, nl));
   CKS(enqueue_accept(m, kv, cfg, o, st, nl));

@@ -3,7 +3,8 @@
 python tools/k1_sweep.py [--quick] > profiles/r01_k1_sweep.txt
 Geometry A = one 7B layer (H = Hkv = 32), geometry B = one 70B TP8 shard (8 q / 1 kv),
 head_dim 128, tree N in {16, 64, 256}, Lc in {512, 4096, 32768}, batch in {1, 8, 32}
-(bounded to <= 8 GB of K/V per set).  Each point: 20 launches captured in a CUDA graph
+(--full: SURVEY's grid N 16..256 x Lc 512..32K x b 1..32, uniform and ragged "~" lengths
+Lc_b spread over [Lc/2, Lc]; bounded to <= 8 GB of K/V per set).  Each point: 20 launches captured in a CUDA graph
 over two alternating buffer sets (> L2), replayed; device time per launch; achieved
 GB/s = algorithmic bytes (K/V of [0, Lc) + tree slots once, Q in, O out) / time."""
 import argparse
@@ -24,21 +25,28 @@ TPEAK = _pk["bf16_tflops"]              # dense bf16 TF/s (burst: one kernel tim
 ap = argparse.ArgumentParser()
 ap.add_argument("--quick", action="store_true")
 ap.add_argument("--tc", type=int, default=1)
+ap.add_argument("--full", action="store_true", help="SURVEY 8.d.1 grid: N 16..256 x Lc 512..32K x b 1..32, "
+                                                     "uniform and ragged lengths")
 a = ap.parse_args()
 sm.set_option("attn_tc", a.tc)
-trees = {16: sm.Tree(synth.SWEEP_TREES[16]), 64: sm.Tree(synth.V64), 256: sm.Tree(synth.SWEEP_TREES[256])}
+trees = {n: (sm.Tree(synth.V64) if n == 64 else sm.Tree(synth.SWEEP_TREES[n])) for n in (16, 32, 64, 128, 256)}
 geoms = [("A 32/32", 32, 32), ("B 8/1", 8, 1)]
 Ns = [16, 64, 256]
 Lcs = [512, 4096, 32768]
 bs = [1, 8, 32]
+RAGGED = [False]
 if a.quick:
     Ns, Lcs, bs = [64], [512, 4096], [1, 8]
+if a.full:
+    Ns, Lcs, bs = [16, 32, 64, 128, 256], [512, 1024, 2048, 4096, 8192, 16384, 32768], [1, 2, 4, 8, 16, 32]
+    RAGGED = [False, True]
 print(f"{'geom':8s} {'b':>3s} {'N':>4s} {'Lc':>6s} {'MB':>8s} {'us':>9s} {'GB/s':>8s} {'TF/s':>7s} {'bound':>6s} "
       f"{'frac':>6s}")
 # flops = 4 H hd sum_b (N Lc + sum_n (depth_n + 1)) (tree part counted sparse);
 # bound = whichever of bytes / HBM peak and flops / tensor peak is larger; frac = that floor / time
 hd = 128
-for gname, H, Hkv in geoms:
+for ragged in RAGGED:
+  for gname, H, Hkv in geoms:
     for b in bs:
         for N in Ns:
             for Lc in Lcs:
@@ -53,7 +61,9 @@ for gname, H, Hkv in geoms:
                     k = torch.randn(b, Hkv, cap, hd, device="cuda").bfloat16()
                     v = torch.randn(b, Hkv, cap, hd, device="cuda").bfloat16()
                     sets.append((q, k, v, torch.empty_like(q)))
-                L = torch.full((b,), Lc, dtype=torch.int32, device="cuda")
+                # ragged: Lc_b spread evenly over [Lc/2, Lc]
+                lens = [Lc // 2 + (Lc - Lc // 2) * i // max(1, b - 1) for i in range(b)] if ragged else [Lc] * b
+                L = torch.tensor(lens, dtype=torch.int32, device="cuda")
                 for i in range(2):
                     q, k, v, o = sets[i]
                     sm.tree_attention(tree, q, k, v, L, H, Hkv, o)
@@ -75,14 +85,15 @@ for gname, H, Hkv in geoms:
                 e1.record()
                 torch.cuda.synchronize()
                 us = e0.elapsed_time(e1) * 1e3 / 60
-                alg = b * Hkv * (Lc + tree.N) * hd * 2 * 2 + 2 * b * tree.N * H * hd * 2
+                alg = sum(Hkv * (lb + tree.N) * hd * 2 * 2 for lb in lens) + 2 * b * tree.N * H * hd * 2
                 dep = tree.query()["node_depth"]
-                flops = 4 * H * hd * b * (tree.N * Lc + int((dep + 1).sum()))
+                flops = sum(4 * H * hd * (tree.N * lb + int((dep + 1).sum())) for lb in lens)
                 gbs = alg / us / 1e3
                 tfs = flops / us / 1e6
                 t_hbm, t_tc = alg / PEAK / 1e3, flops / TPEAK / 1e6  # us
                 bound = "hbm" if t_hbm >= t_tc else "tensor"
-                print(f"{gname:8s} {b:3d} {tree.N:4d} {Lc:6d} {alg / 1e6:8.1f} {us:9.1f} {gbs:8.1f} {tfs:7.1f} {bound:>6s} "
+                tag = gname + ("~" if ragged else "")
+                print(f"{tag:8s} {b:3d} {tree.N:4d} {Lc:6d} {alg / 1e6:8.1f} {us:9.1f} {gbs:8.1f} {tfs:7.1f} {bound:>6s} "
                       f"{max(t_hbm, t_tc) / us:6.3f}", flush=True)
                 del sets, g
                 torch.cuda.empty_cache()
