@@ -526,9 +526,9 @@ static int g_ctas = 0;
 static int g_l2pf = 0;
 static int g_dbg_mode = 0;
 static int g_force_bn = 0;
-// 2-SM MMA (cta_group::2): 0 off; 1 (default) for token tiles of 96..192 rows and for 256-row
-// tiles when there are several (measured faster there, slower at M = 64 and one 256-row tile,
-// DESIGN.md §5.2); 2 for every tile of >= 64 rows (experiments)
+// 2-SM MMA (cta_group::2): 0 off; 1 (default) for token tiles of 96..160 rows and for 256-row
+// tiles when there are several (measured faster there, slower at M = 64 and for one 192- or
+// 256-row tile); 2 for every tile of >= 64 rows (experiments)
 static int g_pair = 1;
 static int g_pre_stages = -1;  // experiments: weight stages issued before griddepcontrol.wait (-1 = ring)  // experiments: fixed token-tile width (0 = gemm_pick_bn)
 static int g_occ = 2;  // GEMM CTAs per SM for BN <= 64 (1..4); grid = 148 * occ
@@ -624,7 +624,10 @@ void gemm_plan(GemmArgs &a, int N, int K, int M, int batch) {
   SplitPlan &p = a.plan;
   p.bn = g_force_bn > 0 ? g_force_bn : gemm_pick_bn(M);
   const int ttiles = (M + p.bn - 1) / p.bn;
-  const bool pair_ok = (g_pair == 1 && p.bn >= 96 && (p.bn < 256 || ttiles > 1)) || (g_pair == 2 && p.bn >= 64);
+  // measured (tools/gemm_pair.py, tools/gemm_m128.py): the pair wins for 96..160-row tiles and for several
+  // 256-row tiles, loses for 64-row tiles, a single 192- or 256-row tile
+  const bool pair_ok = (g_pair == 1 && ((p.bn >= 96 && p.bn <= 160) || (p.bn == 256 && ttiles > 1))) ||
+                       (g_pair == 2 && p.bn >= 64);
   p.pair = (!a.no_pair && batch == 1 && pair_ok) ? 2 : 1;
   p.m_tiles = (N + 128 * p.pair - 1) / (128 * p.pair);
   p.token_tiles = (M + p.bn - 1) / p.bn;
