@@ -24,6 +24,15 @@ SM_DEV uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_sha
 // outputs and all writes must come after), and let the next kernel launch.
 SM_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 SM_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// Kernels that change step-static state (Lc, positions, pad bitmaps) trigger their dependents
+// only after those writes are fenced: kernels downstream read Lc before their own
+// griddepcontrol.wait, and every trigger-at-entry kernel in between would otherwise let them
+// start while the writer still runs.  Every thread of the block must reach this call.
+SM_DEV void pdl_trigger_after_writes() {
+  __threadfence();
+  __syncthreads();
+  pdl_trigger();
+}
 
 SM_DEV float warp_sum(float v) {
 #pragma unroll

@@ -185,19 +185,20 @@ cudaError_t compact_launch(bf16 *kv_base, int L, int b, int Hkv, int cap, int hd
 // ------------------------------------------------------------------ commit
 __global__ void commit_kernel(int32_t *len, const int32_t *n_emit, int32_t *root, const int32_t *root_next,
                               const int32_t *acc_row, const bf16 *hf, int d, bf16 *head_in, int32_t *emitted_total) {
-  pdl_trigger();
   pdl_wait();
   const int bb = blockIdx.x;
   const int ne = n_emit[bb];
-  if (ne <= 0) return;
-  const bf16 *src = hf + (size_t)acc_row[bb] * d;
-  bf16 *dst = head_in + (size_t)bb * d;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = src[i];
-  if (threadIdx.x == 0) {
-    if (len) len[bb] += ne;
-    root[bb] = root_next[bb];
-    if (emitted_total) emitted_total[bb] += ne;
+  if (ne > 0) {
+    const bf16 *src = hf + (size_t)acc_row[bb] * d;
+    bf16 *dst = head_in + (size_t)bb * d;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = src[i];
+    if (threadIdx.x == 0) {
+      if (len) len[bb] += ne;
+      root[bb] = root_next[bb];
+      if (emitted_total) emitted_total[bb] += ne;
+    }
   }
+  pdl_trigger_after_writes();  // Lc changed: see common.cuh
 }
 cudaError_t commit_launch(int b, int32_t *len, const int32_t *n_emit, int32_t *root, const int32_t *root_next,
                           const int32_t *acc_row, const bf16 *hf, int d, bf16 *head_in, int32_t *emitted_total,
@@ -207,10 +208,10 @@ cudaError_t commit_launch(int b, int32_t *len, const int32_t *n_emit, int32_t *r
 }
 
 __global__ void advance_len_kernel(int32_t *len, int seq, int n, int32_t *pos_len) {
-  pdl_trigger();
   pdl_wait();
   len[seq] += n;
   if (pos_len) pos_len[seq] += n;
+  pdl_trigger_after_writes();
 }
 cudaError_t advance_len_launch(int32_t *len, int seq, int n, int32_t *pos_len, cudaStream_t st) {
   return launch_pdl(advance_len_kernel, dim3(1), dim3(1), 0, st, len, seq, n, pos_len);
@@ -221,7 +222,6 @@ SM_DEV void pad_mark(uint32_t *row, int s0, int s1) {  // slots [s0, s1) -> pad 
   for (int s = s0; s < s1; ++s) row[s >> 5] |= 1u << (s & 31);
 }
 __global__ void pad_align_kernel(int b, int32_t *len, uint32_t *pad, int pad_words) {
-  pdl_trigger();
   pdl_wait();
   __shared__ int mx;
   if (threadIdx.x == 0) {
@@ -234,13 +234,13 @@ __global__ void pad_align_kernel(int b, int32_t *len, uint32_t *pad, int pad_wor
     pad_mark(pad + (size_t)i * pad_words, len[i], mx);
     len[i] = mx;
   }
+  pdl_trigger_after_writes();
 }
 cudaError_t pad_align_launch(int b, int32_t *len, uint32_t *pad, int pad_words, cudaStream_t st) {
   return launch_pdl(pad_align_kernel, dim3(1), dim3(32), 0, st, b, len, pad, pad_words);
 }
 __global__ void pad_commit_kernel(int b, int32_t *len, int32_t *pos_len, const int32_t *n_emit, uint32_t *pad,
                                   int pad_words) {
-  pdl_trigger();
   pdl_wait();
   __shared__ int A;
   if (threadIdx.x == 0) {
@@ -255,6 +255,7 @@ __global__ void pad_commit_kernel(int b, int32_t *len, int32_t *pos_len, const i
     len[i] += A;
     pos_len[i] += ne;
   }
+  pdl_trigger_after_writes();
 }
 cudaError_t pad_commit_launch(int b, int32_t *len, int32_t *pos_len, const int32_t *n_emit, uint32_t *pad,
                               int pad_words, cudaStream_t st) {
