@@ -244,6 +244,10 @@ sm_status sm_kv_positions(const sm_kv *kv, int32_t *h_pos);
 /* Prefill one turn of n tokens of sequence `seq` (causal forward at positions
  * [Lc, Lc+n)), then set the pending root (argmax) and the heads' top-k
  * at the last token.  A pending root of a previous turn is dropped (Q15).
+ * The turn runs through the verify path in chunks: bf16 on one GPU, causal chunks of up
+ * to max_rows tokens (K1 masks cache slot Lc + j for token i by j <= i, no ancestor
+ * table); fp32 mode and tensor parallel, chain trees of <= 256 tokens.  Larger max_rows
+ * means larger GEMMs (closer to the tensor-core roofline) at the cost of workspace.
  * SM_ERR_KV_CAPACITY if the host-tracked Lc + n > x.  d_tokens: device int32. */
 sm_status sm_prefill(sm_model *m, sm_kv *kv, int seq, const int32_t *d_tokens, int n, void *stream);
 
@@ -299,6 +303,13 @@ sm_status sm_state_device(const sm_kv *kv, int32_t **d_root, int32_t **d_topk);
 sm_status sm_tree_attention(const sm_tree *t, const void *d_q, const void *d_k, const void *d_v,
                             const int32_t *d_len, int batch, int n_heads, int n_kv_heads, int head_dim, int cap,
                             void *d_out, void *stream);
+/* K1 in prefill mode (f3): the n tokens of a chunk sit at slots [Lc, Lc+n) and token i
+ * attends keys [0, Lc) and slots Lc..Lc+i (causal) -- the mask of a chain tree of n
+ * nodes, computed without an ancestor table, so n may exceed the 256-node tree limit.
+ * Buffers as sm_tree_attention with N = n (1 <= n <= 1024).                       */
+sm_status sm_causal_attention(int n, const void *d_q, const void *d_k, const void *d_v, const int32_t *d_len,
+                              int batch, int n_heads, int n_kv_heads, int head_dim, int cap, void *d_out,
+                              void *stream);
 /* K2 tcgen05 GEMM: out[M][N] fp32 = x[M][K] bf16 * w[N][K]^T bf16.  M <= 1024.
  * d_out NULL: only the GEMM runs (its partials stay in library scratch; timing). */
 sm_status sm_gemm_bf16(const void *d_x, const void *d_w, float *d_out, int M, int N, int K, void *stream);

@@ -523,6 +523,15 @@ def tree_attention(tree: Tree, q, k, v, lengths, n_heads: int, n_kv_heads: int, 
                                    hd, cap, ctypes.c_void_p(_ptr(out)), ctypes.c_void_p(_stream(stream))))
 
 
+def causal_attention(q, k, v, lengths, n_heads: int, n_kv_heads: int, out, stream=None) -> None:
+    """K1 prefill mode: q/out [b][n][H][hd] (token i at slot Lc + i attends [0, Lc + i])."""
+    b, n = q.shape[0], q.shape[1]
+    cap, hd = k.shape[2], k.shape[3]
+    _check(lib().sm_causal_attention(n, ctypes.c_void_p(_ptr(q)), ctypes.c_void_p(_ptr(k)), ctypes.c_void_p(_ptr(v)),
+                                     ctypes.c_void_p(_ptr(lengths)), b, n_heads, n_kv_heads, hd, cap,
+                                     ctypes.c_void_p(_ptr(out)), ctypes.c_void_p(_stream(stream))))
+
+
 def gemm_bf16(x, w, out, stream=None) -> None:
     """K2: out[M][N] fp32 = x[M][K] @ w[N][K]^T (tcgen05); out None = GEMM only (timing)."""
     M, K = x.shape

@@ -58,17 +58,20 @@ __global__ void __launch_bounds__(128) tree_attn_kernel(const __grid_constant__ 
   const int sl = blockIdx.z / a.Hkv, h = blockIdx.z % a.Hkv;
   const int seq = a.seq_base + sl;
   const int Lc = a.len[seq];  // only the step's last kernels change Lc: safe before the wait
-  const int T = Lc + a.Nq;
+  const int R = a.Nq * a.G;
+  // causal prefill chunk: keys past the block's last node are invisible to every row of it
+  const int T = Lc + (a.causal ? min(a.Nq, (min(R, (rblk + 1) * 64) - 1) / a.G + 1) : a.Nq);
   const int chunk = ((T + a.nsplit - 1) / a.nsplit + 63) / 64 * 64;
   const int key0 = min(T, split * chunk);
   const int key1 = min(T, key0 + chunk);
   const int ntiles = (key1 - key0 + 63) / 64;
-  const int R = a.Nq * a.G;
 
   // tree mask rows of this CTA (node of each query row); constant tables
-  for (int i = threadIdx.x; i < 64 * kAncWords; i += blockDim.x) {
-    const int r = rblk * 64 + i / kAncWords;
-    s_anc[i] = (r < R) ? a.anc[(r / a.G) * kAncWords + (i % kAncWords)] : 0ull;
+  if (!a.causal) {
+    for (int i = threadIdx.x; i < 64 * kAncWords; i += blockDim.x) {
+      const int r = rblk * 64 + i / kAncWords;
+      s_anc[i] = (r < R) ? a.anc[(r / a.G) * kAncWords + (i % kAncWords)] : 0ull;
+    }
   }
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&a.tmK);
@@ -184,8 +187,10 @@ __global__ void __launch_bounds__(128) tree_attn_kernel(const __grid_constant__ 
             const int p = p0 + 8 * j + 2 * t + e;
             if (p >= Lc) {
               const int jj = p - Lc;
-              const bool va = jj < a.Nq && ((s_anc[la * kAncWords + (jj >> 6)] >> (jj & 63)) & 1ull);
-              const bool vbb = jj < a.Nq && ((s_anc[lb * kAncWords + (jj >> 6)] >> (jj & 63)) & 1ull);
+              const bool va = jj < a.Nq && (a.causal ? jj <= ra / a.G
+                                                      : ((s_anc[la * kAncWords + (jj >> 6)] >> (jj & 63)) & 1ull));
+              const bool vbb = jj < a.Nq && (a.causal ? jj <= rb / a.G
+                                                       : ((s_anc[lb * kAncWords + (jj >> 6)] >> (jj & 63)) & 1ull));
               if (!va) sc[j][e] = -INFINITY;
               if (!vbb) sc[j][2 + e] = -INFINITY;
             }

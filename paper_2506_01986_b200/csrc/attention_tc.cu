@@ -133,12 +133,13 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
   const int sl = blockIdx.z / a.Hkv, h = blockIdx.z % a.Hkv;
   const int seq = a.seq_base + sl;
   const int Lc = a.len[seq];  // changed only by the step's last kernels: safe before the wait
-  const int T = Lc + a.Nq;
+  const int R = a.Nq * a.G;
+  // causal prefill chunk (f3): keys past the block's last node are invisible to every row of it
+  const int T = Lc + (a.causal ? min(a.Nq, (min(R, (rblk + 1) * ROWS) - 1) / a.G + 1) : a.Nq);
   const int chunk = ((T + a.nsplit - 1) / a.nsplit + KEYS - 1) / KEYS * KEYS;
   const int key0 = min(T, split * chunk);
   const int key1 = min(T, key0 + chunk);
   const int ntiles = (key1 - key0 + KEYS - 1) / KEYS;
-  const int R = a.Nq * a.G;
   const float sl2 = a.scale_log2;
 
   const long long kbase_row = a.k_row0 + (long long)seq * a.seq_rows + (long long)h * a.cap;
@@ -185,7 +186,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
   }
   // softmax threads: the ancestor words of their row's node (static tree tables: safe before the wait)
   uint64_t anc0 = 0, anc1 = 0, anc2 = 0, anc3 = 0;
-  if (warp < 4) {
+  if (warp < 4 && !a.causal) {
     const int r = rblk * ROWS + threadIdx.x;
     if (r < R) {
       const uint64_t *w = a.anc + (r / a.G) * kAncWords;
@@ -310,7 +311,12 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
           for (int j = 0; j < 64; ++j) y[j] = ((pm >> j) & 1ull) ? -INFINITY : y[j];
         }
       }
-      if (p0 + KEYS > Lc) {  // tile reaches past the prefix: visibility bitmask of its 64 keys (Eq. 2)
+      if (a.causal && p0 + KEYS > Lc) {  // prefill chunk: key p visible iff p <= Lc + node
+        const int lim = Lc + rr / a.G + 1 - p0;  // visible keys of this tile
+        const uint64_t vis = lim >= 64 ? ~0ull : (lim <= 0 ? 0ull : (~0ull >> (64 - lim)));
+#pragma unroll
+        for (int j = 0; j < 64; ++j) y[j] = ((vis >> j) & 1ull) ? y[j] : -INFINITY;
+      } else if (p0 + KEYS > Lc) {  // tile reaches past the prefix: visibility bitmask of its 64 keys (Eq. 2)
         const int off = p0 - Lc;  // tree slot of key 0 (may be negative)
         auto word = [&](int q) { return q == 0 ? anc0 : q == 1 ? anc1 : q == 2 ? anc2 : q == 3 ? anc3 : 0ull; };
         uint64_t vis;

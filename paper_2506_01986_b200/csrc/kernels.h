@@ -327,6 +327,7 @@ struct AttnArgs {
   unsigned long long l2_pf_bytes;
   const uint32_t *pad;        // nullable: pad-batching bitmap [seq][pad_words] of masked cache slots (f4)
   int pad_words;
+  int causal;                 // prefill chunk (f3): anc unused, tree slot j visible to node n iff j <= n
 };
 cudaError_t attention_launch(const AttnArgs &a, int head_dim, cudaStream_t st);
 int attention_row_blocks(int Nq, int G, int head_dim);

@@ -415,6 +415,7 @@ struct sm_model {
   int fuse_mask = 0;
   float *ss = nullptr;   // [R][d/64] sum-of-squares partials of kEpiResid
   int *tile_cnt = nullptr, *done_cnt = nullptr;
+  int32_t *iota = nullptr;  // [R] 0, 1, 2, ...: node depths of a causal prefill chunk (f3)
   bf16 *h = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr, *hf = nullptr, *head_in = nullptr,
        *r_buf = nullptr;
   int32_t *argmax = nullptr;
@@ -633,6 +634,15 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
   ALLOC(m->done_cnt, 1, "tile counters");
   cudaMemset(m->tile_cnt, 0, (size_t)kMaxFusedTiles * sizeof(int));
   cudaMemset(m->done_cnt, 0, sizeof(int));
+  ALLOC(m->iota, (size_t)R, "prefill depths");
+  {
+    std::vector<int32_t> io((size_t)R);
+    for (int i = 0; i < R; ++i) io[(size_t)i] = i;
+    if (cudaMemcpy(m->iota, io.data(), io.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+      sm_model_destroy(m);
+      return fail(SM_ERR_CUDA, "prefill depths upload");
+    }
+  }
   ALLOC(m->h, (size_t)R * d * P, "h");
   ALLOC(m->q, (size_t)R * Hhd * (m->f32 ? 2 : 1), "q");  // fp32 q in the parity mode
   ALLOC(m->attn, (size_t)R * Hhd * P, "attn");
@@ -744,6 +754,7 @@ extern "C" void sm_model_destroy(sm_model *m) {
   cudaFree(m->rs);
   cudaFree(m->ss);
   cudaFree(m->tile_cnt);
+  cudaFree(m->iota);
   cudaFree(m->done_cnt);
   cudaFree(m->part);
   cudaFree(m->ws);
@@ -945,6 +956,7 @@ extern "C" sm_status sm_workspace_bytes(const sm_model_cfg *cfg, size_t *bytes) 
   const size_t Hhd = (size_t)c.n_heads * c.head_dim, nmed = std::max(1, c.n_medusa);
   size_t b = 0;
   b += R * d * 4 + R * 4 + R * std::max<size_t>(1, d / 64) * 4 + (size_t)kMaxFusedTiles * 4 + 4;  // x, rs, ss, counters
+  b += R * 4;                                                                                        // prefill depths
   b += R * d * 2 * P + R * Hhd * 2 * (c.dtype == SM_DTYPE_FP32 ? 2 : 1) + R * Hhd * 2 * P;       // h, q, attn
   b += R * c.d_ffn * 2 * P + R * d * 2 * P + R * c.vocab * 4 + R * 4 + R * 3 * 4;                // act, hf, z, argmax, stats
   b += B * d * 2 * P + nmed * B * d * 2 * P + (size_t)c.max_seq_len * (c.head_dim / 2) * 8;       // head_in, r_buf, rope
@@ -1235,6 +1247,7 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
     aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)m->hd));
     aa.pad = kv->pad_mode ? kv->pad : nullptr;
     aa.pad_words = kv->pad_words;
+    aa.causal = tree.anc == nullptr;  // causal prefill chunk (sm_prefill)
     aa.l2_pf = m->wo[l];  // o_proj weights stream into L2 while attention runs
     aa.l2_pf_bytes = (unsigned long long)d * m->H * m->hd * 2;
     cudaEvent_t ev = nullptr;
@@ -1324,10 +1337,17 @@ extern "C" sm_status sm_prefill(sm_model *m, sm_kv *kv, int seq, const int32_t *
   tp_begin(m);
   const TreeDev chain = m->chain->dev();
   const int R = m->R;
+  // bf16, one GPU: causal chunks of up to max_rows tokens (the K1 kernels mask tree slot j for
+  // node n by j <= n, no ancestor table); otherwise chain trees of <= 256 nodes (the fp32 K1
+  // reads the ancestor table; the TP exchange flags are sized for 256-row chunks)
+  const bool causal = !m->f32 && m->tp == 1;
   int done = 0, last = 0;
   while (done < n) {
-    const int P = std::min(std::min(R, kMaxTreeNodes), n - done);  // chain-tree chunks of <= 256 tokens
-    CKS(enqueue_forward(m, kv, d_tokens + done, 1, seq, P, chain, st, nl));
+    const int P = std::min(causal ? R : std::min(R, kMaxTreeNodes), n - done);
+    TreeDev ct{};
+    ct.N = P;
+    ct.depth = m->iota;  // node n of the chunk sits at depth n: RoPE position Lc + n
+    CKS(enqueue_forward(m, kv, d_tokens + done, 1, seq, P, causal ? ct : chain, st, nl));
     CK(advance_len_launch(kv->len, seq, P, kv->pad_mode ? kv->pos_len : nullptr, st));
     done += P;
     last = P;
@@ -1574,18 +1594,13 @@ static sm_status scratch(size_t bytes, void **p) {
   return SM_OK;
 }
 
-extern "C" sm_status sm_tree_attention(const sm_tree *t, const void *d_q, const void *d_k, const void *d_v,
-                                       const int32_t *d_len, int batch, int n_heads, int n_kv_heads, int head_dim,
-                                       int cap, void *d_out, void *stream) {
-  if (!t || !d_q || !d_k || !d_v || !d_len || !d_out || batch < 1 || n_kv_heads < 1 || n_heads % n_kv_heads ||
-      cap < t->N)
-    return fail(SM_ERR_INVALID_ARG, "sm_tree_attention: bad arguments");
+static sm_status attention_stage(const uint64_t *d_anc, int Nq, const void *d_q, const void *d_k, const void *d_v,
+                                 const int32_t *d_len, int batch, int n_heads, int n_kv_heads, int head_dim, int cap,
+                                 void *d_out, void *stream) {
   if (head_dim != 16 && head_dim != 32 && head_dim != 64 && head_dim != 128)
     return fail(SM_ERR_INVALID_ARG, "head_dim must be 16/32/64/128");
-  sm_tree *tt = const_cast<sm_tree *>(t);
-  CKS(tree_upload(tt));
   const int G = n_heads / n_kv_heads;
-  const int nsplit = attention_nsplit(batch * n_kv_heads * attention_row_blocks(t->N, G, head_dim), head_dim);
+  const int nsplit = attention_nsplit(batch * n_kv_heads * attention_row_blocks(Nq, G, head_dim), head_dim);
   AttnArgs aa;
   std::memset(&aa, 0, sizeof(aa));
   const uint64_t rows = (uint64_t)batch * n_kv_heads * cap;
@@ -1594,12 +1609,13 @@ extern "C" sm_status sm_tree_attention(const sm_tree *t, const void *d_q, const 
   aa.q = (const bf16 *)d_q;
   aa.out = (bf16 *)d_out;
   aa.len = d_len;
-  aa.anc = tt->d_anc;
+  aa.anc = d_anc;
+  aa.causal = d_anc == nullptr;
   aa.k_row0 = 0;
   aa.v_row0 = 0;
   aa.seq_rows = (long long)n_kv_heads * cap;
   aa.cap = cap;
-  aa.Nq = t->N;
+  aa.Nq = Nq;
   aa.H = n_heads;
   aa.Hkv = n_kv_heads;
   aa.G = G;
@@ -1609,6 +1625,27 @@ extern "C" sm_status sm_tree_attention(const sm_tree *t, const void *d_q, const 
   aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)head_dim));
   CK(attention_launch(aa, head_dim, (cudaStream_t)stream));
   return SM_OK;
+}
+
+extern "C" sm_status sm_tree_attention(const sm_tree *t, const void *d_q, const void *d_k, const void *d_v,
+                                       const int32_t *d_len, int batch, int n_heads, int n_kv_heads, int head_dim,
+                                       int cap, void *d_out, void *stream) {
+  if (!t || !d_q || !d_k || !d_v || !d_len || !d_out || batch < 1 || n_kv_heads < 1 || n_heads % n_kv_heads ||
+      cap < t->N)
+    return fail(SM_ERR_INVALID_ARG, "sm_tree_attention: bad arguments");
+  sm_tree *tt = const_cast<sm_tree *>(t);
+  CKS(tree_upload(tt));
+  return attention_stage(tt->d_anc, t->N, d_q, d_k, d_v, d_len, batch, n_heads, n_kv_heads, head_dim, cap, d_out,
+                         stream);
+}
+
+extern "C" sm_status sm_causal_attention(int n, const void *d_q, const void *d_k, const void *d_v,
+                                         const int32_t *d_len, int batch, int n_heads, int n_kv_heads, int head_dim,
+                                         int cap, void *d_out, void *stream) {
+  if (n < 1 || n > 1024 || !d_q || !d_k || !d_v || !d_len || !d_out || batch < 1 || n_kv_heads < 1 ||
+      n_heads % n_kv_heads || cap < n)
+    return fail(SM_ERR_INVALID_ARG, "sm_causal_attention: bad arguments (1 <= n <= 1024)");
+  return attention_stage(nullptr, n, d_q, d_k, d_v, d_len, batch, n_heads, n_kv_heads, head_dim, cap, d_out, stream);
 }
 
 extern "C" sm_status sm_gemm_bf16(const void *d_x, const void *d_w, float *d_out, int M, int N, int K,

@@ -154,3 +154,49 @@ def test_topk_matches_oracle_with_ties(sm):
     torch.cuda.synchronize()
     for r in range(rows):
         assert out[r].cpu().tolist() == OM.topk_desc(z[r].astype(np.float64), k)
+
+
+# ------------------------------------------------------------------ K1 prefill mode (causal chunks, f3)
+CAUSAL_CASES = [
+    # (name, n, b, H, Hkv, hd, lens, cap_extra): n > 256 (beyond the tree tables), ragged row blocks
+    ("hd128_n600_fresh", 600, 1, 4, 4, 128, [0], 0),
+    ("hd128_n333_gqa4_prefix", 333, 2, 8, 2, 128, [77, 1000], 5),
+    ("hd128_n1024_split", 1024, 1, 1, 1, 128, [4000], 0),
+    ("hd64_n700_gqa2", 700, 2, 4, 2, 64, [0, 130], 3),
+    ("hd16_n97", 97, 1, 4, 4, 16, [32], 0),
+]
+
+
+@pytest.mark.parametrize("attn_tc", [1, 0], ids=["tc", "mma"])
+@pytest.mark.parametrize("case", CAUSAL_CASES, ids=[c[0] for c in CAUSAL_CASES])
+def test_causal_attention_matches_oracle(sm, case, attn_tc):
+    """Token i of a chunk at slot Lc + i attends [0, Lc + i]: the oracle's attention over
+    exactly that key list, row by row (the same rule as a chain tree, without a tree table)."""
+    name, n, b, H, Hkv, hd, lens, extra = case
+    if attn_tc == 0 and hd != 128:
+        pytest.skip("head_dim < 128 always runs the mma.sync kernel")
+    sm.set_option("attn_tc", attn_tc)
+    cap = max(lens) + n + extra
+    q = bf16_tensor(synth.normal_bits(9, 1, b * n * H * hd), (b, n, H, hd))
+    k = bf16_tensor(synth.normal_bits(9, 2, b * Hkv * cap * hd), (b, Hkv, cap, hd))
+    v = bf16_tensor(synth.normal_bits(9, 3, b * Hkv * cap * hd), (b, Hkv, cap, hd))
+    L = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    out = torch.full((b, n, H, hd), float("nan"), dtype=torch.bfloat16, device="cuda")
+    try:
+        sm.causal_attention(q, k, v, L, H, Hkv, out)
+        torch.cuda.synchronize()
+    finally:
+        sm.set_option("attn_tc", 1)
+    Q, K, V = to64(q), to64(k), to64(v)
+    got = to64(out)
+    assert np.all(np.isfinite(got))
+    g = _Geom(H, Hkv, hd)
+    rows = sorted(set([0, 1, 63, 64, 127, 128, n - 1] + list(range(0, n, 7))))
+    for bi in range(b):
+        Lc = lens[bi]
+        for i in (r for r in rows if r < n):
+            keys = list(range(Lc + i + 1))
+            ref = OM.Model.attention(g, Q[bi, i], K[bi][:, keys, :].transpose(1, 0, 2),
+                                     V[bi][:, keys, :].transpose(1, 0, 2))
+            err = np.abs(got[bi, i] - ref)
+            assert np.all(err <= 2e-2 + 2e-2 * np.abs(ref)), (name, bi, i, float(err.max()))
