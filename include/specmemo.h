@@ -318,7 +318,9 @@ sm_status sm_topk_f32(const float *d_logits, int rows, int V, int k, int32_t *d_
 
 /* Runtime options for experiments (take effect for launches enqueued or graphs
  * captured afterwards): "pdl" (0/1, programmatic dependent launch of the step's
- * kernels), "gemm_ctas" (persistent K2 grid size, 0 = one CTA per SM).
+ * kernels), "gemm_ctas" (persistent K2 grid size, 0 = one CTA per SM), "gemm_rep" (1, default:
+ * when M spans several token tiles, groups of that many CTAs walk the same weight k-blocks
+ * together so each weight stage leaves HBM once; 0: plain stream-K).
  * Unknown names return SM_ERR_INVALID_ARG.                                     */
 sm_status sm_set_option(const char *name, int value);
 

@@ -195,7 +195,8 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const SplitPlan &pl = a.plan;
   const int c = blockIdx.x;
-  const long long u0 = sk_unit0(c, pl), u1 = sk_unit0(c + 1, pl);
+  const int g = c / pl.rep, ttr = c % pl.rep;  // CTA group and token-tile lane (SplitPlan::rep)
+  const long long u0 = sk_unit0(g, pl), u1 = sk_unit0(g + 1, pl);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&a.tmW[0]);
@@ -239,7 +240,7 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
       for (int i = 0; i < pre; ++i) {  // weights first: independent of the previous kernel
         const long long u = u0 + i;
         int bi, tt, mt;
-        sk_decode(sk_tile(u, pl), pl, bi, tt, mt);
+        sk_decode(sk_tile_r(u, pl, ttr), pl, bi, tt, mt);
         mbar_arrive_expect_tx(&full[i], stage_bytes);
         tma_load_2d_hint(sA + i * C::kA, &a.tmW[bi], &full[i], sk_kb(u, pl) * 64, mt * 128, pol_w);
       }
@@ -247,7 +248,7 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
       for (int i = pre; i < pre + a.l2_prefetch && u0 + i < u1; ++i) {
         const long long u = u0 + i;
         int bi, tt, mt;
-        sk_decode(sk_tile(u, pl), pl, bi, tt, mt);
+        sk_decode(sk_tile_r(u, pl, ttr), pl, bi, tt, mt);
         tma_prefetch_l2_2d(&a.tmW[bi], sk_kb(u, pl) * 64, mt * 128);
       }
       pdl_wait();  // activations only after the producer kernel completed
@@ -255,7 +256,7 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
       for (int i = 0; i < pre; ++i) {
         const long long u = u0 + i;
         int bi, tt, mt;
-        sk_decode(sk_tile(u, pl), pl, bi, tt, mt);
+        sk_decode(sk_tile_r(u, pl, ttr), pl, bi, tt, mt);
         issue_x(i, bi, tt, sk_kb(u, pl) * 64);
       }
       for (long long u = u0 + pre; u < u1; ++u) {
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
         const int s = i % C::kStages;
         if (i >= C::kStages) mbar_wait(&empty[s], ((i / C::kStages) - 1) & 1);
         int bi, tt, mt;
-        sk_decode(sk_tile(u, pl), pl, bi, tt, mt);
+        sk_decode(sk_tile_r(u, pl, ttr), pl, bi, tt, mt);
         const int kc = sk_kb(u, pl) * 64;
         mbar_arrive_expect_tx(&full[s], stage_bytes);
         tma_load_2d_hint(sA + s * C::kA, &a.tmW[bi], &full[s], kc, mt * 128, pol_w);
@@ -311,13 +312,13 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
     int seg = 0;
     long long u = u0;
     while (u < u1) {
-      const int t = sk_tile(u, pl);
-      const long long seg_end = min(u1, (long long)(t + 1) * pl.kb_total);
+      const int t = sk_tile_r(u, pl, ttr);
+      const long long seg_end = min(u1, (long long)(t / pl.rep + 1) * pl.kb_total);
       const int buf = seg & 1;
       mbar_wait(&tfull[buf], (seg >> 1) & 1);
       tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(wq * 32) << 16) + buf * BN;
-      float *dst = sk_partial(a.ws, pl, t, c - sk_cta_of((long long)t * pl.kb_total, pl));
+      float *dst = sk_partial(a.ws, pl, t, g - sk_first_grp(t, pl));
       for (int c0 = 0; c0 < BN; c0 += CH) {
         float v[CH];
         tmem_ldc<CH>(tbase + c0, v);
@@ -328,8 +329,7 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
       mbar_arrive(&tempty[buf]);
       if (FUSED && a.epi != kEpiPartial) {  // last contributor of tile t applies the fused epilogue
         const int et = threadIdx.x - 64;
-        const int cf = sk_cta_of((long long)t * pl.kb_total, pl);
-        const int nc = sk_cta_of((long long)(t + 1) * pl.kb_total - 1, pl) - cf + 1;
+        const int nc = sk_ncontrib(t, pl);
         __threadfence();
         epi_bar();
         if (et == 0) *s_flag = atomicAdd(&a.e.tile_cnt[t], 1) == nc - 1;
@@ -405,7 +405,8 @@ __global__ void __launch_bounds__(192, 1) gemm_pair_kernel(const __grid_constant
   const SplitPlan &pl = a.plan;
   const int rank = (int)cluster_ctarank();
   const int c = blockIdx.x >> 1;  // cluster = work unit owner
-  const long long u0 = sk_unit0(c, pl), u1 = sk_unit0(c + 1, pl);
+  const int g = c / pl.rep, ttr = c % pl.rep;  // cluster group and token-tile lane (SplitPlan::rep)
+  const long long u0 = sk_unit0(g, pl), u1 = sk_unit0(g + 1, pl);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&a.tmW[0]);
@@ -434,14 +435,14 @@ __global__ void __launch_bounds__(192, 1) gemm_pair_kernel(const __grid_constant
       const uint32_t full_cl0 = mapa_u32(smem_u32(&full[0]), 0);
       auto load_w = [&](int s, long long u) {
         int bi, tt, mt;
-        sk_decode(sk_tile(u, pl), pl, bi, tt, mt);
+        sk_decode(sk_tile_r(u, pl, ttr), pl, bi, tt, mt);
         if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * C::kStage);  // both CTAs' W and X bytes
         tma_load_2d_cg2_hint(sA + s * C::kA, &a.tmW[0], full_cl0 + 8 * s, sk_kb(u, pl) * 64, (mt * 2 + rank) * 128,
                              pol_w);
       };
       auto load_x = [&](int s, long long u) {
         int bi, tt, mt;
-        sk_decode(sk_tile(u, pl), pl, bi, tt, mt);
+        sk_decode(sk_tile_r(u, pl, ttr), pl, bi, tt, mt);
         tma_load_2d_cg2(sB + s * C::kB, &a.tmX64[0], full_cl0 + 8 * s, sk_kb(u, pl) * 64,
                         a.x_row0 + tt * BN + rank * (BN / 2));
       };
@@ -494,13 +495,13 @@ __global__ void __launch_bounds__(192, 1) gemm_pair_kernel(const __grid_constant
     int seg = 0;
     long long u = u0;
     while (u < u1) {
-      const int t = sk_tile(u, pl);
-      const long long seg_end = min(u1, (long long)(t + 1) * pl.kb_total);
+      const int t = sk_tile_r(u, pl, ttr);
+      const long long seg_end = min(u1, (long long)(t / pl.rep + 1) * pl.kb_total);
       const int buf = seg % C::kNBuf;
       mbar_wait(&tfull[buf], (seg / C::kNBuf) & 1);
       tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(wq * 32) << 16) + buf * BN;
-      float *dst = sk_partial(a.ws, pl, t, c - sk_cta_of((long long)t * pl.kb_total, pl), rank);
+      float *dst = sk_partial(a.ws, pl, t, g - sk_first_grp(t, pl), rank);
       for (int c0 = 0; c0 < BN; c0 += 32) {
         float v[32];
         tmem_ld32(tbase + c0, v);
@@ -523,6 +524,7 @@ __global__ void __launch_bounds__(192, 1) gemm_pair_kernel(const __grid_constant
 
 static bool g_pdl = true;
 static int g_ctas = 0;
+static int g_rep = 1;  // sm_set_option("gemm_rep"): token-tile CTA groups (SplitPlan::rep); 0 = plain stream-K
 static int g_l2pf = 0;
 static int g_dbg_mode = 0;
 static int g_force_bn = 0;
@@ -546,6 +548,7 @@ void gemm_set_debug_mode(int m) { g_dbg_mode = m; }
 void gemm_set_pdl(bool on) { g_pdl = on; }
 bool gemm_pdl() { return g_pdl; }
 void gemm_set_ctas(int n) { g_ctas = n; }
+void gemm_set_rep(int on) { g_rep = on ? 1 : 0; }
 void gemm_set_l2_prefetch(int kblocks) { g_l2pf = kblocks < 0 ? 0 : kblocks; }
 
 template <int BN, int SMEMKB>
@@ -562,7 +565,7 @@ static cudaError_t launch_bn(const GemmArgs &a, cudaStream_t st) {
     attr_set = true;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(a.plan.P);
+  cfg.gridDim = dim3(a.plan.P * a.plan.rep);
   cfg.blockDim = dim3(192);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = st;
@@ -589,7 +592,7 @@ static cudaError_t launch_pair(const GemmArgs &a, cudaStream_t st) {
     attr_set = true;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2 * a.plan.P);
+  cfg.gridDim = dim3(2 * a.plan.P * a.plan.rep);
   cfg.blockDim = dim3(192);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = st;
@@ -633,10 +636,15 @@ void gemm_plan(GemmArgs &a, int N, int K, int M, int batch) {
   p.token_tiles = (M + p.bn - 1) / p.bn;
   p.tiles = p.m_tiles * p.token_tiles * batch;
   p.kb_total = (K + 63) / 64;
-  const long long U = (long long)p.tiles * p.kb_total;
   p.occ = gemm_occ_for(p.bn, N);
   int want = g_ctas > 0 ? g_ctas : kNumSMs * p.occ;
   if (p.pair == 2) want = g_ctas > 0 ? g_ctas / 2 : kNumSMs;  // clusters of 2 CTAs, 2 CTAs per SM
+  // several token tiles (tensor-bound M): groups of token_tiles CTAs walk the same weight
+  // k-blocks together (SplitPlan::rep) -- measured: plain stream-K re-read the weights from HBM
+  // ~3.7x at M = 1024 (the token tiles of a weight tile ran far apart in time)
+  p.rep = (g_rep && p.token_tiles > 1 && !a.no_pair && want / p.token_tiles >= 1) ? p.token_tiles : 1;  // not fused
+  const long long U = (long long)(p.tiles / p.rep) * p.kb_total;
+  want /= p.rep;
   p.P = (int)(U < want ? U : want);
   p.U = U;
   // contributors per tile <= ceil(KB / floor(U/P)) + 1

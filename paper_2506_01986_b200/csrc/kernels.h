@@ -35,12 +35,29 @@ struct SplitPlan {
   int P, bn, m_tiles, token_tiles, tiles, kb_total, maxc;
   int pair;
   int occ;  // GEMM CTAs per SM of the launch (smem variant)
+  // rep > 1 (several token tiles, tensor-bound M): U and P count weight-tile units and CTA
+  // groups; group g is rep CTAs (clusters) that run the same k-range of the same weight tile,
+  // one per token tile, so the weight stage is fetched from HBM once and hit in L2 by the
+  // others.  CTA c = g * rep + token tile.  rep = 1: the plain stream-K partition.
+  int rep;
 };
 __host__ __device__ inline long long sk_unit0(int c, const SplitPlan &p) { return p.U * c / p.P; }
 __host__ __device__ inline int sk_cta_of(long long u, const SplitPlan &p) {
   return (int)(((u + 1) * p.P + p.U - 1) / p.U) - 1;
 }
 __host__ __device__ inline int sk_tile(long long u, const SplitPlan &p) { return (int)(u / p.kb_total); }
+// real tile of unit u for the CTA at token-tile lane ttr of its group (rep = token_tiles: the
+// tile index (bi * m_tiles + mt) * token_tiles + tt with tt = ttr)
+__host__ __device__ inline int sk_tile_r(long long u, const SplitPlan &p, int ttr) {
+  return (int)(u / p.kb_total) * p.rep + ttr;
+}
+// first and last CTA group contributing to real tile t
+__host__ __device__ inline int sk_first_grp(int t, const SplitPlan &p) {
+  return sk_cta_of((long long)(t / p.rep) * p.kb_total, p);
+}
+__host__ __device__ inline int sk_ncontrib(int t, const SplitPlan &p) {
+  return sk_cta_of((long long)(t / p.rep + 1) * p.kb_total - 1, p) - sk_first_grp(t, p) + 1;
+}
 __host__ __device__ inline int sk_kb(long long u, const SplitPlan &p) { return (int)(u % p.kb_total); }
 // token tiles of one weight tile are adjacent units, so a re-read of the same
 // 128 x K weight rows for the next token tile is a near-term L2 hit
@@ -83,8 +100,7 @@ __device__ inline float4 sk_sum4(const PartialView &v, int bi, int m, int n) {
   int t;
   size_t slot0;
   sk_locate(p, bi, m, n, t, slot0);
-  const int cf = sk_cta_of((long long)t * p.kb_total, p), cl = sk_cta_of((long long)(t + 1) * p.kb_total - 1, p);
-  const int nc = cl - cf + 1;
+  const int nc = sk_ncontrib(t, p);
   const float4 *base =
       reinterpret_cast<const float4 *>(v.ws + slot0 * p.bn * 128 + (size_t)(m - tt * p.bn) * 128 + (n & 127));
   const size_t stride = (size_t)p.bn * 128 / 4;  // float4 between contributors
@@ -119,9 +135,8 @@ __device__ inline SkRef sk_ref(const PartialView &v, int bi, int m, int n) {
   int t;
   size_t slot0;
   sk_locate(p, bi, m, n, t, slot0);
-  const int cf = sk_cta_of((long long)t * p.kb_total, p), cl = sk_cta_of((long long)(t + 1) * p.kb_total - 1, p);
   SkRef r;
-  r.nc = cl - cf + 1;
+  r.nc = sk_ncontrib(t, p);
   r.base = reinterpret_cast<const float4 *>(v.ws + slot0 * p.bn * 128 + (size_t)(m - tt * p.bn) * 128 + (n & 127));
   r.stride = (size_t)p.bn * 128 / 4;
   return r;
@@ -158,8 +173,7 @@ __device__ inline float sk_sum1(const PartialView &v, int bi, int m, int n) {
   int t;
   size_t slot0;
   sk_locate(p, bi, m, n, t, slot0);
-  const int cf = sk_cta_of((long long)t * p.kb_total, p), cl = sk_cta_of((long long)(t + 1) * p.kb_total - 1, p);
-  const int nc = cl - cf + 1;
+  const int nc = sk_ncontrib(t, p);
   const float *base = v.ws + slot0 * p.bn * 128 + (size_t)(m - tt * p.bn) * 128 + (n & 127);
   const size_t stride = (size_t)p.bn * 128;
   float acc = 0.f;
@@ -300,6 +314,7 @@ size_t gemm_ws_floats(const GemmArgs &a);
 void gemm_set_pdl(bool on);
 bool gemm_pdl();
 void gemm_set_ctas(int n);
+void gemm_set_rep(int on);
 void gemm_set_l2_prefetch(int kblocks);
 void gemm_set_debug_mode(int m);
 void gemm_set_small(int v);

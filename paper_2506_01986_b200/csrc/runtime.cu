@@ -1706,6 +1706,8 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
     gemm_set_pdl(value != 0);
   } else if (n == "gemm_ctas") {
     gemm_set_ctas(value);
+  } else if (n == "gemm_rep") {  // token-tile CTA groups for M > one token tile (default 1)
+    gemm_set_rep(value);
   } else if (n == "l2_prefetch") {
     gemm_set_l2_prefetch(value);
   } else if (n == "gemm_bn") {

@@ -63,6 +63,21 @@ def test_gemm_matches_fp64(sm, M, N, K):
     assert np.all(err <= 2e-6 * bound + 1e-30), float((err / (bound + 1e-30)).max())
 
 
+@pytest.mark.parametrize("pair", [0, 1], ids=["single_sm", "pair"])
+@pytest.mark.parametrize("rep", [1, 0], ids=["groups", "plain"])
+@pytest.mark.parametrize("M,N,K", [(640, 1000, 320), (1024, 2304, 512), (300, 384, 1024), (513, 4352, 192)])
+def test_gemm_token_tile_groups_match_fp64(sm, M, N, K, rep, pair):
+    """Several token tiles: CTA groups walking the same weight k-blocks (gemm_rep = 1, SplitPlan::rep)
+    and the plain stream-K partition, single-SM and 2-SM kernels."""
+    sm.set_option("gemm_rep", rep)
+    sm.set_option("gemm_pair", pair)
+    try:
+        test_gemm_matches_fp64(sm, M, N, K)
+    finally:
+        sm.set_option("gemm_rep", 1)
+        sm.set_option("gemm_pair", 1)
+
+
 @pytest.mark.parametrize("M,N,K", [(64, 4096, 512), (100, 1000, 320), (160, 8192, 1024), (256, 384, 8192),
                                    (77, 4352, 640)])
 def test_gemm_pair_matches_fp64(sm, M, N, K):
