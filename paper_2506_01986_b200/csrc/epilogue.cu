@@ -164,12 +164,72 @@ __global__ void __launch_bounds__(kNormThreads) resid_norm_split_kernel(PartialV
   if (threadIdx.x == 0) ss_out[(size_t)m * cs + rank] = ss;
   if (threadIdx.x == 0) SM_GT_END(1);
 }
+// M >= 256: four token rows per CTA, every partial and residual load issued up front (see the
+// SiLU consumer); per-row sums reduced in the same warp-then-block order as block_sum.
+__global__ void __launch_bounds__(kNormThreads) resid_norm_split4_kernel(PartialView pv, int has_pv, float *x,
+                                                                         const bf16 *g, bf16 *h, int d, int M, int hp,
+                                                                         float *ss_out) {
+  constexpr int RPC = 4, NM = 4;
+  __shared__ float red[RPC][kNormThreads / 32];
+  pdl_trigger();
+  pdl_wait();
+  const int rank = blockIdx.x, cs = gridDim.x, m0 = blockIdx.y * RPC;
+  const int i = rank * kNormCols + threadIdx.x * 4;
+  float sq[RPC] = {0.f, 0.f, 0.f, 0.f};
+  if (i < d) {
+    SkRef ref[RPC];
+    float4 ys[RPC][NM], a[RPC];
+#pragma unroll
+    for (int q = 0; q < RPC; ++q) {
+      const int m = min(m0 + q, M - 1);
+      if (has_pv) {
+        ref[q] = sk_ref(pv, 0, m, i);
+        sk_load<NM>(ref[q], ys[q]);
+      }
+      a[q] = *reinterpret_cast<const float4 *>(x + (size_t)m * d + i);
+    }
+    const __nv_bfloat162 g01 = *reinterpret_cast<const __nv_bfloat162 *>(g + i);
+    const __nv_bfloat162 g23 = *reinterpret_cast<const __nv_bfloat162 *>(g + i + 2);
+#pragma unroll
+    for (int q = 0; q < RPC; ++q) {
+      const int m = m0 + q;
+      if (m >= M) break;
+      float4 v = a[q];
+      if (has_pv) {
+        const float4 y = sk_reduce<NM>(ref[q], ys[q]);  // R5/R7
+        v.x += y.x;
+        v.y += y.y;
+        v.z += y.z;
+        v.w += y.w;
+        *reinterpret_cast<float4 *>(x + (size_t)m * d + i) = v;
+      }
+      store_act4(h, hp, m, d, i, v.x * __low2float(g01), v.y * __high2float(g01), v.z * __low2float(g23),
+                 v.w * __high2float(g23));
+      sq[q] = v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    }
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < RPC; ++q) {
+    const float v = warp_sum(sq[q]);
+    if (l == 0) red[q][w] = v;
+  }
+  __syncthreads();
+  if (w < RPC && m0 + w < M) {  // warp q: the block sum of row m0 + q (same order as block_sum)
+    float r = l < kNormThreads / 32 ? red[w][l] : 0.f;
+    r = warp_sum(r);
+    if (l == 0) ss_out[(size_t)(m0 + w) * cs + rank] = r;
+  }
+}
 cudaError_t resid_norm_split_launch(const PartialView *pv, float *x, const bf16 *g, bf16 *h, int M, int d, int hp,
                                     float *ss, cudaStream_t st) {
   const int cs = resid_norm_slices(d);
   if (d % 4) return cudaErrorInvalidValue;
   PartialView v{};
   if (pv) v = *pv;
+  if (M >= 256 && v.planes <= 1)
+    return launch_pdl(resid_norm_split4_kernel, dim3(cs, (M + 3) / 4), dim3(kNormThreads), 0, st, v, pv ? 1 : 0, x,
+                      g, h, d, M, hp, ss);
   return launch_pdl(resid_norm_split_kernel, dim3(cs, M), dim3(kNormThreads), 0, st, v, pv ? 1 : 0, x, g, h, d, hp,
                     ss);
 }
@@ -349,38 +409,60 @@ cudaError_t qkv_consumer_launch(const PartialView &pv, RowCtx rc, int H, int Hkv
 
 // ------------------------------------------------------------------ SiLU(gate) * up
 // fused weight rows: tile t = [gate 64t..64t+63 | up 64t..64t+63]
+// RPC token rows per CTA: 1 for decode-sized M (latency: one round trip per CTA); 4 for
+// M >= 256 (prefill chunks, C4-V64), where the partials stream from HBM and one-row CTAs
+// spend more time launching than loading -- all RPC rows' loads are issued before any add.
+template <int RPC>
 __global__ void __launch_bounds__(256) silu_consumer_kernel(PartialView pv, int F, bf16 *act, RsArgs rs) {
   SM_GT_BEGIN();
   pdl_trigger();
   pdl_wait();
   SM_GT_WAITED();
-  const int m = blockIdx.y;
   const int f = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (f >= F) return;
   const int ng = (f >> 6) * 128 + (f & 63);
-  float4 g, u;
-  if (pv.planes > 1) {
-    g = sk_get4(pv, 0, m, ng);
-    u = sk_get4(pv, 0, m, ng + 64);
-  } else {
-    const SkRef rg = sk_ref(pv, 0, m, ng), ru = sk_ref(pv, 0, m, ng + 64);
-    float4 xg[8], xu[8];
-    sk_load<8>(rg, xg);
-    sk_load<8>(ru, xu);
-    g = sk_reduce<8>(rg, xg);
-    u = sk_reduce<8>(ru, xu);
-  }
-  const float r = rs_of(rs, m);  // deferred RMSNorm scale (R2)
-  const float gg[4] = {g.x * r, g.y * r, g.z * r, g.w * r}, uu[4] = {u.x * r, u.y * r, u.z * r, u.w * r};
-  float o[4];
+  if (RPC == 1 && pv.planes > 1) {
+    const int m = blockIdx.y;
+    const float4 g = sk_get4(pv, 0, m, ng), u = sk_get4(pv, 0, m, ng + 64);
+    const float r = rs_of(rs, m);  // deferred RMSNorm scale (R2)
+    const float gg[4] = {g.x * r, g.y * r, g.z * r, g.w * r}, uu[4] = {u.x * r, u.y * r, u.z * r, u.w * r};
+    float o[4];
 #pragma unroll
-  for (int e = 0; e < 4; ++e) o[e] = gg[e] / (1.0f + expf(-gg[e])) * uu[e];
-  store_act4(act, pv.planes, m, F, f, o[0], o[1], o[2], o[3]);
+    for (int e = 0; e < 4; ++e) o[e] = gg[e] / (1.0f + expf(-gg[e])) * uu[e];
+    store_act4(act, pv.planes, m, F, f, o[0], o[1], o[2], o[3]);
+  } else {
+    constexpr int NM = RPC == 1 ? 8 : 2;  // contributors loaded up front per row (more: sk_reduce)
+    SkRef rg[RPC], ru[RPC];
+    float4 xg[RPC][NM], xu[RPC][NM];
+#pragma unroll
+    for (int q = 0; q < RPC; ++q) {
+      const int m = min((int)blockIdx.y * RPC + q, pv.M - 1);
+      rg[q] = sk_ref(pv, 0, m, ng);
+      ru[q] = sk_ref(pv, 0, m, ng + 64);
+      sk_load<NM>(rg[q], xg[q]);
+      sk_load<NM>(ru[q], xu[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < RPC; ++q) {
+      const int m = blockIdx.y * RPC + q;
+      if (m >= pv.M) break;
+      const float4 g = sk_reduce<NM>(rg[q], xg[q]), u = sk_reduce<NM>(ru[q], xu[q]);
+      const float r = rs_of(rs, m);  // deferred RMSNorm scale (R2)
+      const float gg[4] = {g.x * r, g.y * r, g.z * r, g.w * r}, uu[4] = {u.x * r, u.y * r, u.z * r, u.w * r};
+      float o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) o[e] = gg[e] / (1.0f + expf(-gg[e])) * uu[e];
+      store_act4(act, pv.planes, m, F, f, o[0], o[1], o[2], o[3]);
+    }
+  }
   if (threadIdx.x == 0) SM_GT_END(3);
 }
 cudaError_t silu_consumer_launch(const PartialView &pv, int F, bf16 *act, RsArgs rs, cudaStream_t st) {
   const int nt = g_consumer_threads;
-  return launch_pdl(silu_consumer_kernel, dim3((F / 4 + nt - 1) / nt, pv.M), dim3(nt), 0, st, pv, F, act, rs);
+  const int gx = (F / 4 + nt - 1) / nt;
+  if (pv.M >= 256 && pv.planes <= 1)
+    return launch_pdl(silu_consumer_kernel<4>, dim3(gx, (pv.M + 3) / 4), dim3(nt), 0, st, pv, F, act, rs);
+  return launch_pdl(silu_consumer_kernel<1>, dim3(gx, pv.M), dim3(nt), 0, st, pv, F, act, rs);
 }
 
 // ------------------------------------------------------------------ logits: argmax + typical stats
@@ -713,9 +795,11 @@ void epilogue_preload() {  // force-load (see gemm_preload)
   cudaFuncGetAttributes(&fa, resid_norm_kernel);
   cudaFuncGetAttributes(&fa, resid_norm_tp_kernel);
   cudaFuncGetAttributes(&fa, resid_norm_split_kernel);
+  cudaFuncGetAttributes(&fa, resid_norm_split4_kernel);
   cudaFuncGetAttributes(&fa, qkv_consumer_kernel<false>);
   cudaFuncGetAttributes(&fa, qkv_consumer_kernel<true>);
-  cudaFuncGetAttributes(&fa, silu_consumer_kernel);
+  cudaFuncGetAttributes(&fa, silu_consumer_kernel<1>);
+  cudaFuncGetAttributes(&fa, silu_consumer_kernel<4>);
   cudaFuncGetAttributes(&fa, logits_kernel<true>);
   cudaFuncGetAttributes(&fa, logits_kernel<false>);
   cudaFuncGetAttributes(&fa, topk_kernel<true, 10>);
