@@ -109,6 +109,8 @@ SM_DEV void tmem_st32_f(uint32_t taddr, const float *v) {
 // sm_set_option("attn_l2pf"): prefetch the o_proj weights into L2 during attention.  Measured:
 // the o_proj GEMM gains ~0.8 us per layer, attention loses ~2.3 us (its K/V reads compete) -> off.
 __device__ int g_attn_l2pf = 0;
+// CAUSAL: prefill chunk (AttnArgs::causal), compiled separately so the tree kernel keeps its code
+template <bool CAUSAL>
 __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_constant__ AttnArgs a) {
   using namespace tc;
   extern __shared__ uint8_t smem_raw[];
@@ -135,7 +137,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
   const int Lc = a.len[seq];  // changed only by the step's last kernels: safe before the wait
   const int R = a.Nq * a.G;
   // causal prefill chunk (f3): keys past the block's last node are invisible to every row of it
-  const int T = Lc + (a.causal ? min(a.Nq, (min(R, (rblk + 1) * ROWS) - 1) / a.G + 1) : a.Nq);
+  const int T = Lc + (CAUSAL ? min(a.Nq, (min(R, (rblk + 1) * ROWS) - 1) / a.G + 1) : a.Nq);
   const int chunk = ((T + a.nsplit - 1) / a.nsplit + KEYS - 1) / KEYS * KEYS;
   const int key0 = min(T, split * chunk);
   const int key1 = min(T, key0 + chunk);
@@ -186,7 +188,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
   }
   // softmax threads: the ancestor words of their row's node (static tree tables: safe before the wait)
   uint64_t anc0 = 0, anc1 = 0, anc2 = 0, anc3 = 0;
-  if (warp < 4 && !a.causal) {
+  if (warp < 4 && !CAUSAL) {
     const int r = rblk * ROWS + threadIdx.x;
     if (r < R) {
       const uint64_t *w = a.anc + (r / a.G) * kAncWords;
@@ -311,7 +313,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
           for (int j = 0; j < 64; ++j) y[j] = ((pm >> j) & 1ull) ? -INFINITY : y[j];
         }
       }
-      if (a.causal && p0 + KEYS > Lc) {  // prefill chunk: key p visible iff p <= Lc + node
+      if (CAUSAL && p0 + KEYS > Lc) {  // prefill chunk: key p visible iff p <= Lc + node
         const int lim = Lc + rr / a.G + 1 - p0;  // visible keys of this tile
         const uint64_t vis = lim >= 64 ? ~0ull : (lim <= 0 ? 0ull : (~0ull >> (64 - lim)));
 #pragma unroll
@@ -537,7 +539,10 @@ int attention_tc_nsplit(int units) {  // 1 CTA per SM: aim for ~one wave of 148
 cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tree_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(tree_attn_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         tc::SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(tree_attn_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -555,14 +560,16 @@ cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
   attrs[1].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = a.nsplit > 1 ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel, a);
+  if (a.causal) return cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<true>, a);
+  return cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<false>, a);
 }
 
 void attention_set_l2pf(int on) { cudaMemcpyToSymbol(g_attn_l2pf, &on, sizeof(int)); }
 
 void attention_tc_preload() {  // force-load (see gemm_preload)
   cudaFuncAttributes fa;
-  cudaFuncGetAttributes(&fa, tree_attn_tc_kernel);
+  cudaFuncGetAttributes(&fa, tree_attn_tc_kernel<false>);
+  cudaFuncGetAttributes(&fa, tree_attn_tc_kernel<true>);
 }
 
 }  // namespace sm

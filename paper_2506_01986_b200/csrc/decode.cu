@@ -183,8 +183,14 @@ cudaError_t compact_launch(bf16 *kv_base, int L, int b, int Hkv, int cap, int hd
 }
 
 // ------------------------------------------------------------------ commit
+// LATE: trigger dependents only after the Lc write is fenced (common.cuh).  Inside the step's
+// CUDA graph nothing after the commit reads Lc before its wait and the next replay is a full
+// dependency, so the captured commit triggers at entry (the heads GEMM then streams its first
+// weight stages while accept / compact / commit run); eager launches (sm_accept) use LATE.
+template <bool LATE>
 __global__ void commit_kernel(int32_t *len, const int32_t *n_emit, int32_t *root, const int32_t *root_next,
                               const int32_t *acc_row, const bf16 *hf, int d, bf16 *head_in, int32_t *emitted_total) {
+  if (!LATE) pdl_trigger();
   pdl_wait();
   const int bb = blockIdx.x;
   const int ne = n_emit[bb];
@@ -198,13 +204,18 @@ __global__ void commit_kernel(int32_t *len, const int32_t *n_emit, int32_t *root
       if (emitted_total) emitted_total[bb] += ne;
     }
   }
-  pdl_trigger_after_writes();  // Lc changed: see common.cuh
+  if (LATE) pdl_trigger_after_writes();  // Lc changed: see common.cuh
 }
 cudaError_t commit_launch(int b, int32_t *len, const int32_t *n_emit, int32_t *root, const int32_t *root_next,
                           const int32_t *acc_row, const bf16 *hf, int d, bf16 *head_in, int32_t *emitted_total,
                           cudaStream_t st) {
-  return launch_pdl(commit_kernel, dim3(b), dim3(256), 0, st, len, n_emit, root, root_next, acc_row, hf, d, head_in,
-                    emitted_total);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) return cudaErrorInvalidValue;
+  if (cs == cudaStreamCaptureStatusActive)
+    return launch_pdl(commit_kernel<false>, dim3(b), dim3(256), 0, st, len, n_emit, root, root_next, acc_row, hf, d,
+                      head_in, emitted_total);
+  return launch_pdl(commit_kernel<true>, dim3(b), dim3(256), 0, st, len, n_emit, root, root_next, acc_row, hf, d,
+                    head_in, emitted_total);
 }
 
 __global__ void advance_len_kernel(int32_t *len, int seq, int n, int32_t *pos_len) {
@@ -331,7 +342,8 @@ void decode_preload() {  // force-load (see gemm_preload)
   cudaFuncGetAttributes(&fa, propose_kernel);
   cudaFuncGetAttributes(&fa, accept_kernel);
   cudaFuncGetAttributes(&fa, compact_kernel);
-  cudaFuncGetAttributes(&fa, commit_kernel);
+  cudaFuncGetAttributes(&fa, commit_kernel<false>);
+  cudaFuncGetAttributes(&fa, commit_kernel<true>);
   cudaFuncGetAttributes(&fa, advance_len_kernel);
   cudaFuncGetAttributes(&fa, pad_align_kernel);
   cudaFuncGetAttributes(&fa, pad_commit_kernel);

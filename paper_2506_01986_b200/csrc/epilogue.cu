@@ -328,6 +328,8 @@ cudaError_t resid_norm_tp_launch(const PartialView &pv, float *x, const bf16 *g,
 // ------------------------------------------------------------------ QKV consumer (RoPE + cache write)
 // thread -> 4 consecutive rotary pairs (c .. c+3) of one head of one token row
 // F32 (fp32 parity mode): q and the K/V cache hold fp32, partial rows come in 3 planes.
+// thread -> 4 consecutive rotary pairs (c .. c+3) of one head of one token row
+// F32 (fp32 parity mode): q and the K/V cache hold fp32, partial rows come in 3 planes.
 template <bool F32>
 __global__ void __launch_bounds__(256) qkv_consumer_kernel(PartialView pv, RowCtx rc, int H, int Hkv, int hd,
                                                            const float2 *rope, void *q_, void *kc_, void *vc_, int cap,
@@ -395,25 +397,141 @@ __global__ void __launch_bounds__(256) qkv_consumer_kernel(PartialView pv, RowCt
   }
   if (threadIdx.x == 0) SM_GT_END(2);
 }
+// RPC token rows per CTA (bf16 only): 4 for M >= 256, all rows' partial loads issued first (see
+// the SiLU consumer below).
+template <bool F32, int RPC>
+__global__ void __launch_bounds__(256) qkv_consumer_rows_kernel(PartialView pv, RowCtx rc, int H, int Hkv, int hd,
+                                                           const float2 *rope, void *q_, void *kc_, void *vc_, int cap,
+                                                           RsArgs rs) {
+  SM_GT_BEGIN();
+  using T = typename std::conditional<F32, float, bf16>::type;
+  T *q = static_cast<T *>(q_), *kc = static_cast<T *>(kc_), *vc = static_cast<T *>(vc_);
+  pdl_trigger();
+  pdl_wait();
+  SM_GT_WAITED();
+  const int half = hd / 2;
+  const int quads = half / 4;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (H + 2 * Hkv) * quads) return;
+  const int hh = idx / quads, c = (idx % quads) * 4;
+  const int n0 = hh * hd + c;
+  constexpr int NM = RPC == 1 ? 8 : 2;
+  float4 av[RPC], bv[RPC];
+  if constexpr (F32) {
+    av[0] = sk_get4(pv, 0, blockIdx.y, n0);
+    bv[0] = sk_get4(pv, 0, blockIdx.y, n0 + half);
+  } else {
+    SkRef ra[RPC], rb[RPC];
+    float4 xa[RPC][NM], xb[RPC][NM];
+#pragma unroll
+    for (int u = 0; u < RPC; ++u) {
+      const int m = min((int)blockIdx.y * RPC + u, rc.M - 1);
+      ra[u] = sk_ref(pv, 0, m, n0);
+      rb[u] = sk_ref(pv, 0, m, n0 + half);
+      sk_load<NM>(ra[u], xa[u]);
+      sk_load<NM>(rb[u], xb[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < RPC; ++u) {
+      av[u] = sk_reduce<NM>(ra[u], xa[u]);
+      bv[u] = sk_reduce<NM>(rb[u], xb[u]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < RPC; ++u) {
+    const int m = blockIdx.y * RPC + u;
+    if (m >= rc.M) break;
+    const float4 a = av[u], b = bv[u];
+    const float r = rs_of(rs, m);  // deferred RMSNorm scale of the input row (R2)
+    float x0[4] = {a.x * r, a.y * r, a.z * r, a.w * r}, x1[4] = {b.x * r, b.y * r, b.z * r, b.w * r};
+    const int sl = m / rc.Nq, node = m % rc.Nq;
+    const int seq = rc.seq_base + sl;
+    const int Lc = rc.len[seq];
+    if (hh < H + Hkv) {  // rotate-half RoPE at pos = Lc + depth (pad batching: token count + depth)
+      const float2 *cs = rope + (size_t)((rc.pos ? rc.pos[seq] : Lc) + rc.depth[node]) * half + c;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 rr = cs[e];
+        const float y0 = x0[e] * rr.x - x1[e] * rr.y;
+        const float y1 = x1[e] * rr.x + x0[e] * rr.y;
+        x0[e] = y0;
+        x1[e] = y1;
+      }
+    }
+    T *dst;
+    if (hh < H) {
+      dst = q + ((size_t)m * H + hh) * hd;
+    } else if (hh < H + Hkv) {
+      dst = kc + (((size_t)seq * Hkv + (hh - H)) * cap + Lc + node) * hd;
+    } else {
+      dst = vc + (((size_t)seq * Hkv + (hh - H - Hkv)) * cap + Lc + node) * hd;
+    }
+    if constexpr (F32) {
+      *reinterpret_cast<float4 *>(dst + c) = make_float4(x0[0], x0[1], x0[2], x0[3]);
+      *reinterpret_cast<float4 *>(dst + c + half) = make_float4(x1[0], x1[1], x1[2], x1[3]);
+    } else {
+      uint2 lo, hi;
+      lo.x = pack_bf16(x0[0], x0[1]);
+      lo.y = pack_bf16(x0[2], x0[3]);
+      hi.x = pack_bf16(x1[0], x1[1]);
+      hi.y = pack_bf16(x1[2], x1[3]);
+      *reinterpret_cast<uint2 *>(dst + c) = lo;
+      *reinterpret_cast<uint2 *>(dst + c + half) = hi;
+    }
+  }
+  if (threadIdx.x == 0) SM_GT_END(2);
+}
 cudaError_t qkv_consumer_launch(const PartialView &pv, RowCtx rc, int H, int Hkv, int hd, const float2 *rope, void *q,
                                 void *kcache, void *vcache, int cap, RsArgs rs, cudaStream_t st) {
   const int work = (H + 2 * Hkv) * (hd / 8);
   const int nt = g_consumer_threads;
-  const dim3 grid((work + nt - 1) / nt, rc.M);
+  const int gx = (work + nt - 1) / nt;
   if (pv.planes > 1)
-    return launch_pdl(qkv_consumer_kernel<true>, grid, dim3(nt), 0, st, pv, rc, H, Hkv, hd, rope, q, kcache, vcache,
-                      cap, rs);
-  return launch_pdl(qkv_consumer_kernel<false>, grid, dim3(nt), 0, st, pv, rc, H, Hkv, hd, rope, q, kcache, vcache,
-                    cap, rs);
+    return launch_pdl(qkv_consumer_kernel<true>, dim3(gx, rc.M), dim3(nt), 0, st, pv, rc, H, Hkv, hd, rope, q,
+                      kcache, vcache, cap, rs);
+  if (rc.M >= 256)
+    return launch_pdl(qkv_consumer_rows_kernel<false, 4>, dim3(gx, (rc.M + 3) / 4), dim3(nt), 0, st, pv, rc, H, Hkv,
+                      hd, rope, q, kcache, vcache, cap, rs);
+  return launch_pdl(qkv_consumer_kernel<false>, dim3(gx, rc.M), dim3(nt), 0, st, pv, rc, H, Hkv, hd, rope, q,
+                    kcache, vcache, cap, rs);
 }
 
 // ------------------------------------------------------------------ SiLU(gate) * up
 // fused weight rows: tile t = [gate 64t..64t+63 | up 64t..64t+63]
+__global__ void __launch_bounds__(256) silu_consumer_kernel(PartialView pv, int F, bf16 *act, RsArgs rs) {
+  SM_GT_BEGIN();
+  pdl_trigger();
+  pdl_wait();
+  SM_GT_WAITED();
+  const int m = blockIdx.y;
+  const int f = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (f >= F) return;
+  const int ng = (f >> 6) * 128 + (f & 63);
+  float4 g, u;
+  if (pv.planes > 1) {
+    g = sk_get4(pv, 0, m, ng);
+    u = sk_get4(pv, 0, m, ng + 64);
+  } else {
+    const SkRef rg = sk_ref(pv, 0, m, ng), ru = sk_ref(pv, 0, m, ng + 64);
+    float4 xg[8], xu[8];
+    sk_load<8>(rg, xg);
+    sk_load<8>(ru, xu);
+    g = sk_reduce<8>(rg, xg);
+    u = sk_reduce<8>(ru, xu);
+  }
+  const float r = rs_of(rs, m);  // deferred RMSNorm scale (R2)
+  const float gg[4] = {g.x * r, g.y * r, g.z * r, g.w * r}, uu[4] = {u.x * r, u.y * r, u.z * r, u.w * r};
+  float o[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) o[e] = gg[e] / (1.0f + expf(-gg[e])) * uu[e];
+  store_act4(act, pv.planes, m, F, f, o[0], o[1], o[2], o[3]);
+  if (threadIdx.x == 0) SM_GT_END(3);
+}
 // RPC token rows per CTA: 1 for decode-sized M (latency: one round trip per CTA); 4 for
 // M >= 256 (prefill chunks, C4-V64), where the partials stream from HBM and one-row CTAs
 // spend more time launching than loading -- all RPC rows' loads are issued before any add.
 template <int RPC>
-__global__ void __launch_bounds__(256) silu_consumer_kernel(PartialView pv, int F, bf16 *act, RsArgs rs) {
+__global__ void __launch_bounds__(256) silu_consumer_rows_kernel(PartialView pv, int F, bf16 *act, RsArgs rs) {
   SM_GT_BEGIN();
   pdl_trigger();
   pdl_wait();
@@ -461,8 +579,8 @@ cudaError_t silu_consumer_launch(const PartialView &pv, int F, bf16 *act, RsArgs
   const int nt = g_consumer_threads;
   const int gx = (F / 4 + nt - 1) / nt;
   if (pv.M >= 256 && pv.planes <= 1)
-    return launch_pdl(silu_consumer_kernel<4>, dim3(gx, (pv.M + 3) / 4), dim3(nt), 0, st, pv, F, act, rs);
-  return launch_pdl(silu_consumer_kernel<1>, dim3(gx, pv.M), dim3(nt), 0, st, pv, F, act, rs);
+    return launch_pdl(silu_consumer_rows_kernel<4>, dim3(gx, (pv.M + 3) / 4), dim3(nt), 0, st, pv, F, act, rs);
+  return launch_pdl(silu_consumer_kernel, dim3(gx, pv.M), dim3(nt), 0, st, pv, F, act, rs);
 }
 
 // ------------------------------------------------------------------ logits: argmax + typical stats
@@ -798,8 +916,9 @@ void epilogue_preload() {  // force-load (see gemm_preload)
   cudaFuncGetAttributes(&fa, resid_norm_split4_kernel);
   cudaFuncGetAttributes(&fa, qkv_consumer_kernel<false>);
   cudaFuncGetAttributes(&fa, qkv_consumer_kernel<true>);
-  cudaFuncGetAttributes(&fa, silu_consumer_kernel<1>);
-  cudaFuncGetAttributes(&fa, silu_consumer_kernel<4>);
+  cudaFuncGetAttributes(&fa, qkv_consumer_rows_kernel<false, 4>);
+  cudaFuncGetAttributes(&fa, silu_consumer_kernel);
+  cudaFuncGetAttributes(&fa, silu_consumer_rows_kernel<4>);
   cudaFuncGetAttributes(&fa, logits_kernel<true>);
   cudaFuncGetAttributes(&fa, logits_kernel<false>);
   cudaFuncGetAttributes(&fa, topk_kernel<true, 10>);

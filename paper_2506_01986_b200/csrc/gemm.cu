@@ -176,7 +176,9 @@ SM_DEV void resid_rs(const GemmArgs &a, int et) {
 // FUSED: compiled with the tile-epilogue fixup (GemmArgs.epi != 0).  The plain variant
 // carries none of that code: its register count (96) leaves room on an SM for the
 // consumer kernel's CTAs to become resident (and wait) while the GEMM still runs.
-template <int BN, int SMEMKB, bool FUSED>
+// GROUPS: compiled for token-tile CTA groups (SplitPlan::rep > 1, BN = 256 only); the decode
+// variants keep rep = 1 as a compile-time constant (their index math folds away).
+template <int BN, int SMEMKB, bool FUSED, bool GROUPS = false>
 __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_constant__ GemmArgs a) {
   using C = GemmCfg<BN, SMEMKB>;
   constexpr int CH = C::kChunk;
@@ -195,7 +197,8 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const SplitPlan &pl = a.plan;
   const int c = blockIdx.x;
-  const int g = c / pl.rep, ttr = c % pl.rep;  // CTA group and token-tile lane (SplitPlan::rep)
+  const int rep = GROUPS ? pl.rep : 1;
+  const int g = c / rep, ttr = c % rep;  // CTA group and token-tile lane (SplitPlan::rep)
   const long long u0 = sk_unit0(g, pl), u1 = sk_unit0(g + 1, pl);
 
   if (warp == 0 && lane == 0) {
@@ -240,7 +243,7 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
       for (int i = 0; i < pre; ++i) {  // weights first: independent of the previous kernel
         const long long u = u0 + i;
         int bi, tt, mt;
-        sk_decode(sk_tile_r(u, pl, ttr), pl, bi, tt, mt);
+        sk_decode((int)(u / pl.kb_total) * rep + ttr, pl, bi, tt, mt);
         mbar_arrive_expect_tx(&full[i], stage_bytes);
         tma_load_2d_hint(sA + i * C::kA, &a.tmW[bi], &full[i], sk_kb(u, pl) * 64, mt * 128, pol_w);
       }
@@ -248,7 +251,7 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
       for (int i = pre; i < pre + a.l2_prefetch && u0 + i < u1; ++i) {
         const long long u = u0 + i;
         int bi, tt, mt;
-        sk_decode(sk_tile_r(u, pl, ttr), pl, bi, tt, mt);
+        sk_decode((int)(u / pl.kb_total) * rep + ttr, pl, bi, tt, mt);
         tma_prefetch_l2_2d(&a.tmW[bi], sk_kb(u, pl) * 64, mt * 128);
       }
       pdl_wait();  // activations only after the producer kernel completed
@@ -256,7 +259,7 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
       for (int i = 0; i < pre; ++i) {
         const long long u = u0 + i;
         int bi, tt, mt;
-        sk_decode(sk_tile_r(u, pl, ttr), pl, bi, tt, mt);
+        sk_decode((int)(u / pl.kb_total) * rep + ttr, pl, bi, tt, mt);
         issue_x(i, bi, tt, sk_kb(u, pl) * 64);
       }
       for (long long u = u0 + pre; u < u1; ++u) {
@@ -264,7 +267,7 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
         const int s = i % C::kStages;
         if (i >= C::kStages) mbar_wait(&empty[s], ((i / C::kStages) - 1) & 1);
         int bi, tt, mt;
-        sk_decode(sk_tile_r(u, pl, ttr), pl, bi, tt, mt);
+        sk_decode((int)(u / pl.kb_total) * rep + ttr, pl, bi, tt, mt);
         const int kc = sk_kb(u, pl) * 64;
         mbar_arrive_expect_tx(&full[s], stage_bytes);
         tma_load_2d_hint(sA + s * C::kA, &a.tmW[bi], &full[s], kc, mt * 128, pol_w);
@@ -312,13 +315,13 @@ __global__ void __launch_bounds__(192, 1) gemm_streamk_kernel(const __grid_const
     int seg = 0;
     long long u = u0;
     while (u < u1) {
-      const int t = sk_tile_r(u, pl, ttr);
-      const long long seg_end = min(u1, (long long)(t / pl.rep + 1) * pl.kb_total);
+      const int t = (int)(u / pl.kb_total) * rep + ttr;
+      const long long seg_end = min(u1, (long long)(t / rep + 1) * pl.kb_total);
       const int buf = seg & 1;
       mbar_wait(&tfull[buf], (seg >> 1) & 1);
       tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(wq * 32) << 16) + buf * BN;
-      float *dst = sk_partial(a.ws, pl, t, g - sk_first_grp(t, pl));
+      float *dst = sk_partial(a.ws, pl, t, g - sk_cta_of((long long)(t / rep) * pl.kb_total, pl));
       for (int c0 = 0; c0 < BN; c0 += CH) {
         float v[CH];
         tmem_ldc<CH>(tbase + c0, v);
@@ -386,7 +389,7 @@ struct PairCfg {
   static constexpr int kSmem = kStages * kStage + 1024 + 256;
 };
 
-template <int BN, int SMEMKB>
+template <int BN, int SMEMKB, bool GROUPS = false>
 __global__ void __launch_bounds__(192, 1) gemm_pair_kernel(const __grid_constant__ GemmArgs a) {
   using C = PairCfg<BN, SMEMKB>;
   static_assert(BN % 32 == 0 && BN >= 64, "pair tiles: BN >= 64, BN/2 a multiple of 16");
@@ -405,7 +408,8 @@ __global__ void __launch_bounds__(192, 1) gemm_pair_kernel(const __grid_constant
   const SplitPlan &pl = a.plan;
   const int rank = (int)cluster_ctarank();
   const int c = blockIdx.x >> 1;  // cluster = work unit owner
-  const int g = c / pl.rep, ttr = c % pl.rep;  // cluster group and token-tile lane (SplitPlan::rep)
+  const int rep = GROUPS ? pl.rep : 1;
+  const int g = c / rep, ttr = c % rep;  // cluster group and token-tile lane (SplitPlan::rep)
   const long long u0 = sk_unit0(g, pl), u1 = sk_unit0(g + 1, pl);
 
   if (warp == 0 && lane == 0) {
@@ -435,14 +439,14 @@ __global__ void __launch_bounds__(192, 1) gemm_pair_kernel(const __grid_constant
       const uint32_t full_cl0 = mapa_u32(smem_u32(&full[0]), 0);
       auto load_w = [&](int s, long long u) {
         int bi, tt, mt;
-        sk_decode(sk_tile_r(u, pl, ttr), pl, bi, tt, mt);
+        sk_decode((int)(u / pl.kb_total) * rep + ttr, pl, bi, tt, mt);
         if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * C::kStage);  // both CTAs' W and X bytes
         tma_load_2d_cg2_hint(sA + s * C::kA, &a.tmW[0], full_cl0 + 8 * s, sk_kb(u, pl) * 64, (mt * 2 + rank) * 128,
                              pol_w);
       };
       auto load_x = [&](int s, long long u) {
         int bi, tt, mt;
-        sk_decode(sk_tile_r(u, pl, ttr), pl, bi, tt, mt);
+        sk_decode((int)(u / pl.kb_total) * rep + ttr, pl, bi, tt, mt);
         tma_load_2d_cg2(sB + s * C::kB, &a.tmX64[0], full_cl0 + 8 * s, sk_kb(u, pl) * 64,
                         a.x_row0 + tt * BN + rank * (BN / 2));
       };
@@ -495,13 +499,13 @@ __global__ void __launch_bounds__(192, 1) gemm_pair_kernel(const __grid_constant
     int seg = 0;
     long long u = u0;
     while (u < u1) {
-      const int t = sk_tile_r(u, pl, ttr);
-      const long long seg_end = min(u1, (long long)(t / pl.rep + 1) * pl.kb_total);
+      const int t = (int)(u / pl.kb_total) * rep + ttr;
+      const long long seg_end = min(u1, (long long)(t / rep + 1) * pl.kb_total);
       const int buf = seg % C::kNBuf;
       mbar_wait(&tfull[buf], (seg / C::kNBuf) & 1);
       tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(wq * 32) << 16) + buf * BN;
-      float *dst = sk_partial(a.ws, pl, t, g - sk_first_grp(t, pl), rank);
+      float *dst = sk_partial(a.ws, pl, t, g - sk_cta_of((long long)(t / rep) * pl.kb_total, pl), rank);
       for (int c0 = 0; c0 < BN; c0 += 32) {
         float v[32];
         tmem_ld32(tbase + c0, v);
@@ -553,6 +557,29 @@ void gemm_set_l2_prefetch(int kblocks) { g_l2pf = kblocks < 0 ? 0 : kblocks; }
 
 template <int BN, int SMEMKB>
 static cudaError_t launch_bn(const GemmArgs &a, cudaStream_t st) {
+  if constexpr (BN == 256) {
+    if (a.plan.rep > 1) {  // token-tile groups (plain partial epilogue only)
+      static bool gattr = false;
+      if (!gattr) {
+        cudaError_t e = cudaFuncSetAttribute(gemm_streamk_kernel<BN, SMEMKB, false, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN, SMEMKB>::kSmem);
+        if (e != cudaSuccess) return e;
+        gattr = true;
+      }
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(a.plan.P * a.plan.rep);
+      cfg.blockDim = dim3(192);
+      cfg.dynamicSmemBytes = GemmCfg<BN, SMEMKB>::kSmem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      return cudaLaunchKernelEx(&cfg, gemm_streamk_kernel<BN, SMEMKB, false, true>, a);
+    }
+  }
+  if (a.plan.rep > 1) return cudaErrorInvalidValue;
   using C = GemmCfg<BN, SMEMKB>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -565,7 +592,7 @@ static cudaError_t launch_bn(const GemmArgs &a, cudaStream_t st) {
     attr_set = true;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(a.plan.P * a.plan.rep);
+  cfg.gridDim = dim3(a.plan.P);
   cfg.blockDim = dim3(192);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = st;
@@ -581,18 +608,18 @@ static cudaError_t launch_bn(const GemmArgs &a, cudaStream_t st) {
 // Token-tile width: the smallest supported UMMA N (multiple of 16) covering M, so one
 // token tile holds every row up to 256 (each weight tile then crosses shared memory
 // once) and padding MMA work stays small (C4: b*N = 10 x 16 = 160 rows -> BN 160).
-template <int BN, int SMEMKB>
-static cudaError_t launch_pair(const GemmArgs &a, cudaStream_t st) {
+template <int BN, int SMEMKB, bool GROUPS>
+static cudaError_t launch_pair_v(const GemmArgs &a, cudaStream_t st) {
   using C = PairCfg<BN, SMEMKB>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_pair_kernel<BN, SMEMKB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(gemm_pair_kernel<BN, SMEMKB, GROUPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2 * a.plan.P * a.plan.rep);
+  cfg.gridDim = dim3(2 * a.plan.P * (GROUPS ? a.plan.rep : 1));
   cfg.blockDim = dim3(192);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = st;
@@ -605,7 +632,15 @@ static cudaError_t launch_pair(const GemmArgs &a, cudaStream_t st) {
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, gemm_pair_kernel<BN, SMEMKB>, a);
+  return cudaLaunchKernelEx(&cfg, gemm_pair_kernel<BN, SMEMKB, GROUPS>, a);
+}
+template <int BN, int SMEMKB>
+static cudaError_t launch_pair(const GemmArgs &a, cudaStream_t st) {
+  if constexpr (BN == 256) {
+    if (a.plan.rep > 1) return launch_pair_v<BN, SMEMKB, true>(a, st);
+  }
+  if (a.plan.rep > 1) return cudaErrorInvalidValue;
+  return launch_pair_v<BN, SMEMKB, false>(a, st);
 }
 
 int gemm_pick_bn(int M) {
@@ -642,7 +677,8 @@ void gemm_plan(GemmArgs &a, int N, int K, int M, int batch) {
   // several token tiles (tensor-bound M): groups of token_tiles CTAs walk the same weight
   // k-blocks together (SplitPlan::rep) -- measured: plain stream-K re-read the weights from HBM
   // ~3.7x at M = 1024 (the token tiles of a weight tile ran far apart in time)
-  p.rep = (g_rep && p.token_tiles > 1 && !a.no_pair && want / p.token_tiles >= 1) ? p.token_tiles : 1;  // not fused
+  p.rep = (g_rep && p.bn == 256 && p.token_tiles > 1 && !a.no_pair && want / p.token_tiles >= 1) ? p.token_tiles
+                                                                                                  : 1;  // not fused
   const long long U = (long long)(p.tiles / p.rep) * p.kb_total;
   want /= p.rep;
   p.P = (int)(U < want ? U : want);
@@ -712,6 +748,8 @@ void gemm_preload() {
   cudaFuncGetAttributes(&fa, gemm_pair_kernel<160, 104>);
   cudaFuncGetAttributes(&fa, gemm_pair_kernel<192, 104>);
   cudaFuncGetAttributes(&fa, gemm_pair_kernel<256, 104>);
+  cudaFuncGetAttributes(&fa, gemm_pair_kernel<256, 104, true>);
+  cudaFuncGetAttributes(&fa, gemm_streamk_kernel<256, 216, false, true>);
 }
 
 SM_GT_READER(sm_gtrace_read_gemm)

@@ -53,10 +53,11 @@ __host__ __device__ inline int sk_tile_r(long long u, const SplitPlan &p, int tt
 }
 // first and last CTA group contributing to real tile t
 __host__ __device__ inline int sk_first_grp(int t, const SplitPlan &p) {
-  return sk_cta_of((long long)(t / p.rep) * p.kb_total, p);
+  return sk_cta_of((long long)(p.rep == 1 ? t : t / p.rep) * p.kb_total, p);
 }
 __host__ __device__ inline int sk_ncontrib(int t, const SplitPlan &p) {
-  return sk_cta_of((long long)(t / p.rep + 1) * p.kb_total - 1, p) - sk_first_grp(t, p) + 1;
+  const int tw = p.rep == 1 ? t : t / p.rep;  // (no division on the decode path)
+  return sk_cta_of((long long)(tw + 1) * p.kb_total - 1, p) - sk_cta_of((long long)tw * p.kb_total, p) + 1;
 }
 __host__ __device__ inline int sk_kb(long long u, const SplitPlan &p) { return (int)(u % p.kb_total); }
 // token tiles of one weight tile are adjacent units, so a re-read of the same
@@ -75,11 +76,16 @@ __host__ __device__ inline float *sk_partial(float *ws, const SplitPlan &p, int 
   return ws + (((size_t)t * sk_pair(p) + r) * p.maxc + k) * p.bn * 128;
 }
 // (unit tile t, first partial slot) of output column n (any 128-row half) for token row m
-__host__ __device__ inline void sk_locate(const SplitPlan &p, int bi, int m, int n, int &t, size_t &slot0) {
+// tw: the tile's index in the unit space (t itself; the weight tile when rep > 1) -- no division
+__host__ __device__ inline void sk_locate(const SplitPlan &p, int bi, int m, int n, int &t, size_t &slot0, int &tw) {
   const int pr = sk_pair(p);
   const int tt = m / p.bn, mt = n >> 7;
   t = sk_tile_of(p, bi, tt, mt / pr);
+  tw = p.rep > 1 ? bi * p.m_tiles + mt / pr : t;
   slot0 = ((size_t)t * pr + (mt % pr)) * p.maxc;
+}
+__host__ __device__ inline int sk_ncontrib_w(int tw, const SplitPlan &p) {
+  return sk_cta_of((long long)(tw + 1) * p.kb_total - 1, p) - sk_cta_of((long long)tw * p.kb_total, p) + 1;
 }
 // Where a GEMM's partials live, for the consumer kernels.  planes = 3 in the fp32
 // parity mode: every logical activation row m was fed to the GEMM as three bf16
@@ -99,8 +105,9 @@ __device__ inline float4 sk_sum4(const PartialView &v, int bi, int m, int n) {
   const int tt = m / p.bn;
   int t;
   size_t slot0;
-  sk_locate(p, bi, m, n, t, slot0);
-  const int nc = sk_ncontrib(t, p);
+  int tw;
+  sk_locate(p, bi, m, n, t, slot0, tw);
+  const int nc = sk_ncontrib_w(tw, p);
   const float4 *base =
       reinterpret_cast<const float4 *>(v.ws + slot0 * p.bn * 128 + (size_t)(m - tt * p.bn) * 128 + (n & 127));
   const size_t stride = (size_t)p.bn * 128 / 4;  // float4 between contributors
@@ -134,9 +141,10 @@ __device__ inline SkRef sk_ref(const PartialView &v, int bi, int m, int n) {
   const int tt = m / p.bn;
   int t;
   size_t slot0;
-  sk_locate(p, bi, m, n, t, slot0);
+  int tw;
+  sk_locate(p, bi, m, n, t, slot0, tw);
   SkRef r;
-  r.nc = sk_ncontrib(t, p);
+  r.nc = sk_ncontrib_w(tw, p);
   r.base = reinterpret_cast<const float4 *>(v.ws + slot0 * p.bn * 128 + (size_t)(m - tt * p.bn) * 128 + (n & 127));
   r.stride = (size_t)p.bn * 128 / 4;
   return r;
@@ -172,8 +180,9 @@ __device__ inline float sk_sum1(const PartialView &v, int bi, int m, int n) {
   const int tt = m / p.bn;
   int t;
   size_t slot0;
-  sk_locate(p, bi, m, n, t, slot0);
-  const int nc = sk_ncontrib(t, p);
+  int tw;
+  sk_locate(p, bi, m, n, t, slot0, tw);
+  const int nc = sk_ncontrib_w(tw, p);
   const float *base = v.ws + slot0 * p.bn * 128 + (size_t)(m - tt * p.bn) * 128 + (n & 127);
   const size_t stride = (size_t)p.bn * 128;
   float acc = 0.f;

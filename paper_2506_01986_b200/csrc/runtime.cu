@@ -634,15 +634,6 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
   ALLOC(m->done_cnt, 1, "tile counters");
   cudaMemset(m->tile_cnt, 0, (size_t)kMaxFusedTiles * sizeof(int));
   cudaMemset(m->done_cnt, 0, sizeof(int));
-  ALLOC(m->iota, (size_t)R, "prefill depths");
-  {
-    std::vector<int32_t> io((size_t)R);
-    for (int i = 0; i < R; ++i) io[(size_t)i] = i;
-    if (cudaMemcpy(m->iota, io.data(), io.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
-      sm_model_destroy(m);
-      return fail(SM_ERR_CUDA, "prefill depths upload");
-    }
-  }
   ALLOC(m->h, (size_t)R * d * P, "h");
   ALLOC(m->q, (size_t)R * Hhd * (m->f32 ? 2 : 1), "q");  // fp32 q in the parity mode
   ALLOC(m->attn, (size_t)R * Hhd * P, "attn");
@@ -734,6 +725,15 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
   }
   ALLOC(m->ws, need, "stream-K partials");
   m->ws_floats = need;
+  ALLOC(m->iota, (size_t)R, "prefill depths");  // last: the decode buffers keep their placement
+  {
+    std::vector<int32_t> io((size_t)R);
+    for (int i = 0; i < R; ++i) io[(size_t)i] = i;
+    if (cudaMemcpy(m->iota, io.data(), io.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+      sm_model_destroy(m);
+      return fail(SM_ERR_CUDA, "prefill depths upload");
+    }
+  }
 #undef ALLOC
   if ((s = sm_tree_create_chain(std::min(R, kMaxTreeNodes), &m->chain)) != SM_OK ||
       (s = tree_upload(m->chain)) != SM_OK) {
