@@ -536,7 +536,10 @@ static int g_force_bn = 0;
 // tiles when there are several (measured faster there, slower at M = 64 and for one 192- or
 // 256-row tile); 2 for every tile of >= 64 rows (experiments)
 static int g_pair = 1;
-static int g_pre_stages = -1;  // experiments: weight stages issued before griddepcontrol.wait (-1 = ring)  // experiments: fixed token-tile width (0 = gemm_pick_bn)
+// weight stages issued before griddepcontrol.wait: -2 (default) = 2 for single-SM GEMMs of one token tile
+// (decode: measured -0.5 % C2 step vs the whole ring, tools/bench A/B), the whole ring otherwise;
+// -1 = the whole ring; n >= 0 = n stages (sm_set_option "gemm_pre")
+static int g_pre_stages = -2;
 static int g_occ = 2;  // GEMM CTAs per SM for BN <= 64 (1..4); grid = 148 * occ
 void gemm_set_bn(int bn) { g_force_bn = bn; }
 void gemm_set_pair(int mode) { g_pair = mode < 0 ? 0 : (mode > 2 ? 2 : mode); }
@@ -695,7 +698,7 @@ size_t gemm_ws_floats(const GemmArgs &a) {
 cudaError_t gemm_launch(const GemmArgs &a0, cudaStream_t st) {
   GemmArgs a = a0;
   a.l2_prefetch = g_pdl ? g_l2pf : 0;
-  a.pre_stages = g_pre_stages;
+  a.pre_stages = g_pre_stages != -2 ? g_pre_stages : (a.plan.pair == 1 && a.plan.token_tiles == 1 ? 2 : -1);
   a.dbg_mode = g_dbg_mode;
   if (a.plan.pair == 2) {
     switch (a.plan.bn) {
