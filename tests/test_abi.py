@@ -82,3 +82,19 @@ def test_product_path_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
+
+
+def test_stage_entries_reject_bad_arguments_before_any_launch(sm):
+    """SM_ERR_INVALID_ARG (1) with a message, nothing enqueued -- checked on the host (no GPU needed)."""
+    import ctypes
+    lib = sm.lib()
+    p = ctypes.c_void_p(16)  # never dereferenced: the argument check fails first
+    for n in (0, 1025):      # K1 prefill mode: 1 <= n <= 1024
+        assert lib.sm_causal_attention(n, p, p, p, p, 1, 4, 4, 128, 2048, p, None) == 1
+        assert "sm_causal_attention" in lib.sm_last_error().decode()
+    assert lib.sm_causal_attention(16, p, p, p, p, 1, 6, 4, 128, 2048, p, None) == 1  # H % Hkv != 0
+    assert lib.sm_causal_attention(16, p, p, p, p, 1, 4, 4, 128, 8, p, None) == 1     # cap < n
+    assert lib.sm_tree_attention(None, p, p, p, p, 1, 4, 4, 128, 2048, p, None) == 1
+    assert lib.sm_gemm_bf16(p, p, None, 0, 128, 64, None) == 1                         # M < 1
+    assert lib.sm_gemm_bf16(p, p, None, 1025, 128, 64, None) == 1                      # M > 1024
+    assert lib.sm_gemm_bf16(p, p, None, 16, 128, 60, None) == 1                        # K % 8
