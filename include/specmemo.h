@@ -256,7 +256,8 @@ typedef struct {
   sm_accept_mode mode;
   float temperature, eps, alpha;   /* typical: P[tok] > min(eps, alpha*exp(-H)) at temperature T (Q10) */
   const int32_t *d_max_new;        /* [b] remaining per-turn budget, NULL = unbounded (Q15)           */
-  const int32_t *d_forced_path;    /* [b][l+1] test hook, NULL = off: accept this node path instead   */
+  const int32_t *d_forced_path;    /* [b][l+1] test hook, NULL = off: accept this node path instead;
+                                      a row starting with -1 leaves that sequence unforced          */
 } sm_accept_cfg;
 
 /* Device outputs of one step (caller-allocated int32 buffers):
@@ -280,6 +281,15 @@ sm_status sm_accept(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, const sm_a
  * lengths).  Captured into a CUDA graph on first use per (mode, hooks) and
  * replayed; graph-capturable itself.                                          */
 sm_status sm_step(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, const sm_accept_out *out, void *stream);
+/* Device-detected conditions (SURVEY §8(b) "surfaced by the next call's return code"): when the
+ * accept kernel writes status[b] = 3 (sequence b reached the bound x, nothing emitted for it;
+ * OOM reason "Cache", bound P:62-65) it also latches a mapped host word of the kv.  The
+ * next sm_verify / sm_accept / sm_step whose host call runs after that step completed returns
+ * SM_ERR_KV_CAPACITY without enqueuing anything and clears the latch (no synchronisation: a call
+ * enqueued while the detecting step still runs reports it on a later call).  With tp_size > 1
+ * the latch is reported only by sm_kv_status (ranks must issue identical calls).
+ * sm_kv_status synchronises the device and returns (and clears) the latched status (0 = none). */
+sm_status sm_kv_status(sm_kv *kv, int *h_status);
 /* Number of kernels one sm_step launches (for the bench's gpu_launches).     */
 sm_status sm_step_launches(const sm_kv *kv, int *n);
 /* Kernel timing for the bench's roofline: with enable = 1 the next sm_step
@@ -311,7 +321,10 @@ sm_status sm_causal_attention(int n, const void *d_q, const void *d_k, const voi
                               int batch, int n_heads, int n_kv_heads, int head_dim, int cap, void *d_out,
                               void *stream);
 /* K2 tcgen05 GEMM: out[M][N] fp32 = x[M][K] bf16 * w[N][K]^T bf16.  M <= 1024.
- * d_out NULL: only the GEMM runs (its partials stay in library scratch; timing). */
+ * d_out NULL: only the GEMM runs (its partials stay in library scratch; timing).
+ * The stream-K partial sums live in library scratch owned per stream (calls on different streams
+ * never share it).  Growing it synchronises the device, so under stream capture the first call of
+ * that size on that stream must have run uncaptured (else SM_ERR_UNSUPPORTED).               */
 sm_status sm_gemm_bf16(const void *d_x, const void *d_w, float *d_out, int M, int N, int K, void *stream);
 /* K3 top-k rows of fp32 logits: idx[r][k] by (value desc, index asc).        */
 sm_status sm_topk_f32(const float *d_logits, int rows, int V, int k, int32_t *d_idx, void *stream);
@@ -323,6 +336,9 @@ sm_status sm_topk_f32(const float *d_logits, int rows, int V, int k, int32_t *d_
  * together so each weight stage leaves HBM once; 0: plain stream-K).
  * Unknown names return SM_ERR_INVALID_ARG.                                     */
 sm_status sm_set_option(const char *name, int value);
+/* Restore every sm_set_option knob to the library default.  Both calls invalidate the per-step
+ * graphs captured under the previous knobs (the next sm_step re-captures).                  */
+sm_status sm_reset_options(void);
 
 const char *sm_last_error(void);
 const char *sm_version(void);

@@ -28,6 +28,7 @@ same position with the same keys (invariants I1/I3).
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 
@@ -49,9 +50,24 @@ def round_bf16(x):
 
 
 # ----------------------------------------------------------------- weights
-def _w(seed, stream, rows, cols):
-    bits = synth.weight_bits(seed, stream, rows * cols)
-    return synth.bf16_bits_to_f32(bits).astype(np.float64).reshape(rows, cols)
+def _w(seed, stream, rows, cols, dtype=np.float64):
+    n = rows * cols
+    if n <= (1 << 24):
+        bits = synth.weight_bits(seed, stream, n)
+        return synth.bf16_bits_to_f32(bits).astype(dtype).reshape(rows, cols)
+    # large tensors (timing variant at full model size): the same values, generated in chunks on
+    # several threads (numpy releases the GIL inside its ufuncs)
+    from concurrent.futures import ThreadPoolExecutor
+    out = np.empty(n, dtype=dtype)
+    chunk = 1 << 22
+
+    def fill(i0):
+        i1 = min(n, i0 + chunk)
+        out[i0:i1] = synth.bf16_bits_to_f32(synth.weight_bits(seed, stream, i1 - i0, start=i0))
+
+    with ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 1)) as ex:
+        list(ex.map(fill, range(0, n, chunk)))
+    return out.reshape(rows, cols)
 
 
 class Weights:
@@ -59,29 +75,31 @@ class Weights:
     PyTorch ``nn.Linear`` one: ``[out_features][in_features]``."""
 
     def __init__(self, cfg: dict, n_medusa: int, seed: int = 0, medusa_init: bool = False,
-                 layers: list[int] | None = None):
+                 layers: list[int] | None = None, dtype=np.float64):
         d, H, Hkv, hd, F, V = (cfg[k] for k in ("d_model", "n_heads", "n_kv_heads", "head_dim", "d_ffn", "vocab"))
         self.cfg = cfg
         self.seed = seed
-        self.embed = _w(seed, synth.STREAM_EMBED, V, d)
-        self.lm_head = _w(seed, synth.STREAM_LM_HEAD, V, d)
-        self.final_norm = np.ones(d)
+        w = lambda stream, r, c_: _w(seed, stream, r, c_, dtype)  # noqa: E731
+        self.embed = w(synth.STREAM_EMBED, V, d)
+        self.lm_head = w(synth.STREAM_LM_HEAD, V, d)
+        self.final_norm = np.ones(d, dtype=dtype)
         self.layers = []
         for li in (range(cfg["n_layers"]) if layers is None else layers):
-            s = lambda w: synth.stream_layer(li, w)  # noqa: E731
+            s = lambda name: synth.stream_layer(li, name)  # noqa: E731
             self.layers.append(dict(
-                attn_norm=np.ones(d),
-                wq=_w(seed, s("wq"), H * hd, d), wk=_w(seed, s("wk"), Hkv * hd, d),
-                wv=_w(seed, s("wv"), Hkv * hd, d), wo=_w(seed, s("wo"), d, H * hd),
-                mlp_norm=np.ones(d),
-                wg=_w(seed, s("wg"), F, d), wu=_w(seed, s("wu"), F, d), wd=_w(seed, s("wd"), d, F)))
+                attn_norm=np.ones(d, dtype=dtype),
+                wq=w(s("wq"), H * hd, d), wk=w(s("wk"), Hkv * hd, d),
+                wv=w(s("wv"), Hkv * hd, d), wo=w(s("wo"), d, H * hd),
+                mlp_norm=np.ones(d, dtype=dtype),
+                wg=w(s("wg"), F, d), wu=w(s("wu"), F, d), wd=w(s("wd"), d, F)))
         self.medusa = []
         for i in range(n_medusa):
             if medusa_init:  # Q18 "Medusa-init": R = 0, U = W_lm
-                self.medusa.append(dict(R=np.zeros((d, d)), beta=np.zeros(d), U=self.lm_head))
+                self.medusa.append(dict(R=np.zeros((d, d), dtype=dtype), beta=np.zeros(d, dtype=dtype),
+                                        U=self.lm_head))
             else:
-                self.medusa.append(dict(R=_w(seed, synth.stream_medusa(i, "R"), d, d), beta=np.zeros(d),
-                                        U=_w(seed, synth.stream_medusa(i, "U"), V, d)))
+                self.medusa.append(dict(R=w(synth.stream_medusa(i, "R"), d, d), beta=np.zeros(d, dtype=dtype),
+                                        U=w(synth.stream_medusa(i, "U"), V, d)))
 
 
 # ----------------------------------------------------------------- model
@@ -183,10 +201,84 @@ class Model:
         z = self.r32(W.lm_head @ hf)                                    # R9
         return z, hf
 
+    def forward_rows(self, kv, seq: int, toks, poss, slots, key_lists):
+        """``forward_row`` for several token rows at once, layer by layer: the same
+        arithmetic and storage points, with the projections of all rows done as one
+        matrix product per weight (BLAS; only the fp64 summation order differs from
+        the row-at-a-time routine).  In each layer every row's K/V is written before
+        any row attends, so a row may attend to slots of rows earlier in the same
+        call (tree ancestors, causal prefill tokens).  Returns (Z [n][V], HF [n][d]).
+
+        The weights' array dtype is the arithmetic type: float64 (default, the parity
+        oracle) or float32 (``Weights(dtype=np.float32)``: the timing variant of
+        SURVEY §8.d.5 for the bench's cpu_baseline, fp32 batched BLAS)."""
+        W = self.W
+        dt = W.embed.dtype
+        c = lambda a: np.asarray(a, dtype=dt)  # noqa: E731  (storage rounding works in float64)
+        n = len(toks)
+        toks = [int(t) for t in toks]
+        X = c(self.r16(W.embed[toks]))                                  # R1
+        for li, Lw in enumerate(W.layers):
+            h = c(self.r16(X * Lw["attn_norm"]))                        # R2 (deferred RMSNorm)
+            rs = c(self.r32(self._rms_scale_rows(X)))[:, None]
+            q = (rs * (h @ Lw["wq"].T)).reshape(n, self.H, self.hd)    # R3
+            k = (rs * (h @ Lw["wk"].T)).reshape(n, self.Hkv, self.hd)
+            v = (rs * (h @ Lw["wv"].T)).reshape(n, self.Hkv, self.hd)
+            Q = np.empty_like(q)
+            for i in range(n):
+                Q[i] = c(self.r16(self.rope(self.r32(q[i]), poss[i])))
+                kv.K[li][seq][:, slots[i], :] = self.r16(self.rope(self.r32(k[i]), poss[i]))
+                kv.V[li][seq][:, slots[i], :] = self.r16(v[i])
+            O = c(self.r16(self._attention_rows(Q, kv.K[li][seq], kv.V[li][seq], key_lists)))  # R4
+            X = c(self.r32(X + self.r32(O @ Lw["wo"].T)))              # R5
+            h2 = c(self.r16(X * Lw["mlp_norm"]))                        # R2 (deferred)
+            rs2 = c(self.r32(self._rms_scale_rows(X)))[:, None]
+            A = c(self.r16(self.silu(self.r32(rs2 * (h2 @ Lw["wg"].T))) * self.r32(rs2 * (h2 @ Lw["wu"].T))))  # R6
+            X = c(self.r32(X + self.r32(A @ Lw["wd"].T)))              # R7
+        X64 = np.asarray(X, dtype=np.float64)
+        HF = c(self.r16(X64 / np.sqrt(np.mean(X64 * X64, axis=1) + self.eps)[:, None] * W.final_norm))  # R8
+        Z = self.r32(HF @ W.lm_head.T)                                  # R9
+        return Z, HF
+
+    def _attention_rows(self, Q, Kl, Vl, key_lists):
+        """``attention`` for several rows: Q [n][H][hd]; Kl, Vl [Hkv][cap][hd] (one sequence's
+        cache layer).  The key slots shared by every row (the common prefix 0..c-1: the committed
+        cache) are scored for all rows in one product per kv head; each row's remaining slots
+        (its tree ancestors and itself, or its causal chunk tokens) are scored on their own; the
+        softmax runs over the row's full key list in the same logical order, and P.V is the sum
+        of the two parts.  Returns O [n][H * hd]."""
+        n = Q.shape[0]
+        c = min(len(k) for k in key_lists)
+        for k in key_lists:                       # longest prefix 0, 1, ..., c-1 shared by all rows
+            a = np.asarray(k[:c])
+            bad = np.flatnonzero(a != np.arange(a.size))
+            c = int(bad[0]) if bad.size else c
+        scale = 1.0 / math.sqrt(self.hd)
+        O = np.zeros((n, self.H, self.hd), dtype=Q.dtype)
+        for h in range(self.Hkv):
+            hs = slice(h * self.G, (h + 1) * self.G)
+            Kh, Vh = Kl[h], Vl[h]
+            Sp = (Q[:, hs, :].reshape(n * self.G, self.hd) @ Kh[:c].T).reshape(n, self.G, c) * scale
+            for i in range(n):
+                rest = key_lists[i][c:]
+                Sr = (Q[i, hs, :] @ Kh[rest].T) * scale                     # [G][r]
+                S = np.concatenate([Sp[i], Sr], axis=1)
+                p = np.exp(S - S.max(axis=1, keepdims=True))
+                p = p / p.sum(axis=1, keepdims=True)
+                O[i, hs, :] = p[:, :c] @ Vh[:c] + p[:, c:] @ Vh[rest]
+        return O.reshape(n, self.H * self.hd)
+
+    def _rms_scale_rows(self, X):
+        """rs per row = 1 / sqrt(mean(x^2) + eps) (as rms_scale, in float64)."""
+        X = np.asarray(X, dtype=np.float64)
+        return 1.0 / np.sqrt(np.mean(X * X, axis=1) + self.eps)
+
     def head_logits(self, i: int, hf):
         """Medusa-1 head i: u = U_i (hf + SiLU(R_i hf + beta_i))   (R10)."""
         Hw = self.W.medusa[i]
-        r = self.r16(hf + self.silu(self.r32(Hw["R"] @ hf + Hw["beta"])))
+        dt = Hw["U"].dtype
+        hf = np.asarray(hf, dtype=dt)
+        r = np.asarray(self.r16(hf + self.silu(self.r32(Hw["R"] @ hf + Hw["beta"]))), dtype=dt)
         return self.r32(Hw["U"] @ r)
 
 
@@ -194,10 +286,10 @@ class KVCache:
     """Bounded KV cache (Eq. 1): per layer [b][Hkv][x + N][hd]; the last
     N slots of each sequence are the tree scratch (reading Q14)."""
 
-    def __init__(self, n_layers: int, batch: int, n_kv_heads: int, capacity: int, head_dim: int):
+    def __init__(self, n_layers: int, batch: int, n_kv_heads: int, capacity: int, head_dim: int, dtype=np.float64):
         self.capacity = capacity
-        self.K = [np.zeros((batch, n_kv_heads, capacity, head_dim)) for _ in range(n_layers)]
-        self.V = [np.zeros((batch, n_kv_heads, capacity, head_dim)) for _ in range(n_layers)]
+        self.K = [np.zeros((batch, n_kv_heads, capacity, head_dim), dtype=dtype) for _ in range(n_layers)]
+        self.V = [np.zeros((batch, n_kv_heads, capacity, head_dim), dtype=dtype) for _ in range(n_layers)]
 
 
 def argmax_lowest(z) -> int:

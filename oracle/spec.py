@@ -51,8 +51,13 @@ def typical_stats(z, temperature: float):
 class Session:
     """b independent sequences sharing one model and one static tree."""
 
-    def __init__(self, model: Model, choices: list[list[int]], batch: int, max_seq_len: int, topk: int = 10):
+    def __init__(self, model: Model, choices: list[list[int]], batch: int, max_seq_len: int, topk: int = 10,
+                 batched: bool = False):
+        """batched=True: prefill and verify push all their rows through ``Model.forward_rows``
+        (one BLAS product per weight and layer) instead of one row at a time -- the same
+        arithmetic up to fp64 summation order, for wide models in tests and for timing."""
         self.m = model
+        self.batched = batched
         self.tree = T.build(choices, topk) if choices else T.build([], topk)
         self.N = self.tree.N
         self.l = max(self.tree.max_depth, 0)
@@ -61,10 +66,13 @@ class Session:
         self.K = topk
         self.x = max_seq_len
         self.b = batch
-        self.kv = KVCache(model.n_layers, batch, model.Hkv, max_seq_len + self.N, model.hd)
+        self.kv = KVCache(model.n_layers, batch, model.Hkv, max_seq_len + self.N, model.hd,
+                          dtype=model.W.embed.dtype)
         self.Lc = [0] * batch
         self.root = [None] * batch
         self.topk_tok = [None] * batch                   # [l][K] token ids per sequence
+        self.last_z = [None] * batch
+        self.last_hf = [None] * batch
         self.committed = [[] for _ in range(batch)]
         self.leaves = T.leaves(self.tree)
         self.dfs = T.dfs_order(self.tree)
@@ -72,6 +80,7 @@ class Session:
 
     # ------------------------------------------------------------ heads
     def _propose_state(self, seq, z, hf):
+        self.last_z[seq], self.last_hf[seq] = z, hf                # the accepted node's rows (tests)
         self.root[seq] = argmax_lowest(z)                       # Q8: root = argmax in both modes
         self.topk_tok[seq] = [topk_desc(self.m.head_logits(i, hf), self.K) for i in range(self.l)]
 
@@ -85,9 +94,17 @@ class Session:
         if self.Lc[seq] + P > self.x:
             raise KVCapacityError(f"prefill {P} at Lc={self.Lc[seq]} exceeds x={self.x}")
         z = hf = None
-        for i, tok in enumerate(tokens):
-            pos = self.Lc[seq] + i
-            z, hf = self.m.forward_row(self.kv, seq, int(tok), pos, pos, list(range(pos + 1)))
+        if self.batched:
+            Lc = self.Lc[seq]
+            for c0 in range(0, P, 256):  # causal chunks
+                idx = range(c0, min(P, c0 + 256))
+                Z, HF = self.m.forward_rows(self.kv, seq, [tokens[i] for i in idx], [Lc + i for i in idx],
+                                            [Lc + i for i in idx], [list(range(Lc + i + 1)) for i in idx])
+            z, hf = Z[-1], HF[-1]
+        else:
+            for i, tok in enumerate(tokens):
+                pos = self.Lc[seq] + i
+                z, hf = self.m.forward_row(self.kv, seq, int(tok), pos, pos, list(range(pos + 1)))
         self.Lc[seq] += P
         self.committed[seq].extend(int(t) for t in tokens)
         self._propose_state(seq, z, hf)
@@ -107,6 +124,11 @@ class Session:
         if Lc >= self.x:
             raise KVCapacityError(f"verify at Lc={Lc} >= x={self.x}")
         tr = self.tree
+        if self.batched:
+            keys = [list(range(Lc)) + [Lc + a for a in T.ancestors(tr, n)] + [Lc + n] for n in range(self.N)]
+            Z, HF = self.m.forward_rows(self.kv, seq, tok, [Lc + tr.depth[n] for n in range(self.N)],
+                                        [Lc + n for n in range(self.N)], keys)
+            return list(Z), list(HF)
         Z, HF = [None] * self.N, [None] * self.N
         for n in range(self.N):                                   # canonical order: parents first
             keys = list(range(Lc)) + [Lc + a for a in T.ancestors(tr, n)] + [Lc + n]
@@ -166,6 +188,10 @@ class Session:
         a_eff = min(a, budget-1, x-Lc-1) (Q14, Q15); tau = a_eff + 1."""
         tok, pos = self.propose(seq)
         Z, HF = self.verify(seq, tok)
+        return self.finish(seq, tok, pos, Z, HF, mode, budget, **typ)
+
+    def finish(self, seq: int, tok, pos, Z, HF, mode: str = "greedy", budget: int | None = None, **typ):
+        """Steps 3-6 of a step on verified rows: accept, emit, compact, next state."""
         a, chosen, best_leaf, path = self.accept(tok, Z, mode, **typ)
         Lc = self.Lc[seq]
         a_eff = a

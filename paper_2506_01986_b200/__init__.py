@@ -459,6 +459,12 @@ class KVCache:
         _check(lib().sm_kv_positions(self._h, out.ctypes.data_as(ctypes.c_void_p)))
         return out
 
+    def status(self) -> int:
+        """sm_kv_status: latched device-detected status (3 = a sequence reached the bound x), cleared."""
+        v = ctypes.c_int()
+        _check(lib().sm_kv_status(self._h, ctypes.byref(v)))
+        return v.value
+
     def lengths(self) -> np.ndarray:
         out = np.zeros(self.batch, np.int32)
         _check(lib().sm_kv_lengths(self._h, out.ctypes.data_as(ctypes.c_void_p)))
@@ -553,3 +559,8 @@ def version() -> str:
 def set_option(name: str, value: int) -> None:
     """sm_set_option: process-wide launch knobs ("pdl", "gemm_ctas", "attn_tc", ...)."""
     _check(lib().sm_set_option(name.encode(), int(value)))
+
+
+def reset_options() -> None:
+    """sm_reset_options: every knob back to the library default."""
+    _check(lib().sm_reset_options())

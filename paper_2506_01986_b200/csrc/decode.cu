@@ -76,8 +76,8 @@ __global__ void __launch_bounds__(256) accept_kernel(const __grid_constant__ Acc
     // walk every node's ancestor chain (depth <= l), pick (depth, ll, -dfs) max
     int best = 0, bdep = 0, bdfs = a.t.dfs_pos[0];
     float bll = 0.f;
-    if (a.forced_path) {
-      const int32_t *fp = a.forced_path + (size_t)bb * (a.t.l + 1);
+    const int32_t *fp = a.forced_path ? a.forced_path + (size_t)bb * (a.t.l + 1) : nullptr;
+    if (fp && fp[0] >= 0) {  // test hook: this sequence accepts the given path (row -1.. = not forced)
       for (int j = 0; j <= a.t.l; ++j)
         if (fp[j] >= 0) best = fp[j];
     } else {
@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(256) accept_kernel(const __grid_constant__ Acc
   }
   a.n_emit[bb] = a_eff + 1;
   a.status[bb] = status;
+  if (status && a.sticky) *(volatile int32_t *)a.sticky = status;  // surfaced by the next host call
   if (a_eff >= 0) {
     const int row = (int)rowbase + path[a_eff];
     a.acc_row[bb] = row;
@@ -208,10 +209,11 @@ __global__ void commit_kernel(int32_t *len, const int32_t *n_emit, int32_t *root
 }
 cudaError_t commit_launch(int b, int32_t *len, const int32_t *n_emit, int32_t *root, const int32_t *root_next,
                           const int32_t *acc_row, const bf16 *hf, int d, bf16 *head_in, int32_t *emitted_total,
-                          cudaStream_t st) {
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) return cudaErrorInvalidValue;
-  if (cs == cudaStreamCaptureStatusActive)
+                          bool early, cudaStream_t st) {
+  // early (entry) trigger only inside the library's own per-step graph (sm_step's capture): a
+  // caller that captures several steps into its own graph gets the late trigger, so the next
+  // step's tree attention (it reads Lc before its griddepcontrol.wait) cannot race this write.
+  if (early)
     return launch_pdl(commit_kernel<false>, dim3(b), dim3(256), 0, st, len, n_emit, root, root_next, acc_row, hf, d,
                       head_in, emitted_total);
   return launch_pdl(commit_kernel<true>, dim3(b), dim3(256), 0, st, len, n_emit, root, root_next, acc_row, hf, d,

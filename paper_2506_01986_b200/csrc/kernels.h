@@ -438,13 +438,14 @@ struct AcceptArgs {
   int32_t *acc_len, *best_leaf, *path, *emit_tok, *n_emit, *status;
   int32_t *acc_row;            // [b] row index of the last emitted node
   int32_t *root_next;          // [b]
+  int32_t *sticky;             // nullable: mapped host word, set to a nonzero status (sm_kv surfacing)
 };
 cudaError_t accept_launch(const AcceptArgs &a, cudaStream_t st);
 cudaError_t compact_launch(bf16 *kv_base, int L, int b, int Hkv, int cap, int hd, const int32_t *len,
                            const int32_t *path, int path_ld, const int32_t *n_emit, cudaStream_t st);
 cudaError_t commit_launch(int b, int32_t *len, const int32_t *n_emit, int32_t *root, const int32_t *root_next,
                           const int32_t *acc_row, const bf16 *hf, int d, bf16 *head_in, int32_t *emitted_total,
-                          cudaStream_t st);  // len == nullptr: lengths advanced elsewhere (pad batching)
+                          bool early, cudaStream_t st);  // len == nullptr: lengths advanced elsewhere (pad batching)
 cudaError_t advance_len_launch(int32_t *len, int seq, int n, int32_t *pos_len, cudaStream_t st);
 cudaError_t set_root_launch(int32_t *root, int seq, const int32_t *argmax_row, const bf16 *hf_row, int d,
                             bf16 *head_in_row, cudaStream_t st);

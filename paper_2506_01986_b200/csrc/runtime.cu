@@ -976,14 +976,21 @@ extern "C" sm_status sm_workspace_bytes(const sm_model_cfg *cfg, size_t *bytes) 
 }
 
 // ---------------------------------------------------------------- bounded KV
+// Bumped by sm_set_option / sm_reset_options: a graph captured under other launch knobs is stale
+// (the knobs are process-wide and baked into the captured kernels).
+static int g_opt_version = 0;
+// True while sm_step captures its own per-step graph (the only place the commit may trigger early).
+static thread_local bool g_lib_capture = false;
+
 struct GraphKey {
+  int ver;
   int prof;
   int mode;
   float T, eps, alpha;
   const void *max_new, *forced, *o0, *o1, *o2, *o3, *o4, *o5;
   bool operator<(const GraphKey &o) const {
-    return std::tie(prof, mode, T, eps, alpha, max_new, forced, o0, o1, o2, o3, o4, o5) <
-           std::tie(o.prof, o.mode, o.T, o.eps, o.alpha, o.max_new, o.forced, o.o0, o.o1, o.o2, o.o3, o.o4, o.o5);
+    return std::tie(ver, prof, mode, T, eps, alpha, max_new, forced, o0, o1, o2, o3, o4, o5) <
+           std::tie(o.ver, o.prof, o.mode, o.T, o.eps, o.alpha, o.max_new, o.forced, o.o0, o.o1, o.o2, o.o3, o.o4, o.o5);
   }
 };
 
@@ -1003,6 +1010,7 @@ struct sm_kv {
   int pad_words = 0;
   CUtensorMap tmKV;
   std::map<GraphKey, cudaGraphExec_t> graphs;
+  int32_t *h_sticky = nullptr, *d_sticky = nullptr;  // mapped host word: device-detected status
   int step_launches = 0;
   int prof = 0;
   std::vector<ProfEvent> prof_events;
@@ -1058,6 +1066,12 @@ extern "C" sm_status sm_kv_bind(sm_model *m, const sm_tree *tree, int batch, int
     sm_kv_destroy(kv);
     return s;
   }
+  if (cudaHostAlloc((void **)&kv->h_sticky, sizeof(int32_t), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer((void **)&kv->d_sticky, kv->h_sticky, 0) != cudaSuccess) {
+    sm_kv_destroy(kv);
+    return fail(SM_ERR_DEVICE_OOM, "Buffer: mapped status word");
+  }
+  *(volatile int32_t *)kv->h_sticky = 0;
   const uint64_t rows = (uint64_t)need / 2 / m->hd;
   if (!m->f32 && (s = kv_map(&kv->tmKV, d_mem, rows, m->hd)) != SM_OK) {  // bf16 kernels' TMA view
     sm_kv_destroy(kv);
@@ -1097,6 +1111,7 @@ extern "C" void sm_kv_destroy(sm_kv *kv) {
   cudaFree(kv->tree_tok);
   cudaFree(kv->pos_len);
   cudaFree(kv->pad);
+  if (kv->h_sticky) cudaFreeHost(kv->h_sticky);
   if (kv->t) sm_tree_destroy(kv->t);
   delete kv;
 }
@@ -1429,12 +1444,13 @@ static sm_status enqueue_accept(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg
   a.status = o->status;
   a.acc_row = kv->acc_row;
   a.root_next = kv->root_next;
+  a.sticky = kv->d_sticky;
   CK(accept_launch(a, st));
   ++nl;
   CK(compact_launch(kv->base, m->L, kv->b, m->Hkv, kv->cap, m->hdu, kv->len, o->path, kv->t->l + 1, o->n_emit, st));
   ++nl;
   CK(commit_launch(kv->b, kv->pad_mode ? nullptr : kv->len, o->n_emit, kv->root, kv->root_next, kv->acc_row, m->hf,
-                   m->d * m->P, m->head_in, kv->emitted, st));
+                   m->d * m->P, m->head_in, kv->emitted, g_lib_capture, st));
   ++nl;
   if (kv->pad_mode) {  // every cache advances by the batch's longest acceptance; the rest are pads
     CK(pad_commit_launch(kv->b, kv->len, kv->pos_len, o->n_emit, kv->pad, kv->pad_words, st));
@@ -1452,6 +1468,33 @@ static sm_status check_accept(const sm_accept_cfg *cfg, const sm_accept_out *o) 
   return SM_OK;
 }
 
+// Device-detected conditions (accept kernel: status[b] = 3, a sequence reached the bound x) are
+// latched in a mapped host word and returned, once, by the next sm_verify / sm_accept / sm_step
+// whose host call runs after the detecting step completed (no synchronisation: a call enqueued
+// while that step is still running reports it on a later call; sm_kv_status synchronises).
+static sm_status kv_surface(sm_kv *kv) {
+  // tensor parallel: every rank must issue the same calls, and ranks observe the word at different
+  // times -- there only the synchronising sm_kv_status reports it
+  if (kv->m->tp > 1) return SM_OK;
+  volatile int32_t *w = (volatile int32_t *)kv->h_sticky;
+  if (!w || *w == 0) return SM_OK;
+  const int v = *w;
+  *w = 0;
+  if (v == 3)
+    return fail(SM_ERR_KV_CAPACITY, "Cache: a sequence reached the KV bound x at an earlier step (status[b] = 3, "
+                                    "nothing emitted for it); this call enqueued nothing");
+  return fail(SM_ERR_CUDA, "device-detected status " + std::to_string(v));
+}
+
+extern "C" sm_status sm_kv_status(sm_kv *kv, int *h_status) {
+  if (!kv || !h_status) return fail(SM_ERR_INVALID_ARG, "sm_kv_status: null");
+  CK(cudaDeviceSynchronize());
+  volatile int32_t *w = (volatile int32_t *)kv->h_sticky;
+  *h_status = *w;
+  *w = 0;
+  return SM_OK;
+}
+
 extern "C" sm_status sm_propose(sm_model *m, sm_kv *kv, int32_t *d_tree_tok, int32_t *d_pos, void *stream) {
   if (!m || !kv || !d_tree_tok) return fail(SM_ERR_INVALID_ARG, "sm_propose: bad arguments");
   int nl = 0;
@@ -1461,6 +1504,7 @@ extern "C" sm_status sm_propose(sm_model *m, sm_kv *kv, int32_t *d_tree_tok, int
 
 extern "C" sm_status sm_verify(sm_model *m, sm_kv *kv, const int32_t *d_tree_tok, float *d_logits, void *stream) {
   if (!m || !kv || !d_tree_tok) return fail(SM_ERR_INVALID_ARG, "sm_verify: bad arguments");
+  CKS(kv_surface(kv));
   cudaStream_t st = (cudaStream_t)stream;
   int nl = 0;
   if (d_tree_tok != kv->tree_tok)
@@ -1478,6 +1522,7 @@ extern "C" sm_status sm_accept(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg,
                                void *stream) {
   if (!m || !kv) return fail(SM_ERR_INVALID_ARG, "sm_accept: bad arguments");
   CKS(check_accept(cfg, out));
+  CKS(kv_surface(kv));
   int nl = 0;
   tp_begin(m);
   CKS(enqueue_accept(m, kv, cfg, out, (cudaStream_t)stream, nl));
@@ -1504,8 +1549,9 @@ extern "C" sm_status sm_step(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, c
                              void *stream) {
   if (!m || !kv) return fail(SM_ERR_INVALID_ARG, "sm_step: bad arguments");
   CKS(check_accept(cfg, out));
+  CKS(kv_surface(kv));
   cudaStream_t st = (cudaStream_t)stream;
-  GraphKey key{kv->prof, (int)cfg->mode, cfg->temperature, cfg->eps, cfg->alpha, cfg->d_max_new, cfg->d_forced_path,
+  GraphKey key{g_opt_version, kv->prof, (int)cfg->mode, cfg->temperature, cfg->eps, cfg->alpha, cfg->d_max_new, cfg->d_forced_path,
                out->acc_len, out->best_leaf, out->path, out->emit_tok, out->n_emit, out->status};
   auto it = kv->graphs.find(key);
   if (it == kv->graphs.end()) {
@@ -1529,7 +1575,9 @@ extern "C" sm_status sm_step(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, c
     CK(cudaStreamBeginCapture(m->cap_stream, cudaStreamCaptureModeRelaxed));
     cudaEvent_t ev_step = nullptr;
     prof_begin(m->cap_stream, &ev_step);  // kind 3: the whole (event-serialised) step
+    g_lib_capture = true;
     sm_status s = enqueue_step(m, kv, cfg, out, m->cap_stream, nl);
+    g_lib_capture = false;
     prof_end(m->cap_stream, ev_step, 3, 0.0);
     cudaError_t e = cudaStreamEndCapture(m->cap_stream, &g);
     g_prof = nullptr;
@@ -1580,17 +1628,25 @@ extern "C" sm_status sm_step_launches(const sm_kv *kv, int *n) {
 }
 
 // ---------------------------------------------------------------- stage APIs (parity tests, K1 sweep)
-static void *g_scratch = nullptr;
-static size_t g_scratch_bytes = 0;
-static sm_status scratch(size_t bytes, void **p) {
-  if (bytes > g_scratch_bytes) {
-    cudaFree(g_scratch);
-    g_scratch = nullptr;
-    g_scratch_bytes = 0;
-    if (cudaMalloc(&g_scratch, bytes) != cudaSuccess) return fail(SM_ERR_DEVICE_OOM, "Buffer: stage scratch");
-    g_scratch_bytes = bytes;
+// Stage entries (sm_gemm_bf16) keep their stream-K partial sums in scratch owned per stream, so
+// calls on different streams never share it.  Growing it frees the old buffer after a device sync,
+// which stream capture forbids: under capture the scratch must already be large enough (a first
+// uncaptured call of the same size on that stream sizes it), else SM_ERR_UNSUPPORTED.
+static std::map<cudaStream_t, std::pair<void *, size_t>> g_scratch;
+static sm_status scratch(size_t bytes, cudaStream_t st, void **p) {
+  auto &e = g_scratch[st];
+  if (bytes > e.second) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(st, &cs));
+    if (cs != cudaStreamCaptureStatusNone)
+      return fail(SM_ERR_UNSUPPORTED, "stage scratch must grow during stream capture: call once uncaptured first");
+    CK(cudaDeviceSynchronize());  // earlier work on any stream may still read the old buffer
+    cudaFree(e.first);
+    e = {nullptr, 0};
+    if (cudaMalloc(&e.first, bytes) != cudaSuccess) return fail(SM_ERR_DEVICE_OOM, "Buffer: stage scratch");
+    e.second = bytes;
   }
-  *p = g_scratch;
+  *p = e.first;
   return SM_OK;
 }
 
@@ -1657,7 +1713,7 @@ extern "C" sm_status sm_gemm_bf16(const void *d_x, const void *d_w, float *d_out
   CKS(act_map(a, 0, d_x, M, K));
   const size_t need = ws_need(a, M);
   void *scr = nullptr;
-  CKS(scratch(need * 4, &scr));
+  CKS(scratch(need * 4, (cudaStream_t)stream, &scr));
   int nl = 0;
   PartialView pv;
   if (g_epi_test && !d_out) {  // experiments: the fused SiLU tile epilogue on scratch buffers
@@ -1699,9 +1755,32 @@ extern "C" sm_status sm_topk_f32(const float *d_logits, int rows, int V, int k, 
   return SM_OK;
 }
 
+extern "C" sm_status sm_reset_options(void) {
+  gemm_set_pdl(true);
+  gemm_set_ctas(0);
+  gemm_set_rep(1);
+  gemm_set_l2_prefetch(0);
+  gemm_set_bn(0);
+  gemm_set_small(2);
+  gemm_set_debug_mode(0);
+  gemm_set_occ_smalln(0);
+  gemm_set_pair(1);
+  gemm_set_pre_stages(-2);
+  consumer_set_threads(256);
+  attention_set_tc(1);
+  attention_set_l2pf(0);
+  attention_set_splits(0);
+  g_fused = 0;
+  g_epi_test = 0;
+  g_ablate = 0;
+  ++g_opt_version;
+  return SM_OK;
+}
+
 extern "C" sm_status sm_set_option(const char *name, int value) {
   if (!name) return fail(SM_ERR_INVALID_ARG, "sm_set_option: null name");
   const std::string n(name);
+  ++g_opt_version;
   if (n == "pdl") {
     gemm_set_pdl(value != 0);
   } else if (n == "gemm_ctas") {

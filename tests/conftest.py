@@ -16,3 +16,15 @@ def pytest_configure(config):
 @pytest.fixture(scope="session")
 def golden_dir():
     return os.path.join(ROOT, "tests", "golden")
+
+
+@pytest.fixture(autouse=True)
+def _restore_library_options(request):
+    """sm_set_option knobs are process-wide: restore the library defaults after every GPU test
+    so a test that flips one (gemm_pair, fused_epilogue, pdl, ...) cannot leak it into the next."""
+    yield
+    if request.node.get_closest_marker("gpu") is None:
+        return
+    mod = sys.modules.get("paper_2506_01986_b200")
+    if mod is not None and getattr(mod, "_lib", None) is not None:
+        mod.reset_options()

@@ -86,7 +86,7 @@ def test_gemm_pair_matches_fp64(sm, M, N, K):
     try:
         test_gemm_matches_fp64(sm, M, N, K)
     finally:
-        sm.set_option("gemm_pair", 0)
+        sm.reset_options()  # the library defaults (gemm_pair = 1)
 
 
 # ------------------------------------------------------------------ K1 tree attention

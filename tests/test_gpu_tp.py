@@ -30,9 +30,13 @@ def sm():
     assert torch.cuda.is_available(), "GPU tests need a CUDA device"
     import paper_2506_01986_b200 as sm
     sm.lib()
+    return sm
+
+
+@pytest.fixture(autouse=True)
+def _no_pdl(sm):
+    """Every test of this module runs with PDL off (conftest restores the defaults after each)."""
     sm.set_option("pdl", 0)
-    yield sm
-    sm.set_option("pdl", 1)
 
 
 class Ranks:
