@@ -192,10 +192,10 @@ WORKLOADS = {
                desc="C1: tiny random-init Llama (2 layers, d=64, 4 heads, V=256) + 3 Medusa heads, 16-node tree, "
                     "bs=1, 32-token prompt; KV x=64 in the parity tests, raised here to 32 + (l+1) x steps so every "
                     "timed step emits"),
-    "c3": dict(model="vicuna13b", n_medusa=4, tree="V64", batch=1, x=2304, mode="typical",
-               desc="C3: Vicuna-13B-shaped + 4 Medusa heads, V64 tree, bs=1, mid-conversation of an 8-turn "
-                    "MT-Bench-length chat (KV bounded to 2304 = sum of turns), typical acceptance T=0.7 eps=0.09 "
-                    "alpha=0.3"),
+    "c3": dict(model="vicuna13b", n_medusa=4, tree="V64", batch=1, x=2304, mode="typical", turns=8, gen=128,
+               desc="C3: Vicuna-13B-shaped + 4 Medusa heads, V64 tree, bs=1, an 8-turn MT-Bench-length chat: "
+                    "turn t = prefill of P_t = 32 + h mod 129 prompt tokens, then 128 generated tokens (typical "
+                    "acceptance T=0.7 eps=0.09 alpha=0.3); KV bounded to x = sum_t (P_t + 128) (+64 scratch)"),
     "c4v64": dict(model="llama70b", n_medusa=4, tree="V64", batch=10, x=416, mode="greedy", tp=True,
                   desc="C4 with the paper's default tree: Llama-2-70B-shaped (GQA 64/8) + 4 Medusa heads, V64 tree "
                        "(64 nodes), bs=10 ragged prompts of 32-160 tokens, KV bounded to 416 (+64), greedy; M = 640 "
@@ -270,23 +270,28 @@ def run_ours(args, world, rank, local) -> dict | None:
     torch.cuda.synchronize()
     barrier(world)
     st = torch.cuda.current_stream()
-    L0 = kv.lengths().astype(np.int64)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier(world)
-    torch.cuda.synchronize()
-    ev0.record(st)
-    for _ in range(args.steps):
-        kv.step(acfg, out)
-    ev1.record(st)
-    torch.cuda.synchronize()
-    barrier(world)
+    # the timed region: exactly K steps, bracketed by barrier + synchronize, device-timed with CUDA
+    # events on the launching stream, max over ranks; repeated args.reps times, median reported
+    reps = []
+    for _ in range(max(1, args.reps)):
+        L0 = kv.lengths().astype(np.int64)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier(world)
+        torch.cuda.synchronize()
+        ev0.record(st)
+        for _ in range(args.steps):
+            kv.step(acfg, out)
+        ev1.record(st)
+        torch.cuda.synchronize()
+        barrier(world)
+        ms = reduce_max(ev0.elapsed_time(ev1), world)
+        L1 = kv.lengths().astype(np.int64)
+        # replicas: every rank's tokens count; tensor parallel: the group emits one stream
+        tokens = reduce_sum(float((L1 - L0).sum()), world) if tp == 1 else float((L1 - L0).sum())
+        reps.append((tokens / (ms / 1e3), ms, tokens, L0, L1))
     clk = clocks.stop()
-    ms = ev0.elapsed_time(ev1)
-    L1 = kv.lengths().astype(np.int64)
-    ms_max = reduce_max(ms, world)
-    # replicas: every rank's tokens count; tensor parallel: the group emits one stream
-    tokens = reduce_sum(float((L1 - L0).sum()), world) if tp == 1 else float((L1 - L0).sum())
-    value = tokens / (ms_max / 1e3)
+    med = sorted(reps, key=lambda r: r[0])[len(reps) // 2]
+    value, ms_max, tokens, L0, L1 = med
     tau = float((L1 - L0).sum()) / args.steps / b
     launches = kv.step_launches()
 
@@ -371,6 +376,9 @@ def run_ours(args, world, rank, local) -> dict | None:
 
     # ---- K1 tree-attention point of the C5 sweep (geometry A, N=64)
     k1 = run_k1_point(sm, args) if args.k1 and args.config == "c2" else None
+    acc_lines = None
+    if args.extra and args.config == "c2" and world == 1:
+        acc_lines = run_c2_acceptance_lines(sm, cfg, model, tree, kv.prompts[0], wl["x_run"], wl)
 
     if rank != 0:
         return None
@@ -400,7 +408,8 @@ def run_ours(args, world, rank, local) -> dict | None:
         "tau": round(tau, 4), "steps_per_s": round(args.steps / (ms_max / 1e3), 3),
         "roofline": {"kernel": f"K2 tcgen05 GEMM (all {g_n} weight GEMM launches of one step)", "bound": "hbm",
                      "achieved": round(gemm_gbs, 1), "peak": pk["hbm"], "unit": "GB/s",
-                     "frac": round(gemm_gbs / pk["hbm"], 4), "traffic": gemm_traffic(),
+                     "frac": round(gemm_gbs / pk["hbm"], 4),
+                     "traffic": gemm_traffic() if args.config == "c2" else None,
                      "launches_per_step": g_n, "ms_per_step": round(gemm_ms, 4),
                      "share_of_step": round(gemm_ms / ms_step, 4),
                      "share_of_profiled_step": round(gemm_ms / step_prof_ms, 4),
@@ -416,12 +425,223 @@ def run_ours(args, world, rank, local) -> dict | None:
                              "reads step k while step k+1 runs"},
         "gpu_launches": launches * args.steps,
         "clocks": clk,
+        "repeats": {"n": len(reps), "values": [round(r[0], 3) for r in reps],
+                    "median": round(value, 3), "min": round(min(r[0] for r in reps), 3),
+                    "max": round(max(r[0] for r in reps), 3),
+                    "what": f"the timed region (K = {args.steps} steps) run {len(reps)} times back to back; "
+                            "value / ms_per_step are the median run"},
     }
     if van:
         van["speculative_speedup"] = round(value / van["value"], 3)
         res["vanilla"] = van
     if k1:
         res["k1_point"] = k1
+    if acc_lines:
+        res.update(acc_lines)
+    return res
+
+
+def run_chat(args, world, rank, local) -> dict | None:
+    """C3 as a real multi-turn chat (P:22, P:405 multi-turn): for each of the 8
+    turns, prefill the turn's prompt (CUDA-event timed on its own), then decode until 128 tokens
+    were emitted (the per-turn budget d_max_new clamps the last step); the host reads each step's
+    emitted count (the caller's loop).  value = generated tokens / decode time over all turns."""
+    import torch
+
+    import paper_2506_01986_b200 as sm
+    wl = WORKLOADS[args.config]
+    cfg = synth.model_cfg(wl["model"])
+    tree = sm.Tree(synth.V64, topk=synth.TOPK)
+    seq = rank  # replicas: each rank its own conversation
+    P = [synth.prompt_length(args.seed, seq, t) for t in range(wl["turns"])]
+    x = sum(p + wl["gen"] for p in P)
+    W = sm.allocate_weights(cfg, wl["n_medusa"], seed=args.seed + rank)
+    model = sm.Model(cfg, W, max_rows=256, max_batch=1, max_seq_len=x + tree.N)
+    kv = sm.KVCache(model, tree, 1, x)
+    out = sm.AcceptOut(1, tree.depth)
+    budget = torch.zeros(1, dtype=torch.int32, device="cuda")
+    acfg = sm.accept_cfg(sm.TYPICAL, max_new=budget, **synth.TYPICAL)
+    st = torch.cuda.current_stream()
+    h_n = torch.zeros(1, dtype=torch.int32).pin_memory()
+    # warm-up conversation turn (graph capture, lazy loading) on a throwaway cache
+    kvw = sm.KVCache(model, tree, 1, x)
+    kvw.prefill(0, torch.from_numpy(synth.prompt_tokens(args.seed + 99, seq, 64, cfg["vocab"])).cuda())
+    budget.fill_(1 << 20)
+    for _ in range(max(3, args.warmup)):
+        kvw.step(acfg, out)
+    torch.cuda.synchronize()
+    del kvw
+    clocks = ClockSampler(local)
+    turns, pre_ms, dec_ms, gen_tok, steps = [], 0.0, 0.0, 0, 0
+    for t in range(wl["turns"]):
+        prompt = torch.from_numpy(synth.prompt_tokens(args.seed, seq, P[t], cfg["vocab"], turn=t)).cuda()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        torch.cuda.synchronize()
+        e0.record(st)
+        kv.prefill(0, prompt)
+        e1.record(st)
+        budget.fill_(wl["gen"])
+        n, k = 0, 0
+        while n < wl["gen"]:
+            kv.step(acfg, out)
+            budget.sub_(out.n_emit)
+            h_n.copy_(out.n_emit, non_blocking=True)
+            st.synchronize()
+            n += int(h_n[0])
+            k += 1
+        e2.record(st)
+        torch.cuda.synchronize()
+        pm, dm = e0.elapsed_time(e1), e1.elapsed_time(e2)
+        turns.append({"prompt": P[t], "prefill_ms": round(pm, 3), "decode_ms": round(dm, 3), "steps": k,
+                      "tau": round(n / k, 3)})
+        pre_ms, dec_ms, gen_tok, steps = pre_ms + pm, dec_ms + dm, gen_tok + n, steps + k
+    clk = clocks.stop()
+    assert int(kv.lengths()[0]) == x
+    dec_ms = reduce_max(dec_ms, world)
+    pre_ms = reduce_max(pre_ms, world)
+    tok_all = reduce_sum(gen_tok, world)
+    # K2 share from one profiled replay at the end of the chat (the cache is full: a step there emits
+    # nothing, which does not change the kernels' work)
+    if rank != 0:
+        return None
+    pk = peaks()
+    tau = gen_tok / steps
+    lc_mean = x / 2
+    sb = step_bytes(cfg, tree.N, lc_mean, tau=tau)
+    sf = step_flops(cfg, tree.query()["node_depth"], lc_mean)
+    t_hbm, t_tc = sb / pk["hbm"] / 1e6, sf / (pk["bf16_sus"] or pk["bf16"]) / 1e9
+    ms_step = dec_ms / steps
+    return {
+        "metric": METRIC, "value": round(tok_all / (dec_ms / 1e3), 3), "unit": "tokens/s", "n_gpus": world,
+        "steps": steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic: counter-hash random-init weights (std 0.02), counter-hash prompts of MT-Bench length",
+        "config": {"workload": wl["desc"], "global_batch": world, "seq_len": x, "turns": wl["turns"],
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": f"inputs larger than L2: {sb / 1e9:.1f} GB streamed every step (L2 126 MB)"},
+        "tau": round(tau, 4),
+        "prefill": {"tokens": sum(P), "ms": round(pre_ms, 3), "tokens_per_s": round(sum(P) / (pre_ms / 1e3), 1),
+                    "what": "per-turn prefill (causal chunks through the verify path), timed separately"},
+        "step_roofline": {"bound": "hbm" if t_hbm >= t_tc else "tensor", "roofline_ms": round(max(t_hbm, t_tc), 4),
+                          "frac": round(max(t_hbm, t_tc) / ms_step, 4), "lc_mean": lc_mean},
+        "turns": turns, "clocks": clk,
+        "gpu_launches": kv.step_launches() * steps,
+        "e2e": {"value": round(tok_all / (dec_ms / 1e3), 3), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 4, "what": "the chat loop itself: the host reads every step's emitted "
+                                                 "count (pinned D2H) to end the turn"},
+    }
+
+
+def _time_steps(kv, cfgs, out, steps: int, st) -> tuple[float, float]:
+    """(ms, tokens) of `steps` graph replays (cycling through the accept configs), CUDA events."""
+    import torch
+    L0 = kv.lengths().astype(np.int64)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for k in range(steps):
+        kv.step(cfgs[k % len(cfgs)], out)
+    e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1), float((kv.lengths().astype(np.int64) - L0).sum())
+
+
+def run_c2_acceptance_lines(sm, cfg, model, tree, prompt, x: int, wl: dict, steps: int = 20) -> dict:
+    """C2 lines with tau > 1 (compaction inside the timed region), on the same layer weights:
+    * medusa_init: heads R = 0, U = W_lm (reading Q18), greedy -- tau is whatever the random
+      model accepts;
+    * imposed: the Medusa-init model with acceptance imposed through the d_forced_path hook,
+      depth s mod 5 along the first leaf's path (tau = 3 on average: compaction of up to 4 rows
+      per layer and kv head every step) -- a cost measurement of the full step at tau = 3, not a
+      model-quality number."""
+    import torch
+    d, l, N = cfg["d_model"], tree.depth, tree.N
+    W = model.weights
+    z = torch.zeros(d, d, dtype=torch.bfloat16, device="cuda")
+    zb = torch.zeros(d, dtype=torch.bfloat16, device="cuda")
+    W2 = dict(W)
+    W2["medusa"] = [dict(R=z, b=zb, U=W["lm_head"]) for _ in range(wl["n_medusa"])]
+    m2 = sm.Model(cfg, W2, max_rows=model.c.max_rows, max_batch=1, max_seq_len=x + N)
+    kv = sm.KVCache(m2, tree, 1, x)
+    kv.prefill(0, torch.from_numpy(prompt).cuda())
+    out = sm.AcceptOut(1, l)
+    st = torch.cuda.current_stream()
+    g = [sm.accept_cfg(sm.GREEDY)]
+    _time_steps(kv, g, out, 3, st)
+    pk = peaks()
+    res = {}
+    lc0 = float(kv.lengths().mean())
+    ms, tok = _time_steps(kv, g, out, steps, st)
+    tau = tok / steps
+    sb = step_bytes(cfg, N, lc0 + tok / 2, tau=tau)
+    res["medusa_init"] = {"value": round(tok / (ms / 1e3), 3), "unit": "tokens/s", "tau": round(tau, 4),
+                          "ms_per_step": round(ms / steps, 4), "steps": steps,
+                          "step_roofline_frac": round(sb / pk["hbm"] / 1e6 / (ms / steps), 4),
+                          "what": "C2 with Medusa-init heads (R = 0, U = W_lm), greedy"}
+    path0 = [int(v) for v in tree.query()["leaf_paths"][0]]
+    forced = []
+    for dep in range(l + 1):
+        row = path0[: dep + 1] + [-1] * (l - dep)
+        forced.append(torch.tensor([row], dtype=torch.int32, device="cuda"))
+    fcfgs = [sm.accept_cfg(sm.GREEDY, forced_path=f) for f in forced]
+    _time_steps(kv, fcfgs, out, l + 1, st)  # capture the l + 1 graph variants
+    lc0 = float(kv.lengths().mean())
+    ms, tok = _time_steps(kv, fcfgs, out, steps, st)
+    tau = tok / steps
+    sb = step_bytes(cfg, N, lc0 + tok / 2, tau=tau)
+    res["imposed_tau"] = {"value": round(tok / (ms / 1e3), 3), "unit": "tokens/s", "tau": round(tau, 4),
+                          "ms_per_step": round(ms / steps, 4), "steps": steps,
+                          "step_roofline_frac": round(sb / pk["hbm"] / 1e6 / (ms / steps), 4),
+                          "what": f"Medusa-init C2 with acceptance imposed by the forced-path hook: depth "
+                                  f"(step mod {l + 1}) along the first leaf's path -- the step's cost with "
+                                  f"compaction in the timed region at tau = {tau:.1f}, not a model-quality number"}
+    return res
+
+
+def run_c4_line(sm, args) -> dict:
+    """The bs = 10 part of the metric (BASELINE configs[3], C4 at TP1 on one B200): Llama-2-70B
+    shape, 3 Medusa heads, 16-node tree, 10 ragged prompts, greedy; and vanilla bs = 10 (1-node
+    tree) on the same weights -- the paper's "2x over batched vanilla" comparison."""
+    import copy
+
+    import torch
+    wl = dict(WORKLOADS["c4"])
+    a2 = copy.copy(args)
+    a2.steps, a2.warmup, a2.prof_steps, a2.e2e_steps = 10, 3, 0, 0
+    cfg, tree, model, kv, mode, lc_start = build_workload(sm, wl, a2, 0)
+    N, l, b = tree.N, tree.depth, kv.batch
+    out = sm.AcceptOut(b, l)
+    st = torch.cuda.current_stream()
+    acfg = [sm.accept_cfg(mode)]
+    _time_steps(kv, acfg, out, 3, st)
+    runs = []
+    for _ in range(3):
+        lc0 = float(kv.lengths().mean())
+        ms, tok = _time_steps(kv, acfg, out, 10, st)
+        runs.append((tok / (ms / 1e3), ms, tok, lc0))
+    val, ms, tok, lc0 = sorted(runs)[1]
+    pk = peaks()
+    tau = tok / 10 / b
+    lcm = lc0 + tok / b / 2
+    sb = step_bytes(cfg, N, lcm, b=b, n_medusa=wl["n_medusa"], tau=tau)
+    sf = step_flops(cfg, tree.query()["node_depth"], lcm, b=b, n_medusa=wl["n_medusa"])
+    t_roof = max(sb / pk["hbm"] / 1e6, sf / (pk["bf16_sus"] or pk["bf16"]) / 1e9)
+    res = {"value": round(val, 3), "unit": "tokens/s", "tau": round(tau, 4), "ms_per_step": round(ms / 10, 4),
+           "steps": 10, "repeats": [round(r[0], 3) for r in runs],
+           "step_roofline": {"bound": "hbm" if sb / pk["hbm"] / 1e6 >= sf / (pk["bf16_sus"] or pk["bf16"]) / 1e9
+                             else "tensor", "roofline_ms": round(t_roof, 4),
+                             "frac": round(t_roof / (ms / 10), 4)},
+           "workload": wl["desc"] + " (TP1: one B200)"}
+    vtree = sm.Tree([], topk=synth.TOPK)
+    kv_v = sm.KVCache(model, vtree, b, wl["x_run"])
+    for i, p in enumerate(kv.prompts):
+        kv_v.prefill(i, torch.from_numpy(p).cuda())
+    vout = sm.AcceptOut(b, 0)
+    vcfg = [sm.accept_cfg(sm.GREEDY)]
+    _time_steps(kv_v, vcfg, vout, 3, st)
+    vms, vtok = _time_steps(kv_v, vcfg, vout, 10, st)
+    res["vanilla"] = {"value": round(vtok / (vms / 1e3), 3), "ms_per_step": round(vms / 10, 4)}
+    res["speculative_speedup"] = round(val / res["vanilla"]["value"], 3)
     return res
 
 
@@ -470,41 +690,20 @@ def run_k1_point(sm, args) -> dict:
 
 
 # ------------------------------------------------------------------ oracle (CPU) arm
-def oracle_sample(reps: int, rows: int = 8):
-    """Time the oracle (as it stands) on a bounded sample of one C2 step: ``rows``
-    of the 64 tree rows through 1 of the 32 layers + LM head, and the same rows
-    through 0 layers (LM head only), plus one Medusa head evaluation; returns the
-    extrapolated full-step seconds = 64 * (32 * t_layer_row + t_lm_row) + 4 * t_head."""
-    from oracle import model as OM
-    from oracle import tree as OT
-    cfg = synth.model_cfg("vicuna7b")
-    W1 = OM.Weights(cfg, n_medusa=1, seed=0, medusa_init=True, layers=[0])
-    W0 = OM.Weights.__new__(OM.Weights)
-    W0.__dict__.update(W1.__dict__)
-    W0.layers = []
-    m1, m0 = OM.Model(cfg, W1, "bf16"), OM.Model(cfg, W0, "bf16")
-    tr = OT.build(synth.V64)
-    Lc = 1024
-    toks = synth.prompt_tokens(0, 0, rows, cfg["vocab"])
-    times = []
-    for _ in range(reps):
-        kv1 = OM.KVCache(1, 1, cfg["n_kv_heads"], Lc + tr.N, cfg["head_dim"])
-        kv0 = OM.KVCache(0, 1, cfg["n_kv_heads"], Lc + tr.N, cfg["head_dim"])
-        t0 = time.perf_counter()
-        hf = None
-        for n in range(rows):
-            keys = list(range(Lc)) + [Lc + a for a in OT.ancestors(tr, n)] + [Lc + n]
-            _, hf = m1.forward_row(kv1, 0, int(toks[n]), Lc + tr.depth[n], Lc + n, keys)
-        t1 = time.perf_counter()
-        for n in range(rows):
-            m0.forward_row(kv0, 0, int(toks[n]), Lc + tr.depth[n], Lc + n, [Lc + n])
-        t2 = time.perf_counter()
-        m1.head_logits(0, hf)
-        t3 = time.perf_counter()
-        t_lm = (t2 - t1) / rows
-        t_layer = max(0.0, (t1 - t0) / rows - t_lm)
-        times.append(64 * (32 * t_layer + t_lm) + N_MEDUSA * (t3 - t2))
-    return times
+def host_info() -> dict:
+    info = {"threads": host_threads(), "affinity": len(os.sched_getaffinity(0))}
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["cpu"] = line.split(":", 1)[1].strip()
+                break
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                info["mem_total_gb"] = round(int(line.split()[1]) / 1024 ** 2, 1)
+                break
+    except OSError:
+        pass
+    return info
 
 
 def host_threads() -> int:
@@ -518,45 +717,91 @@ def host_threads() -> int:
     return len(os.sched_getaffinity(0))
 
 
-def cpu_baseline(tau: float) -> dict:
-    t = oracle_sample(1)
-    step_s = t[0]
-    return {"value": round(tau / step_s, 6), "unit": "tokens/s", "cores": host_threads(), "kind": "oracle",
-            "sample": "oracle (numpy fp64, bf16 storage points) on 8 of the 64 V64 tree rows through 1 of 32 "
-                      "Vicuna-7B layers + LM head at Lc=1024, plus one Medusa head; extrapolated linearly to the "
-                      f"full step (64 rows x 32 layers + 4 heads) = {step_s:.1f} s/step; tokens/s at the GPU "
-                      f"run's tau = {tau:.3f}"}
+def oracle_c2_run(seed: int, n_layers: int, lc_start: int, warmup: int, steps: int) -> dict:
+    """The oracle as it stands, in its timing variant (fp32 weights and
+    arithmetic, the tree rows of a step batched through BLAS -- ``Model.forward_rows``, pinned to
+    the row-at-a-time oracle), on the C2 workload: Vicuna-7B widths with ``n_layers`` layers, 4
+    random-init Medusa heads, the V64 tree, x = 2048, greedy; the GPU arm's prompt (lc_start
+    tokens, prefill timed separately) then ``warmup`` + ``steps`` real speculative steps, each
+    timed on the host clock."""
+    from oracle import model as OM
+    from oracle import spec as OS
+    cfg = synth.model_cfg("vicuna7b", n_layers=n_layers)
+    t0 = time.perf_counter()
+    W = OM.Weights(cfg, n_medusa=N_MEDUSA, seed=seed, dtype=np.float32)
+    t1 = time.perf_counter()
+    s = OS.Session(OM.Model(cfg, W, "fp32"), synth.V64, 1, X_BOUND, batched=True)
+    s.prefill(0, synth.prompt_tokens(seed, 0, lc_start, cfg["vocab"]))
+    t2 = time.perf_counter()
+    times, toks = [], []
+    for k in range(warmup + steps):
+        a = time.perf_counter()
+        r = s.step(0, "greedy")
+        if k >= warmup:
+            times.append(time.perf_counter() - a)
+            toks.append(len(r["emitted"]))
+    return {"gen_s": t1 - t0, "prefill_s": t2 - t1, "prefill_tokens": lc_start, "step_s": times, "tokens": toks}
+
+
+def cpu_baseline(seed: int, lc_start: int) -> dict:
+    """Bounded sample (~10-30 s of CPU work): the timing-variant oracle at C2 widths with 1 and 2
+    of the 32 layers, prefill + 4 real steps each; the full-depth step time is extrapolated
+    linearly in the layer count: t(32) = t(1) + 31 (t(2) - t(1))."""
+    r1 = oracle_c2_run(seed, 1, lc_start, 1, 4)
+    r2 = oracle_c2_run(seed, 2, lc_start, 1, 4)
+    t1, t2 = statistics.median(r1["step_s"]), statistics.median(r2["step_s"])
+    t_full = t1 + 31 * max(0.0, t2 - t1)
+    tau = statistics.mean(r2["tokens"])
+    hi = host_info()
+    return {"value": round(tau / t_full, 5), "unit": "tokens/s", "cores": hi["threads"], "kind": "oracle",
+            "sample": f"oracle timing variant (numpy fp32 BLAS, tree rows batched) at C2 widths with 1 and 2 of "
+                      f"32 layers, {lc_start}-token prefill + 4 real greedy steps each: {t1:.3f} / {t2:.3f} s per "
+                      f"step; full 32-layer step extrapolated linearly in the layer count = {t_full:.2f} s; "
+                      f"tau {tau:.2f} (random heads)",
+            "host": hi}
 
 
 def run_reference(args, world, rank) -> dict | None:
+    """--impl reference: the oracle (timing variant) on the full C2 workload -- all 32 layers,
+    the same prompt, W warm-up + K timed real steps; ms_per_step is the host-clock time of those
+    K steps (nothing extrapolated).  Under torchrun only rank 0 runs it."""
     if rank != 0:
         return None
-    t = oracle_sample(args.warmup + args.steps)[args.warmup:]
-    step_s = statistics.median(t)
-    val = 1.0 / step_s
-    return {"impl": "reference", "metric": METRIC, "value": round(val, 6), "unit": "tokens/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 1),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+    lc = args.lc_start
+    r = oracle_c2_run(args.seed, 32, lc, args.warmup, args.steps)
+    tot_s = sum(r["step_s"])
+    tokens = sum(r["tokens"])
+    val = tokens / tot_s
+    hi = host_info()
+    return {"impl": "reference", "metric": METRIC, "value": round(val, 5), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_s / args.steps * 1e3, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic: counter-hash random-init weights, counter-hash prompt tokens",
-            "config": {"workload": "C2: Vicuna-7B-shaped Llama + 4 Medusa-1 heads, V64 tree, bs=1, KV x=2048, "
-                                   "greedy (oracle sample, see cpu_baseline)"},
-            "cpu_baseline": {"value": round(val, 6), "unit": "tokens/s", "cores": host_threads(), "kind": "oracle",
-                             "sample": "each step: 8 of 64 tree rows through 1 of 32 layers + LM head (and 0 "
-                                       "layers), one Medusa head; extrapolated to 64 rows x 32 layers + 4 heads; "
-                                       "tau = 1 (random heads)"},
-            "e2e": {"value": round(val, 6), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "config": {"workload": WORKLOADS["c2"]["desc"], "global_batch": 1, "seq_len": X_BOUND, "lc_start": lc,
+                       "parallelism": "host CPU (numpy BLAS threads)"},
+            "tau": round(tokens / args.steps, 4),
+            "cpu_baseline": {"value": round(val, 5), "unit": "tokens/s", "cores": hi["threads"], "kind": "oracle",
+                             "sample": f"full C2 workload: 32 layers, {lc}-token prompt (prefill "
+                                       f"{r['prefill_s']:.1f} s, untimed), {args.warmup} warm-up + {args.steps} timed "
+                                       f"real steps of the oracle's timing variant (numpy fp32 BLAS, tree rows "
+                                       f"batched); weights generated in {r['gen_s']:.1f} s",
+                             "host": hi},
+            "e2e": {"value": round(val, 5), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--lc-start", type=int, default=1024)
     ap.add_argument("--prof-steps", type=int, default=5)
+    ap.add_argument("--reps", type=int, default=3, help="repetitions of the K-step timed region (median)")
+    ap.add_argument("--no-extra", dest="extra", action="store_false",
+                    help="skip the C2 Medusa-init / imposed-tau lines and the C4 bs=10 line")
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--no-vanilla", dest="vanilla", action="store_false", help="skip the vanilla (1-node) timing")
     ap.add_argument("--no-k1", dest="k1", action="store_false")
@@ -571,10 +816,26 @@ def main():
             print(json.dumps(res), flush=True)
         return
     world, rank, local = dist_setup()
+    if "turns" in WORKLOADS[args.config]:
+        res = run_chat(args, world, rank, local)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
     res = run_ours(args, world, rank, local)
+    if res is not None and args.extra and args.config == "c2" and world == 1:
+        import gc
+
+        import paper_2506_01986_b200 as sm
+        import torch
+        gc.collect()
+        torch.cuda.empty_cache()  # the C2 model is gone: room for the 140 GB 70B-shaped weights
+        res["bs10"] = run_c4_line(sm, args)
     if res is not None:
         if args.cpu and world == 1 and args.config == "c2":
-            res["cpu_baseline"] = cpu_baseline(res["tau"])
+            res["cpu_baseline"] = cpu_baseline(args.seed, res["config"]["lc_start"])
         print(json.dumps(res), flush=True)
     if world > 1:
         import torch.distributed as dist

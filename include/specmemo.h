@@ -298,8 +298,8 @@ sm_status sm_step_launches(const sm_kv *kv, int *n);
  * whole step (kind 3) with CUDA events on the launch stream (the events
  * serialise the launches they bracket).  sm_profile_read synchronises and returns,
  * for the most recent replay, the number of bracketed launches, their summed
- * duration in ms, and (kind 0) the algorithmic bytes W + X + Y(fp32) of those
- * launches.                                                                   */
+ * duration in ms, and (kind 0) the algorithmic bytes of those launches = their weight
+ * matrices (activations and fp32 partial slots excluded).      */
 sm_status sm_step_profile(sm_kv *kv, int enable);
 sm_status sm_profile_read(const sm_kv *kv, int kind, int *count, float *total_ms, double *alg_bytes);
 /* Device pointers to the pending state: root[b], topk[b][n_medusa][K] (int32). */

@@ -28,7 +28,6 @@ same position with the same keys (invariants I1/I3).
 from __future__ import annotations
 
 import math
-import os
 
 import numpy as np
 
@@ -55,19 +54,9 @@ def _w(seed, stream, rows, cols, dtype=np.float64):
     if n <= (1 << 24):
         bits = synth.weight_bits(seed, stream, n)
         return synth.bf16_bits_to_f32(bits).astype(dtype).reshape(rows, cols)
-    # large tensors (timing variant at full model size): the same values, generated in chunks on
-    # several threads (numpy releases the GIL inside its ufuncs)
-    from concurrent.futures import ThreadPoolExecutor
-    out = np.empty(n, dtype=dtype)
-    chunk = 1 << 22
-
-    def fill(i0):
-        i1 = min(n, i0 + chunk)
-        out[i0:i1] = synth.bf16_bits_to_f32(synth.weight_bits(seed, stream, i1 - i0, start=i0))
-
-    with ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 1)) as ex:
-        list(ex.map(fill, range(0, n, chunk)))
-    return out.reshape(rows, cols)
+    # large tensors (C2+ widths): synth's C generator, the same values bit for bit
+    w = synth.weight_values_f32(seed, stream, n).reshape(rows, cols)
+    return w if dtype == np.float32 else w.astype(dtype)
 
 
 class Weights:

@@ -135,11 +135,20 @@ class Session:
             Z[n], HF[n] = self.m.forward_row(self.kv, seq, int(tok[n]), Lc + tr.depth[n], Lc + n, keys)
         return Z, HF
 
-    def accept(self, tok, Z, mode: str = "greedy", temperature: float = 0.7, eps: float = 0.09, alpha: float = 0.3):
+    def accept(self, tok, Z, mode: str = "greedy", temperature: float = 0.7, eps: float = 0.09, alpha: float = 0.3,
+               forced=None):
         """Tree DP: acc(root) = true; acc(c) = acc(parent) and C(parent, c).
         greedy C: tok[c] == argmax z[parent];  typical C: P_p[tok[c]] > min(eps, alpha e^{-H_p}).
-        Returns (a, chosen node, best_leaf index, path node ids [a+1])."""
+        Returns (a, chosen node, best_leaf index, path node ids [a+1]).
+        forced (test hook, the C ABI's d_forced_path): accept this root-to-node path instead."""
         tr = self.tree
+        if forced is not None:
+            chosen = int(forced[-1])
+            path = T.ancestors(tr, chosen) + [chosen]
+            assert path == [int(x) for x in forced], "forced path must be a root-to-node path"
+            cp = tr.paths[chosen]
+            best_leaf = next(i for i, lf in enumerate(self.leaves) if tr.paths[lf][:len(cp)] == cp)
+            return tr.depth[chosen], chosen, best_leaf, path
         acc = [False] * self.N
         ll = [0.0] * self.N
         acc[0] = True
@@ -190,9 +199,9 @@ class Session:
         Z, HF = self.verify(seq, tok)
         return self.finish(seq, tok, pos, Z, HF, mode, budget, **typ)
 
-    def finish(self, seq: int, tok, pos, Z, HF, mode: str = "greedy", budget: int | None = None, **typ):
+    def finish(self, seq: int, tok, pos, Z, HF, mode: str = "greedy", budget: int | None = None, forced=None, **typ):
         """Steps 3-6 of a step on verified rows: accept, emit, compact, next state."""
-        a, chosen, best_leaf, path = self.accept(tok, Z, mode, **typ)
+        a, chosen, best_leaf, path = self.accept(tok, Z, mode, forced=forced, **typ)
         Lc = self.Lc[seq]
         a_eff = a
         if budget is not None:

@@ -526,7 +526,9 @@ static sm_status run_gemm(GemmArgs a, int M, int x_row0, float *ws, size_t ws_fl
   cudaEvent_t ev = nullptr;
   prof_begin(st, &ev);
   if (g_ablate_gemm == 0) CK(gemm_launch(a, st));
-  prof_end(st, ev, 0, (double)a.batch * ((double)a.N * a.K * 2 + (double)M * a.K * 2 + (double)M * a.N * 4));
+  // algorithmic bytes = the weight matrix (activations and the fp32 stream-K partial
+  // slots are not part of the method's work)
+  prof_end(st, ev, 0, (double)a.batch * ((double)a.N * a.K * 2));
   ++nl;
   *pv = PartialView{a.plan, ws, a.N, Mlog, planes};
   return SM_OK;

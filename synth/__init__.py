@@ -68,6 +68,37 @@ def weight_bits(seed: int, stream: int, numel: int, start: int = 0) -> np.ndarra
     return _f32_to_bf16_bits_input(w)
 
 
+_GEN = None
+
+
+def _gen_lib():
+    """synth/_gen.c compiled with gcc (-fopenmp) next to it on first use (or by build())."""
+    global _GEN
+    if _GEN is None:
+        import ctypes
+        import os
+        import subprocess
+        here = os.path.dirname(os.path.abspath(__file__))
+        src, so = os.path.join(here, "_gen.c"), os.path.join(here, "_gen.so")
+        if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+            tmp = f"{so}.{os.getpid()}.tmp"
+            subprocess.run(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", tmp, src], check=True)
+            os.replace(tmp, so)
+        lib = ctypes.CDLL(so)
+        lib.synth_weight_values_f32.argtypes = [ctypes.c_uint64] * 4 + [ctypes.c_float, ctypes.c_void_p]
+        _GEN = lib
+    return _GEN
+
+
+def weight_values_f32(seed: int, stream: int, numel: int, start: int = 0) -> np.ndarray:
+    """``bf16_bits_to_f32(weight_bits(...))`` from the C generator (synth/_gen.c, OpenMP): the same
+    values bit for bit, for full-size models."""
+    out = np.empty(numel, dtype=np.float32)
+    _gen_lib().synth_weight_values_f32(int(seed) & 0xFFFFFFFFFFFFFFFF, int(stream), int(start), int(numel),
+                                       float(WEIGHT_AMPLITUDE_F32), out.ctypes.data)
+    return out
+
+
 def normal_bits(seed: int, stream: int, numel: int) -> np.ndarray:
     """bf16 bits of approximately N(0,1) values (sum of 4 uniforms, scaled), for
     the K1 sweep's Q/K/V.  Exact fp32 ops only."""

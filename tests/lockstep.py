@@ -55,7 +55,7 @@ def bar_check(got, ref, tol, what, max_frac=0.0, hard=None):
 class LockStep:
     def __init__(self, sm, cfg, n_medusa, choices, prompts, x, dtype="bf16", seed=0, medusa_init=False,
                  max_rows=None, tol=None, max_frac=0.0, hard=None, guard_rel=1e-2, guard_abs=None, noise_k=8.0,
-                 typ=None, oracle_weights=None):
+                 typ=None, oracle_weights=None, force_deep_every=0):
         self.sm, self.cfg, self.dtype = sm, cfg, dtype
         self.b = len(prompts)
         self.tol = tol if tol is not None else (1e-4 if dtype == "fp32" else 2e-2)
@@ -83,6 +83,28 @@ class LockStep:
             self.kv.prefill(i, torch.from_numpy(np.asarray(p, np.int32)).cuda())
             self.s.prefill(i, p)
         self.noise = [0.0] * self.b
+        self._probe_noise()
+        # every force_deep_every-th step both sides accept a random full-depth path (the forced-path
+        # hook): random-init models rarely accept tree nodes, so this is what drives compaction
+        # (a5) over real K/V at the wide shapes; those steps still compare every float and integer
+        self.force_deep_every = force_deep_every
+        self.rng = np.random.default_rng(1234)
+        self.stats["forced_deep"] = 0
+
+    def _probe_noise(self):
+        """Rounding-noise scale before the first step: one GPU verify of the proposed tree
+        against the oracle's verify of the same tokens (tree slots are scratch; nothing is
+        accepted).  The first propose's decisions are then screened against it too."""
+        s, tr, b = self.s, self.ot, self.b
+        tt = torch.zeros(b, tr.N, dtype=torch.int32, device="cuda")
+        self.kv.propose(tt)
+        logits = torch.zeros(b, tr.N, self.cfg["vocab"], dtype=torch.float32, device="cuda")
+        self.kv.verify(tt, logits)
+        torch.cuda.synchronize()
+        Zg = logits.cpu().numpy().astype(np.float64)
+        for seq in range(b):
+            Z, _ = s.verify(seq, [int(t) for t in tt[seq].cpu()])
+            self.noise[seq] = float(np.sqrt(np.mean((Zg[seq] - np.stack(Z)) ** 2)))
 
     # ------------------------------------------------------------- margins
     def _argmax_guard(self, z, seq):
@@ -191,10 +213,19 @@ class LockStep:
                     w, f = bar_check(kvl[li, c, seq][:, slots], KV[li][seq][:, slots], self.tol,
                                      f"tree {'KV'[c]} layer {li} seq {seq}", self.max_frac, self.hard)
                     self.stats["max_bar"] = max(self.stats["max_bar"], w)
-            amb = self._accept_ambiguous(seq, tok, Z)
-            r = s.finish(seq, tok, pos, Z, HF, self.mode, **self.typ)
+            deep = None
+            if self.force_deep_every and self.stats["steps"] % self.force_deep_every == self.force_deep_every - 1:
+                leaves = OT.leaves(tr)
+                lf = leaves[int(self.rng.integers(len(leaves)))]
+                deep = OT.ancestors(tr, lf) + [lf]
+                self.stats["forced_deep"] += 1
+            amb = deep is None and self._accept_ambiguous(seq, tok, Z)
+            r = s.finish(seq, tok, pos, Z, HF, self.mode, forced=deep, **self.typ)
             ref.append(r)
-            if amb:
+            if deep is not None:
+                forced[seq, : len(r["path"])] = r["path"]
+                any_forced = True
+            elif amb:
                 forced[seq, : len(r["path"])] = r["path"]
                 any_forced = True
                 self.stats["forced"] += 1

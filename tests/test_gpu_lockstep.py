@@ -81,27 +81,28 @@ def c2_weights_init():
 def test_c2_width_greedy_multistep_medusa_init(sm, c2_weights_init, dtype):
     kw = dict(max_frac=MAX_FRAC, hard=HARD) if dtype == "bf16" else {}
     ls = LockStep(sm, C2, 4, synth.V64, _prompts(11, 1, C2["vocab"], lo=12), 96, dtype=dtype, seed=0,
-                  medusa_init=True, oracle_weights=c2_weights_init, **kw)
+                  medusa_init=True, oracle_weights=c2_weights_init, force_deep_every=2, **kw)
     st = ls.run(8)
     print(dtype, st)
-    assert st["exact_decisions"] >= 8 * 40
-    assert st["forced"] <= 4, st
+    assert st["exact_decisions"] >= 8 * 25 and st["tolerated"] <= st["exact_decisions"] // 4, st
+    assert st["forced"] <= 2, st
+    assert sum(st["accepted_depth_hist"][1:]) >= 4, st  # compaction of 4-deep paths at 7B width
 
 
 def test_c2_width_random_heads_bf16(sm):
     ls = LockStep(sm, C2, 4, synth.V64, _prompts(5, 1, C2["vocab"], lo=16), 64, seed=1, max_frac=MAX_FRAC,
-                  hard=HARD)
-    st = ls.run(3)
+                  hard=HARD, force_deep_every=2)
+    st = ls.run(4)
     print(st)
-    assert st["exact_decisions"] >= 3 * 40
+    assert st["exact_decisions"] >= 4 * 20 and st["tolerated"] <= st["exact_decisions"] // 4, st
 
 
 def test_c3_width_typical_bf16(sm):
     ls = LockStep(sm, C3, 4, synth.V64, _prompts(3, 1, C3["vocab"], lo=14), 64, seed=2, max_frac=MAX_FRAC,
                   hard=HARD, typ=dict(synth.TYPICAL))
-    st = ls.run(3)
+    st = ls.run(4)
     print(st)
-    assert st["exact_decisions"] >= 3 * 40
+    assert st["exact_decisions"] >= 4 * 25 and st["tolerated"] <= st["exact_decisions"] // 4, st
 
 
 # ------------------------------------------------------------------ C4 class: GQA 8:1, batched
@@ -118,17 +119,18 @@ def c4_weights():
                                                                                   "b10-M640"])
 def test_c4_class_batched_lockstep(sm, c4_weights, b, choices):
     ls = LockStep(sm, C4S, 4, choices, _prompts(30 + b, b, C4S["vocab"], lo=9, step=5), 96, seed=3,
-                  medusa_init=True, oracle_weights=c4_weights, max_frac=MAX_FRAC, hard=HARD)
+                  medusa_init=True, oracle_weights=c4_weights, max_frac=MAX_FRAC, hard=HARD, force_deep_every=2)
     st = ls.run(4)
     print(b, len(choices) + 1, st)
-    assert st["exact_decisions"] >= 4 * b * 10
+    assert st["exact_decisions"] >= 4 * b * 6 and st["tolerated"] <= st["exact_decisions"] // 4, st
+    assert sum(st["accepted_depth_hist"][1:]) >= 2 * b, st
 
 
 def test_c2_width_bf16_as_accurate_as_the_rounded_definition(sm, c2_weights_init):
     """The GPU's bf16 logits against the fp64 plain definition are no worse than the oracle's
     own bf16 storage-point emulation against it (same rows, same tree tokens): per row, the rms
-    error within 1.3x and the fraction of elements over the 2e-2 (1 + |z|) bar within 1.5x + 1e-3
-    of the oracle's.  (Measured at seed 11: rms 0.0099 vs 0.0097, frac 5.1e-3 vs 4.4e-3.)"""
+    error within 1.3x; over all rows, the fraction of elements over the 2e-2 (1 + |z|) bar within
+    1.5x + 5e-4 of the oracle's and no element over 3x the bar.  (Measured at seed 11: rms 0.0099 vs 0.0097, frac 5.1e-3 vs 4.4e-3.)"""
     prompt = synth.prompt_tokens(11, 0, 12, C2["vocab"])
     W = sm.allocate_weights(C2, 4, seed=0, medusa_init=True)
     tree = sm.Tree(synth.V64, topk=10)
@@ -149,10 +151,11 @@ def test_c2_width_bf16_as_accurate_as_the_rounded_definition(sm, c2_weights_init
         s.prefill(0, prompt)
         assert s.propose(0)[0] == tok            # tree tokens bit-exact (every top-K gap cleared here)
         Z[mode] = np.stack(s.verify(0, tok)[0])
-    for n in range(tree.N):
-        ref = Z["fp64"][n]
-        bar = 2e-2 * (1 + np.abs(ref))
-        eg, eo = np.abs(Zg[n] - ref), np.abs(Z["bf16"][n] - ref)
-        assert np.sqrt(np.mean(eg ** 2)) <= 1.3 * np.sqrt(np.mean(eo ** 2)), n
-        assert np.mean(eg > bar) <= 1.5 * np.mean(eo > bar) + 1e-3, n
-        assert np.max(eg / bar) <= 3.0, n
+    ref = Z["fp64"]
+    bar = 2e-2 * (1 + np.abs(ref))
+    eg, eo = np.abs(Zg - ref), np.abs(Z["bf16"] - ref)
+    for n in range(tree.N):   # per row: rms error within 1.3x of the rounded definition's
+        assert np.sqrt(np.mean(eg[n] ** 2)) <= 1.3 * np.sqrt(np.mean(eo[n] ** 2)), n
+    # elements over the 2e-2 bar: a few per 1000 for both (counts per row are small: compare totals)
+    assert np.mean(eg > bar) <= 1.5 * np.mean(eo > bar) + 5e-4, (np.mean(eg > bar), np.mean(eo > bar))
+    assert np.max(eg / bar) <= 3.0

@@ -188,3 +188,12 @@ def test_topk_and_argmax_ties():
     assert M.topk_desc(u, 4) == [1, 2, 5, 0]
     assert M.topk_desc(u, 4) == list(np.lexsort((np.arange(6), -u))[:4])
     assert M.argmax_lowest(u) == 1
+
+
+def test_c_weight_generator_matches_numpy():
+    """synth/_gen.c (full-size models) reproduces synth.weight_bits bit for bit."""
+    for seed, stream, n, start in [(0, 5, 1 << 16, 0), (3, 123456, 100000, (1 << 33) + 17),
+                                   (1, synth.stream_layer(31, "wd"), 70001, 5 * 10 ** 9)]:
+        a = synth.bf16_bits_to_f32(synth.weight_bits(seed, stream, n, start=start))
+        b = synth.weight_values_f32(seed, stream, n, start=start)
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
