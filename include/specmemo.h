@@ -76,6 +76,20 @@ sm_status sm_tree_create_full(int k, int l, sm_tree **out);
 sm_status sm_tree_prune(const sm_tree *t, int target_nodes, sm_tree **out);
 sm_status sm_tree_create_pruned_full(int k, int l, float r_min, float r_max, float mid, float steep, sm_tree **out);
 sm_status sm_tree_create_custom(int n_nodes, int n_leaves, int k, int l, sm_tree **out);
+/* Tree-size selection (the paper's choice of heads x mask by measured per-token
+ * latency, fig:maskmodel P:326-401, "Using 3 heads with mask of size 44 gives the best latency",
+ * P:399).  Host only.
+ *   sm_tree_expected_tau  E[tau] of tree t under the independent acceptance model of SPEC's simulator
+ *       (S:336-337): the node at level j with sibling rank r is accepted with probability
+ *       alpha[j-1] * rho^r; the longest all-accepted root path is taken; tau = its depth + 1.
+ *       h_alpha[n_alpha >= depth] in [0, 1]; 0 < rho <= 1.  Errors: SM_ERR_INVALID_ARG.
+ *   sm_select_tree  among n candidate trees with MEASURED step times h_step_ms[n] (the caller
+ *       times sm_step on its model, batch and cache length), the index maximising the expected
+ *       decode throughput batch * E[tau] / step_ms (ties: fewer nodes, then lower index);
+ *       h_tokens_per_s[n] (nullable) receives every candidate's expected tokens/s.           */
+sm_status sm_tree_expected_tau(const sm_tree *t, const float *h_alpha, int n_alpha, float rho, double *tau);
+sm_status sm_select_tree(const sm_tree *const *cands, int n, const double *h_step_ms, const float *h_alpha,
+                         int n_alpha, float rho, int batch, int *best, double *h_tokens_per_s);
 /* Query the canonical tables (host outputs, any pointer may be NULL):
  *   N, S (leaves), depth (max depth l), parent[N], node_depth[N], rank[N],
  *   anc_bits[N][4] (bit j of word j/64 = node j is n or an ancestor of n),

@@ -234,3 +234,49 @@ def build_custom_tree(n_nodes: int, n_leaves: int, k: int, l: int) -> list[list[
     for _ in range(widen):
         widen_one()
     return sorted(paths, key=lambda p: (len(p), p))
+
+
+# ----------------------------------------------------------------- tree-size selection (f1)
+def expected_tau(choices: list[list[int]], alpha, rho: float = 1.0, topk: int = 10) -> float:
+    """Expected acceptance length tau of a tree under the independent acceptance model of
+    SPEC's simulator (AcceptanceModel): the non-root node at level j with sibling
+    rank r is accepted with probability alpha_j * rho^r, independently; the accepted path is the
+    longest root path whose nodes are all accepted ("the longest candidate sequence that
+    verified its tokens is accepted"); tau = its depth + 1 (reading Q12).
+
+    E[tau] = 1 + sum_{D=1}^{l} P(max accepted depth >= D), and P(max >= D) = f_D(root) with
+    f_D(n) = 1 if depth(n) >= D, else 1 - prod_{c child of n} (1 - a(c) f_D(c))
+    (a path reaching depth D exists below n iff some child is accepted and has one below it)."""
+    t = build(choices, topk)
+    a = [0.0] + [float(alpha[t.depth[n] - 1]) * float(rho) ** t.rank[n] for n in range(1, t.N)]
+    kids = [[] for _ in range(t.N)]
+    for n in range(1, t.N):
+        kids[t.parent[n]].append(n)
+    tau = 1.0
+    for D in range(1, t.max_depth + 1):
+        f = [0.0] * t.N
+        for n in reversed(range(t.N)):          # canonical order lists parents before children
+            if t.depth[n] >= D:
+                f[n] = 1.0
+            else:
+                miss = 1.0
+                for c in kids[n]:
+                    miss *= 1.0 - a[c] * f[c]
+                f[n] = 1.0 - miss
+        tau += f[0]
+    return tau
+
+
+def select_tree(candidates: list[list[list[int]]], step_ms, alpha, rho: float = 1.0, batch: int = 1,
+                topk: int = 10) -> tuple[int, list[float]]:
+    """Tree-size selection (the paper's choice of heads x mask by measured
+    per-token latency, fig:maskmodel P:326-401, "3 heads with mask of size 44 gives the best
+    latency" P:399): expected decode throughput of candidate i = batch * E[tau_i] / step_ms[i]
+    (tokens per ms); pick the largest, ties to fewer nodes, then the lower index.
+    Returns (index, per-candidate expected tokens/s)."""
+    tps = [batch * expected_tau(c, alpha, rho, topk) / float(step_ms[i]) * 1e3 for i, c in enumerate(candidates)]
+    best = 0
+    for i in range(1, len(candidates)):
+        if tps[i] > tps[best] or (tps[i] == tps[best] and len(candidates[i]) < len(candidates[best])):
+            best = i
+    return best, tps

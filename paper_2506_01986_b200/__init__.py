@@ -161,6 +161,13 @@ class Tree:
                                            ctypes.c_int(l), ctypes.byref(h)))
         return cls._from_handle(h, k)
 
+    def expected_tau(self, alpha, rho: float = 1.0) -> float:
+        """E[tau] under SPEC's independent acceptance model (include/specmemo.h)."""
+        a = (ctypes.c_float * len(alpha))(*[float(v) for v in alpha])
+        t = ctypes.c_double()
+        _check(lib().sm_tree_expected_tau(self._h, a, len(alpha), ctypes.c_float(rho), ctypes.byref(t)))
+        return t.value
+
     def paths(self) -> list[list[int]]:
         """Rank paths of nodes 1..N-1 in canonical order (root implicit)."""
         q = self.query()
@@ -190,6 +197,19 @@ class Tree:
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:
             _lib.sm_tree_destroy(self._h)
+
+
+def select_tree(cands: list, step_ms, alpha, rho: float = 1.0, batch: int = 1) -> tuple[int, list[float]]:
+    """sm_select_tree: index of the candidate Tree with the largest batch * E[tau] / step_ms, and
+    every candidate's expected tokens/s."""
+    n = len(cands)
+    arr = (ctypes.c_void_p * n)(*[c._h.value for c in cands])
+    ms = (ctypes.c_double * n)(*[float(v) for v in step_ms])
+    a = (ctypes.c_float * len(alpha))(*[float(v) for v in alpha])
+    best = ctypes.c_int()
+    tps = (ctypes.c_double * n)()
+    _check(lib().sm_select_tree(arr, n, ms, a, len(alpha), ctypes.c_float(rho), batch, ctypes.byref(best), tps))
+    return best.value, list(tps)
 
 
 # ------------------------------------------------------------------ tensor-parallel placement (host logic)

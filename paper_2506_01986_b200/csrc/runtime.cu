@@ -368,6 +368,66 @@ extern "C" sm_status sm_tree_create_custom(int n_nodes, int n_leaves, int k, int
   return tree_from_paths(ps, k, out);
 }
 
+// ---------------------------------------------------------------- tree-size selection (f1)
+// E[tau] under SPEC's independent acceptance model: non-root node at level j, sibling
+// rank r accepted with probability alpha_j rho^r; tau = depth of the longest all-accepted root path
+// + 1.  E[tau] = 1 + sum_D f_D(root), f_D(n) = 1 if depth(n) >= D, else
+// 1 - prod_children (1 - a(c) f_D(c)); children are visited in canonical order (same products, same
+// order as oracle/tree.py expected_tau).
+static double tree_expected_tau(const sm_tree *t, const float *alpha, float rho) {
+  std::vector<double> a(t->N, 0.0), f(t->N, 0.0);
+  std::vector<std::vector<int>> kids(t->N);
+  for (int n = 1; n < t->N; ++n) {
+    a[n] = (double)alpha[t->depth[n] - 1] * std::pow((double)rho, (double)t->rank[n]);
+    kids[t->parent[n]].push_back(n);
+  }
+  double tau = 1.0;
+  for (int D = 1; D <= t->l; ++D) {
+    for (int n = t->N - 1; n >= 0; --n) {
+      if (t->depth[n] >= D) {
+        f[n] = 1.0;
+      } else {
+        double miss = 1.0;
+        for (int c : kids[n]) miss *= 1.0 - a[c] * f[c];
+        f[n] = 1.0 - miss;
+      }
+    }
+    tau += f[0];
+  }
+  return tau;
+}
+
+extern "C" sm_status sm_tree_expected_tau(const sm_tree *t, const float *h_alpha, int n_alpha, float rho,
+                                          double *tau) {
+  if (!t || !h_alpha || !tau || n_alpha < t->l || !(rho > 0.f && rho <= 1.f))
+    return fail(SM_ERR_INVALID_ARG, "sm_tree_expected_tau: need alpha[>= depth] in [0,1], 0 < rho <= 1");
+  for (int j = 0; j < t->l; ++j)
+    if (!(h_alpha[j] >= 0.f && h_alpha[j] <= 1.f)) return fail(SM_ERR_INVALID_ARG, "alpha outside [0, 1]");
+  *tau = tree_expected_tau(t, h_alpha, rho);
+  return SM_OK;
+}
+
+extern "C" sm_status sm_select_tree(const sm_tree *const *cands, int n, const double *h_step_ms, const float *h_alpha,
+                                    int n_alpha, float rho, int batch, int *best, double *h_tokens_per_s) {
+  if (!cands || n < 1 || !h_step_ms || !h_alpha || !best || batch < 1)
+    return fail(SM_ERR_INVALID_ARG, "sm_select_tree: bad arguments");
+  int b = -1;
+  double bv = 0.0;
+  for (int i = 0; i < n; ++i) {
+    double tau;
+    CKS(sm_tree_expected_tau(cands[i], h_alpha, n_alpha, rho, &tau));
+    if (!(h_step_ms[i] > 0.0)) return fail(SM_ERR_INVALID_ARG, "sm_select_tree: step_ms must be > 0");
+    const double v = batch * tau / h_step_ms[i] * 1e3;  // expected tokens/s
+    if (h_tokens_per_s) h_tokens_per_s[i] = v;
+    if (b < 0 || v > bv || (v == bv && cands[i]->N < cands[b]->N)) {
+      b = i;
+      bv = v;
+    }
+  }
+  *best = b;
+  return SM_OK;
+}
+
 extern "C" sm_status sm_tree_query(const sm_tree *t, int *N, int *S, int *depth, int32_t *parent, int32_t *node_depth,
                                    int32_t *rank, uint64_t *anc_bits, int32_t *leaf_paths) {
   if (!t) return fail(SM_ERR_INVALID_ARG, "sm_tree_query: null tree");

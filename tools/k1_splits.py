@@ -1,0 +1,63 @@
+"""K1 split-count probe (GPU box): device time per launch for forced key splits 1/2/4/8 and the
+automatic choice, over representative C5 points and the C2 in-step shape.
+
+python tools/k1_splits.py > gpurun_out/k1_splits.txt"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2506_01986_b200 as sm  # noqa: E402
+import synth  # noqa: E402
+
+PEAK = 6543.4
+pts = [("A", 32, 32, b, N, Lc) for (b, N, Lc) in
+       [(1, 64, 1100), (1, 64, 2048), (1, 16, 4096), (1, 64, 8192), (2, 64, 2048), (2, 128, 4096), (4, 64, 1024),
+        (4, 128, 2048), (8, 64, 1024), (8, 64, 4096), (16, 64, 2048), (32, 16, 1024), (1, 256, 8192),
+        (8, 256, 2048)]] + \
+      [("B", 8, 1, b, N, Lc) for (b, N, Lc) in [(1, 64, 4096), (8, 64, 4096), (8, 16, 8192), (32, 64, 4096),
+                                               (16, 16, 32768)]]
+hd = 128
+print(f"{'g':2s} {'b':>3s} {'N':>4s} {'Lc':>6s} {'MB':>7s} " + " ".join(f"{'s' + str(s):>7s}" for s in (0, 1, 2, 4, 8)))
+for g, H, Hkv, b, N, Lc in pts:
+    tree = sm.Tree(synth.SWEEP_TREES[N]) if N != 64 else sm.Tree(synth.V64)
+    cap = Lc + tree.N
+    sets = []
+    for _ in range(2):
+        q = torch.randn(b, tree.N, H, hd, device="cuda").bfloat16()
+        k = torch.randn(b, Hkv, cap, hd, device="cuda").bfloat16()
+        v = torch.randn(b, Hkv, cap, hd, device="cuda").bfloat16()
+        sets.append((q, k, v, torch.empty_like(q)))
+    L = torch.full((b,), Lc, dtype=torch.int32, device="cuda")
+    alg = b * Hkv * cap * hd * 4 + 2 * b * tree.N * H * hd * 2
+    row = []
+    for s in (0, 1, 2, 4, 8):
+        sm.set_option("attn_splits", s)
+        for i in range(2):
+            q, k, v, o = sets[i]
+            sm.tree_attention(tree, q, k, v, L, H, Hkv, o)
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            gr.capture_begin()
+            for i in range(20):
+                q, k, v, o = sets[i % 2]
+                sm.tree_attention(tree, q, k, v, L, H, Hkv, o, stream=st)
+            gr.capture_end()
+        gr.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            gr.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        row.append(e0.elapsed_time(e1) * 1e3 / 60)
+        del gr
+    sm.set_option("attn_splits", 0)
+    print(f"{g:2s} {b:3d} {tree.N:4d} {Lc:6d} {alg / 1e6:7.1f} " + " ".join(f"{u:7.1f}" for u in row) +
+          "   best frac " + f"{alg / min(row) / 1e3 / PEAK:.3f}", flush=True)
+    del sets
+    torch.cuda.empty_cache()
