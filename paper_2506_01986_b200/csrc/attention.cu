@@ -22,6 +22,8 @@
 //  * programmatic dependent launch: the committed prefix [0, Lc) does not change
 //    during the forward, so its first K/V tiles are requested before
 //    griddepcontrol.wait; Q and the tree tiles only after it.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -335,6 +337,12 @@ __global__ void __launch_bounds__(128) tree_attn_kernel(const __grid_constant__ 
 
 static int g_attn_tc = 1;  // head_dim 128 on tcgen05 (sm_set_option "attn_tc")
 static int g_attn_splits = 0;  // experiments: force the key-split count (sm_set_option "attn_splits", 0 = auto)
+// tree mode, head_dim 128: the stream-K ("lean") tcgen05 kernel (1, default) or the cluster-split one (0)
+static int g_attn_lean = 0;
+static int g_lean_div = 16;  // lean K1: minimum tiles per CTA = max(2, live rows per unit / g_lean_div)
+void attention_set_lean(int on) { g_attn_lean = on; }
+void attention_set_lean_div(int d) { g_lean_div = d < 1 ? 1 : d; }
+int attention_lean_min_tiles(int Nq, int G) { return std::max(2, std::min(128, Nq * G) / g_lean_div); }
 void attention_set_tc(int on) { g_attn_tc = on; }
 void attention_set_splits(int n) { g_attn_splits = n; }
 static bool use_tc(int head_dim) { return g_attn_tc && head_dim == 128; }
@@ -386,7 +394,10 @@ cudaError_t attention_launch(const AttnArgs &a, int head_dim, cudaStream_t st) {
     case 16: return launch_hd<16>(a, st);
     case 32: return launch_hd<32>(a, st);
     case 64: return launch_hd<64>(a, st);
-    case 128: return use_tc(128) ? attention_tc_launch(a, st) : launch_hd<128>(a, st);
+    case 128:
+      if (use_tc(128) && g_attn_lean && !a.causal && a.lean_part && a.nseq <= kLeanMaxSeq)
+        return attention_lean_launch(a, st);
+      return use_tc(128) ? attention_tc_launch(a, st) : launch_hd<128>(a, st);
     default: return cudaErrorInvalidValue;
   }
 }

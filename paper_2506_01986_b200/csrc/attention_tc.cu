@@ -34,14 +34,16 @@ constexpr int HD = 128;
 constexpr int ROWS = 128;                     // query rows per CTA (UMMA M)
 constexpr int KEYS = 64;                      // keys per tile
 constexpr int TILE = KEYS * HD * 2;           // 16 KB: one K (or V) tile
-constexpr int STAGES = 4;
+// P never touches shared memory: the softmax writes it (bf16 pairs) over its S buffer in TMEM and
+// the PV MMA reads its A operand from there (tcgen05.mma ... [a_tmem]), so the ring gets the 32 KB
+// the two P buffers took: 6 stages = 192 KB of K/V in flight per SM (4 stages held ~4.6 TB/s)
+constexpr int STAGES = 6;
 constexpr int QB = ROWS * HD * 2;             // 32 KB
-constexpr int PB = ROWS * KEYS * 2;           // 16 KB per P buffer (two)
 constexpr int OFF_Q = 0;
-constexpr int OFF_P = OFF_Q + QB;
-constexpr int OFF_KV = OFF_P + 2 * PB;
+constexpr int OFF_KV = OFF_Q + QB;
 constexpr int OFF_BAR = OFF_KV + STAGES * 2 * TILE;
 constexpr int SMEM = OFF_BAR + 256 + 1024;    // + barriers + alignment slack
+static_assert(SMEM <= 232448, "K1 shared memory");
 constexpr float RESCALE_LOG2 = 8.0f;          // lazy-rescale threshold (log2 units)
 }  // namespace tc
 
@@ -106,6 +108,17 @@ SM_DEV void tmem_st32_f(uint32_t taddr, const float *v) {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+SM_DEV void tmem_st32_u(uint32_t taddr, const uint32_t *v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]));
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
 // sm_set_option("attn_l2pf"): prefetch the o_proj weights into L2 during attention.  Measured:
 // the o_proj GEMM gains ~0.8 us per layer, attention loses ~2.3 us (its K/V reads compete) -> off.
 __device__ int g_attn_l2pf = 0;
@@ -116,13 +129,12 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sQ = smem + OFF_Q;
-  uint8_t *sP = smem + OFF_P;
   uint8_t *sKV = smem + OFF_KV;
   uint64_t *kv_full = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
   uint64_t *kv_empty = kv_full + STAGES;
   uint64_t *s_full = kv_empty + STAGES;  // [2]
-  uint64_t *s_free = s_full + 2;         // [2]
-  uint64_t *p_full = s_free + 2;         // [2] P buffers
+  uint64_t *s_free = s_full + 2;         // [2] (unused: S(i+2) is issued after PV(i), in order)
+  uint64_t *p_full = s_free + 2;         // [2] P(i) written over S buffer i & 1
   uint64_t *o_done = p_full + 2;         // [2] PV(i) commits to o_done[i & 1]
   uint64_t *q_full = o_done + 2;
   uint32_t *tslot = reinterpret_cast<uint32_t *>(q_full + 1);
@@ -223,12 +235,12 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
     if (lane == 0 && ntiles > 0) {
       constexpr uint32_t idesc_s = idesc_bf16_major(ROWS, KEYS, 0, 0);  // Q (K-major) x K^T (K-major)
       constexpr uint32_t idesc_o = idesc_bf16_major(ROWS, HD, 0, 1);    // P (K-major) x V (MN-major)
-      const uint32_t q_u = smem_u32(sQ), p_u = smem_u32(sP), kv_u = smem_u32(sKV);
+      const uint32_t q_u = smem_u32(sQ), kv_u = smem_u32(sKV);
       mbar_wait(q_full, 0);
       SM_STAMP(14);
       auto issue_s = [&](int i) {
         const int sb = i & 1, st = i % STAGES;
-        if (i >= 2) mbar_wait(&s_free[sb], ((i >> 1) - 1) & 1);
+        // S buffer sb last held S(i-2) / P(i-2): its PV was issued before this MMA (tensor pipe order)
         mbar_wait(&kv_full[st], (i / STAGES) & 1);
         tc_fence_after();
         const uint32_t kb = kv_u + st * 2 * TILE;
@@ -247,10 +259,9 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
         tc_fence_after();
         const uint32_t vb = kv_u + (i % STAGES) * 2 * TILE + TILE;
 #pragma unroll
-        for (int k = 0; k < KEYS / 16; ++k) {  // keys in 16-row steps
-          const uint64_t ad = umma_desc_sw128(p_u + (i & 1) * PB + k * 32);
+        for (int k = 0; k < KEYS / 16; ++k) {  // keys in 16-row steps: 8 TMEM columns of bf16 pairs
           const uint64_t bd = umma_desc_mn_sw128(vb + k * 2048, 8192);
-          umma_bf16(tmem + 2 * KEYS, ad, bd, idesc_o, (i > 0 || k > 0) ? 1u : 0u);
+          umma_bf16_ts(tmem + 2 * KEYS, tmem + (i & 1) * KEYS + k * 8, bd, idesc_o, (i > 0 || k > 0) ? 1u : 0u);
         }
         umma_commit(&kv_empty[i % STAGES]);
         umma_commit(&o_done[i & 1]);
@@ -282,7 +293,6 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
     }
     if (threadIdx.x == 0) SM_STAMP(3);
     const int Nq = a.Nq;
-    const uint32_t p_u = smem_u32(sP);
     float m_run = -INFINITY, l = 0.f;  // running max in log2 units (lazy), running sum
     const bool warp_live = rblk * ROWS + warp * 32 < R;  // warps of padding rows only keep the handshakes
     for (int i = 0; i < ntiles; ++i) {
@@ -295,15 +305,12 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
       }
       if (!warp_live) {
         tc_fence_before();
-        mbar_arrive(&s_free[sb]);
         mbar_arrive(&p_full[sb]);
         continue;
       }
       float y[64];
       tmem_ld32_f(lane_base + sb * KEYS, y);
       tmem_ld32_f(lane_base + sb * KEYS + 32, y + 32);
-      tc_fence_before();
-      mbar_arrive(&s_free[sb]);
       const int p0 = key0 + i * KEYS;
       if (a.pad && p0 < Lc) {  // pad batching (f4): masked cache slots of this sequence's prefix
         const uint32_t *pw = a.pad + (size_t)seq * a.pad_words + (p0 >> 5);
@@ -366,8 +373,6 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
       }
       l = l * alpha + ((s0 + s1) + (s2 + s3));
       m_run = m_new;
-      // P buffer (i & 1) is free once PV(i-2) has completed
-      if (i >= 2) mbar_wait(&o_done[sb], ((i >> 1) - 1) & 1);
       if (__any_sync(0xffffffffu, resc) && i > 0) {
         mbar_wait(&o_done[sb ^ 1], ((i - 1) >> 1) & 1);  // PV(i-1) done: O is stable
         tc_fence_after();
@@ -380,10 +385,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
           tmem_st32_f(lane_base + 2 * KEYS + c0, o);
         }
       }
-      const uint32_t prow = p_u + sb * PB;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) st_shared_v4(prow + sw128_off(r, c), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-      fence_proxy_async();
+      tmem_st32_u(lane_base + sb * KEYS, pk);  // P(i) over S(i): columns [sb * 64, sb * 64 + 32)
       tc_fence_before();
       mbar_arrive(&p_full[sb]);
     }
@@ -446,7 +448,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
     if (threadIdx.x == 0) SM_STAMP(8);
     const float *so = reinterpret_cast<const float *>(sKV);
     const float *sml = so + ROWS * HD;
-    float *swt = reinterpret_cast<float *>(sP);  // [rows_per][8] combine weights w_q / L
+    float *swt = reinterpret_cast<float *>(sKV + ROWS * HD * 4 + ROWS * 2 * 4);  // [rows_per][8] weights w_q / L
     const uint32_t so_u = smem_u32(so), sml_u = smem_u32(sml);
     // the block's LIVE rows are dealt evenly to the ranks (N*G = 64 of 128 rows: 16 per rank
     // at 4 splits instead of 32 on two ranks and none on the others)
@@ -523,6 +525,536 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
   if (threadIdx.x == 0) SM_GT_END(5);
 }
 
+// ============================================================================ K1, stream-K ("lean") variant
+// The tree-mode kernel above gives every (row block, sequence, kv head) unit nsplit CTAs of a
+// cluster (nsplit <= 8, combined over DSMEM): with 1 CTA per SM (192 KB of shared memory) the grid
+// is units x nsplit CTAs, so b Hkv = 8 units (C2 b = 8) run 256 CTAs = 1.73 waves on 148 SMs and
+// b Hkv = 32 (C2 in-step) runs 64 CTAs.  Here the key tiles of ALL units are one flat sequence
+// (unit-major, Ttot tiles in total, known only on the device: Lc lives there) and CTA c of
+// Peff <= 148 persistent CTAs takes tiles [c Ttot / Peff, (c+1) Ttot / Peff): every SM streams the
+// same number of tiles.  A CTA's range crosses unit boundaries ("segments"); a unit fully inside
+// one CTA is written directly, otherwise each covering CTA (a "piece") stores its (m, l, O) rows
+// unnormalised to a global slot, and after a grid barrier (all Peff CTAs are co-resident: one per
+// SM) the CTAs combine those units in piece order (deterministic), rows spread over all warps.
+// Per CTA: two Q buffers (the next segment's Q is staged while this one runs), S double-buffered
+// in TMEM, two O accumulators (the next segment's PV starts while this one's O is drained).
+namespace lean {
+// P in TMEM (over its S buffer, as in the cluster kernel): 2 Q buffers + 5 K/V stages
+constexpr int HD = 128, ROWS = 128, KEYS = 64, TILE = KEYS * HD * 2, STAGES = 5;
+constexpr int QB = ROWS * HD * 2;   // 32 KB
+constexpr int OFF_Q = 0;            // 2 Q buffers
+constexpr int OFF_KV = 2 * QB;
+constexpr int OFF_BAR = OFF_KV + STAGES * 2 * TILE;  // 229376
+constexpr int OFF_SPRE = OFF_BAR + 256;
+constexpr int SMEM = OFF_SPRE + (kLeanMaxSeq + 1) * 4 + 16 + 1024;
+static_assert(SMEM <= 232448, "lean K1 shared memory");
+constexpr int WARPS = 6;
+}  // namespace lean
+
+struct LeanSeg {
+  int s, u, h, rb, t0, t1, Ts;  // sequence, unit, kv head, row block, tiles [t0, t1) of Ts
+  long long pre;                // first global tile of the unit
+};
+
+__global__ void __launch_bounds__(192, 1) tree_attn_lean_kernel(const __grid_constant__ AttnArgs a) {
+  using namespace lean;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sQ = smem + OFF_Q;
+  uint8_t *sKV = smem + OFF_KV;
+  uint64_t *kv_full = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
+  uint64_t *kv_empty = kv_full + STAGES;
+  uint64_t *s_full = kv_empty + STAGES;  // [2]
+  uint64_t *s_free = s_full + 2;         // [2]
+  uint64_t *p_full = s_free + 2;         // [2]
+  uint64_t *o_done = p_full + 2;         // [2] PV(i) commits to o_done[i & 1]
+  uint64_t *q_full = o_done + 2;         // [2] Q buffers
+  uint64_t *q_free = q_full + 2;         // [2]
+  uint64_t *o_free = q_free + 2;         // [2] O accumulators
+  int *spre = reinterpret_cast<int *>(smem + OFF_SPRE);  // per-sequence first global tile, [nseq + 1]
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(spre + kLeanMaxSeq + 1);
+
+  pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int R = a.Nq * a.G;
+  const int RB = (R + ROWS - 1) / ROWS;
+  const int UPS = a.Hkv * RB;  // units per sequence
+  // ---- the flat tile sequence (Lc is read before griddepcontrol.wait: only the step's last kernels
+  // change it, see common.cuh)
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int s = 0; s < a.nseq; ++s) {
+      spre[s] = acc;
+      acc += ((a.len[a.seq_base + s] + a.Nq + KEYS - 1) / KEYS) * UPS;
+    }
+    spre[a.nseq] = acc;
+  }
+  __syncthreads();
+  const long long Ttot = spre[a.nseq];
+  const int Peff = (int)min((long long)gridDim.x, max(1LL, Ttot / max(1, a.lean_min_tiles)));
+  const int c = blockIdx.x;
+  if (c >= Peff) return;
+  const long long g_lo = (long long)c * Ttot / Peff, g_hi = (long long)(c + 1) * Ttot / Peff;
+  auto owner = [&](long long g) { return (int)(((g + 1) * Peff - 1) / Ttot); };
+  auto seg_at = [&](long long g, LeanSeg &sg) {
+    int s = 0;
+    while (s + 1 < a.nseq && spre[s + 1] <= g) ++s;
+    sg.s = s;
+    sg.Ts = (spre[s + 1] - spre[s]) / UPS;
+    const long long within = g - spre[s];
+    const int ui = (int)(within / sg.Ts);
+    sg.u = s * UPS + ui;
+    sg.h = ui / RB;
+    sg.rb = ui % RB;
+    sg.t0 = (int)(within % sg.Ts);
+    sg.t1 = (int)min((long long)sg.Ts, sg.t0 + (g_hi - g));
+    sg.pre = spre[s] + (long long)ui * sg.Ts;
+  };
+  const float sl2 = a.scale_log2;
+  auto kv_rows = [&](const LeanSeg &sg, long long &kr, long long &vr) {
+    const int seq = a.seq_base + sg.s;
+    kr = a.k_row0 + (long long)seq * a.seq_rows + (long long)sg.h * a.cap;
+    vr = a.v_row0 + (long long)seq * a.seq_rows + (long long)sg.h * a.cap;
+  };
+  auto issue = [&](int i, long long kr, long long vr, int p) {  // K and V of keys [p, p+64) -> ring stage
+    const int st = i % STAGES;
+    uint8_t *kb = sKV + st * 2 * TILE;
+    uint8_t *vb = kb + TILE;
+    mbar_arrive_expect_tx(&kv_full[st], 2 * TILE);
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      tma_load_2d(kb + hf * 8192, &a.tmK, &kv_full[st], hf * 64, (int)(kr + p));
+      tma_load_2d(vb + hf * 8192, &a.tmV, &kv_full[st], hf * 64, (int)(vr + p));
+    }
+  };
+
+  if (threadIdx.x == 128) {
+    tma_prefetch_desc(&a.tmK);
+    tma_prefetch_desc(&a.tmV);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_free[b], 128);
+      mbar_init(&p_full[b], 128);
+      mbar_init(&o_done[b], 1);
+      mbar_init(&q_full[b], 128);
+      mbar_init(&q_free[b], 1);
+      mbar_init(&o_free[b], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;  // S0 [0,64), S1 [64,128), O0 [128,256), O1 [256,384)
+
+  if (warp == 4) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      bool waited = false;
+      int i = 0;
+      for (long long g = g_lo; g < g_hi;) {
+        LeanSeg sg;
+        seg_at(g, sg);
+        long long kr, vr;
+        kv_rows(sg, kr, vr);
+        const int Lc = a.len[a.seq_base + sg.s];
+        for (int t = sg.t0; t < sg.t1; ++t, ++i) {
+          const int p = t * KEYS;
+          // tiles entirely inside the committed prefix do not depend on this step: the first ring
+          // fill of them is issued before griddepcontrol.wait
+          if (!waited && (i >= STAGES || p + KEYS > Lc)) {
+            pdl_wait();
+            waited = true;
+          }
+          if (i >= STAGES) mbar_wait(&kv_empty[i % STAGES], ((i / STAGES) - 1) & 1);
+          issue(i, kr, vr, p);
+        }
+        g += sg.t1 - sg.t0;
+      }
+      if (!waited) pdl_wait();
+    }
+  } else if (warp == 5) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16_major(ROWS, KEYS, 0, 0);
+      constexpr uint32_t idesc_o = idesc_bf16_major(ROWS, HD, 0, 1);
+      const uint32_t q_u0 = smem_u32(sQ), kv_u = smem_u32(sKV);
+      int i = 0, k = 0;
+      for (long long g = g_lo; g < g_hi; ++k) {
+        LeanSeg sg;
+        seg_at(g, sg);
+        const int nt = sg.t1 - sg.t0;
+        const uint32_t q_u = q_u0 + (k & 1) * QB;
+        const uint32_t o_col = 2 * KEYS + (k & 1) * HD;
+        mbar_wait(&q_full[k & 1], (k >> 1) & 1);
+        auto issue_s = [&](int ii) {
+          const int sb = ii & 1, st = ii % STAGES;  // S buffer: PV(ii - 2) was issued before (pipe order)
+          mbar_wait(&kv_full[st], (ii / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t kb = kv_u + st * 2 * TILE;
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint64_t ad = umma_desc_sw128(q_u + (kk >> 2) * 16384 + (kk & 3) * 32);
+            const uint64_t bd = umma_desc_sw128(kb + (kk >> 2) * 8192 + (kk & 3) * 32);
+            umma_bf16(tmem + sb * KEYS, ad, bd, idesc_s, kk > 0);
+          }
+          umma_commit(&s_full[sb]);
+        };
+        issue_s(i);
+        if (nt == 1) umma_commit(&q_free[k & 1]);
+        if (k >= 2) mbar_wait(&o_free[k & 1], ((k >> 1) - 1) & 1);  // segment k-2 drained this O
+        for (int j = 0; j < nt; ++j, ++i) {
+          if (j + 1 < nt) {
+            issue_s(i + 1);
+            if (j + 2 == nt) umma_commit(&q_free[k & 1]);  // the segment's last S reads Q
+          }
+          mbar_wait(&p_full[i & 1], (i >> 1) & 1);
+          tc_fence_after();
+          const uint32_t vb = kv_u + (i % STAGES) * 2 * TILE + TILE;
+#pragma unroll
+          for (int kk = 0; kk < KEYS / 16; ++kk) {
+            const uint64_t bd = umma_desc_mn_sw128(vb + kk * 2048, 8192);
+            umma_bf16_ts(tmem + o_col, tmem + (i & 1) * KEYS + kk * 8, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&kv_empty[i % STAGES]);
+          umma_commit(&o_done[i & 1]);
+        }
+        g += nt;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax warps 0..3 (row = TMEM lane)
+    const int r = warp * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    pdl_wait();  // q comes from the preceding kernel; partial slots are rewritten below
+    auto load_q = [&](const LeanSeg &sg, int buf) {  // this row of the unit's Q -> K-major SW128 layout
+      const int rr = sg.rb * ROWS + r;
+      const bool live = rr < R;
+      const uint4 *src = nullptr;
+      if (live) {
+        const int n = rr / a.G, gg = rr % a.G;
+        src = reinterpret_cast<const uint4 *>(a.q + (((long long)sg.s * a.Nq + n) * a.H + (long long)sg.h * a.G + gg) *
+                                                        HD);
+      }
+      uint4 v[16];
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) v[cc] = live ? __ldg(src + cc) : make_uint4(0, 0, 0, 0);
+      const uint32_t q_u = smem_u32(sQ) + buf * QB;
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc)
+        st_shared_v4(q_u + (cc >> 3) * 16384 + sw128_off(r, cc), v[cc].x, v[cc].y, v[cc].z, v[cc].w);
+      fence_proxy_async();
+      mbar_arrive(&q_full[buf]);
+    };
+    const int Nq = a.Nq;
+    int i = 0, k = 0;
+    LeanSeg sg;
+    if (g_lo < g_hi) {
+      seg_at(g_lo, sg);
+      load_q(sg, 0);
+    }
+    for (long long g = g_lo; g < g_hi; ++k) {
+      const int nt = sg.t1 - sg.t0;
+      const long long gn = g + nt;
+      LeanSeg nx;
+      if (gn < g_hi) {  // stage the next segment's Q now (its buffer's last S MMAs are done: k - 1)
+        seg_at(gn, nx);
+        if (k + 1 >= 2) mbar_wait(&q_free[(k + 1) & 1], (((k + 1) >> 1) - 1) & 1);
+        load_q(nx, (k + 1) & 1);
+      }
+      const int ob = k & 1;
+      const uint32_t o_col = 2 * KEYS + ob * HD;
+      const int rr = sg.rb * ROWS + r;
+      const bool live = rr < R;
+      const bool warp_live = sg.rb * ROWS + warp * 32 < R;
+      const int seq = a.seq_base + sg.s;
+      const int Lc = a.len[seq];
+      uint64_t anc0 = 0, anc1 = 0, anc2 = 0, anc3 = 0;
+      if (live) {
+        const uint64_t *w = a.anc + (rr / a.G) * kAncWords;
+        anc0 = w[0];
+        anc1 = w[1];
+        anc2 = w[2];
+        anc3 = w[3];
+      }
+      float m_run = -INFINITY, l = 0.f;
+      for (int j = 0; j < nt; ++j, ++i) {
+        const int sb = i & 1;
+        mbar_wait(&s_full[sb], (i >> 1) & 1);
+        tc_fence_after();
+        if (!warp_live) {
+          tc_fence_before();
+          mbar_arrive(&p_full[sb]);
+          continue;
+        }
+        float y[64];
+        tmem_ld32_f(lane_base + sb * KEYS, y);
+        tmem_ld32_f(lane_base + sb * KEYS + 32, y + 32);
+        const int p0 = (sg.t0 + j) * KEYS;
+        if (a.pad && p0 < Lc) {  // pad batching (f4): masked cache slots of this sequence's prefix
+          const uint32_t *pw = a.pad + (size_t)seq * a.pad_words + (p0 >> 5);
+          const uint64_t pm = (uint64_t)pw[0] | ((uint64_t)pw[1] << 32);
+          if (pm) {
+#pragma unroll
+            for (int jj = 0; jj < 64; ++jj) y[jj] = ((pm >> jj) & 1ull) ? -INFINITY : y[jj];
+          }
+        }
+        if (p0 + KEYS > Lc) {  // tile reaches past the prefix: visibility of its 64 keys (Eq. 2)
+          const int off = p0 - Lc;
+          auto word = [&](int q) { return q == 0 ? anc0 : q == 1 ? anc1 : q == 2 ? anc2 : q == 3 ? anc3 : 0ull; };
+          uint64_t vis;
+          if (off < 0) {
+            vis = (~0ull >> (64 + off)) | (anc0 << (-off));
+          } else {
+            const int q = off >> 6, sh = off & 63;
+            const uint64_t lo = word(q), hi = word(q + 1);
+            vis = sh ? ((lo >> sh) | (hi << (64 - sh))) : lo;
+          }
+          if (Nq - off < 64) vis &= (Nq - off <= 0) ? 0ull : (~0ull >> (64 - (Nq - off)));
+#pragma unroll
+          for (int jj = 0; jj < 64; ++jj) y[jj] = ((vis >> jj) & 1ull) ? y[jj] : -INFINITY;
+        }
+        float mx0 = y[0], mx1 = y[1];
+#pragma unroll
+        for (int jj = 2; jj < 64; jj += 2) {
+          mx0 = fmaxf(mx0, y[jj]);
+          mx1 = fmaxf(mx1, y[jj + 1]);
+        }
+        const float mx = fmaxf(mx0, mx1) * sl2;
+        float m_new = m_run, alpha = 1.f;
+        bool resc = false;
+        if (m_run == -INFINITY) {
+          m_new = mx;
+        } else if (mx > m_run + tc::RESCALE_LOG2) {
+          m_new = mx;
+          alpha = exp2f(m_run - m_new);
+          resc = true;
+        }
+        const float nb = (m_new == -INFINITY) ? 0.f : -m_new;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        uint32_t pk[32];
+#pragma unroll
+        for (int jj = 0; jj < 32; jj += 2) {
+          const float e0 = ex2(fmaf(y[2 * jj], sl2, nb)), e1 = ex2(fmaf(y[2 * jj + 1], sl2, nb));
+          const float e2 = ex2(fmaf(y[2 * jj + 2], sl2, nb)), e3 = ex2(fmaf(y[2 * jj + 3], sl2, nb));
+          s0 += e0;
+          s1 += e1;
+          s2 += e2;
+          s3 += e3;
+          pk[jj] = pack_bf16(e0, e1);
+          pk[jj + 1] = pack_bf16(e2, e3);
+        }
+        l = l * alpha + ((s0 + s1) + (s2 + s3));
+        m_run = m_new;
+        if (__any_sync(0xffffffffu, resc) && j > 0) {
+          mbar_wait(&o_done[sb ^ 1], ((i - 1) >> 1) & 1);  // PV(i-1) done: O is stable
+          tc_fence_after();
+#pragma unroll 1
+          for (int c0 = 0; c0 < HD; c0 += 32) {
+            float o[32];
+            tmem_ld32_f(lane_base + o_col + c0, o);
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) o[jj] *= alpha;
+            tmem_st32_f(lane_base + o_col + c0, o);
+          }
+        }
+        tmem_st32_u(lane_base + sb * KEYS, pk);  // P(i) over S(i)
+        tc_fence_before();
+        mbar_arrive(&p_full[sb]);
+      }
+      // ---- segment end: O of this unit's piece
+      const int il = i - 1;
+      mbar_wait(&o_done[il & 1], (il >> 1) & 1);
+      tc_fence_after();
+      const int own0 = owner(sg.pre);
+      const int npieces = owner(sg.pre + sg.Ts - 1) - own0 + 1;
+      if (warp_live) {
+        if (npieces == 1) {  // the whole unit in this CTA: final output
+          const float inv = live ? 1.f / l : 0.f;
+          bf16 *dst = a.out + (((long long)sg.s * a.Nq + rr / a.G) * a.H + (long long)sg.h * a.G + rr % a.G) * HD;
+#pragma unroll
+          for (int c0 = 0; c0 < HD; c0 += 32) {
+            float o[32];
+            tmem_ld32_f(lane_base + o_col + c0, o);
+            if (live) {
+#pragma unroll
+              for (int cc = 0; cc < 4; ++cc) {
+                uint4 w;
+                w.x = pack_bf16(o[8 * cc] * inv, o[8 * cc + 1] * inv);
+                w.y = pack_bf16(o[8 * cc + 2] * inv, o[8 * cc + 3] * inv);
+                w.z = pack_bf16(o[8 * cc + 4] * inv, o[8 * cc + 5] * inv);
+                w.w = pack_bf16(o[8 * cc + 6] * inv, o[8 * cc + 7] * inv);
+                reinterpret_cast<uint4 *>(dst + c0)[cc] = w;
+              }
+            }
+          }
+        } else {  // a piece: unnormalised (m, l, O) column-major in its slot (coalesced over rows)
+          const long long slot = (long long)sg.u + own0 + (c - own0);
+          float *po = a.lean_part + slot * (long long)(ROWS * (HD + 2));
+#pragma unroll
+          for (int c0 = 0; c0 < HD; c0 += 32) {
+            float o[32];
+            tmem_ld32_f(lane_base + o_col + c0, o);
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) __stcg(po + (size_t)(c0 + jj) * ROWS + r, o[jj]);
+          }
+          __stcg(po + (size_t)HD * ROWS + r, live ? m_run : -INFINITY);
+          __stcg(po + (size_t)(HD + 1) * ROWS + r, live ? l : 0.f);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&o_free[ob]);
+      g = gn;
+      sg = nx;
+    }
+  }
+
+  // ---- grid barrier (all Peff CTAs are resident: one per SM, Peff <= SMs), then the combine
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(&a.lean_sync[0], 1);
+    while (ld_acquire_gpu(&a.lean_sync[0]) < Peff) __nanosleep(64);
+  }
+  __syncthreads();
+  {
+    // Units with more than one piece are exactly those a CTA boundary falls inside; unit u is
+    // enumerated once, by the first boundary inside it (CTA b starts inside u and CTA b - 1 starts
+    // at or before u's first tile).  Work item = (boundary b, 32-row group, 32-column chunk), one
+    // warp each, lane = row; decoded directly (no per-item scan).  Loads are batched (8 pieces'
+    // (m, l), then 2 pieces x 32 columns): ~np / 2 + 2 dependent L2 round trips per item.
+    const int gw = c * WARPS + warp, nw = Peff * WARPS;
+    constexpr long long PS = (long long)ROWS * (HD + 2);  // floats per piece slot
+    const int n_items = (Peff - 1) * 16;
+    for (int it2 = gw; it2 < n_items; it2 += nw) {
+      const int b = it2 / 16 + 1, rg = (it2 / 4) % 4, c0 = (it2 % 4) * 32;
+      const long long gb = (long long)b * Ttot / Peff;  // first tile of CTA b
+      LeanSeg su;
+      {
+        int s = 0;
+        while (s + 1 < a.nseq && spre[s + 1] <= gb) ++s;
+        su.s = s;
+        su.Ts = (spre[s + 1] - spre[s]) / UPS;
+        const int ui = (int)((gb - spre[s]) / su.Ts);
+        su.u = s * UPS + ui;
+        su.h = ui / RB;
+        su.rb = ui % RB;
+        su.pre = spre[s] + (long long)ui * su.Ts;
+      }
+      if (gb == su.pre || owner(su.pre) != b - 1) continue;  // not split here, or not its first boundary
+      const int u = su.u, s = su.s, h = su.h, rb = su.rb;
+      const int own0 = b - 1;
+      const int np = owner(su.pre + su.Ts - 1) - own0 + 1;
+      const int live_rows = min(ROWS, R - rb * ROWS);
+      const int w0 = rg * 32;
+      if (w0 >= live_rows) continue;
+      {
+        {
+          const int r = w0 + lane;
+          const bool live = r < live_rows;
+          const float *base = a.lean_part + ((long long)u + own0) * PS;
+          float M = -INFINITY, L = 0.f;
+          for (int q0 = 0; q0 < np; q0 += 8) {
+            float mq[8], lq[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const bool ok = q0 + e < np;
+              mq[e] = ok ? __ldcg(base + (q0 + e) * PS + HD * ROWS + r) : -INFINITY;
+              lq[e] = ok ? __ldcg(base + (q0 + e) * PS + (HD + 1) * ROWS + r) : 0.f;
+            }
+            float Mb = -INFINITY;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) Mb = fmaxf(Mb, mq[e]);
+            const float Mn = fmaxf(M, Mb);
+            float Lb = 0.f;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) Lb += mq[e] == -INFINITY ? 0.f : exp2f(mq[e] - Mn) * lq[e];
+            L = (M == -INFINITY ? 0.f : L * exp2f(M - Mn)) + Lb;
+            M = Mn;
+          }
+          const float invL = live ? 1.f / L : 0.f;
+          float acc[32];
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) acc[jj] = 0.f;
+          for (int q = 0; q < np; q += 2) {  // piece order: deterministic
+            float v0[32], v1[32], w[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const bool ok = q + e < np;
+              const float mq = ok ? __ldcg(base + (q + e) * PS + HD * ROWS + r) : -INFINITY;
+              w[e] = mq == -INFINITY ? 0.f : exp2f(mq - M) * invL;
+            }
+            const float *b0 = base + q * PS + (size_t)c0 * ROWS + r;
+            const float *b1 = q + 1 < np ? b0 + PS : b0;
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) {
+              v0[jj] = __ldcg(b0 + (size_t)jj * ROWS);
+              v1[jj] = __ldcg(b1 + (size_t)jj * ROWS);
+            }
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) acc[jj] += w[0] * v0[jj] + w[1] * v1[jj];
+          }
+          if (live) {
+            const int rr = rb * ROWS + r;
+            bf16 *dst = a.out + (((long long)s * a.Nq + rr / a.G) * a.H + (long long)h * a.G + rr % a.G) * HD + c0;
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+              uint4 wv;
+              wv.x = pack_bf16(acc[8 * cc], acc[8 * cc + 1]);
+              wv.y = pack_bf16(acc[8 * cc + 2], acc[8 * cc + 3]);
+              wv.z = pack_bf16(acc[8 * cc + 4], acc[8 * cc + 5]);
+              wv.w = pack_bf16(acc[8 * cc + 6], acc[8 * cc + 7]);
+              reinterpret_cast<uint4 *>(dst)[cc] = wv;
+            }
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // the last CTA out resets the barrier for the next launch (every CTA has passed the wait)
+    if (atomicAdd(&a.lean_sync[1], 1) == Peff - 1) {
+      a.lean_sync[0] = 0;
+      a.lean_sync[1] = 0;
+      __threadfence();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 5) tmem_dealloc<512>(tmem);
+}
+
+cudaError_t attention_lean_launch(const AttnArgs &a, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tree_attn_lean_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lean::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (a.nseq > kLeanMaxSeq || !a.lean_part || !a.lean_sync) return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(kNumSMs);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = lean::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = gemm_pdl() ? 1 : 0;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, tree_attn_lean_kernel, a);
+}
+
+// Partial slots the lean kernel may use for nunits units: nunits + 148 of [128 rows][hd + 2] fp32.
+size_t attention_lean_part_floats(int nunits) { return (size_t)(nunits + kNumSMs) * lean::ROWS * (lean::HD + 2); }
+
 SM_GT_READER(sm_gtrace_read_attn)
 #ifdef SM_TRACE
 extern "C" int sm_trace_read(long long *dst, int n) {  // diagnostics build only
@@ -568,6 +1100,7 @@ void attention_set_l2pf(int on) { cudaMemcpyToSymbol(g_attn_l2pf, &on, sizeof(in
 
 void attention_tc_preload() {  // force-load (see gemm_preload)
   cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, tree_attn_lean_kernel);
   cudaFuncGetAttributes(&fa, tree_attn_tc_kernel<false>);
   cudaFuncGetAttributes(&fa, tree_attn_tc_kernel<true>);
 }

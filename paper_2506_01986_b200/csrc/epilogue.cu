@@ -234,13 +234,22 @@ cudaError_t resid_norm_split_launch(const PartialView *pv, float *x, const bf16 
                     ss);
 }
 
-// Tensor-parallel variant (a7): the residual all-reduce fused in.  Each rank reduces
-// its own split-K partials of a row slice, publishes the fp32 slice in its symmetric
-// buffer, raises a per-CTA epoch flag in every peer, waits for the peers' flags of
-// the same CTA and sums the t slices in rank order -- every rank then holds bitwise
-// the same residual.  Persistent over rows (grid <= resident capacity) so the CTA a
-// rank waits on is always running on the peer.  The DSMEM sum-of-squares slots are
-// double-buffered by iteration parity.
+// Tensor-parallel variant (a7): the residual all-reduce fused in.  Each rank reduces its own
+// split-K partials of a row slice and publishes the fp32 slice in its symmetric buffer.
+//  * one-shot (t = 2): raise a per-CTA flag in every peer, wait for the peers' flags of the same
+//    CTA, read the t - 1 peer slices and sum the t slices in rank order: (t - 1) slice reads.
+//  * reduce-scatter + all-gather (RSAG, t >= 4): the slice is cut into t sub-chunks; rank r sums
+//    sub-chunk r over the ranks (rank order), writes the sum over its own partial of that
+//    sub-chunk, raises a second flag, and every rank gathers the other t - 1 reduced sub-chunks:
+//    2 (t - 1) / t of a slice read per rank instead of t - 1 (t = 8: 1.75 vs 7 slices), one more
+//    flag round trip.  The owner's sum has the same operands in the same order as the one-shot
+//    sum, so both variants give every rank bitwise the same residual.
+// Flags: exchange k of the call raises 2 (seq + k + 1) - 1 after publishing the partial and
+// 2 (seq + k + 1) after publishing its reduced sub-chunk (monotone across exchanges; tp.cu's merges
+// use the even value).  Persistent over rows (grid <= resident capacity) so the CTA a rank waits
+// on is always running on the peer.  The DSMEM sum-of-squares slots are double-buffered by
+// iteration parity.
+template <bool RSAG>
 __global__ void __launch_bounds__(kNormThreads) resid_norm_tp_kernel(PartialView pv, float *x, const bf16 *g, bf16 *h,
                                                                      int M, int d, float eps, TpArgs tp,
                                                                      float *rs_out) {
@@ -251,8 +260,21 @@ __global__ void __launch_bounds__(kNormThreads) resid_norm_tp_kernel(PartialView
   pdl_wait();
   const int crank = blockIdx.x, cs = gridDim.x;
   const int i = crank * kNormCols + threadIdx.x * 4;
-  const long long ep = *tp.seq + tp.point + 1;
+  const long long ep = 2 * (*tp.seq + tp.point + 1);
+  // RSAG: this thread's 4 columns belong to sub-chunk own_j of the CTA's slice
+  const int width4 = (min(kNormCols, d - crank * kNormCols) + 3) / 4;  // 4-column groups in the slice
+  const int own_j = (int)(((long long)threadIdx.x * tp.t) / max(1, width4));
   int it = 0;
+  auto signal_wait = [&](int idx, long long v) {
+    __threadfence_system();
+    __syncthreads();
+    const int q = threadIdx.x;
+    if (q < tp.t && q != tp.rank) {
+      st_release_sys(tp.flags[q] + (size_t)tp.rank * kTpFlagSlots + idx, v);
+      tp_wait_flag(tp.flags[tp.rank] + (size_t)q * kTpFlagSlots + idx, v, tp.err);
+    }
+    __syncthreads();
+  };
   for (int m = blockIdx.y; m < M; m += gridDim.y, ++it) {
     float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
     if (i < d) {
@@ -262,32 +284,35 @@ __global__ void __launch_bounds__(kNormThreads) resid_norm_tp_kernel(PartialView
       y = sk_reduce<16>(ref, ys);
       __stcg(reinterpret_cast<float4 *>(tp.data[tp.rank] + (size_t)m * d + i), y);
     }
-    __threadfence_system();
-    __syncthreads();
     const int idx = m * cs + crank;
-    const int q = threadIdx.x;
-    if (q < tp.t && q != tp.rank) {
-      st_release_sys(tp.flags[q] + (size_t)tp.rank * kTpFlagSlots + idx, ep);
-      tp_wait_flag(tp.flags[tp.rank] + (size_t)q * kTpFlagSlots + idx, ep, tp.err);
+    signal_wait(idx, ep - 1);
+    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!RSAG || own_j == tp.rank) {  // sum this sub-chunk (one-shot: the whole slice) in rank order
+      if (i < d) {
+        float4 part[kMaxTP];
+#pragma unroll
+        for (int r = 0; r < kMaxTP; ++r)
+          if (r < tp.t)
+            part[r] = r == tp.rank ? y : __ldcv(reinterpret_cast<const float4 *>(tp.data[r] + (size_t)m * d + i));
+#pragma unroll
+        for (int r = 0; r < kMaxTP; ++r) {  // rank order: identical on every rank
+          if (r < tp.t) {
+            sum.x += part[r].x;
+            sum.y += part[r].y;
+            sum.z += part[r].z;
+            sum.w += part[r].w;
+          }
+        }
+        if (RSAG) __stcg(reinterpret_cast<float4 *>(tp.data[tp.rank] + (size_t)m * d + i), sum);
+      }
     }
-    __syncthreads();
+    if (RSAG) {
+      signal_wait(idx, ep);
+      if (own_j != tp.rank && i < d)  // gather the owner's reduced sub-chunk
+        sum = __ldcv(reinterpret_cast<const float4 *>(tp.data[own_j] + (size_t)m * d + i));
+    }
     float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
     if (i < d) {
-      float4 part[kMaxTP];
-#pragma unroll
-      for (int r = 0; r < kMaxTP; ++r)
-        if (r < tp.t)
-          part[r] = r == tp.rank ? y : __ldcv(reinterpret_cast<const float4 *>(tp.data[r] + (size_t)m * d + i));
-      float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int r = 0; r < kMaxTP; ++r) {  // rank order: identical on every rank
-        if (r < tp.t) {
-          sum.x += part[r].x;
-          sum.y += part[r].y;
-          sum.z += part[r].z;
-          sum.w += part[r].w;
-        }
-      }
       float *xr = x + (size_t)m * d;
       a = *reinterpret_cast<const float4 *>(xr + i);
       a.x += sum.x;
@@ -316,13 +341,19 @@ __global__ void __launch_bounds__(kNormThreads) resid_norm_tp_kernel(PartialView
   }
   if (it == 0) cluster_wait();  // no rows: complete the start barrier phase
 }
+static int g_tp_rsag = -1;  // sm_set_option("tp_rsag"): -1 auto (t >= 4), 0 one-shot, 1 reduce-scatter + all-gather
+void tp_set_rsag(int mode) { g_tp_rsag = mode; }
 cudaError_t resid_norm_tp_launch(const PartialView &pv, float *x, const bf16 *g, bf16 *h, int M, int d, float eps,
                                  const TpArgs &tp, float *rs_out, cudaStream_t st) {
   const int cs = (d + kNormCols - 1) / kNormCols;
   if (cs > 8 || d % 4 || M * cs > kTpFlagSlots) return cudaErrorInvalidValue;
   const int rows_par = M < 64 ? M : 64;  // cs x 64 CTAs: always co-resident
-  return launch_pdl_cluster(resid_norm_tp_kernel, dim3(cs, rows_par), dim3(kNormThreads), 0, st, cs, pv, x, g, h, M, d,
-                            eps, tp, rs_out);
+  const bool rsag = g_tp_rsag < 0 ? tp.t >= 4 : g_tp_rsag != 0;
+  if (rsag)
+    return launch_pdl_cluster(resid_norm_tp_kernel<true>, dim3(cs, rows_par), dim3(kNormThreads), 0, st, cs, pv, x, g,
+                              h, M, d, eps, tp, rs_out);
+  return launch_pdl_cluster(resid_norm_tp_kernel<false>, dim3(cs, rows_par), dim3(kNormThreads), 0, st, cs, pv, x, g, h,
+                            M, d, eps, tp, rs_out);
 }
 
 // ------------------------------------------------------------------ QKV consumer (RoPE + cache write)
@@ -911,7 +942,8 @@ void epilogue_preload() {  // force-load (see gemm_preload)
   cudaFuncAttributes fa;
   cudaFuncGetAttributes(&fa, embed_kernel);
   cudaFuncGetAttributes(&fa, resid_norm_kernel);
-  cudaFuncGetAttributes(&fa, resid_norm_tp_kernel);
+  cudaFuncGetAttributes(&fa, resid_norm_tp_kernel<false>);
+  cudaFuncGetAttributes(&fa, resid_norm_tp_kernel<true>);
   cudaFuncGetAttributes(&fa, resid_norm_split_kernel);
   cudaFuncGetAttributes(&fa, resid_norm_split4_kernel);
   cudaFuncGetAttributes(&fa, qkv_consumer_kernel<false>);

@@ -352,6 +352,11 @@ struct AttnArgs {
   const uint32_t *pad;        // nullable: pad-batching bitmap [seq][pad_words] of masked cache slots (f4)
   int pad_words;
   int causal;                 // prefill chunk (f3): anc unused, tree slot j visible to node n iff j <= n
+  // stream-K ("lean") tree kernel (attention_tc.cu): partial slots, barrier counters (zeroed once,
+  // reset by the kernel), minimum tiles per CTA
+  float *lean_part;
+  int *lean_sync;
+  int lean_min_tiles;
 };
 cudaError_t attention_launch(const AttnArgs &a, int head_dim, cudaStream_t st);
 int attention_row_blocks(int Nq, int G, int head_dim);
@@ -361,6 +366,12 @@ cudaError_t attention_f32_launch(const float *q, const float *k, const float *v,
                                  const uint64_t *anc, int Nq, int H, int Hkv, int hd, int cap, int nseq, int seq_base,
                                  const uint32_t *pad, int pad_words, bf16 *out, cudaStream_t st);
 int attention_nsplit(int units, int head_dim);  // units = row blocks * sequences * kv heads
+constexpr int kLeanMaxSeq = 64;                 // sequences per lean K1 launch
+cudaError_t attention_lean_launch(const AttnArgs &a, cudaStream_t st);
+size_t attention_lean_part_floats(int nunits);
+void attention_set_lean(int on);
+void attention_set_lean_div(int d);
+int attention_lean_min_tiles(int Nq, int G);
 void attention_set_splits(int n);               // experiments: force key splits (0 = auto)
 void attention_set_tc(int on);                  // head_dim 128: tcgen05 kernel (1, default) or mma.sync (0)
 void attention_set_l2pf(int on);                // experiments: L2 prefetch of AttnArgs.l2_pf (0, default)
@@ -467,6 +478,7 @@ struct TpArgs {
   int *err;                       // set to 1 when a wait times out
 };
 // Residual all-reduce fused into residual + RMSNorm (pv = this rank's o_proj / down partials).
+void tp_set_rsag(int mode);  // -1 auto (t >= 4), 0 one-shot, 1 reduce-scatter + all-gather
 cudaError_t resid_norm_tp_launch(const PartialView &pv, float *x, const bf16 *g, bf16 *h, int M, int d, float eps,
                                  const TpArgs &tp, float *rs_out, cudaStream_t st);
 // Merge the vocab-parallel LM head statistics of rows [0, rows): in = this rank's

@@ -496,7 +496,13 @@ struct sm_model {
   int tp_point = 0;              // host: exchange index within the current top-level call
   float *amax = nullptr, *cand = nullptr, *tk_val = nullptr;
   int32_t *tk_idx = nullptr;
+  float *lean_part = nullptr;  // stream-K K1 partial slots (bf16 path, head_dim 128)
+  int *lean_sync = nullptr;    // its grid-barrier counters (zero between launches)
 };
+
+// Most K1 units (sequence x kv head x 128-row block) one forward can have: nseq <= B sequences of
+// Nq nodes with nseq Nq <= R rows, so nseq ceil(Nq G / 128) <= B + R G / 128.
+static int lean_units_max(int Hkv, int G, int R, int B) { return Hkv * (B + (R * G + 127) / 128); }
 
 static size_t tp_slot_floats(const sm_model_cfg &c) {
   return std::max({(size_t)c.max_rows * c.d_model, (size_t)c.max_rows * 8,
@@ -711,6 +717,11 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
   ALLOC(m->cand, (size_t)R, "cand");
   ALLOC(m->tk_val, (size_t)B * std::max(1, m->nmed) * 32, "topk values");
   ALLOC(m->tk_idx, (size_t)B * std::max(1, m->nmed) * 32, "topk indices");
+  if (!m->f32 && m->hd == 128) {
+    ALLOC(m->lean_part, attention_lean_part_floats(lean_units_max(m->Hkv, m->G, R, B)), "K1 partial slots");
+    ALLOC(m->lean_sync, 2, "K1 barrier");
+    cudaMemset(m->lean_sync, 0, 2 * sizeof(int));
+  }
   ALLOC(m->tp_seq, 1, "tp epoch");
   ALLOC(m->tp_err, 1, "tp error flag");
   cudaMemset(m->tp_seq, 0, sizeof(long long));
@@ -812,6 +823,8 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
 
 extern "C" void sm_model_destroy(sm_model *m) {
   if (!m) return;
+  cudaFree(m->lean_part);
+  cudaFree(m->lean_sync);
   cudaFree(m->x);
   cudaFree(m->rs);
   cudaFree(m->ss);
@@ -1023,6 +1036,8 @@ extern "C" sm_status sm_workspace_bytes(const sm_model_cfg *cfg, size_t *bytes) 
   b += R * c.d_ffn * 2 * P + R * d * 2 * P + R * c.vocab * 4 + R * 4 + R * 3 * 4;                // act, hf, z, argmax, stats
   b += B * d * 2 * P + nmed * B * d * 2 * P + (size_t)c.max_seq_len * (c.head_dim / 2) * 8;       // head_in, r_buf, rope
   b += 2 * R * 4 + 2 * B * nmed * 32 * 4 + 16;                                                      // amax, cand, top-k
+  if (c.dtype != SM_DTYPE_FP32 && c.head_dim == 128)                                                 // K1 partials
+    b += attention_lean_part_floats(lean_units_max(c.n_kv_heads, c.n_heads / c.n_kv_heads, (int)R, (int)B)) * 4 + 8;
   // stream-K partial slots: the largest need over the model's GEMMs
   size_t need = 0;
   const int Rg = (int)(R * P);
@@ -1325,6 +1340,9 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
     aa.pad = kv->pad_mode ? kv->pad : nullptr;
     aa.pad_words = kv->pad_words;
     aa.causal = tree.anc == nullptr;  // causal prefill chunk (sm_prefill)
+    aa.lean_part = m->lean_part;
+    aa.lean_sync = m->lean_sync;
+    aa.lean_min_tiles = attention_lean_min_tiles(Nq, m->G);
     aa.l2_pf = m->wo[l];  // o_proj weights stream into L2 while attention runs
     aa.l2_pf_bytes = (unsigned long long)d * m->H * m->hd * 2;
     cudaEvent_t ev = nullptr;
@@ -1712,6 +1730,27 @@ static sm_status scratch(size_t bytes, cudaStream_t st, void **p) {
   return SM_OK;
 }
 
+// The stage K1's lean workspace: [256 B: barrier counters, zero between launches][partial slots],
+// per stream (a growth re-zeroes the counters; same capture rule as scratch()).
+static std::map<cudaStream_t, std::pair<void *, size_t>> g_lean_scratch;
+static sm_status lean_scratch(size_t bytes, cudaStream_t st, void **p) {
+  auto &e = g_lean_scratch[st];
+  if (bytes + 256 > e.second) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(st, &cs));
+    if (cs != cudaStreamCaptureStatusNone)
+      return fail(SM_ERR_UNSUPPORTED, "stage scratch must grow during stream capture: call once uncaptured first");
+    CK(cudaDeviceSynchronize());
+    cudaFree(e.first);
+    e = {nullptr, 0};
+    if (cudaMalloc(&e.first, bytes + 256) != cudaSuccess) return fail(SM_ERR_DEVICE_OOM, "Buffer: K1 stage scratch");
+    CK(cudaMemset(e.first, 0, 256));
+    e.second = bytes + 256;
+  }
+  *p = e.first;
+  return SM_OK;
+}
+
 static sm_status attention_stage(const uint64_t *d_anc, int Nq, const void *d_q, const void *d_k, const void *d_v,
                                  const int32_t *d_len, int batch, int n_heads, int n_kv_heads, int head_dim, int cap,
                                  void *d_out, void *stream) {
@@ -1741,6 +1780,14 @@ static sm_status attention_stage(const uint64_t *d_anc, int Nq, const void *d_q,
   aa.seq_base = 0;
   aa.nsplit = nsplit;
   aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)head_dim));
+  if (head_dim == 128 && d_anc) {  // stream-K K1: per-stream partial slots + zeroed barrier counters
+    const int units = batch * n_kv_heads * attention_row_blocks(Nq, G, head_dim);
+    void *p = nullptr;
+    CKS(lean_scratch(attention_lean_part_floats(units) * 4, (cudaStream_t)stream, &p));
+    aa.lean_sync = reinterpret_cast<int *>(p);
+    aa.lean_part = reinterpret_cast<float *>(reinterpret_cast<char *>(p) + 256);
+    aa.lean_min_tiles = attention_lean_min_tiles(Nq, G);
+  }
   CK(attention_launch(aa, head_dim, (cudaStream_t)stream));
   return SM_OK;
 }
@@ -1832,6 +1879,9 @@ extern "C" sm_status sm_reset_options(void) {
   attention_set_tc(1);
   attention_set_l2pf(0);
   attention_set_splits(0);
+  attention_set_lean(0);
+  attention_set_lean_div(16);
+  tp_set_rsag(-1);
   g_fused = 0;
   g_epi_test = 0;
   g_ablate = 0;
@@ -1880,6 +1930,12 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
     attention_set_l2pf(value);
   } else if (n == "attn_splits") {
     attention_set_splits(value);
+  } else if (n == "tp_rsag") {  // TP residual exchange: -1 auto (t >= 4 RS+AG), 0 one-shot, 1 RS+AG
+    tp_set_rsag(value);
+  } else if (n == "attn_lean") {  // tree-mode K1 (hd 128): stream-K kernel (1, default) or cluster splits (0)
+    attention_set_lean(value);
+  } else if (n == "attn_lean_div") {  // lean K1: minimum tiles per CTA = max(2, live rows / value)
+    attention_set_lean_div(value);
   } else {
     return fail(SM_ERR_INVALID_ARG, "sm_set_option: unknown option " + n);
   }

@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(1024) tp_merge_logits_kernel(int rows, const f
                                                                float *cand, TpArgs tp) {
   pdl_trigger();
   pdl_wait();
-  const long long ep = *tp.seq + tp.point + 1;
+  const long long ep = 2 * (*tp.seq + tp.point + 1);  // even: see resid_norm_tp_kernel
   const int r = threadIdx.x;
   if (r < rows) {
     float c = __int_as_float(0x7fc00000);  // NaN: this rank does not own the candidate token
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(256) tp_merge_topk_kernel(int entries, int K, 
                                                             const int32_t *idx_local, int32_t *idx_out, TpArgs tp) {
   pdl_trigger();
   pdl_wait();
-  const long long ep = *tp.seq + tp.point + 1;
+  const long long ep = 2 * (*tp.seq + tp.point + 1);  // even: see resid_norm_tp_kernel
   for (int e = threadIdx.x; e < entries; e += blockDim.x) {
     float *dst = tp.data[tp.rank] + (size_t)e * 2 * K;
     for (int k = 0; k < K; ++k) {

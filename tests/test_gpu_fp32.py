@@ -158,11 +158,20 @@ def test_c2_shape_two_layers_sampled_rows(sm, c2_oracle_weights, dtype):
     s = OS.Session(m, synth.V64, 1, 64)
     s.prefill(0, prompt)
     tok_ref, _ = s.propose(0)
-    # tree tokens are integer outputs (root argmax + head top-K): bit-exact in fp32; in
-    # bf16 a top-10 near-tie of the 32000 logits may swap two ranks, so only most must agree
+    # tree tokens are integer outputs (root argmax + head top-K): bit-exact wherever the oracle's
+    # top-K gap clears the guard (every one at fp32), else a valid near-tie choice
     assert tok_gpu[0] == tok_ref[0]
-    agree = sum(int(a == b) for a, b in zip(tok_gpu, tok_ref))
-    assert agree == tree.N if dtype == "fp32" else agree >= 56, (agree, tok_gpu, tok_ref)
+    tr0 = s.tree
+    u = np.asarray(m.head_logits(0, s.last_hf[0]), np.float64)  # Medusa-init: every head = LM head
+    order = OM.topk_desc(u, 11)
+    guard = 1e-5 if dtype == "fp32" else 0.05
+    for n in range(1, tree.N):
+        rk = tr0.rank[n]
+        gap = min(u[order[rk - 1]] - u[order[rk]] if rk > 0 else np.inf, u[order[rk]] - u[order[rk + 1]])
+        if gap >= guard:
+            assert tok_gpu[n] == tok_ref[n], (n, tok_gpu[n], tok_ref[n])
+        else:
+            assert abs(u[tok_gpu[n]] - u[order[rk]]) <= 2 * guard, n
     tr = s.tree
     Zg = logits[0].cpu().numpy().astype(np.float64)
     kvl = kv.layout()
@@ -175,15 +184,13 @@ def test_c2_shape_two_layers_sampled_rows(sm, c2_oracle_weights, dtype):
             assert ok, (dtype, n, err)
             assert int(np.argmax(Zg[n])) == OM.argmax_lowest(z)
         else:
-            # bf16 at 7B width (reading Q29): storage-point roundings that differ by one
-            # ulp cascade through the layers (measured: ~60% of layer-1 K elements differ by 1 ulp,
-            # logit error rms ~0.008 at |z| rms 1.28), so 2e-2 is read scale-relative: max error
-            # <= 2e-2 max|z| and ||dz|| <= 2e-2 ||z||; the elementwise bar is the fp32 mode's.
-            e = np.abs(Zg[n] - z)
-            assert e.max() <= tol * np.abs(z).max(), (n, e.max())
-            assert np.linalg.norm(Zg[n] - z) <= tol * np.linalg.norm(z), n
+            # bf16 at 7B width (reading Q29): per row at most 1 % of the elements over the
+            # 2e-2 (1 + |z|) bar and none over 3x it (one-ulp storage-point differences cascade);
+            # argmax decisions with margin are bit-exact
+            r = np.abs(Zg[n] - z) / (tol * (1 + np.abs(z)))
+            assert np.mean(r > 1) <= 1e-2 and r.max() <= 3.0, (n, np.mean(r > 1), r.max())
             zs = np.sort(z)[::-1]
-            if zs[0] - zs[1] > 2 * tol * np.abs(z).max():  # argmax decisions with margin are bit-exact
+            if zs[0] - zs[1] > 1e-2 * np.abs(z).max():
                 assert int(np.argmax(Zg[n])) == OM.argmax_lowest(z)
     for li in range(2):
         for c in (0, 1):
@@ -194,12 +201,12 @@ def test_c2_shape_two_layers_sampled_rows(sm, c2_oracle_weights, dtype):
             if dtype == "fp32":
                 ok, err = close(g, r, tol)
                 assert ok, (dtype, li, c, err)
-            else:  # scale-relative (reading Q29, as for the logits); layer 0 is elementwise
-                assert np.abs(g - r).max() <= tol * np.abs(r).max(), (li, c)
-                assert np.linalg.norm(g - r) <= tol * np.linalg.norm(r), (li, c)
+            else:  # reading Q29: layer 0 elementwise; deeper layers the per-row exceedance bound
+                r = np.abs(g - r) / (tol * (1 + np.abs(r)))
                 if li == 0:
-                    ok, err = close(g, r, tol)
-                    assert ok, (dtype, li, c, err)
+                    assert r.max() <= 1.0, (li, c, r.max())
+                else:
+                    assert np.mean(r > 1) <= 1e-2 and r.max() <= 3.0, (li, c, np.mean(r > 1), r.max())
 
 
 # ------------------------------------------------------------------ fused K2 tile epilogues (hd = 128)
@@ -292,14 +299,18 @@ def test_c2_width_batched_pair_path_matches_unbatched(sm):
     tb, zb, kb = run(3, prompts)
     for i, p in enumerate(prompts):
         t1, z1, k1 = run(1, [p])
-        agree = int((tb[i] == t1[0]).sum())
-        assert agree >= 56, agree                       # tree tokens (top-10 near-ties aside)
-        if agree == tree.N:
-            e = (zb[i] - z1[0]).abs()
-            assert float(e.max()) <= 2e-2 * float(z1[0].abs().max())
-            assert float((zb[i] - z1[0]).norm()) <= 2e-2 * float(z1[0].norm())
+        # same prefill, same heads path: the tree tokens are bit-identical
+        assert torch.equal(tb[i], t1[0])
+        # verify rows: M = 192 on the 2-SM K2 vs M = 64 single-SM -- only the fp32 summation order of
+        # the split-K partials differs; the bf16 bar per row (Q29: <= 1 % of elements over
+        # 2e-2 (1 + |z|), none over 3x)
         L = len(p)
+        for n in range(tree.N):
+            bar = 2e-2 * (1 + z1[0, n].abs())
+            r = (zb[i, n] - z1[0, n]).abs() / bar
+            assert float((r > 1).double().mean()) <= 1e-2 and float(r.max()) <= 3.0, n
         for li in range(2):
             for c in (0, 1):
-                a, r = kb[li, c, i][:, :L], k1[li, c, 0][:, :L]   # prompt K/V (prefill: M = L rows)
-                assert float((a - r).abs().max()) <= 2e-2 * float(r.abs().max())
+                a, ref = kb[li, c, i][:, :L + tree.N], k1[li, c, 0][:, :L + tree.N]  # prompt + tree slots
+                r = (a - ref).abs() / (2e-2 * (1 + ref.abs()))
+                assert float((r > 1).double().mean()) <= 1e-2 and float(r.max()) <= 3.0, (li, c)

@@ -129,16 +129,27 @@ ATTN_CASES = [
     # one split (no cluster) with padding rows inside a live warp (16 or 48 live rows of 128)
     ("n16_ns1_mha", synth.SWEEP_TREES[16], None, 4, 32, 32, 128, [512, 100, 7, 300], 0),
     ("n16_ns1_g3", synth.TINY16, None, 20, 24, 8, 128, [(37 * i) % 300 for i in range(20)], 1),
+    # stream-K K1: one unit over many CTAs (pieces), many small ragged units, units of 4 row blocks
+    ("lean_one_unit_long", synth.V64, None, 1, 1, 1, 128, [9000], 0),
+    ("lean_many_units", synth.V64[:31], None, 40, 4, 2, 128, [(211 * i) % 2500 for i in range(40)], 3),
+    ("lean_gqa8_4blocks", synth.V64, None, 3, 8, 1, 128, [3000, 5, 1200], 0),
 ]
 
 
-@pytest.mark.parametrize("attn_tc", [1, 0], ids=["tc", "mma"])
+# K1 variants for head_dim 128: the stream-K tcgen05 kernel (default; min tiles per CTA = live rows
+# per unit / 16, and / 2 for many more pieces per unit), the cluster-split tcgen05 kernel, mma.sync
+VARIANTS = {"default": dict(), "lean": dict(attn_tc=1, attn_lean=1),
+            "lean_div2": dict(attn_tc=1, attn_lean=1, attn_lean_div=2), "mma": dict(attn_tc=0)}
+
+
+@pytest.mark.parametrize("variant", list(VARIANTS))
 @pytest.mark.parametrize("case", ATTN_CASES, ids=[c[0] for c in ATTN_CASES])
-def test_tree_attention_matches_oracle(sm, case, attn_tc):
+def test_tree_attention_matches_oracle(sm, case, variant):
     name, choices, chain, b, H, Hkv, hd, lens, extra = case
-    if attn_tc == 0 and hd != 128:
+    if variant != "default" and hd != 128:
         pytest.skip("head_dim < 128 always runs the mma.sync kernel")
-    sm.set_option("attn_tc", attn_tc)
+    for k, v in VARIANTS[variant].items():
+        sm.set_option(k, v)
     tree = sm.Tree(choices, topk=10) if chain is None else sm.Tree(None, chain=chain)
     N = tree.N
     cap = max(lens) + N + extra
@@ -153,7 +164,6 @@ def test_tree_attention_matches_oracle(sm, case, attn_tc):
     got = to64(out)
     assert np.all(np.isfinite(got))
     err = np.abs(got - ref)
-    sm.set_option("attn_tc", 1)
     assert np.all(err <= 2e-2 + 2e-2 * np.abs(ref)), float(err.max())
 
 

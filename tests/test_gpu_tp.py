@@ -40,16 +40,16 @@ def _no_pdl(sm):
 
 
 class Ranks:
-    def __init__(self, sm, t, seed=0, n_medusa=3, choices=synth.TINY16, batch=1, medusa_init=False):
+    def __init__(self, sm, t, seed=0, n_medusa=3, choices=synth.TINY16, batch=1, medusa_init=False, cfg=CFG):
         self.sm, self.t = sm, t
         self.tree = sm.Tree(choices, topk=10)
         R = max(batch * self.tree.N, 64)
-        nbytes = sm.tp_sym_bytes(CFG, R, batch, n_medusa)
+        nbytes = sm.tp_sym_bytes(cfg, R, batch, n_medusa)
         self.sym = [torch.zeros(nbytes, dtype=torch.uint8, device="cuda") for _ in range(t)]
         ptrs = [s.data_ptr() for s in self.sym]
-        self.W = [sm.allocate_weights(CFG, n_medusa, seed=seed, medusa_init=medusa_init, tp_rank=r, tp_size=t)
+        self.W = [sm.allocate_weights(cfg, n_medusa, seed=seed, medusa_init=medusa_init, tp_rank=r, tp_size=t)
                   for r in range(t)]
-        self.models = [sm.Model(CFG, self.W[r], R, batch, X + self.tree.N, peer_sym=ptrs) for r in range(t)]
+        self.models = [sm.Model(cfg, self.W[r], R, batch, X + self.tree.N, peer_sym=ptrs) for r in range(t)]
         self.kvs = [sm.KVCache(m, self.tree, batch, X) for m in self.models]
         self.streams = [torch.cuda.Stream() for _ in range(t)]
         self.outs = [sm.AcceptOut(batch, self.tree.depth) for _ in range(t)]
@@ -174,3 +174,120 @@ def test_tp_typical_accept_matches_tp1(sm, seed):
         assert torch.equal(toks[r], tok1)
         for name in ("acc_len", "best_leaf", "path", "emit_tok", "n_emit"):
             assert torch.equal(getattr(rk.outs[r], name), getattr(o1, name)), name
+
+
+# ------------------------------------------------------------------ t = 8 (the 70B shape's TP8 placement)
+# 8 kv heads so every rank owns one (C4 at TP8: Hkv / t = 1), d = 128, F = 512 (F / 64 divisible by 8)
+CFG8 = synth.model_cfg("tiny", d_model=128, n_heads=8, n_kv_heads=8, head_dim=16, d_ffn=512, vocab=256)
+
+
+def _greedy_ref(cfg, seed, n):
+    prompt = synth.prompt_tokens(seed, 0, 32, cfg["vocab"])
+    s = OS.Session(OM.Model(cfg, OM.Weights(cfg, n_medusa=3, seed=seed), "bf16"), synth.TINY16, batch=1,
+                   max_seq_len=X)
+    s.prefill(0, prompt)
+    ref = []
+    while len(ref) < n:
+        ref += s.step(0, budget=n - len(ref))["emitted"]
+    assert ref == OS.vanilla_generate(s.m, prompt, n)[0]
+    return prompt, ref
+
+
+@pytest.mark.parametrize("pdl", [1, 0], ids=["pdl", "nopdl"])
+@pytest.mark.parametrize("seed", [0, 2])
+def test_tp8_greedy_tokens_equal_oracle(sm, seed, pdl):
+    """t = 8 ranks on one GPU (8 streams of one process), with and without programmatic dependent
+    launch: every rank emits the oracle's greedy stream (= vanilla greedy)."""
+    sm.set_option("pdl", pdl)
+    t, n = 8, 24
+    prompt, ref = _greedy_ref(CFG8, seed, n)
+    rk = Ranks(sm, t, seed=seed, cfg=CFG8)
+    pt = torch.from_numpy(prompt).cuda()
+    rk.each(lambda r, kv, st: kv.prefill(0, pt, stream=st))
+    budgets = [torch.full((1,), n, dtype=torch.int32, device="cuda") for _ in range(t)]
+    cfgs = [sm.accept_cfg(sm.GREEDY, max_new=budgets[r]) for r in range(t)]
+    toks = [[] for _ in range(t)]
+    for _ in range(2 * n):
+        if len(toks[0]) >= n:
+            break
+        rk.each(lambda r, kv, st: kv.step(cfgs[r], rk.outs[r], stream=st))
+        for r in range(t):
+            o = rk.outs[r]
+            ne = int(o.n_emit.cpu()[0])
+            toks[r] += o.emit_tok.cpu().numpy()[0][:ne].tolist()
+            budgets[r] -= o.n_emit
+    assert not rk.timed_out()
+    for r in range(t):
+        assert toks[r] == toks[0]
+    assert toks[0] == ref
+
+
+# ------------------------------------------------------------------ two processes, CUDA IPC
+def _ipc_rank(rank, world, port, seed, n, q):
+    import os
+
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2506_01986_b200 as sm
+        torch.cuda.set_device(0)
+        tree = sm.Tree(synth.TINY16, topk=10)
+        W = sm.allocate_weights(CFG, 3, seed=seed, tp_rank=rank, tp_size=world)
+        sym = torch.zeros(sm.tp_sym_bytes(CFG, 64, 1, 3), dtype=torch.uint8, device="cuda")
+        hs = [None] * world
+        dist.all_gather_object(hs, sm.ipc_handle(sym))
+        peers = [sym.data_ptr() if r == rank else sm.ipc_open(hs[r]) for r in range(world)]
+        model = sm.Model(CFG, W, 64, 1, X + tree.N, peer_sym=peers)
+        torch.cuda.synchronize()
+        dist.barrier()  # every rank's buffer is zeroed before any exchange
+        kv = sm.KVCache(model, tree, 1, X)
+        kv.prefill(0, torch.from_numpy(synth.prompt_tokens(seed, 0, 32, CFG["vocab"])).cuda())
+        budget = torch.full((1,), n, dtype=torch.int32, device="cuda")
+        cfg = sm.accept_cfg(sm.GREEDY, max_new=budget)
+        out = sm.AcceptOut(1, tree.depth)
+        toks = []
+        for _ in range(2 * n):
+            if len(toks) >= n:
+                break
+            kv.step(cfg, out)
+            ne = int(out.n_emit.cpu()[0])
+            toks += out.emit_tok.cpu().numpy()[0][:ne].tolist()
+            budget -= out.n_emit
+        q.put((rank, toks, model.tp_timed_out()))
+        torch.cuda.synchronize()
+        dist.barrier()
+        for r, p in enumerate(peers):
+            if r != rank:
+                sm.ipc_close(p)
+    except Exception as e:  # report instead of hanging the parent
+        q.put((rank, repr(e), True))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_tp2_two_processes_cuda_ipc(sm):
+    """The multi-process TP path: two processes on one GPU, symmetric buffers exchanged as CUDA
+    IPC handles over torch.distributed (gloo), the fused residual all-reduce and vocabulary-
+    parallel merges running across process boundaries (the kernels time-slice between the two
+    contexts; the exchange flags are polled with a timeout, sm_tp_status).  Tokens = oracle."""
+    import socket
+
+    import torch.multiprocessing as mp
+    seed, n = 1, 16
+    _, ref = _greedy_ref(CFG, seed, n)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_rank, args=(r, 2, port, seed, n, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+    for rank, toks, timed_out in res:
+        assert not timed_out, (rank, toks)
+        assert toks == ref, (rank, toks, ref)

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_kernels.py -x -q -k "attention" > gpurun_out/k1c.log 2>&1; echo "rc=$?" >> gpurun_out/k1c.log
+timeout 600 python tools/k1_splits.py > gpurun_out/k1_splits_c.txt 2>&1
+timeout 60 python tools/tp8_diag.py 256 0 8 0 > gpurun_out/tp8_state.txt 2>&1

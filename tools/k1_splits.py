@@ -1,5 +1,6 @@
-"""K1 split-count probe (GPU box): device time per launch for forced key splits 1/2/4/8 and the
-automatic choice, over representative C5 points and the C2 in-step shape.
+"""K1 variant probe (GPU box): device time per launch, over representative C5 points and the C2
+in-step shape, for the cluster-split kernel (automatic split count "cl") and the stream-K kernel
+with minimum tiles per CTA = live rows / div (div 32, 16, 8, 4).
 
 python tools/k1_splits.py > gpurun_out/k1_splits.txt"""
 import os
@@ -19,7 +20,9 @@ pts = [("A", 32, 32, b, N, Lc) for (b, N, Lc) in
       [("B", 8, 1, b, N, Lc) for (b, N, Lc) in [(1, 64, 4096), (8, 64, 4096), (8, 16, 8192), (32, 64, 4096),
                                                (16, 16, 32768)]]
 hd = 128
-print(f"{'g':2s} {'b':>3s} {'N':>4s} {'Lc':>6s} {'MB':>7s} " + " ".join(f"{'s' + str(s):>7s}" for s in (0, 1, 2, 4, 8)))
+VARS = [("cl", dict(attn_lean=0)), ("l32", dict(attn_lean=1, attn_lean_div=32)), ("l16", dict(attn_lean=1, attn_lean_div=16)),
+        ("l8", dict(attn_lean=1, attn_lean_div=8)), ("l4", dict(attn_lean=1, attn_lean_div=4))]
+print(f"{'g':2s} {'b':>3s} {'N':>4s} {'Lc':>6s} {'MB':>7s} " + " ".join(f"{n:>7s}" for n, _ in VARS))
 for g, H, Hkv, b, N, Lc in pts:
     tree = sm.Tree(synth.SWEEP_TREES[N]) if N != 64 else sm.Tree(synth.V64)
     cap = Lc + tree.N
@@ -32,14 +35,15 @@ for g, H, Hkv, b, N, Lc in pts:
     L = torch.full((b,), Lc, dtype=torch.int32, device="cuda")
     alg = b * Hkv * cap * hd * 4 + 2 * b * tree.N * H * hd * 2
     row = []
-    for s in (0, 1, 2, 4, 8):
-        sm.set_option("attn_splits", s)
-        for i in range(2):
+    for _, opts in VARS:
+        for kk, vv in opts.items():
+            sm.set_option(kk, vv)
+        st = torch.cuda.Stream()
+        for i in range(2):  # on the capture stream: sizes its stage scratch before the capture
             q, k, v, o = sets[i]
-            sm.tree_attention(tree, q, k, v, L, H, Hkv, o)
+            sm.tree_attention(tree, q, k, v, L, H, Hkv, o, stream=st)
         torch.cuda.synchronize()
         gr = torch.cuda.CUDAGraph()
-        st = torch.cuda.Stream()
         with torch.cuda.stream(st):
             gr.capture_begin()
             for i in range(20):
@@ -56,7 +60,7 @@ for g, H, Hkv, b, N, Lc in pts:
         torch.cuda.synchronize()
         row.append(e0.elapsed_time(e1) * 1e3 / 60)
         del gr
-    sm.set_option("attn_splits", 0)
+    sm.reset_options()
     print(f"{g:2s} {b:3d} {tree.N:4d} {Lc:6d} {alg / 1e6:7.1f} " + " ".join(f"{u:7.1f}" for u in row) +
           "   best frac " + f"{alg / min(row) / 1e3 / PEAK:.3f}", flush=True)
     del sets

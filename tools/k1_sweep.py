@@ -64,12 +64,12 @@ for ragged in RAGGED:
                 # ragged: Lc_b spread evenly over [Lc/2, Lc]
                 lens = [Lc // 2 + (Lc - Lc // 2) * i // max(1, b - 1) for i in range(b)] if ragged else [Lc] * b
                 L = torch.tensor(lens, dtype=torch.int32, device="cuda")
-                for i in range(2):
+                st = torch.cuda.Stream()
+                for i in range(2):  # on the capture stream: sizes its stage scratch before the capture
                     q, k, v, o = sets[i]
-                    sm.tree_attention(tree, q, k, v, L, H, Hkv, o)
+                    sm.tree_attention(tree, q, k, v, L, H, Hkv, o, stream=st)
                 torch.cuda.synchronize()
                 g = torch.cuda.CUDAGraph()
-                st = torch.cuda.Stream()
                 with torch.cuda.stream(st):
                     g.capture_begin()
                     for i in range(20):
