@@ -228,7 +228,9 @@ def build_workload(sm, wl: dict, args, rank: int, world: int = 1, tp: int = 1):
         peers = peer_syms(sm, sym, world, rank)
     else:
         W = sm.allocate_weights(cfg, wl["n_medusa"], seed=args.seed + rank)
-    model = sm.Model(cfg, W, max_rows=R, max_batch=b, max_seq_len=x + tree.N, peer_sym=peers)
+    # RoPE table: room for the largest tree any caller binds to this model (run_c4_line's candidates)
+    model = sm.Model(cfg, W, max_rows=R, max_batch=b, max_seq_len=x + max(tree.N, wl.get("max_tree_n", 0)),
+                     peer_sym=peers)
     barrier(world)  # every rank's model exists (its buffer zeroed) before any exchange
     kv = sm.KVCache(model, tree, b, x)
     if b == 1:
@@ -633,6 +635,7 @@ def run_c4_line(sm, args) -> dict:
     import torch
     wl = dict(WORKLOADS["c4"])
     wl["max_rows"] = 640
+    wl["max_tree_n"] = max(len(ch) + 1 for _, ch in c4_candidates())
     a2 = copy.copy(args)
     a2.steps, a2.warmup, a2.prof_steps, a2.e2e_steps = 10, 3, 0, 0
     cfg, tree0, model, kv0, mode, lc_start = build_workload(sm, wl, a2, 0)

@@ -246,3 +246,89 @@ def vanilla_generate(model: Model, prompt, n_new: int, max_seq_len: int | None =
         pos += 1
         nxt = argmax_lowest(z)
     return out, kv
+
+
+class PadSession(Session):
+    """The paper's batched speculative decoding with pads (f4 comparison mode), step by
+    step in the paper's order:
+
+      * "candidate tokens are discarded after token rejection in a cumulative way.  Input IDs for
+        the accepted tokens across batch dimension are padded to a fixed-length sequences to form
+        uniform tensors" -- every sequence's cache advances by the batch's longest acceptance
+        A = max_s (a_eff_s + 1); the slots a sequence did not fill are pads;
+      * "Each batch maps Input IDs to Position IDs in a way to ignore the pad tokens, so that
+        positional embeddings continue from the latest sequence length" -- positions count real
+        tokens only (``pos``), the cache slot index (``Lc``) counts pads too;
+      * "cached tokens are searched for pad tokens and the corresponding locations in the
+        attention mask are set to -inf" -- pad slots are left out of every row's visible keys.
+
+    Ragged prompts are aligned before the first step the same way (the shorter caches padded to
+    the longest).  ``Lc[s]`` is the slot count (uniform after ``align``), ``pos[s]`` the real
+    token count, ``pad[s]`` the set of pad slots."""
+
+    def __init__(self, *a, **k):
+        super().__init__(*a, **k)
+        self.pos = [0] * self.b
+        self.pad = [set() for _ in range(self.b)]
+
+    def prefill(self, seq: int, tokens) -> None:
+        assert not self.pad[seq], "pad mode starts after the prompts (as the C ABI's sm_kv_set_pad_mode)"
+        super().prefill(seq, tokens)
+        self.pos[seq] = self.Lc[seq]
+
+    def align(self) -> None:
+        mx = max(self.Lc)
+        for s in range(self.b):
+            self.pad[s].update(range(self.Lc[s], mx))
+            self.Lc[s] = mx
+
+    def propose(self, seq: int):
+        tr = self.tree
+        tok = [self.root[seq]] + [self.topk_tok[seq][tr.depth[n] - 1][tr.rank[n]] for n in range(1, self.N)]
+        pos = [self.pos[seq] + tr.depth[n] for n in range(self.N)]
+        return tok, pos
+
+    def verify(self, seq: int, tok):
+        """As Session.verify, with positions pos + depth and the pad slots masked out of [0, Lc)."""
+        Lc = self.Lc[seq]
+        if Lc >= self.x:
+            raise KVCapacityError(f"verify at Lc={Lc} >= x={self.x}")
+        tr = self.tree
+        prefix = [j for j in range(Lc) if j not in self.pad[seq]]
+        Z, HF = [None] * self.N, [None] * self.N
+        for n in range(self.N):
+            keys = prefix + [Lc + a for a in T.ancestors(tr, n)] + [Lc + n]
+            Z[n], HF[n] = self.m.forward_row(self.kv, seq, int(tok[n]), self.pos[seq] + tr.depth[n], Lc + n, keys)
+        return Z, HF
+
+    def step_batch(self, mode: str = "greedy", budgets=None, forced=None, **typ):
+        """One batched step: align, then every sequence proposes / verifies / accepts / compacts
+        at the common slot Lc; the caches then advance by A = max_s (a_eff_s + 1) with slots
+        [Lc + a_eff_s + 1, Lc + A) of sequence s marked as pads.  forced[s]: root-to-node path or
+        None (the C ABI's d_forced_path test hook)."""
+        self.align()
+        res = []
+        for s in range(self.b):
+            tok, pos = self.propose(s)
+            Z, HF = self.verify(s, tok)
+            a, chosen, best_leaf, path = self.accept(tok, Z, mode, forced=None if forced is None else forced[s],
+                                                     **typ)
+            Lc = self.Lc[s]
+            a_eff = a
+            if budgets is not None:
+                a_eff = min(a_eff, budgets[s] - 1)
+            a_eff = min(a_eff, self.x - Lc - 1)
+            self.compact(s, path, a_eff)
+            emitted = [int(tok[path[j]]) for j in range(a_eff + 1)]
+            self.committed[s].extend(emitted)
+            last = path[a_eff]
+            self._propose_state(s, Z[last], HF[last])
+            res.append(dict(tok=tok, pos=pos, Z=Z, a=a, a_eff=a_eff, best_leaf=best_leaf, path=path,
+                            emitted=emitted, chosen=chosen))
+        A = max(len(r["emitted"]) for r in res)
+        for s, r in enumerate(res):
+            ne = len(r["emitted"])
+            self.pad[s].update(range(self.Lc[s] + ne, self.Lc[s] + A))
+            self.Lc[s] += A
+            self.pos[s] += ne
+        return res

@@ -91,6 +91,16 @@ SM_DEV void tmem_ld32_f(uint32_t taddr, float *v) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
+SM_DEV void tmem_ld64_f(uint32_t taddr, float *v) {  // 64 consecutive columns, one wait
+  uint32_t r[64];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
+}
 SM_DEV void tmem_st32_f(uint32_t taddr, const float *v) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
@@ -226,6 +236,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
       for (int i = pre; i < first; ++i) issue(i);
       for (int i = STAGES; i < ntiles; ++i) {
         mbar_wait(&kv_empty[i % STAGES], ((i / STAGES) - 1) & 1);
+        if (i == 9) SM_STAMP(22);
         issue(i);
       }
       SM_STAMP(13);
@@ -242,6 +253,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
         const int sb = i & 1, st = i % STAGES;
         // S buffer sb last held S(i-2) / P(i-2): its PV was issued before this MMA (tensor pipe order)
         mbar_wait(&kv_full[st], (i / STAGES) & 1);
+        if (i == 9) SM_STAMP(20);
         tc_fence_after();
         const uint32_t kb = kv_u + st * 2 * TILE;
 #pragma unroll
@@ -256,6 +268,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
       for (int i = 0; i < ntiles; ++i) {
         if (i + 1 < ntiles) issue_s(i + 1);
         mbar_wait(&p_full[i & 1], (i >> 1) & 1);
+        if (i == 8) SM_STAMP(19);
         tc_fence_after();
         const uint32_t vb = kv_u + (i % STAGES) * 2 * TILE + TILE;
 #pragma unroll
@@ -302,6 +315,8 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
       if (threadIdx.x == 0) {
         if (i == 0) SM_STAMP(4);
         if (i == ntiles - 1) SM_STAMP(5);
+        if (i == 8) SM_STAMP(15);
+        if (i == 9) SM_STAMP(21);
       }
       if (!warp_live) {
         tc_fence_before();
@@ -309,8 +324,8 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
         continue;
       }
       float y[64];
-      tmem_ld32_f(lane_base + sb * KEYS, y);
-      tmem_ld32_f(lane_base + sb * KEYS + 32, y + 32);
+      tmem_ld64_f(lane_base + sb * KEYS, y);
+      if (threadIdx.x == 0 && i == 8) SM_STAMP(16);
       const int p0 = key0 + i * KEYS;
       if (a.pad && p0 < Lc) {  // pad batching (f4): masked cache slots of this sequence's prefix
         const uint32_t *pw = a.pad + (size_t)seq * a.pad_words + (p0 >> 5);
@@ -340,13 +355,15 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
 #pragma unroll
         for (int j = 0; j < 64; ++j) y[j] = ((vis >> j) & 1ull) ? y[j] : -INFINITY;
       }
-      float mx0 = y[0], mx1 = y[1];
+      float mx0 = y[0], mx1 = y[1], mx2 = y[2], mx3 = y[3];  // four independent chains
 #pragma unroll
-      for (int j = 2; j < 64; j += 2) {
+      for (int j = 4; j < 64; j += 4) {
         mx0 = fmaxf(mx0, y[j]);
         mx1 = fmaxf(mx1, y[j + 1]);
+        mx2 = fmaxf(mx2, y[j + 2]);
+        mx3 = fmaxf(mx3, y[j + 3]);
       }
-      const float mx = fmaxf(mx0, mx1) * sl2;
+      const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
       // lazy max: raised only when a tile exceeds it by more than 2^8 (exact: l and O share the stale max)
       float m_new = m_run, alpha = 1.f;
       bool resc = false;
@@ -385,9 +402,11 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
           tmem_st32_f(lane_base + 2 * KEYS + c0, o);
         }
       }
+      if (threadIdx.x == 0 && i == 8) SM_STAMP(17);
       tmem_st32_u(lane_base + sb * KEYS, pk);  // P(i) over S(i): columns [sb * 64, sb * 64 + 32)
       tc_fence_before();
       mbar_arrive(&p_full[sb]);
+      if (threadIdx.x == 0 && i == 8) SM_STAMP(18);
     }
     // final O row
     if (ntiles > 0) {
@@ -793,8 +812,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_lean_kernel(const __grid_con
           continue;
         }
         float y[64];
-        tmem_ld32_f(lane_base + sb * KEYS, y);
-        tmem_ld32_f(lane_base + sb * KEYS + 32, y + 32);
+        tmem_ld64_f(lane_base + sb * KEYS, y);
         const int p0 = (sg.t0 + j) * KEYS;
         if (a.pad && p0 < Lc) {  // pad batching (f4): masked cache slots of this sequence's prefix
           const uint32_t *pw = a.pad + (size_t)seq * a.pad_words + (p0 >> 5);

@@ -78,3 +78,67 @@ def test_pad_batching_equals_ragged(sm):
     emitted = [len(t) for t in tp]
     assert lp[-1][0][0] > max(p + e for p, e in zip(plen, emitted)) - 1
     assert lp[-1][0][0] - lp[-1][1].min() >= 3            # pads exist (forced depths 3 / 0 / 1)
+
+
+def test_pad_batching_matches_oracle(sm):
+    """GPU pad mode against the oracle's PadSession (pinned in test_oracle_padbatch.py)
+    on the same seeded inputs: every step the tree tokens, their positions (real tokens only), the
+    cache slot counts, the emitted tokens, and the K/V of every committed (non-pad) slot must
+    agree -- integers bit-exact, floats within the 2e-2 bar -- and the verify logits of steps 2..6
+    within the bar.  Acceptance is imposed through the forced-path hook on both sides (depths 3 / 0
+    / 1, rotating), so the sequences' caches fill with pads at different slots."""
+    from oracle import model as OM
+    from oracle import spec as OS
+    from oracle import tree as OT
+    from lockstep import bar_check
+
+    b, x, seed = 3, 128, 9
+    prompts = [synth.prompt_tokens(seed, i, 20 + 7 * i, CFG["vocab"]) for i in range(b)]
+    W = sm.allocate_weights(CFG, 3, seed=seed)
+    tree = sm.Tree(synth.TINY16, topk=10)
+    model = sm.Model(CFG, W, max_rows=64, max_batch=b, max_seq_len=x + tree.N)
+    kv = sm.KVCache(model, tree, b, x)
+    ps = OS.PadSession(OM.Model(CFG, OM.Weights(CFG, n_medusa=3, seed=seed), "bf16"), synth.TINY16, b, x)
+    for i, p in enumerate(prompts):
+        kv.prefill(i, torch.from_numpy(p).cuda())
+        ps.prefill(i, p)
+    kv.set_pad_mode(True)
+    ot = ps.tree
+    deep = next(n for n in range(ot.N) if ot.depth[n] == 3)
+    d1 = [n for n in range(ot.N) if ot.depth[n] == 1][1]
+    paths = [OT.ancestors(ot, deep) + [deep], [0], [0, d1]]
+    out = sm.AcceptOut(b, tree.depth)
+    L = CFG["n_layers"]
+    for step in range(6):
+        fz = [paths[(s + step) % 3] for s in range(b)]
+        forced = torch.full((b, tree.depth + 1), -1, dtype=torch.int32)
+        for s in range(b):
+            forced[s, : len(fz[s])] = torch.tensor(fz[s], dtype=torch.int32)
+        acfg = sm.accept_cfg(forced_path=forced.cuda())
+        res = ps.step_batch(forced=fz)
+        if step == 0:  # the first step through sm_step: it aligns the ragged prompts
+            kv.step(acfg, out)
+        else:
+            tt = torch.zeros(b, tree.N, dtype=torch.int32, device="cuda")
+            pos = torch.zeros(b, tree.N, dtype=torch.int32, device="cuda")
+            kv.propose(tt, pos)
+            z = torch.zeros(b, tree.N, CFG["vocab"], dtype=torch.float32, device="cuda")
+            kv.verify(tt, z)
+            kv.accept(acfg, out)
+            torch.cuda.synchronize()
+            for s in range(b):
+                assert tt[s].cpu().tolist() == res[s]["tok"], (step, s)
+                assert pos[s].cpu().tolist() == res[s]["pos"], (step, s)
+                bar_check(z[s].cpu().numpy(), np.stack(res[s]["Z"]), 2e-2, f"logits step {step} seq {s}")
+        ne = out.n_emit.cpu().numpy()
+        et = out.emit_tok.cpu().numpy()
+        for s in range(b):
+            assert et[s][: ne[s]].tolist() == res[s]["emitted"], (step, s)
+        assert kv.lengths().tolist() == ps.Lc and kv.positions().tolist() == ps.pos
+    # K/V of every non-pad slot (pad slots hold stale scratch: never read, never compared)
+    mem = kv.layout().float().cpu().numpy()
+    for s in range(b):
+        real = [j for j in range(ps.Lc[s]) if j not in ps.pad[s]]
+        for li in range(L):
+            bar_check(mem[li, 0, s][:, real], ps.kv.K[li][s][:, real, :], 2e-2, f"K layer {li} seq {s}")
+            bar_check(mem[li, 1, s][:, real], ps.kv.V[li][s][:, real, :], 2e-2, f"V layer {li} seq {s}")
