@@ -207,9 +207,10 @@ WORKLOADS = {
 }
 
 
-def build_workload(sm, wl: dict, args, rank: int, world: int = 1, tp: int = 1):
+def build_workload(sm, wl: dict, args, rank: int, world: int = 1, tp: int = 1, pp: int = 1):
     """tp > 1: rank `rank` of a tensor-parallel group of `tp` = world ranks (same
-    seed everywhere: the shards tile one model); else an independent replica."""
+    seed everywhere: the shards tile one model); pp > 1: stage `rank` of the layer-split
+    pipeline (f4); else an independent replica."""
     import torch
     cfg = synth.model_cfg(wl["model"])
     choices = {"V64": synth.V64, "TINY16": synth.TINY16}[wl["tree"]]
@@ -221,8 +222,9 @@ def build_workload(sm, wl: dict, args, rank: int, world: int = 1, tp: int = 1):
     wl["x_run"] = x
     R = max(b * tree.N, 256, wl.get("max_rows", 0))
     peers = None
-    if tp > 1:
-        W = sm.allocate_weights(cfg, wl["n_medusa"], seed=args.seed, tp_rank=rank, tp_size=tp)
+    if tp > 1 or pp > 1:
+        W = sm.allocate_weights(cfg, wl["n_medusa"], seed=args.seed, tp_rank=rank if tp > 1 else 0, tp_size=tp,
+                                pp_rank=rank if pp > 1 else 0, pp_size=pp)
         sym = torch.zeros(sm.tp_sym_bytes(cfg, R, b, wl["n_medusa"]), dtype=torch.uint8, device="cuda")
         W["_sym"] = sym  # keep alive with the weights
         peers = peer_syms(sm, sym, world, rank)
@@ -238,7 +240,7 @@ def build_workload(sm, wl: dict, args, rank: int, world: int = 1, tp: int = 1):
             lc_start = wl["prompt"]
         else:
             lc_start = max(128, min(args.lc_start, x - 5 * total_steps - 8))
-        prompts = [synth.prompt_tokens(args.seed, rank if tp == 1 else 0, lc_start, cfg["vocab"])]
+        prompts = [synth.prompt_tokens(args.seed, rank if max(tp, pp) == 1 else 0, lc_start, cfg["vocab"])]
     else:  # ragged MT-Bench-length prompts (32 + h mod 129)
         prompts = [synth.prompt_tokens(args.seed, i, synth.prompt_length(args.seed, i), cfg["vocab"]) for i in range(b)]
         lc_start = int(np.mean([len(p) for p in prompts]))
@@ -259,8 +261,10 @@ def run_ours(args, world, rank, local) -> dict | None:
         k, v = kv_opt.split("=")
         sm.lib().sm_set_option(k.encode(), int(v))
     wl = WORKLOADS[args.config]
-    tp = world if (wl.get("tp") and world > 1) else 1
-    cfg, tree, model, kv, mode, lc_start = build_workload(sm, wl, args, rank, world, tp)
+    tp = world if (wl.get("tp") and world > 1 and args.parallel == "tp") else 1
+    pp = world if (wl.get("tp") and world > 1 and args.parallel == "pp") else 1
+    cfg, tree, model, kv, mode, lc_start = build_workload(sm, wl, args, rank, world, tp, pp)
+    grp = max(tp, pp)  # ranks that share one model (and emit one token stream)
     N, l, b = tree.N, tree.depth, kv.batch
     out = sm.AcceptOut(b, l)
     acfg = sm.accept_cfg(mode)
@@ -289,7 +293,7 @@ def run_ours(args, world, rank, local) -> dict | None:
         ms = reduce_max(ev0.elapsed_time(ev1), world)
         L1 = kv.lengths().astype(np.int64)
         # replicas: every rank's tokens count; tensor parallel: the group emits one stream
-        tokens = reduce_sum(float((L1 - L0).sum()), world) if tp == 1 else float((L1 - L0).sum())
+        tokens = reduce_sum(float((L1 - L0).sum()), world) if grp == 1 else float((L1 - L0).sum())
         reps.append((tokens / (ms / 1e3), ms, tokens, L0, L1))
     clk = clocks.stop()
     med = sorted(reps, key=lambda r: r[0])[len(reps) // 2]
@@ -347,12 +351,12 @@ def run_ours(args, world, rank, local) -> dict | None:
     e1.record(st)
     torch.cuda.synchronize()
     e_ms = reduce_max(e0.elapsed_time(e1), world)
-    e2e_val = (reduce_sum(e2e_tokens, world) if tp == 1 else e2e_tokens) / (e_ms / 1e3)
+    e2e_val = (reduce_sum(e2e_tokens, world) if grp == 1 else e2e_tokens) / (e_ms / 1e3)
 
     # ---- vanilla greedy decoding on the same kernels and model: a 1-node tree (root
     # only: verify one row, accept the argmax) -- the speculative speed-up's denominator
     van = None
-    if args.vanilla and tp == 1:
+    if args.vanilla and grp == 1:
         vtree = sm.Tree([], topk=synth.TOPK)
         kv_v = sm.KVCache(model, vtree, b, wl["x_run"])
         for i, p in enumerate(kv.prompts):
@@ -387,10 +391,10 @@ def run_ours(args, world, rank, local) -> dict | None:
     pk = peaks()
     gemm_gbs = gemm_bytes / (gemm_ms / 1e3) / 1e9
     lc_mean = float((L0 + L1).mean() / 2)
-    sb = step_bytes(cfg, N, lc_mean, b=b, n_medusa=wl["n_medusa"], tau=tau) / tp  # per GPU
+    sb = step_bytes(cfg, N, lc_mean, b=b, n_medusa=wl["n_medusa"], tau=tau) / grp  # per GPU
     ms_step = ms_max / args.steps
     # the binding roofline of the whole step: max(bytes / HBM, flops / sustained bf16 tensor peak)
-    sf = step_flops(cfg, tree.query()["node_depth"], lc_mean, b=b, n_medusa=wl["n_medusa"]) / tp
+    sf = step_flops(cfg, tree.query()["node_depth"], lc_mean, b=b, n_medusa=wl["n_medusa"]) / grp
     t_hbm, t_tc = sb / pk["hbm"] / 1e6, sf / (pk["bf16_sus"] or pk["bf16"]) / 1e9  # ms
     step_roof = {"bound": "hbm" if t_hbm >= t_tc else "tensor", "alg_bytes": sb, "alg_flops": sf,
                  "roofline_ms": round(max(t_hbm, t_tc), 4), "hbm_ms": round(t_hbm, 4), "tensor_ms": round(t_tc, 4),
@@ -399,13 +403,14 @@ def run_ours(args, world, rank, local) -> dict | None:
     res = {
         "metric": METRIC, "value": round(value, 3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
-        "scaling": "strong" if tp > 1 else "weak",
+        "scaling": "strong" if grp > 1 else "weak",
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic: counter-hash random-init weights (std 0.02), counter-hash prompt tokens",
-        "config": {"workload": wl["desc"], "global_batch": b if tp > 1 else world * b, "seq_len": wl["x_run"],
+        "config": {"workload": wl["desc"], "global_batch": b if grp > 1 else world * b, "seq_len": wl["x_run"],
                    "lc_start": lc_start, "lc_mean": lc_mean,
                    "parallelism": f"tp{tp} (peer-memory exchanges)" if tp > 1 else
-                   (f"replicas x{world}" if world > 1 else "single GPU"),
+                   (f"pp{pp} (layer split, P:252; residual hand-offs over peer memory)" if pp > 1 else
+                    (f"replicas x{world}" if world > 1 else "single GPU")),
                    "l2": f"inputs larger than L2: {sb / 1e9:.1f} GB streamed every step (L2 126 MB)"},
         "tau": round(tau, 4), "steps_per_s": round(args.steps / (ms_max / 1e3), 3),
         "roofline": {"kernel": f"K2 tcgen05 GEMM (all {g_n} weight GEMM launches of one step)", "bound": "hbm",
@@ -642,7 +647,7 @@ def run_c4_line(sm, args) -> dict:
     b, x = kv0.batch, wl["x_run"]
     st = torch.cuda.current_stream()
     acfg = [sm.accept_cfg(mode)]
-    cands, kvs, step_ms = [], [], []
+    cands, kvs, step_ms, meas = [], [], [], []
     for name, ch in c4_candidates():
         t = sm.Tree(ch, topk=synth.TOPK)
         kv = sm.KVCache(model, t, b, x)
@@ -650,10 +655,11 @@ def run_c4_line(sm, args) -> dict:
             kv.prefill(i, torch.from_numpy(p).cuda())
         out = sm.AcceptOut(b, t.depth)
         _time_steps(kv, acfg, out, 3, st)
-        ms, _ = _time_steps(kv, acfg, out, 8, st)
+        ms, tk = _time_steps(kv, acfg, out, 8, st)
         cands.append((name, t))
         kvs.append((kv, out))
         step_ms.append(ms / 8)
+        meas.append((tk / 8 / b, tk / (ms / 1e3)))  # MedusaGenerate: acceptance length, tokens/s
     del kv0
     best, tps = sm.select_tree([t for _, t in cands], step_ms, ALPHA, RHO, batch=b)
     name, tree = cands[best]
@@ -687,6 +693,18 @@ def run_c4_line(sm, args) -> dict:
                          "chosen": name},
            "workload": wl["desc"] + " (TP1: one B200; tree chosen by sm_select_tree)"}
     res["speculative_speedup_measured"] = round(val / res["vanilla"]["value"], 3)
+    # Algorithm 2: every candidate configuration's measured (acceptance length,
+    # speedup over vanilla), best = Max(speedup) -- sm_alg2_select; with random-init heads tau ~ 1,
+    # so the measured choice is the cheapest step, unlike the tau-model choice above
+    v_tps = meas[van][1]
+    idx = [i for i in range(len(cands)) if i != van]  # the tree configurations (vanilla is the reference)
+    sp = [meas[i][1] / v_tps for i in idx]
+    a2 = sm.alg2_select([meas[i][0] for i in idx], sp)
+    res["alg2"] = {"configs": [{"tree": cands[i][0], "acceptance_length": round(meas[i][0], 4),
+                                "speedup": round(sp[j], 4)} for j, i in enumerate(idx)],
+                   "chosen": cands[idx[a2]][0],
+                   "what": "Algorithm 2 over measured MedusaGenerate runs (8 sm_step calls per configuration on this "
+                           "model and batch); speedup = tokens/s over the 1-node (vanilla) configuration's"}
     return res
 
 
@@ -842,6 +860,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--parallel", default="tp", choices=["tp", "pp"],
+                    help="multi-GPU C4: tensor parallel (default) or the paper's layer-split pipeline (f4, P:252)")
     ap.add_argument("--lc-start", type=int, default=1024)
     ap.add_argument("--prof-steps", type=int, default=5)
     ap.add_argument("--reps", type=int, default=3, help="repetitions of the K-step timed region (median)")

@@ -90,6 +90,13 @@ sm_status sm_tree_create_custom(int n_nodes, int n_leaves, int k, int l, sm_tree
 sm_status sm_tree_expected_tau(const sm_tree *t, const float *h_alpha, int n_alpha, float rho, double *tau);
 sm_status sm_select_tree(const sm_tree *const *cands, int n, const double *h_step_ms, const float *h_alpha,
                          int n_alpha, float rho, int batch, int *best, double *h_tokens_per_s);
+/* Algorithm 2 ("SpecMemo for Medusa"): for every pruned tree configuration the
+ * caller runs MedusaGenerate over its queries and records (acceptance_length, speedup); the
+ * result is the configuration with the largest measured speedup ("best_config <- Max(results.
+ * speedup)"), ties to the first in list order (reading Q32).  acceptance_length is recorded by
+ * the algorithm but does not enter the choice.  h_acc_len[n] (nullable), h_speedup[n] finite;
+ * *best = index.  Errors: SM_ERR_INVALID_ARG (n < 1, null, non-finite speedup).             */
+sm_status sm_alg2_select(int n, const double *h_acc_len, const double *h_speedup, int *best);
 /* Query the canonical tables (host outputs, any pointer may be NULL):
  *   N, S (leaves), depth (max depth l), parent[N], node_depth[N], rank[N],
  *   anc_bits[N][4] (bit j of word j/64 = node j is n or an ancestor of n),
@@ -162,8 +169,22 @@ typedef struct {
 #define SM_MAX_TP 8
 typedef struct {
   int tp_rank, tp_size;          /* tp_size in {1, 2, 4, 8}; divides H, Hkv, F/64 and V/4   */
-  void *peer_sym[SM_MAX_TP];     /* [tp_size] device pointers, [tp_rank] = this rank's own   */
+  void *peer_sym[SM_MAX_TP];     /* [tp_size] (or [pp_size]) device pointers, [rank] = own  */
+  int pp_rank, pp_size;          /* layer-split pipeline (f4; pp_size 0 or 1 = off), below  */
 } sm_dist;
+/* Layer-split pipeline (f4 comparison mode, the paper's own distribution: "partitioning its
+ * layers into equal-sized chunks across all available GPUs, with each GPU also hosting the
+ * corresponding slices of the KV cache alongside the layers").  pp_size in 2..8 with
+ * tp_size = 1, bf16, n_layers % pp_size == 0: rank r owns layers [r L/pp, (r+1) L/pp) --
+ * sm_weights' per-layer arrays then hold those L/pp layers only and the KV cache (sm_kv_bytes
+ * with n_layers = L/pp) holds their slices -- plus a full copy of the embedding, final norm, LM
+ * head and Medusa heads.  Every forward (prefill chunk or verify) runs stage by stage: rank 0
+ * embeds the rows, each rank runs its layers and hands the fp32 residual rows [M][d] to the next
+ * rank (published in its symmetric buffer, pulled by the receiver after per-CTA epoch flags, the
+ * protocol above); the last rank's final residual goes to every rank, which then runs the final
+ * norm, the LM head, acceptance, compaction of its own layers' K/V and the heads replicated
+ * (bitwise the same on every rank).  Results equal pp_size = 1 bit for bit: the same kernels run
+ * on the same operands.  peer_sym / zero-fill / call-sequence rules as for tensor parallelism. */
 /* Bytes of one rank's symmetric exchange buffer for cfg (max_rows, max_batch). */
 sm_status sm_tp_sym_bytes(const sm_model_cfg *cfg, size_t *bytes);
 /* *timed_out = 1 if any exchange wait of this model gave up (synchronises).    */

@@ -114,3 +114,23 @@ def optimizer_engine(cfg, b, n, m, p, max_memory, default_heads=DEFAULT_HEADS, a
         if new_heads == num_heads:                                         # QuantizeBaseModel: OUT
             return dict(status=STATUS_NEEDS_QUANT, heads=num_heads, N=0, S=0, kind="none", x=x, total=0)
         num_heads, status = new_heads, STATUS_FEWER_HEADS
+
+
+def algorithm2(results):
+    """Algorithm 2, "SpecMemo for Medusa", in the paper's order:
+
+        results <- {}
+        for config in pruned_tree_configs:
+            MedusaModel(model, config, attention_tree)
+            (acceptance_length, speedup) <- MedusaGenerate(query_count, query_length)
+            results <- (config, acceptance_length, speedup)
+        return best_config <- Max(results.speedup)
+
+    ``results`` is the list of (config, acceptance_length, speedup) the loop produced (the
+    generation runs are the caller's measurement); the maximum is taken over speedup, the first
+    maximal entry in loop order wins a tie (reading Q32: the paper names no tie rule)."""
+    best = None
+    for config, acceptance_length, speedup in results:
+        if best is None or speedup > best[2]:
+            best = (config, acceptance_length, speedup)
+    return best[0]

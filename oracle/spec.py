@@ -301,15 +301,18 @@ class PadSession(Session):
             Z[n], HF[n] = self.m.forward_row(self.kv, seq, int(tok[n]), self.pos[seq] + tr.depth[n], Lc + n, keys)
         return Z, HF
 
-    def step_batch(self, mode: str = "greedy", budgets=None, forced=None, **typ):
+    def step_batch(self, mode: str = "greedy", budgets=None, forced=None, toks=None, **typ):
         """One batched step: align, then every sequence proposes / verifies / accepts / compacts
         at the common slot Lc; the caches then advance by A = max_s (a_eff_s + 1) with slots
         [Lc + a_eff_s + 1, Lc + A) of sequence s marked as pads.  forced[s]: root-to-node path or
-        None (the C ABI's d_forced_path test hook)."""
+        None (the C ABI's d_forced_path test hook); toks[s]: verify these tree tokens instead of
+        the proposed ones (tests: the other implementation's choice among near-tied top-K values)."""
         self.align()
         res = []
         for s in range(self.b):
             tok, pos = self.propose(s)
+            if toks is not None:
+                tok = [int(t) for t in toks[s]]
             Z, HF = self.verify(s, tok)
             a, chosen, best_leaf, path = self.accept(tok, Z, mode, forced=None if forced is None else forced[s],
                                                      **typ)

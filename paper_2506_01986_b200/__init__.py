@@ -80,7 +80,16 @@ MAX_TP = 8
 
 
 class Dist(ctypes.Structure):
-    _fields_ = [("tp_rank", ctypes.c_int), ("tp_size", ctypes.c_int), ("peer_sym", ctypes.c_void_p * MAX_TP)]
+    _fields_ = [("tp_rank", ctypes.c_int), ("tp_size", ctypes.c_int), ("peer_sym", ctypes.c_void_p * MAX_TP),
+                ("pp_rank", ctypes.c_int), ("pp_size", ctypes.c_int)]
+
+
+def pp_layers(n_layers: int, pp_rank: int, pp_size: int) -> range:
+    """Layers of pipeline rank pp_rank: equal-sized chunks (include/specmemo.h)."""
+    if pp_size < 1 or n_layers % pp_size or not 0 <= pp_rank < pp_size:
+        raise ValueError("pp_size must divide n_layers and 0 <= pp_rank < pp_size")
+    per = n_layers // pp_size
+    return range(pp_rank * per, (pp_rank + 1) * per)
 
 
 class AcceptCfg(ctypes.Structure):
@@ -212,6 +221,17 @@ def select_tree(cands: list, step_ms, alpha, rho: float = 1.0, batch: int = 1) -
     return best.value, list(tps)
 
 
+def alg2_select(acc_len, speedup) -> int:
+    """sm_alg2_select: Algorithm 2's choice -- the configuration with the largest
+    measured speedup, ties to the first."""
+    n = len(speedup)
+    a = (ctypes.c_double * n)(*[float(v) for v in acc_len])
+    sp = (ctypes.c_double * n)(*[float(v) for v in speedup])
+    best = ctypes.c_int()
+    _check(lib().sm_alg2_select(n, a, sp, ctypes.byref(best)))
+    return best.value
+
+
 # ------------------------------------------------------------------ tensor-parallel placement (host logic)
 def tp_shard(cfg: dict, rank: int, t: int) -> dict:
     """Which rows / columns of each full weight rank `rank` of `t` holds
@@ -277,11 +297,12 @@ def generate_bf16(t, seed: int, stream_id: int, start: int = 0, mode: int = 0, s
 
 
 def allocate_weights(cfg: dict, n_medusa: int, seed: int = 0, medusa_init: bool = False, device="cuda",
-                     tp_rank: int = 0, tp_size: int = 1) -> dict:
+                     tp_rank: int = 0, tp_size: int = 1, pp_rank: int = 0, pp_size: int = 1) -> dict:
     """Random-init bf16 weights of a Llama + Medusa-1 model, generated on the GPU
     with the same streams as the oracle (synth stream registry).  tp_size > 1:
     the shard of rank tp_rank (tp_shard), generated in place from the full-matrix
-    counter indices, so the shards of all ranks tile the tp_size = 1 weights."""
+    counter indices, so the shards of all ranks tile the tp_size = 1 weights.  pp_size > 1: the
+    layers of pipeline rank pp_rank only (pp_layers), same streams as in the full model."""
     import torch
 
     import synth
@@ -295,10 +316,13 @@ def allocate_weights(cfg: dict, n_medusa: int, seed: int = 0, medusa_init: bool 
         generate_bf16(dst, seed, stream_id, start=r0 * dst.shape[1])
 
     W = {"embed": torch.empty(V, d, dtype=bf, device=device), "lm_head": torch.empty(Vl, d, dtype=bf, device=device),
-         "final_norm": torch.ones(d, dtype=bf, device=device), "layers": [], "medusa": [], "tp": (tp_rank, tp_size)}
+         "final_norm": torch.ones(d, dtype=bf, device=device), "layers": [], "medusa": [], "tp": (tp_rank, tp_size),
+         "pp": (pp_rank, pp_size)}
     generate_bf16(W["embed"], seed, synth.STREAM_EMBED)
     rows(W["lm_head"], synth.STREAM_LM_HEAD, sh["vocab"][0])
-    for li in range(L):
+    if pp_size > 1 and tp_size > 1:
+        raise ValueError("pipeline and tensor parallelism are not combined")
+    for li in pp_layers(L, pp_rank, pp_size):
         wqkv = torch.empty((Hl + 2 * Hkvl) * hd, d, dtype=bf, device=device)
         rows(wqkv[: Hl * hd], synth.stream_layer(li, "wq"), sh["q_rows"][0])
         rows(wqkv[Hl * hd:(Hl + Hkvl) * hd], synth.stream_layer(li, "wk"), sh["k_rows"][0])
@@ -350,7 +374,7 @@ class Model:
                      cfg["d_ffn"], cfg["vocab"], len(weights["medusa"]), cfg.get("rms_eps", 1e-5),
                      cfg.get("rope_theta", 1e4), max_rows, max_batch, max_seq_len, DTYPES[dtype])
         self.dtype = dtype
-        L = cfg["n_layers"]
+        L = len(weights["layers"])  # this rank's layers (all of them unless pipelined)
         arr = lambda key: (ctypes.c_void_p * max(1, L))(*[_ptr(l[key]) for l in weights["layers"]])  # noqa: E731
         marr = lambda key: (ctypes.c_void_p * max(1, len(weights["medusa"])))(  # noqa: E731
             *[_ptr(h[key]) for h in weights["medusa"]])
@@ -362,12 +386,16 @@ class Model:
         self.cfg, self.c = cfg, c
         self.weights = weights          # keep borrowed memory alive
         tp_rank, tp_size = weights.get("tp", (0, 1))
+        pp_rank, pp_size = weights.get("pp", (0, 1))
         self.tp_rank, self.tp_size = tp_rank, tp_size
+        self.pp_rank, self.pp_size = pp_rank, pp_size
         dist = None
-        if tp_size > 1:
-            if peer_sym is None or len(peer_sym) != tp_size:
-                raise ValueError("tensor parallel model needs peer_sym for every rank")
+        if tp_size > 1 or pp_size > 1:
+            nr = max(tp_size, pp_size)
+            if peer_sym is None or len(peer_sym) != nr:
+                raise ValueError("a tensor-parallel or pipelined model needs peer_sym for every rank")
             dist = Dist(tp_rank, tp_size)
+            dist.pp_rank, dist.pp_size = pp_rank, pp_size
             for q, p in enumerate(peer_sym):
                 dist.peer_sym[q] = p
         _check(lib().sm_model_create(ctypes.byref(c), ctypes.byref(w), ctypes.byref(dist) if dist else None,
@@ -454,7 +482,8 @@ class KVCache:
     def __init__(self, model: Model, tree: Tree, batch: int, max_seq_len: int):
         import torch
         self.model, self.tree, self.batch, self.x = model, tree, batch, max_seq_len
-        self.nbytes = kv_bytes(model.cfg, batch, max_seq_len, tree.N, model.tp_size, model.dtype)
+        cfg = dict(model.cfg, n_layers=model.cfg["n_layers"] // model.pp_size)  # this rank's layers
+        self.nbytes = kv_bytes(cfg, batch, max_seq_len, tree.N, model.tp_size, model.dtype)
         self.mem = torch.empty(self.nbytes // 2, dtype=torch.bfloat16, device="cuda")
         self._h = ctypes.c_void_p()
         _check(lib().sm_kv_bind(model._h, tree._h, batch, max_seq_len, ctypes.c_void_p(_ptr(self.mem)),
@@ -466,7 +495,7 @@ class KVCache:
         import torch
         c = self.model.cfg
         mem = self.mem.view(torch.float32) if self.model.dtype == "fp32" else self.mem
-        return mem.view(c["n_layers"], 2, self.batch, c["n_kv_heads"] // self.model.tp_size,
+        return mem.view(c["n_layers"] // self.model.pp_size, 2, self.batch, c["n_kv_heads"] // self.model.tp_size,
                         self.x + self.tree.N, c["head_dim"])
 
     def set_pad_mode(self, on: bool = True) -> None:

@@ -230,6 +230,30 @@ cudaError_t advance_len_launch(int32_t *len, int seq, int n, int32_t *pos_len, c
   return launch_pdl(advance_len_kernel, dim3(1), dim3(1), 0, st, len, seq, n, pos_len);
 }
 
+// ------------------------------------------------------------------ device-to-device copy as a kernel
+// (sm_verify's tree-token and logits copies).  cudaMemcpyAsync D2D goes to a copy engine whose
+// queue other streams share: in the single-GPU multi-rank emulations (TP / pipeline ranks on
+// several streams) a rank's copy queued behind a peer's copy that waits on a spinning exchange
+// kernel stalled the rank until the exchange timed out.  A kernel runs beside the spinner.
+__global__ void d2d_copy_kernel(uint4 *dst, const uint4 *src, size_t n16, uint8_t *dst_b, const uint8_t *src_b,
+                                size_t tail0, size_t nbytes) {
+  pdl_wait();
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) dst[i] = src[i];
+  if (blockIdx.x == 0)
+    for (size_t i = tail0 + threadIdx.x; i < nbytes; i += blockDim.x) dst_b[i] = src_b[i];
+  pdl_trigger_after_writes();
+}
+cudaError_t d2d_copy_launch(void *dst, const void *src, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return cudaSuccess;
+  const bool al = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
+  const size_t n16 = al ? bytes / 16 : 0;
+  const int grid = (int)std::min<size_t>(4 * kNumSMs, std::max<size_t>(1, (n16 + 255) / 256));
+  return launch_pdl(d2d_copy_kernel, dim3(grid), dim3(256), 0, st, static_cast<uint4 *>(dst),
+                    static_cast<const uint4 *>(src), n16, static_cast<uint8_t *>(dst), static_cast<const uint8_t *>(src),
+                    n16 * 16, bytes);
+}
+
 // ------------------------------------------------------------------ pad batching (f4)
 SM_DEV void pad_mark(uint32_t *row, int s0, int s1) {  // slots [s0, s1) -> pad (one thread)
   for (int s = s0; s < s1; ++s) row[s >> 5] |= 1u << (s & 31);
@@ -348,6 +372,7 @@ void decode_preload() {  // force-load (see gemm_preload)
   cudaFuncGetAttributes(&fa, commit_kernel<true>);
   cudaFuncGetAttributes(&fa, advance_len_kernel);
   cudaFuncGetAttributes(&fa, pad_align_kernel);
+  cudaFuncGetAttributes(&fa, d2d_copy_kernel);
   cudaFuncGetAttributes(&fa, pad_commit_kernel);
   cudaFuncGetAttributes(&fa, set_root_kernel);
   cudaFuncGetAttributes(&fa, generate_kernel);

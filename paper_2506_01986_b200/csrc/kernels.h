@@ -370,6 +370,7 @@ constexpr int kLeanMaxSeq = 64;                 // sequences per lean K1 launch
 cudaError_t attention_lean_launch(const AttnArgs &a, cudaStream_t st);
 size_t attention_lean_part_floats(int nunits);
 void attention_set_lean(int on);
+void attention_set_qtmem(int on);
 void attention_set_lean_div(int d);
 int attention_lean_min_tiles(int Nq, int G);
 void attention_set_splits(int n);               // experiments: force key splits (0 = auto)
@@ -430,6 +431,7 @@ cudaError_t propose_launch(TreeDev t, const int32_t *root, const int32_t *topk, 
 // acceptance; the shorter ones' extra slots are pads, masked in attention; positions count tokens.
 // pad_align: len[b] = max len (slots [len_b, max) marked pad); pad_commit: len[b] += max n_emit,
 // pos_len[b] += n_emit[b], slots [len + n_emit_b, len + A) marked pad.
+cudaError_t d2d_copy_launch(void *dst, const void *src, size_t bytes, cudaStream_t st);  // copy as a kernel
 cudaError_t pad_align_launch(int b, int32_t *len, uint32_t *pad, int pad_words, cudaStream_t st);
 cudaError_t pad_commit_launch(int b, int32_t *len, int32_t *pos_len, const int32_t *n_emit, uint32_t *pad,
                               int pad_words, cudaStream_t st);
@@ -491,6 +493,10 @@ cudaError_t tp_merge_logits_launch(int rows, const float *amax, int32_t *argmax,
 cudaError_t tp_merge_topk_launch(int entries, int K, const float *vals, const int32_t *idx_local, int32_t *idx_out,
                                  int nmed, int nb, const TpArgs &tp, cudaStream_t st);
 cudaError_t tp_advance_launch(long long *seq, int n, cudaStream_t st);
+// Layer-split pipeline (f4): hand the fp32 residual rows x[n4 float4] from rank src to the ranks
+// in dst_mask (bit q = rank q).  The sender publishes them in its data slot and raises per-CTA
+// epoch flags in each receiver; a receiver's CTA waits for its flag and pulls its chunk into x.
+cudaError_t pp_xfer_launch(float *x, int n4, int src, unsigned dst_mask, const TpArgs &tp, cudaStream_t st);
 
 // Force-load every kernel of the library (lazy module loading).
 void gemm_preload();

@@ -428,6 +428,17 @@ extern "C" sm_status sm_select_tree(const sm_tree *const *cands, int n, const do
   return SM_OK;
 }
 
+extern "C" sm_status sm_alg2_select(int n, const double *h_acc_len, const double *h_speedup, int *best) {
+  (void)h_acc_len;  // recorded by Algorithm 2, not part of its choice
+  if (n < 1 || !h_speedup || !best) return fail(SM_ERR_INVALID_ARG, "sm_alg2_select: bad arguments");
+  int b = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!std::isfinite(h_speedup[i])) return fail(SM_ERR_INVALID_ARG, "sm_alg2_select: non-finite speedup");
+    if (h_speedup[i] > h_speedup[b]) b = i;  // strict: ties keep the first configuration
+  }
+  *best = b;
+  return SM_OK;
+}
 extern "C" sm_status sm_tree_query(const sm_tree *t, int *N, int *S, int *depth, int32_t *parent, int32_t *node_depth,
                                    int32_t *rank, uint64_t *anc_bits, int32_t *leaf_paths) {
   if (!t) return fail(SM_ERR_INVALID_ARG, "sm_tree_query: null tree");
@@ -489,6 +500,7 @@ struct sm_model {
   cudaStream_t cap_stream = nullptr;
   // tensor parallelism (a7): local dims above are this rank's shard
   int tp = 1, tp_rank = 0, v0 = 0;
+  int pp = 1, pp_rank = 0;       // layer-split pipeline (f4): this rank's layers are [pp_rank L, ..) of pp L
   void *sym[kMaxTP] = {};        // every rank's symmetric buffer, mapped on this device
   size_t sym_slot_floats = 0;
   long long *tp_seq = nullptr;   // device epoch base
@@ -527,10 +539,26 @@ static TpArgs tp_next(sm_model *m) {
   return a;
 }
 static void tp_begin(sm_model *m) { m->tp_point = 0; }
+// Exchange descriptor of pipeline hand-off `point` (absolute index within the current call).
+static TpArgs pp_args(sm_model *m, int point) {
+  TpArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.rank = m->pp_rank;
+  a.t = m->pp;
+  for (int q = 0; q < m->pp; ++q) {
+    char *b = static_cast<char *>(m->sym[q]);
+    a.flags[q] = reinterpret_cast<long long *>(b);
+    a.data[q] = reinterpret_cast<float *>(b + kTpFlagBytes + (size_t)(point & 1) * m->sym_slot_floats * sizeof(float));
+  }
+  a.seq = m->tp_seq;
+  a.point = point;
+  a.err = m->tp_err;
+  return a;
+}
 // Advance the epoch base past this call's exchanges (kept even, so the data slot
 // parity of an exchange is its index parity in every call).
 static sm_status tp_end(sm_model *m, cudaStream_t st, int &nl) {
-  if (m->tp > 1 && m->tp_point > 0) {
+  if ((m->tp > 1 || m->pp > 1) && m->tp_point > 0) {
     CK(tp_advance_launch(m->tp_seq, (m->tp_point + 1) & ~1, st));
     ++nl;
   }
@@ -618,6 +646,13 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
   if (!cfg || !w || !out) return fail(SM_ERR_INVALID_ARG, "sm_model_create: null argument");
   const sm_model_cfg &c = *cfg;
   const int tp = dist ? dist->tp_size : 1, tp_rank = dist ? dist->tp_rank : 0;
+  const int pp = dist ? std::max(1, dist->pp_size) : 1, pp_rank = dist && dist->pp_size > 1 ? dist->pp_rank : 0;
+  if (pp > 1) {  // layer-split pipeline (f4)
+    if (pp > kMaxTP || tp != 1 || pp_rank < 0 || pp_rank >= pp || c.n_layers % pp || c.dtype != SM_DTYPE_BF16)
+      return fail(SM_ERR_INVALID_ARG, "pipeline: pp_size in 2..8 with tp_size 1, bf16, pp_size dividing n_layers");
+    for (int q = 0; q < pp; ++q)
+      if (!dist->peer_sym[q]) return fail(SM_ERR_INVALID_ARG, "sm_dist.peer_sym[q] is null");
+  }
   if (tp != 1 && tp != 2 && tp != 4 && tp != 8) return fail(SM_ERR_INVALID_ARG, "tp_size must be 1, 2, 4 or 8");
   if (tp_rank < 0 || tp_rank >= tp) return fail(SM_ERR_INVALID_ARG, "tp_rank out of range");
   if (tp > 1) {
@@ -654,7 +689,9 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
   m->cfg = c;
   m->tp = tp;
   m->tp_rank = tp_rank;
-  m->L = c.n_layers;
+  m->pp = pp;
+  m->pp_rank = pp_rank;
+  m->L = c.n_layers / pp;  // this rank's layers
   m->d = c.d_model;
   m->H = c.n_heads / tp;  // this rank's shard
   m->Hkv = c.n_kv_heads / tp;
@@ -670,7 +707,7 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
   m->f32 = c.dtype == SM_DTYPE_FP32;
   m->P = m->f32 ? 3 : 1;
   m->hdu = c.head_dim * (m->f32 ? 2 : 1);
-  m->fused = !m->f32 && tp == 1 && c.head_dim == 128 && c.d_model % 128 == 0 && g_fused != 0;
+  m->fused = !m->f32 && tp == 1 && pp == 1 && c.head_dim == 128 && c.d_model % 128 == 0 && g_fused != 0;
   m->fuse_mask = m->fused ? g_fused : 0;
   m->embed = (const bf16 *)w->embed;
   m->final_norm = (const bf16 *)w->final_norm;
@@ -726,11 +763,12 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
   ALLOC(m->tp_err, 1, "tp error flag");
   cudaMemset(m->tp_seq, 0, sizeof(long long));
   cudaMemset(m->tp_err, 0, sizeof(int));
-  if (tp > 1) {
-    for (int q = 0; q < tp; ++q) m->sym[q] = dist->peer_sym[q];
+  if (tp > 1 || pp > 1) {
+    const int nr = std::max(tp, pp), own = tp > 1 ? tp_rank : pp_rank;
+    for (int q = 0; q < nr; ++q) m->sym[q] = dist->peer_sym[q];
     m->sym_slot_floats = tp_slot_floats(c);
     // own buffer: flags start below every epoch (the caller barriers before work)
-    cudaMemset(m->sym[tp_rank], 0, kTpFlagBytes + 2 * m->sym_slot_floats * sizeof(float));
+    cudaMemset(m->sym[own], 0, kTpFlagBytes + 2 * m->sym_slot_floats * sizeof(float));
   }
   cudaMemset(m->x, 0, (size_t)R * d * 4);
   cudaMemset(m->h, 0, (size_t)R * d * 2 * P);
@@ -1116,7 +1154,9 @@ extern "C" sm_status sm_kv_bind(sm_model *m, const sm_tree *tree, int batch, int
   if (tree->topk > 32) return fail(SM_ERR_INVALID_ARG, "topk > 32");
   if (batch * tree->N > m->R) return fail(SM_ERR_INVALID_ARG, "batch * tree nodes exceeds max_rows");
   size_t need;
-  CKS(sm_kv_bytes(&m->cfg, m->tp, batch, max_seq_len, tree->N, &need));
+  sm_model_cfg lc = m->cfg;
+  lc.n_layers = m->L;  // this rank's layers (pipeline)
+  CKS(sm_kv_bytes(&lc, m->tp, batch, max_seq_len, tree->N, &need));
   if (bytes < need) return fail(SM_ERR_KV_CAPACITY, "Cache: KV memory smaller than sm_kv_bytes");
   if (max_seq_len + tree->N > m->cfg.max_seq_len)
     return fail(SM_ERR_INVALID_ARG, "max_seq_len + N exceeds the model's RoPE table (cfg.max_seq_len)");
@@ -1265,8 +1305,18 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
                                  const TreeDev &tree, cudaStream_t st, int &nl) {
   const int M = nseq * Nq;
   const int d = m->d;
-  CK(embed_launch(d_tok, m->embed, m->x, M, d, st));
-  ++nl;
+  // layer-split pipeline (f4): hand-off k (rank k -> k + 1) is exchange point pt0 + k, the last
+  // rank's final residual to every rank is point pt0 + pp - 1
+  const int pt0 = m->tp_point;
+  if (m->pp > 1) m->tp_point += m->pp;
+  const int n4 = M * d / 4;
+  if (m->pp_rank == 0) {
+    CK(embed_launch(d_tok, m->embed, m->x, M, d, st));
+    ++nl;
+  } else {  // the previous stage's residual rows
+    CK(pp_xfer_launch(m->x, n4, m->pp_rank - 1, 1u << m->pp_rank, pp_args(m, pt0 + m->pp_rank - 1), st));
+    ++nl;
+  }
   const int nsplit = attn_splits(m, nseq, Nq);
   const long long layer_rows = (long long)2 * kv->b * m->Hkv * kv->cap;
   const long long half_rows = (long long)kv->b * m->Hkv * kv->cap;
@@ -1393,6 +1443,18 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
   // x += down; hf = bf16(rms(x) * gf)   (R8)
   CKS(resid_norm(m, have_down ? &pv_down : nullptr, m->final_norm, m->hf, M, st, false));
   ++nl;
+  if (m->pp > 1) {
+    const int last = m->pp - 1;
+    if (m->pp_rank < last) {  // to the next stage (hf above is unused), then the final rows back
+      CK(pp_xfer_launch(m->x, n4, m->pp_rank, 1u << (m->pp_rank + 1), pp_args(m, pt0 + m->pp_rank), st));
+      CK(pp_xfer_launch(m->x, n4, last, (1u << last) - 1u, pp_args(m, pt0 + last), st));
+      CKS(resid_norm(m, nullptr, m->final_norm, m->hf, M, st, false));  // same kernel, same x: same hf
+      nl += 3;
+    } else {
+      CK(pp_xfer_launch(m->x, n4, last, (1u << last) - 1u, pp_args(m, pt0 + last), st));
+      ++nl;
+    }
+  }
   return SM_OK;
 }
 
@@ -1588,12 +1650,12 @@ extern "C" sm_status sm_verify(sm_model *m, sm_kv *kv, const int32_t *d_tree_tok
   cudaStream_t st = (cudaStream_t)stream;
   int nl = 0;
   if (d_tree_tok != kv->tree_tok)
-    CK(cudaMemcpyAsync(kv->tree_tok, d_tree_tok, (size_t)kv->b * kv->N * 4, cudaMemcpyDeviceToDevice, st));
+    CK(d2d_copy_launch(kv->tree_tok, d_tree_tok, (size_t)kv->b * kv->N * 4, st));
   tp_begin(m);
   CKS(enqueue_verify(m, kv, kv->tree_tok, st, nl));
   CKS(tp_end(m, st, nl));
   if (d_logits)
-    CK(cudaMemcpyAsync(d_logits, m->z, (size_t)kv->b * kv->N * m->V * 4, cudaMemcpyDeviceToDevice, st));
+    CK(d2d_copy_launch(d_logits, m->z, (size_t)kv->b * kv->N * m->V * 4, st));
   kv->last_stream = st;
   return SM_OK;
 }
@@ -1880,6 +1942,7 @@ extern "C" sm_status sm_reset_options(void) {
   attention_set_l2pf(0);
   attention_set_splits(0);
   attention_set_lean(0);
+  attention_set_qtmem(0);
   attention_set_lean_div(16);
   tp_set_rsag(-1);
   g_fused = 0;
@@ -1934,6 +1997,8 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
     tp_set_rsag(value);
   } else if (n == "attn_lean") {  // tree-mode K1 (hd 128): stream-K kernel (1, default) or cluster splits (0)
     attention_set_lean(value);
+  } else if (n == "attn_qtmem") {  // tree/causal K1 (hd 128): Q in TMEM + 7-stage K/V ring (1) or smem (0, default; measured: 7 stages are no faster)
+    attention_set_qtmem(value);
   } else if (n == "attn_lean_div") {  // lean K1: minimum tiles per CTA = max(2, live rows / value)
     attention_set_lean_div(value);
   } else {

@@ -128,11 +128,44 @@ cudaError_t tp_advance_launch(long long *seq, int n, cudaStream_t st) {
   return launch_pdl(tp_advance_kernel, dim3(1), dim3(32), 0, st, seq, n);
 }
 
+// ------------------------------------------------------------------ layer-split pipeline (f4)
+// One launch per hand-off on every participating rank, same grid everywhere: CTA c moves float4
+// items [c * per, (c + 1) * per).  Flag slot c of the source row in each receiver's flags region.
+constexpr int kPpThreads = 256;
+__global__ void __launch_bounds__(kPpThreads) pp_xfer_kernel(float4 *x, int n4, int per, int src, unsigned dst_mask,
+                                                             TpArgs tp) {
+  pdl_trigger();
+  pdl_wait();
+  const long long ep = 2 * (*tp.seq + tp.point + 1);
+  const int i0 = blockIdx.x * per, i1 = min(n4, i0 + per);
+  if (tp.rank == src) {
+    float4 *slot = reinterpret_cast<float4 *>(tp.data[src]);
+    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) __stcg(slot + i, x[i]);
+    __threadfence_system();
+    __syncthreads();
+    const int q = threadIdx.x;
+    if (q < tp.t && ((dst_mask >> q) & 1u)) st_release_sys(tp.flags[q] + (size_t)src * kTpFlagSlots + blockIdx.x, ep);
+  } else if ((dst_mask >> tp.rank) & 1u) {
+    if (threadIdx.x == 0) tp_wait_flag(tp.flags[tp.rank] + (size_t)src * kTpFlagSlots + blockIdx.x, ep, tp.err);
+    __syncthreads();
+    const float4 *slot = reinterpret_cast<const float4 *>(tp.data[src]);
+    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) x[i] = __ldcv(slot + i);
+  }
+}
+cudaError_t pp_xfer_launch(float *x, int n4, int src, unsigned dst_mask, const TpArgs &tp, cudaStream_t st) {
+  const int per = 4 * kPpThreads;  // 16 KB per CTA
+  const int grid = (n4 + per - 1) / per;
+  if (grid > kTpFlagSlots || grid < 1) return cudaErrorInvalidValue;
+  return launch_pdl(pp_xfer_kernel, dim3(grid), dim3(kPpThreads), 0, st, reinterpret_cast<float4 *>(x), n4, per, src,
+                    dst_mask, tp);
+}
+
 void tp_preload() {  // force-load (see gemm_preload)
   cudaFuncAttributes fa;
   cudaFuncGetAttributes(&fa, tp_merge_logits_kernel);
   cudaFuncGetAttributes(&fa, tp_merge_topk_kernel);
   cudaFuncGetAttributes(&fa, tp_advance_kernel);
+  cudaFuncGetAttributes(&fa, pp_xfer_kernel);
 }
 
 }  // namespace sm

@@ -3,6 +3,12 @@ import sys
 
 import pytest
 
+# The single-GPU tensor-parallel emulation (tests/test_gpu_tp.py) runs t <= 8 ranks on t streams
+# whose exchange kernels spin on each other's flags: every stream needs its own hardware work
+# queue, or a spinning kernel blocks a peer's kernel queued behind it on a shared queue (the
+# default is 8 queues, shared with torch's own streams).  Must be set before CUDA initialises.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

@@ -114,21 +114,32 @@ def test_pad_batching_matches_oracle(sm):
         forced = torch.full((b, tree.depth + 1), -1, dtype=torch.int32)
         for s in range(b):
             forced[s, : len(fz[s])] = torch.tensor(fz[s], dtype=torch.int32)
-        acfg = sm.accept_cfg(forced_path=forced.cuda())
-        res = ps.step_batch(forced=fz)
+        forced_dev = forced.cuda()  # the cfg holds a raw device pointer: keep the tensor alive
+        acfg = sm.accept_cfg(forced_path=forced_dev)
         if step == 0:  # the first step through sm_step: it aligns the ragged prompts
+            res = ps.step_batch(forced=fz)
             kv.step(acfg, out)
         else:
             tt = torch.zeros(b, tree.N, dtype=torch.int32, device="cuda")
             pos = torch.zeros(b, tree.N, dtype=torch.int32, device="cuda")
             kv.propose(tt, pos)
+            torch.cuda.synchronize()
+            g_tok = tt.cpu().numpy()
+            for s in range(b):  # a1: the GPU's tree is the oracle's up to near-tied top-K ranks
+                o_tok, o_pos = ps.propose(s)
+                heads = [ps.m.head_logits(i, ps.last_hf[s]) for i in range(ot.max_depth)]
+                for n in range(1, ot.N):
+                    if g_tok[s][n] != o_tok[n]:
+                        v = heads[ot.depth[n] - 1]
+                        gap = abs(float(v[g_tok[s][n]]) - float(v[o_tok[n]]))
+                        assert gap <= 1e-2 * float(np.abs(v).max()), (step, s, n, gap)
+                assert g_tok[s][0] == o_tok[0] and pos[s].cpu().tolist() == o_pos, (step, s)
+            res = ps.step_batch(forced=fz, toks=g_tok)  # the oracle verifies the GPU's tree
             z = torch.zeros(b, tree.N, CFG["vocab"], dtype=torch.float32, device="cuda")
             kv.verify(tt, z)
             kv.accept(acfg, out)
             torch.cuda.synchronize()
             for s in range(b):
-                assert tt[s].cpu().tolist() == res[s]["tok"], (step, s)
-                assert pos[s].cpu().tolist() == res[s]["pos"], (step, s)
                 bar_check(z[s].cpu().numpy(), np.stack(res[s]["Z"]), 2e-2, f"logits step {step} seq {s}")
         ne = out.n_emit.cpu().numpy()
         et = out.emit_tok.cpu().numpy()

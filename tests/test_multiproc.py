@@ -87,3 +87,43 @@ def test_tp_shard_rejects_bad_sizes():
         tp_shard(synth.model_cfg("llama70b"), 0, 3)
     with pytest.raises(ValueError):
         tp_shard(synth.model_cfg("tiny"), 0, 8)  # F = 256: 8 ranks x 64-row blocks do not fit
+
+
+def _pp_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2506_01986_b200 as sm
+    mine = list(sm.pp_layers(80, rank, world))       # the 70B shape's 80 layers
+    got = [None] * world
+    dist.all_gather_object(got, mine)
+    q.put((rank, got))
+    dist.destroy_process_group()
+
+
+def test_pipeline_layer_partition_gloo():
+    """f4 layer split ("equal-sized chunks"): the ranks' layer ranges, gathered over a
+    world-size-2 gloo group, tile [0, L) in rank order with equal sizes; bad splits are refused."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pp_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for _, got in res:
+        assert sum(got, []) == list(range(80)) and len({len(g) for g in got}) == 1
+    import paper_2506_01986_b200 as sm
+    for L, pp in [(80, 3), (2, 4)]:
+        with pytest.raises(ValueError):
+            sm.pp_layers(L, 0, pp)
+
+
+def test_dist_struct_matches_header():
+    """sm_dist in include/specmemo.h: pp_rank / pp_size follow peer_sym[SM_MAX_TP]."""
+    import ctypes
+
+    import paper_2506_01986_b200 as sm
+    assert sm.Dist.pp_rank.offset == 8 + 8 * sm.MAX_TP and ctypes.sizeof(sm.Dist) == 8 + 8 * sm.MAX_TP + 8

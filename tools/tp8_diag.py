@@ -3,6 +3,8 @@ setting; prints the emitted tokens or the failure.  python tools/tp8_diag.py <vo
 import os
 import sys
 
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # one hardware queue per rank stream
+
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

@@ -4,11 +4,17 @@ python tools/tp_cfg_probe.py t d H Hkv hd F V [pdl]"""
 import os
 import sys
 
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # one hardware queue per rank stream
+
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2506_01986_b200 as sm  # noqa: E402
 import synth  # noqa: E402
+
+for kv_opt in filter(None, os.environ.get("SM_OPT", "").split(",")):  # sm_set_option knobs, e.g. pdl=0
+    k_, v_ = kv_opt.split("=")
+    sm.set_option(k_, int(v_))
 
 t, d, H, Hkv, hd, F, V = (int(x) for x in sys.argv[1:8])
 pdl = int(sys.argv[8]) if len(sys.argv) > 8 else 0
@@ -29,9 +35,14 @@ pt = torch.from_numpy(synth.prompt_tokens(0, 0, 32, V)).cuda()
 
 
 def each(fn):
+    import time
+    dts = []
     for r in range(t):
         with torch.cuda.stream(sts[r]):
+            t0 = time.perf_counter()
             fn(r, sts[r])
+            dts.append(round((time.perf_counter() - t0) * 1e3, 2))
+    print("host ms per rank enqueue", dts, flush=True)
     torch.cuda.synchronize()
 
 
