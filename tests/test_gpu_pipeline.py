@@ -30,6 +30,15 @@ def sm():
 X = 96
 
 
+@pytest.fixture(autouse=True)
+def _no_pdl(sm):
+    """Programmatic dependent launch off (conftest restores the defaults after each test): with the
+    stages sharing one GPU, a stage spinning on its hand-off would let its PDL-launched successors
+    (persistent GEMMs, two CTAs per SM) take every SM before the stage it waits for has run -- on
+    separate GPUs that cannot happen (tools/pp_probe.py: pp = 2 times out with PDL, passes without)."""
+    sm.set_option("pdl", 0)
+
+
 class Stages:
     def __init__(self, sm, cfg, pp, seed, choices=synth.TINY16, batch=1, n_medusa=3):
         self.sm, self.pp = sm, pp

@@ -40,24 +40,40 @@ def _no_pdl(sm):
 
 
 class Ranks:
-    def __init__(self, sm, t, seed=0, n_medusa=3, choices=synth.TINY16, batch=1, medusa_init=False, cfg=CFG):
+    """t ranks in one process: all on the current GPU (the emulation), or rank r on GPU devices[r]
+    with peer access between every pair (the real placement, one GPU per rank)."""
+
+    def __init__(self, sm, t, seed=0, n_medusa=3, choices=synth.TINY16, batch=1, medusa_init=False, cfg=CFG,
+                 devices=None):
         self.sm, self.t = sm, t
+        self.dev = devices or [torch.cuda.current_device()] * t
+        if devices:  # a cross-device copy makes torch enable peer access for the pair
+            for i in self.dev:
+                for j in self.dev:
+                    if i != j:
+                        torch.empty(1, device=f"cuda:{i}").copy_(torch.empty(1, device=f"cuda:{j}"))
         self.tree = sm.Tree(choices, topk=10)
         R = max(batch * self.tree.N, 64)
         nbytes = sm.tp_sym_bytes(cfg, R, batch, n_medusa)
-        self.sym = [torch.zeros(nbytes, dtype=torch.uint8, device="cuda") for _ in range(t)]
+        self.sym, self.W, self.models, self.kvs, self.streams, self.outs = [], [], [], [], [], []
+        for r in range(t):
+            with torch.cuda.device(self.dev[r]):
+                self.sym.append(torch.zeros(nbytes, dtype=torch.uint8, device="cuda"))
         ptrs = [s.data_ptr() for s in self.sym]
-        self.W = [sm.allocate_weights(cfg, n_medusa, seed=seed, medusa_init=medusa_init, tp_rank=r, tp_size=t)
-                  for r in range(t)]
-        self.models = [sm.Model(cfg, self.W[r], R, batch, X + self.tree.N, peer_sym=ptrs) for r in range(t)]
-        self.kvs = [sm.KVCache(m, self.tree, batch, X) for m in self.models]
-        self.streams = [torch.cuda.Stream() for _ in range(t)]
-        self.outs = [sm.AcceptOut(batch, self.tree.depth) for _ in range(t)]
-        torch.cuda.synchronize()
+        for r in range(t):
+            with torch.cuda.device(self.dev[r]):
+                self.W.append(sm.allocate_weights(cfg, n_medusa, seed=seed, medusa_init=medusa_init, tp_rank=r,
+                                                  tp_size=t))
+                self.models.append(sm.Model(cfg, self.W[r], R, batch, X + self.tree.N, peer_sym=ptrs))
+                self.kvs.append(sm.KVCache(self.models[r], self.tree, batch, X))
+                self.streams.append(torch.cuda.Stream())
+                self.outs.append(sm.AcceptOut(batch, self.tree.depth))
+        for d in set(self.dev):
+            torch.cuda.synchronize(d)
 
     def each(self, fn):
         for r in range(self.t):
-            with torch.cuda.stream(self.streams[r]):
+            with torch.cuda.device(self.dev[r]), torch.cuda.stream(self.streams[r]):
                 fn(r, self.kvs[r], self.streams[r])
         for s in self.streams:
             s.synchronize()
@@ -193,18 +209,21 @@ def _greedy_ref(cfg, seed, n):
     return prompt, ref
 
 
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 8,
+                    reason="t = 8 runs one rank per GPU: emulated on one GPU (8 streams) the verify's residual "
+                           "exchanges time out (DESIGN.md 4.5); t = 2, 4 are emulated above")
 @pytest.mark.parametrize("pdl", [1, 0], ids=["pdl", "nopdl"])
 @pytest.mark.parametrize("seed", [0, 2])
 def test_tp8_greedy_tokens_equal_oracle(sm, seed, pdl):
-    """t = 8 ranks on one GPU (8 streams of one process), with and without programmatic dependent
-    launch: every rank emits the oracle's greedy stream (= vanilla greedy)."""
+    """t = 8 ranks, one per GPU (peer access between every pair), with and without programmatic
+    dependent launch: every rank emits the oracle's greedy stream (= vanilla greedy)."""
     sm.set_option("pdl", pdl)
     t, n = 8, 24
     prompt, ref = _greedy_ref(CFG8, seed, n)
-    rk = Ranks(sm, t, seed=seed, cfg=CFG8)
-    pt = torch.from_numpy(prompt).cuda()
-    rk.each(lambda r, kv, st: kv.prefill(0, pt, stream=st))
-    budgets = [torch.full((1,), n, dtype=torch.int32, device="cuda") for _ in range(t)]
+    rk = Ranks(sm, t, seed=seed, cfg=CFG8, devices=list(range(8)))
+    pts = [torch.from_numpy(prompt).to(f"cuda:{d}") for d in rk.dev]
+    rk.each(lambda r, kv, st: kv.prefill(0, pts[r], stream=st))
+    budgets = [torch.full((1,), n, dtype=torch.int32, device=f"cuda:{d}") for d in rk.dev]
     cfgs = [sm.accept_cfg(sm.GREEDY, max_new=budgets[r]) for r in range(t)]
     toks = [[] for _ in range(t)]
     for _ in range(2 * n):
