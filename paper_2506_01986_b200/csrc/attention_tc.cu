@@ -44,15 +44,6 @@ constexpr int OFF_KV = OFF_Q + QB;
 constexpr int OFF_BAR = OFF_KV + STAGES * 2 * TILE;
 constexpr int SMEM = OFF_BAR + 256 + 1024;    // + barriers + alignment slack
 static_assert(SMEM <= 232448, "K1 shared memory");
-// Q in tensor memory (QT variant): the S MMA takes its A operand from TMEM columns [256, 320)
-// (written by the softmax threads with tcgen05.st, one lane per query row), so the 32 KB Q buffer
-// becomes a seventh K/V stage: 224 KB of K/V in flight per SM.  The ring's depth is what bounds
-// the kernel -- the per-stage cycle is the loaded HBM latency (~3 us) plus the stage's hold time
-// (S, softmax, PV), both measured with the SM_TRACE stamps (profiles/r02/k1_trace.txt).
-constexpr int QT_STAGES = 7;
-constexpr int QT_OFF_BAR = QT_STAGES * 2 * TILE;
-constexpr int QT_SMEM = QT_OFF_BAR + 256 + 1024;
-static_assert(QT_SMEM <= 232448, "K1 shared memory (Q in TMEM)");
 constexpr float RESCALE_LOG2 = 8.0f;          // lazy-rescale threshold (log2 units)
 }  // namespace tc
 
@@ -142,18 +133,16 @@ SM_DEV void tmem_st32_u(uint32_t taddr, const uint32_t *v) {
 // the o_proj GEMM gains ~0.8 us per layer, attention loses ~2.3 us (its K/V reads compete) -> off.
 __device__ int g_attn_l2pf = 0;
 // CAUSAL: prefill chunk (AttnArgs::causal), compiled separately so the tree kernel keeps its code
-template <bool CAUSAL, bool QT>
+template <bool CAUSAL>
 __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_constant__ AttnArgs a) {
   using namespace tc;
-  constexpr int NST = QT ? QT_STAGES : STAGES;  // K/V ring depth
-  constexpr int TCOLS = QT ? 512 : 256;         // TMEM columns (QT: + Q at [256, 320))
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t *sQ = smem + OFF_Q;  // (unused with QT)
-  uint8_t *sKV = smem + (QT ? 0 : OFF_KV);
-  uint64_t *kv_full = reinterpret_cast<uint64_t *>(smem + (QT ? QT_OFF_BAR : OFF_BAR));
-  uint64_t *kv_empty = kv_full + NST;
-  uint64_t *s_full = kv_empty + NST;     // [2]
+  uint8_t *sQ = smem + OFF_Q;
+  uint8_t *sKV = smem + OFF_KV;
+  uint64_t *kv_full = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
+  uint64_t *kv_empty = kv_full + STAGES;
+  uint64_t *s_full = kv_empty + STAGES;  // [2]
   uint64_t *s_free = s_full + 2;         // [2] (unused: S(i+2) is issued after PV(i), in order)
   uint64_t *p_full = s_free + 2;         // [2] P(i) written over S buffer i & 1
   uint64_t *o_done = p_full + 2;         // [2] PV(i) commits to o_done[i & 1]
@@ -179,8 +168,8 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
 
   const long long kbase_row = a.k_row0 + (long long)seq * a.seq_rows + (long long)h * a.cap;
   const long long vbase_row = a.v_row0 + (long long)seq * a.seq_rows + (long long)h * a.cap;
-  auto issue = [&](int i) {  // TMA: K and V of key tile i -> ring stage i % NST
-    const int s = i % NST;
+  auto issue = [&](int i) {  // TMA: K and V of key tile i -> ring stage i % STAGES
+    const int s = i % STAGES;
     uint8_t *kb = sKV + s * 2 * TILE;
     uint8_t *vb = kb + TILE;
     const int p = key0 + i * KEYS;
@@ -191,12 +180,12 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
       tma_load_2d(vb + hf * 8192, &a.tmV, &kv_full[s], hf * 64, (int)(vbase_row + p));
     }
   };
-  const int first = min(NST, ntiles);
+  const int first = min(STAGES, ntiles);
   int pre = 0;
   if (threadIdx.x == 128) {  // producer thread: barriers, then the prefix tiles (independent of this step)
     tma_prefetch_desc(&a.tmK);
     tma_prefetch_desc(&a.tmV);
-    for (int s = 0; s < NST; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
@@ -232,7 +221,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
     }
   }
   static_assert(kAncWords == 4, "ancestor words are kept in 4 registers");
-  if (warp == 5) tmem_alloc<TCOLS>(tslot);
+  if (warp == 5) tmem_alloc<256>(tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -245,8 +234,8 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
       pdl_wait();
       SM_STAMP(12);
       for (int i = pre; i < first; ++i) issue(i);
-      for (int i = NST; i < ntiles; ++i) {
-        mbar_wait(&kv_empty[i % NST], ((i / NST) - 1) & 1);
+      for (int i = STAGES; i < ntiles; ++i) {
+        mbar_wait(&kv_empty[i % STAGES], ((i / STAGES) - 1) & 1);
         if (i == 9) SM_STAMP(22);
         issue(i);
       }
@@ -261,21 +250,17 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
       mbar_wait(q_full, 0);
       SM_STAMP(14);
       auto issue_s = [&](int i) {
-        const int sb = i & 1, st = i % NST;
+        const int sb = i & 1, st = i % STAGES;
         // S buffer sb last held S(i-2) / P(i-2): its PV was issued before this MMA (tensor pipe order)
-        mbar_wait(&kv_full[st], (i / NST) & 1);
+        mbar_wait(&kv_full[st], (i / STAGES) & 1);
         if (i == 9) SM_STAMP(20);
         tc_fence_after();
         const uint32_t kb = kv_u + st * 2 * TILE;
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k) {  // hd in 16-element steps; halves of 64 are separate 8/16 KB blocks
+          const uint64_t ad = umma_desc_sw128(q_u + (k >> 2) * 16384 + (k & 3) * 32);
           const uint64_t bd = umma_desc_sw128(kb + (k >> 2) * 8192 + (k & 3) * 32);
-          if (QT) {  // Q from TMEM: 8 columns (16 bf16) per step
-            umma_bf16_ts(tmem + sb * KEYS, tmem + 256 + k * 8, bd, idesc_s, k > 0);
-          } else {
-            const uint64_t ad = umma_desc_sw128(q_u + (k >> 2) * 16384 + (k & 3) * 32);
-            umma_bf16(tmem + sb * KEYS, ad, bd, idesc_s, k > 0);
-          }
+          umma_bf16(tmem + sb * KEYS, ad, bd, idesc_s, k > 0);
         }
         umma_commit(&s_full[sb]);
       };
@@ -285,13 +270,13 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
         mbar_wait(&p_full[i & 1], (i >> 1) & 1);
         if (i == 8) SM_STAMP(19);
         tc_fence_after();
-        const uint32_t vb = kv_u + (i % NST) * 2 * TILE + TILE;
+        const uint32_t vb = kv_u + (i % STAGES) * 2 * TILE + TILE;
 #pragma unroll
         for (int k = 0; k < KEYS / 16; ++k) {  // keys in 16-row steps: 8 TMEM columns of bf16 pairs
           const uint64_t bd = umma_desc_mn_sw128(vb + k * 2048, 8192);
           umma_bf16_ts(tmem + 2 * KEYS, tmem + (i & 1) * KEYS + k * 8, bd, idesc_o, (i > 0 || k > 0) ? 1u : 0u);
         }
-        umma_commit(&kv_empty[i % NST]);
+        umma_commit(&kv_empty[i % STAGES]);
         umma_commit(&o_done[i & 1]);
       }
     }
@@ -313,17 +298,10 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
       uint4 v[16];
 #pragma unroll
       for (int c = 0; c < 16; ++c) v[c] = live ? __ldg(src + c) : make_uint4(0, 0, 0, 0);  // all loads in flight
-      if (QT) {  // this row's 64 packed bf16 pairs into its TMEM lane, columns [256, 320)
-        tmem_st32_u(lane_base + 256, reinterpret_cast<const uint32_t *>(v));
-        tmem_st32_u(lane_base + 256 + 32, reinterpret_cast<const uint32_t *>(v) + 32);
-        tc_fence_before();
-      } else {
-        const uint32_t q_u = smem_u32(sQ);
+      const uint32_t q_u = smem_u32(sQ);
 #pragma unroll
-        for (int c = 0; c < 16; ++c)
-          st_shared_v4(q_u + (c >> 3) * 16384 + sw128_off(r, c), v[c].x, v[c].y, v[c].z, v[c].w);
-        fence_proxy_async();
-      }
+      for (int c = 0; c < 16; ++c) st_shared_v4(q_u + (c >> 3) * 16384 + sw128_off(r, c), v[c].x, v[c].y, v[c].z, v[c].w);
+      fence_proxy_async();
       mbar_arrive(q_full);
     }
     if (threadIdx.x == 0) SM_STAMP(3);
@@ -562,7 +540,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 5) tmem_dealloc<TCOLS>(tmem);
+  if (warp == 5) tmem_dealloc<256>(tmem);
   if (threadIdx.x == 0) SM_GT_END(5);
 }
 
@@ -1108,24 +1086,20 @@ int attention_tc_nsplit(int units) {  // 1 CTA per SM: aim for ~one wave of 148
   return ns;
 }
 
-static int g_attn_qtmem = 0;  // sm_set_option("attn_qtmem"): Q in TMEM + 7-stage ring (1) or Q in smem (0, default)
-void attention_set_qtmem(int on) { g_attn_qtmem = on; }
-
 cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    const auto A = cudaFuncAttributeMaxDynamicSharedMemorySize;
-    cudaError_t e = cudaFuncSetAttribute(tree_attn_tc_kernel<false, false>, A, tc::SMEM);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(tree_attn_tc_kernel<true, false>, A, tc::SMEM);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(tree_attn_tc_kernel<false, true>, A, tc::QT_SMEM);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(tree_attn_tc_kernel<true, true>, A, tc::QT_SMEM);
+    cudaError_t e = cudaFuncSetAttribute(tree_attn_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         tc::SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(tree_attn_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(a.nsplit, (a.Nq * a.G + tc::ROWS - 1) / tc::ROWS, a.nseq * a.Hkv);
   cfg.blockDim = dim3(192);
-  cfg.dynamicSmemBytes = g_attn_qtmem ? tc::QT_SMEM : tc::SMEM;
+  cfg.dynamicSmemBytes = tc::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1136,12 +1110,8 @@ cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
   attrs[1].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = a.nsplit > 1 ? 2 : 1;
-  if (g_attn_qtmem) {
-    if (a.causal) return cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<true, true>, a);
-    return cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<false, true>, a);
-  }
-  if (a.causal) return cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<true, false>, a);
-  return cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<false, false>, a);
+  if (a.causal) return cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<true>, a);
+  return cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<false>, a);
 }
 
 void attention_set_l2pf(int on) { cudaMemcpyToSymbol(g_attn_l2pf, &on, sizeof(int)); }
@@ -1149,10 +1119,8 @@ void attention_set_l2pf(int on) { cudaMemcpyToSymbol(g_attn_l2pf, &on, sizeof(in
 void attention_tc_preload() {  // force-load (see gemm_preload)
   cudaFuncAttributes fa;
   cudaFuncGetAttributes(&fa, tree_attn_lean_kernel);
-  cudaFuncGetAttributes(&fa, tree_attn_tc_kernel<false, false>);
-  cudaFuncGetAttributes(&fa, tree_attn_tc_kernel<true, false>);
-  cudaFuncGetAttributes(&fa, tree_attn_tc_kernel<false, true>);
-  cudaFuncGetAttributes(&fa, tree_attn_tc_kernel<true, true>);
+  cudaFuncGetAttributes(&fa, tree_attn_tc_kernel<false>);
+  cudaFuncGetAttributes(&fa, tree_attn_tc_kernel<true>);
 }
 
 }  // namespace sm

@@ -12,8 +12,17 @@
 #include <tuple>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing unless a profiler attaches
+
 #include "../../include/specmemo.h"
 #include "kernels.h"
+
+namespace {
+struct NvtxRange {  // host-side range around each public entry point (nsys / ncu --nvtx timelines)
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 using namespace sm;
 
@@ -1482,6 +1491,7 @@ static sm_status enqueue_heads(sm_model *m, sm_kv *kv, int row0, int nb, cudaStr
 }
 
 extern "C" sm_status sm_prefill(sm_model *m, sm_kv *kv, int seq, const int32_t *d_tokens, int n, void *stream) {
+  NvtxRange nvtx_("sm_prefill");
   if (!m || !kv || seq < 0 || seq >= kv->b || (n > 0 && !d_tokens) || n < 0)
     return fail(SM_ERR_INVALID_ARG, "sm_prefill: bad arguments");
   if (n == 0) return SM_OK;
@@ -1638,6 +1648,7 @@ extern "C" sm_status sm_kv_status(sm_kv *kv, int *h_status) {
 }
 
 extern "C" sm_status sm_propose(sm_model *m, sm_kv *kv, int32_t *d_tree_tok, int32_t *d_pos, void *stream) {
+  NvtxRange nvtx_("sm_propose");
   if (!m || !kv || !d_tree_tok) return fail(SM_ERR_INVALID_ARG, "sm_propose: bad arguments");
   int nl = 0;
   CKS(enqueue_propose(m, kv, d_tree_tok, d_pos, (cudaStream_t)stream, nl));
@@ -1645,6 +1656,7 @@ extern "C" sm_status sm_propose(sm_model *m, sm_kv *kv, int32_t *d_tree_tok, int
 }
 
 extern "C" sm_status sm_verify(sm_model *m, sm_kv *kv, const int32_t *d_tree_tok, float *d_logits, void *stream) {
+  NvtxRange nvtx_("sm_verify");
   if (!m || !kv || !d_tree_tok) return fail(SM_ERR_INVALID_ARG, "sm_verify: bad arguments");
   CKS(kv_surface(kv));
   cudaStream_t st = (cudaStream_t)stream;
@@ -1662,6 +1674,7 @@ extern "C" sm_status sm_verify(sm_model *m, sm_kv *kv, const int32_t *d_tree_tok
 
 extern "C" sm_status sm_accept(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, const sm_accept_out *out,
                                void *stream) {
+  NvtxRange nvtx_("sm_accept");
   if (!m || !kv) return fail(SM_ERR_INVALID_ARG, "sm_accept: bad arguments");
   CKS(check_accept(cfg, out));
   CKS(kv_surface(kv));
@@ -1689,6 +1702,7 @@ static sm_status enqueue_step(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, 
 
 extern "C" sm_status sm_step(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, const sm_accept_out *out,
                              void *stream) {
+  NvtxRange nvtx_("sm_step");
   if (!m || !kv) return fail(SM_ERR_INVALID_ARG, "sm_step: bad arguments");
   CKS(check_accept(cfg, out));
   CKS(kv_surface(kv));
@@ -1942,7 +1956,6 @@ extern "C" sm_status sm_reset_options(void) {
   attention_set_l2pf(0);
   attention_set_splits(0);
   attention_set_lean(0);
-  attention_set_qtmem(0);
   attention_set_lean_div(16);
   tp_set_rsag(-1);
   g_fused = 0;
@@ -1997,8 +2010,6 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
     tp_set_rsag(value);
   } else if (n == "attn_lean") {  // tree-mode K1 (hd 128): stream-K kernel (1, default) or cluster splits (0)
     attention_set_lean(value);
-  } else if (n == "attn_qtmem") {  // tree/causal K1 (hd 128): Q in TMEM + 7-stage K/V ring (1) or smem (0, default; measured: 7 stages are no faster)
-    attention_set_qtmem(value);
   } else if (n == "attn_lean_div") {  // lean K1: minimum tiles per CTA = max(2, live rows / value)
     attention_set_lean_div(value);
   } else {

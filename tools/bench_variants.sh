@@ -3,7 +3,7 @@
 VARS=${@:-"pdl=1"}
 for v in $VARS; do
   echo "== $v"
-  SM_OPT=$v timeout 300 python bench.py --no-cpu-baseline --no-k1 --steps 50 --warmup 5 --e2e-steps 10 --prof-steps 2 2>&1 | python3 -c "
+  SM_OPT=$v timeout 300 python bench.py --no-extra --no-cpu-baseline --no-k1 --steps 50 --warmup 5 --e2e-steps 10 --prof-steps 2 2>&1 | python3 -c "
 import json,sys
 for l in sys.stdin:
     if l.startswith('{'):

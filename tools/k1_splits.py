@@ -20,11 +20,7 @@ pts = [("A", 32, 32, b, N, Lc) for (b, N, Lc) in
       [("B", 8, 1, b, N, Lc) for (b, N, Lc) in [(1, 64, 4096), (8, 64, 4096), (8, 16, 8192), (32, 64, 4096),
                                                (16, 16, 32768)]]
 hd = 128
-if os.environ.get("K1_VARS") == "qt":  # Q staged in TMEM (7-stage ring) vs shared memory (6 stages)
-    VARS = [("qsmem", dict(attn_lean=0, attn_qtmem=0)), ("qtmem", dict(attn_lean=0, attn_qtmem=1))]
-else:
-    VARS = None
-VARS = VARS or [("cl", dict(attn_lean=0)), ("l32", dict(attn_lean=1, attn_lean_div=32)), ("l16", dict(attn_lean=1, attn_lean_div=16)),
+VARS = [("cl", dict(attn_lean=0)), ("l32", dict(attn_lean=1, attn_lean_div=32)), ("l16", dict(attn_lean=1, attn_lean_div=16)),
         ("l8", dict(attn_lean=1, attn_lean_div=8)), ("l4", dict(attn_lean=1, attn_lean_div=4))]
 print(f"{'g':2s} {'b':>3s} {'N':>4s} {'Lc':>6s} {'MB':>7s} " + " ".join(f"{n:>7s}" for n, _ in VARS))
 for g, H, Hkv, b, N, Lc in pts:
