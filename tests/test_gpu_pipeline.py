@@ -127,3 +127,34 @@ def test_pipeline_rejects_bad_splits(sm):
     cfg = synth.model_cfg("tiny", n_layers=3)
     with pytest.raises(ValueError):
         sm.allocate_weights(cfg, 3, pp_rank=0, pp_size=2)
+
+
+def test_pipeline_c2_width_bitwise(sm):
+    """pp = 2 at the C2 width (d 4096, 32 heads, hd 128, F 11008, V 32000; 2 layers, one per stage,
+    V64 tree): the tcgen05 GEMMs, the tcgen05 K1 and the 4096-wide residual hand-offs; every stage's
+    logits, tree tokens and K/V equal pp = 1 bit for bit."""
+    cfg = synth.model_cfg("vicuna7b", n_layers=2)
+    seed, n = 3, 6
+    prompts = [synth.prompt_tokens(seed, 0, 40, cfg["vocab"])]
+
+    def run(pp):
+        st = Stages(sm, cfg, pp, seed, choices=synth.V64, n_medusa=4)
+        pt = torch.from_numpy(prompts[0]).cuda()
+        st.each(lambda r, kv, s: kv.prefill(0, pt, stream=s))
+        cfgs = [sm.accept_cfg(sm.GREEDY) for _ in range(pp)]
+        for _ in range(n):
+            st.each(lambda r, kv, s: kv.step(cfgs[r], st.outs[r], stream=s))
+        tts = [torch.zeros(1, st.tree.N, dtype=torch.int32, device="cuda") for _ in range(pp)]
+        zs = [torch.zeros(1, st.tree.N, cfg["vocab"], dtype=torch.float32, device="cuda") for _ in range(pp)]
+        st.each(lambda r, kv, s: kv.propose(tts[r], stream=s))
+        st.each(lambda r, kv, s: kv.verify(tts[r], zs[r], stream=s))
+        assert not st.timed_out()
+        return st, tts, zs
+
+    one, tt1, z1 = run(1)
+    two, tt2, z2 = run(2)
+    kv1 = one.kvs[0].layout()
+    for r in range(2):
+        assert torch.equal(tt2[r], tt1[0]) and torch.equal(z2[r], z1[0])
+        assert np.array_equal(two.kvs[r].lengths(), one.kvs[0].lengths())
+        assert torch.equal(two.kvs[r].layout(), kv1[r:r + 1])
