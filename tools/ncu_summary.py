@@ -10,7 +10,9 @@ DETAILS = ["Duration", "Elapsed Cycles", "SM Frequency", "DRAM Throughput", "Mem
            "Compute (SM) Throughput", "Achieved Occupancy", "Registers Per Thread", "Dynamic Shared Memory Per Block",
            "Grid Size", "Block Size", "Cluster Size"]
 RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active",
-       "sm__inst_executed_pipe_tc.sum", "smsp__inst_executed.sum", "lts__t_sector_hit_rate.pct"]
+       "sm__inst_executed_pipe_tc.sum", "smsp__inst_executed.sum", "lts__t_sector_hit_rate.pct",
+       "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+       "sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg", "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"]
 
 
 def page(rep, name):
@@ -35,9 +37,10 @@ for j, r in enumerate(raw[2:]):
     d = by.get(r[rh.index("ID")]) if "ID" in rh else None
     if d is None:
         continue
-    for m in RAW:
-        if m in rh:
-            d[m] = r[rh.index(m)]
+    for m in RAW:  # some raw names carry a section prefix ("TPC.TriageCompute.<metric>")
+        col = next((c for c, name in enumerate(rh) if name == m or name.endswith("." + m)), None)
+        if col is not None:
+            d[m] = r[col]
 print(f"ncu --set full capture: {rep}")
 for lid, d in by.items():
     print(f"\n[{lid}] {d['name'][:100]}")
