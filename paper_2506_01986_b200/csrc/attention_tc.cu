@@ -544,6 +544,443 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
   if (threadIdx.x == 0) SM_GT_END(5);
 }
 
+// ============================================================================ K1, key-split row packing (KS)
+// For N G <= 64 live query rows (the C2 in-step shape: 64 nodes x 1 head per kv head; N 16-32 with
+// G <= 2) half or more of the tree kernel's 128 MMA rows are padding, and the softmax of the live
+// rows runs on two (or one) of the four SM sub-partitions (TMEM lane quadrant = sub-partition).
+// Here the live rows are replicated F = 128 / RP times (RP = 64 or 32 rows per copy) and the key
+// tile is 128 keys: copy f of row r (MMA row f RP + r) owns keys [f 128/F, (f+1) 128/F) of every
+// tile -- its P is zero at the other keys -- so all four sub-partitions share the softmax of a
+// 128-key tile and each thread handles 128/F keys of it.  Tensor work per key is unchanged (S:
+// M 128 x N 128 x K 128, PV: M 128 x N 128 x K 128 per 128 keys = the tree kernel's per-64-key
+// work twice).  Each copy keeps its own (m, l, O); the F partials of a row are merged in the CTA
+// (fixed copy order) and the result enters the split-KV cluster combine as in tree_attn_tc_kernel.
+namespace ks {
+constexpr int HD = 128, ROWS = 128, KEYS = 128;
+constexpr int HALF = KEYS * 64 * 2;        // 16 KB: one hd-half (64 columns) of a 128-key K or V tile
+constexpr int TILE = 2 * HALF;             // 32 KB: a 128-key K (or V) tile
+constexpr int STAGES = 3;                  // 3 x (K + V) = 192 KB
+constexpr int QB = ROWS * HD * 2;          // 32 KB
+constexpr int OFF_Q = 0;
+constexpr int OFF_KV = OFF_Q + QB;
+constexpr int OFF_BAR = OFF_KV + STAGES * 2 * TILE;
+constexpr int SMEM = OFF_BAR + 256 + 1024;
+static_assert(SMEM <= 232448, "K1 (KS) shared memory");
+// end-of-kernel staging in the idle ring: merged rows for the cluster combine at offset 0 (the tree
+// kernel's layout: so [128][HD] fp32 + sml [128][2] + swt), the copies' partials above 80 KB
+constexpr int OFF_PART = 80 * 1024;        // [ROWS][HD] fp32 (copy f of row r at f RP + r) + [ROWS] (m, l)
+}  // namespace ks
+
+template <int F>
+__global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_constant__ AttnArgs a) {
+  constexpr int HD = ks::HD, ROWS = ks::ROWS, KEYS = ks::KEYS, STAGES = ks::STAGES;
+  constexpr int RP = ROWS / F;      // rows per copy
+  constexpr int KT = KEYS / F;      // keys per thread per tile
+  static_assert(F == 1 || F == 2 || F == 4, "copies");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sQ = smem + ks::OFF_Q;
+  uint8_t *sKV = smem + ks::OFF_KV;
+  uint64_t *kv_full = reinterpret_cast<uint64_t *>(smem + ks::OFF_BAR);
+  uint64_t *kv_empty = kv_full + STAGES;
+  uint64_t *s_full = kv_empty + STAGES;  // [2]
+  uint64_t *p_full = s_full + 2;         // [2]
+  uint64_t *o_done = p_full + 2;         // [2]
+  uint64_t *q_full = o_done + 2;
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(q_full + 1);
+
+  pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int split = blockIdx.x;  // one row block (R <= RP)
+  const int sl = blockIdx.z / a.Hkv, h = blockIdx.z % a.Hkv;
+  const int seq = a.seq_base + sl;
+  const int Lc = a.len[seq];  // changed only by the step's last kernels: safe before the wait
+  const int R = a.Nq * a.G;
+  const int T = Lc + a.Nq;
+  const int chunk = ((T + a.nsplit - 1) / a.nsplit + KEYS - 1) / KEYS * KEYS;
+  const int key0 = min(T, split * chunk);
+  const int key1 = min(T, key0 + chunk);
+  const int ntiles = (key1 - key0 + KEYS - 1) / KEYS;
+  const float sl2 = a.scale_log2;
+
+  const long long kbase_row = a.k_row0 + (long long)seq * a.seq_rows + (long long)h * a.cap;
+  const long long vbase_row = a.v_row0 + (long long)seq * a.seq_rows + (long long)h * a.cap;
+  auto issue = [&](int i) {  // K and V of keys [p, p + 128) -> stage i % STAGES, [hd half][128 keys][64]
+    const int s = i % STAGES;
+    uint8_t *kb = sKV + s * 2 * ks::TILE;
+    uint8_t *vb = kb + ks::TILE;
+    const int p = key0 + i * KEYS;
+    mbar_arrive_expect_tx(&kv_full[s], 2 * ks::TILE);
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+#pragma unroll
+      for (int kh = 0; kh < 2; ++kh) {  // two 64-key boxes per hd half, consecutive rows
+        tma_load_2d(kb + hf * ks::HALF + kh * 8192, &a.tmK, &kv_full[s], hf * 64, (int)(kbase_row + p + kh * 64));
+        tma_load_2d(vb + hf * ks::HALF + kh * 8192, &a.tmV, &kv_full[s], hf * 64, (int)(vbase_row + p + kh * 64));
+      }
+    }
+  };
+  const int first = min(STAGES, ntiles);
+  int pre = 0;
+  if (threadIdx.x == 128) {
+    tma_prefetch_desc(&a.tmK);
+    tma_prefetch_desc(&a.tmV);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&p_full[b], 128);
+      mbar_init(&o_done[b], 1);
+    }
+    mbar_init(q_full, 128);
+    fence_barrier_init();
+    while (pre < first && key0 + (pre + 1) * KEYS <= Lc) issue(pre++);
+  }
+  // softmax threads: copy f of query row r; the ancestor words of its node
+  const int rr_lane = (warp < 4) ? warp * 32 + lane : 0;
+  const int cf = rr_lane / RP, qr = rr_lane % RP;  // copy, query row
+  uint64_t anc0 = 0, anc1 = 0, anc2 = 0, anc3 = 0;
+  if (warp < 4 && qr < R) {
+    const uint64_t *w = a.anc + (qr / a.G) * kAncWords;
+    anc0 = w[0];
+    anc1 = w[1];
+    anc2 = w[2];
+    anc3 = w[3];
+  }
+  static_assert(kAncWords == 4, "ancestor words are kept in 4 registers");
+  if (warp == 5) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;  // S0: cols [0,128), S1: [128,256), O: [256,384)
+
+  if (warp == 4) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      pdl_wait();
+      for (int i = pre; i < first; ++i) issue(i);
+      for (int i = STAGES; i < ntiles; ++i) {
+        mbar_wait(&kv_empty[i % STAGES], ((i / STAGES) - 1) & 1);
+        issue(i);
+      }
+    }
+  } else if (warp == 5) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0 && ntiles > 0) {
+      constexpr uint32_t idesc_s = idesc_bf16_major(ROWS, KEYS, 0, 0);  // Q (K-major) x K^T (K-major)
+      constexpr uint32_t idesc_o = idesc_bf16_major(ROWS, HD, 0, 1);    // P (TMEM) x V (MN-major)
+      const uint32_t q_u = smem_u32(sQ), kv_u = smem_u32(sKV);
+      mbar_wait(q_full, 0);
+      auto issue_s = [&](int i) {
+        const int sb = i & 1, st = i % STAGES;
+        mbar_wait(&kv_full[st], (i / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t kb = kv_u + st * 2 * ks::TILE;
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const uint64_t ad = umma_desc_sw128(q_u + (k >> 2) * 16384 + (k & 3) * 32);
+          const uint64_t bd = umma_desc_sw128(kb + (k >> 2) * ks::HALF + (k & 3) * 32);
+          umma_bf16(tmem + sb * KEYS, ad, bd, idesc_s, k > 0);
+        }
+        umma_commit(&s_full[sb]);
+      };
+      issue_s(0);
+      for (int i = 0; i < ntiles; ++i) {
+        if (i + 1 < ntiles) issue_s(i + 1);
+        mbar_wait(&p_full[i & 1], (i >> 1) & 1);
+        tc_fence_after();
+        const uint32_t vb = kv_u + (i % STAGES) * 2 * ks::TILE + ks::TILE;
+#pragma unroll
+        for (int k = 0; k < KEYS / 16; ++k) {  // 16 keys per step: 8 TMEM columns of packed P
+          const uint64_t bd = umma_desc_mn_sw128(vb + k * 2048, ks::HALF);
+          umma_bf16_ts(tmem + 2 * KEYS, tmem + (i & 1) * KEYS + k * 8, bd, idesc_o, (i > 0 || k > 0) ? 1u : 0u);
+        }
+        umma_commit(&kv_empty[i % STAGES]);
+        umma_commit(&o_done[i & 1]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax warps 0..3 (MMA row = TMEM lane)
+    const int r = warp * 32 + lane;  // = cf * RP + qr
+    const bool live = qr < R;
+    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    pdl_wait();
+    {  // stage Q row qr (every copy) into the K-major SW128 layout
+      const uint4 *src = nullptr;
+      if (live) {
+        const int n = qr / a.G, gg = qr % a.G;
+        src = reinterpret_cast<const uint4 *>(a.q + (((long long)sl * a.Nq + n) * a.H + (long long)h * a.G + gg) * HD);
+      }
+      uint4 v[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) v[c] = live ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
+      const uint32_t q_u = smem_u32(sQ);
+#pragma unroll
+      for (int c = 0; c < 16; ++c) st_shared_v4(q_u + (c >> 3) * 16384 + sw128_off(r, c), v[c].x, v[c].y, v[c].z, v[c].w);
+      fence_proxy_async();
+      mbar_arrive(q_full);
+    }
+    const int Nq = a.Nq;
+    float m_run = -INFINITY, l = 0.f;
+    const bool warp_live = (warp * 32) % RP < R;  // warps of padding rows only keep the handshakes
+    for (int i = 0; i < ntiles; ++i) {
+      const int sb = i & 1;
+      mbar_wait(&s_full[sb], (i >> 1) & 1);
+      tc_fence_after();
+      if (!warp_live) {
+        tc_fence_before();
+        mbar_arrive(&p_full[sb]);
+        continue;
+      }
+      float y[KT];
+      if constexpr (KT == 128) {
+        tmem_ld64_f(lane_base + sb * KEYS, y);
+        tmem_ld64_f(lane_base + sb * KEYS + 64, y + 64);
+      } else if constexpr (KT == 64) {
+        tmem_ld64_f(lane_base + sb * KEYS + cf * KT, y);
+      } else {
+        tmem_ld32_f(lane_base + sb * KEYS + cf * KT, y);
+      }
+      const int pt = key0 + i * KEYS + cf * KT;  // this thread's first key
+      constexpr int NH = KT >= 64 ? KT / 64 : 1;  // 64-key windows of this thread's keys
+#pragma unroll
+      for (int hh = 0; hh < NH; ++hh) {
+        constexpr int W = KT >= 64 ? 64 : KT;
+        float *yw = y + hh * 64;
+        const int p0 = pt + hh * 64;
+        if (a.pad && p0 < Lc) {  // pad batching (f4): masked cache slots of the prefix
+          const uint32_t *pw = a.pad + (size_t)seq * a.pad_words + (p0 >> 5);
+          const uint64_t pm = (uint64_t)pw[0] | (W == 64 ? ((uint64_t)pw[1] << 32) : 0ull);
+          if (pm) {
+#pragma unroll
+            for (int j = 0; j < W; ++j) yw[j] = ((pm >> j) & 1ull) ? -INFINITY : yw[j];
+          }
+        }
+        if (p0 + W > Lc) {  // keys past the prefix: visibility bitmask (Eq. 2)
+          const int off = p0 - Lc;
+          auto word = [&](int q) { return q == 0 ? anc0 : q == 1 ? anc1 : q == 2 ? anc2 : q == 3 ? anc3 : 0ull; };
+          uint64_t vis;
+          if (off < 0) {
+            vis = (off <= -64 ? ~0ull : (~0ull >> (64 + off))) | (off <= -64 ? 0ull : (anc0 << (-off)));
+          } else {
+            const int q = off >> 6, sh = off & 63;
+            const uint64_t lo = word(q), hi = word(q + 1);
+            vis = sh ? ((lo >> sh) | (hi << (64 - sh))) : lo;
+          }
+          if (Nq - off < 64) vis &= (Nq - off <= 0) ? 0ull : (~0ull >> (64 - (Nq - off)));
+#pragma unroll
+          for (int j = 0; j < W; ++j) yw[j] = ((vis >> j) & 1ull) ? yw[j] : -INFINITY;
+        }
+      }
+      float mx0 = y[0], mx1 = y[1], mx2 = y[2], mx3 = y[3];
+#pragma unroll
+      for (int j = 4; j < KT; j += 4) {
+        mx0 = fmaxf(mx0, y[j]);
+        mx1 = fmaxf(mx1, y[j + 1]);
+        mx2 = fmaxf(mx2, y[j + 2]);
+        mx3 = fmaxf(mx3, y[j + 3]);
+      }
+      const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+      float m_new = m_run, alpha = 1.f;
+      bool resc = false;
+      if (m_run == -INFINITY) {
+        m_new = mx;
+      } else if (mx > m_run + tc::RESCALE_LOG2) {
+        m_new = mx;
+        alpha = exp2f(m_run - m_new);
+        resc = true;
+      }
+      const float nb = (m_new == -INFINITY) ? 0.f : -m_new;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+      uint32_t pe[KT / 2];  // this copy's keys, packed in pairs
+#pragma unroll
+      for (int j = 0; j < KT / 2; j += 2) {
+        const float e0 = ex2(fmaf(y[2 * j], sl2, nb)), e1 = ex2(fmaf(y[2 * j + 1], sl2, nb));
+        const float e2 = ex2(fmaf(y[2 * j + 2], sl2, nb)), e3 = ex2(fmaf(y[2 * j + 3], sl2, nb));
+        s0 += e0;
+        s1 += e1;
+        s2 += e2;
+        s3 += e3;
+        pe[j] = pack_bf16(e0, e1);
+        pe[j + 1] = pack_bf16(e2, e3);
+      }
+      uint32_t pk[64];  // the row's 64 packed P columns: this copy's keys, zeros elsewhere
+#pragma unroll
+      for (int j = 0; j < 64; ++j) pk[j] = (j / (KT / 2) == cf) ? pe[j % (KT / 2)] : 0u;
+      l = l * alpha + ((s0 + s1) + (s2 + s3));
+      m_run = m_new;
+      if (__any_sync(0xffffffffu, resc) && i > 0) {
+        mbar_wait(&o_done[sb ^ 1], ((i - 1) >> 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c0 = 0; c0 < HD; c0 += 32) {
+          float o[32];
+          tmem_ld32_f(lane_base + 2 * KEYS + c0, o);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] *= alpha;
+          tmem_st32_f(lane_base + 2 * KEYS + c0, o);
+        }
+      }
+      tmem_st32_u(lane_base + sb * KEYS, pk);  // P(i) over S(i): packed columns [sb * 128, sb * 128 + 64)
+      tmem_st32_u(lane_base + sb * KEYS + 32, pk + 32);
+      tc_fence_before();
+      mbar_arrive(&p_full[sb]);
+    }
+    if (ntiles > 0) {
+      mbar_wait(&o_done[(ntiles - 1) & 1], ((ntiles - 1) >> 1) & 1);
+      tc_fence_after();
+    }
+    // ---- stage this copy's (m, l, O) at MMA row r (ring idle: every MMA and load is complete)
+    float *spart = reinterpret_cast<float *>(sKV + ks::OFF_PART);  // [ROWS][HD]
+    float *spml = spart + ROWS * HD;                                // [ROWS][2]
+    spml[2 * r] = live ? m_run : -INFINITY;
+    spml[2 * r + 1] = live ? l : 0.f;
+    if (warp_live) {
+#pragma unroll
+      for (int c0 = 0; c0 < HD; c0 += 32) {
+        float o[32];
+        if (ntiles > 0) {
+          tmem_ld32_f(lane_base + 2 * KEYS + c0, o);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] = 0.f;
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<float4 *>(spart + r * HD + 4 * ((c0 / 4 + c) ^ (r & 7))) =
+              make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+      }
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");  // the four softmax warps
+    // ---- merge the F copies of query row qr (copy order), threads of copy 0 only
+    if (cf == 0 && live) {
+      float mq[F], lq[F];
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        mq[f] = spml[2 * (f * RP + qr)];
+        lq[f] = spml[2 * (f * RP + qr) + 1];
+      }
+      float M = mq[0];
+#pragma unroll
+      for (int f = 1; f < F; ++f) M = fmaxf(M, mq[f]);
+      float wq[F], L = 0.f;
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        wq[f] = mq[f] == -INFINITY ? 0.f : exp2f(mq[f] - M);
+        L += wq[f] * lq[f];
+      }
+      float *so = reinterpret_cast<float *>(sKV);  // [128][HD]: the tree kernel's staging layout
+      float *sml = so + ROWS * HD;
+      bf16 *dst = a.out + (((long long)sl * a.Nq + qr / a.G) * a.H + (long long)h * a.G + qr % a.G) * HD;
+      const float inv = L > 0.f ? 1.f / L : 0.f;
+#pragma unroll 4
+      for (int c4 = 0; c4 < HD / 4; ++c4) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+          const int rf = f * RP + qr;
+          const float4 v = *reinterpret_cast<const float4 *>(spart + rf * HD + 4 * (c4 ^ (rf & 7)));
+          acc.x += wq[f] * v.x;
+          acc.y += wq[f] * v.y;
+          acc.z += wq[f] * v.z;
+          acc.w += wq[f] * v.w;
+        }
+        if (a.nsplit == 1) {
+          uint2 pk2;
+          pk2.x = pack_bf16(acc.x * inv, acc.y * inv);
+          pk2.y = pack_bf16(acc.z * inv, acc.w * inv);
+          *reinterpret_cast<uint2 *>(dst + 4 * c4) = pk2;
+        } else {
+          *reinterpret_cast<float4 *>(so + qr * HD + 4 * (c4 ^ (qr & 7))) = acc;
+        }
+      }
+      if (a.nsplit > 1) {
+        sml[2 * qr] = M;
+        sml[2 * qr + 1] = L;
+      }
+    }
+  }
+
+  if (a.nsplit > 1) {
+    // split-KV combine over DSMEM (pull), as tree_attn_tc_kernel: rank q owns live rows
+    // [q rows_per, (q+1) rows_per) and reads only live rows
+    cluster_sync_all();
+    const float *so = reinterpret_cast<const float *>(sKV);
+    const float *sml = so + ROWS * HD;
+    float *swt = reinterpret_cast<float *>(sKV + ROWS * HD * 4 + ROWS * 2 * 4);
+    const uint32_t so_u = smem_u32(so), sml_u = smem_u32(sml);
+    const int live_tot = min(RP, R);
+    const int rows_per = (live_tot + a.nsplit - 1) / a.nsplit;
+    const int lr0 = split * rows_per;
+    const int live_rows = max(0, min(rows_per, live_tot - lr0));
+    for (int lr = threadIdx.x; lr < live_rows; lr += blockDim.x) {
+      float mq[8], lq[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float2 v = q < a.nsplit ? ld_dsmem_f32x2(mapa_u32(sml_u + 8 * (lr0 + lr), q)) : make_float2(-INFINITY, 0.f);
+        mq[q] = v.x;
+        lq[q] = v.y;
+      }
+      float M = -INFINITY;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) M = fmaxf(M, mq[q]);
+      float wq[8], L = 0.f;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        wq[q] = mq[q] == -INFINITY ? 0.f : exp2f(mq[q] - M);
+        L += wq[q] * lq[q];
+      }
+      const float inv = 1.f / L;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) swt[lr * 8 + q] = wq[q] * inv;
+    }
+    __syncthreads();
+    const int items = live_rows * (HD / 4);
+    for (int e0 = threadIdx.x; e0 < items; e0 += 2 * blockDim.x) {
+      float4 v[2][8];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int e = min(e0 + u * (int)blockDim.x, items - 1);
+        const int lr = e / (HD / 4), c4 = e % (HD / 4);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < a.nsplit) v[u][q] = ld_dsmem_f32x4(mapa_u32(so_u + 4 * ((lr0 + lr) * HD + 4 * (c4 ^ ((lr0 + lr) & 7))), q));
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int e = e0 + u * (int)blockDim.x;
+        if (e >= items) continue;
+        const int lr = e / (HD / 4), c4 = e % (HD / 4);
+        const int row = lr0 + lr;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (q < a.nsplit) {
+            const float w = swt[lr * 8 + q];
+            acc.x += w * v[u][q].x;
+            acc.y += w * v[u][q].y;
+            acc.z += w * v[u][q].z;
+            acc.w += w * v[u][q].w;
+          }
+        }
+        const int n = row / a.G, gg = row % a.G;
+        uint2 pk2;
+        pk2.x = pack_bf16(acc.x, acc.y);
+        pk2.y = pack_bf16(acc.z, acc.w);
+        *reinterpret_cast<uint2 *>(a.out + (((long long)sl * a.Nq + n) * a.H + (long long)h * a.G + gg) * HD + 4 * c4) =
+            pk2;
+      }
+    }
+    cluster_sync_all();  // peers may still be reading this CTA's shared memory
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 5) tmem_dealloc<512>(tmem);
+}
+
 // ============================================================================ K1, stream-K ("lean") variant
 // The tree-mode kernel above gives every (row block, sequence, kv head) unit nsplit CTAs of a
 // cluster (nsplit <= 8, combined over DSMEM): with 1 CTA per SM (192 KB of shared memory) the grid
@@ -1086,6 +1523,9 @@ int attention_tc_nsplit(int units) {  // 1 CTA per SM: aim for ~one wave of 148
   return ns;
 }
 
+static int g_attn_ks = 1;  // sm_set_option("attn_ks"): key-split row packing for N G <= 64 (1) or off (0)
+void attention_set_ks(int on) { g_attn_ks = on; }
+
 cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
@@ -1110,6 +1550,26 @@ cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
   attrs[1].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = a.nsplit > 1 ? 2 : 1;
+  const int R = a.Nq * a.G;
+  // key-split row packing (F = 128 / RP copies of <= RP live rows) where each CTA streams a long key
+  // range; the short split ranges of the C2 in-step shape (cap / nsplit ~ 530 keys) stay on the
+  // 128-row kernel (its 64-key tiles split them more evenly: profiles/r02/k1_experiments.txt)
+  if (g_attn_ks && !a.causal && R <= (g_attn_ks > 1 ? 128 : 64) && (a.nsplit == 1 || a.cap >= 1024 * a.nsplit)) {
+    static bool ks_attr = false;
+    if (!ks_attr) {
+      const auto A = cudaFuncAttributeMaxDynamicSharedMemorySize;
+      cudaError_t e = cudaFuncSetAttribute(tree_attn_ks_kernel<2>, A, ks::SMEM);
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(tree_attn_ks_kernel<4>, A, ks::SMEM);
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(tree_attn_ks_kernel<1>, A, ks::SMEM);
+      if (e != cudaSuccess) return e;
+      ks_attr = true;
+    }
+    cfg.dynamicSmemBytes = ks::SMEM;
+    cfg.gridDim.y = 1;
+    if (R <= 32) return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<4>, a);
+    if (R <= 64) return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<2>, a);
+    return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<1>, a);  // 128 rows, 128-key tiles (attn_ks = 2)
+  }
   if (a.causal) return cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<true>, a);
   return cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<false>, a);
 }
@@ -1121,6 +1581,9 @@ void attention_tc_preload() {  // force-load (see gemm_preload)
   cudaFuncGetAttributes(&fa, tree_attn_lean_kernel);
   cudaFuncGetAttributes(&fa, tree_attn_tc_kernel<false>);
   cudaFuncGetAttributes(&fa, tree_attn_tc_kernel<true>);
+  cudaFuncGetAttributes(&fa, tree_attn_ks_kernel<2>);
+  cudaFuncGetAttributes(&fa, tree_attn_ks_kernel<4>);
+  cudaFuncGetAttributes(&fa, tree_attn_ks_kernel<1>);
 }
 
 }  // namespace sm

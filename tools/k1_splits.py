@@ -20,7 +20,12 @@ pts = [("A", 32, 32, b, N, Lc) for (b, N, Lc) in
       [("B", 8, 1, b, N, Lc) for (b, N, Lc) in [(1, 64, 4096), (8, 64, 4096), (8, 16, 8192), (32, 64, 4096),
                                                (16, 16, 32768)]]
 hd = 128
-VARS = [("cl", dict(attn_lean=0)), ("l32", dict(attn_lean=1, attn_lean_div=32)), ("l16", dict(attn_lean=1, attn_lean_div=16)),
+if os.environ.get("K1_VARS") == "ks":  # 128-row kernel vs key-split row packing (N G <= 64)
+    VARS = [("rows128", dict(attn_lean=0, attn_ks=0)), ("ks", dict(attn_lean=0, attn_ks=1)),
+            ("ks2", dict(attn_lean=0, attn_ks=2))]
+else:
+    VARS = None
+VARS = VARS or [("cl", dict(attn_lean=0)), ("l32", dict(attn_lean=1, attn_lean_div=32)), ("l16", dict(attn_lean=1, attn_lean_div=16)),
         ("l8", dict(attn_lean=1, attn_lean_div=8)), ("l4", dict(attn_lean=1, attn_lean_div=4))]
 print(f"{'g':2s} {'b':>3s} {'N':>4s} {'Lc':>6s} {'MB':>7s} " + " ".join(f"{n:>7s}" for n, _ in VARS))
 for g, H, Hkv, b, N, Lc in pts:

@@ -29,6 +29,9 @@ ap.add_argument("--full", action="store_true", help="SURVEY 8.d.1 grid: N 16..25
                                                      "uniform and ragged lengths")
 a = ap.parse_args()
 sm.set_option("attn_tc", a.tc)
+for kv_opt in filter(None, os.environ.get("SM_OPT", "").split(",")):  # sm_set_option knobs, e.g. attn_ks=2
+    k_, v_ = kv_opt.split("=")
+    sm.set_option(k_, int(v_))
 trees = {n: (sm.Tree(synth.V64) if n == 64 else sm.Tree(synth.SWEEP_TREES[n])) for n in (16, 32, 64, 128, 256)}
 geoms = [("A 32/32", 32, 32), ("B 8/1", 8, 1)]
 Ns = [16, 64, 256]
