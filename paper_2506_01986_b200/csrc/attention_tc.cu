@@ -101,6 +101,17 @@ SM_DEV void tmem_ld64_f(uint32_t taddr, float *v) {  // 64 consecutive columns, 
 #pragma unroll
   for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
 }
+SM_DEV void tmem_ld16_f(uint32_t taddr, float *v) {  // 16 consecutive columns
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
 SM_DEV void tmem_st32_f(uint32_t taddr, const float *v) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
@@ -556,14 +567,19 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
 // work twice).  Each copy keeps its own (m, l, O); the F partials of a row are merged in the CTA
 // (fixed copy order) and the result enters the split-KV cluster combine as in tree_attn_tc_kernel.
 namespace ks {
-constexpr int HD = 128, ROWS = 128, KEYS = 128;
-constexpr int HALF = KEYS * 64 * 2;        // 16 KB: one hd-half (64 columns) of a 128-key K or V tile
-constexpr int TILE = 2 * HALF;             // 32 KB: a 128-key K (or V) tile
-constexpr int STAGES = 3;                  // 3 x (K + V) = 192 KB
+// KEYS = 128 (long key ranges: 3 stages of 64 KB) or 64 (the short split ranges of the C2 in-step
+// shape: 6 stages of 32 KB, the 128-row kernel's tile granularity with the softmax on four
+// sub-partitions); the ring is 192 KB either way
+constexpr int HD = 128, ROWS = 128;
+template <int KEYS> struct Cfg {
+  static constexpr int HALF = KEYS * 64 * 2;        // one hd-half (64 columns) of a K or V tile
+  static constexpr int TILE = 2 * HALF;             // a K (or V) tile
+  static constexpr int STAGES = KEYS == 128 ? 3 : 6;
+};
 constexpr int QB = ROWS * HD * 2;          // 32 KB
 constexpr int OFF_Q = 0;
 constexpr int OFF_KV = OFF_Q + QB;
-constexpr int OFF_BAR = OFF_KV + STAGES * 2 * TILE;
+constexpr int OFF_BAR = OFF_KV + 192 * 1024;
 constexpr int SMEM = OFF_BAR + 256 + 1024;
 static_assert(SMEM <= 232448, "K1 (KS) shared memory");
 // end-of-kernel staging in the idle ring: merged rows for the cluster combine at offset 0 (the tree
@@ -571,12 +587,16 @@ static_assert(SMEM <= 232448, "K1 (KS) shared memory");
 constexpr int OFF_PART = 80 * 1024;        // [ROWS][HD] fp32 (copy f of row r at f RP + r) + [ROWS] (m, l)
 }  // namespace ks
 
-template <int F>
+template <int F, int KEYS>
 __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_constant__ AttnArgs a) {
-  constexpr int HD = ks::HD, ROWS = ks::ROWS, KEYS = ks::KEYS, STAGES = ks::STAGES;
+  constexpr int HD = ks::HD, ROWS = ks::ROWS, STAGES = ks::Cfg<KEYS>::STAGES;
+  constexpr int HALF = ks::Cfg<KEYS>::HALF, TILE = ks::Cfg<KEYS>::TILE;
+  constexpr int TCOLS = KEYS == 128 ? 512 : 256;  // S0, S1 (KEYS columns each), O (128)
   constexpr int RP = ROWS / F;      // rows per copy
   constexpr int KT = KEYS / F;      // keys per thread per tile
   static_assert(F == 1 || F == 2 || F == 4, "copies");
+  static_assert(KEYS == 64 || KEYS == 128, "key tile");
+  static_assert(KT >= 16, "keys per thread");
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sQ = smem + ks::OFF_Q;
@@ -605,18 +625,18 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
 
   const long long kbase_row = a.k_row0 + (long long)seq * a.seq_rows + (long long)h * a.cap;
   const long long vbase_row = a.v_row0 + (long long)seq * a.seq_rows + (long long)h * a.cap;
-  auto issue = [&](int i) {  // K and V of keys [p, p + 128) -> stage i % STAGES, [hd half][128 keys][64]
+  auto issue = [&](int i) {  // K and V of keys [p, p + KEYS) -> stage i % STAGES, [hd half][KEYS keys][64]
     const int s = i % STAGES;
-    uint8_t *kb = sKV + s * 2 * ks::TILE;
-    uint8_t *vb = kb + ks::TILE;
+    uint8_t *kb = sKV + s * 2 * TILE;
+    uint8_t *vb = kb + TILE;
     const int p = key0 + i * KEYS;
-    mbar_arrive_expect_tx(&kv_full[s], 2 * ks::TILE);
+    mbar_arrive_expect_tx(&kv_full[s], 2 * TILE);
 #pragma unroll
     for (int hf = 0; hf < 2; ++hf) {
 #pragma unroll
-      for (int kh = 0; kh < 2; ++kh) {  // two 64-key boxes per hd half, consecutive rows
-        tma_load_2d(kb + hf * ks::HALF + kh * 8192, &a.tmK, &kv_full[s], hf * 64, (int)(kbase_row + p + kh * 64));
-        tma_load_2d(vb + hf * ks::HALF + kh * 8192, &a.tmV, &kv_full[s], hf * 64, (int)(vbase_row + p + kh * 64));
+      for (int kh = 0; kh < KEYS / 64; ++kh) {  // 64-key boxes per hd half, consecutive rows
+        tma_load_2d(kb + hf * HALF + kh * 8192, &a.tmK, &kv_full[s], hf * 64, (int)(kbase_row + p + kh * 64));
+        tma_load_2d(vb + hf * HALF + kh * 8192, &a.tmV, &kv_full[s], hf * 64, (int)(vbase_row + p + kh * 64));
       }
     }
   };
@@ -650,11 +670,11 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
     anc3 = w[3];
   }
   static_assert(kAncWords == 4, "ancestor words are kept in 4 registers");
-  if (warp == 5) tmem_alloc<512>(tslot);
+  if (warp == 5) tmem_alloc<TCOLS>(tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tslot;  // S0: cols [0,128), S1: [128,256), O: [256,384)
+  const uint32_t tmem = *tslot;  // S0: cols [0, KEYS), S1: [KEYS, 2 KEYS), O: [2 KEYS, 2 KEYS + 128)
 
   if (warp == 4) {
     // ------------------------------------------------------------ TMA producer
@@ -677,11 +697,11 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
         const int sb = i & 1, st = i % STAGES;
         mbar_wait(&kv_full[st], (i / STAGES) & 1);
         tc_fence_after();
-        const uint32_t kb = kv_u + st * 2 * ks::TILE;
+        const uint32_t kb = kv_u + st * 2 * TILE;
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k) {
           const uint64_t ad = umma_desc_sw128(q_u + (k >> 2) * 16384 + (k & 3) * 32);
-          const uint64_t bd = umma_desc_sw128(kb + (k >> 2) * ks::HALF + (k & 3) * 32);
+          const uint64_t bd = umma_desc_sw128(kb + (k >> 2) * HALF + (k & 3) * 32);
           umma_bf16(tmem + sb * KEYS, ad, bd, idesc_s, k > 0);
         }
         umma_commit(&s_full[sb]);
@@ -691,10 +711,10 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
         if (i + 1 < ntiles) issue_s(i + 1);
         mbar_wait(&p_full[i & 1], (i >> 1) & 1);
         tc_fence_after();
-        const uint32_t vb = kv_u + (i % STAGES) * 2 * ks::TILE + ks::TILE;
+        const uint32_t vb = kv_u + (i % STAGES) * 2 * TILE + TILE;
 #pragma unroll
         for (int k = 0; k < KEYS / 16; ++k) {  // 16 keys per step: 8 TMEM columns of packed P
-          const uint64_t bd = umma_desc_mn_sw128(vb + k * 2048, ks::HALF);
+          const uint64_t bd = umma_desc_mn_sw128(vb + k * 2048, HALF);
           umma_bf16_ts(tmem + 2 * KEYS, tmem + (i & 1) * KEYS + k * 8, bd, idesc_o, (i > 0 || k > 0) ? 1u : 0u);
         }
         umma_commit(&kv_empty[i % STAGES]);
@@ -740,8 +760,10 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
         tmem_ld64_f(lane_base + sb * KEYS + 64, y + 64);
       } else if constexpr (KT == 64) {
         tmem_ld64_f(lane_base + sb * KEYS + cf * KT, y);
-      } else {
+      } else if constexpr (KT == 32) {
         tmem_ld32_f(lane_base + sb * KEYS + cf * KT, y);
+      } else {
+        tmem_ld16_f(lane_base + sb * KEYS + cf * KT, y);
       }
       const int pt = key0 + i * KEYS + cf * KT;  // this thread's first key
       constexpr int NH = KT >= 64 ? KT / 64 : 1;  // 64-key windows of this thread's keys
@@ -806,9 +828,9 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
         pe[j] = pack_bf16(e0, e1);
         pe[j + 1] = pack_bf16(e2, e3);
       }
-      uint32_t pk[64];  // the row's 64 packed P columns: this copy's keys, zeros elsewhere
+      uint32_t pk[KEYS / 2];  // the row's packed P columns: this copy's keys, zeros elsewhere
 #pragma unroll
-      for (int j = 0; j < 64; ++j) pk[j] = (j / (KT / 2) == cf) ? pe[j % (KT / 2)] : 0u;
+      for (int j = 0; j < KEYS / 2; ++j) pk[j] = (j / (KT / 2) == cf) ? pe[j % (KT / 2)] : 0u;
       l = l * alpha + ((s0 + s1) + (s2 + s3));
       m_run = m_new;
       if (__any_sync(0xffffffffu, resc) && i > 0) {
@@ -823,8 +845,8 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
           tmem_st32_f(lane_base + 2 * KEYS + c0, o);
         }
       }
-      tmem_st32_u(lane_base + sb * KEYS, pk);  // P(i) over S(i): packed columns [sb * 128, sb * 128 + 64)
-      tmem_st32_u(lane_base + sb * KEYS + 32, pk + 32);
+      tmem_st32_u(lane_base + sb * KEYS, pk);  // P(i) over S(i): packed columns [sb KEYS, sb KEYS + KEYS / 2)
+      if constexpr (KEYS == 128) tmem_st32_u(lane_base + sb * KEYS + 32, pk + 32);
       tc_fence_before();
       mbar_arrive(&p_full[sb]);
     }
@@ -978,7 +1000,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 5) tmem_dealloc<512>(tmem);
+  if (warp == 5) tmem_dealloc<TCOLS>(tmem);
 }
 
 // ============================================================================ K1, stream-K ("lean") variant
@@ -1523,7 +1545,7 @@ int attention_tc_nsplit(int units) {  // 1 CTA per SM: aim for ~one wave of 148
   return ns;
 }
 
-static int g_attn_ks = 1;  // sm_set_option("attn_ks"): key-split row packing for N G <= 64 (1) or off (0)
+static int g_attn_ks = 2;  // sm_set_option("attn_ks"): KS kernel for N G <= 128 (2, default), <= 64 (1), off (0), 3 = long ranges only
 void attention_set_ks(int on) { g_attn_ks = on; }
 
 cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
@@ -1554,21 +1576,28 @@ cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
   // key-split row packing (F = 128 / RP copies of <= RP live rows) where each CTA streams a long key
   // range; the short split ranges of the C2 in-step shape (cap / nsplit ~ 530 keys) stay on the
   // 128-row kernel (its 64-key tiles split them more evenly: profiles/r02/k1_experiments.txt)
-  if (g_attn_ks && !a.causal && R <= (g_attn_ks > 1 ? 128 : 64) && (a.nsplit == 1 || a.cap >= 1024 * a.nsplit)) {
+  const bool long_range = a.nsplit == 1 || a.cap >= 1024 * a.nsplit;  // 128-key tiles; else 64-key tiles
+  if (g_attn_ks && !a.causal && R <= (g_attn_ks > 1 ? 128 : 64) && (g_attn_ks != 3 || long_range)) {
     static bool ks_attr = false;
     if (!ks_attr) {
       const auto A = cudaFuncAttributeMaxDynamicSharedMemorySize;
-      cudaError_t e = cudaFuncSetAttribute(tree_attn_ks_kernel<2>, A, ks::SMEM);
-      if (e == cudaSuccess) e = cudaFuncSetAttribute(tree_attn_ks_kernel<4>, A, ks::SMEM);
-      if (e == cudaSuccess) e = cudaFuncSetAttribute(tree_attn_ks_kernel<1>, A, ks::SMEM);
+      cudaError_t e = cudaSuccess;
+      for (auto fn : {tree_attn_ks_kernel<4, 128>, tree_attn_ks_kernel<2, 128>, tree_attn_ks_kernel<1, 128>,
+                      tree_attn_ks_kernel<4, 64>, tree_attn_ks_kernel<2, 64>, tree_attn_ks_kernel<1, 64>})
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, A, ks::SMEM);
       if (e != cudaSuccess) return e;
       ks_attr = true;
     }
     cfg.dynamicSmemBytes = ks::SMEM;
     cfg.gridDim.y = 1;
-    if (R <= 32) return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<4>, a);
-    if (R <= 64) return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<2>, a);
-    return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<1>, a);  // 128 rows, 128-key tiles (attn_ks = 2)
+    if (long_range) {
+      if (R <= 32) return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<4, 128>, a);
+      if (R <= 64) return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<2, 128>, a);
+      return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<1, 128>, a);
+    }
+    if (R <= 32) return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<4, 64>, a);
+    if (R <= 64) return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<2, 64>, a);
+    return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<1, 64>, a);
   }
   if (a.causal) return cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<true>, a);
   return cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<false>, a);
@@ -1581,9 +1610,12 @@ void attention_tc_preload() {  // force-load (see gemm_preload)
   cudaFuncGetAttributes(&fa, tree_attn_lean_kernel);
   cudaFuncGetAttributes(&fa, tree_attn_tc_kernel<false>);
   cudaFuncGetAttributes(&fa, tree_attn_tc_kernel<true>);
-  cudaFuncGetAttributes(&fa, tree_attn_ks_kernel<2>);
-  cudaFuncGetAttributes(&fa, tree_attn_ks_kernel<4>);
-  cudaFuncGetAttributes(&fa, tree_attn_ks_kernel<1>);
+  cudaFuncGetAttributes(&fa, tree_attn_ks_kernel<4, 128>);
+  cudaFuncGetAttributes(&fa, tree_attn_ks_kernel<2, 128>);
+  cudaFuncGetAttributes(&fa, tree_attn_ks_kernel<1, 128>);
+  cudaFuncGetAttributes(&fa, tree_attn_ks_kernel<4, 64>);
+  cudaFuncGetAttributes(&fa, tree_attn_ks_kernel<2, 64>);
+  cudaFuncGetAttributes(&fa, tree_attn_ks_kernel<1, 64>);
 }
 
 }  // namespace sm
