@@ -567,9 +567,8 @@ __global__ void __launch_bounds__(192, 1) tree_attn_tc_kernel(const __grid_const
 // work twice).  Each copy keeps its own (m, l, O); the F partials of a row are merged in the CTA
 // (fixed copy order) and the result enters the split-KV cluster combine as in tree_attn_tc_kernel.
 namespace ks {
-// KEYS = 128 (long key ranges: 3 stages of 64 KB) or 64 (the short split ranges of the C2 in-step
-// shape: 6 stages of 32 KB, the 128-row kernel's tile granularity with the softmax on four
-// sub-partitions); the ring is 192 KB either way
+// KEYS = 128: 3 stages of 64 KB.  (KEYS = 64, 6 stages of 32 KB, for the short split ranges of the C2
+// in-step shape measured 13 % slower than the 128-row kernel there: profiles/r02/k1_experiments.txt)
 constexpr int HD = 128, ROWS = 128;
 template <int KEYS> struct Cfg {
   static constexpr int HALF = KEYS * 64 * 2;        // one hd-half (64 columns) of a K or V tile
@@ -1545,7 +1544,7 @@ int attention_tc_nsplit(int units) {  // 1 CTA per SM: aim for ~one wave of 148
   return ns;
 }
 
-static int g_attn_ks = 2;  // sm_set_option("attn_ks"): KS kernel for N G <= 128 (2, default), <= 64 (1), off (0), 3 = long ranges only
+static int g_attn_ks = 2;  // sm_set_option("attn_ks"): row-copy kernel for N G <= 128 (2, default), <= 64 (1), off (0)
 void attention_set_ks(int on) { g_attn_ks = on; }
 
 cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
@@ -1576,28 +1575,22 @@ cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
   // key-split row packing (F = 128 / RP copies of <= RP live rows) where each CTA streams a long key
   // range; the short split ranges of the C2 in-step shape (cap / nsplit ~ 530 keys) stay on the
   // 128-row kernel (its 64-key tiles split them more evenly: profiles/r02/k1_experiments.txt)
-  const bool long_range = a.nsplit == 1 || a.cap >= 1024 * a.nsplit;  // 128-key tiles; else 64-key tiles
-  if (g_attn_ks && !a.causal && R <= (g_attn_ks > 1 ? 128 : 64) && (g_attn_ks != 3 || long_range)) {
+  const bool long_range = a.nsplit == 1 || a.cap >= 1024 * a.nsplit;
+  if (g_attn_ks && !a.causal && R <= (g_attn_ks > 1 ? 128 : 64) && long_range) {
     static bool ks_attr = false;
     if (!ks_attr) {
       const auto A = cudaFuncAttributeMaxDynamicSharedMemorySize;
       cudaError_t e = cudaSuccess;
-      for (auto fn : {tree_attn_ks_kernel<4, 128>, tree_attn_ks_kernel<2, 128>, tree_attn_ks_kernel<1, 128>,
-                      tree_attn_ks_kernel<4, 64>, tree_attn_ks_kernel<2, 64>, tree_attn_ks_kernel<1, 64>})
+      for (auto fn : {tree_attn_ks_kernel<4, 128>, tree_attn_ks_kernel<2, 128>, tree_attn_ks_kernel<1, 128>})
         if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, A, ks::SMEM);
       if (e != cudaSuccess) return e;
       ks_attr = true;
     }
     cfg.dynamicSmemBytes = ks::SMEM;
     cfg.gridDim.y = 1;
-    if (long_range) {
-      if (R <= 32) return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<4, 128>, a);
-      if (R <= 64) return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<2, 128>, a);
-      return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<1, 128>, a);
-    }
-    if (R <= 32) return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<4, 64>, a);
-    if (R <= 64) return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<2, 64>, a);
-    return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<1, 64>, a);
+    if (R <= 32) return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<4, 128>, a);
+    if (R <= 64) return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<2, 128>, a);
+    return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<1, 128>, a);
   }
   if (a.causal) return cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<true>, a);
   return cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<false>, a);
@@ -1613,9 +1606,6 @@ void attention_tc_preload() {  // force-load (see gemm_preload)
   cudaFuncGetAttributes(&fa, tree_attn_ks_kernel<4, 128>);
   cudaFuncGetAttributes(&fa, tree_attn_ks_kernel<2, 128>);
   cudaFuncGetAttributes(&fa, tree_attn_ks_kernel<1, 128>);
-  cudaFuncGetAttributes(&fa, tree_attn_ks_kernel<4, 64>);
-  cudaFuncGetAttributes(&fa, tree_attn_ks_kernel<2, 64>);
-  cudaFuncGetAttributes(&fa, tree_attn_ks_kernel<1, 64>);
 }
 
 }  // namespace sm

@@ -2011,7 +2011,7 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
     tp_set_rsag(value);
   } else if (n == "attn_lean") {  // tree-mode K1 (hd 128): stream-K kernel (1, default) or cluster splits (0)
     attention_set_lean(value);
-  } else if (n == "attn_ks") {  // K1 row-copy kernel (N G <= 128): 0 off, 1 N G <= 64, 2 <= 128 (default), 3 = 2 on long key ranges only
+  } else if (n == "attn_ks") {  // K1 row-copy kernel on long key ranges: 0 off, 1 N G <= 64, 2 N G <= 128 (default)
     attention_set_ks(value);
   } else if (n == "attn_lean_div") {  // lean K1: minimum tiles per CTA = max(2, live rows / value)
     attention_set_lean_div(value);

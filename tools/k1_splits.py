@@ -21,8 +21,7 @@ pts = [("A", 32, 32, b, N, Lc) for (b, N, Lc) in
                                                (16, 16, 32768)]]
 hd = 128
 if os.environ.get("K1_VARS") == "ks":  # 128-row kernel vs key-split row packing (N G <= 64)
-    VARS = [("rows128", dict(attn_lean=0, attn_ks=0)), ("ks_long", dict(attn_lean=0, attn_ks=3)),
-            ("ks", dict(attn_lean=0, attn_ks=2))]
+    VARS = [("rows128", dict(attn_lean=0, attn_ks=0)), ("ks", dict(attn_lean=0, attn_ks=2))]
 else:
     VARS = None
 VARS = VARS or [("cl", dict(attn_lean=0)), ("l32", dict(attn_lean=1, attn_lean_div=32)), ("l16", dict(attn_lean=1, attn_lean_div=16)),
