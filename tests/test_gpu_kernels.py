@@ -133,12 +133,16 @@ ATTN_CASES = [
     ("lean_one_unit_long", synth.V64, None, 1, 1, 1, 128, [9000], 0),
     ("lean_many_units", synth.V64[:31], None, 40, 4, 2, 128, [(211 * i) % 2500 for i in range(40)], 3),
     ("lean_gqa8_4blocks", synth.V64, None, 3, 8, 1, 128, [3000, 5, 1200], 0),
+    # 128-key-tile kernel over several 128-row blocks (geometry B: N G = 512; N 256): one split per unit
+    ("ks_rows512_long", synth.V64, None, 20, 8, 1, 128, [1000 + 37 * i for i in range(20)], 3),
 ]
 
 
 # K1 variants for head_dim 128: the stream-K tcgen05 kernel (default; min tiles per CTA = live rows
 # per unit / 16, and / 2 for many more pieces per unit), the cluster-split tcgen05 kernel, mma.sync
-VARIANTS = {"default": dict(), "rows128": dict(attn_ks=0), "ks64": dict(attn_ks=1), "lean": dict(attn_tc=1, attn_lean=1),
+VARIANTS = {"default": dict(), "rows128": dict(attn_ks=0, attn_tb=0), "ks64": dict(attn_ks=1),
+            "no_tb": dict(attn_tb=0), "ns1": dict(attn_splits=1),
+            "lean": dict(attn_tc=1, attn_lean=1),
             "lean_div2": dict(attn_tc=1, attn_lean=1, attn_lean_div=2), "mma": dict(attn_tc=0)}
 
 

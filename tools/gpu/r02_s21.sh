@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_kernels.py -q -m gpu -x -k "tree_attention" > gpurun_out/s21_k1tests.log 2>&1; echo "rc=$?" >> gpurun_out/s21_k1tests.log
+K1_VARS=tb timeout 600 python tools/k1_splits.py > gpurun_out/s21_k1_tb.txt 2>&1
+timeout 2400 python tools/k1_sweep.py --full > gpurun_out/s21_k1_sweep_full.txt 2>&1
