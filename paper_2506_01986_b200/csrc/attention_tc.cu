@@ -1003,402 +1003,6 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
   if (warp == 5) tmem_dealloc<TCOLS>(tmem);
 }
 
-// ============================================================================ K1, two row blocks per CTA (TB)
-// For N G > 128 query rows per kv head (geometry B: the 70B TP8 shard, 8 query heads per kv head;
-// N 256) the 128-row kernels give every 128-row block its own CTA, which streams the same K/V and
-// runs S -> softmax -> PV with the tensor pipe idle while its one softmax warpgroup works.  Here a
-// CTA owns two row blocks: two softmax warpgroups (one per block, each with its own Q, S buffers,
-// O and (m, l)) consume every K/V tile, so the tile is loaded once for 256 rows and the MMAs of
-// one block run while the other block's softmax does (tensor-bound shapes: S and PV are
-// M 128 x N 64 x K 128 and M 128 x N 128 x K 64 per block and tile).
-// Warps: 0-3 block 0, 4-7 block 1 (TMEM lane quadrant = warp & 3), 8 TMA producer, 9 MMA issuer.
-// TMEM: block g at columns [256 g, 256 g + 256): S0, S1 (64 each), O (128).
-namespace tb {
-constexpr int HD = 128, ROWS = 128, KEYS = 64, TILE = KEYS * HD * 2;  // 16 KB
-constexpr int STAGES = 5;                                               // 5 x 32 KB
-constexpr int QB = ROWS * HD * 2;                                       // 32 KB per block
-constexpr int OFF_Q = 0;
-constexpr int OFF_KV = 2 * QB;
-constexpr int OFF_BAR = OFF_KV + STAGES * 2 * TILE;
-constexpr int SMEM = OFF_BAR + 256 + 1024;
-static_assert(SMEM <= 232448, "K1 (TB) shared memory");
-}  // namespace tb
-
-__global__ void __launch_bounds__(320, 1) tree_attn_tb_kernel(const __grid_constant__ AttnArgs a) {
-  constexpr int HD = tb::HD, ROWS = tb::ROWS, KEYS = tb::KEYS, TILE = tb::TILE, STAGES = tb::STAGES;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t *sKV = smem + tb::OFF_KV;
-  uint64_t *kv_full = reinterpret_cast<uint64_t *>(smem + tb::OFF_BAR);
-  uint64_t *kv_empty = kv_full + STAGES;
-  uint64_t *s_full = kv_empty + STAGES;  // [2 blocks][2]
-  uint64_t *p_full = s_full + 4;         // [2][2]
-  uint64_t *o_done = p_full + 4;         // [2][2]
-  uint64_t *q_full = o_done + 4;         // [2]
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(q_full + 2);
-
-  pdl_trigger();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int split = blockIdx.x, pblk = blockIdx.y;  // pair of row blocks
-  const int sl = blockIdx.z / a.Hkv, h = blockIdx.z % a.Hkv;
-  const int seq = a.seq_base + sl;
-  const int Lc = a.len[seq];
-  const int R = a.Nq * a.G;
-  const int T = Lc + a.Nq;
-  const int chunk = ((T + a.nsplit - 1) / a.nsplit + KEYS - 1) / KEYS * KEYS;
-  const int key0 = min(T, split * chunk);
-  const int key1 = min(T, key0 + chunk);
-  const int ntiles = (key1 - key0 + KEYS - 1) / KEYS;
-  const float sl2 = a.scale_log2;
-  const bool blk1_live = (2 * pblk + 1) * ROWS < R;  // the second block has live rows
-
-  const long long kbase_row = a.k_row0 + (long long)seq * a.seq_rows + (long long)h * a.cap;
-  const long long vbase_row = a.v_row0 + (long long)seq * a.seq_rows + (long long)h * a.cap;
-  auto issue = [&](int i) {
-    const int s = i % STAGES;
-    uint8_t *kb = sKV + s * 2 * TILE;
-    uint8_t *vb = kb + TILE;
-    const int p = key0 + i * KEYS;
-    mbar_arrive_expect_tx(&kv_full[s], 2 * TILE);
-#pragma unroll
-    for (int hf = 0; hf < 2; ++hf) {
-      tma_load_2d(kb + hf * 8192, &a.tmK, &kv_full[s], hf * 64, (int)(kbase_row + p));
-      tma_load_2d(vb + hf * 8192, &a.tmV, &kv_full[s], hf * 64, (int)(vbase_row + p));
-    }
-  };
-  const int first = min(STAGES, ntiles);
-  int pre = 0;
-  if (threadIdx.x == 256) {
-    tma_prefetch_desc(&a.tmK);
-    tma_prefetch_desc(&a.tmV);
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
-    }
-    for (int b = 0; b < 4; ++b) {
-      mbar_init(&s_full[b], 1);
-      mbar_init(&p_full[b], 128);
-      mbar_init(&o_done[b], 1);
-    }
-    mbar_init(&q_full[0], 128);
-    mbar_init(&q_full[1], 128);
-    fence_barrier_init();
-    while (pre < first && key0 + (pre + 1) * KEYS <= Lc) issue(pre++);
-  }
-  const int grp = (warp >> 2) & 1, quad = warp & 3;
-  const int row0 = (2 * pblk + grp) * ROWS;  // this softmax warpgroup's row block
-  uint64_t anc0 = 0, anc1 = 0, anc2 = 0, anc3 = 0;
-  if (warp < 8) {
-    const int rr = row0 + quad * 32 + lane;
-    if (rr < R) {
-      const uint64_t *w = a.anc + (rr / a.G) * kAncWords;
-      anc0 = w[0];
-      anc1 = w[1];
-      anc2 = w[2];
-      anc3 = w[3];
-    }
-  }
-  static_assert(kAncWords == 4, "ancestor words are kept in 4 registers");
-  if (warp == 9) tmem_alloc<512>(tslot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tslot;
-
-  if (warp == 8) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      pdl_wait();
-      for (int i = pre; i < first; ++i) issue(i);
-      for (int i = STAGES; i < ntiles; ++i) {
-        mbar_wait(&kv_empty[i % STAGES], ((i / STAGES) - 1) & 1);
-        issue(i);
-      }
-    }
-  } else if (warp == 9) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0 && ntiles > 0) {
-      constexpr uint32_t idesc_s = idesc_bf16_major(ROWS, KEYS, 0, 0);
-      constexpr uint32_t idesc_o = idesc_bf16_major(ROWS, HD, 0, 1);
-      const uint32_t kv_u = smem_u32(sKV);
-      const int nb = blk1_live ? 2 : 1;
-      mbar_wait(&q_full[0], 0);
-      if (nb > 1) mbar_wait(&q_full[1], 0);
-      auto issue_s = [&](int i) {  // S(i) of both blocks (buffer i & 1 of each)
-        const int sb = i & 1, st = i % STAGES;
-        mbar_wait(&kv_full[st], (i / STAGES) & 1);
-        tc_fence_after();
-        const uint32_t kb = kv_u + st * 2 * TILE;
-        for (int g = 0; g < nb; ++g) {
-          const uint32_t q_u = smem_u32(smem + tb::OFF_Q + g * tb::QB);
-#pragma unroll
-          for (int k = 0; k < HD / 16; ++k) {
-            const uint64_t ad = umma_desc_sw128(q_u + (k >> 2) * 16384 + (k & 3) * 32);
-            const uint64_t bd = umma_desc_sw128(kb + (k >> 2) * 8192 + (k & 3) * 32);
-            umma_bf16(tmem + g * 256 + sb * KEYS, ad, bd, idesc_s, k > 0);
-          }
-          umma_commit(&s_full[g * 2 + sb]);
-        }
-      };
-      issue_s(0);
-      for (int i = 0; i < ntiles; ++i) {
-        if (i + 1 < ntiles) issue_s(i + 1);
-        const uint32_t vb = kv_u + (i % STAGES) * 2 * TILE + TILE;
-        for (int g = 0; g < nb; ++g) {
-          mbar_wait(&p_full[g * 2 + (i & 1)], (i >> 1) & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int k = 0; k < KEYS / 16; ++k) {
-            const uint64_t bd = umma_desc_mn_sw128(vb + k * 2048, 8192);
-            umma_bf16_ts(tmem + g * 256 + 2 * KEYS, tmem + g * 256 + (i & 1) * KEYS + k * 8, bd, idesc_o,
-                         (i > 0 || k > 0) ? 1u : 0u);
-          }
-          umma_commit(&o_done[g * 2 + (i & 1)]);
-        }
-        umma_commit(&kv_empty[i % STAGES]);
-      }
-    }
-  } else {
-    // ------------------------------------------------------------ softmax warpgroups
-    const int r = quad * 32 + lane;
-    const int rr = row0 + r;
-    const bool live = rr < R;
-    const bool grp_live = grp == 0 || blk1_live;
-    const uint32_t gbase = tmem + grp * 256;
-    const uint32_t lane_base = gbase + ((uint32_t)(quad * 32) << 16);
-    pdl_wait();
-    {  // stage this row of Q into the block's K-major SW128 buffer
-      const uint4 *src = nullptr;
-      if (live) {
-        const int n = rr / a.G, gg = rr % a.G;
-        src = reinterpret_cast<const uint4 *>(a.q + (((long long)sl * a.Nq + n) * a.H + (long long)h * a.G + gg) * HD);
-      }
-      uint4 v[16];
-#pragma unroll
-      for (int c = 0; c < 16; ++c) v[c] = live ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
-      const uint32_t q_u = smem_u32(smem + tb::OFF_Q + grp * tb::QB);
-#pragma unroll
-      for (int c = 0; c < 16; ++c) st_shared_v4(q_u + (c >> 3) * 16384 + sw128_off(r, c), v[c].x, v[c].y, v[c].z, v[c].w);
-      fence_proxy_async();
-      mbar_arrive(&q_full[grp]);
-    }
-    const int Nq = a.Nq;
-    float m_run = -INFINITY, l = 0.f;
-    const bool warp_live = grp_live && row0 + quad * 32 < R;
-    for (int i = 0; i < ntiles && grp_live; ++i) {
-      const int sb = i & 1;
-      mbar_wait(&s_full[grp * 2 + sb], (i >> 1) & 1);
-      tc_fence_after();
-      if (!warp_live) {
-        tc_fence_before();
-        mbar_arrive(&p_full[grp * 2 + sb]);
-        continue;
-      }
-      float y[64];
-      tmem_ld64_f(lane_base + sb * KEYS, y);
-      const int p0 = key0 + i * KEYS;
-      if (a.pad && p0 < Lc) {
-        const uint32_t *pw = a.pad + (size_t)seq * a.pad_words + (p0 >> 5);
-        const uint64_t pm = (uint64_t)pw[0] | ((uint64_t)pw[1] << 32);
-        if (pm) {
-#pragma unroll
-          for (int j = 0; j < 64; ++j) y[j] = ((pm >> j) & 1ull) ? -INFINITY : y[j];
-        }
-      }
-      if (p0 + KEYS > Lc) {  // visibility bitmask (Eq. 2)
-        const int off = p0 - Lc;
-        auto word = [&](int q) { return q == 0 ? anc0 : q == 1 ? anc1 : q == 2 ? anc2 : q == 3 ? anc3 : 0ull; };
-        uint64_t vis;
-        if (off < 0) {
-          vis = (~0ull >> (64 + off)) | (anc0 << (-off));
-        } else {
-          const int q = off >> 6, sh = off & 63;
-          const uint64_t lo = word(q), hi = word(q + 1);
-          vis = sh ? ((lo >> sh) | (hi << (64 - sh))) : lo;
-        }
-        if (Nq - off < 64) vis &= (Nq - off <= 0) ? 0ull : (~0ull >> (64 - (Nq - off)));
-#pragma unroll
-        for (int j = 0; j < 64; ++j) y[j] = ((vis >> j) & 1ull) ? y[j] : -INFINITY;
-      }
-      float mx0 = y[0], mx1 = y[1], mx2 = y[2], mx3 = y[3];
-#pragma unroll
-      for (int j = 4; j < 64; j += 4) {
-        mx0 = fmaxf(mx0, y[j]);
-        mx1 = fmaxf(mx1, y[j + 1]);
-        mx2 = fmaxf(mx2, y[j + 2]);
-        mx3 = fmaxf(mx3, y[j + 3]);
-      }
-      const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
-      float m_new = m_run, alpha = 1.f;
-      bool resc = false;
-      if (m_run == -INFINITY) {
-        m_new = mx;
-      } else if (mx > m_run + tc::RESCALE_LOG2) {
-        m_new = mx;
-        alpha = exp2f(m_run - m_new);
-        resc = true;
-      }
-      const float nb = (m_new == -INFINITY) ? 0.f : -m_new;
-      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-      uint32_t pk[32];
-#pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        const float e0 = ex2(fmaf(y[2 * j], sl2, nb)), e1 = ex2(fmaf(y[2 * j + 1], sl2, nb));
-        const float e2 = ex2(fmaf(y[2 * j + 2], sl2, nb)), e3 = ex2(fmaf(y[2 * j + 3], sl2, nb));
-        s0 += e0;
-        s1 += e1;
-        s2 += e2;
-        s3 += e3;
-        pk[j] = pack_bf16(e0, e1);
-        pk[j + 1] = pack_bf16(e2, e3);
-      }
-      l = l * alpha + ((s0 + s1) + (s2 + s3));
-      m_run = m_new;
-      if (__any_sync(0xffffffffu, resc) && i > 0) {
-        mbar_wait(&o_done[grp * 2 + (sb ^ 1)], ((i - 1) >> 1) & 1);
-        tc_fence_after();
-#pragma unroll 1
-        for (int c0 = 0; c0 < HD; c0 += 32) {
-          float o[32];
-          tmem_ld32_f(lane_base + 2 * KEYS + c0, o);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) o[j] *= alpha;
-          tmem_st32_f(lane_base + 2 * KEYS + c0, o);
-        }
-      }
-      tmem_st32_u(lane_base + sb * KEYS, pk);
-      tc_fence_before();
-      mbar_arrive(&p_full[grp * 2 + sb]);
-    }
-    if (ntiles > 0 && grp_live) {
-      mbar_wait(&o_done[grp * 2 + ((ntiles - 1) & 1)], ((ntiles - 1) >> 1) & 1);
-      tc_fence_after();
-    }
-    const float fin_m = live ? m_run : -INFINITY, fin_l = live ? l : 0.f;
-    if (a.nsplit == 1) {
-      if (warp_live && ntiles > 0) {
-        const float inv = live ? 1.f / l : 0.f;
-        bf16 *dst = a.out + (((long long)sl * a.Nq + rr / a.G) * a.H + (long long)h * a.G + rr % a.G) * HD;
-#pragma unroll
-        for (int c0 = 0; c0 < HD; c0 += 32) {
-          float o[32];
-          tmem_ld32_f(lane_base + 2 * KEYS + c0, o);
-          if (live) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint4 w;
-              w.x = pack_bf16(o[8 * c] * inv, o[8 * c + 1] * inv);
-              w.y = pack_bf16(o[8 * c + 2] * inv, o[8 * c + 3] * inv);
-              w.z = pack_bf16(o[8 * c + 4] * inv, o[8 * c + 5] * inv);
-              w.w = pack_bf16(o[8 * c + 6] * inv, o[8 * c + 7] * inv);
-              reinterpret_cast<uint4 *>(dst + c0)[c] = w;
-            }
-          }
-        }
-      }
-    } else {
-      // stage (m, l, O) of both blocks in the idle ring: row (grp 128 + r) of a 256-row layout
-      float *so = reinterpret_cast<float *>(sKV);  // [256][HD]
-      float *sml = so + 2 * ROWS * HD;             // [256][2]
-      const int sr = grp * ROWS + r;
-      sml[2 * sr] = fin_m;
-      sml[2 * sr + 1] = fin_l;
-      if (warp_live) {
-#pragma unroll
-        for (int c0 = 0; c0 < HD; c0 += 32) {
-          float o[32];
-          if (ntiles > 0) {
-            tmem_ld32_f(lane_base + 2 * KEYS + c0, o);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) o[j] = 0.f;
-          }
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-            *reinterpret_cast<float4 *>(so + sr * HD + 4 * ((c0 / 4 + c) ^ (sr & 7))) =
-                make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
-        }
-      }
-    }
-  }
-
-  if (a.nsplit > 1) {
-    // split-KV combine over DSMEM (pull), as tree_attn_tc_kernel, over the pair's 256 rows
-    cluster_sync_all();
-    const float *so = reinterpret_cast<const float *>(sKV);
-    const float *sml = so + 2 * ROWS * HD;
-    float *swt = reinterpret_cast<float *>(sKV + 2 * ROWS * HD * 4 + 2 * ROWS * 2 * 4);
-    const uint32_t so_u = smem_u32(so), sml_u = smem_u32(sml);
-    const int live_tot = max(0, min(2 * ROWS, R - pblk * 2 * ROWS));
-    const int rows_per = (live_tot + a.nsplit - 1) / a.nsplit;
-    const int lr0 = split * rows_per;
-    const int live_rows = max(0, min(rows_per, live_tot - lr0));
-    for (int lr = threadIdx.x; lr < live_rows; lr += blockDim.x) {
-      float mq[8], lq[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float2 v = q < a.nsplit ? ld_dsmem_f32x2(mapa_u32(sml_u + 8 * (lr0 + lr), q)) : make_float2(-INFINITY, 0.f);
-        mq[q] = v.x;
-        lq[q] = v.y;
-      }
-      float M = -INFINITY;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) M = fmaxf(M, mq[q]);
-      float wq[8], L = 0.f;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        wq[q] = mq[q] == -INFINITY ? 0.f : exp2f(mq[q] - M);
-        L += wq[q] * lq[q];
-      }
-      const float inv = 1.f / L;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) swt[lr * 8 + q] = wq[q] * inv;
-    }
-    __syncthreads();
-    const int items = live_rows * (HD / 4);
-    for (int e0 = threadIdx.x; e0 < items; e0 += 2 * blockDim.x) {
-      float4 v[2][8];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int e = min(e0 + u * (int)blockDim.x, items - 1);
-        const int lr = e / (HD / 4), c4 = e % (HD / 4);
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (q < a.nsplit) v[u][q] = ld_dsmem_f32x4(mapa_u32(so_u + 4 * ((lr0 + lr) * HD + 4 * (c4 ^ ((lr0 + lr) & 7))), q));
-      }
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int e = e0 + u * (int)blockDim.x;
-        if (e >= items) continue;
-        const int lr = e / (HD / 4), c4 = e % (HD / 4);
-        const int row = pblk * 2 * ROWS + lr0 + lr;
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          if (q < a.nsplit) {
-            const float w = swt[lr * 8 + q];
-            acc.x += w * v[u][q].x;
-            acc.y += w * v[u][q].y;
-            acc.z += w * v[u][q].z;
-            acc.w += w * v[u][q].w;
-          }
-        }
-        const int n = row / a.G, gg = row % a.G;
-        uint2 pk2;
-        pk2.x = pack_bf16(acc.x, acc.y);
-        pk2.y = pack_bf16(acc.z, acc.w);
-        *reinterpret_cast<uint2 *>(a.out + (((long long)sl * a.Nq + n) * a.H + (long long)h * a.G + gg) * HD + 4 * c4) =
-            pk2;
-      }
-    }
-    cluster_sync_all();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 9) tmem_dealloc<512>(tmem);
-}
-
 // ============================================================================ K1, stream-K ("lean") variant
 // The tree-mode kernel above gives every (row block, sequence, kv head) unit nsplit CTAs of a
 // cluster (nsplit <= 8, combined over DSMEM): with 1 CTA per SM (192 KB of shared memory) the grid
@@ -1941,8 +1545,6 @@ int attention_tc_nsplit(int units) {  // 1 CTA per SM: aim for ~one wave of 148
   return ns;
 }
 
-static int g_attn_tb = 0;  // sm_set_option("attn_tb"): two row blocks per CTA for N G > 128 (1, default) or off (0)
-void attention_set_tb(int on) { g_attn_tb = on; }
 static int g_attn_ks = 2;  // sm_set_option("attn_ks"): 128-key-tile kernel on long key ranges, all N G (2, default), N G <= 64 (1), off (0)
 void attention_set_ks(int on) { g_attn_ks = on; }
 
@@ -1974,18 +1576,6 @@ cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
   // 128-key-tile kernel (row copies F = 128 / RP for <= 64 live rows) unless the key range is cut into
   // short splits (cache capacity / nsplit < 1024: the C2 in-step shape, ~530 keys per split), where
   // the 128-row kernel measured faster (profiles/r02/k1_experiments.txt)
-  if (g_attn_tb && !a.causal && R > 128) {  // two 128-row blocks per CTA (tensor-bound N G > 128)
-    static bool tb_attr = false;
-    if (!tb_attr) {
-      cudaError_t e = cudaFuncSetAttribute(tree_attn_tb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tb::SMEM);
-      if (e != cudaSuccess) return e;
-      tb_attr = true;
-    }
-    cfg.gridDim.y = (R + 2 * tb::ROWS - 1) / (2 * tb::ROWS);
-    cfg.blockDim = dim3(320);
-    cfg.dynamicSmemBytes = tb::SMEM;
-    return cudaLaunchKernelEx(&cfg, tree_attn_tb_kernel, a);
-  }
   const bool long_range = a.nsplit == 1 || a.cap >= 1024 * a.nsplit;
   if (g_attn_ks && !a.causal && (g_attn_ks > 1 || R <= 64) && long_range) {
     static bool ks_attr = false;
@@ -2013,7 +1603,6 @@ void attention_tc_preload() {  // force-load (see gemm_preload)
   cudaFuncGetAttributes(&fa, tree_attn_lean_kernel);
   cudaFuncGetAttributes(&fa, tree_attn_tc_kernel<false>);
   cudaFuncGetAttributes(&fa, tree_attn_tc_kernel<true>);
-  cudaFuncGetAttributes(&fa, tree_attn_tb_kernel);
   cudaFuncGetAttributes(&fa, tree_attn_ks_kernel<4, 128>);
   cudaFuncGetAttributes(&fa, tree_attn_ks_kernel<2, 128>);
   cudaFuncGetAttributes(&fa, tree_attn_ks_kernel<1, 128>);

@@ -1957,7 +1957,6 @@ extern "C" sm_status sm_reset_options(void) {
   attention_set_splits(0);
   attention_set_lean(0);
   attention_set_ks(2);
-  attention_set_tb(0);
   attention_set_lean_div(16);
   tp_set_rsag(-1);
   g_fused = 0;
@@ -2012,8 +2011,6 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
     tp_set_rsag(value);
   } else if (n == "attn_lean") {  // tree-mode K1 (hd 128): stream-K kernel (1, default) or cluster splits (0)
     attention_set_lean(value);
-  } else if (n == "attn_tb") {  // K1 two row blocks per CTA for N G > 128: 1 (default) or 0
-    attention_set_tb(value);
   } else if (n == "attn_ks") {  // K1 128-key-tile (row-copy) kernel on long key ranges: 0 off, 1 N G <= 64, 2 all (default)
     attention_set_ks(value);
   } else if (n == "attn_lean_div") {  // lean K1: minimum tiles per CTA = max(2, live rows / value)

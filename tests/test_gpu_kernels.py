@@ -140,8 +140,7 @@ ATTN_CASES = [
 
 # K1 variants for head_dim 128: the stream-K tcgen05 kernel (default; min tiles per CTA = live rows
 # per unit / 16, and / 2 for many more pieces per unit), the cluster-split tcgen05 kernel, mma.sync
-VARIANTS = {"default": dict(), "rows128": dict(attn_ks=0, attn_tb=0), "ks64": dict(attn_ks=1),
-            "no_tb": dict(attn_tb=0), "ns1": dict(attn_splits=1),
+VARIANTS = {"default": dict(), "rows128": dict(attn_ks=0), "ks64": dict(attn_ks=1), "ns1": dict(attn_splits=1),
             "lean": dict(attn_tc=1, attn_lean=1),
             "lean_div2": dict(attn_tc=1, attn_lean=1, attn_lean_div=2), "mma": dict(attn_tc=0)}
 

@@ -20,10 +20,7 @@ pts = [("A", 32, 32, b, N, Lc) for (b, N, Lc) in
       [("B", 8, 1, b, N, Lc) for (b, N, Lc) in [(1, 64, 4096), (8, 64, 4096), (8, 16, 8192), (32, 64, 4096),
                                                (16, 16, 32768)]]
 hd = 128
-if os.environ.get("K1_VARS") == "tb":  # N G > 128: one row block per CTA (128-row / 128-key-tile kernels) vs two
-    VARS = [("rows128", dict(attn_lean=0, attn_ks=0, attn_tb=0)), ("ks", dict(attn_lean=0, attn_tb=0)),
-            ("tb", dict(attn_lean=0, attn_tb=1))]
-elif os.environ.get("K1_VARS") == "ks":  # 128-row kernel vs key-split row packing (N G <= 64)
+if os.environ.get("K1_VARS") == "ks":  # 128-row kernel vs key-split row packing (N G <= 64)
     VARS = [("rows128", dict(attn_lean=0, attn_ks=0)), ("ks", dict(attn_lean=0, attn_ks=2))]
 else:
     VARS = None
