@@ -382,6 +382,7 @@ def run_ours(args, world, rank, local) -> dict | None:
 
     # ---- K1 tree-attention point of the C5 sweep (geometry A, N=64)
     k1 = run_k1_point(sm, args) if args.k1 and args.config == "c2" else None
+    k1_grid = run_k1_grid(sm, args) if args.k1 and args.config == "c2" and world == 1 else None
     acc_lines = None
     if args.extra and args.config == "c2" and world == 1:
         acc_lines = run_c2_acceptance_lines(sm, cfg, model, tree, kv.prompts[0], wl["x_run"], wl)
@@ -443,6 +444,8 @@ def run_ours(args, world, rank, local) -> dict | None:
         res["vanilla"] = van
     if k1:
         res["k1_point"] = k1
+    if k1_grid:
+        res["k1_grid"] = k1_grid
     if acc_lines:
         res.update(acc_lines)
     return res
@@ -750,6 +753,65 @@ def run_k1_point(sm, args) -> dict:
     pk = peaks()
     return {"geometry": "A: H=Hkv=32, hd=128", "N": N, "b": b, "Lc": Lc, "alg_bytes": byt, "ms": round(ms, 4),
             "achieved_gbs": round(gbs, 1), "peak": pk["hbm"], "frac": round(gbs / pk["hbm"], 4)}
+
+
+def run_k1_grid(sm, args) -> dict:
+    """C5 (BASELINE configs[4]) in brief, timed live: tree nodes {16, 64, 128} x KV length {1024, 4096,
+    16384} x batch {1, 8, 32} in geometry A (one 7B layer: 32 q = 32 kv heads) and geometry B (one 70B TP8
+    shard: 8 q heads on 1 kv head), head_dim 128, uniform lengths; bounded to <= 4 GB of K/V per point.
+    Per point: 10 launches over two alternating buffer sets (> L2), CUDA events; frac = max(bytes / HBM
+    peak, flops / bf16 peak) / time (the binding roofline).  The full 810-point grid is
+    tools/k1_sweep.py --full (profiles/r02/k1_sweep_full.txt)."""
+    import statistics
+
+    import torch
+    pk = peaks()
+    trees = {16: sm.Tree(synth.SWEEP_TREES[16]), 64: sm.Tree(synth.V64), 128: sm.Tree(synth.SWEEP_TREES[128])}
+    hd, pts = 128, []
+    for geom, H, Hkv in (("A", 32, 32), ("B", 8, 1)):
+        for b in (1, 8, 32):
+            for N in (16, 64, 128):
+                for Lc in (1024, 4096, 16384):
+                    tree = trees[N]
+                    cap = Lc + tree.N
+                    if b * Hkv * cap * hd * 4 > 4e9:
+                        continue
+                    sets = []
+                    for s_ in range(2):
+                        q = torch.empty(b, tree.N, H, hd, dtype=torch.bfloat16, device="cuda")
+                        k = torch.empty(b, Hkv, cap, hd, dtype=torch.bfloat16, device="cuda")
+                        v = torch.empty_like(k)
+                        for i, t in enumerate((q, k, v)):
+                            sm.generate_bf16(t, 11 + s_, 200 + i, mode=1)
+                        sets.append((q, k, v, torch.empty_like(q)))
+                    L = torch.full((b,), Lc, dtype=torch.int32, device="cuda")
+                    for i in range(2):
+                        q, k, v, o = sets[i % 2]
+                        sm.tree_attention(tree, q, k, v, L, H, Hkv, o)
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    for i in range(10):
+                        q, k, v, o = sets[i % 2]
+                        sm.tree_attention(tree, q, k, v, L, H, Hkv, o)
+                    e1.record()
+                    torch.cuda.synchronize()
+                    us = e0.elapsed_time(e1) * 1e3 / 10
+                    byt = b * Hkv * cap * hd * 4 + 2 * b * tree.N * H * hd * 2
+                    depth = tree.query()["node_depth"]
+                    flops = 4 * H * hd * b * (tree.N * Lc + int(sum(int(x) + 1 for x in depth)))
+                    t_hbm, t_tc = byt / pk["hbm"] / 1e3, flops / pk["bf16"] / 1e6  # us
+                    pts.append(dict(g=geom, b=b, N=tree.N, Lc=Lc, MB=round(byt / 1e6, 1), us=round(us, 1),
+                                    bound="hbm" if t_hbm >= t_tc else "tensor", frac=round(max(t_hbm, t_tc) / us, 3)))
+                    del sets
+    torch.cuda.empty_cache()
+    a_big = [p_["frac"] for p_ in pts if p_["g"] == "A" and p_["bound"] == "hbm" and p_["MB"] >= 64]
+    b_big = [p_["frac"] for p_ in pts if p_["g"] == "B" and p_["b"] >= 8 and p_["Lc"] >= 4096]
+    return {"what": run_k1_grid.__doc__.split("\n")[0].strip(),
+            "points": len(pts),
+            "A_hbm_bound_ge_64MB": {"n": len(a_big), "median_frac": round(statistics.median(a_big), 3),
+                                    "n_ge_0.70": sum(f >= 0.7 for f in a_big)} if a_big else None,
+            "B_b_ge_8_Lc_ge_4096": {"n": len(b_big), "median_frac": round(statistics.median(b_big), 3)} if b_big else None,
+            "grid": [f"{p_['g']} b{p_['b']} N{p_['N']} Lc{p_['Lc']}: {p_['us']} us {p_['bound']} {p_['frac']}" for p_ in pts]}
 
 
 # ------------------------------------------------------------------ oracle (CPU) arm
