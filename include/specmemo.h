@@ -171,7 +171,21 @@ typedef struct {
   int tp_rank, tp_size;          /* tp_size in {1, 2, 4, 8}; divides H, Hkv, F/64 and V/4   */
   void *peer_sym[SM_MAX_TP];     /* [tp_size] (or [pp_size]) device pointers, [rank] = own  */
   int pp_rank, pp_size;          /* layer-split pipeline (f4; pp_size 0 or 1 = off), below  */
+  void *emu_group;               /* NULL on real multi-GPU placements; see sm_emu_group_create */
 } sm_dist;
+/* Host-ordered emulation: several ranks sharing ONE GPU in one process (tests on a 1-GPU box).
+ * There a kernel must never spin on a flag raised by another rank's launch -- nothing guarantees
+ * that the two run at the same time -- so with emu_group set every exchange runs as segment
+ * launches (publish; [reduce-scatter;] merge) with no device-side wait, and the ranks' host
+ * threads order the segments with CUDA events: a rank records "published" on its stream and its
+ * peers' streams wait for that record before their next segment.  The arithmetic, the rank-order
+ * sums and therefore the results are bitwise those of the fused flag protocol.  Contract: every
+ * rank's calls are issued from its own host thread (an exchange blocks the thread until its
+ * peers have published, ~60 s at most, then SM_ERR_CUDA), all ranks share one group, and
+ * sm_step runs eagerly (no step graph) on such a model.  One group per set of ranks; destroy it
+ * after the models. */
+sm_status sm_emu_group_create(int n_ranks, void **group);
+void sm_emu_group_destroy(void *group);
 /* Layer-split pipeline (f4 comparison mode, the paper's own distribution: "partitioning its
  * layers into equal-sized chunks across all available GPUs, with each GPU also hosting the
  * corresponding slices of the KV cache alongside the layers").  pp_size in 2..8 with

@@ -81,7 +81,7 @@ MAX_TP = 8
 
 class Dist(ctypes.Structure):
     _fields_ = [("tp_rank", ctypes.c_int), ("tp_size", ctypes.c_int), ("peer_sym", ctypes.c_void_p * MAX_TP),
-                ("pp_rank", ctypes.c_int), ("pp_size", ctypes.c_int)]
+                ("pp_rank", ctypes.c_int), ("pp_size", ctypes.c_int), ("emu_group", ctypes.c_void_p)]
 
 
 def pp_layers(n_layers: int, pp_rank: int, pp_size: int) -> range:
@@ -270,6 +270,50 @@ def tp_sym_bytes(cfg: dict, max_rows: int, max_batch: int, n_medusa: int) -> int
     return n.value
 
 
+class EmuGroup:
+    """Host-ordered emulation group for several ranks sharing one GPU in one process
+    (sm_emu_group_create, include/specmemo.h): the ranks' exchanges run as segment launches
+    joined by CUDA events instead of device-side flag waits.  Drive each rank from its own
+    host thread (run_ranks); keep the group alive until the models are gone."""
+
+    def __init__(self, n_ranks: int):
+        self._h = ctypes.c_void_p()
+        _check(lib().sm_emu_group_create(n_ranks, ctypes.byref(self._h)))
+        self.n_ranks = n_ranks
+
+    @property
+    def handle(self) -> int:
+        return self._h.value
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value and _lib is not None:
+            _lib.sm_emu_group_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+
+def run_ranks(fns: list) -> list:
+    """Run fns[r]() on one host thread per rank (the emulation contract: an exchange blocks its
+    rank's thread until the peers have published) and return their results; re-raises the first
+    exception after every thread has finished."""
+    import threading
+    res, err = [None] * len(fns), [None] * len(fns)
+
+    def body(r):
+        try:
+            res[r] = fns[r]()
+        except BaseException as e:  # noqa: BLE001 -- re-raised below
+            err[r] = e
+    th = [threading.Thread(target=body, args=(r,)) for r in range(len(fns))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for e in err:
+        if e is not None:
+            raise e
+    return res
+
+
 def ipc_handle(t) -> bytes:
     h = (ctypes.c_ubyte * 64)()
     _check(lib().sm_ipc_get_handle(ctypes.c_void_p(_ptr(t)), h))
@@ -369,7 +413,7 @@ class Model:
     be constructed before any rank issues work."""
 
     def __init__(self, cfg: dict, weights: dict, max_rows: int, max_batch: int, max_seq_len: int,
-                 peer_sym: list | None = None, dtype: str = "bf16"):
+                 peer_sym: list | None = None, dtype: str = "bf16", emu_group: "EmuGroup | None" = None):
         c = ModelCfg(cfg["n_layers"], cfg["d_model"], cfg["n_heads"], cfg["n_kv_heads"], cfg["head_dim"],
                      cfg["d_ffn"], cfg["vocab"], len(weights["medusa"]), cfg.get("rms_eps", 1e-5),
                      cfg.get("rope_theta", 1e4), max_rows, max_batch, max_seq_len, DTYPES[dtype])
@@ -398,6 +442,9 @@ class Model:
             dist.pp_rank, dist.pp_size = pp_rank, pp_size
             for q, p in enumerate(peer_sym):
                 dist.peer_sym[q] = p
+            if emu_group is not None:
+                dist.emu_group = emu_group.handle
+                self._emu = emu_group  # the group outlives this model
         _check(lib().sm_model_create(ctypes.byref(c), ctypes.byref(w), ctypes.byref(dist) if dist else None,
                                      ctypes.byref(self._h)))
 

@@ -275,19 +275,56 @@ __global__ void __launch_bounds__(kNormThreads) resid_norm_tp_kernel(PartialView
     }
     __syncthreads();
   };
+  // host-ordered emulation (tp.phase >= 1): segment 1 = publish this rank's slice, RSAG segment 2 =
+  // the owner's sub-chunk sum; the last segment (2, RSAG 3) = gather + residual + norm.  Each
+  // segment is its own launch, the host orders the ranks' segments with events (emu_exchange).
+  const int ph = tp.phase;
+  if (ph == 1 || (RSAG && ph == 2)) {
+    for (int m = blockIdx.y; m < M; m += gridDim.y) {
+      if (i >= d) continue;
+      float4 *own = reinterpret_cast<float4 *>(tp.data[tp.rank] + (size_t)m * d + i);
+      if (ph == 1) {
+        float4 ys[16];
+        const SkRef ref = sk_ref(pv, 0, m, i);
+        sk_load<16>(ref, ys);
+        __stcg(own, sk_reduce<16>(ref, ys));
+      } else if (own_j == tp.rank) {  // every rank's slice is published: sum sub-chunk own_j in rank order
+        float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int r = 0; r < kMaxTP; ++r) {
+          if (r < tp.t) {
+            const float4 v = __ldcv(reinterpret_cast<const float4 *>(tp.data[r] + (size_t)m * d + i));
+            sum.x += v.x;
+            sum.y += v.y;
+            sum.z += v.z;
+            sum.w += v.w;
+          }
+        }
+        __stcg(own, sum);
+      }
+    }
+    cluster_wait();  // complete the start barrier phase
+    return;
+  }
   for (int m = blockIdx.y; m < M; m += gridDim.y, ++it) {
     float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (i < d) {
-      float4 ys[16];
-      const SkRef ref = sk_ref(pv, 0, m, i);
-      sk_load<16>(ref, ys);
-      y = sk_reduce<16>(ref, ys);
-      __stcg(reinterpret_cast<float4 *>(tp.data[tp.rank] + (size_t)m * d + i), y);
-    }
     const int idx = m * cs + crank;
-    signal_wait(idx, ep - 1);
+    if (ph == 0) {
+      if (i < d) {
+        float4 ys[16];
+        const SkRef ref = sk_ref(pv, 0, m, i);
+        sk_load<16>(ref, ys);
+        y = sk_reduce<16>(ref, ys);
+        __stcg(reinterpret_cast<float4 *>(tp.data[tp.rank] + (size_t)m * d + i), y);
+      }
+      signal_wait(idx, ep - 1);
+    } else if (!RSAG && i < d) {  // emulation: this rank's slice as published in segment 1 (bitwise y)
+      y = __ldcv(reinterpret_cast<const float4 *>(tp.data[tp.rank] + (size_t)m * d + i));
+    }
     float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (!RSAG || own_j == tp.rank) {  // sum this sub-chunk (one-shot: the whole slice) in rank order
+    if (RSAG && ph != 0) {  // emulation: every sub-chunk (the own one too) from its owner's slot
+      if (i < d) sum = __ldcv(reinterpret_cast<const float4 *>(tp.data[own_j] + (size_t)m * d + i));
+    } else if (!RSAG || own_j == tp.rank) {  // sum this sub-chunk (one-shot: the whole slice) in rank order
       if (i < d) {
         float4 part[kMaxTP];
 #pragma unroll
@@ -306,7 +343,7 @@ __global__ void __launch_bounds__(kNormThreads) resid_norm_tp_kernel(PartialView
         if (RSAG) __stcg(reinterpret_cast<float4 *>(tp.data[tp.rank] + (size_t)m * d + i), sum);
       }
     }
-    if (RSAG) {
+    if (RSAG && ph == 0) {
       signal_wait(idx, ep);
       if (own_j != tp.rank && i < d)  // gather the owner's reduced sub-chunk
         sum = __ldcv(reinterpret_cast<const float4 *>(tp.data[own_j] + (size_t)m * d + i));
@@ -349,11 +386,23 @@ cudaError_t resid_norm_tp_launch(const PartialView &pv, float *x, const bf16 *g,
   if (cs > 8 || d % 4 || M * cs > kTpFlagSlots) return cudaErrorInvalidValue;
   const int rows_par = M < 64 ? M : 64;  // cs x 64 CTAs: always co-resident
   const bool rsag = g_tp_rsag < 0 ? tp.t >= 4 : g_tp_rsag != 0;
-  if (rsag)
-    return launch_pdl_cluster(resid_norm_tp_kernel<true>, dim3(cs, rows_par), dim3(kNormThreads), 0, st, cs, pv, x, g,
-                              h, M, d, eps, tp, rs_out);
-  return launch_pdl_cluster(resid_norm_tp_kernel<false>, dim3(cs, rows_par), dim3(kNormThreads), 0, st, cs, pv, x, g, h,
-                            M, d, eps, tp, rs_out);
+  auto launch = [&](const TpArgs &a) {
+    if (rsag)
+      return launch_pdl_cluster(resid_norm_tp_kernel<true>, dim3(cs, rows_par), dim3(kNormThreads), 0, st, cs, pv, x,
+                                g, h, M, d, eps, a, rs_out);
+    return launch_pdl_cluster(resid_norm_tp_kernel<false>, dim3(cs, rows_par), dim3(kNormThreads), 0, st, cs, pv, x, g,
+                              h, M, d, eps, a, rs_out);
+  };
+  if (!tp.emu) return launch(tp);
+  // host-ordered emulation: segment launches separated by event joins over all ranks
+  TpArgs a = tp;
+  const int segs = rsag ? 3 : 2;
+  for (a.phase = 1; a.phase <= segs; ++a.phase) {
+    cudaError_t e = launch(a);
+    if (e == cudaSuccess && a.phase < segs) e = emu_exchange(a, a.phase - 1, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 // ------------------------------------------------------------------ QKV consumer (RoPE + cache write)

@@ -478,7 +478,24 @@ struct TpArgs {
   const long long *seq;           // this rank's epoch base (device)
   int point;                      // exchange index within the current top-level call
   int *err;                       // set to 1 when a wait times out
+  // Host-ordered emulation (several ranks on one GPU; guide: kernels that wait on one another must
+  // not run as separate launches there).  phase 0 = the fused kernel with flag waits; phase p >= 1 =
+  // only segment p of it, no flag wait: the launch function orders the segments of all ranks with
+  // CUDA events (emu_publish / emu_wait) between launches instead.
+  int phase;
+  void *emu;                      // host only: EmuGroup of the ranks (nullptr = real multi-GPU)
+  long long gen;                  // host only: this exchange's generation (monotone per rank)
 };
+// Host-ordered exchange emulation: rank `rank` of the group records "segment `sub` of exchange gen
+// done" on st (emu_publish); emu_wait makes st wait for rank q's record of the same (gen, sub).
+// emu_wait blocks the calling host thread until rank q has published (each rank is driven by its
+// own host thread), ~60 s at most (then cudaErrorTimeout).
+struct EmuGroup;
+EmuGroup *emu_group_create(int t);
+void emu_group_destroy(EmuGroup *g);
+cudaError_t emu_publish(const TpArgs &tp, int sub, cudaStream_t st);
+cudaError_t emu_wait(const TpArgs &tp, int q, int sub, cudaStream_t st);
+cudaError_t emu_exchange(const TpArgs &tp, int sub, cudaStream_t st);  // publish, then wait for every peer
 // Residual all-reduce fused into residual + RMSNorm (pv = this rank's o_proj / down partials).
 void tp_set_rsag(int mode);  // -1 auto (t >= 4), 0 one-shot, 1 reduce-scatter + all-gather
 cudaError_t resid_norm_tp_launch(const PartialView &pv, float *x, const bf16 *g, bf16 *h, int M, int d, float eps,

@@ -515,6 +515,8 @@ struct sm_model {
   long long *tp_seq = nullptr;   // device epoch base
   int *tp_err = nullptr;         // device: a wait timed out
   int tp_point = 0;              // host: exchange index within the current top-level call
+  EmuGroup *emu = nullptr;       // host-ordered emulation group (several ranks on one GPU), borrowed
+  long long emu_call = 0;        // host: top-level calls with exchanges so far (same on every rank)
   float *amax = nullptr, *cand = nullptr, *tk_val = nullptr;
   int32_t *tk_idx = nullptr;
   float *lean_part = nullptr;  // stream-K K1 partial slots (bf16 path, head_dim 128)
@@ -545,6 +547,8 @@ static TpArgs tp_next(sm_model *m) {
   a.seq = m->tp_seq;
   a.point = pt;
   a.err = m->tp_err;
+  a.emu = m->emu;
+  a.gen = (m->emu_call << 16) + pt;
   return a;
 }
 static void tp_begin(sm_model *m) { m->tp_point = 0; }
@@ -562,6 +566,8 @@ static TpArgs pp_args(sm_model *m, int point) {
   a.seq = m->tp_seq;
   a.point = point;
   a.err = m->tp_err;
+  a.emu = m->emu;
+  a.gen = (m->emu_call << 16) + point;
   return a;
 }
 // Advance the epoch base past this call's exchanges (kept even, so the data slot
@@ -570,6 +576,7 @@ static sm_status tp_end(sm_model *m, cudaStream_t st, int &nl) {
   if ((m->tp > 1 || m->pp > 1) && m->tp_point > 0) {
     CK(tp_advance_launch(m->tp_seq, (m->tp_point + 1) & ~1, st));
     ++nl;
+    ++m->emu_call;
   }
   m->tp_point = 0;
   return SM_OK;
@@ -698,6 +705,7 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
   m->cfg = c;
   m->tp = tp;
   m->tp_rank = tp_rank;
+  m->emu = (tp > 1 || pp > 1) ? static_cast<EmuGroup *>(dist->emu_group) : nullptr;
   m->pp = pp;
   m->pp_rank = pp_rank;
   m->L = c.n_layers / pp;  // this rank's layers
@@ -918,6 +926,14 @@ extern "C" sm_status sm_generate_bf16_2d(void *dst, int rows, int cols, int full
 }
 
 // ---------------------------------------------------------------- tensor parallel plumbing
+extern "C" sm_status sm_emu_group_create(int n_ranks, void **group) {
+  if (!group || n_ranks < 2 || n_ranks > kMaxTP) return fail(SM_ERR_INVALID_ARG, "sm_emu_group_create: 2..8 ranks");
+  *group = emu_group_create(n_ranks);
+  if (!*group) return fail(SM_ERR_CUDA, "sm_emu_group_create: event creation failed");
+  return SM_OK;
+}
+extern "C" void sm_emu_group_destroy(void *group) { emu_group_destroy(static_cast<EmuGroup *>(group)); }
+
 extern "C" sm_status sm_tp_sym_bytes(const sm_model_cfg *cfg, size_t *bytes) {
   if (!cfg || !bytes || cfg->max_rows < 1 || cfg->d_model < 1 || cfg->max_batch < 1)
     return fail(SM_ERR_INVALID_ARG, "sm_tp_sym_bytes: bad arguments");
@@ -1710,6 +1726,12 @@ extern "C" sm_status sm_step(sm_model *m, sm_kv *kv, const sm_accept_cfg *cfg, c
   GraphKey key{g_opt_version, kv->prof, (int)cfg->mode, cfg->temperature, cfg->eps, cfg->alpha, cfg->d_max_new, cfg->d_forced_path,
                out->acc_len, out->best_leaf, out->path, out->emit_tok, out->n_emit, out->status};
   auto it = kv->graphs.find(key);
+  if (m->emu) {  // host-ordered emulation: the exchanges join the ranks' streams from their host threads
+    int nl = 0;
+    CKS(enqueue_step(m, kv, cfg, out, st, nl));
+    kv->last_stream = st;
+    return SM_OK;
+  }
   if (it == kv->graphs.end()) {
     cudaStreamCaptureStatus cs;
     CK(cudaStreamIsCapturing(st, &cs));

@@ -3,10 +3,10 @@ import sys
 
 import pytest
 
-# The single-GPU tensor-parallel emulation (tests/test_gpu_tp.py) runs t <= 8 ranks on t streams
-# whose exchange kernels spin on each other's flags: every stream needs its own hardware work
-# queue, or a spinning kernel blocks a peer's kernel queued behind it on a shared queue (the
-# default is 8 queues, shared with torch's own streams).  Must be set before CUDA initialises.
+# The single-GPU tensor-parallel / pipeline emulation runs t <= 8 ranks on t streams (host-ordered:
+# no kernel waits on another rank's launch).  One hardware work queue per stream keeps a rank's
+# queued launches from serialising behind a peer's (the default is 8 queues, shared with torch's
+# own streams).  Must be set before CUDA initialises.
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

@@ -4,8 +4,10 @@
 all available GPUs, with each GPU also hosting the corresponding slices of the KV cache alongside
 the layers".  pp ranks = pp sm_models in one process on one device, rank r holding layers
 [r L/pp, (r+1) L/pp) and their KV slices; the residual rows move between stages through the
-symmetric buffers (the same kernels and flag protocol as across GPUs, where the peer pointers come
-from CUDA IPC).  The split changes no arithmetic, so every rank must produce the pp = 1 results
+symmetric buffers (the same kernels and data layout as across GPUs, where the peer pointers come
+from CUDA IPC).  On one GPU no kernel may spin on a hand-off another rank's launch raises, so the
+stages share an EmuGroup (host-ordered emulation, include/specmemo.h): a receiver's stream waits
+for the sender's "published" event, each stage driven by its own host thread.  The split changes no arithmetic, so every rank must produce the pp = 1 results
 bit for bit -- logits, tree tokens, emitted tokens, the K/V of its layers -- and the greedy stream
 must equal the oracle's (= vanilla greedy) on the screened seeds."""
 import numpy as np
@@ -30,15 +32,6 @@ def sm():
 X = 96
 
 
-@pytest.fixture(autouse=True)
-def _no_pdl(sm):
-    """Programmatic dependent launch off (conftest restores the defaults after each test): with the
-    stages sharing one GPU, a stage spinning on its hand-off would let its PDL-launched successors
-    (persistent GEMMs, two CTAs per SM) take every SM before the stage it waits for has run -- on
-    separate GPUs that cannot happen (tools/pp_probe.py: pp = 2 times out with PDL, passes without)."""
-    sm.set_option("pdl", 0)
-
-
 class Stages:
     def __init__(self, sm, cfg, pp, seed, choices=synth.TINY16, batch=1, n_medusa=3):
         self.sm, self.pp = sm, pp
@@ -47,17 +40,22 @@ class Stages:
         self.sym = [torch.zeros(sm.tp_sym_bytes(cfg, R, batch, n_medusa), dtype=torch.uint8, device="cuda")
                     for _ in range(pp)] if pp > 1 else None
         ptrs = [s.data_ptr() for s in self.sym] if pp > 1 else None
+        self.emu = sm.EmuGroup(pp) if pp > 1 else None
         self.W = [sm.allocate_weights(cfg, n_medusa, seed=seed, pp_rank=r, pp_size=pp) for r in range(pp)]
-        self.models = [sm.Model(cfg, self.W[r], R, batch, X + self.tree.N, peer_sym=ptrs) for r in range(pp)]
+        self.models = [sm.Model(cfg, self.W[r], R, batch, X + self.tree.N, peer_sym=ptrs, emu_group=self.emu)
+                       for r in range(pp)]
         self.kvs = [sm.KVCache(m, self.tree, batch, X) for m in self.models]
         self.streams = [torch.cuda.Stream() for _ in range(pp)]
         self.outs = [sm.AcceptOut(batch, self.tree.depth) for _ in range(pp)]
         torch.cuda.synchronize()
 
     def each(self, fn):
-        for r in range(self.pp):
-            with torch.cuda.stream(self.streams[r]):
-                fn(r, self.kvs[r], self.streams[r])
+        def run(r):
+            def go():
+                with torch.cuda.stream(self.streams[r]):
+                    fn(r, self.kvs[r], self.streams[r])
+            return go
+        self.sm.run_ranks([run(r) for r in range(self.pp)])  # one host thread per stage
         for s in self.streams:
             s.synchronize()
 

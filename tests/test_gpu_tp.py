@@ -2,11 +2,16 @@
 
 t ranks = t sm_models in one process on the same device, each holding its shard
 (allocate_weights(tp_rank, tp_size)) and exchanging through the other ranks'
-symmetric buffers -- the same kernels and flag protocol a multi-GPU run uses
-over NVLink peer memory (there the peer pointers come from CUDA IPC).  Each
-rank's work runs on its own stream; programmatic dependent launch is disabled
-here because ranks sharing one GPU could otherwise hold each other's SMs while
-spinning (on separate GPUs that cannot happen).
+symmetric buffers -- the same kernels and data layout a multi-GPU run uses over
+NVLink peer memory (there the peer pointers come from CUDA IPC).  On one GPU no
+kernel may spin on a flag another rank's launch raises (nothing guarantees the
+two run at the same time; B200_PROFILING.md), so the ranks share an EmuGroup:
+every exchange runs as segment launches (publish; [reduce-scatter;] merge) and
+each rank's host thread joins its stream to its peers' "published" events
+between segments (host-ordered emulation, include/specmemo.h).  The arithmetic
+and the rank-order sums are those of the fused flag protocol, so the results
+are the same bits.  Programmatic dependent launch stays on (the default): with
+no device-side waits a rank's early-launched successors can only delay a peer.
 
 Parity: the tp run must emit the oracle's greedy tokens on the screened seeds
 (the same bar as tp = 1), and its vocabulary-parallel logits, concatenated over
@@ -33,15 +38,10 @@ def sm():
     return sm
 
 
-@pytest.fixture(autouse=True)
-def _no_pdl(sm):
-    """Every test of this module runs with PDL off (conftest restores the defaults after each)."""
-    sm.set_option("pdl", 0)
-
-
 class Ranks:
-    """t ranks in one process: all on the current GPU (the emulation), or rank r on GPU devices[r]
-    with peer access between every pair (the real placement, one GPU per rank)."""
+    """t ranks in one process: all on the current GPU (host-ordered emulation, one host thread per
+    rank), or rank r on GPU devices[r] with peer access between every pair (the real placement,
+    one GPU per rank, fused flag protocol)."""
 
     def __init__(self, sm, t, seed=0, n_medusa=3, choices=synth.TINY16, batch=1, medusa_init=False, cfg=CFG,
                  devices=None):
@@ -56,6 +56,7 @@ class Ranks:
         R = max(batch * self.tree.N, 64)
         nbytes = sm.tp_sym_bytes(cfg, R, batch, n_medusa)
         self.sym, self.W, self.models, self.kvs, self.streams, self.outs = [], [], [], [], [], []
+        self.emu = sm.EmuGroup(t) if len(set(self.dev)) < t else None
         for r in range(t):
             with torch.cuda.device(self.dev[r]):
                 self.sym.append(torch.zeros(nbytes, dtype=torch.uint8, device="cuda"))
@@ -64,7 +65,8 @@ class Ranks:
             with torch.cuda.device(self.dev[r]):
                 self.W.append(sm.allocate_weights(cfg, n_medusa, seed=seed, medusa_init=medusa_init, tp_rank=r,
                                                   tp_size=t))
-                self.models.append(sm.Model(cfg, self.W[r], R, batch, X + self.tree.N, peer_sym=ptrs))
+                self.models.append(sm.Model(cfg, self.W[r], R, batch, X + self.tree.N, peer_sym=ptrs,
+                                            emu_group=self.emu))
                 self.kvs.append(sm.KVCache(self.models[r], self.tree, batch, X))
                 self.streams.append(torch.cuda.Stream())
                 self.outs.append(sm.AcceptOut(batch, self.tree.depth))
@@ -72,9 +74,16 @@ class Ranks:
             torch.cuda.synchronize(d)
 
     def each(self, fn):
-        for r in range(self.t):
-            with torch.cuda.device(self.dev[r]), torch.cuda.stream(self.streams[r]):
-                fn(r, self.kvs[r], self.streams[r])
+        def run(r):
+            def go():
+                with torch.cuda.device(self.dev[r]), torch.cuda.stream(self.streams[r]):
+                    fn(r, self.kvs[r], self.streams[r])
+            return go
+        if self.emu is not None:  # one host thread per rank: an exchange blocks until the peers published
+            self.sm.run_ranks([run(r) for r in range(self.t)])
+        else:
+            for r in range(self.t):
+                run(r)()
         for s in self.streams:
             s.synchronize()
 
@@ -209,18 +218,18 @@ def _greedy_ref(cfg, seed, n):
     return prompt, ref
 
 
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 8,
-                    reason="t = 8 runs one rank per GPU: emulated on one GPU (8 streams) the verify's residual "
-                           "exchanges time out (DESIGN.md 4.5); t = 2, 4 are emulated above")
-@pytest.mark.parametrize("pdl", [1, 0], ids=["pdl", "nopdl"])
+@pytest.mark.parametrize("rsag", [-1, 0], ids=["rsag", "oneshot"])
 @pytest.mark.parametrize("seed", [0, 2])
-def test_tp8_greedy_tokens_equal_oracle(sm, seed, pdl):
-    """t = 8 ranks, one per GPU (peer access between every pair), with and without programmatic
-    dependent launch: every rank emits the oracle's greedy stream (= vanilla greedy)."""
-    sm.set_option("pdl", pdl)
+def test_tp8_greedy_tokens_equal_oracle(sm, seed, rsag):
+    """t = 8 ranks (the 70B shape's TP8 placement: one kv head per rank), one per GPU when the box
+    has 8 (fused flag protocol over peer memory), else host-ordered emulation on one GPU; residual
+    exchange as reduce-scatter + all-gather (the t >= 4 default) and as the one-shot sum: every
+    rank emits the oracle's greedy stream (= vanilla greedy)."""
+    sm.set_option("tp_rsag", rsag)
+    devices = list(range(8)) if torch.cuda.device_count() >= 8 else None
     t, n = 8, 24
     prompt, ref = _greedy_ref(CFG8, seed, n)
-    rk = Ranks(sm, t, seed=seed, cfg=CFG8, devices=list(range(8)))
+    rk = Ranks(sm, t, seed=seed, cfg=CFG8, devices=devices)
     pts = [torch.from_numpy(prompt).to(f"cuda:{d}") for d in rk.dev]
     rk.each(lambda r, kv, st: kv.prefill(0, pts[r], stream=st))
     budgets = [torch.full((1,), n, dtype=torch.int32, device=f"cuda:{d}") for d in rk.dev]

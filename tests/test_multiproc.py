@@ -122,8 +122,14 @@ def test_pipeline_layer_partition_gloo():
 
 
 def test_dist_struct_matches_header():
-    """sm_dist in include/specmemo.h: pp_rank / pp_size follow peer_sym[SM_MAX_TP]."""
+    """sm_dist in include/specmemo.h: pp_rank / pp_size follow peer_sym[SM_MAX_TP], then emu_group."""
     import ctypes
 
     import paper_2506_01986_b200 as sm
-    assert sm.Dist.pp_rank.offset == 8 + 8 * sm.MAX_TP and ctypes.sizeof(sm.Dist) == 8 + 8 * sm.MAX_TP + 8
+    assert sm.Dist.pp_rank.offset == 8 + 8 * sm.MAX_TP
+    assert sm.Dist.emu_group.offset == 16 + 8 * sm.MAX_TP and ctypes.sizeof(sm.Dist) == 16 + 8 * sm.MAX_TP + 8
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include",
+                            "specmemo.h")).read()
+    body = hdr[hdr.index("typedef struct {\n  int tp_rank, tp_size;"):hdr.index("} sm_dist;")]
+    assert [ln.split()[1].rstrip(";").split("[")[0].lstrip("*") for ln in body.splitlines()[1:] if ln.strip()] == \
+        ["tp_rank,", "peer_sym", "pp_rank,", "emu_group"]

@@ -1,7 +1,8 @@
 """One small speculative decode for compute-sanitizer (tools/sanitize.sh): c1 = the tiny
 C1 model (mma.sync K1, hd 16); s128 = a hd-128 model (tcgen05 K1 with split-KV cluster
 combine, tcgen05 K2, 2 sequences, prefill + 6 greedy steps with compaction); pp2 = the
-layer-split pipeline (two stages on one GPU, residual hand-offs, PDL off); pad = s128 in pad
+layer-split pipeline (two stages on one GPU, host-ordered emulation: residual hand-offs joined by
+events, one host thread per stage); pad = s128 in pad
 batching through sm_propose / sm_verify / sm_accept (pad masks, the copy kernels)."""
 import os
 import sys
@@ -14,13 +15,13 @@ import synth  # noqa: E402
 
 case = sys.argv[1]
 if case == "pp2":
-    sm.set_option("pdl", 0)
     cfg, X = synth.model_cfg("tiny", n_layers=4), 96
     tree = sm.Tree(synth.TINY16, topk=10)
     sym = [torch.zeros(sm.tp_sym_bytes(cfg, 64, 1, 3), dtype=torch.uint8, device="cuda") for _ in range(2)]
     ptrs = [t.data_ptr() for t in sym]
     Ws = [sm.allocate_weights(cfg, 3, seed=1, pp_rank=r, pp_size=2) for r in range(2)]
-    models = [sm.Model(cfg, Ws[r], 64, 1, X + tree.N, peer_sym=ptrs) for r in range(2)]
+    emu = sm.EmuGroup(2)
+    models = [sm.Model(cfg, Ws[r], 64, 1, X + tree.N, peer_sym=ptrs, emu_group=emu) for r in range(2)]
     kvs = [sm.KVCache(m, tree, 1, X) for m in models]
     sts = [torch.cuda.Stream() for _ in range(2)]
     outs = [sm.AcceptOut(1, tree.depth) for _ in range(2)]
@@ -28,9 +29,12 @@ if case == "pp2":
     pt = torch.from_numpy(synth.prompt_tokens(1, 0, 32, cfg["vocab"])).cuda()
 
     def each(fn):
-        for r in range(2):
-            with torch.cuda.stream(sts[r]):
-                fn(r, sts[r])
+        def go(r):
+            def body():
+                with torch.cuda.stream(sts[r]):
+                    fn(r, sts[r])
+            return body
+        sm.run_ranks([go(r) for r in range(2)])
         torch.cuda.synchronize()
     each(lambda r, s: kvs[r].prefill(0, pt, stream=s))
     for _ in range(4):
