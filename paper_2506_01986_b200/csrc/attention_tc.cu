@@ -586,6 +586,35 @@ static_assert(SMEM <= 232448, "K1 (KS) shared memory");
 constexpr int OFF_PART = 80 * 1024;        // [ROWS][HD] fp32 (copy f of row r at f RP + r) + [ROWS] (m, l)
 }  // namespace ks
 
+#ifdef SM_TRACE
+// diagnostics build: per-CTA %globaltimer stamps of the row-copy kernel, by linear CTA index:
+// [smid, entry, Q staged (MMA sees q_full), first K/V tile landed, last PV retired, exit, partials
+// staged, copies merged]
+constexpr int kKsTr = 8192;
+static __device__ long long g_ks_tr[kKsTr][8];
+#define KS_TR(slot, v) do { if (ks_lin < kKsTr) g_ks_tr[ks_lin][slot] = (v); } while (0)
+extern "C" int sm_trace_read_ks(long long *dst, int n) {
+  return (int)cudaMemcpyFromSymbol(dst, g_ks_tr, sizeof(long long) * 8 * (size_t)min(n, kKsTr));
+}
+#else
+#define KS_TR(slot, v) do { } while (0)
+#endif
+
+// K and V rows [p0, p1) of (seq, kv head h) -> L2 (bulk prefetch, 64 KB pieces): a hint that lets a
+// CTA's whole key range stream at HBM rate while the ring holds only STAGES tiles
+SM_DEV void ks_prefetch_l2(const AttnArgs &a, int seq, int h, int p0, int p1) {
+  if (p1 <= p0) return;
+  const long long r0 = (long long)seq * a.seq_rows + (long long)h * a.cap + p0;
+  const char *kb = reinterpret_cast<const char *>(a.k_base + (a.k_row0 + r0) * ks::HD);
+  const char *vb = reinterpret_cast<const char *>(a.v_base + (a.v_row0 + r0) * ks::HD);
+  const long long bytes = (long long)(p1 - p0) * ks::HD * 2;
+  for (long long off = 0; off < bytes; off += 65536) {
+    const uint32_t n = (uint32_t)min(65536ll, bytes - off);
+    prefetch_l2_bulk(kb + off, n);
+    prefetch_l2_bulk(vb + off, n);
+  }
+}
+
 template <int F, int KEYS>
 __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_constant__ AttnArgs a) {
   constexpr int HD = ks::HD, ROWS = ks::ROWS, STAGES = ks::Cfg<KEYS>::STAGES;
@@ -609,6 +638,15 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
   uint32_t *tslot = reinterpret_cast<uint32_t *>(q_full + 1);
 
   pdl_trigger();
+#ifdef SM_TRACE
+  const long long ks_lin = blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z);
+  if (threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    KS_TR(0, smid);
+    KS_TR(1, gtime());
+  }
+#endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int split = blockIdx.x;
   const int row0 = F == 1 ? blockIdx.y * ROWS : 0;  // query rows of this block (several blocks only with F = 1)
@@ -657,6 +695,8 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
     mbar_init(q_full, 128);
     fence_barrier_init();
     while (pre < first && key0 + (pre + 1) * KEYS <= Lc) issue(pre++);
+    if (a.l2_ahead & 1)  // the rest of this CTA's cached prefix -> L2 now (the ring then refills from L2)
+      ks_prefetch_l2(a, seq, h, key0 + first * KEYS, min(key1, Lc));
   }
   // softmax threads: copy f of query row r; the ancestor words of its node
   const int rr_lane = (warp < 4) ? warp * 32 + lane : 0;
@@ -686,6 +726,26 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
         issue(i);
       }
     }
+    __syncwarp();
+    if (a.l2_ahead & 2) {  // Q rows and the first ring's worth of K/V of the CTA one wave later -> L2
+      const long long lin = blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z);
+      const long long nx = lin + kNumSMs;  // 1 CTA per SM: roughly the CTA that takes this SM next
+      const long long per_z = (long long)gridDim.x * gridDim.y;
+      if (nx < per_z * gridDim.z) {
+        const int nz = (int)(nx / per_z), nsplit_i = (int)(nx % gridDim.x), nrb = (int)((nx / gridDim.x) % gridDim.y);
+        const int nsl = nz / a.Hkv, nh = nz % a.Hkv, nseq = a.seq_base + nsl;
+        if (lane == 0) {
+          const int nLc = a.len[nseq], nT = nLc + a.Nq;
+          const int nchunk = ((nT + a.nsplit - 1) / a.nsplit + KEYS - 1) / KEYS * KEYS;
+          const int nk0 = min(nT, nsplit_i * nchunk), nk1 = min(nT, nk0 + nchunk);
+          ks_prefetch_l2(a, nseq, nh, nk0, min(min(nk1, nLc), nk0 + STAGES * KEYS));
+        }
+        // its query rows: nodes of row block nrb, G heads (contiguous) each
+        const int r0 = F == 1 ? nrb * ROWS : 0, r1 = min(R, r0 + (F == 1 ? ROWS : RP));
+        for (int n = r0 / a.G + lane; n * a.G < r1; n += 32)
+          prefetch_l2_bulk(a.q + (((long long)nsl * a.Nq + n) * a.H + (long long)nh * a.G) * HD, a.G * HD * 2);
+      }
+    }
   } else if (warp == 5) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0 && ntiles > 0) {
@@ -693,9 +753,11 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
       constexpr uint32_t idesc_o = idesc_bf16_major(ROWS, HD, 0, 1);    // P (TMEM) x V (MN-major)
       const uint32_t q_u = smem_u32(sQ), kv_u = smem_u32(sKV);
       mbar_wait(q_full, 0);
+      KS_TR(2, gtime());
       auto issue_s = [&](int i) {
         const int sb = i & 1, st = i % STAGES;
         mbar_wait(&kv_full[st], (i / STAGES) & 1);
+        if (i == 0) KS_TR(3, gtime());
         tc_fence_after();
         const uint32_t kb = kv_u + st * 2 * TILE;
 #pragma unroll
@@ -854,6 +916,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
       mbar_wait(&o_done[(ntiles - 1) & 1], ((ntiles - 1) >> 1) & 1);
       tc_fence_after();
     }
+    if (threadIdx.x == 0) KS_TR(4, gtime());
     // ---- stage this copy's (m, l, O) at MMA row r (ring idle: every MMA and load is complete)
     float *spart = reinterpret_cast<float *>(sKV + ks::OFF_PART);  // [ROWS][HD]
     float *spml = spart + ROWS * HD;                                // [ROWS][2]
@@ -875,6 +938,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
               make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
       }
     }
+    if (threadIdx.x == 0) KS_TR(6, gtime());
     asm volatile("bar.sync 1, 128;" ::: "memory");  // the four softmax warps
     // ---- merge the F copies of query row qr (copy order), threads of copy 0 only
     if (cf == 0 && live) {
@@ -925,6 +989,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
     }
   }
 
+  if (threadIdx.x == 0) KS_TR(7, gtime());
   if (a.nsplit > 1) {
     // split-KV combine over DSMEM (pull), as tree_attn_tc_kernel: rank q owns live rows
     // [q rows_per, (q+1) rows_per) and reads only live rows
@@ -1000,6 +1065,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (threadIdx.x == 0) KS_TR(5, gtime());
   if (warp == 5) tmem_dealloc<TCOLS>(tmem);
 }
 
@@ -1545,6 +1611,12 @@ int attention_tc_nsplit(int units) {  // 1 CTA per SM: aim for ~one wave of 148
   return ns;
 }
 
+// sm_set_option("attn_l2ahead"), AttnArgs::l2_ahead.  Default 2: the next wave's first ring and Q rows go
+// to L2 once a CTA has issued its last tile (profiles/r02/k1_experiments.txt: 3-5 % on multi-wave launches,
+// neutral elsewhere); bit 0 (the CTA's own range at entry) measured 5-40 % slower (it floods the
+// memory system ahead of the ring's own loads) and stays off
+static int g_attn_l2ahead = 2;
+void attention_set_l2ahead(int mode) { g_attn_l2ahead = mode & 3; }
 static int g_attn_ks = 2;  // sm_set_option("attn_ks"): 128-key-tile kernel on long key ranges, all N G (2, default), N G <= 64 (1), off (0)
 void attention_set_ks(int on) { g_attn_ks = on; }
 
@@ -1588,9 +1660,11 @@ cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
       ks_attr = true;
     }
     cfg.dynamicSmemBytes = ks::SMEM;
-    if (R <= 32) return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<4, 128>, a);
-    if (R <= 64) return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<2, 128>, a);
-    return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<1, 128>, a);  // ceil(R / 128) row blocks (grid y)
+    AttnArgs b = a;
+    b.l2_ahead = (a.k_base && a.v_base) ? g_attn_l2ahead : 0;
+    if (R <= 32) return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<4, 128>, b);
+    if (R <= 64) return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<2, 128>, b);
+    return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<1, 128>, b);  // ceil(R / 128) row blocks (grid y)
   }
   if (a.causal) return cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<true>, a);
   return cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<false>, a);

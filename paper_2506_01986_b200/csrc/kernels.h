@@ -357,6 +357,11 @@ struct AttnArgs {
   float *lean_part;
   int *lean_sync;
   int lean_min_tiles;
+  // raw K / V bases of tmK / tmV (tmap row r = base + r hd elements) for L2 prefetch ahead of the
+  // TMA ring (K1 row-copy kernel): l2_ahead bit 0 = this CTA's own key range past the ring, bit 1 =
+  // the first ring's worth of the CTA one wave later (set by attention_tc_launch from the option)
+  const bf16 *k_base, *v_base;
+  int l2_ahead;
 };
 cudaError_t attention_launch(const AttnArgs &a, int head_dim, cudaStream_t st);
 int attention_row_blocks(int Nq, int G, int head_dim);
@@ -371,6 +376,7 @@ cudaError_t attention_lean_launch(const AttnArgs &a, cudaStream_t st);
 size_t attention_lean_part_floats(int nunits);
 void attention_set_lean(int on);
 void attention_set_ks(int on);
+void attention_set_l2ahead(int mode);
 void attention_set_lean_div(int d);
 int attention_lean_min_tiles(int Nq, int G);
 void attention_set_splits(int n);               // experiments: force key splits (0 = auto)

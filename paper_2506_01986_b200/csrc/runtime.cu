@@ -1418,6 +1418,8 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
     aa.lean_part = m->lean_part;
     aa.lean_sync = m->lean_sync;
     aa.lean_min_tiles = attention_lean_min_tiles(Nq, m->G);
+    aa.k_base = kv->base;
+    aa.v_base = kv->base;
     aa.l2_pf = m->wo[l];  // o_proj weights stream into L2 while attention runs
     aa.l2_pf_bytes = (unsigned long long)d * m->H * m->hd * 2;
     cudaEvent_t ev = nullptr;
@@ -1868,6 +1870,8 @@ static sm_status attention_stage(const uint64_t *d_anc, int Nq, const void *d_q,
   aa.causal = d_anc == nullptr;
   aa.k_row0 = 0;
   aa.v_row0 = 0;
+  aa.k_base = (const bf16 *)d_k;
+  aa.v_base = (const bf16 *)d_v;
   aa.seq_rows = (long long)n_kv_heads * cap;
   aa.cap = cap;
   aa.Nq = Nq;
@@ -1979,6 +1983,7 @@ extern "C" sm_status sm_reset_options(void) {
   attention_set_splits(0);
   attention_set_lean(0);
   attention_set_ks(2);
+  attention_set_l2ahead(2);
   attention_set_lean_div(16);
   tp_set_rsag(-1);
   g_fused = 0;
@@ -2033,6 +2038,8 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
     tp_set_rsag(value);
   } else if (n == "attn_lean") {  // tree-mode K1 (hd 128): stream-K kernel (1, default) or cluster splits (0)
     attention_set_lean(value);
+  } else if (n == "attn_l2ahead") {  // K1 row-copy kernel: L2 prefetch ahead of the ring (bit 0 own range, bit 1 next wave)
+    attention_set_l2ahead(value);
   } else if (n == "attn_ks") {  // K1 128-key-tile (row-copy) kernel on long key ranges: 0 off, 1 N G <= 64, 2 all (default)
     attention_set_ks(value);
   } else if (n == "attn_lean_div") {  // lean K1: minimum tiles per CTA = max(2, live rows / value)

@@ -22,6 +22,9 @@ pts = [("A", 32, 32, b, N, Lc) for (b, N, Lc) in
 hd = 128
 if os.environ.get("K1_VARS") == "ks":  # 128-row kernel vs key-split row packing (N G <= 64)
     VARS = [("rows128", dict(attn_lean=0, attn_ks=0)), ("ks", dict(attn_lean=0, attn_ks=2))]
+elif os.environ.get("K1_VARS") == "l2":  # row-copy kernel: L2 prefetch ahead of the ring (attn_l2ahead bits)
+    VARS = [("ks", dict(attn_l2ahead=0)), ("own", dict(attn_l2ahead=1)), ("next", dict(attn_l2ahead=2)),
+            ("both", dict(attn_l2ahead=3))]
 else:
     VARS = None
 VARS = VARS or [("cl", dict(attn_lean=0)), ("l32", dict(attn_lean=1, attn_lean_div=32)), ("l16", dict(attn_lean=1, attn_lean_div=16)),
