@@ -1069,6 +1069,401 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
   if (warp == 5) tmem_dealloc<TCOLS>(tmem);
 }
 
+// ============================================================================ K1, persistent row-copy kernel (KSP)
+// The row-copy kernel above runs one (sequence, kv head, row block) unit per CTA.  With one key split
+// and more units than SMs (C5 b >= 8 at geometry A: 256-1024 units) every SM runs several CTAs back to
+// back, and each pays its entry (barriers, TMEM, Q and first tiles: 2.5-4 us under load) and its exit
+// (staging and merging the copies: ~2.8 us) while its ring is empty (profiles/r02/k1_experiments.txt:
+// the SMs streamed for 0.56 of the span at b 32 / Lc 1024).  Here min(units, 148) CTAs walk units
+// c, c + P, c + 2P, ...: the producer streams the key tiles of consecutive units through the same
+// 3-stage ring without a break, so the next unit's first tiles land while this unit's epilogue runs.
+// The epilogue stages the copies' O in the (then idle) Q buffer, one 64-column half at a time, and
+// frees the O accumulator as soon as it is read; the next unit's Q is staged after it.  Arithmetic,
+// copy order and merge order are the row-copy kernel's: the output is bitwise the same.
+namespace ksp {
+constexpr int HD = 128, ROWS = 128, KEYS = 128, STAGES = 3;
+constexpr int HALF = KEYS * 64 * 2, TILE = 2 * HALF;
+constexpr int OFF_Q = 0;                               // Q [128][128] bf16; epilogue: O half [128][64] fp32
+constexpr int OFF_KV = 32 * 1024;
+constexpr int OFF_BAR = OFF_KV + STAGES * 2 * TILE;    // 229376
+constexpr int OFF_ML = OFF_BAR + 256;                  // (m, l) of every MMA row [128][2] fp32
+constexpr int SMEM = OFF_ML + 1024 + 1024;
+static_assert(SMEM <= 232448, "K1 (KSP) shared memory");
+}  // namespace ksp
+
+template <int F>
+__global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_constant__ AttnArgs a, int units,
+                                                               int nrb) {
+  constexpr int HD = ksp::HD, ROWS = ksp::ROWS, KEYS = ksp::KEYS, STAGES = ksp::STAGES;
+  constexpr int HALF = ksp::HALF, TILE = ksp::TILE;
+  constexpr int TCOLS = 512;        // S0, S1 (128 columns each), O (128)
+  constexpr int RP = ROWS / F;      // rows per copy
+  constexpr int KT = KEYS / F;      // keys per thread per tile
+  static_assert(F == 1 || F == 2 || F == 4, "copies");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sQ = smem + ksp::OFF_Q;
+  uint8_t *sKV = smem + ksp::OFF_KV;
+  uint64_t *kv_full = reinterpret_cast<uint64_t *>(smem + ksp::OFF_BAR);
+  uint64_t *kv_empty = kv_full + STAGES;
+  uint64_t *s_full = kv_empty + STAGES;  // [2]
+  uint64_t *p_full = s_full + 2;         // [2]
+  uint64_t *o_done = p_full + 2;         // [2]
+  uint64_t *q_full = o_done + 2;         // one phase per unit
+  uint64_t *o_free = q_full + 1;         // one phase per unit: its O has been read out of TMEM
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(o_free + 1);
+  float *sml = reinterpret_cast<float *>(smem + ksp::OFF_ML);
+
+  pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int R = a.Nq * a.G;
+  const int P = gridDim.x;
+  const float sl2 = a.scale_log2;
+  struct Unit {
+    int seq, sl, h, row0, Lc, ntiles;
+    long long kb, vb;  // tmap rows of slot 0 of this (seq, kv head)
+  };
+  auto unit_of = [&](int u) {
+    Unit x;
+    const int rb = u % nrb, z = u / nrb;
+    x.sl = z / a.Hkv;
+    x.h = z % a.Hkv;
+    x.seq = a.seq_base + x.sl;
+    x.row0 = F == 1 ? rb * ROWS : 0;
+    x.Lc = a.len[x.seq];  // changed only by the step's last kernels: safe before the wait
+    x.ntiles = (x.Lc + a.Nq + KEYS - 1) / KEYS;
+    x.kb = a.k_row0 + (long long)x.seq * a.seq_rows + (long long)x.h * a.cap;
+    x.vb = a.v_row0 + (long long)x.seq * a.seq_rows + (long long)x.h * a.cap;
+    return x;
+  };
+  auto issue = [&](const Unit &x, int i, long long g) {  // K and V of keys [i KEYS, +KEYS) -> stage g % STAGES
+    const int s = (int)(g % STAGES);
+    uint8_t *kb = sKV + s * 2 * TILE;
+    uint8_t *vb = kb + TILE;
+    const int p = i * KEYS;
+    mbar_arrive_expect_tx(&kv_full[s], 2 * TILE);
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+#pragma unroll
+      for (int kh = 0; kh < KEYS / 64; ++kh) {
+        tma_load_2d(kb + hf * HALF + kh * 8192, &a.tmK, &kv_full[s], hf * 64, (int)(x.kb + p + kh * 64));
+        tma_load_2d(vb + hf * HALF + kh * 8192, &a.tmV, &kv_full[s], hf * 64, (int)(x.vb + p + kh * 64));
+      }
+    }
+  };
+  int pre = 0;  // prefix tiles of the first unit issued before the wait
+  if (threadIdx.x == 128) {
+    tma_prefetch_desc(&a.tmK);
+    tma_prefetch_desc(&a.tmV);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&p_full[b], 128);
+      mbar_init(&o_done[b], 1);
+    }
+    mbar_init(q_full, 128);
+    mbar_init(o_free, 128);
+    fence_barrier_init();
+    const Unit x = unit_of(blockIdx.x);
+    const int first = min(STAGES, x.ntiles);
+    while (pre < first && (pre + 1) * KEYS <= x.Lc) {
+      issue(x, pre, pre);
+      ++pre;
+    }
+  }
+  const int rr_lane = (warp < 4) ? warp * 32 + lane : 0;
+  const int cf = rr_lane / RP;  // copy of this softmax thread
+  if (warp == 5) tmem_alloc<TCOLS>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;  // S0: [0, 128), S1: [128, 256), O: [256, 384)
+
+  if (warp == 4) {
+    // ------------------------------------------------------------ TMA producer: every unit's tiles, one ring
+    if (lane == 0) {
+      pdl_wait();
+      long long g = 0;
+      for (int u = blockIdx.x, k = 0; u < units; u += P, ++k) {
+        const Unit x = unit_of(u);
+        if (k > 0) {  // this unit's Q rows -> L2 while the previous unit finishes (its softmax warps load them next)
+          const int r0 = x.row0, r1 = min(R, x.row0 + (F == 1 ? ROWS : RP));
+          for (int n = r0 / a.G; n * a.G < r1; ++n)
+            prefetch_l2_bulk(a.q + (((long long)x.sl * a.Nq + n) * a.H + (long long)x.h * a.G) * HD, a.G * HD * 2);
+        }
+        for (int i = 0; i < x.ntiles; ++i, ++g) {
+          if (k == 0 && i < pre) continue;
+          if (g >= STAGES) mbar_wait(&kv_empty[g % STAGES], (int)(((g / STAGES) - 1) & 1));
+          issue(x, i, g);
+        }
+      }
+    }
+  } else if (warp == 5) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16_major(ROWS, KEYS, 0, 0);  // Q (K-major) x K^T (K-major)
+      constexpr uint32_t idesc_o = idesc_bf16_major(ROWS, HD, 0, 1);    // P (TMEM) x V (MN-major)
+      const uint32_t q_u = smem_u32(sQ), kv_u = smem_u32(sKV);
+      long long g0 = 0;
+      for (int u = blockIdx.x, k = 0; u < units; u += P, ++k) {
+        const int ntiles = unit_of(u).ntiles;
+        mbar_wait(q_full, k & 1);
+        auto issue_s = [&](long long g) {
+          const int sb = (int)(g & 1), st = (int)(g % STAGES);
+          mbar_wait(&kv_full[st], (int)((g / STAGES) & 1));
+          tc_fence_after();
+          const uint32_t kb = kv_u + st * 2 * TILE;
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint64_t ad = umma_desc_sw128(q_u + (kk >> 2) * 16384 + (kk & 3) * 32);
+            const uint64_t bd = umma_desc_sw128(kb + (kk >> 2) * HALF + (kk & 3) * 32);
+            umma_bf16(tmem + sb * KEYS, ad, bd, idesc_s, kk > 0);
+          }
+          umma_commit(&s_full[sb]);
+        };
+        issue_s(g0);
+        for (int i = 0; i < ntiles; ++i) {
+          const long long g = g0 + i;
+          if (i + 1 < ntiles) issue_s(g + 1);
+          mbar_wait(&p_full[g & 1], (int)((g >> 1) & 1));
+          if (i == 0 && k > 0) mbar_wait(o_free, (k - 1) & 1);  // the previous unit's O has been read
+          tc_fence_after();
+          const uint32_t vb = kv_u + (int)(g % STAGES) * 2 * TILE + TILE;
+#pragma unroll
+          for (int kk = 0; kk < KEYS / 16; ++kk) {
+            const uint64_t bd = umma_desc_mn_sw128(vb + kk * 2048, HALF);
+            umma_bf16_ts(tmem + 2 * KEYS, tmem + (int)(g & 1) * KEYS + kk * 8, bd, idesc_o, (i > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&kv_empty[g % STAGES]);
+          umma_commit(&o_done[g & 1]);
+        }
+        g0 += ntiles;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax warps 0..3 (MMA row = TMEM lane)
+    const int r = warp * 32 + lane;  // MMA row = cf RP + (query row - row0)
+    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    const int Nq = a.Nq;
+    pdl_wait();
+    long long g0 = 0;
+    uint64_t anc0 = 0, anc1 = 0, anc2 = 0, anc3 = 0;
+    int anc_row0 = -1;
+    for (int u = blockIdx.x, k = 0; u < units; u += P, ++k) {
+      const Unit x = unit_of(u);
+      const int qr = x.row0 + r % RP;  // this thread's query row
+      const bool live = qr < R;
+      const bool warp_live = x.row0 + (warp * 32) % RP < R;
+      if (x.row0 != anc_row0) {  // ancestor words of the row's node (static tree tables)
+        anc_row0 = x.row0;
+        anc0 = anc1 = anc2 = anc3 = 0;
+        if (live) {
+          const uint64_t *w = a.anc + (qr / a.G) * kAncWords;
+          anc0 = w[0];
+          anc1 = w[1];
+          anc2 = w[2];
+          anc3 = w[3];
+        }
+      }
+      {  // stage Q row qr (every copy) into the K-major SW128 layout (the buffer is free: see the epilogue)
+        const uint4 *src = nullptr;
+        if (live) {
+          const int n = qr / a.G, gg = qr % a.G;
+          src = reinterpret_cast<const uint4 *>(a.q + (((long long)x.sl * Nq + n) * a.H + (long long)x.h * a.G + gg) * HD);
+        }
+        uint4 v[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) v[c] = live ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
+        const uint32_t q_u = smem_u32(sQ);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) st_shared_v4(q_u + (c >> 3) * 16384 + sw128_off(r, c), v[c].x, v[c].y, v[c].z, v[c].w);
+        fence_proxy_async();
+        mbar_arrive(q_full);
+      }
+      const int Lc = x.Lc;
+      float m_run = -INFINITY, l = 0.f;
+      for (int i = 0; i < x.ntiles; ++i) {
+        const long long g = g0 + i;
+        const int sb = (int)(g & 1);
+        mbar_wait(&s_full[sb], (int)((g >> 1) & 1));
+        tc_fence_after();
+        if (!warp_live) {
+          tc_fence_before();
+          mbar_arrive(&p_full[sb]);
+          continue;
+        }
+        float y[KT];
+        if constexpr (KT == 128) {
+          tmem_ld64_f(lane_base + sb * KEYS, y);
+          tmem_ld64_f(lane_base + sb * KEYS + 64, y + 64);
+        } else if constexpr (KT == 64) {
+          tmem_ld64_f(lane_base + sb * KEYS + cf * KT, y);
+        } else {
+          tmem_ld32_f(lane_base + sb * KEYS + cf * KT, y);
+        }
+        const int pt = i * KEYS + cf * KT;  // this thread's first key
+        constexpr int NH = KT >= 64 ? KT / 64 : 1;
+#pragma unroll
+        for (int hh = 0; hh < NH; ++hh) {
+          constexpr int W = KT >= 64 ? 64 : KT;
+          float *yw = y + hh * 64;
+          const int p0 = pt + hh * 64;
+          if (a.pad && p0 < Lc) {  // pad batching (f4): masked cache slots of the prefix
+            const uint32_t *pw = a.pad + (size_t)x.seq * a.pad_words + (p0 >> 5);
+            const uint64_t pm = (uint64_t)pw[0] | (W == 64 ? ((uint64_t)pw[1] << 32) : 0ull);
+            if (pm) {
+#pragma unroll
+              for (int j = 0; j < W; ++j) yw[j] = ((pm >> j) & 1ull) ? -INFINITY : yw[j];
+            }
+          }
+          if (p0 + W > Lc) {  // keys past the prefix: visibility bitmask (Eq. 2)
+            const int off = p0 - Lc;
+            auto word = [&](int q) { return q == 0 ? anc0 : q == 1 ? anc1 : q == 2 ? anc2 : q == 3 ? anc3 : 0ull; };
+            uint64_t vis;
+            if (off < 0) {
+              vis = (off <= -64 ? ~0ull : (~0ull >> (64 + off))) | (off <= -64 ? 0ull : (anc0 << (-off)));
+            } else {
+              const int q = off >> 6, sh = off & 63;
+              const uint64_t lo = word(q), hi = word(q + 1);
+              vis = sh ? ((lo >> sh) | (hi << (64 - sh))) : lo;
+            }
+            if (Nq - off < 64) vis &= (Nq - off <= 0) ? 0ull : (~0ull >> (64 - (Nq - off)));
+#pragma unroll
+            for (int j = 0; j < W; ++j) yw[j] = ((vis >> j) & 1ull) ? yw[j] : -INFINITY;
+          }
+        }
+        float mx0 = y[0], mx1 = y[1], mx2 = y[2], mx3 = y[3];
+#pragma unroll
+        for (int j = 4; j < KT; j += 4) {
+          mx0 = fmaxf(mx0, y[j]);
+          mx1 = fmaxf(mx1, y[j + 1]);
+          mx2 = fmaxf(mx2, y[j + 2]);
+          mx3 = fmaxf(mx3, y[j + 3]);
+        }
+        const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+        float m_new = m_run, alpha = 1.f;
+        bool resc = false;
+        if (m_run == -INFINITY) {
+          m_new = mx;
+        } else if (mx > m_run + tc::RESCALE_LOG2) {
+          m_new = mx;
+          alpha = exp2f(m_run - m_new);
+          resc = true;
+        }
+        const float nb = (m_new == -INFINITY) ? 0.f : -m_new;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        uint32_t pe[KT / 2];
+#pragma unroll
+        for (int j = 0; j < KT / 2; j += 2) {
+          const float e0 = ex2(fmaf(y[2 * j], sl2, nb)), e1 = ex2(fmaf(y[2 * j + 1], sl2, nb));
+          const float e2 = ex2(fmaf(y[2 * j + 2], sl2, nb)), e3 = ex2(fmaf(y[2 * j + 3], sl2, nb));
+          s0 += e0;
+          s1 += e1;
+          s2 += e2;
+          s3 += e3;
+          pe[j] = pack_bf16(e0, e1);
+          pe[j + 1] = pack_bf16(e2, e3);
+        }
+        uint32_t pk[KEYS / 2];
+#pragma unroll
+        for (int j = 0; j < KEYS / 2; ++j) pk[j] = (j / (KT / 2) == cf) ? pe[j % (KT / 2)] : 0u;
+        l = l * alpha + ((s0 + s1) + (s2 + s3));
+        m_run = m_new;
+        if (__any_sync(0xffffffffu, resc) && i > 0) {
+          mbar_wait(&o_done[(g - 1) & 1], (int)(((g - 1) >> 1) & 1));
+          tc_fence_after();
+#pragma unroll 1
+          for (int c0 = 0; c0 < HD; c0 += 32) {
+            float o[32];
+            tmem_ld32_f(lane_base + 2 * KEYS + c0, o);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) o[j] *= alpha;
+            tmem_st32_f(lane_base + 2 * KEYS + c0, o);
+          }
+        }
+        tmem_st32_u(lane_base + sb * KEYS, pk);
+        tmem_st32_u(lane_base + sb * KEYS + 32, pk + 32);
+        tc_fence_before();
+        mbar_arrive(&p_full[sb]);
+      }
+      {  // last PV of this unit
+        const long long gl = g0 + x.ntiles - 1;
+        mbar_wait(&o_done[gl & 1], (int)((gl >> 1) & 1));
+        tc_fence_after();
+      }
+      // ---- epilogue: (m, l) of every MMA row; O staged in the Q buffer one 64-column half at a time
+      // ([128][64] fp32 = 32 KB, 16-byte chunks XOR-swizzled by row), merged by the copy-0 threads
+      sml[2 * r] = live ? m_run : -INFINITY;
+      sml[2 * r + 1] = live ? l : 0.f;
+      float *spart = reinterpret_cast<float *>(sQ);
+      bf16 *dst = a.out + (((long long)x.sl * Nq + qr / a.G) * a.H + (long long)x.h * a.G + qr % a.G) * HD;
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        if (warp_live) {
+#pragma unroll
+          for (int c0 = 0; c0 < 64; c0 += 32) {
+            float o[32];
+            tmem_ld32_f(lane_base + 2 * KEYS + half * 64 + c0, o);
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              *reinterpret_cast<float4 *>(spart + r * 64 + 4 * ((c0 / 4 + c) ^ (r & 7))) =
+                  make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+          }
+        }
+        if (half == 1) {  // every O column has been read: the next unit's first PV may overwrite it
+          tc_fence_before();
+          mbar_arrive(o_free);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // the four softmax warps
+        if (cf == 0 && live) {  // merge the F copies of row qr (copy order), as tree_attn_ks_kernel
+          float mq[F], lq[F];
+#pragma unroll
+          for (int f = 0; f < F; ++f) {
+            mq[f] = sml[2 * (f * RP + qr - x.row0)];
+            lq[f] = sml[2 * (f * RP + qr - x.row0) + 1];
+          }
+          float M = mq[0];
+#pragma unroll
+          for (int f = 1; f < F; ++f) M = fmaxf(M, mq[f]);
+          float wq[F], L = 0.f;
+#pragma unroll
+          for (int f = 0; f < F; ++f) {
+            wq[f] = mq[f] == -INFINITY ? 0.f : exp2f(mq[f] - M);
+            L += wq[f] * lq[f];
+          }
+          const float inv = L > 0.f ? 1.f / L : 0.f;
+#pragma unroll 4
+          for (int c4 = 0; c4 < 16; ++c4) {
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int f = 0; f < F; ++f) {
+              const int rf = f * RP + qr - x.row0;
+              const float4 v = *reinterpret_cast<const float4 *>(spart + rf * 64 + 4 * (c4 ^ (rf & 7)));
+              acc.x += wq[f] * v.x;
+              acc.y += wq[f] * v.y;
+              acc.z += wq[f] * v.z;
+              acc.w += wq[f] * v.w;
+            }
+            uint2 pk2;
+            pk2.x = pack_bf16(acc.x * inv, acc.y * inv);
+            pk2.y = pack_bf16(acc.z * inv, acc.w * inv);
+            *reinterpret_cast<uint2 *>(dst + half * 64 + 4 * c4) = pk2;
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // staging buffer (then Q) reused
+      }
+      g0 += x.ntiles;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 5) tmem_dealloc<TCOLS>(tmem);
+}
+
 // ============================================================================ K1, stream-K ("lean") variant
 // The tree-mode kernel above gives every (row block, sequence, kv head) unit nsplit CTAs of a
 // cluster (nsplit <= 8, combined over DSMEM): with 1 CTA per SM (192 KB of shared memory) the grid
@@ -1617,6 +2012,10 @@ int attention_tc_nsplit(int units) {  // 1 CTA per SM: aim for ~one wave of 148
 // memory system ahead of the ring's own loads) and stays off
 static int g_attn_l2ahead = 2;
 void attention_set_l2ahead(int mode) { g_attn_l2ahead = mode & 3; }
+// sm_set_option("attn_ksp"): persistent row-copy kernel when a one-split launch has more units than SMs (1,
+// default: 3-14 % faster on every multi-wave C5 point, profiles/r02/k1_experiments.txt) or never (0)
+static int g_attn_ksp = 1;
+void attention_set_ksp(int on) { g_attn_ksp = on; }
 static int g_attn_ks = 2;  // sm_set_option("attn_ks"): 128-key-tile kernel on long key ranges, all N G (2, default), N G <= 64 (1), off (0)
 void attention_set_ks(int on) { g_attn_ks = on; }
 
@@ -1658,6 +2057,25 @@ cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
         if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, A, ks::SMEM);
       if (e != cudaSuccess) return e;
       ks_attr = true;
+    }
+    const int nrb = R <= 64 ? 1 : (R + 127) / 128;
+    const int units = a.nseq * a.Hkv * nrb;
+    if (g_attn_ksp && a.nsplit == 1 && units > kNumSMs) {  // several units per SM: persistent (KSP)
+      static bool ksp_attr = false;
+      if (!ksp_attr) {
+        const auto A = cudaFuncAttributeMaxDynamicSharedMemorySize;
+        cudaError_t e = cudaSuccess;
+        for (auto fn : {tree_attn_ksp_kernel<4>, tree_attn_ksp_kernel<2>, tree_attn_ksp_kernel<1>})
+          if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, A, ksp::SMEM);
+        if (e != cudaSuccess) return e;
+        ksp_attr = true;
+      }
+      cfg.gridDim = dim3(kNumSMs);
+      cfg.dynamicSmemBytes = ksp::SMEM;
+      cfg.numAttrs = 1;
+      if (R <= 32) return cudaLaunchKernelEx(&cfg, tree_attn_ksp_kernel<4>, a, units, nrb);
+      if (R <= 64) return cudaLaunchKernelEx(&cfg, tree_attn_ksp_kernel<2>, a, units, nrb);
+      return cudaLaunchKernelEx(&cfg, tree_attn_ksp_kernel<1>, a, units, nrb);
     }
     cfg.dynamicSmemBytes = ks::SMEM;
     AttnArgs b = a;

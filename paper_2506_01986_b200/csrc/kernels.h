@@ -377,6 +377,7 @@ size_t attention_lean_part_floats(int nunits);
 void attention_set_lean(int on);
 void attention_set_ks(int on);
 void attention_set_l2ahead(int mode);
+void attention_set_ksp(int on);
 void attention_set_lean_div(int d);
 int attention_lean_min_tiles(int Nq, int G);
 void attention_set_splits(int n);               // experiments: force key splits (0 = auto)

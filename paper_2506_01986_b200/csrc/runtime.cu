@@ -1984,6 +1984,7 @@ extern "C" sm_status sm_reset_options(void) {
   attention_set_lean(0);
   attention_set_ks(2);
   attention_set_l2ahead(2);
+  attention_set_ksp(1);
   attention_set_lean_div(16);
   tp_set_rsag(-1);
   g_fused = 0;
@@ -2040,6 +2041,8 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
     attention_set_lean(value);
   } else if (n == "attn_l2ahead") {  // K1 row-copy kernel: L2 prefetch ahead of the ring (bit 0 own range, bit 1 next wave)
     attention_set_l2ahead(value);
+  } else if (n == "attn_ksp") {  // K1: persistent row-copy kernel for one-split launches with > 148 units
+    attention_set_ksp(value);
   } else if (n == "attn_ks") {  // K1 128-key-tile (row-copy) kernel on long key ranges: 0 off, 1 N G <= 64, 2 all (default)
     attention_set_ks(value);
   } else if (n == "attn_lean_div") {  // lean K1: minimum tiles per CTA = max(2, live rows / value)

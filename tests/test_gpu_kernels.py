@@ -135,12 +135,17 @@ ATTN_CASES = [
     ("lean_gqa8_4blocks", synth.V64, None, 3, 8, 1, 128, [3000, 5, 1200], 0),
     # 128-key-tile kernel over several 128-row blocks (geometry B: N G = 512; N 256): one split per unit
     ("ks_rows512_long", synth.V64, None, 20, 8, 1, 128, [1000 + 37 * i for i in range(20)], 3),
+    # persistent row-copy kernel (one split, more units than SMs): 4 / 2 / 1 copies, ragged lengths
+    # (empty prefix included), units of 4 row blocks
+    ("ksp_f4_ragged", synth.SWEEP_TREES[16], None, 10, 16, 16, 128, [(97 * i) % 700 for i in range(10)], 2),
+    ("ksp_f2_v64", synth.V64, None, 5, 32, 32, 128, [0, 129, 511, 300, 64], 0),
+    ("ksp_f1_rows512", synth.V64, None, 20, 16, 2, 128, [(53 * i) % 400 for i in range(20)], 1),
 ]
 
 
 # K1 variants for head_dim 128: the stream-K tcgen05 kernel (default; min tiles per CTA = live rows
 # per unit / 16, and / 2 for many more pieces per unit), the cluster-split tcgen05 kernel, mma.sync
-VARIANTS = {"default": dict(), "rows128": dict(attn_ks=0), "ks64": dict(attn_ks=1), "ns1": dict(attn_splits=1),
+VARIANTS = {"default": dict(), "ksp": dict(attn_ksp=1), "noksp": dict(attn_ksp=0), "rows128": dict(attn_ks=0), "ks64": dict(attn_ks=1), "ns1": dict(attn_splits=1),
             "lean": dict(attn_tc=1, attn_lean=1),
             "lean_div2": dict(attn_tc=1, attn_lean=1, attn_lean_div=2), "mma": dict(attn_tc=0)}
 
@@ -168,6 +173,28 @@ def test_tree_attention_matches_oracle(sm, case, variant):
     assert np.all(np.isfinite(got))
     err = np.abs(got - ref)
     assert np.all(err <= 2e-2 + 2e-2 * np.abs(ref)), float(err.max())
+
+
+@pytest.mark.parametrize("case", [c for c in ATTN_CASES if c[0].startswith("ksp")], ids=lambda c: c[0])
+def test_persistent_row_copy_kernel_is_bitwise_the_row_copy_kernel(sm, case):
+    """KSP walks several units per CTA through one ring but keeps the row-copy kernel's arithmetic,
+    copy order and merge order: its output must equal the one-unit-per-CTA kernel's bit for bit."""
+    name, choices, chain, b, H, Hkv, hd, lens, extra = case
+    tree = sm.Tree(choices, topk=10)
+    N = tree.N
+    cap = max(lens) + N + extra
+    q = bf16_tensor(synth.normal_bits(6, 1, b * N * H * hd), (b, N, H, hd))
+    k = bf16_tensor(synth.normal_bits(6, 2, b * Hkv * cap * hd), (b, Hkv, cap, hd))
+    v = bf16_tensor(synth.normal_bits(6, 3, b * Hkv * cap * hd), (b, Hkv, cap, hd))
+    L = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    outs = []
+    for ksp in (0, 1):
+        sm.set_option("attn_ksp", ksp)
+        o = torch.full((b, N, H, hd), float("nan"), dtype=torch.bfloat16, device="cuda")
+        sm.tree_attention(tree, q, k, v, L, H, Hkv, o)
+        outs.append(o)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
 
 
 # ------------------------------------------------------------------ K3 top-k

@@ -13,15 +13,24 @@ import paper_2506_01986_b200 as sm  # noqa: E402
 import synth  # noqa: E402
 
 PEAK = 6543.4
+if os.environ.get("K1_PTS") == "multiwave":  # geometry A launches with more units than SMs (one key split)
+    pts_mw = [("A", 32, 32, b, N, Lc) for (b, N, Lc) in
+              [(8, 16, 1024), (8, 64, 1024), (8, 128, 1024), (8, 64, 2048), (8, 64, 4096), (16, 64, 2048),
+               (32, 16, 1024), (32, 64, 1024), (32, 128, 1024), (8, 256, 2048), (16, 16, 512), (32, 64, 512)]]
+else:
+    pts_mw = None
 pts = [("A", 32, 32, b, N, Lc) for (b, N, Lc) in
        [(1, 64, 1100), (1, 64, 2048), (1, 16, 4096), (1, 64, 8192), (2, 64, 2048), (2, 128, 4096), (4, 64, 1024),
         (4, 128, 2048), (8, 64, 1024), (8, 64, 4096), (16, 64, 2048), (32, 16, 1024), (1, 256, 8192),
         (8, 256, 2048)]] + \
       [("B", 8, 1, b, N, Lc) for (b, N, Lc) in [(1, 64, 4096), (8, 64, 4096), (8, 16, 8192), (32, 64, 4096),
                                                (16, 16, 32768)]]
+pts = pts_mw or pts
 hd = 128
 if os.environ.get("K1_VARS") == "ks":  # 128-row kernel vs key-split row packing (N G <= 64)
     VARS = [("rows128", dict(attn_lean=0, attn_ks=0)), ("ks", dict(attn_lean=0, attn_ks=2))]
+elif os.environ.get("K1_VARS") == "ksp":  # one-unit-per-CTA row-copy kernel vs the persistent one (units > 148)
+    VARS = [("ks", dict(attn_ksp=0)), ("ksp", dict(attn_ksp=1))]
 elif os.environ.get("K1_VARS") == "l2":  # row-copy kernel: L2 prefetch ahead of the ring (attn_l2ahead bits)
     VARS = [("ks", dict(attn_l2ahead=0)), ("own", dict(attn_l2ahead=1)), ("next", dict(attn_l2ahead=2)),
             ("both", dict(attn_l2ahead=3))]
