@@ -1097,6 +1097,10 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_cons
   constexpr int HD = ksp::HD, ROWS = ksp::ROWS, KEYS = ksp::KEYS, STAGES = ksp::STAGES;
   constexpr int HALF = ksp::HALF, TILE = ksp::TILE;
   constexpr int TCOLS = 512;        // S0, S1 (128 columns each), O (128)
+  // Units after the first come from a launch-wide counter (a CTA that finishes early takes the next
+  // unit: ragged lengths balance like separate CTAs would), handed to the MMA and softmax warps in
+  // order through a kUq-slot queue: the producer is at most STAGES units ahead (every unit has a tile)
+  constexpr int kUq = 8;
   constexpr int RP = ROWS / F;      // rows per copy
   constexpr int KT = KEYS / F;      // keys per thread per tile
   static_assert(F == 1 || F == 2 || F == 4, "copies");
@@ -1111,7 +1115,9 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_cons
   uint64_t *o_done = p_full + 2;         // [2]
   uint64_t *q_full = o_done + 2;         // one phase per unit
   uint64_t *o_free = q_full + 1;         // one phase per unit: its O has been read out of TMEM
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(o_free + 1);
+  uint64_t *u_full = o_free + 1;         // [kUq] unit queue slots (producer -> MMA / softmax)
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(u_full + kUq);
+  int *uq = reinterpret_cast<int *>(tslot + 1);  // [kUq] unit ids, -1 = no more work
   float *sml = reinterpret_cast<float *>(smem + ksp::OFF_ML);
 
   pdl_trigger();
@@ -1166,6 +1172,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_cons
     }
     mbar_init(q_full, 128);
     mbar_init(o_free, 128);
+    for (int j = 0; j < kUq; ++j) mbar_init(&u_full[j], 1);
     fence_barrier_init();
     const Unit x = unit_of(blockIdx.x);
     const int first = min(STAGES, x.ntiles);
@@ -1187,7 +1194,21 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_cons
     if (lane == 0) {
       pdl_wait();
       long long g = 0;
-      for (int u = blockIdx.x, k = 0; u < units; u += P, ++k) {
+      int *work = a.lean_sync + 2, *done = a.lean_sync + 3;  // zero between launches
+      for (int u = blockIdx.x, k = 0;; ++k) {
+        if (k > 0) {
+          u = P + atomicAdd(work, 1);
+          if (u >= units) u = -1;
+          uq[(k - 1) % kUq] = u;
+          mbar_arrive(&u_full[(k - 1) % kUq]);
+          if (u < 0) {
+            if (atomicAdd(done, 1) == P - 1) {  // the last CTA out resets the counters
+              *work = 0;
+              *done = 0;
+            }
+            break;
+          }
+        }
         const Unit x = unit_of(u);
         if (k > 0) {  // this unit's Q rows -> L2 while the previous unit finishes (its softmax warps load them next)
           const int r0 = x.row0, r1 = min(R, x.row0 + (F == 1 ? ROWS : RP));
@@ -1208,7 +1229,12 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_cons
       constexpr uint32_t idesc_o = idesc_bf16_major(ROWS, HD, 0, 1);    // P (TMEM) x V (MN-major)
       const uint32_t q_u = smem_u32(sQ), kv_u = smem_u32(sKV);
       long long g0 = 0;
-      for (int u = blockIdx.x, k = 0; u < units; u += P, ++k) {
+      for (int u = blockIdx.x, k = 0;; ++k) {
+        if (k > 0) {
+          mbar_wait(&u_full[(k - 1) % kUq], ((k - 1) / kUq) & 1);
+          u = *(volatile int *)&uq[(k - 1) % kUq];
+          if (u < 0) break;
+        }
         const int ntiles = unit_of(u).ntiles;
         mbar_wait(q_full, k & 1);
         auto issue_s = [&](long long g) {
@@ -1252,7 +1278,12 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_cons
     long long g0 = 0;
     uint64_t anc0 = 0, anc1 = 0, anc2 = 0, anc3 = 0;
     int anc_row0 = -1;
-    for (int u = blockIdx.x, k = 0; u < units; u += P, ++k) {
+    for (int u = blockIdx.x, k = 0;; ++k) {
+      if (k > 0) {
+        mbar_wait(&u_full[(k - 1) % kUq], ((k - 1) / kUq) & 1);
+        u = *(volatile int *)&uq[(k - 1) % kUq];
+        if (u < 0) break;
+      }
       const Unit x = unit_of(u);
       const int qr = x.row0 + r % RP;  // this thread's query row
       const bool live = qr < R;
@@ -2060,7 +2091,7 @@ cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
     }
     const int nrb = R <= 64 ? 1 : (R + 127) / 128;
     const int units = a.nseq * a.Hkv * nrb;
-    if (g_attn_ksp && a.nsplit == 1 && units > kNumSMs) {  // several units per SM: persistent (KSP)
+    if (g_attn_ksp && a.nsplit == 1 && units > kNumSMs && a.lean_sync) {  // several units per SM: persistent (KSP)
       static bool ksp_attr = false;
       if (!ksp_attr) {
         const auto A = cudaFuncAttributeMaxDynamicSharedMemorySize;

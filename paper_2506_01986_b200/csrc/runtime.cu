@@ -773,8 +773,8 @@ extern "C" sm_status sm_model_create(const sm_model_cfg *cfg, const sm_weights *
   ALLOC(m->tk_idx, (size_t)B * std::max(1, m->nmed) * 32, "topk indices");
   if (!m->f32 && m->hd == 128) {
     ALLOC(m->lean_part, attention_lean_part_floats(lean_units_max(m->Hkv, m->G, R, B)), "K1 partial slots");
-    ALLOC(m->lean_sync, 2, "K1 barrier");
-    cudaMemset(m->lean_sync, 0, 2 * sizeof(int));
+    ALLOC(m->lean_sync, 4, "K1 barrier and unit counters");  // [0, 1] lean grid barrier, [2, 3] KSP work queue
+    cudaMemset(m->lean_sync, 0, 4 * sizeof(int));
   }
   ALLOC(m->tp_seq, 1, "tp epoch");
   ALLOC(m->tp_err, 1, "tp error flag");
@@ -1100,7 +1100,7 @@ extern "C" sm_status sm_workspace_bytes(const sm_model_cfg *cfg, size_t *bytes) 
   b += B * d * 2 * P + nmed * B * d * 2 * P + (size_t)c.max_seq_len * (c.head_dim / 2) * 8;       // head_in, r_buf, rope
   b += 2 * R * 4 + 2 * B * nmed * 32 * 4 + 16;                                                      // amax, cand, top-k
   if (c.dtype != SM_DTYPE_FP32 && c.head_dim == 128)                                                 // K1 partials
-    b += attention_lean_part_floats(lean_units_max(c.n_kv_heads, c.n_heads / c.n_kv_heads, (int)R, (int)B)) * 4 + 8;
+    b += attention_lean_part_floats(lean_units_max(c.n_kv_heads, c.n_heads / c.n_kv_heads, (int)R, (int)B)) * 4 + 16;
   // stream-K partial slots: the largest need over the model's GEMMs
   size_t need = 0;
   const int Rg = (int)(R * P);

@@ -13,7 +13,12 @@ import paper_2506_01986_b200 as sm  # noqa: E402
 import synth  # noqa: E402
 
 PEAK = 6543.4
-if os.environ.get("K1_PTS") == "multiwave":  # geometry A launches with more units than SMs (one key split)
+if os.environ.get("K1_PTS") == "ragged":  # as multiwave, lengths spread over [Lc/2, Lc] (the sweep's "~" rows)
+    pts_mw = [("A", 32, 32, b, N, Lc) for (b, N, Lc) in
+              [(8, 64, 1024), (8, 128, 1024), (8, 64, 2048), (8, 64, 4096), (8, 64, 8192), (16, 128, 2048),
+               (32, 64, 1024)]]
+    RAGGED = True
+elif os.environ.get("K1_PTS") == "multiwave":  # geometry A launches with more units than SMs (one key split)
     pts_mw = [("A", 32, 32, b, N, Lc) for (b, N, Lc) in
               [(8, 16, 1024), (8, 64, 1024), (8, 128, 1024), (8, 64, 2048), (8, 64, 4096), (16, 64, 2048),
                (32, 16, 1024), (32, 64, 1024), (32, 128, 1024), (8, 256, 2048), (16, 16, 512), (32, 64, 512)]]
@@ -48,8 +53,13 @@ for g, H, Hkv, b, N, Lc in pts:
         k = torch.randn(b, Hkv, cap, hd, device="cuda").bfloat16()
         v = torch.randn(b, Hkv, cap, hd, device="cuda").bfloat16()
         sets.append((q, k, v, torch.empty_like(q)))
-    L = torch.full((b,), Lc, dtype=torch.int32, device="cuda")
-    alg = b * Hkv * cap * hd * 4 + 2 * b * tree.N * H * hd * 2
+    if globals().get("RAGGED"):
+        lens = [Lc // 2 + (Lc - Lc // 2) * i // max(1, b - 1) for i in range(b)]
+        L = torch.tensor(lens, dtype=torch.int32, device="cuda")
+        alg = sum(Hkv * (lb + tree.N) * hd * 4 for lb in lens) + 2 * b * tree.N * H * hd * 2
+    else:
+        L = torch.full((b,), Lc, dtype=torch.int32, device="cuda")
+        alg = b * Hkv * cap * hd * 4 + 2 * b * tree.N * H * hd * 2
     row = []
     for _, opts in VARS:
         for kk, vv in opts.items():
