@@ -378,12 +378,12 @@ static cudaError_t launch_hd(const AttnArgs &a, cudaStream_t st) {
 }
 
 // nsplit = cluster size in {1, 2, 4, 8}: enough CTAs to cover ~2 waves of SMs
-int attention_tc_nsplit(int units);
+int attention_tc_nsplit(int units, int cap);
 cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st);
 
-int attention_nsplit(int units, int head_dim) {
-  if (g_attn_splits == 1 || g_attn_splits == 2 || g_attn_splits == 4 || g_attn_splits == 8) return g_attn_splits;
-  if (use_tc(head_dim)) return attention_tc_nsplit(units);
+int attention_nsplit(int units, int head_dim, int cap) {
+  if (g_attn_splits >= 1 && g_attn_splits <= 8) return g_attn_splits;
+  if (use_tc(head_dim)) return attention_tc_nsplit(units, cap);
   int ns = 1;
   while (ns < 8 && units * ns < 2 * kNumSMs) ns *= 2;
   return ns;

@@ -2031,10 +2031,59 @@ extern "C" int sm_trace_read(long long *dst, int n) {  // diagnostics build only
 }
 #endif
 
-int attention_tc_nsplit(int units) {  // 1 CTA per SM: aim for ~one wave of 148
-  int ns = 1;
-  while (ns < 8 && units * ns * 2 <= kNumSMs) ns *= 2;
-  return ns;
+// Most clusters of ns CTAs of the one-CTA-per-SM K1 kernels that can be co-resident, queried once per ns:
+// clusters must fit inside a GPC, so e.g. only 15 clusters of 8 run at a time (120 of 148 SMs) and
+// 16 units x 8 splits took two waves (profiles/r02/k1_experiments.txt, geometry B b 16 / Lc 32K).
+static int active_clusters(int ns) {
+  static int cache[9] = {0};
+  if (ns <= 1) return kNumSMs;
+  if (cache[ns] == 0) {
+    int n = 0;
+    if (cudaFuncSetAttribute(tree_attn_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM) ==
+        cudaSuccess) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(ns, 1, 256);
+      cfg.blockDim = dim3(192);
+      cfg.dynamicSmemBytes = tc::SMEM;
+      cudaLaunchAttribute at;
+      at.id = cudaLaunchAttributeClusterDimension;
+      at.val.clusterDim.x = ns;
+      at.val.clusterDim.y = 1;
+      at.val.clusterDim.z = 1;
+      cfg.attrs = &at;
+      cfg.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&n, (void *)tree_attn_tc_kernel<false>, &cfg) != cudaSuccess) n = 0;
+    }
+    cudaGetLastError();
+    cache[ns] = n > 0 ? n : kNumSMs / ns;
+  }
+  return cache[ns];
+}
+
+// Key splits (= cluster size, 1..8) for `units` (sequence, kv head, row block) units of up to cap keys:
+// minimise waves x (keys per CTA + a fixed per-CTA cost of ~256 keys), waves = units over the clusters of
+// that size that fit at once.
+static int g_split_model = 1;  // sm_set_option("attn_split_model"): 1 occupancy-aware (default), 0 round-1 rule
+void attention_set_split_model(int m) { g_split_model = m; }
+int attention_tc_nsplit(int units, int cap) {
+  if (g_split_model == 0) {  // round 1: powers of two up to ~one wave of 148 CTAs
+    int ns = 1;
+    while (ns < 8 && units * ns * 2 <= kNumSMs) ns *= 2;
+    return ns;
+  }
+  constexpr long long kOverheadKeys = 256;
+  int best = 1;
+  long long best_cost = -1;
+  for (int ns = 1; ns <= 8; ++ns) {
+    const long long act = active_clusters(ns);
+    const long long waves = (units + act - 1) / act;
+    const long long cost = waves * ((cap + ns - 1) / ns + kOverheadKeys);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = ns;
+    }
+  }
+  return best;
 }
 
 // sm_set_option("attn_l2ahead"), AttnArgs::l2_ahead.  Default 2: the next wave's first ring and Q rows go

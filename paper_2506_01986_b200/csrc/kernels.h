@@ -370,7 +370,7 @@ int attention_row_blocks(int Nq, int G, int head_dim);
 cudaError_t attention_f32_launch(const float *q, const float *k, const float *v, const int32_t *len,
                                  const uint64_t *anc, int Nq, int H, int Hkv, int hd, int cap, int nseq, int seq_base,
                                  const uint32_t *pad, int pad_words, bf16 *out, cudaStream_t st);
-int attention_nsplit(int units, int head_dim);  // units = row blocks * sequences * kv heads
+int attention_nsplit(int units, int head_dim, int cap);  // units = row blocks * sequences * kv heads; cap = keys
 constexpr int kLeanMaxSeq = 64;                 // sequences per lean K1 launch
 cudaError_t attention_lean_launch(const AttnArgs &a, cudaStream_t st);
 size_t attention_lean_part_floats(int nunits);
@@ -378,6 +378,7 @@ void attention_set_lean(int on);
 void attention_set_ks(int on);
 void attention_set_l2ahead(int mode);
 void attention_set_ksp(int on);
+void attention_set_split_model(int m);
 void attention_set_lean_div(int d);
 int attention_lean_min_tiles(int Nq, int G);
 void attention_set_splits(int n);               // experiments: force key splits (0 = auto)

@@ -1294,8 +1294,8 @@ extern "C" sm_status sm_state_device(const sm_kv *kv, int32_t **d_root, int32_t 
 }
 
 // ---------------------------------------------------------------- forward (a2 + a3)
-static int attn_splits(const sm_model *m, int nseq, int Nq) {
-  return attention_nsplit(nseq * m->Hkv * attention_row_blocks(Nq, m->G, m->hd), m->hd);
+static int attn_splits(const sm_model *m, int nseq, int Nq, int cap) {
+  return attention_nsplit(nseq * m->Hkv * attention_row_blocks(Nq, m->G, m->hd), m->hd, cap);
 }
 
 // Timing ablation (sm_set_option "ablate", experiments only -- results become
@@ -1342,7 +1342,7 @@ static sm_status enqueue_forward(sm_model *m, sm_kv *kv, const int32_t *d_tok, i
     CK(pp_xfer_launch(m->x, n4, m->pp_rank - 1, 1u << m->pp_rank, pp_args(m, pt0 + m->pp_rank - 1), st));
     ++nl;
   }
-  const int nsplit = attn_splits(m, nseq, Nq);
+  const int nsplit = attn_splits(m, nseq, Nq, kv->cap);
   const long long layer_rows = (long long)2 * kv->b * m->Hkv * kv->cap;
   const long long half_rows = (long long)kv->b * m->Hkv * kv->cap;
   RowCtx rc{M, Nq, seq_base, kv->len, tree.depth, kv->pad_mode ? kv->pos_len : nullptr};
@@ -1857,7 +1857,7 @@ static sm_status attention_stage(const uint64_t *d_anc, int Nq, const void *d_q,
   if (head_dim != 16 && head_dim != 32 && head_dim != 64 && head_dim != 128)
     return fail(SM_ERR_INVALID_ARG, "head_dim must be 16/32/64/128");
   const int G = n_heads / n_kv_heads;
-  const int nsplit = attention_nsplit(batch * n_kv_heads * attention_row_blocks(Nq, G, head_dim), head_dim);
+  const int nsplit = attention_nsplit(batch * n_kv_heads * attention_row_blocks(Nq, G, head_dim), head_dim, cap);
   AttnArgs aa;
   std::memset(&aa, 0, sizeof(aa));
   const uint64_t rows = (uint64_t)batch * n_kv_heads * cap;
@@ -1985,6 +1985,7 @@ extern "C" sm_status sm_reset_options(void) {
   attention_set_ks(2);
   attention_set_l2ahead(2);
   attention_set_ksp(1);
+  attention_set_split_model(1);
   attention_set_lean_div(16);
   tp_set_rsag(-1);
   g_fused = 0;
@@ -2041,6 +2042,8 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
     attention_set_lean(value);
   } else if (n == "attn_l2ahead") {  // K1 row-copy kernel: L2 prefetch ahead of the ring (bit 0 own range, bit 1 next wave)
     attention_set_l2ahead(value);
+  } else if (n == "attn_split_model") {  // K1 key splits: 1 occupancy-aware cost model (default), 0 round-1 rule
+    attention_set_split_model(value);
   } else if (n == "attn_ksp") {  // K1: persistent row-copy kernel for one-split launches with > 148 units
     attention_set_ksp(value);
   } else if (n == "attn_ks") {  // K1 128-key-tile (row-copy) kernel on long key ranges: 0 off, 1 N G <= 64, 2 all (default)

@@ -140,12 +140,16 @@ ATTN_CASES = [
     ("ksp_f4_ragged", synth.SWEEP_TREES[16], None, 10, 16, 16, 128, [(97 * i) % 700 for i in range(10)], 2),
     ("ksp_f2_v64", synth.V64, None, 5, 32, 32, 128, [0, 129, 511, 300, 64], 0),
     ("ksp_f1_rows512", synth.V64, None, 20, 16, 2, 128, [(53 * i) % 400 for i in range(20)], 1),
+    # 16 units of long ranges (geometry B shape): the occupancy-aware split count picks a non-power-of-two
+    # cluster (7 splits: 16 clusters of 8 do not fit at once)
+    ("b16_gqa8_odd_splits", synth.SWEEP_TREES[16], None, 16, 8, 1, 128, [1500 + 211 * i for i in range(16)], 3),
 ]
 
 
 # K1 variants for head_dim 128: the stream-K tcgen05 kernel (default; min tiles per CTA = live rows
 # per unit / 16, and / 2 for many more pieces per unit), the cluster-split tcgen05 kernel, mma.sync
-VARIANTS = {"default": dict(), "ksp": dict(attn_ksp=1), "noksp": dict(attn_ksp=0), "rows128": dict(attn_ks=0), "ks64": dict(attn_ks=1), "ns1": dict(attn_splits=1),
+VARIANTS = {"default": dict(), "ns3": dict(attn_splits=3), "ns7": dict(attn_splits=7),
+            "rule_splits": dict(attn_split_model=0), "ksp": dict(attn_ksp=1), "noksp": dict(attn_ksp=0), "rows128": dict(attn_ks=0), "ks64": dict(attn_ks=1), "ns1": dict(attn_splits=1),
             "lean": dict(attn_tc=1, attn_lean=1),
             "lean_div2": dict(attn_tc=1, attn_lean=1, attn_lean_div=2), "mma": dict(attn_tc=0)}
 

@@ -13,7 +13,13 @@ import paper_2506_01986_b200 as sm  # noqa: E402
 import synth  # noqa: E402
 
 PEAK = 6543.4
-if os.environ.get("K1_PTS") == "ragged":  # as multiwave, lengths spread over [Lc/2, Lc] (the sweep's "~" rows)
+if os.environ.get("K1_PTS") == "geomB":  # 70B TP8 shard (8 q heads, 1 kv head)
+    pts_mw = [("B", 8, 1, b, N, Lc) for (b, N, Lc) in
+              [(16, 16, 32768), (16, 16, 8192), (4, 64, 8192), (2, 128, 16384), (8, 32, 8192), (8, 64, 4096),
+               (8, 16, 8192), (32, 64, 4096), (1, 64, 4096), (16, 64, 16384)]] + \
+             [("A", 32, 32, b, N, Lc) for (b, N, Lc) in [(1, 64, 1100), (1, 64, 4096), (2, 64, 2048), (4, 64, 1024),
+                                                          (1, 16, 32768), (2, 128, 8192)]]
+elif os.environ.get("K1_PTS") == "ragged":  # as multiwave, lengths spread over [Lc/2, Lc] (the sweep's "~" rows)
     pts_mw = [("A", 32, 32, b, N, Lc) for (b, N, Lc) in
               [(8, 64, 1024), (8, 128, 1024), (8, 64, 2048), (8, 64, 4096), (8, 64, 8192), (16, 128, 2048),
                (32, 64, 1024)]]
@@ -36,6 +42,8 @@ if os.environ.get("K1_VARS") == "ks":  # 128-row kernel vs key-split row packing
     VARS = [("rows128", dict(attn_lean=0, attn_ks=0)), ("ks", dict(attn_lean=0, attn_ks=2))]
 elif os.environ.get("K1_VARS") == "ksp":  # one-unit-per-CTA row-copy kernel vs the persistent one (units > 148)
     VARS = [("ks", dict(attn_ksp=0)), ("ksp", dict(attn_ksp=1))]
+elif os.environ.get("K1_VARS") == "split":  # key-split count: round-1 rule vs occupancy-aware cost model
+    VARS = [("rule", dict(attn_split_model=0)), ("model", dict(attn_split_model=1))]
 elif os.environ.get("K1_VARS") == "l2":  # row-copy kernel: L2 prefetch ahead of the ring (attn_l2ahead bits)
     VARS = [("ks", dict(attn_l2ahead=0)), ("own", dict(attn_l2ahead=1)), ("next", dict(attn_l2ahead=2)),
             ("both", dict(attn_l2ahead=3))]

@@ -26,7 +26,7 @@ for kv_opt in filter(None, os.environ.get("SM_OPT", "").split(",")):
 args = [int(x) for x in sys.argv[1:]]
 pts = [tuple(args[i:i + 3]) for i in range(0, len(args), 3)] or [(8, 64, 1024), (1, 64, 4096), (32, 64, 1024),
                                                                   (8, 64, 4096)]
-H = Hkv = 32
+H, Hkv = (int(x) for x in os.environ.get("K1_GEOM", "32,32").split(","))  # B: K1_GEOM=8,1
 hd = 128
 for b, N, Lc in pts:
     tree = sm.Tree(synth.SWEEP_TREES[N]) if N != 64 else sm.Tree(synth.V64)
@@ -56,7 +56,7 @@ for b, N, Lc in pts:
     smid = rec[:, 0]
     alg = b * Hkv * cap * hd * 4 + 2 * b * tree.N * H * hd * 2
     span = ex.max()
-    print(f"== A b{b} N{tree.N} Lc{Lc}: {len(rec)} CTAs, span {span:.1f} us ({alg / span / 1e3:.0f} GB/s)")
+    print(f"== H{H}/{Hkv} b{b} N{tree.N} Lc{Lc}: {len(rec)} CTAs, span {span:.1f} us ({alg / span / 1e3:.0f} GB/s)")
     print(f"   median phases (us): entry->Q {np.median(qs - ent):.2f}  entry->K/V(0) {np.median(kv0 - ent):.2f}  "
           f"K/V(0)->last PV {np.median(pv - kv0):.2f}  last PV->exit {np.median(ex - pv):.2f}  "
           f"lifetime {np.median(ex - ent):.2f}")
