@@ -24,6 +24,8 @@
 //    griddepcontrol.wait; Q and the tree tiles after it.
 // Warp roles (192 threads): warps 0-3 softmax / epilogue (TMEM lanes = rows),
 // warp 4 TMA producer, warp 5 MMA issuer + TMEM allocator.
+#include <cmath>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -1093,7 +1095,7 @@ static_assert(SMEM <= 232448, "K1 (KSP) shared memory");
 
 template <int F>
 __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_constant__ AttnArgs a, int units,
-                                                               int nrb) {
+                                                               int nrb, int dyn) {
   constexpr int HD = ksp::HD, ROWS = ksp::ROWS, KEYS = ksp::KEYS, STAGES = ksp::STAGES;
   constexpr int HALF = ksp::HALF, TILE = ksp::TILE;
   constexpr int TCOLS = 512;        // S0, S1 (128 columns each), O (128)
@@ -1197,12 +1199,12 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_cons
       int *work = a.lean_sync + 2, *done = a.lean_sync + 3;  // zero between launches
       for (int u = blockIdx.x, k = 0;; ++k) {
         if (k > 0) {
-          u = P + atomicAdd(work, 1);
+          u = dyn ? P + atomicAdd(work, 1) : blockIdx.x + k * P;  // dyn 0: static round robin (experiments)
           if (u >= units) u = -1;
           uq[(k - 1) % kUq] = u;
           mbar_arrive(&u_full[(k - 1) % kUq]);
           if (u < 0) {
-            if (atomicAdd(done, 1) == P - 1) {  // the last CTA out resets the counters
+            if (dyn && atomicAdd(done, 1) == P - 1) {  // the last CTA out resets the counters
               *work = 0;
               *done = 0;
             }
@@ -2063,6 +2065,7 @@ static int active_clusters(int ns) {
 // Key splits (= cluster size, 1..8) for `units` (sequence, kv head, row block) units of up to cap keys:
 // minimise waves x (keys per CTA + a fixed per-CTA cost of ~256 keys), waves = units over the clusters of
 // that size that fit at once.
+static int g_attn_ksp = 1;  // sm_set_option("attn_ksp"), see attention_tc_launch
 static int g_split_model = 1;  // sm_set_option("attn_split_model"): 1 occupancy-aware (default), 0 round-1 rule
 void attention_set_split_model(int m) { g_split_model = m; }
 int attention_tc_nsplit(int units, int cap) {
@@ -2071,13 +2074,14 @@ int attention_tc_nsplit(int units, int cap) {
     while (ns < 8 && units * ns * 2 <= kNumSMs) ns *= 2;
     return ns;
   }
-  constexpr long long kOverheadKeys = 256;
+  constexpr double kOverheadKeys = 256;
   int best = 1;
-  long long best_cost = -1;
+  double best_cost = -1;
   for (int ns = 1; ns <= 8; ++ns) {
-    const long long act = active_clusters(ns);
-    const long long waves = (units + act - 1) / act;
-    const long long cost = waves * ((cap + ns - 1) / ns + kOverheadKeys);
+    const int act = active_clusters(ns);
+    double cost = std::ceil((double)units / act) * ((cap + ns - 1) / ns + kOverheadKeys);
+    if (ns == 1 && units > kNumSMs && g_attn_ksp)  // persistent KSP: units stream back to back, no waves
+      cost = (double)units / kNumSMs * (cap + kOverheadKeys / 2);
     if (best_cost < 0 || cost < best_cost) {
       best_cost = cost;
       best = ns;
@@ -2094,7 +2098,6 @@ static int g_attn_l2ahead = 2;
 void attention_set_l2ahead(int mode) { g_attn_l2ahead = mode & 3; }
 // sm_set_option("attn_ksp"): persistent row-copy kernel when a one-split launch has more units than SMs (1,
 // default: 3-14 % faster on every multi-wave C5 point, profiles/r02/k1_experiments.txt) or never (0)
-static int g_attn_ksp = 1;
 void attention_set_ksp(int on) { g_attn_ksp = on; }
 static int g_attn_ks = 2;  // sm_set_option("attn_ks"): 128-key-tile kernel on long key ranges, all N G (2, default), N G <= 64 (1), off (0)
 void attention_set_ks(int on) { g_attn_ks = on; }
@@ -2153,9 +2156,10 @@ cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
       cfg.gridDim = dim3(kNumSMs);
       cfg.dynamicSmemBytes = ksp::SMEM;
       cfg.numAttrs = 1;
-      if (R <= 32) return cudaLaunchKernelEx(&cfg, tree_attn_ksp_kernel<4>, a, units, nrb);
-      if (R <= 64) return cudaLaunchKernelEx(&cfg, tree_attn_ksp_kernel<2>, a, units, nrb);
-      return cudaLaunchKernelEx(&cfg, tree_attn_ksp_kernel<1>, a, units, nrb);
+      const int dyn = g_attn_ksp == 3 ? 0 : 1;
+      if (R <= 32) return cudaLaunchKernelEx(&cfg, tree_attn_ksp_kernel<4>, a, units, nrb, dyn);
+      if (R <= 64) return cudaLaunchKernelEx(&cfg, tree_attn_ksp_kernel<2>, a, units, nrb, dyn);
+      return cudaLaunchKernelEx(&cfg, tree_attn_ksp_kernel<1>, a, units, nrb, dyn);
     }
     cfg.dynamicSmemBytes = ks::SMEM;
     AttnArgs b = a;

@@ -43,6 +43,14 @@ if a.quick:
 if a.full:
     Ns, Lcs, bs = [16, 32, 64, 128, 256], [512, 1024, 2048, 4096, 8192, 16384, 32768], [1, 2, 4, 8, 16, 32]
     RAGGED = [False, True]
+if os.environ.get("K1_SWEEP_B"):  # restrict (diagnostics): K1_SWEEP_B=8,16 K1_SWEEP_N=128 K1_SWEEP_G=A
+    bs = [int(x) for x in os.environ["K1_SWEEP_B"].split(",")]
+if os.environ.get("K1_SWEEP_N"):
+    Ns = [int(x) for x in os.environ["K1_SWEEP_N"].split(",")]
+if os.environ.get("K1_SWEEP_G"):
+    geoms = [g for g in geoms if g[0][0] == os.environ["K1_SWEEP_G"]]
+if os.environ.get("K1_SWEEP_U"):  # uniform lengths only
+    RAGGED = [False]
 print(f"{'geom':8s} {'b':>3s} {'N':>4s} {'Lc':>6s} {'MB':>8s} {'us':>9s} {'GB/s':>8s} {'TF/s':>7s} {'bound':>6s} "
       f"{'frac':>6s}")
 # flops = 4 H hd sum_b (N Lc + sum_n (depth_n + 1)) (tree part counted sparse);
@@ -88,6 +96,13 @@ for ragged in RAGGED:
                 e1.record()
                 torch.cuda.synchronize()
                 us = e0.elapsed_time(e1) * 1e3 / 60
+                chk = ""
+                if os.environ.get("K1_SWEEP_CHECK"):  # diagnostics: the replayed output vs a fresh launch
+                    q, k, v, o = sets[0]
+                    o2 = torch.empty_like(o)
+                    sm.tree_attention(tree, q, k, v, L, H, Hkv, o2, stream=st)
+                    torch.cuda.synchronize()
+                    chk = " ok" if torch.equal(o, o2) else " MISMATCH"
                 alg = sum(Hkv * (lb + tree.N) * hd * 2 * 2 for lb in lens) + 2 * b * tree.N * H * hd * 2
                 dep = tree.query()["node_depth"]
                 flops = sum(4 * H * hd * (tree.N * lb + int((dep + 1).sum())) for lb in lens)
@@ -97,6 +112,6 @@ for ragged in RAGGED:
                 bound = "hbm" if t_hbm >= t_tc else "tensor"
                 tag = gname + ("~" if ragged else "")
                 print(f"{tag:8s} {b:3d} {tree.N:4d} {Lc:6d} {alg / 1e6:8.1f} {us:9.1f} {gbs:8.1f} {tfs:7.1f} {bound:>6s} "
-                      f"{max(t_hbm, t_tc) / us:6.3f}", flush=True)
+                      f"{max(t_hbm, t_tc) / us:6.3f}{chk}", flush=True)
                 del sets, g
                 torch.cuda.empty_cache()
