@@ -89,13 +89,18 @@ for ragged in RAGGED:
                     g.capture_end()
                 g.replay()
                 torch.cuda.synchronize()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
+                # three timing rounds of 3 replays (60 launches each); the point's time is the median round
+                # (single rounds of a long sweep showed occasional 1.2-1.5x outliers that a re-run did not)
+                rounds = []
                 for _ in range(3):
-                    g.replay()
-                e1.record()
-                torch.cuda.synchronize()
-                us = e0.elapsed_time(e1) * 1e3 / 60
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    for _ in range(3):
+                        g.replay()
+                    e1.record()
+                    torch.cuda.synchronize()
+                    rounds.append(e0.elapsed_time(e1) * 1e3 / 60)
+                us = sorted(rounds)[1]
                 chk = ""
                 if os.environ.get("K1_SWEEP_CHECK"):  # diagnostics: the replayed output vs a fresh launch
                     q, k, v, o = sets[0]
