@@ -13,7 +13,12 @@ import paper_2506_01986_b200 as sm  # noqa: E402
 import synth  # noqa: E402
 
 PEAK = 6543.4
-if os.environ.get("K1_PTS") == "geomB":  # 70B TP8 shard (8 q heads, 1 kv head)
+if os.environ.get("K1_PTS") == "rows256":  # N G >= 256 live rows: geometry B and N 256 at geometry A
+    pts_mw = [("B", 8, 1, b, N, Lc) for (b, N, Lc) in
+              [(8, 64, 4096), (8, 64, 16384), (32, 64, 4096), (32, 64, 16384), (8, 128, 4096), (8, 128, 16384),
+               (32, 128, 4096), (16, 256, 8192), (32, 256, 4096), (8, 32, 8192), (1, 64, 4096), (16, 64, 16384)]] + \
+             [("A", 32, 32, b, N, Lc) for (b, N, Lc) in [(1, 256, 8192), (8, 256, 2048), (4, 256, 8192), (32, 256, 1024)]]
+elif os.environ.get("K1_PTS") == "geomB":  # 70B TP8 shard (8 q heads, 1 kv head)
     pts_mw = [("B", 8, 1, b, N, Lc) for (b, N, Lc) in
               [(16, 16, 32768), (16, 16, 8192), (4, 64, 8192), (2, 128, 16384), (8, 32, 8192), (8, 64, 4096),
                (8, 16, 8192), (32, 64, 4096), (1, 64, 4096), (16, 64, 16384)]] + \
@@ -42,6 +47,8 @@ if os.environ.get("K1_VARS") == "ks":  # 128-row kernel vs key-split row packing
     VARS = [("rows128", dict(attn_lean=0, attn_ks=0)), ("ks", dict(attn_lean=0, attn_ks=2))]
 elif os.environ.get("K1_VARS") == "ksp":  # one-unit-per-CTA row-copy kernel vs the persistent one (units > 148)
     VARS = [("ks", dict(attn_ksp=0)), ("ksp", dict(attn_ksp=1))]
+elif os.environ.get("K1_VARS") == "pair":  # one CTA per 128-row block vs 2-SM row-block pairs (KS2)
+    VARS = [("single", dict(attn_pair=0)), ("pair", dict(attn_pair=1))]
 elif os.environ.get("K1_VARS") == "split":  # key-split count: round-1 rule vs occupancy-aware cost model
     VARS = [("rule", dict(attn_split_model=0)), ("model", dict(attn_split_model=1))]
 elif os.environ.get("K1_VARS") == "l2":  # row-copy kernel: L2 prefetch ahead of the ring (attn_l2ahead bits)
