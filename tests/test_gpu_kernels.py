@@ -192,7 +192,8 @@ def test_persistent_row_copy_kernel_is_bitwise_the_row_copy_kernel(sm, case):
     v = bf16_tensor(synth.normal_bits(6, 3, b * Hkv * cap * hd), (b, Hkv, cap, hd))
     L = torch.tensor(lens, dtype=torch.int32, device="cuda")
     outs = []
-    for ksp in (0, 1):
+    sm.set_option("attn_splits", 1)  # the same (single) key split on both sides: with KSP off the split model
+    for ksp in (0, 1):                 # may otherwise choose 2 splits for 149-222 units
         sm.set_option("attn_ksp", ksp)
         o = torch.full((b, N, H, hd), float("nan"), dtype=torch.bfloat16, device="cuda")
         sm.tree_attention(tree, q, k, v, L, H, Hkv, o)
