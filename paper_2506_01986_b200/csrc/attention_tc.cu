@@ -581,7 +581,8 @@ constexpr int QB = ROWS * HD * 2;          // 32 KB
 constexpr int OFF_Q = 0;
 constexpr int OFF_KV = OFF_Q + QB;
 constexpr int OFF_BAR = OFF_KV + 192 * 1024;
-constexpr int SMEM = OFF_BAR + 256 + 1024;
+constexpr int OFF_SMAX = OFF_BAR + 256;    // W2: [2 key halves][128 rows] fp32 row-max / row-sum exchange
+constexpr int SMEM = OFF_SMAX + 1024 + 1024;
 static_assert(SMEM <= 232448, "K1 (KS) shared memory");
 // end-of-kernel staging in the idle ring: merged rows for the cluster combine at offset 0 (the tree
 // kernel's layout: so [128][HD] fp32 + sml [128][2] + swt), the copies' partials above 80 KB
@@ -617,13 +618,20 @@ SM_DEV void ks_prefetch_l2(const AttnArgs &a, int seq, int h, int p0, int p1) {
   }
 }
 
-template <int F, int KEYS>
-__global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_constant__ AttnArgs a) {
+// W2 (F = 1 only): eight softmax warps, two per TMEM lane quadrant -- warp w and w + 4 share the rows of
+// quadrant w & 3 and take the two 64-key halves of every tile (the row max is exchanged through shared
+// memory; the lower half's warp does the O rescales and the epilogue): the per-thread softmax work of the
+// F = 2 kernel for 128 live rows.
+template <int F, int KEYS, bool W2 = false>
+__global__ void __launch_bounds__(W2 ? 320 : 192, 1) tree_attn_ks_kernel(const __grid_constant__ AttnArgs a) {
   constexpr int HD = ks::HD, ROWS = ks::ROWS, STAGES = ks::Cfg<KEYS>::STAGES;
+  constexpr int NSW = W2 ? 8 : 4;   // softmax warps; producer = warp NSW, MMA issuer = warp NSW + 1
+  constexpr int NST = NSW * 32;     // softmax threads
+  static_assert(!W2 || (F == 1 && KEYS == 128), "W2: 128 live rows, 128-key tiles");
   constexpr int HALF = ks::Cfg<KEYS>::HALF, TILE = ks::Cfg<KEYS>::TILE;
   constexpr int TCOLS = KEYS == 128 ? 512 : 256;  // S0, S1 (KEYS columns each), O (128)
   constexpr int RP = ROWS / F;      // rows per copy
-  constexpr int KT = KEYS / F;      // keys per thread per tile
+  constexpr int KT = W2 ? KEYS / 2 : KEYS / F;  // keys per thread per tile
   static_assert(F == 1 || F == 2 || F == 4, "copies");
   static_assert(KEYS == 64 || KEYS == 128, "key tile");
   static_assert(KT >= 16, "keys per thread");
@@ -682,7 +690,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
   };
   const int first = min(STAGES, ntiles);
   int pre = 0;
-  if (threadIdx.x == 128) {
+  if (threadIdx.x == NST) {
     tma_prefetch_desc(&a.tmK);
     tma_prefetch_desc(&a.tmV);
     for (int s = 0; s < STAGES; ++s) {
@@ -691,7 +699,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&s_full[b], 1);
-      mbar_init(&p_full[b], 128);
+      mbar_init(&p_full[b], NST);
       mbar_init(&o_done[b], 1);
     }
     mbar_init(q_full, 128);
@@ -701,10 +709,11 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
       ks_prefetch_l2(a, seq, h, key0 + first * KEYS, min(key1, Lc));
   }
   // softmax threads: copy f of query row r; the ancestor words of its node
-  const int rr_lane = (warp < 4) ? warp * 32 + lane : 0;
-  const int cf = rr_lane / RP, qr = row0 + rr_lane % RP;  // copy, query row
+  const int rr_lane = (warp < NSW) ? (warp & 3) * 32 + lane : 0;
+  const int cf = W2 ? (warp < NSW ? warp >> 2 : 0) : rr_lane / RP;  // copy (W2: key half), query row
+  const int qr = row0 + rr_lane % RP;
   uint64_t anc0 = 0, anc1 = 0, anc2 = 0, anc3 = 0;
-  if (warp < 4 && qr < R) {
+  if (warp < NSW && qr < R) {
     const uint64_t *w = a.anc + (qr / a.G) * kAncWords;
     anc0 = w[0];
     anc1 = w[1];
@@ -712,13 +721,13 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
     anc3 = w[3];
   }
   static_assert(kAncWords == 4, "ancestor words are kept in 4 registers");
-  if (warp == 5) tmem_alloc<TCOLS>(tslot);
+  if (warp == NSW + 1) tmem_alloc<TCOLS>(tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;  // S0: cols [0, KEYS), S1: [KEYS, 2 KEYS), O: [2 KEYS, 2 KEYS + 128)
 
-  if (warp == 4) {
+  if (warp == NSW) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       pdl_wait();
@@ -748,7 +757,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
           prefetch_l2_bulk(a.q + (((long long)nsl * a.Nq + n) * a.H + (long long)nh * a.G) * HD, a.G * HD * 2);
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == NSW + 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0 && ntiles > 0) {
       constexpr uint32_t idesc_s = idesc_bf16_major(ROWS, KEYS, 0, 0);  // Q (K-major) x K^T (K-major)
@@ -787,11 +796,12 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
     }
   } else {
     // ------------------------------------------------------------ softmax warps 0..3 (MMA row = TMEM lane)
-    const int r = warp * 32 + lane;  // = cf * RP + (qr - row0)
+    const int r = (warp & 3) * 32 + lane;  // MMA row = TMEM lane (F > 1: cf RP + (qr - row0))
     const bool live = qr < R;
-    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    float *smax = reinterpret_cast<float *>(smem + ks::OFF_SMAX);  // W2: [2 key halves][128 rows]
     pdl_wait();
-    {  // stage Q row qr (every copy) into the K-major SW128 layout
+    if (!W2 || cf == 0) {  // stage Q row qr (every copy) into the K-major SW128 layout
       const uint4 *src = nullptr;
       if (live) {
         const int n = qr / a.G, gg = qr % a.G;
@@ -808,7 +818,9 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
     }
     const int Nq = a.Nq;
     float m_run = -INFINITY, l = 0.f;
-    const bool warp_live = row0 + (warp * 32) % RP < R;  // warps of padding rows only keep the handshakes
+    // warps of padding rows only keep the handshakes (W2: they run the tile loop, whose named barriers
+    // count every softmax warp; their rows are never written)
+    const bool warp_live = W2 || row0 + ((warp & 3) * 32) % RP < R;
     for (int i = 0; i < ntiles; ++i) {
       const int sb = i & 1;
       mbar_wait(&s_full[sb], (i >> 1) & 1);
@@ -868,7 +880,12 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
         mx2 = fmaxf(mx2, y[j + 2]);
         mx3 = fmaxf(mx3, y[j + 3]);
       }
-      const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+      float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+      if constexpr (W2) {  // both halves' maxima (every S read of the tile is complete before P is written)
+        smax[cf * 128 + r] = mx;
+        asm volatile("bar.sync 2, 256;" ::: "memory");
+        mx = fmaxf(mx, smax[(cf ^ 1) * 128 + r]);
+      }
       float m_new = m_run, alpha = 1.f;
       bool resc = false;
       if (m_run == -INFINITY) {
@@ -897,7 +914,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
       for (int j = 0; j < KEYS / 2; ++j) pk[j] = (j / (KT / 2) == cf) ? pe[j % (KT / 2)] : 0u;
       l = l * alpha + ((s0 + s1) + (s2 + s3));
       m_run = m_new;
-      if (__any_sync(0xffffffffu, resc) && i > 0) {
+      if (__any_sync(0xffffffffu, resc) && i > 0 && (!W2 || cf == 0)) {
         mbar_wait(&o_done[sb ^ 1], ((i - 1) >> 1) & 1);
         tc_fence_after();
 #pragma unroll 1
@@ -909,8 +926,13 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
           tmem_st32_f(lane_base + 2 * KEYS + c0, o);
         }
       }
-      tmem_st32_u(lane_base + sb * KEYS, pk);  // P(i) over S(i): packed columns [sb KEYS, sb KEYS + KEYS / 2)
-      if constexpr (KEYS == 128) tmem_st32_u(lane_base + sb * KEYS + 32, pk + 32);
+      if constexpr (W2) {
+        tmem_st32_u(lane_base + sb * KEYS + cf * 32, pe);  // this half's 32 packed columns
+        asm volatile("bar.sync 3, 256;" ::: "memory");     // both halves have read smax before its reuse
+      } else {
+        tmem_st32_u(lane_base + sb * KEYS, pk);  // P(i) over S(i): packed columns [sb KEYS, sb KEYS + KEYS / 2)
+        if constexpr (KEYS == 128) tmem_st32_u(lane_base + sb * KEYS + 32, pk + 32);
+      }
       tc_fence_before();
       mbar_arrive(&p_full[sb]);
     }
@@ -922,9 +944,16 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
     // ---- stage this copy's (m, l, O) at MMA row r (ring idle: every MMA and load is complete)
     float *spart = reinterpret_cast<float *>(sKV + ks::OFF_PART);  // [ROWS][HD]
     float *spml = spart + ROWS * HD;                                // [ROWS][2]
-    spml[2 * r] = live ? m_run : -INFINITY;
-    spml[2 * r + 1] = live ? l : 0.f;
-    if (warp_live) {
+    if constexpr (W2) {  // the row's sum is the two halves' sums (same running max)
+      if (cf == 1) smax[r] = l;
+      asm volatile("bar.sync 2, 256;" ::: "memory");
+      if (cf == 0) l += smax[r];
+    }
+    if (!W2 || cf == 0) {
+      spml[2 * r] = live ? m_run : -INFINITY;
+      spml[2 * r + 1] = live ? l : 0.f;
+    }
+    if (warp_live && (!W2 || cf == 0)) {
 #pragma unroll
       for (int c0 = 0; c0 < HD; c0 += 32) {
         float o[32];
@@ -941,7 +970,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
       }
     }
     if (threadIdx.x == 0) KS_TR(6, gtime());
-    asm volatile("bar.sync 1, 128;" ::: "memory");  // the four softmax warps
+    asm volatile("bar.sync 1, %0;" ::"n"(NST) : "memory");  // the softmax warps
     // ---- merge the F copies of query row qr (copy order), threads of copy 0 only
     if (cf == 0 && live) {
       float mq[F], lq[F];
@@ -1068,7 +1097,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ks_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   if (threadIdx.x == 0) KS_TR(5, gtime());
-  if (warp == 5) tmem_dealloc<TCOLS>(tmem);
+  if (warp == NSW + 1) tmem_dealloc<TCOLS>(tmem);
 }
 
 // ============================================================================ K1, persistent row-copy kernel (KSP)
@@ -1093,9 +1122,9 @@ constexpr int SMEM = OFF_ML + 1024 + 1024;
 static_assert(SMEM <= 232448, "K1 (KSP) shared memory");
 }  // namespace ksp
 
-template <int F>
-__global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_constant__ AttnArgs a, int units,
-                                                               int nrb, int dyn) {
+template <int F, bool W2 = false>  // W2: as tree_attn_ks_kernel (F = 1, eight softmax warps)
+__global__ void __launch_bounds__(W2 ? 320 : 192, 1) tree_attn_ksp_kernel(const __grid_constant__ AttnArgs a,
+                                                                         int units, int nrb, int dyn) {
   constexpr int HD = ksp::HD, ROWS = ksp::ROWS, KEYS = ksp::KEYS, STAGES = ksp::STAGES;
   constexpr int HALF = ksp::HALF, TILE = ksp::TILE;
   constexpr int TCOLS = 512;        // S0, S1 (128 columns each), O (128)
@@ -1104,7 +1133,10 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_cons
   // order through a kUq-slot queue: the producer is at most STAGES units ahead (every unit has a tile)
   constexpr int kUq = 8;
   constexpr int RP = ROWS / F;      // rows per copy
-  constexpr int KT = KEYS / F;      // keys per thread per tile
+  constexpr int KT = W2 ? KEYS / 2 : KEYS / F;  // keys per thread per tile
+  constexpr int NSW = W2 ? 8 : 4;   // softmax warps; producer = warp NSW, MMA issuer = warp NSW + 1
+  constexpr int NST = NSW * 32;
+  static_assert(!W2 || F == 1, "W2: 128 live rows");
   static_assert(F == 1 || F == 2 || F == 4, "copies");
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1160,7 +1192,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_cons
     }
   };
   int pre = 0;  // prefix tiles of the first unit issued before the wait
-  if (threadIdx.x == 128) {
+  if (threadIdx.x == NST) {
     tma_prefetch_desc(&a.tmK);
     tma_prefetch_desc(&a.tmV);
     for (int s = 0; s < STAGES; ++s) {
@@ -1169,7 +1201,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_cons
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&s_full[b], 1);
-      mbar_init(&p_full[b], 128);
+      mbar_init(&p_full[b], NST);
       mbar_init(&o_done[b], 1);
     }
     mbar_init(q_full, 128);
@@ -1183,15 +1215,15 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_cons
       ++pre;
     }
   }
-  const int rr_lane = (warp < 4) ? warp * 32 + lane : 0;
-  const int cf = rr_lane / RP;  // copy of this softmax thread
-  if (warp == 5) tmem_alloc<TCOLS>(tslot);
+  const int rr_lane = (warp < NSW) ? (warp & 3) * 32 + lane : 0;
+  const int cf = W2 ? (warp < NSW ? warp >> 2 : 0) : rr_lane / RP;  // copy of this softmax thread (W2: key half)
+  if (warp == NSW + 1) tmem_alloc<TCOLS>(tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;  // S0: [0, 128), S1: [128, 256), O: [256, 384)
 
-  if (warp == 4) {
+  if (warp == NSW) {
     // ------------------------------------------------------------ TMA producer: every unit's tiles, one ring
     if (lane == 0) {
       pdl_wait();
@@ -1224,7 +1256,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_cons
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == NSW + 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc_s = idesc_bf16_major(ROWS, KEYS, 0, 0);  // Q (K-major) x K^T (K-major)
@@ -1273,8 +1305,8 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_cons
     }
   } else {
     // ------------------------------------------------------------ softmax warps 0..3 (MMA row = TMEM lane)
-    const int r = warp * 32 + lane;  // MMA row = cf RP + (query row - row0)
-    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    const int r = (warp & 3) * 32 + lane;  // MMA row = cf RP + (query row - row0) (W2: the quadrant's row)
+    const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     const int Nq = a.Nq;
     pdl_wait();
     long long g0 = 0;
@@ -1289,7 +1321,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_cons
       const Unit x = unit_of(u);
       const int qr = x.row0 + r % RP;  // this thread's query row
       const bool live = qr < R;
-      const bool warp_live = x.row0 + (warp * 32) % RP < R;
+      const bool warp_live = W2 || x.row0 + ((warp & 3) * 32) % RP < R;  // W2: every warp keeps the barriers
       if (x.row0 != anc_row0) {  // ancestor words of the row's node (static tree tables)
         anc_row0 = x.row0;
         anc0 = anc1 = anc2 = anc3 = 0;
@@ -1301,7 +1333,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_cons
           anc3 = w[3];
         }
       }
-      {  // stage Q row qr (every copy) into the K-major SW128 layout (the buffer is free: see the epilogue)
+      if (!W2 || cf == 0) {  // stage Q row qr (every copy) into the K-major SW128 layout (buffer free: epilogue)
         const uint4 *src = nullptr;
         if (live) {
           const int n = qr / a.G, gg = qr % a.G;
@@ -1376,7 +1408,12 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_cons
           mx2 = fmaxf(mx2, y[j + 2]);
           mx3 = fmaxf(mx3, y[j + 3]);
         }
-        const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+        float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+        if constexpr (W2) {  // both halves' maxima (sml doubles as the exchange buffer outside the epilogue)
+          sml[cf * 128 + r] = mx;
+          asm volatile("bar.sync 2, 256;" ::: "memory");
+          mx = fmaxf(mx, sml[(cf ^ 1) * 128 + r]);
+        }
         float m_new = m_run, alpha = 1.f;
         bool resc = false;
         if (m_run == -INFINITY) {
@@ -1405,7 +1442,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_cons
         for (int j = 0; j < KEYS / 2; ++j) pk[j] = (j / (KT / 2) == cf) ? pe[j % (KT / 2)] : 0u;
         l = l * alpha + ((s0 + s1) + (s2 + s3));
         m_run = m_new;
-        if (__any_sync(0xffffffffu, resc) && i > 0) {
+        if (__any_sync(0xffffffffu, resc) && i > 0 && (!W2 || cf == 0)) {
           mbar_wait(&o_done[(g - 1) & 1], (int)(((g - 1) >> 1) & 1));
           tc_fence_after();
 #pragma unroll 1
@@ -1417,8 +1454,13 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_cons
             tmem_st32_f(lane_base + 2 * KEYS + c0, o);
           }
         }
-        tmem_st32_u(lane_base + sb * KEYS, pk);
-        tmem_st32_u(lane_base + sb * KEYS + 32, pk + 32);
+        if constexpr (W2) {
+          tmem_st32_u(lane_base + sb * KEYS + cf * 32, pe);  // this half's 32 packed columns
+          asm volatile("bar.sync 3, 256;" ::: "memory");     // both halves have read the exchange slots
+        } else {
+          tmem_st32_u(lane_base + sb * KEYS, pk);
+          tmem_st32_u(lane_base + sb * KEYS + 32, pk + 32);
+        }
         tc_fence_before();
         mbar_arrive(&p_full[sb]);
       }
@@ -1429,13 +1471,21 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_cons
       }
       // ---- epilogue: (m, l) of every MMA row; O staged in the Q buffer one 64-column half at a time
       // ([128][64] fp32 = 32 KB, 16-byte chunks XOR-swizzled by row), merged by the copy-0 threads
-      sml[2 * r] = live ? m_run : -INFINITY;
-      sml[2 * r + 1] = live ? l : 0.f;
+      if constexpr (W2) {  // the row's sum is the two halves' sums (same running max)
+        if (cf == 1) sml[128 + r] = l;
+        asm volatile("bar.sync 2, 256;" ::: "memory");
+        if (cf == 0) l += sml[128 + r];
+        asm volatile("bar.sync 2, 256;" ::: "memory");
+      }
+      if (!W2 || cf == 0) {
+        sml[2 * r] = live ? m_run : -INFINITY;
+        sml[2 * r + 1] = live ? l : 0.f;
+      }
       float *spart = reinterpret_cast<float *>(sQ);
       bf16 *dst = a.out + (((long long)x.sl * Nq + qr / a.G) * a.H + (long long)x.h * a.G + qr % a.G) * HD;
 #pragma unroll 1
       for (int half = 0; half < 2; ++half) {
-        if (warp_live) {
+        if (warp_live && (!W2 || cf == 0)) {
 #pragma unroll
           for (int c0 = 0; c0 < 64; c0 += 32) {
             float o[32];
@@ -1446,11 +1496,11 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_cons
                   make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
           }
         }
-        if (half == 1) {  // every O column has been read: the next unit's first PV may overwrite it
+        if (half == 1 && (!W2 || cf == 0)) {  // every O column has been read: the next unit's first PV may overwrite it
           tc_fence_before();
           mbar_arrive(o_free);
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // the four softmax warps
+        asm volatile("bar.sync 1, %0;" ::"n"(NST) : "memory");  // the softmax warps
         if (cf == 0 && live) {  // merge the F copies of row qr (copy order), as tree_attn_ks_kernel
           float mq[F], lq[F];
 #pragma unroll
@@ -1486,7 +1536,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_cons
             *reinterpret_cast<uint2 *>(dst + half * 64 + 4 * c4) = pk2;
           }
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // staging buffer (then Q) reused
+        asm volatile("bar.sync 1, %0;" ::"n"(NST) : "memory");  // staging buffer (then Q) reused
       }
       g0 += x.ntiles;
     }
@@ -1494,7 +1544,7 @@ __global__ void __launch_bounds__(192, 1) tree_attn_ksp_kernel(const __grid_cons
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 5) tmem_dealloc<TCOLS>(tmem);
+  if (warp == NSW + 1) tmem_dealloc<TCOLS>(tmem);
 }
 
 // ============================================================================ K1, stream-K ("lean") variant
@@ -2095,6 +2145,10 @@ int attention_tc_nsplit(int units, int cap) {
 // neutral elsewhere); bit 0 (the CTA's own range at entry) measured 5-40 % slower (it floods the
 // memory system ahead of the ring's own loads) and stays off
 static int g_attn_l2ahead = 2;
+// sm_set_option("attn_w2"): row-copy kernels with 128 live rows on 8 softmax warps (1, default: 5-10 % on those
+// launches, profiles/r02/k1_experiments.txt) or 4 (0)
+static int g_attn_w2 = 1;
+void attention_set_w2(int on) { g_attn_w2 = on; }
 void attention_set_l2ahead(int mode) { g_attn_l2ahead = mode & 3; }
 // sm_set_option("attn_ksp"): persistent row-copy kernel when a one-split launch has more units than SMs (1,
 // default: 3-14 % faster on every multi-wave C5 point, profiles/r02/k1_experiments.txt) or never (0)
@@ -2136,7 +2190,8 @@ cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
     if (!ks_attr) {
       const auto A = cudaFuncAttributeMaxDynamicSharedMemorySize;
       cudaError_t e = cudaSuccess;
-      for (auto fn : {tree_attn_ks_kernel<4, 128>, tree_attn_ks_kernel<2, 128>, tree_attn_ks_kernel<1, 128>})
+      for (auto fn : {tree_attn_ks_kernel<4, 128>, tree_attn_ks_kernel<2, 128>, tree_attn_ks_kernel<1, 128>,
+                      tree_attn_ks_kernel<1, 128, true>})
         if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, A, ks::SMEM);
       if (e != cudaSuccess) return e;
       ks_attr = true;
@@ -2148,7 +2203,8 @@ cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
       if (!ksp_attr) {
         const auto A = cudaFuncAttributeMaxDynamicSharedMemorySize;
         cudaError_t e = cudaSuccess;
-        for (auto fn : {tree_attn_ksp_kernel<4>, tree_attn_ksp_kernel<2>, tree_attn_ksp_kernel<1>})
+        for (auto fn : {tree_attn_ksp_kernel<4>, tree_attn_ksp_kernel<2>, tree_attn_ksp_kernel<1>,
+                        tree_attn_ksp_kernel<1, true>})
           if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, A, ksp::SMEM);
         if (e != cudaSuccess) return e;
         ksp_attr = true;
@@ -2159,6 +2215,10 @@ cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
       const int dyn = g_attn_ksp == 3 ? 0 : 1;
       if (R <= 32) return cudaLaunchKernelEx(&cfg, tree_attn_ksp_kernel<4>, a, units, nrb, dyn);
       if (R <= 64) return cudaLaunchKernelEx(&cfg, tree_attn_ksp_kernel<2>, a, units, nrb, dyn);
+      if (g_attn_w2) {
+        cfg.blockDim = dim3(320);
+        return cudaLaunchKernelEx(&cfg, tree_attn_ksp_kernel<1, true>, a, units, nrb, dyn);
+      }
       return cudaLaunchKernelEx(&cfg, tree_attn_ksp_kernel<1>, a, units, nrb, dyn);
     }
     cfg.dynamicSmemBytes = ks::SMEM;
@@ -2166,6 +2226,10 @@ cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
     b.l2_ahead = (a.k_base && a.v_base) ? g_attn_l2ahead : 0;
     if (R <= 32) return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<4, 128>, b);
     if (R <= 64) return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<2, 128>, b);
+    if (g_attn_w2) {  // two softmax warps per row (W2)
+      cfg.blockDim = dim3(320);
+      return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<1, 128, true>, b);
+    }
     return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<1, 128>, b);  // ceil(R / 128) row blocks (grid y)
   }
   if (a.causal) return cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<true>, a);

@@ -1986,6 +1986,7 @@ extern "C" sm_status sm_reset_options(void) {
   attention_set_l2ahead(2);
   attention_set_ksp(1);
   attention_set_split_model(1);
+  attention_set_w2(1);
   attention_set_lean_div(16);
   tp_set_rsag(-1);
   g_fused = 0;
@@ -2042,6 +2043,8 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
     attention_set_lean(value);
   } else if (n == "attn_l2ahead") {  // K1 row-copy kernel: L2 prefetch ahead of the ring (bit 0 own range, bit 1 next wave)
     attention_set_l2ahead(value);
+  } else if (n == "attn_w2") {  // K1 row-copy kernel, 128 live rows: two softmax warps per row (1) or one (0)
+    attention_set_w2(value);
   } else if (n == "attn_split_model") {  // K1 key splits: 1 occupancy-aware cost model (default), 0 round-1 rule
     attention_set_split_model(value);
   } else if (n == "attn_ksp") {  // K1: persistent row-copy kernel for one-split launches with > 148 units
