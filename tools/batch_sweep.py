@@ -68,10 +68,15 @@ def run(b, mode):
     return ms, tok / STEPS / (ms / 1e3), slots / tok
 
 
+for kv_opt in filter(None, os.environ.get("SM_OPT", "").split(",")):  # experiment knobs (sm_set_option)
+    k_, v_ = kv_opt.split("=")
+    sm.set_option(k_, int(v_))
+BS = [int(x) for x in os.environ.get("BATCH_SIZES", "1,2,4,8,10").split(",")]
+MODES = os.environ.get("BATCH_MODES", "vanilla,ragged,pad").split(",")
 print("# f4: batched speculative decoding, ragged vs pad batching (P:253-256) vs vanilla; Vicuna-7B shape, V64,")
 print("# imposed acceptance depth (s mod 5) per sequence s; ms/step, tokens/s, cache slots per committed token")
 print(f"{'bs':>3s} {'mode':8s} {'ms/step':>8s} {'tok/s':>9s} {'slots/tok':>9s}")
-for b in (1, 2, 4, 8, 10):
-    for mode in ("vanilla", "ragged", "pad"):
+for b in BS:
+    for mode in MODES:
         ms, tps, spt = run(b, mode)
         print(f"{b:3d} {mode:8s} {ms:8.3f} {tps:9.1f} {spt:9.2f}", flush=True)
