@@ -721,6 +721,20 @@ __global__ void __launch_bounds__(W2 ? 320 : 192, 1) tree_attn_ks_kernel(const _
     anc3 = w[3];
   }
   static_assert(kAncWords == 4, "ancestor words are kept in 4 registers");
+  // Q row qr in registers before the CTA barrier (option attn_qearly): its load latency overlaps the barrier
+  // and the TMEM allocation; staged into shared memory after the barrier (which publishes q_full's init)
+  uint4 qv[16];
+  const bool qearly = a.q_early && warp < NSW && (!W2 || cf == 0);
+  if (qearly) {
+    pdl_wait();
+    const uint4 *src = nullptr;
+    if (qr < R) {
+      const int n = qr / a.G, gg = qr % a.G;
+      src = reinterpret_cast<const uint4 *>(a.q + (((long long)sl * a.Nq + n) * a.H + (long long)h * a.G + gg) * HD);
+    }
+#pragma unroll
+    for (int c = 0; c < 16; ++c) qv[c] = qr < R ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
+  }
   if (warp == NSW + 1) tmem_alloc<TCOLS>(tslot);
   tc_fence_before();
   __syncthreads();
@@ -800,16 +814,21 @@ __global__ void __launch_bounds__(W2 ? 320 : 192, 1) tree_attn_ks_kernel(const _
     const bool live = qr < R;
     const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     float *smax = reinterpret_cast<float *>(smem + ks::OFF_SMAX);  // W2: [2 key halves][128 rows]
-    pdl_wait();
+    if (!qearly) pdl_wait();
     if (!W2 || cf == 0) {  // stage Q row qr (every copy) into the K-major SW128 layout
-      const uint4 *src = nullptr;
-      if (live) {
-        const int n = qr / a.G, gg = qr % a.G;
-        src = reinterpret_cast<const uint4 *>(a.q + (((long long)sl * a.Nq + n) * a.H + (long long)h * a.G + gg) * HD);
-      }
       uint4 v[16];
+      if (qearly) {
 #pragma unroll
-      for (int c = 0; c < 16; ++c) v[c] = live ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
+        for (int c = 0; c < 16; ++c) v[c] = qv[c];
+      } else {
+        const uint4 *src = nullptr;
+        if (live) {
+          const int n = qr / a.G, gg = qr % a.G;
+          src = reinterpret_cast<const uint4 *>(a.q + (((long long)sl * a.Nq + n) * a.H + (long long)h * a.G + gg) * HD);
+        }
+#pragma unroll
+        for (int c = 0; c < 16; ++c) v[c] = live ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
+      }
       const uint32_t q_u = smem_u32(sQ);
 #pragma unroll
       for (int c = 0; c < 16; ++c) st_shared_v4(q_u + (c >> 3) * 16384 + sw128_off(r, c), v[c].x, v[c].y, v[c].z, v[c].w);
@@ -2148,6 +2167,10 @@ static int g_attn_l2ahead = 2;
 // sm_set_option("attn_w2"): row-copy kernels with 128 live rows on 8 softmax warps (1, default: 5-10 % on those
 // launches, profiles/r02/k1_experiments.txt) or 4 (0)
 static int g_attn_w2 = 1;
+// sm_set_option("attn_qearly"): row-copy kernel loads Q before its CTA barrier (1, default: 0-3 %, never slower,
+// profiles/r02/k1_experiments.txt) or after it (0)
+static int g_attn_qearly = 1;
+void attention_set_qearly(int on) { g_attn_qearly = on; }
 void attention_set_w2(int on) { g_attn_w2 = on; }
 void attention_set_l2ahead(int mode) { g_attn_l2ahead = mode & 3; }
 // sm_set_option("attn_ksp"): persistent row-copy kernel when a one-split launch has more units than SMs (1,
@@ -2224,6 +2247,7 @@ cudaError_t attention_tc_launch(const AttnArgs &a, cudaStream_t st) {
     cfg.dynamicSmemBytes = ks::SMEM;
     AttnArgs b = a;
     b.l2_ahead = (a.k_base && a.v_base) ? g_attn_l2ahead : 0;
+    b.q_early = g_attn_qearly;
     if (R <= 32) return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<4, 128>, b);
     if (R <= 64) return cudaLaunchKernelEx(&cfg, tree_attn_ks_kernel<2, 128>, b);
     if (g_attn_w2) {  // two softmax warps per row (W2)

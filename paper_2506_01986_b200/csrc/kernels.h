@@ -362,6 +362,7 @@ struct AttnArgs {
   // the first ring's worth of the CTA one wave later (set by attention_tc_launch from the option)
   const bf16 *k_base, *v_base;
   int l2_ahead;
+  int q_early;  // row-copy kernel: Q loads issued before the CTA barrier (set by attention_tc_launch)
 };
 cudaError_t attention_launch(const AttnArgs &a, int head_dim, cudaStream_t st);
 int attention_row_blocks(int Nq, int G, int head_dim);
@@ -380,6 +381,7 @@ void attention_set_l2ahead(int mode);
 void attention_set_ksp(int on);
 void attention_set_split_model(int m);
 void attention_set_w2(int on);
+void attention_set_qearly(int on);
 void attention_set_lean_div(int d);
 int attention_lean_min_tiles(int Nq, int G);
 void attention_set_splits(int n);               // experiments: force key splits (0 = auto)

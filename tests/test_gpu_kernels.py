@@ -149,7 +149,7 @@ ATTN_CASES = [
 # K1 variants for head_dim 128: the stream-K tcgen05 kernel (default; min tiles per CTA = live rows
 # per unit / 16, and / 2 for many more pieces per unit), the cluster-split tcgen05 kernel, mma.sync
 VARIANTS = {"default": dict(), "ns3": dict(attn_splits=3), "ns7": dict(attn_splits=7),
-            "rule_splits": dict(attn_split_model=0), "w2": dict(attn_w2=1), "ksp": dict(attn_ksp=1), "noksp": dict(attn_ksp=0), "rows128": dict(attn_ks=0), "ks64": dict(attn_ks=1), "ns1": dict(attn_splits=1),
+            "rule_splits": dict(attn_split_model=0), "w2": dict(attn_w2=1), "qlate": dict(attn_qearly=0), "ksp": dict(attn_ksp=1), "noksp": dict(attn_ksp=0), "rows128": dict(attn_ks=0), "ks64": dict(attn_ks=1), "ns1": dict(attn_splits=1),
             "lean": dict(attn_tc=1, attn_lean=1),
             "lean_div2": dict(attn_tc=1, attn_lean=1, attn_lean_div=2), "mma": dict(attn_tc=0)}
 

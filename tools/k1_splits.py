@@ -47,6 +47,8 @@ if os.environ.get("K1_VARS") == "ks":  # 128-row kernel vs key-split row packing
     VARS = [("rows128", dict(attn_lean=0, attn_ks=0)), ("ks", dict(attn_lean=0, attn_ks=2))]
 elif os.environ.get("K1_VARS") == "ksp":  # one-unit-per-CTA row-copy kernel vs the persistent one (units > 148)
     VARS = [("ks", dict(attn_ksp=0)), ("ksp", dict(attn_ksp=1))]
+elif os.environ.get("K1_VARS") == "qearly":  # row-copy kernel: Q loads before vs after the CTA barrier
+    VARS = [("late", dict(attn_qearly=0)), ("early", dict(attn_qearly=1))]
 elif os.environ.get("K1_VARS") == "w2":  # 128 live rows: one vs two softmax warps per row
     VARS = [("w1", dict(attn_w2=0)), ("w2", dict(attn_w2=1))]
 elif os.environ.get("K1_VARS") == "split":  # key-split count: round-1 rule vs occupancy-aware cost model
