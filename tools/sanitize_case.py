@@ -1,5 +1,6 @@
 """One small speculative decode for compute-sanitizer (tools/sanitize.sh): c1 = the tiny
-C1 model (mma.sync K1, hd 16); s128 = a hd-128 model (tcgen05 K1 with split-KV cluster
+C1 model (mma.sync K1, hd 16); k1new = the session-3 K1 kernels (persistent KSP, two softmax warps per row, odd
+split counts, early Q); tp2emu = t = 2 tensor parallelism in the host-ordered emulation; s128 = a hd-128 model (tcgen05 K1 with split-KV cluster
 combine, tcgen05 K2, 2 sequences, prefill + 6 greedy steps with compaction); pp2 = the
 layer-split pipeline (two stages on one GPU, host-ordered emulation: residual hand-offs joined by
 events, one host thread per stage); pad = s128 in pad
@@ -39,6 +40,51 @@ if case == "pp2":
     each(lambda r, s: kvs[r].prefill(0, pt, stream=s))
     for _ in range(4):
         each(lambda r, s: kvs[r].step(sm.accept_cfg(sm.GREEDY), outs[r], stream=s))
+    print("lengths", [kv.lengths().tolist() for kv in kvs], "timed out", [m.tp_timed_out() for m in models])
+    sys.exit(0)
+if case == "k1new":  # session-3 K1 paths through the stage entry: persistent KSP (160 units, F = 2 and W2
+    # F = 1), the row-copy kernel with W2 and an odd split count, early Q loads
+    hd = 128
+    for (b, H, Hkv, N, Lc, splits) in [(5, 32, 32, 64, 300, 0), (10, 128, 16, 16, 200, 0), (2, 16, 2, 64, 700, 3),
+                                       (1, 8, 1, 16, 2000, 7)]:
+        tree = sm.Tree(synth.V64) if N == 64 else sm.Tree(synth.TINY16, topk=10)
+        sm.set_option("attn_splits", splits)
+        cap = Lc + tree.N + 5
+        q = torch.randn(b, tree.N, H, hd, device="cuda").bfloat16()
+        k = torch.randn(b, Hkv, cap, hd, device="cuda").bfloat16()
+        v = torch.randn(b, Hkv, cap, hd, device="cuda").bfloat16()
+        o = torch.empty_like(q)
+        L = torch.tensor([Lc - 13 * i for i in range(b)], dtype=torch.int32, device="cuda")
+        for _ in range(2):
+            sm.tree_attention(tree, q, k, v, L, H, Hkv, o)
+        torch.cuda.synchronize()
+        print("k1", b, H, Hkv, tree.N, Lc, splits, bool(torch.isfinite(o.float()).all()))
+    sys.exit(0)
+if case == "tp2emu":  # tensor parallel t = 2 in the host-ordered emulation (segment launches + event joins)
+    cfg, X = synth.model_cfg("tiny"), 64
+    tree = sm.Tree(synth.TINY16, topk=10)
+    sym = [torch.zeros(sm.tp_sym_bytes(cfg, 64, 1, 3), dtype=torch.uint8, device="cuda") for _ in range(2)]
+    ptrs = [t.data_ptr() for t in sym]
+    emu = sm.EmuGroup(2)
+    Ws = [sm.allocate_weights(cfg, 3, seed=1, tp_rank=r, tp_size=2) for r in range(2)]
+    models = [sm.Model(cfg, Ws[r], 64, 1, X + tree.N, peer_sym=ptrs, emu_group=emu) for r in range(2)]
+    kvs = [sm.KVCache(m, tree, 1, X) for m in models]
+    sts = [torch.cuda.Stream() for _ in range(2)]
+    outs = [sm.AcceptOut(1, tree.depth) for _ in range(2)]
+    torch.cuda.synchronize()
+    pt = torch.from_numpy(synth.prompt_tokens(1, 0, 32, cfg["vocab"])).cuda()
+
+    def each2(fn):
+        def go(r):
+            def body():
+                with torch.cuda.stream(sts[r]):
+                    fn(r, sts[r])
+            return body
+        sm.run_ranks([go(r) for r in range(2)])
+        torch.cuda.synchronize()
+    each2(lambda r, s: kvs[r].prefill(0, pt, stream=s))
+    for _ in range(4):
+        each2(lambda r, s: kvs[r].step(sm.accept_cfg(sm.GREEDY), outs[r], stream=s))
     print("lengths", [kv.lengths().tolist() for kv in kvs], "timed out", [m.tp_timed_out() for m in models])
     sys.exit(0)
 if case == "c1":
