@@ -35,7 +35,8 @@ typedef enum {
   SM_ERR_KV_CAPACITY = 3,      /* prefill / verify would exceed the bound x (OOM reason "Cache") */
   SM_ERR_DEVICE_OOM = 4,       /* workspace allocation failed (reason Model|Cache|Buffer)        */
   SM_ERR_CUDA = 5,
-  SM_ERR_NCCL = 6,
+  SM_ERR_NCCL = 6,              /* reserved: the exchanges are the library's own peer-memory kernels (no
+                                  * NCCL; a wait that times out is reported by sm_tp_status instead)   */
   SM_ERR_UNSUPPORTED = 7
 } sm_status;
 
