@@ -49,6 +49,9 @@ K1_CASES = [
     # name, b, H, Hkv, lens, samples
     ("geomA_k1_point", 8, 32, 32, [4096] * 8, 40),
     ("geomB_tp8_ragged", 2, 8, 1, [32768, 1111], 40),
+    # 40 sequences x 4 row blocks = 160 units of 128 live rows: the persistent kernel with two softmax warps
+    # per row (KSP, W2), ragged lengths
+    ("geomB_ksp_w2", 40, 8, 1, [4096 - 37 * i for i in range(40)], 40),
 ]
 
 
