@@ -20,7 +20,7 @@ import synth  # noqa: E402
 
 cfg = synth.model_cfg("vicuna7b")
 W = sm.allocate_weights(cfg, 4, seed=0)
-STEPS, X = 30, 2048
+STEPS, X = int(os.environ.get("BATCH_STEPS", "30")), 2048
 tree = sm.Tree(synth.V64)
 q = tree.query()
 depth, parent = q["node_depth"], q["parent"]
