@@ -25,6 +25,12 @@ namespace sm {
 
 // Block size of the qkv / SiLU consumers (sm_set_option "consumer_threads", experiments: 128 or 256).
 static int g_consumer_threads = 256;
+// sm_set_option("consumer_rpc"): token rows per CTA of the QKV / SiLU / residual consumers for M >= 256 (2,
+// default: 64-72 registers, four CTAs per SM instead of two -- the bs 10 step's consumers ran in waves of 296
+// CTAs, tools/gtrace.py GT_BATCH=10; 7B bs 4 / 8 / 10 steps 4-6 % faster; 4 = round 2's four rows, 1 = the
+// one-row kernels)
+static int g_consumer_rpc = 2;
+void consumer_set_rpc(int n) { g_consumer_rpc = n; }
 void consumer_set_threads(int n) { g_consumer_threads = n == 128 ? 128 : 256; }
 
 template <int NT>
@@ -166,16 +172,19 @@ __global__ void __launch_bounds__(kNormThreads) resid_norm_split_kernel(PartialV
 }
 // M >= 256: four token rows per CTA, every partial and residual load issued up front (see the
 // SiLU consumer); per-row sums reduced in the same warp-then-block order as block_sum.
+template <int RPC>
 __global__ void __launch_bounds__(kNormThreads) resid_norm_split4_kernel(PartialView pv, int has_pv, float *x,
                                                                          const bf16 *g, bf16 *h, int d, int M, int hp,
                                                                          float *ss_out) {
-  constexpr int RPC = 4, NM = 4;
+  constexpr int NM = 4;
   __shared__ float red[RPC][kNormThreads / 32];
   pdl_trigger();
   pdl_wait();
   const int rank = blockIdx.x, cs = gridDim.x, m0 = blockIdx.y * RPC;
   const int i = rank * kNormCols + threadIdx.x * 4;
-  float sq[RPC] = {0.f, 0.f, 0.f, 0.f};
+  float sq[RPC];
+#pragma unroll
+  for (int q = 0; q < RPC; ++q) sq[q] = 0.f;
   if (i < d) {
     SkRef ref[RPC];
     float4 ys[RPC][NM], a[RPC];
@@ -227,8 +236,11 @@ cudaError_t resid_norm_split_launch(const PartialView *pv, float *x, const bf16 
   if (d % 4) return cudaErrorInvalidValue;
   PartialView v{};
   if (pv) v = *pv;
-  if (M >= 256 && v.planes <= 1)
-    return launch_pdl(resid_norm_split4_kernel, dim3(cs, (M + 3) / 4), dim3(kNormThreads), 0, st, v, pv ? 1 : 0, x,
+  if (M >= 256 && v.planes <= 1 && g_consumer_rpc == 2)
+    return launch_pdl(resid_norm_split4_kernel<2>, dim3(cs, (M + 1) / 2), dim3(kNormThreads), 0, st, v, pv ? 1 : 0, x,
+                      g, h, d, M, hp, ss);
+  if (M >= 256 && v.planes <= 1 && g_consumer_rpc == 4)
+    return launch_pdl(resid_norm_split4_kernel<4>, dim3(cs, (M + 3) / 4), dim3(kNormThreads), 0, st, v, pv ? 1 : 0, x,
                       g, h, d, M, hp, ss);
   return launch_pdl(resid_norm_split_kernel, dim3(cs, M), dim3(kNormThreads), 0, st, v, pv ? 1 : 0, x, g, h, d, hp,
                     ss);
@@ -569,7 +581,10 @@ cudaError_t qkv_consumer_launch(const PartialView &pv, RowCtx rc, int H, int Hkv
   if (pv.planes > 1)
     return launch_pdl(qkv_consumer_kernel<true>, dim3(gx, rc.M), dim3(nt), 0, st, pv, rc, H, Hkv, hd, rope, q,
                       kcache, vcache, cap, rs);
-  if (rc.M >= 256)
+  if (rc.M >= 256 && g_consumer_rpc == 2)
+    return launch_pdl(qkv_consumer_rows_kernel<false, 2>, dim3(gx, (rc.M + 1) / 2), dim3(nt), 0, st, pv, rc, H, Hkv,
+                      hd, rope, q, kcache, vcache, cap, rs);
+  if (rc.M >= 256 && g_consumer_rpc == 4)
     return launch_pdl(qkv_consumer_rows_kernel<false, 4>, dim3(gx, (rc.M + 3) / 4), dim3(nt), 0, st, pv, rc, H, Hkv,
                       hd, rope, q, kcache, vcache, cap, rs);
   return launch_pdl(qkv_consumer_kernel<false>, dim3(gx, rc.M), dim3(nt), 0, st, pv, rc, H, Hkv, hd, rope, q,
@@ -658,7 +673,9 @@ __global__ void __launch_bounds__(256) silu_consumer_rows_kernel(PartialView pv,
 cudaError_t silu_consumer_launch(const PartialView &pv, int F, bf16 *act, RsArgs rs, cudaStream_t st) {
   const int nt = g_consumer_threads;
   const int gx = (F / 4 + nt - 1) / nt;
-  if (pv.M >= 256 && pv.planes <= 1)
+  if (pv.M >= 256 && pv.planes <= 1 && g_consumer_rpc == 2)
+    return launch_pdl(silu_consumer_rows_kernel<2>, dim3(gx, (pv.M + 1) / 2), dim3(nt), 0, st, pv, F, act, rs);
+  if (pv.M >= 256 && pv.planes <= 1 && g_consumer_rpc == 4)
     return launch_pdl(silu_consumer_rows_kernel<4>, dim3(gx, (pv.M + 3) / 4), dim3(nt), 0, st, pv, F, act, rs);
   return launch_pdl(silu_consumer_kernel, dim3(gx, pv.M), dim3(nt), 0, st, pv, F, act, rs);
 }
@@ -994,12 +1011,15 @@ void epilogue_preload() {  // force-load (see gemm_preload)
   cudaFuncGetAttributes(&fa, resid_norm_tp_kernel<false>);
   cudaFuncGetAttributes(&fa, resid_norm_tp_kernel<true>);
   cudaFuncGetAttributes(&fa, resid_norm_split_kernel);
-  cudaFuncGetAttributes(&fa, resid_norm_split4_kernel);
+  cudaFuncGetAttributes(&fa, resid_norm_split4_kernel<4>);
+  cudaFuncGetAttributes(&fa, resid_norm_split4_kernel<2>);
   cudaFuncGetAttributes(&fa, qkv_consumer_kernel<false>);
   cudaFuncGetAttributes(&fa, qkv_consumer_kernel<true>);
   cudaFuncGetAttributes(&fa, qkv_consumer_rows_kernel<false, 4>);
   cudaFuncGetAttributes(&fa, silu_consumer_kernel);
   cudaFuncGetAttributes(&fa, silu_consumer_rows_kernel<4>);
+  cudaFuncGetAttributes(&fa, silu_consumer_rows_kernel<2>);
+  cudaFuncGetAttributes(&fa, qkv_consumer_rows_kernel<false, 2>);
   cudaFuncGetAttributes(&fa, logits_kernel<true>);
   cudaFuncGetAttributes(&fa, logits_kernel<false>);
   cudaFuncGetAttributes(&fa, topk_kernel<true, 10>);

@@ -1988,6 +1988,7 @@ extern "C" sm_status sm_reset_options(void) {
   attention_set_split_model(1);
   attention_set_w2(1);
   attention_set_qearly(1);
+  consumer_set_rpc(2);
   attention_set_lean_div(16);
   tp_set_rsag(-1);
   g_fused = 0;
@@ -2044,6 +2045,8 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
     attention_set_lean(value);
   } else if (n == "attn_l2ahead") {  // K1 row-copy kernel: L2 prefetch ahead of the ring (bit 0 own range, bit 1 next wave)
     attention_set_l2ahead(value);
+  } else if (n == "consumer_rpc") {  // token rows per CTA of the QKV / SiLU consumers for M >= 256 (experiments)
+    consumer_set_rpc(value);
   } else if (n == "attn_qearly") {  // K1 row-copy kernel: Q loads before the CTA barrier (1) or after (0)
     attention_set_qearly(value);
   } else if (n == "attn_w2") {  // K1 row-copy kernel, 128 live rows: two softmax warps per row (1) or one (0)

@@ -25,10 +25,12 @@ for kv_opt in filter(None, os.environ.get("SM_OPT", "").split(",")):
 cfg = synth.model_cfg("vicuna7b")
 tree = sm.Tree(synth.V64)
 W = sm.allocate_weights(cfg, 4, seed=0)
-model = sm.Model(cfg, W, max_rows=256, max_batch=1, max_seq_len=2048 + tree.N)
-kv = sm.KVCache(model, tree, 1, 2048)
-kv.prefill(0, torch.from_numpy(synth.prompt_tokens(0, 0, 1024, cfg["vocab"])).cuda())
-out = sm.AcceptOut(1, tree.depth)
+B = int(os.environ.get("GT_BATCH", "1"))  # GT_BATCH=10: the batched step (M = 640)
+model = sm.Model(cfg, W, max_rows=max(256, B * tree.N), max_batch=B, max_seq_len=2048 + tree.N)
+kv = sm.KVCache(model, tree, B, 2048)
+for i in range(B):
+    kv.prefill(i, torch.from_numpy(synth.prompt_tokens(0, i, 1024 if B == 1 else 512 + 16 * i, cfg["vocab"])).cuda())
+out = sm.AcceptOut(B, tree.depth)
 acfg = sm.accept_cfg(sm.GREEDY)
 for _ in range(4):
     kv.step(acfg, out)
