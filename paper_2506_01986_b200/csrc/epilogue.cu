@@ -30,6 +30,16 @@ static int g_consumer_threads = 256;
 // CTAs, tools/gtrace.py GT_BATCH=10; 7B bs 4 / 8 / 10 steps 4-6 % faster; 4 = round 2's four rows, 1 = the
 // one-row kernels)
 static int g_consumer_rpc = 2;
+// sm_set_option("consumer_nm"): contributors loaded up front by the one-row QKV / SiLU consumers (4, default:
+// 62-64 registers instead of 78-79, so a consumer CTA and two CTAs of the next GEMM share an SM -- C2 step 3.768
+// -> 3.723 ms, interleaved; their GEMMs have <= 5 contributors per tile, more are loaded serially), or 8
+static int g_consumer_nm = 4;
+void consumer_set_nm(int n) { g_consumer_nm = n == 8 ? 8 : 4; }
+// sm_set_option("resid_nm"): the same for the one-row residual consumer (8, default: 64 registers instead of 93,
+// two CTAs beside the next GEMM's; its GEMMs have ~10 contributors per tile, the rest load serially: C2 step
+// 3.73 -> 3.71 ms, interleaved), or 16
+static int g_resid_nm = 8;
+void resid_set_nm(int n) { g_resid_nm = n == 16 ? 16 : 8; }
 void consumer_set_rpc(int n) { g_consumer_rpc = n; }
 void consumer_set_threads(int n) { g_consumer_threads = n == 128 ? 128 : 256; }
 
@@ -133,6 +143,7 @@ cudaError_t resid_norm_launch(const PartialView *pv, float *x, const bf16 *g, bf
 // Split variant (deferred norm): no cluster exchange -- each CTA's slice sum of squares goes to
 // ss[m][slice] and the next consumer finishes rs (rs_of).  Same arithmetic, same order.
 int resid_norm_slices(int d) { return (d + kNormCols - 1) / kNormCols; }
+template <int NM>
 __global__ void __launch_bounds__(kNormThreads) resid_norm_split_kernel(PartialView pv, int has_pv, float *x,
                                                                         const bf16 *g, bf16 *h, int d, int hp,
                                                                         float *ss_out) {
@@ -146,15 +157,15 @@ __global__ void __launch_bounds__(kNormThreads) resid_norm_split_kernel(PartialV
   float *xr = x + (size_t)m * d;
   float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
   if (i < d) {
-    float4 ys[16];
+    float4 ys[NM];
     SkRef ref{};
     if (has_pv && pv.planes <= 1) {
       ref = sk_ref(pv, 0, m, i);
-      sk_load<16>(ref, ys);
+      sk_load<NM>(ref, ys);
     }
     a = *reinterpret_cast<const float4 *>(xr + i);
     if (has_pv) {
-      const float4 y = pv.planes <= 1 ? sk_reduce<16>(ref, ys) : sk_get4(pv, 0, m, i);  // R5/R7
+      const float4 y = pv.planes <= 1 ? sk_reduce<NM>(ref, ys) : sk_get4(pv, 0, m, i);  // R5/R7
       a.x += y.x;
       a.y += y.y;
       a.z += y.z;
@@ -242,8 +253,11 @@ cudaError_t resid_norm_split_launch(const PartialView *pv, float *x, const bf16 
   if (M >= 256 && v.planes <= 1 && g_consumer_rpc == 4)
     return launch_pdl(resid_norm_split4_kernel<4>, dim3(cs, (M + 3) / 4), dim3(kNormThreads), 0, st, v, pv ? 1 : 0, x,
                       g, h, d, M, hp, ss);
-  return launch_pdl(resid_norm_split_kernel, dim3(cs, M), dim3(kNormThreads), 0, st, v, pv ? 1 : 0, x, g, h, d, hp,
-                    ss);
+  if (g_resid_nm == 8)
+    return launch_pdl(resid_norm_split_kernel<8>, dim3(cs, M), dim3(kNormThreads), 0, st, v, pv ? 1 : 0, x, g, h, d,
+                      hp, ss);
+  return launch_pdl(resid_norm_split_kernel<16>, dim3(cs, M), dim3(kNormThreads), 0, st, v, pv ? 1 : 0, x, g, h, d,
+                    hp, ss);
 }
 
 // Tensor-parallel variant (a7): the residual all-reduce fused in.  Each rank reduces its own
@@ -422,7 +436,7 @@ cudaError_t resid_norm_tp_launch(const PartialView &pv, float *x, const bf16 *g,
 // F32 (fp32 parity mode): q and the K/V cache hold fp32, partial rows come in 3 planes.
 // thread -> 4 consecutive rotary pairs (c .. c+3) of one head of one token row
 // F32 (fp32 parity mode): q and the K/V cache hold fp32, partial rows come in 3 planes.
-template <bool F32>
+template <bool F32, int NM = 8>
 __global__ void __launch_bounds__(256) qkv_consumer_kernel(PartialView pv, RowCtx rc, int H, int Hkv, int hd,
                                                            const float2 *rope, void *q_, void *kc_, void *vc_, int cap,
                                                            RsArgs rs) {
@@ -445,11 +459,11 @@ __global__ void __launch_bounds__(256) qkv_consumer_kernel(PartialView pv, RowCt
     b = sk_get4(pv, 0, m, n0 + half);
   } else {
     const SkRef ra = sk_ref(pv, 0, m, n0), rb = sk_ref(pv, 0, m, n0 + half);
-    float4 xa[8], xb[8];
-    sk_load<8>(ra, xa);
-    sk_load<8>(rb, xb);
-    a = sk_reduce<8>(ra, xa);
-    b = sk_reduce<8>(rb, xb);
+    float4 xa[NM], xb[NM];
+    sk_load<NM>(ra, xa);
+    sk_load<NM>(rb, xb);
+    a = sk_reduce<NM>(ra, xa);
+    b = sk_reduce<NM>(rb, xb);
   }
   const float r = rs_of(rs, m);  // deferred RMSNorm scale of the input row (R2)
   float x0[4] = {a.x * r, a.y * r, a.z * r, a.w * r}, x1[4] = {b.x * r, b.y * r, b.z * r, b.w * r};
@@ -587,12 +601,16 @@ cudaError_t qkv_consumer_launch(const PartialView &pv, RowCtx rc, int H, int Hkv
   if (rc.M >= 256 && g_consumer_rpc == 4)
     return launch_pdl(qkv_consumer_rows_kernel<false, 4>, dim3(gx, (rc.M + 3) / 4), dim3(nt), 0, st, pv, rc, H, Hkv,
                       hd, rope, q, kcache, vcache, cap, rs);
+  if (g_consumer_nm == 4)
+    return launch_pdl(qkv_consumer_kernel<false, 4>, dim3(gx, rc.M), dim3(nt), 0, st, pv, rc, H, Hkv, hd, rope, q,
+                      kcache, vcache, cap, rs);
   return launch_pdl(qkv_consumer_kernel<false>, dim3(gx, rc.M), dim3(nt), 0, st, pv, rc, H, Hkv, hd, rope, q,
                     kcache, vcache, cap, rs);
 }
 
 // ------------------------------------------------------------------ SiLU(gate) * up
 // fused weight rows: tile t = [gate 64t..64t+63 | up 64t..64t+63]
+template <int NM>  // contributors loaded up front (more: sk_reduce loads them serially)
 __global__ void __launch_bounds__(256) silu_consumer_kernel(PartialView pv, int F, bf16 *act, RsArgs rs) {
   SM_GT_BEGIN();
   pdl_trigger();
@@ -608,11 +626,11 @@ __global__ void __launch_bounds__(256) silu_consumer_kernel(PartialView pv, int 
     u = sk_get4(pv, 0, m, ng + 64);
   } else {
     const SkRef rg = sk_ref(pv, 0, m, ng), ru = sk_ref(pv, 0, m, ng + 64);
-    float4 xg[8], xu[8];
-    sk_load<8>(rg, xg);
-    sk_load<8>(ru, xu);
-    g = sk_reduce<8>(rg, xg);
-    u = sk_reduce<8>(ru, xu);
+    float4 xg[NM], xu[NM];
+    sk_load<NM>(rg, xg);
+    sk_load<NM>(ru, xu);
+    g = sk_reduce<NM>(rg, xg);
+    u = sk_reduce<NM>(ru, xu);
   }
   const float r = rs_of(rs, m);  // deferred RMSNorm scale (R2)
   const float gg[4] = {g.x * r, g.y * r, g.z * r, g.w * r}, uu[4] = {u.x * r, u.y * r, u.z * r, u.w * r};
@@ -677,7 +695,9 @@ cudaError_t silu_consumer_launch(const PartialView &pv, int F, bf16 *act, RsArgs
     return launch_pdl(silu_consumer_rows_kernel<2>, dim3(gx, (pv.M + 1) / 2), dim3(nt), 0, st, pv, F, act, rs);
   if (pv.M >= 256 && pv.planes <= 1 && g_consumer_rpc == 4)
     return launch_pdl(silu_consumer_rows_kernel<4>, dim3(gx, (pv.M + 3) / 4), dim3(nt), 0, st, pv, F, act, rs);
-  return launch_pdl(silu_consumer_kernel, dim3(gx, pv.M), dim3(nt), 0, st, pv, F, act, rs);
+  if (g_consumer_nm == 4)
+    return launch_pdl(silu_consumer_kernel<4>, dim3(gx, pv.M), dim3(nt), 0, st, pv, F, act, rs);
+  return launch_pdl(silu_consumer_kernel<8>, dim3(gx, pv.M), dim3(nt), 0, st, pv, F, act, rs);
 }
 
 // ------------------------------------------------------------------ logits: argmax + typical stats
@@ -1010,13 +1030,16 @@ void epilogue_preload() {  // force-load (see gemm_preload)
   cudaFuncGetAttributes(&fa, resid_norm_kernel);
   cudaFuncGetAttributes(&fa, resid_norm_tp_kernel<false>);
   cudaFuncGetAttributes(&fa, resid_norm_tp_kernel<true>);
-  cudaFuncGetAttributes(&fa, resid_norm_split_kernel);
+  cudaFuncGetAttributes(&fa, resid_norm_split_kernel<16>);
+  cudaFuncGetAttributes(&fa, resid_norm_split_kernel<8>);
   cudaFuncGetAttributes(&fa, resid_norm_split4_kernel<4>);
   cudaFuncGetAttributes(&fa, resid_norm_split4_kernel<2>);
   cudaFuncGetAttributes(&fa, qkv_consumer_kernel<false>);
+  cudaFuncGetAttributes(&fa, qkv_consumer_kernel<false, 4>);
   cudaFuncGetAttributes(&fa, qkv_consumer_kernel<true>);
   cudaFuncGetAttributes(&fa, qkv_consumer_rows_kernel<false, 4>);
-  cudaFuncGetAttributes(&fa, silu_consumer_kernel);
+  cudaFuncGetAttributes(&fa, silu_consumer_kernel<8>);
+  cudaFuncGetAttributes(&fa, silu_consumer_kernel<4>);
   cudaFuncGetAttributes(&fa, silu_consumer_rows_kernel<4>);
   cudaFuncGetAttributes(&fa, silu_consumer_rows_kernel<2>);
   cudaFuncGetAttributes(&fa, qkv_consumer_rows_kernel<false, 2>);

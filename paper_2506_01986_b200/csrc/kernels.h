@@ -383,6 +383,8 @@ void attention_set_split_model(int m);
 void attention_set_w2(int on);
 void attention_set_qearly(int on);
 void consumer_set_rpc(int n);
+void consumer_set_nm(int n);
+void resid_set_nm(int n);
 void attention_set_lean_div(int d);
 int attention_lean_min_tiles(int Nq, int G);
 void attention_set_splits(int n);               // experiments: force key splits (0 = auto)

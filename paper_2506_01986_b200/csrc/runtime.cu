@@ -1989,6 +1989,8 @@ extern "C" sm_status sm_reset_options(void) {
   attention_set_w2(1);
   attention_set_qearly(1);
   consumer_set_rpc(2);
+  consumer_set_nm(4);
+  resid_set_nm(8);
   attention_set_lean_div(16);
   tp_set_rsag(-1);
   g_fused = 0;
@@ -2045,6 +2047,10 @@ extern "C" sm_status sm_set_option(const char *name, int value) {
     attention_set_lean(value);
   } else if (n == "attn_l2ahead") {  // K1 row-copy kernel: L2 prefetch ahead of the ring (bit 0 own range, bit 1 next wave)
     attention_set_l2ahead(value);
+  } else if (n == "resid_nm") {  // one-row residual consumer: contributors loaded up front (16 or 8)
+    resid_set_nm(value);
+  } else if (n == "consumer_nm") {  // one-row QKV / SiLU consumers: contributors loaded up front (8 or 4)
+    consumer_set_nm(value);
   } else if (n == "consumer_rpc") {  // token rows per CTA of the QKV / SiLU consumers for M >= 256 (experiments)
     consumer_set_rpc(value);
   } else if (n == "attn_qearly") {  // K1 row-copy kernel: Q loads before the CTA barrier (1) or after (0)
